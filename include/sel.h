@@ -1,0 +1,212 @@
+/*
+ * sel.h — C ABI of libsel: the exact-selectivity probe on B200 (sm_100a).
+ *
+ * The method (Shin 2018, "Novel Selectivity Estimation Strategy for Modern DBMS",
+ * arXiv 1806.08384; PAPER.md = /root/reference/PAPER.md):
+ *   - sel_count    = Listing 3.1: `SELECT COUNT(*) FROM R WHERE <pushed-down
+ *                    predicate>`, "the exact cardinality of the given selection",
+ *                    computed by iterating "through all the tuples and simply increase a counter
+ *                    whenever it finds a tuple which satisfies the given condition".
+ *   - sel_pushdown = materialising sigma(R) with the projection pushed down (PAPER.md:141, 235,
+ *                    329; Algorithm 1 lines 380-383 / Execute): selected row ids
+ *                    plus projected columns, with the Execute(isSPD, maxSize) capacity gate
+ *                    "if count > maxSize throw" as a distinguishable outcome.
+ *
+ * Everything the library touches on the device is caller-owned (torch tensors in the Python
+ * binding). The library never allocates, frees or copies column data; it owns only metadata and
+ * a small per-context scratch area (tile status words, per-CTA partials, a pinned 16-byte result
+ * slot). A context is not re-entrant: one call at a time per context.
+ *
+ * Errors: calls returning sel_status return the code; calls returning uint64_t return SEL_ERR on
+ * a hard error. Both set a thread-local status + message readable with sel_last_error() and
+ * sel_last_error_message(). A successful call sets the thread-local status to SEL_OK.
+ */
+#ifndef SEL_H_
+#define SEL_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SEL_ABI_VERSION 1
+#define SEL_ERR UINT64_MAX /* error sentinel for uint64_t-returning calls */
+
+typedef enum {
+  SEL_OK = 0,
+  SEL_E_ARG = 1,       /* bad argument (null pointer, out-of-range index, bad sizes)            */
+  SEL_E_ALIGN = 2,     /* column data pointer not 16-byte aligned                               */
+  SEL_E_TYPE = 3,      /* unknown column type, or a constant not representable in its column   */
+  SEL_E_PROGRAM = 4,   /* malformed predicate program (see "Program validation" below)          */
+  SEL_E_TOO_LARGE = 5, /* global_rows >= 2^32 (row ids are uint32)                              */
+  SEL_E_CUDA = 6,      /* CUDA runtime failure (message carries cudaGetErrorString)             */
+  SEL_E_NCCL = 7,      /* NCCL failure or NCCL library not loadable                              */
+  SEL_E_STATE = 8      /* call not valid in the context's state                                  */
+} sel_status;
+
+/* Column element types (PAPER.md:475-479 INTEGER, TEXT, DECIMAL(15,2); DATE at PAPER.md:681;
+ * integer-coded dimension attributes at PAPER.md:725-726). Widths in bytes in brackets.
+ *   SEL_INT32   [4]  signed two's complement
+ *   SEL_INT64   [8]  signed two's complement (DECIMAL(15,2) as scaled cents)
+ *   SEL_FLOAT32 [4]  IEEE-754 binary32; NaN compares false, -0 == +0
+ *   SEL_DATE32  [4]  int32 days since 1970-01-01, compared as int32
+ *   SEL_DICT8   [1], SEL_DICT16 [2], SEL_DICT32 [4]  unsigned dictionary codes of a sorted
+ *               dictionary (code order == string order), compared as unsigned integers       */
+typedef enum {
+  SEL_INT32 = 1,
+  SEL_INT64 = 2,
+  SEL_FLOAT32 = 3,
+  SEL_DATE32 = 4,
+  SEL_DICT8 = 5,
+  SEL_DICT16 = 6,
+  SEL_DICT32 = 7
+} sel_type;
+
+/* One column of the local shard: `data` is a DEVICE pointer to local_rows elements of `type`,
+ * 16-byte aligned, contiguous (columnar layout). dict_size is informational
+ * for SEL_DICT* (codes >= dict_size simply never occur) and ignored otherwise. */
+typedef struct {
+  sel_type type;
+  const void* data;
+  uint32_t dict_size;
+} sel_column;
+
+typedef struct sel_ctx_s* sel_ctx;
+typedef struct sel_table_s* sel_table;
+
+/* ---- contexts ------------------------------------------------------------------------------
+ * sel_ctx_create: binds to `cuda_device` (the caller's current device is not changed on return).
+ *   Errors: SEL_E_ARG (null out), SEL_E_CUDA (bad device). */
+sel_status sel_ctx_create(int cuda_device, sel_ctx* out);
+
+/* sel_ctx_set_comm: make the context one rank of an `nranks`-GPU group (rows sharded
+ * contiguously, one process per GPU). `nccl_unique_id` points to the 128-byte ncclUniqueId that
+ * rank 0 produced with sel_nccl_unique_id and broadcast out of band (torch.distributed).
+ * Collective: every rank must call it. NCCL is loaded with dlopen("libnccl.so.2") on first use.
+ * nranks == 1 is allowed (a one-rank communicator). Errors: SEL_E_ARG, SEL_E_NCCL, SEL_E_STATE
+ * (already set). */
+sel_status sel_ctx_set_comm(sel_ctx ctx, int nranks, int rank, const void* nccl_unique_id);
+
+/* Writes a fresh 128-byte ncclUniqueId into `out128` (call on rank 0 only). SEL_E_NCCL on
+ * failure. */
+sel_status sel_nccl_unique_id(void* out128);
+
+/* Destroys the context and its communicator. Tables registered on it must be released first. */
+void sel_ctx_destroy(sel_ctx ctx);
+
+/* Kernel timing (for bench.py's roofline): when enabled, every probe records CUDA events around
+ * its device kernels on the caller's stream; sel_ctx_last_kernel_ms reports the last probe's
+ * main-kernel duration in milliseconds (0 if timing is off). */
+sel_status sel_ctx_set_timing(sel_ctx ctx, int enable);
+sel_status sel_ctx_last_kernel_ms(sel_ctx ctx, float* ms);
+
+/* ---- tables --------------------------------------------------------------------------------
+ * sel_table_register: records descriptors of `ncols` (1..255) columns that
+ * hold rows [global_row_offset, global_row_offset + local_rows) of a table with global_rows rows.
+ * The descriptors are copied; the column memory must stay alive and unmodified while the table
+ * exists. No data moves.
+ *   Errors: SEL_E_ARG (null cols/out, ncols 0 or > 255, null data with local_rows > 0,
+ *           global_row_offset + local_rows > global_rows, dict_size above the code range),
+ *           SEL_E_TYPE (unknown type), SEL_E_ALIGN (data not 16-byte aligned),
+ *           SEL_E_TOO_LARGE (global_rows >= 2^32). */
+sel_status sel_table_register(sel_ctx ctx, const sel_column* cols, uint32_t ncols,
+                              uint64_t local_rows, uint64_t global_row_offset,
+                              uint64_t global_rows, sel_table* out);
+void sel_table_release(sel_table table);
+
+/* ---- probes --------------------------------------------------------------------------------
+ * sel_count: exact |{ i : P(row i) }| over the table's rows. With a
+ * communicator it is the sum over all ranks (one 8-byte NCCL all-reduce) and every rank gets
+ * the global count. Enqueues on `cuda_stream` (a cudaStream_t; NULL = legacy default stream)
+ * and blocks until the count is on the host (the optimizer needs the number).
+ * `prog` is host memory, copied during the call.
+ * Returns the count, or SEL_ERR (SEL_E_ARG, SEL_E_PROGRAM, SEL_E_TYPE, SEL_E_CUDA, SEL_E_NCCL). */
+uint64_t sel_count(sel_table table, const void* prog, size_t prog_bytes, void* cuda_stream);
+
+/* sel_pushdown: materialise sigma_P pi_proj(R) for the local shard.
+ *   out_rowids : device uint32[capacity_rows], receives GLOBAL row ids (global_row_offset + i)
+ *                of the selected local rows in ascending order.
+ *   out_cols[j]: device buffer of capacity_rows elements of column proj_cols[j]'s type;
+ *                out_cols[j][k] = column proj_cols[j] at row out_rowids[k] - global_row_offset.
+ *   proj_cols  : host array of nproj column indices (< ncols; repeats allowed); nproj may be 0.
+ *   Capacity gate (Algorithm 1): the call always computes the exact count;
+ *   if the local count exceeds capacity_rows, exactly the first capacity_rows selected rows
+ *   (ascending) are written and nothing beyond. This is not an error; the caller compares
+ *   *out_local_count with its capacity ("throw" -> revert).
+ *   out_local_count (host, may be NULL): selected rows in this shard.
+ *   out_global_offset (host, may be NULL): exclusive prefix of the per-rank counts in rank order
+ *   (0 without a communicator) = this shard's position in the global ascending result.
+ * Returns the global count (sum over ranks), or SEL_ERR. Blocks like sel_count.
+ * Errors: as sel_count, plus SEL_E_ARG for a bad projection index or null outputs with
+ * capacity_rows > 0. */
+uint64_t sel_pushdown(sel_table table, const void* prog, size_t prog_bytes,
+                      const uint32_t* proj_cols, uint32_t nproj, uint32_t* out_rowids,
+                      void* const* out_cols, uint64_t capacity_rows, uint64_t* out_local_count,
+                      uint64_t* out_global_offset, void* cuda_stream);
+
+/* Validate a program against column types without running it (host only; no GPU needed).
+ * Returns SEL_OK or the status sel_count would report for it. */
+sel_status sel_program_check(const void* prog, size_t prog_bytes, const sel_type* types,
+                             uint32_t ncols);
+
+/* Which device path a program takes after canonicalisation: 0 = generic interpreter,
+ * 1 = conjunctive interval fast path, 2 = constant (folded to TRUE/FALSE, no scan needed);
+ * negative status on error. Host only. */
+int sel_program_path(const void* prog, size_t prog_bytes, const sel_type* types, uint32_t ncols);
+
+sel_status sel_last_error(void);
+const char* sel_last_error_message(void);
+int sel_abi_version(void);
+
+/* ==== Program byte format, version 1 (little-endian) ==========================================
+ *
+ * A predicate program is postfix code over a boolean stack (the paper's predicates are AND/OR
+ * combinations of column-vs-constant comparisons).
+ *
+ *   header   12 B : u32 magic = bytes "SELP" | u16 version = 1 | u16 n_instr | u16 n_consts
+ *                   | u16 reserved = 0
+ *   n_instr x 8 B : u8 op | u8 col | u16 a | u16 b | u16 reserved = 0
+ *   n_consts x 8 B: u64 constant slots
+ *
+ * Constant slots hold a value in the type of the column it is compared with:
+ *   INT32, DATE32 : the int32 value sign-extended to 64 bits
+ *   INT64         : the raw 64-bit value
+ *   FLOAT32       : the binary32 bit pattern in the low 32 bits, high 32 bits zero
+ *   DICT8/16/32   : the code zero-extended (must be < 2^8, 2^16, 2^32 respectively)
+ *
+ * Opcodes (v = the column `col` value of the current row; k[i] = constant slot i):
+ *   0x01 TRUE                  push true          (col, a, b must be 0)
+ *   0x02 FALSE                 push false         (col, a, b must be 0)
+ *   0x10 EQ  push v == k[a]    0x11 LT push v < k[a]    0x12 GT push v > k[a]
+ *   0x13 LE  push v <= k[a]    0x14 GE push v >= k[a]   (b must be 0)
+ *   0x20 BETWEEN               push k[a] <= v && v <= k[b]  (inclusive; empty if k[a] > k[b])
+ *   0x30 IN                    push v == k[a] || ... || v == k[a+b-1]   (1 <= b <= 256)
+ *   0x40 AND, 0x41 OR          pop y, pop x, push x AND/OR y      (col, a, b must be 0)
+ *   0x42 NOT                   pop x, push NOT x                  (col, a, b must be 0)
+ * Comparisons use the column type's order: signed for INT32/INT64/DATE32, unsigned for DICT*,
+ * IEEE-754 for FLOAT32 (any comparison with NaN is false; -0 == +0). Logic is two-valued (no
+ * NULLs). The row is selected iff the single value left on the stack is true.
+ *
+ * Program validation (first failing check wins, in this order):
+ *   1. prog_bytes < 12, magic != "SELP", version != 1, n_instr == 0, n_instr > 128,
+ *      n_consts > 512, header reserved != 0, or prog_bytes != 12 + 8*(n_instr + n_consts)
+ *      -> SEL_E_PROGRAM.
+ *   2. For each instruction in order:
+ *      a. reserved != 0, unknown op                                          -> SEL_E_PROGRAM
+ *      b. TRUE/FALSE/AND/OR/NOT with col, a or b nonzero                      -> SEL_E_PROGRAM
+ *      c. comparison/BETWEEN/IN: col >= ncols; EQ..GE with b != 0 or a >= n_consts;
+ *         BETWEEN with a or b >= n_consts; IN with b == 0, b > 256 or a + b > n_consts
+ *                                                                             -> SEL_E_PROGRAM
+ *      d. stack underflow (AND/OR need 2, NOT needs 1), or depth after the instruction > 16
+ *                                                                             -> SEL_E_PROGRAM
+ *      e. a referenced constant slot not representable in the column's type   -> SEL_E_TYPE
+ *   3. stack depth after the last instruction != 1                            -> SEL_E_PROGRAM
+ * Maximum program size: 12 + 8 * (128 + 512) = 5,132 bytes.
+ */
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SEL_H_ */
