@@ -1,0 +1,431 @@
+#!/usr/bin/env python
+"""bench.py — the exact-selectivity probe on B200 (BASELINE.json metric: "selectivity-probe latency
+(ms) and scanned GB/s vs HBM peak at 1/2/4/8 B200").
+
+One step = one pass of the whole hot path over the worked example R of the
+paper (BASELINE.json configs[1]): 600M rows, predicate
+`A = 2 AND B < 2001 AND B > 1000 AND (C = 1 OR C = 4)` (Listing 3.1):
+  a2-a5  sel_count   -> the exact count (100,200,000), all-reduced over ranks when N > 1
+  a6-a7  sel_pushdown -> ascending row ids + projected A, C, D, offsets over ranks
+Rows are sharded contiguously over ranks (strong scaling: the global table is fixed).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config c2|...]
+Under torchrun (N > 1) every rank runs its shard; rank 0 prints one JSON line.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "selectivity-probe latency (ms) and scanned GB/s vs HBM peak at 1/2/4/8 B200"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="c2", choices=["c2", "c3", "c4", "c5"])
+    ap.add_argument("--rows", type=int, default=0, help="override global rows (testing only)")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=5)
+    return ap.parse_args()
+
+
+# ---- workloads ---------------------------------------------------------------------------------
+
+def workload(name, rows):
+    """(generator(row_start, row_count, device) -> Table, program AST, projection, description)."""
+    from selgen import configs
+    if name == "c2":
+        n = rows or configs.C2_ROWS
+        return (n, lambda s, c, d: configs.gen_c2(n, s, c, device=d),
+                configs.c2_probes()["listing"], configs.C2_PROJECT,
+                "worked example R (PAPER.md:55-64): 600M rows, Listing 3.1 COUNT + push-down of A,C,D")
+    if name == "c3":
+        n = rows or 300_000_000
+        cols = ["l_orderkey", "l_discount", "l_extendedprice", "l_returnflag", "l_shipdate"]
+        def gen(s, c, d):
+            return configs.gen_lineitem(n, s, c, device=d, columns=cols)
+        probe = configs.lineitem_probes(gen(0, 16, "cpu"))["q10"]
+        return n, gen, probe, [0, 2, 1], "TPC-H SF-50 lineitem, Q10-style predicate"
+    if name == "c4":
+        n = rows or 480_000_000
+        return (n, lambda s, c, d: configs.gen_lineorder(n, s, c, device=d),
+                configs.lineorder_probes()["q1.1"], [3], "SSB SF-80 lineorder, Q1.1 predicate")
+    n = rows or configs.C5_ROWS
+    return (n, lambda s, c, d: configs.gen_sweep(n, s, c, device=d),
+            configs.sweep_probe(configs.sweep_threshold(n, 0.01)), [1],
+            "1e9-row sweep, x < 0.01 N")
+
+
+def shard(n, world, rank):
+    return n * rank // world, n * (rank + 1) // world
+
+
+def algo_bytes(table, prog_cols, proj, local_count):
+    """SURVEY §8d algorithmic bytes: count = rows x sum of distinct predicate-column widths (+8 B
+    result); push-down = the count bytes + selected x (non-predicate projected widths) read +
+    selected x (4 + projected widths) written."""
+    w = [c.width for c in table.columns]
+    scan = table.n_rows * sum(w[c] for c in prog_cols)
+    count_b = scan + 8
+    gather = local_count * sum(w[c] for c in set(proj) if c not in prog_cols)
+    write = local_count * (4 + sum(w[c] for c in proj))
+    return count_b, scan + gather + write
+
+
+def prog_columns(node):
+    from selgen.program import Cmp, Between, In, And, Or, Not
+    if isinstance(node, (Cmp, Between, In)):
+        return {node.col}
+    if isinstance(node, (And, Or)):
+        return prog_columns(node.l) | prog_columns(node.r)
+    if isinstance(node, Not):
+        return prog_columns(node.x)
+    return set()
+
+
+# ---- clocks ----------------------------------------------------------------------------------------
+
+class ClockSampler:
+    """NVML sampling of SM clock and throttle reasons DURING the timed region."""
+
+    def __init__(self, index):
+        self.samples, self.reasons, self.max_mhz = [], set(), None
+        self._stop = threading.Event()
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self.nv = None
+
+    def _run(self):
+        nv = self.nv
+        names = {
+            "hw_slowdown": getattr(nv, "nvmlClocksEventReasonHwSlowdown", 0x8),
+            "sw_thermal_slowdown": getattr(nv, "nvmlClocksEventReasonSwThermalSlowdown", 0x20),
+            "hw_thermal_slowdown": getattr(nv, "nvmlClocksEventReasonHwThermalSlowdown", 0x40),
+            "sw_power_cap": getattr(nv, "nvmlClocksEventReasonSwPowerCap", 0x4),
+            "hw_power_brake_slowdown": getattr(nv, "nvmlClocksEventReasonHwPowerBrakeSlowdown", 0x80),
+        }
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+                r = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for k, bit in names.items():
+                    if r & bit:
+                        self.reasons.add(k)
+            except Exception:
+                pass
+            time.sleep(0.005)
+
+    def __enter__(self):
+        if self.nv is not None:
+            self._t = threading.Thread(target=self._run, daemon=True)
+            self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self.nv is not None:
+            self._t.join()
+
+    def summary(self):
+        med = statistics.median(self.samples) if self.samples else None
+        return {"sm_mhz": med, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
+                "samples": len(self.samples)}
+
+
+def measured_peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        return {}
+
+
+def ncu_traffic(kernel, config):
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch from the committed ncu capture."""
+    try:
+        d = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))
+        return d.get(config, {}).get(kernel)
+    except Exception:
+        return None
+
+
+# ---- the oracle as baseline / reference arm ------------------------------------------------------
+
+def cpu_baseline(host_cols, types, prog, proj, n_sample, per_row_count_b, per_row_scan_b,
+                 selected_frac, proj_w, nthreads):
+    import oracle
+    cols = [c[:n_sample] for c in host_cols]
+    t0 = time.perf_counter()
+    cnt = oracle.count_mt(cols, types, prog, nthreads)
+    t1 = time.perf_counter()
+    c2, ids, outs = oracle.pushdown(cols, types, prog, proj=proj)
+    t2 = time.perf_counter()
+    assert c2 == cnt
+    by = n_sample * per_row_count_b + n_sample * per_row_scan_b + cnt * proj_w
+    return by, t2 - t0, t1 - t0, t2 - t1, cnt
+
+
+def run_reference(args):
+    """--impl reference: the CPU oracle as it stands, on the host cores, on a bounded sample."""
+    import numpy as np
+    import oracle
+    from selgen import encode
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    n, gen, node, proj, desc = workload(args.config, args.rows)
+    sample = min(n, 12_000_000)
+    T = gen(0, sample, "cpu")
+    cols = [c.numpy() for c in T.columns]
+    prog = encode(node, T.types)
+    pc = prog_columns(node)
+    nthreads = os.cpu_count() or 1
+    w = [c.width for c in T.columns]
+    def step():
+        t0 = time.perf_counter()
+        cnt = oracle.count_mt(cols, T.types, prog, nthreads)
+        c2, ids, outs = oracle.pushdown(cols, T.types, prog, proj=proj)
+        return time.perf_counter() - t0, cnt
+    for _ in range(args.warmup):
+        step()
+    times = []
+    cnt = 0
+    for _ in range(args.steps):
+        dt, cnt = step()
+        times.append(dt)
+    cb, pb = algo_bytes(T, pc, proj, cnt)
+    total = cb + pb
+    ms = 1000 * sum(times) / len(times)
+    value = total / (ms / 1000) / 1e9
+    line = {"metric": METRIC, "value": round(value, 3), "unit": "GB/s", "impl": "reference",
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": round(ms, 3), "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "int32/u8 compare, u64 count", "data": "synthetic",
+            "config": {"workload": f"{args.config}: {desc}", "global_rows": n,
+                       "sample_rows": sample},
+            "cpu_baseline": {"value": round(value, 3), "unit": "GB/s", "cores": nthreads,
+                             "kind": "oracle",
+                             "sample": f"first {sample} rows of the workload; count on {nthreads} threads (oracle_count_mt), push-down single-threaded (oracle_pushdown)"},
+            "e2e": {"value": round(value, 3), "unit": "GB/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ---- our arm ---------------------------------------------------------------------------------------
+
+def run_ours(args):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import paper_1806_08384_b200 as sel
+    from selgen import encode
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        args.gpus = world
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    n, gen, node, proj, desc = workload(args.config, args.rows)
+    s, e = shard(n, world, rank)
+    T = gen(s, e - s, dev)
+    torch.cuda.synchronize()
+    ctx = sel.Context(dev)
+    if world > 1:
+        obj = [sel.Context.new_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        ctx.set_comm(world, rank, obj[0])
+    names = [c.name for c in T.columns]
+    table = sel.Table(ctx, names, T.types, [c.data for c in T.columns], row_offset=s, global_rows=n)
+    prog = encode(node, T.types)
+    pc = prog_columns(node)
+    proj_names = [names[j] for j in proj]
+    stream = torch.cuda.current_stream(dev)
+
+    # exact-size outputs from a first count (Algorithm 1: count, then materialise)
+    probe = table.pushdown(prog, project=proj_names)
+    local_count = probe.local_count
+    global_count = probe.count
+    cap = max(local_count, 1)
+    out_ids = torch.empty(cap, dtype=torch.int32, device=dev)
+    out_cols = [torch.empty(cap, dtype=c.data.dtype, device=dev) for c in (T.columns[j] for j in proj)]
+
+    count_ms, push_ms, count_lat, push_lat = [], [], [], []
+
+    def step(record):
+        t0 = time.perf_counter()
+        c = table.count(prog)
+        k1 = ctx.last_kernel_ms()
+        t1 = time.perf_counter()
+        r = table.pushdown(prog, project=proj_names, capacity=local_count, out=(out_ids, out_cols))
+        k2 = ctx.last_kernel_ms()
+        t2 = time.perf_counter()
+        if record:
+            count_ms.append(k1); push_ms.append(k2)
+            count_lat.append(1000 * (t1 - t0)); push_lat.append(1000 * (t2 - t1))
+        return c, r
+
+    ctx.enable_timing(True)
+    for _ in range(max(args.warmup, 3)):
+        c, r = step(False)
+        assert c == global_count and r.count == global_count
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local_rank) as clk:
+        ev0.record(stream)
+        for _ in range(args.steps):
+            step(True)
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    dev_ms = ev0.elapsed_time(ev1)
+    cb, pb = algo_bytes(T, pc, proj, local_count)
+    my_bytes = cb + pb
+    t = torch.tensor([dev_ms, my_bytes, cb, pb, statistics.mean(count_ms), statistics.mean(push_ms)],
+                     dtype=torch.float64, device=dev)
+    if world > 1:
+        tmax = t.clone(); dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
+        tsum = t.clone(); dist.all_reduce(tsum, op=dist.ReduceOp.SUM)
+    else:
+        tmax = tsum = t
+    total_ms = float(tmax[0])
+    ms_per_step = total_ms / args.steps
+    agg_bytes = float(tsum[1])
+    value_gbs = agg_bytes / (ms_per_step / 1000) / 1e9
+
+    peaks = measured_peaks()
+    hbm = peaks.get("hbm_gbs")
+    peak_note = "MEASURED_PEAKS.json hbm_gbs (copy, read+write)"
+    if not hbm:
+        hbm, peak_note = 6650.0, "fallback 6.65 TB/s (B200_PROFILING.md)"
+    push_k = statistics.mean(push_ms)
+    count_k = statistics.mean(count_ms)
+    push_gbs = pb / (push_k / 1000) / 1e9
+    count_gbs = cb / (count_k / 1000) / 1e9
+
+    # ---- e2e: the same step through the public API from pinned host buffers ----
+    e2e = None
+    if not args.no_e2e:
+        host = [c.data.cpu().pin_memory() for c in T.columns]
+        dcols = [c.data for c in T.columns]
+        h_ids = torch.empty(cap, dtype=torch.int32).pin_memory()
+        h_cols = [torch.empty(cap, dtype=o.dtype).pin_memory() for o in out_cols]
+        h2d = sum(h.numel() * h.element_size() for h in host)
+        d2h = cap * 4 + sum(h.numel() * h.element_size() for h in h_cols) + 8
+        def e2e_step():
+            for d, h in zip(dcols, host):
+                d.copy_(h, non_blocking=True)
+            c = table.count(prog)
+            r = table.pushdown(prog, project=proj_names, capacity=local_count, out=(out_ids, out_cols))
+            h_ids.copy_(out_ids, non_blocking=True)
+            for h, o in zip(h_cols, out_cols):
+                h.copy_(o, non_blocking=True)
+            torch.cuda.synchronize()
+            return c
+        e2e_step()
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        ea, eb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ea.record(stream)
+        for _ in range(args.e2e_steps):
+            assert e2e_step() == global_count
+        eb.record(stream)
+        torch.cuda.synchronize()
+        e_ms = torch.tensor([ea.elapsed_time(eb)], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(e_ms, op=dist.ReduceOp.MAX)
+        e_step = float(e_ms[0]) / args.e2e_steps
+        e2e = {"value": round(agg_bytes / (e_step / 1000) / 1e9, 3), "unit": "GB/s",
+               "ms_per_step": round(e_step, 3), "h2d_bytes_per_step": int(h2d),
+               "d2h_bytes_per_step": int(d2h), "steps": args.e2e_steps}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        host_cols = [c.data[: min(T.n_rows, 60_000_000)].cpu().numpy().view(
+            {1: np.int32, 2: np.int64, 3: np.float32, 4: np.int32, 5: np.uint8, 6: np.uint16,
+             7: np.uint32}[c.ctype]) for c in T.columns]
+        ns = len(host_cols[0])
+        w = [c.width for c in T.columns]
+        scan_w = sum(w[c] for c in pc)
+        proj_w = 4 + sum(w[c] for c in proj) + sum(w[c] for c in set(proj) if c not in pc)
+        nthreads = os.cpu_count() or 1
+        by, dt, t_cnt, t_push, cnt = cpu_baseline(host_cols, T.types, prog, proj, ns, scan_w, scan_w,
+                                                  None, proj_w, nthreads)
+        cpu = {"value": round(by / dt / 1e9, 3), "unit": "GB/s", "cores": nthreads, "kind": "oracle",
+               "sample": f"first {ns} of {n} rows; count on {nthreads} threads ({t_cnt:.2f} s), "
+                         f"push-down on 1 thread ({t_push:.2f} s)"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": round(value_gbs, 3), "unit": "GB/s",
+            "n_gpus": world, "steps": args.steps, "warmup": max(args.warmup, 3),
+            "ms_per_step": round(ms_per_step, 4), "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "int32/u8 compare, u64 count", "data": "synthetic",
+            "config": {"workload": f"{args.config}: {desc}", "global_rows": n,
+                       "rows_per_gpu": e - s, "selected": global_count,
+                       "parallelism": f"row-shard x{world}",
+                       "l2": "inputs larger than L2 (no flush needed)",
+                       "step": "sel_count + sel_pushdown (exact-size outputs)"},
+            "latency_ms": {"count_probe_median": round(statistics.median(count_lat), 4),
+                           "count_probe_min": round(min(count_lat), 4),
+                           "pushdown_probe_median": round(statistics.median(push_lat), 4),
+                           "count_kernel": round(count_k, 4), "pushdown_kernel": round(push_k, 4)},
+            "roofline": {"bound": "hbm", "achieved": round(push_gbs, 2), "peak": hbm, "unit": "GB/s",
+                         "frac": round(push_gbs / hbm, 4),
+                         "traffic": ncu_traffic("pushdown_kernel", args.config),
+                         "kernel": "pushdown_kernel", "peak_source": peak_note,
+                         "algorithmic_bytes_per_launch": int(pb)},
+            "roofline_count": {"bound": "hbm", "achieved": round(count_gbs, 2), "peak": hbm,
+                               "unit": "GB/s", "frac": round(count_gbs / hbm, 4),
+                               "traffic": ncu_traffic("count_kernel", args.config),
+                               "algorithmic_bytes_per_launch": int(cb)},
+            "clocks": clk.summary(),
+            "e2e": e2e,
+            "gpu_launches": 2 * args.steps,
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(line), flush=True)
+    table.release()
+    ctx.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

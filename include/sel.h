@@ -156,6 +156,17 @@ sel_status sel_program_check(const void* prog, size_t prog_bytes, const sel_type
  * negative status on error. Host only. */
 int sel_program_path(const void* prog, size_t prog_bytes, const sel_type* types, uint32_t ncols);
 
+/* The canonical plan the device would execute, as JSON, for host-side inspection and tests:
+ *   {"path": p, "const": b, "max_depth": d,
+ *    "ops": [[opcode, arg], ...],              opcode 0 = leaf(arg), 1 = AND, 2 = OR (postfix)
+ *    "leaves": [{"col": c, "wclass": w, "fkey": f, "lo": [...], "span": [...]}, ...]}
+ * lo/span are the packed device values: a row value v (its raw bits, zero-extended; FLOAT32
+ * first mapped through the sortable key) lies in the leaf iff ((v - lo) mod 2^W) <= span for
+ * some interval, W = 64 for 8-byte columns and 32 otherwise. Writes at most `cap` bytes
+ * (NUL-terminated when it fits) and returns the full length, or -status on a bad program. */
+long sel_program_plan_json(const void* prog, size_t prog_bytes, const sel_type* types,
+                           uint32_t ncols, char* buf, size_t cap);
+
 sel_status sel_last_error(void);
 const char* sel_last_error_message(void);
 int sel_abi_version(void);

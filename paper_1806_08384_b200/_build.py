@@ -1,0 +1,53 @@
+"""Builds libsel.so in-tree with nvcc for sm_100a (no JIT cache: the .so travels with the repo
+snapshot to the GPU box). Host code (canon.cpp, api.cpp) and kernels (kernels.cu) link into one
+shared library with a static CUDA runtime; NCCL is dlopen'd at run time."""
+
+from __future__ import annotations
+
+import os
+import subprocess
+import sysconfig
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(HERE)
+CSRC = os.path.join(HERE, "csrc")
+LIB = os.path.join(HERE, "libsel.so")
+SOURCES = [os.path.join(CSRC, f) for f in ("kernels.cu", "canon.cpp", "api.cpp")]
+HEADERS = [os.path.join(CSRC, f) for f in ("sel_internal.h", "canon.h")] + \
+          [os.path.join(ROOT, "include", "sel.h")]
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+
+
+def _nccl_dirs():
+    site = sysconfig.get_paths()["purelib"]
+    base = os.path.join(site, "nvidia", "nccl")
+    inc = os.path.join(base, "include")
+    lib = os.path.join(base, "lib", "libnccl.so.2")
+    if not os.path.exists(os.path.join(inc, "nccl.h")):
+        inc = "/usr/include"
+    return inc, lib
+
+
+def _stale() -> bool:
+    if not os.path.exists(LIB):
+        return True
+    t = os.path.getmtime(LIB)
+    return any(os.path.getmtime(f) > t for f in SOURCES + HEADERS)
+
+
+def build(force: bool = False, verbose: bool = False) -> str:
+    if not force and not _stale():
+        return LIB
+    nccl_inc, nccl_lib = _nccl_dirs()
+    cmd = ["nvcc", *ARCH, "-O3", "-lineinfo", "-std=c++17", "-shared", "-cudart", "static",
+           "-Xcompiler", "-fPIC", "-Xptxas", "-v" if verbose else "-O3",
+           "-I", os.path.join(ROOT, "include"), "-I", nccl_inc,
+           f'-DSEL_NCCL_FALLBACK="{nccl_lib}"', *SOURCES, "-o", LIB + ".tmp", "-ldl"]
+    subprocess.run(cmd, check=True)
+    os.replace(LIB + ".tmp", LIB)
+    return LIB
+
+
+if __name__ == "__main__":
+    import sys
+    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))

@@ -1,0 +1,227 @@
+"""Python API over libsel (argument marshalling only; torch provides device memory and streams).
+
+    ctx = Context()                                   # one per process / GPU
+    t = Table.from_tensors(ctx, {"A": a, "B": b, "C": c}, dicts={"C": [...]})
+    n = t.count((col("A") == 2) & (col("B") < 2001) & (col("B") > 1000) & col("C").isin([1, 4]))
+    res = t.pushdown(pred, project=["A", "C", "D"])    # count first, then materialise (Alg. 1)
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+from typing import Mapping, Sequence
+
+import torch
+
+from . import _native
+from ._native import SEL_ERR, SelError, check, last_error, lib, sel_column
+from .predicate import (Expr, compile_predicate, INT32, INT64, FLOAT32, DATE32, DICT8, DICT16,
+                        DICT32)
+
+_DEFAULT_TYPE = {torch.int32: INT32, torch.int64: INT64, torch.float32: FLOAT32,
+                 torch.uint8: DICT8, torch.int16: DICT16, torch.uint16: DICT16}
+_WIDTH = {INT32: 4, INT64: 8, FLOAT32: 4, DATE32: 4, DICT8: 1, DICT16: 2, DICT32: 4}
+_OUT_DTYPE = {INT32: torch.int32, INT64: torch.int64, FLOAT32: torch.float32, DATE32: torch.int32,
+              DICT8: torch.uint8, DICT16: torch.int16, DICT32: torch.int32}
+
+
+def _stream_ptr(stream, device) -> int:
+    s = stream if stream is not None else torch.cuda.current_stream(device)
+    return int(s.cuda_stream)
+
+
+class Context:
+    """A libsel context bound to one CUDA device (one process per GPU)."""
+
+    def __init__(self, device=None):
+        if device is None:
+            device = torch.cuda.current_device()
+        self.device = torch.device("cuda", int(torch.device(device).index if not isinstance(device, int) else device))
+        h = ctypes.c_void_p()
+        check(lib().sel_ctx_create(self.device.index, ctypes.byref(h)))
+        self._h = h
+        self.nranks, self.rank = 1, 0
+
+    @staticmethod
+    def new_unique_id() -> bytes:
+        buf = ctypes.create_string_buffer(128)
+        check(lib().sel_nccl_unique_id(buf))
+        return buf.raw
+
+    def set_comm(self, nranks: int, rank: int, unique_id: bytes) -> None:
+        buf = ctypes.create_string_buffer(bytes(unique_id), 128)
+        check(lib().sel_ctx_set_comm(self._h, nranks, rank, buf))
+        self.nranks, self.rank = nranks, rank
+
+    def enable_timing(self, on: bool = True) -> None:
+        check(lib().sel_ctx_set_timing(self._h, 1 if on else 0))
+
+    def last_kernel_ms(self) -> float:
+        ms = ctypes.c_float(0.0)
+        check(lib().sel_ctx_last_kernel_ms(self._h, ctypes.byref(ms)))
+        return float(ms.value)
+
+    def close(self) -> None:
+        if getattr(self, "_h", None):
+            lib().sel_ctx_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+@dataclass
+class PushdownResult:
+    rowids: torch.Tensor          # uint32 global row ids (as int32 storage), ascending
+    columns: dict                 # name -> tensor of projected values
+    count: int                    # global count (all ranks)
+    local_count: int              # rows selected in this shard (may exceed capacity)
+    offset: int                   # exclusive prefix over ranks (position of this shard's slice)
+
+    @property
+    def gated(self) -> bool:
+        """Algorithm 1's 'count > maxSize' outcome: output truncated."""
+        return self.local_count > self.rowids.numel()
+
+
+class Table:
+    """A registered table shard: rows [row_offset, row_offset + local_rows) of global_rows."""
+
+    def __init__(self, ctx: Context, names: Sequence[str], types: Sequence[int],
+                 tensors: Sequence[torch.Tensor], dicts: Mapping[str, list] | None = None,
+                 row_offset: int = 0, global_rows: int | None = None):
+        if not tensors:
+            raise ValueError("a table needs at least one column")
+        n = tensors[0].numel()
+        for name, t, x in zip(names, types, tensors):
+            if not x.is_cuda or x.device != ctx.device:
+                raise ValueError(f"column {name} must live on {ctx.device}")
+            if x.dim() != 1 or not x.is_contiguous() or x.numel() != n:
+                raise ValueError(f"column {name} must be 1-D, contiguous, with {n} rows")
+            if x.element_size() != _WIDTH[t]:
+                raise ValueError(f"column {name}: element size {x.element_size()} != {_WIDTH[t]}")
+        self.ctx = ctx
+        self.names = list(names)
+        self.types = [int(t) for t in types]
+        self.tensors = list(tensors)          # keep the memory alive while registered
+        self.dicts = dict(dicts or {})
+        self.local_rows = n
+        self.row_offset = int(row_offset)
+        self.global_rows = int(global_rows if global_rows is not None else row_offset + n)
+        arr = (sel_column * len(tensors))()
+        for i, (t, x) in enumerate(zip(self.types, self.tensors)):
+            arr[i].type = t
+            arr[i].data = x.data_ptr() if n > 0 else None
+            arr[i].dict_size = len(self.dicts.get(self.names[i], [])) if t in (DICT8, DICT16, DICT32) else 0
+        h = ctypes.c_void_p()
+        check(lib().sel_table_register(ctx._h, arr, len(tensors), n, self.row_offset,
+                                       self.global_rows, ctypes.byref(h)))
+        self._h = h
+
+    @classmethod
+    def from_tensors(cls, ctx: Context, columns, types: Mapping[str, int] | None = None,
+                     dicts: Mapping[str, list] | None = None, row_offset: int = 0,
+                     global_rows: int | None = None) -> "Table":
+        items = list(columns.items()) if isinstance(columns, Mapping) else list(columns)
+        types = dict(types or {})
+        names = [k for k, _ in items]
+        tensors = [v for _, v in items]
+        tys = [types.get(k, _DEFAULT_TYPE.get(v.dtype)) for k, v in items]
+        if any(t is None for t in tys):
+            raise ValueError("column type could not be inferred; pass types={name: sel_type}")
+        return cls(ctx, names, tys, tensors, dicts, row_offset, global_rows)
+
+    @property
+    def schema(self):
+        return [(n, t, self.dicts.get(n)) for n, t in zip(self.names, self.types)]
+
+    def program(self, pred) -> bytes:
+        if isinstance(pred, (bytes, bytearray)):
+            return bytes(pred)
+        return compile_predicate(pred, self.schema)
+
+    def count(self, pred, stream=None) -> int:
+        """Exact |sigma_P(R)| (Listing 3.1); global over ranks."""
+        prog = self.program(pred)
+        r = lib().sel_count(self._h, prog, len(prog), _stream_ptr(stream, self.ctx.device))
+        if r == SEL_ERR:
+            raise last_error()
+        return int(r)
+
+    def pushdown(self, pred, project: Sequence[str | int] = (), capacity: int | None = None,
+                 stream=None, out=None) -> PushdownResult:
+        """Materialise sigma_P pi_project(R). capacity=None sizes the output
+        exactly from a count probe first (Algorithm 1's order: count, then execute); an integer
+        capacity is the single-pass gated form (count > capacity => truncated, see `.gated`)."""
+        prog = self.program(pred)
+        proj = [self.names.index(p) if isinstance(p, str) else int(p) for p in project]
+        if capacity is None:
+            capacity = self._local_count(prog, stream)
+        dev = self.ctx.device
+        if out is None:
+            rowids = torch.empty(max(capacity, 1), dtype=torch.int32, device=dev)
+            outs = [torch.empty(max(capacity, 1), dtype=_OUT_DTYPE[self.types[j]], device=dev) for j in proj]
+        else:
+            rowids, outs = out
+        ptrs = (ctypes.c_void_p * max(len(outs), 1))(*[o.data_ptr() for o in outs])
+        pj = (ctypes.c_uint32 * max(len(proj), 1))(*proj)
+        local = ctypes.c_uint64(0)
+        off = ctypes.c_uint64(0)
+        r = lib().sel_pushdown(self._h, prog, len(prog), pj, len(proj), rowids.data_ptr(), ptrs,
+                               capacity, ctypes.byref(local), ctypes.byref(off),
+                               _stream_ptr(stream, dev))
+        if r == SEL_ERR:
+            raise last_error()
+        k = min(int(local.value), capacity)
+        cols = {self.names[j] if isinstance(p, str) else j: o[:k]
+                for p, j, o in zip(project, proj, outs)}
+        return PushdownResult(rowids[:k], cols, int(r), int(local.value), int(off.value))
+
+    def _local_count(self, prog: bytes, stream) -> int:
+        if self.ctx.nranks == 1:
+            return self.count(prog, stream)
+        # local count of this shard: a push-down with capacity 0 returns it without writing
+        local = ctypes.c_uint64(0)
+        r = lib().sel_pushdown(self._h, prog, len(prog), None, 0, None, None, 0,
+                               ctypes.byref(local), None, _stream_ptr(stream, self.ctx.device))
+        if r == SEL_ERR:
+            raise last_error()
+        return int(local.value)
+
+    def release(self) -> None:
+        if getattr(self, "_h", None):
+            lib().sel_table_release(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.release()
+        except Exception:
+            pass
+
+
+def program_check(prog: bytes, types: Sequence[int]) -> int:
+    """Validation status of a program against column types (host only, no GPU needed)."""
+    arr = (ctypes.c_int * max(len(types), 1))(*types)
+    return int(lib().sel_program_check(prog, len(prog), arr, len(types)))
+
+
+def program_path(prog: bytes, types: Sequence[int]) -> int:
+    arr = (ctypes.c_int * max(len(types), 1))(*types)
+    return int(lib().sel_program_path(prog, len(prog), arr, len(types)))
+
+
+def program_plan(prog: bytes, types: Sequence[int]) -> dict:
+    """The canonical device plan (include/sel.h sel_program_plan_json) as a dict."""
+    import json
+    arr = (ctypes.c_int * max(len(types), 1))(*types)
+    n = lib().sel_program_plan_json(prog, len(prog), arr, len(types), None, 0)
+    if n < 0:
+        raise SelError(-n, "invalid program")
+    buf = ctypes.create_string_buffer(n + 1)
+    lib().sel_program_plan_json(prog, len(prog), arr, len(types), buf, n + 1)
+    return json.loads(buf.value.decode())

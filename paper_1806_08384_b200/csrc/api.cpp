@@ -1,0 +1,591 @@
+// api.cpp — the C ABI of libsel (include/sel.h): contexts, table registry, probe orchestration,
+// NCCL (dlopen'd) for the cross-GPU count all-reduce and push-down offset all-gather.
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/sel.h"
+#include "canon.h"
+#include "sel_internal.h"
+
+using namespace sel;
+
+// ---- thread-local error state ----------------------------------------------------------------
+namespace {
+thread_local sel_status g_status = SEL_OK;
+thread_local std::string g_message;
+
+sel_status set_error(sel_status st, const std::string& msg) {
+  g_status = st;
+  g_message = msg;
+  return st;
+}
+void clear_error() {
+  g_status = SEL_OK;
+  g_message.clear();
+}
+uint64_t fail64(sel_status st, const std::string& msg) {
+  set_error(st, msg);
+  return SEL_ERR;
+}
+std::string cuda_msg(const char* what, cudaError_t e) {
+  return std::string(what) + ": " + cudaGetErrorName(e) + " (" + cudaGetErrorString(e) + ")";
+}
+
+struct DeviceGuard {
+  int prev = -1;
+  bool ok = false;
+  explicit DeviceGuard(int dev) {
+    if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+    ok = cudaSetDevice(dev) == cudaSuccess;
+  }
+  ~DeviceGuard() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+};
+
+// ---- NCCL via dlopen (torch's bundled libnccl.so.2 is normally already loaded) ----------------
+struct NcclApi {
+  bool loaded = false;
+  std::string error;
+  ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                            cudaStream_t) = nullptr;
+  ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t,
+                            cudaStream_t) = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  const char* (*GetErrorString)(ncclResult_t) = nullptr;
+};
+
+NcclApi& nccl() {
+  static NcclApi api = [] {
+    NcclApi a;
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+#ifdef SEL_NCCL_FALLBACK
+    if (!h) h = dlopen(SEL_NCCL_FALLBACK, RTLD_NOW | RTLD_GLOBAL);
+#endif
+    if (!h) {
+      a.error = std::string("dlopen libnccl.so.2 failed: ") + dlerror();
+      return a;
+    }
+    a.GetUniqueId = (decltype(a.GetUniqueId))dlsym(h, "ncclGetUniqueId");
+    a.CommInitRank = (decltype(a.CommInitRank))dlsym(h, "ncclCommInitRank");
+    a.AllReduce = (decltype(a.AllReduce))dlsym(h, "ncclAllReduce");
+    a.AllGather = (decltype(a.AllGather))dlsym(h, "ncclAllGather");
+    a.CommDestroy = (decltype(a.CommDestroy))dlsym(h, "ncclCommDestroy");
+    a.GetErrorString = (decltype(a.GetErrorString))dlsym(h, "ncclGetErrorString");
+    a.loaded = a.GetUniqueId && a.CommInitRank && a.AllReduce && a.AllGather && a.CommDestroy &&
+               a.GetErrorString;
+    if (!a.loaded) a.error = "libnccl.so.2 lacks a required symbol";
+    return a;
+  }();
+  return api;
+}
+
+std::string nccl_msg(const char* what, ncclResult_t r) {
+  return std::string(what) + ": " + (nccl().GetErrorString ? nccl().GetErrorString(r) : "?");
+}
+
+int width_of(int type) {
+  switch (type) {
+    case SEL_INT64: return 8;
+    case SEL_DICT8: return 1;
+    case SEL_DICT16: return 2;
+    default: return 4;
+  }
+}
+uint8_t wclass_of(int type) {
+  switch (width_of(type)) {
+    case 1: return W1;
+    case 2: return W2;
+    case 4: return W4;
+    default: return W8;
+  }
+}
+bool known_type(int t) { return t >= SEL_INT32 && t <= SEL_DICT32; }
+
+}  // namespace
+
+// ---- objects ------------------------------------------------------------------------------------
+struct sel_ctx_s {
+  int device = 0;
+  int num_sms = 148;
+  int occ_count_small = 1, occ_count_large = 1, occ_push_small = 1, occ_push_large = 1;
+  Scratch s{};
+  uint64_t* h_result = nullptr;   // pinned: [0] local count, [1..nranks] gathered counts
+  uint64_t ticket_base = 0;
+  uint32_t epoch = 0;
+  ncclComm_t comm = nullptr;
+  int nranks = 1, rank = 0;
+  bool timing = false;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  float last_ms = 0.f;
+  int live_tables = 0;
+};
+
+struct sel_table_s {
+  sel_ctx ctx;
+  std::vector<sel_column> cols;
+  std::vector<int> types;
+  uint64_t local_rows, row_offset, global_rows;
+};
+
+namespace {
+
+constexpr int kMaxGrid = 148 * 32;
+constexpr int kMaxRanks = 1024;
+
+template <class P>
+bool fits_block(const Plan& plan, size_t nslots, uint32_t nproj) {
+  return plan.op.size() <= (size_t)P::kMaxOps && plan.leaves.size() <= (size_t)P::kMaxLeaves &&
+         plan.n_intervals <= (size_t)P::kMaxIv && nslots <= (size_t)P::kMaxSlots &&
+         nproj <= (uint32_t)P::kMaxProj;
+}
+
+// Plan -> kernel parameter block. TRUE (PATH_CONST with value true) packs as an empty conjunction.
+template <class P>
+void pack(const Plan& plan, const sel_table_s* t, P* p) {
+  std::memset(p, 0, sizeof(P));
+  std::vector<int> slot_of(t->cols.size(), -1);
+  uint32_t nslots = 0, iv = 0;
+  p->n_ops = (uint32_t)plan.op.size();
+  p->n_leaves = (uint32_t)plan.leaves.size();
+  p->conj = plan.path != PATH_INTERP ? 1u : 0u;
+  for (size_t i = 0; i < plan.op.size(); ++i) {
+    p->op[i] = plan.op[i];
+    p->arg[i] = plan.arg[i];
+  }
+  for (size_t l = 0; l < plan.leaves.size(); ++l) {
+    const PlanLeaf& L = plan.leaves[l];
+    if (slot_of[L.col] < 0) {
+      slot_of[L.col] = (int)nslots;
+      p->col[nslots++] = t->cols[L.col].data;
+    }
+    const int type = t->types[L.col];
+    DevLeaf& d = p->leaf[l];
+    d.slot = (uint8_t)slot_of[L.col];
+    d.wclass = wclass_of(type);
+    d.fkey = type == SEL_FLOAT32 ? 1 : 0;
+    d.iv_begin = (uint16_t)iv;
+    d.iv_count = (uint16_t)L.iv.size();
+    const uint64_t bias = key_sign_bias(type);
+    for (const Interval& x : L.iv) {
+      p->lo[iv] = x.lo ^ bias;
+      p->span[iv] = x.hi - x.lo;
+      ++iv;
+    }
+  }
+}
+
+size_t count_slots(const Plan& plan) {
+  std::vector<int> cols;
+  for (auto& L : plan.leaves) cols.push_back(L.col);
+  std::sort(cols.begin(), cols.end());
+  return (size_t)(std::unique(cols.begin(), cols.end()) - cols.begin());
+}
+
+sel_status plan_for(sel_table t, const void* prog, size_t bytes, Plan* plan) {
+  Program P;
+  std::string msg;
+  const int st = decode_program(prog, bytes, t->types.data(), (uint32_t)t->types.size(), &P, &msg);
+  if (st != SEL_OK) return set_error((sel_status)st, msg);
+  plan_program(P, t->types.data(), plan);
+  if (plan->max_depth > kMaxDeviceStack)
+    return set_error(SEL_E_PROGRAM, "program too deep after canonicalisation");
+  return SEL_OK;
+}
+
+int grid_for(sel_ctx c, uint64_t units, int occ) {
+  const uint64_t persistent = (uint64_t)c->num_sms * (uint64_t)std::max(1, occ);
+  return (int)std::max<uint64_t>(1, std::min<uint64_t>({persistent, units, (uint64_t)kMaxGrid}));
+}
+
+sel_status ensure_status(sel_ctx c, uint64_t ntiles, cudaStream_t stream) {
+  if (c->s.status_cap >= ntiles) return SEL_OK;
+  cudaError_t e = cudaStreamSynchronize(stream);
+  if (e != cudaSuccess) return set_error(SEL_E_CUDA, cuda_msg("cudaStreamSynchronize", e));
+  if (c->s.status) cudaFree(c->s.status);
+  c->s.status = nullptr;
+  c->s.status_cap = 0;
+  const uint64_t cap = std::max<uint64_t>(ntiles, 1024) * 2;
+  e = cudaMalloc(&c->s.status, cap * sizeof(uint64_t));
+  if (e != cudaSuccess) return set_error(SEL_E_CUDA, cuda_msg("cudaMalloc(status)", e));
+  e = cudaMemsetAsync(c->s.status, 0, cap * sizeof(uint64_t), stream);
+  if (e != cudaSuccess) return set_error(SEL_E_CUDA, cuda_msg("cudaMemsetAsync(status)", e));
+  c->s.status_cap = cap;
+  c->epoch = 0;
+  return SEL_OK;
+}
+
+}  // namespace
+
+// ---- ABI -------------------------------------------------------------------------------------------
+extern "C" {
+
+int sel_abi_version(void) { return SEL_ABI_VERSION; }
+sel_status sel_last_error(void) { return g_status; }
+const char* sel_last_error_message(void) { return g_message.c_str(); }
+
+sel_status sel_ctx_create(int cuda_device, sel_ctx* out) {
+  clear_error();
+  if (!out) return set_error(SEL_E_ARG, "null out");
+  *out = nullptr;
+  int ndev = 0;
+  cudaError_t e = cudaGetDeviceCount(&ndev);
+  if (e != cudaSuccess) return set_error(SEL_E_CUDA, cuda_msg("cudaGetDeviceCount", e));
+  if (cuda_device < 0 || cuda_device >= ndev) return set_error(SEL_E_CUDA, "no such CUDA device");
+  DeviceGuard g(cuda_device);
+  if (!g.ok) return set_error(SEL_E_CUDA, "cudaSetDevice failed");
+  sel_ctx c = new sel_ctx_s();
+  c->device = cuda_device;
+  cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, cuda_device);
+  c->occ_count_small = occupancy_count_small();
+  c->occ_count_large = occupancy_count_large();
+  c->occ_push_small = occupancy_pushdown_small();
+  c->occ_push_large = occupancy_pushdown_large();
+  const char* env = std::getenv("SEL_CTAS_PER_SM");
+  if (env && std::atoi(env) > 0) {
+    const int v = std::atoi(env);
+    c->occ_count_small = std::min(c->occ_count_small, v);
+    c->occ_count_large = std::min(c->occ_count_large, v);
+  }
+  bool okay = cudaMalloc(&c->s.partials, kMaxGrid * sizeof(uint64_t)) == cudaSuccess &&
+              cudaMalloc(&c->s.done, sizeof(unsigned int)) == cudaSuccess &&
+              cudaMalloc(&c->s.result, (1 + kMaxRanks) * sizeof(uint64_t)) == cudaSuccess &&
+              cudaMalloc(&c->s.ticket, sizeof(unsigned long long)) == cudaSuccess &&
+              cudaMallocHost(&c->h_result, (1 + kMaxRanks) * sizeof(uint64_t)) == cudaSuccess &&
+              cudaMemset(c->s.done, 0, sizeof(unsigned int)) == cudaSuccess &&
+              cudaMemset(c->s.ticket, 0, sizeof(unsigned long long)) == cudaSuccess &&
+              cudaMemset(c->s.result, 0, (1 + kMaxRanks) * sizeof(uint64_t)) == cudaSuccess &&
+              cudaEventCreate(&c->ev0) == cudaSuccess && cudaEventCreate(&c->ev1) == cudaSuccess &&
+              cudaDeviceSynchronize() == cudaSuccess;
+  if (!okay) {
+    cudaError_t le = cudaGetLastError();
+    sel_ctx_destroy(c);
+    return set_error(SEL_E_CUDA, cuda_msg("context allocation", le));
+  }
+  *out = c;
+  return SEL_OK;
+}
+
+sel_status sel_nccl_unique_id(void* out128) {
+  clear_error();
+  if (!out128) return set_error(SEL_E_ARG, "null out");
+  NcclApi& n = nccl();
+  if (!n.loaded) return set_error(SEL_E_NCCL, n.error);
+  ncclUniqueId id;
+  ncclResult_t r = n.GetUniqueId(&id);
+  if (r != ncclSuccess) return set_error(SEL_E_NCCL, nccl_msg("ncclGetUniqueId", r));
+  std::memcpy(out128, &id, sizeof(id));
+  return SEL_OK;
+}
+
+sel_status sel_ctx_set_comm(sel_ctx ctx, int nranks, int rank, const void* nccl_unique_id) {
+  clear_error();
+  if (!ctx || !nccl_unique_id || nranks < 1 || nranks > kMaxRanks || rank < 0 || rank >= nranks)
+    return set_error(SEL_E_ARG, "bad communicator arguments");
+  if (ctx->comm) return set_error(SEL_E_STATE, "communicator already set");
+  NcclApi& n = nccl();
+  if (!n.loaded) return set_error(SEL_E_NCCL, n.error);
+  DeviceGuard g(ctx->device);
+  ncclUniqueId id;
+  std::memcpy(&id, nccl_unique_id, sizeof(id));
+  ncclComm_t comm = nullptr;
+  ncclResult_t r = n.CommInitRank(&comm, nranks, id, rank);
+  if (r != ncclSuccess) return set_error(SEL_E_NCCL, nccl_msg("ncclCommInitRank", r));
+  ctx->comm = comm;
+  ctx->nranks = nranks;
+  ctx->rank = rank;
+  return SEL_OK;
+}
+
+void sel_ctx_destroy(sel_ctx c) {
+  if (!c) return;
+  DeviceGuard g(c->device);
+  if (c->comm && nccl().loaded) nccl().CommDestroy(c->comm);
+  if (c->s.partials) cudaFree(c->s.partials);
+  if (c->s.done) cudaFree(c->s.done);
+  if (c->s.result) cudaFree(c->s.result);
+  if (c->s.ticket) cudaFree(c->s.ticket);
+  if (c->s.status) cudaFree(c->s.status);
+  if (c->h_result) cudaFreeHost(c->h_result);
+  if (c->ev0) cudaEventDestroy(c->ev0);
+  if (c->ev1) cudaEventDestroy(c->ev1);
+  delete c;
+}
+
+sel_status sel_ctx_set_timing(sel_ctx ctx, int enable) {
+  clear_error();
+  if (!ctx) return set_error(SEL_E_ARG, "null ctx");
+  ctx->timing = enable != 0;
+  ctx->last_ms = 0.f;
+  return SEL_OK;
+}
+
+sel_status sel_ctx_last_kernel_ms(sel_ctx ctx, float* ms) {
+  clear_error();
+  if (!ctx || !ms) return set_error(SEL_E_ARG, "null argument");
+  *ms = ctx->timing ? ctx->last_ms : 0.f;
+  return SEL_OK;
+}
+
+sel_status sel_table_register(sel_ctx ctx, const sel_column* cols, uint32_t ncols,
+                              uint64_t local_rows, uint64_t global_row_offset,
+                              uint64_t global_rows, sel_table* out) {
+  clear_error();
+  if (!ctx || !cols || !out) return set_error(SEL_E_ARG, "null argument");
+  *out = nullptr;
+  if (ncols == 0 || ncols > 255) return set_error(SEL_E_ARG, "ncols must be 1..255");
+  if (global_rows >= (1ull << 32)) return set_error(SEL_E_TOO_LARGE, "global_rows must be < 2^32");
+  if (global_row_offset > global_rows || local_rows > global_rows - global_row_offset)
+    return set_error(SEL_E_ARG, "shard [offset, offset + local_rows) exceeds global_rows");
+  for (uint32_t c = 0; c < ncols; ++c) {
+    const sel_column& col = cols[c];
+    if (!known_type(col.type)) return set_error(SEL_E_TYPE, "unknown column type at " + std::to_string(c));
+    if (local_rows > 0 && col.data == nullptr) return set_error(SEL_E_ARG, "null column data at " + std::to_string(c));
+    if (((uintptr_t)col.data & 15u) != 0) return set_error(SEL_E_ALIGN, "column data not 16-byte aligned at " + std::to_string(c));
+    const uint64_t code_range = col.type == SEL_DICT8 ? (1ull << 8) : col.type == SEL_DICT16 ? (1ull << 16) : (1ull << 32);
+    if ((col.type == SEL_DICT8 || col.type == SEL_DICT16) && col.dict_size > code_range)
+      return set_error(SEL_E_ARG, "dict_size above the code range at " + std::to_string(c));
+  }
+  sel_table t = new sel_table_s();
+  t->ctx = ctx;
+  t->cols.assign(cols, cols + ncols);
+  for (uint32_t c = 0; c < ncols; ++c) t->types.push_back((int)cols[c].type);
+  t->local_rows = local_rows;
+  t->row_offset = global_row_offset;
+  t->global_rows = global_rows;
+  ctx->live_tables++;
+  *out = t;
+  return SEL_OK;
+}
+
+void sel_table_release(sel_table t) {
+  if (!t) return;
+  t->ctx->live_tables--;
+  delete t;
+}
+
+sel_status sel_program_check(const void* prog, size_t prog_bytes, const sel_type* types,
+                             uint32_t ncols) {
+  clear_error();
+  std::vector<int> ty(ncols);
+  for (uint32_t c = 0; c < ncols; ++c) {
+    if (!types || !known_type(types[c])) return set_error(SEL_E_TYPE, "unknown column type");
+    ty[c] = (int)types[c];
+  }
+  Program P;
+  std::string msg;
+  const int st = decode_program(prog, prog_bytes, ty.data(), ncols, &P, &msg);
+  if (st != SEL_OK) return set_error((sel_status)st, msg);
+  return SEL_OK;
+}
+
+int sel_program_path(const void* prog, size_t prog_bytes, const sel_type* types, uint32_t ncols) {
+  const sel_status st = sel_program_check(prog, prog_bytes, types, ncols);
+  if (st != SEL_OK) return -(int)st;
+  std::vector<int> ty(types, types + ncols);
+  Program P;
+  decode_program(prog, prog_bytes, ty.data(), ncols, &P, nullptr);
+  Plan plan;
+  plan_program(P, ty.data(), &plan);
+  return plan.path;
+}
+
+long sel_program_plan_json(const void* prog, size_t prog_bytes, const sel_type* types,
+                           uint32_t ncols, char* buf, size_t cap) {
+  const sel_status st = sel_program_check(prog, prog_bytes, types, ncols);
+  if (st != SEL_OK) return -(long)st;
+  std::vector<int> ty(types, types + ncols);
+  Program P;
+  decode_program(prog, prog_bytes, ty.data(), ncols, &P, nullptr);
+  Plan plan;
+  plan_program(P, ty.data(), &plan);
+  std::string js = "{\"path\": " + std::to_string(plan.path) +
+                   ", \"const\": " + (plan.const_value ? "true" : "false") +
+                   ", \"max_depth\": " + std::to_string(plan.max_depth) + ", \"ops\": [";
+  for (size_t i = 0; i < plan.op.size(); ++i)
+    js += (i ? ", [" : "[") + std::to_string(plan.op[i]) + ", " + std::to_string(plan.arg[i]) + "]";
+  js += "], \"leaves\": [";
+  for (size_t l = 0; l < plan.leaves.size(); ++l) {
+    const PlanLeaf& L = plan.leaves[l];
+    const int type = ty[L.col];
+    const uint64_t bias = key_sign_bias(type);
+    std::string lo, sp;
+    for (size_t i = 0; i < L.iv.size(); ++i) {
+      lo += (i ? ", " : "") + std::to_string(L.iv[i].lo ^ bias);
+      sp += (i ? ", " : "") + std::to_string(L.iv[i].hi - L.iv[i].lo);
+    }
+    js += (l ? ", " : "") + std::string("{\"col\": ") + std::to_string(L.col) +
+          ", \"wclass\": " + std::to_string(wclass_of(type)) +
+          ", \"fkey\": " + (type == SEL_FLOAT32 ? "1" : "0") + ", \"lo\": [" + lo +
+          "], \"span\": [" + sp + "]}";
+  }
+  js += "]}";
+  if (buf && cap > 0) {
+    const size_t n = std::min(cap - 1, js.size());
+    std::memcpy(buf, js.data(), n);
+    buf[n] = '\0';
+  }
+  return (long)js.size();
+}
+
+uint64_t sel_count(sel_table t, const void* prog, size_t prog_bytes, void* cuda_stream) {
+  clear_error();
+  if (!t) return fail64(SEL_E_ARG, "null table");
+  sel_ctx c = t->ctx;
+  Plan plan;
+  if (plan_for(t, prog, prog_bytes, &plan) != SEL_OK) return SEL_ERR;
+  cudaStream_t stream = (cudaStream_t)cuda_stream;
+  DeviceGuard g(c->device);
+  if (!g.ok) return fail64(SEL_E_CUDA, "cudaSetDevice failed");
+  c->last_ms = 0.f;
+  const uint64_t n = t->local_rows;
+  const bool scan = n > 0 && plan.path != PATH_CONST;
+  uint64_t local = 0;
+  if (!scan) local = plan.path == PATH_CONST && plan.const_value ? n : 0;
+  if (!scan && !c->comm) return local;
+
+  cudaError_t e;
+  if (scan) {
+    const uint64_t nchunks = (n + kChunkRows - 1) / kChunkRows;
+    const uint64_t units = (nchunks + kWarpsPerCta - 1) / kWarpsPerCta;
+    const size_t nslots = count_slots(plan);
+    if (c->timing) cudaEventRecord(c->ev0, stream);
+    int le;
+    if (fits_block<DevProgramSmall>(plan, nslots, 0)) {
+      DevProgramSmall p;
+      pack(plan, t, &p);
+      le = launch_count_small(p, n, grid_for(c, units, c->occ_count_small), c->s, stream);
+    } else {
+      static thread_local DevProgramLarge p;
+      pack(plan, t, &p);
+      le = launch_count_large(p, n, grid_for(c, units, c->occ_count_large), c->s, stream);
+    }
+    if (le != cudaSuccess) return fail64(SEL_E_CUDA, cuda_msg("count kernel launch", (cudaError_t)le));
+    if (c->timing) cudaEventRecord(c->ev1, stream);
+  } else {
+    c->h_result[0] = local;
+    e = cudaMemcpyAsync(c->s.result, c->h_result, sizeof(uint64_t), cudaMemcpyHostToDevice, stream);
+    if (e != cudaSuccess) return fail64(SEL_E_CUDA, cuda_msg("cudaMemcpyAsync", e));
+  }
+  if (c->comm) {  // one 8-byte all-reduce on the probe stream
+    ncclResult_t r = nccl().AllReduce(c->s.result, c->s.result, 1, ncclUint64, ncclSum, c->comm, stream);
+    if (r != ncclSuccess) return fail64(SEL_E_NCCL, nccl_msg("ncclAllReduce", r));
+  }
+  e = cudaMemcpyAsync(c->h_result, c->s.result, sizeof(uint64_t), cudaMemcpyDeviceToHost, stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(stream);
+  if (e != cudaSuccess) return fail64(SEL_E_CUDA, cuda_msg("count result", e));
+  if (scan && c->timing) cudaEventElapsedTime(&c->last_ms, c->ev0, c->ev1);
+  return c->h_result[0];
+}
+
+uint64_t sel_pushdown(sel_table t, const void* prog, size_t prog_bytes, const uint32_t* proj_cols,
+                      uint32_t nproj, uint32_t* out_rowids, void* const* out_cols,
+                      uint64_t capacity_rows, uint64_t* out_local_count,
+                      uint64_t* out_global_offset, void* cuda_stream) {
+  clear_error();
+  if (!t) return fail64(SEL_E_ARG, "null table");
+  sel_ctx c = t->ctx;
+  if (nproj > 0 && !proj_cols) return fail64(SEL_E_ARG, "null proj_cols");
+  if (nproj > 255) return fail64(SEL_E_ARG, "nproj must be <= 255");
+  for (uint32_t j = 0; j < nproj; ++j)
+    if (proj_cols[j] >= t->cols.size()) return fail64(SEL_E_ARG, "projection index out of range");
+  if (capacity_rows > 0) {
+    if (!out_rowids) return fail64(SEL_E_ARG, "null out_rowids with capacity > 0");
+    if (nproj > 0 && !out_cols) return fail64(SEL_E_ARG, "null out_cols with capacity > 0");
+    for (uint32_t j = 0; j < nproj; ++j)
+      if (!out_cols[j]) return fail64(SEL_E_ARG, "null out_cols entry with capacity > 0");
+  }
+  Plan plan;
+  if (plan_for(t, prog, prog_bytes, &plan) != SEL_OK) return SEL_ERR;
+  cudaStream_t stream = (cudaStream_t)cuda_stream;
+  DeviceGuard g(c->device);
+  if (!g.ok) return fail64(SEL_E_CUDA, "cudaSetDevice failed");
+  c->last_ms = 0.f;
+  const uint64_t n = t->local_rows;
+  const bool scan = n > 0 && !(plan.path == PATH_CONST && !plan.const_value);
+  cudaError_t e;
+  if (scan) {
+    const uint64_t ntiles = (n + kTileRows - 1) / kTileRows;
+    if (ensure_status(c, ntiles, stream) != SEL_OK) return SEL_ERR;
+    if (++c->epoch >= (1u << 30)) {
+      e = cudaMemsetAsync(c->s.status, 0, c->s.status_cap * sizeof(uint64_t), stream);
+      if (e != cudaSuccess) return fail64(SEL_E_CUDA, cuda_msg("cudaMemsetAsync(status)", e));
+      c->epoch = 1;
+    }
+    const size_t nslots = count_slots(plan);
+    auto fill = [&](auto* p) {
+      pack(plan, t, p);
+      p->row_offset = t->row_offset;
+      p->capacity = capacity_rows;
+      p->n_proj = capacity_rows > 0 ? nproj : 0;
+      for (uint32_t j = 0; j < p->n_proj; ++j) {
+        p->proj_src[j] = t->cols[proj_cols[j]].data;
+        p->proj_dst[j] = out_cols[j];
+        p->proj_wclass[j] = wclass_of(t->types[proj_cols[j]]);
+      }
+    };
+    if (c->timing) cudaEventRecord(c->ev0, stream);
+    int le, grid;
+    if (fits_block<DevProgramSmall>(plan, nslots, nproj)) {
+      DevProgramSmall p;
+      fill(&p);
+      grid = grid_for(c, ntiles, c->occ_push_small);
+      le = launch_pushdown_small(p, n, out_rowids, grid, c->s, c->ticket_base, c->epoch, stream);
+    } else {
+      static thread_local DevProgramLarge p;
+      fill(&p);
+      grid = grid_for(c, ntiles, c->occ_push_large);
+      le = launch_pushdown_large(p, n, out_rowids, grid, c->s, c->ticket_base, c->epoch, stream);
+    }
+    if (le != cudaSuccess) {
+      cudaMemsetAsync(c->s.ticket, 0, sizeof(unsigned long long), stream);
+      c->ticket_base = 0;
+      return fail64(SEL_E_CUDA, cuda_msg("push-down kernel launch", (cudaError_t)le));
+    }
+    c->ticket_base += ntiles + (uint64_t)grid;  // every CTA draws one ticket past the last tile
+    if (c->timing) cudaEventRecord(c->ev1, stream);
+  } else {
+    c->h_result[0] = 0;
+    if (c->comm) {
+      e = cudaMemcpyAsync(c->s.result, c->h_result, sizeof(uint64_t), cudaMemcpyHostToDevice, stream);
+      if (e != cudaSuccess) return fail64(SEL_E_CUDA, cuda_msg("cudaMemcpyAsync", e));
+    }
+  }
+  uint64_t local = 0, offset = 0, total = 0;
+  if (c->comm) {  // all-gather the per-rank counts, exclusive scan on the host
+    ncclResult_t r = nccl().AllGather(c->s.result, c->s.result + 1, 1, ncclUint64, c->comm, stream);
+    if (r != ncclSuccess) return fail64(SEL_E_NCCL, nccl_msg("ncclAllGather", r));
+    e = cudaMemcpyAsync(c->h_result + 1, c->s.result + 1, c->nranks * sizeof(uint64_t),
+                        cudaMemcpyDeviceToHost, stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(stream);
+    if (e != cudaSuccess) return fail64(SEL_E_CUDA, cuda_msg("push-down result", e));
+    for (int r2 = 0; r2 < c->nranks; ++r2) {
+      if (r2 < c->rank) offset += c->h_result[1 + r2];
+      total += c->h_result[1 + r2];
+    }
+    local = c->h_result[1 + c->rank];
+  } else {
+    if (scan) {
+      e = cudaMemcpyAsync(c->h_result, c->s.result, sizeof(uint64_t), cudaMemcpyDeviceToHost, stream);
+      if (e == cudaSuccess) e = cudaStreamSynchronize(stream);
+      if (e != cudaSuccess) return fail64(SEL_E_CUDA, cuda_msg("push-down result", e));
+    }
+    local = total = c->h_result[0];
+  }
+  if (scan && c->timing) cudaEventElapsedTime(&c->last_ms, c->ev0, c->ev1);
+  if (out_local_count) *out_local_count = local;
+  if (out_global_offset) *out_global_offset = offset;
+  return total;
+}
+
+}  // extern "C"

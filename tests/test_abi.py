@@ -1,0 +1,166 @@
+"""The C-ABI boundary on CPU (no compute calls need a GPU here):
+  * libsel.so loads and exports exactly the functions include/sel.h declares;
+  * its validator (canon.cpp) agrees with the oracle's (oracle.c) on the spec cases and on
+    fuzzed/mutated program bytes — two independent implementations of include/sel.h;
+  * its canonical plan is exact: the packed device arithmetic ((v - lo) mod 2^W <= span per
+    interval, AND/OR postfix), emulated here in NumPy, selects exactly the oracle's rows;
+  * the Python predicate builder writes the same bytes as the input generator.
+"""
+
+import ctypes
+import math
+import os
+import re
+import subprocess
+
+import numpy as np
+import pytest
+
+import oracle
+import paper_1806_08384_b200 as sel
+from paper_1806_08384_b200 import _native, col
+from selgen.program import (Cmp, Between, In, And, Or, Not, Const, encode, encode_raw,
+                            random_program, INT32, INT64, FLOAT32, DATE32, DICT8, DICT16, DICT32)
+
+from helpers import random_table
+from test_oracle_pins import VALIDATOR_CASES
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _declared():
+    hdr = open(os.path.join(ROOT, "include", "sel.h")).read()
+    hdr = re.sub(r"/\*.*?\*/", "", hdr, flags=re.S)
+    return sorted(set(re.findall(r"\b(sel_[a-z_0-9]+)\s*\(", hdr)))
+
+
+def test_library_exports_every_declared_symbol():
+    lib = _native.lib()
+    declared = _declared()
+    assert declared == sorted(_native.EXPORTS)
+    out = subprocess.run(["nm", "-D", "--defined-only", _native.LIB_PATH], capture_output=True,
+                         text=True, check=True).stdout
+    exported = sorted(set(re.findall(r" T (sel_[a-z_0-9]+)$", out, flags=re.M)))
+    assert exported == declared
+    for name in declared:
+        assert hasattr(lib, name)
+    assert lib.sel_abi_version() == 1
+
+
+@pytest.mark.parametrize("name,prog,types,want", VALIDATOR_CASES, ids=[c[0] for c in VALIDATOR_CASES])
+def test_validator_matches_spec(name, prog, types, want):
+    assert sel.program_check(prog, types) == want
+
+
+def test_validator_parity_fuzz():
+    rng = np.random.default_rng(99)
+    types = [INT32, DICT8, FLOAT32, INT64, DICT16]
+    cols, pools = random_table(rng, types, 10)
+    seeds = [encode(random_program(rng, types, pools, 3), types) for _ in range(200)]
+    n = 0
+    for base in seeds:
+        for _ in range(25):
+            b = bytearray(base)
+            k = int(rng.integers(1, 4))
+            for _ in range(k):
+                r = rng.random()
+                if r < 0.6 and len(b):
+                    b[int(rng.integers(len(b)))] = int(rng.integers(256))
+                elif r < 0.8:
+                    b = b[: int(rng.integers(len(b) + 1))]
+                else:
+                    b += bytes(rng.integers(0, 256, int(rng.integers(1, 9)), dtype=np.uint8))
+            b = bytes(b)
+            assert sel.program_check(b, types) == oracle.check(b, types), b.hex()
+            n += 1
+    assert n == 5000
+
+
+def test_error_message_thread_local_and_set():
+    assert sel.program_check(b"nope", [INT32]) == 4
+    assert "short" in _native.lib().sel_last_error_message().decode()
+    assert _native.lib().sel_last_error() == 4
+    assert sel.program_check(encode(Cmp("=", 0, 1), [INT32]), [INT32]) == 0
+    assert _native.lib().sel_last_error() == 0
+
+
+# ---- canonicaliser exactness (device arithmetic emulated in NumPy) ----------------------------
+
+_U = {INT32: np.uint32, DATE32: np.uint32, FLOAT32: np.uint32, DICT32: np.uint32, INT64: np.uint64,
+      DICT8: np.uint8, DICT16: np.uint16}
+
+
+def emulate_plan(plan, cols, types, n):
+    if plan["path"] == 2:
+        return np.full(n, plan["const"])
+    masks = []
+    for L in plan["leaves"]:
+        c = L["col"]
+        raw = cols[c].view(_U[types[c]]).astype(np.uint64)
+        if L["fkey"]:
+            sign = (raw >> np.uint64(31)) & np.uint64(1)
+            raw = raw ^ np.where(sign == 1, np.uint64(0xFFFFFFFF), np.uint64(0x80000000))
+        W = 64 if L["wclass"] == 3 else 32
+        mod = np.uint64((1 << 64) - 1) if W == 64 else np.uint64(0xFFFFFFFF)
+        m = np.zeros(n, dtype=bool)
+        for lo, sp in zip(L["lo"], L["span"]):
+            m |= ((raw - np.uint64(lo)) & mod) <= np.uint64(sp)
+        masks.append(m)
+    st = []
+    for op, arg in plan["ops"]:
+        if op == 0:
+            st.append(masks[arg])
+        else:
+            y, x = st.pop(), st.pop()
+            st.append(x & y if op == 1 else x | y)
+    assert len(st) == 1
+    return st[0]
+
+
+@pytest.mark.parametrize("types", [
+    [INT32, DICT8, FLOAT32], [INT64, DATE32, DICT16], [DICT32, INT32, INT64, FLOAT32],
+])
+def test_plan_is_exact_vs_oracle(types):
+    rng = np.random.default_rng(sum(types) + 5)
+    n = 2000
+    cols, pools = random_table(rng, types, n, with_nan=FLOAT32 in types)
+    paths = set()
+    with np.errstate(over="ignore"):
+        for _ in range(300):
+            node = random_program(rng, types, pools, max_depth=4)
+            prog = encode(node, types)
+            plan = sel.program_plan(prog, types)
+            paths.add(plan["path"])
+            got = np.flatnonzero(emulate_plan(plan, cols, types, n))
+            _, want, _ = oracle.pushdown(cols, types, prog)
+            np.testing.assert_array_equal(got, want, err_msg=str(node))
+    assert paths == {0, 1, 2}
+
+
+def test_plan_paths_of_the_paper_predicates():
+    from selgen import configs
+    for node in configs.c2_probes().values():
+        assert sel.program_path(encode(node, [INT32, INT32, DICT8, INT32]), [INT32, INT32, DICT8, INT32]) == 1
+    assert sel.program_path(encode(Or(Cmp("=", 0, 1), Cmp("=", 1, 2)), [INT32, INT32]), [INT32, INT32]) == 0
+    assert sel.program_path(encode(Or(Cmp("<", 0, 5), Cmp(">=", 0, 5)), [INT32]), [INT32]) == 2
+    # NOT(x < c) on floats keeps NaN rows: never rewritten as x >= c
+    plan = sel.program_plan(encode(Not(Cmp("<", 0, 1.0)), [FLOAT32]), [FLOAT32])
+    assert len(plan["leaves"][0]["lo"]) == 2
+
+
+# ---- predicate builder ---------------------------------------------------------------------------
+
+def test_builder_bytes_match_generator():
+    schema = [("A", INT32, None), ("B", INT32, None), ("C", DICT8, ["a", "b", "c", "d", "e"])]
+    types = [INT32, INT32, DICT8]
+    cases = [
+        ((col("A") == 2) & (col("B") < 2001) & (col("B") > 1000) & ((col("C") == 1) | (col("C") == 4)),
+         And(And(And(Cmp("=", 0, 2), Cmp("<", 1, 2001)), Cmp(">", 1, 1000)), Or(Cmp("=", 2, 1), Cmp("=", 2, 4)))),
+        (col("B").between(-5, 7) | ~col("C").isin([0, 3]), Or(Between(1, -5, 7), Not(In(2, (0, 3))))),
+        (col("C").isin(["b", "e", "zz"]), In(2, (1, 4))),
+        (col("C") == "zz", Const(False)),
+        (col("C") < "c", Cmp("<", 2, 2)),
+        (col("C") <= "bb", Cmp("<=", 2, 1)),
+    ]
+    for expr, node in cases:
+        assert sel.predicate.compile_predicate(expr, schema) == encode(node, types)

@@ -1,0 +1,248 @@
+"""GPU parity: libsel's sm_100a kernels (through the C ABI) vs the CPU oracle, element by element,
+bit-exact (counts, ascending row-id sets and gathered values are unique).
+
+Sizes span several 1024-row warp chunks and 8192-row CTA tiles plus ragged tails; the full-size
+worked example (600M rows, BASELINE.json configs[1]) runs in bench.py's launch configuration and
+is checked against the closed form of its tuple multiset."""
+
+import math
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import paper_1806_08384_b200 as sel
+from selgen import configs
+from selgen.program import (Cmp, Between, In, And, Or, Not, Const, F32Bits, encode, encode_raw,
+                            random_program, INT32, INT64, FLOAT32, DATE32, DICT8, DICT16, DICT32)
+
+from helpers import random_table
+
+pytestmark = pytest.mark.gpu
+
+_TORCH = {INT32: torch.int32, INT64: torch.int64, FLOAT32: torch.float32, DATE32: torch.int32,
+          DICT8: torch.uint8, DICT16: torch.int16, DICT32: torch.int32}
+
+
+@pytest.fixture(scope="module")
+def ctx(cuda_device):
+    c = sel.Context(cuda_device)
+    yield c
+    c.close()
+
+
+def to_gpu(arr, t, dev):
+    a = np.ascontiguousarray(arr)
+    view = {INT32: np.int32, INT64: np.int64, FLOAT32: np.float32, DATE32: np.int32,
+            DICT8: np.uint8, DICT16: np.int16, DICT32: np.int32}[t]
+    return torch.from_numpy(a.view(view).copy()).to(dev)
+
+
+def register(ctx, cols, types, row_offset=0, global_rows=None):
+    names = [f"c{i}" for i in range(len(cols))]
+    tens = [to_gpu(c, t, ctx.device) for c, t in zip(cols, types)]
+    return sel.Table(ctx, names, types, tens, row_offset=row_offset, global_rows=global_rows)
+
+
+def check_parity(table, cols, types, node, proj=None, capacity=None, row_offset=0):
+    prog = encode(node, types)
+    want_count, want_ids, want_cols = oracle.pushdown(cols, types, prog, proj=proj or [],
+                                                      capacity=capacity, row_offset=row_offset)
+    assert table.count(prog) == want_count, node
+    res = table.pushdown(prog, project=proj or [], capacity=capacity)
+    assert res.count == want_count and res.local_count == want_count
+    got_ids = res.rowids.cpu().numpy().view(np.uint32)
+    np.testing.assert_array_equal(got_ids, want_ids, err_msg=str(node))
+    for j, c in enumerate(proj or []):
+        got = res.columns[c].cpu().numpy().view(want_cols[j].dtype)
+        np.testing.assert_array_equal(got, want_cols[j])
+
+
+def test_worked_example_scaled(ctx):
+    n = 6_000_000
+    T = configs.gen_c2(n)
+    cols = [c.numpy() for c in T.columns]
+    t = register(ctx, cols, T.types)
+    for node in configs.c2_probes().values():
+        check_parity(t, cols, T.types, node, proj=configs.C2_PROJECT)
+        assert t.count(encode(node, T.types)) == 1_002_000
+
+
+SIZES = [1, 3, 4, 5, 31, 1023, 1024, 1025, 4097, 8191, 8192, 8193, 65537, 250_003]
+
+
+@pytest.mark.parametrize("n", SIZES)
+def test_random_programs_ragged_sizes(ctx, n):
+    rng = np.random.default_rng(n)
+    types = [INT32, DICT8, INT64, FLOAT32, DICT16, DATE32, DICT32]
+    cols, pools = random_table(rng, types, n)
+    t = register(ctx, cols, types)
+    for _ in range(25):
+        node = random_program(rng, types, pools, max_depth=4)
+        check_parity(t, cols, types, node, proj=[0, 1, 2, 3, 4, 5, 6])
+
+
+def test_float_nan_signed_zero_subnormal(ctx):
+    rng = np.random.default_rng(17)
+    types = [FLOAT32, FLOAT32]
+    cols, pools = random_table(rng, types, 20_000, with_nan=True)
+    t = register(ctx, cols, types)
+    for _ in range(60):
+        check_parity(t, cols, types, random_program(rng, types, pools, max_depth=4), proj=[0])
+    for node in [Cmp("=", 0, 0.0), Not(Cmp("<", 0, 1.0)), Cmp("<", 0, F32Bits(0x7FC00000)),
+                 Not(Cmp("=", 0, F32Bits(0x7FC00000))), Cmp(">", 0, 1e-45), Between(0, -0.0, 0.0)]:
+        check_parity(t, cols, types, node, proj=[1])
+
+
+def test_empty_table_and_constants(ctx):
+    types = [INT32]
+    t = register(ctx, [np.zeros(0, np.int32)], types)
+    for node in [Cmp("=", 0, 1), Const(True), Const(False)]:
+        assert t.count(encode(node, types)) == 0
+        assert t.pushdown(encode(node, types), capacity=10).count == 0
+    x = np.arange(-50, 10_000, dtype=np.int32)
+    t2 = register(ctx, [x], types)
+    for node in [Const(True), Const(False), Or(Cmp("<", 0, 5), Cmp(">=", 0, 5)),
+                 And(Cmp("<", 0, 5), Cmp(">=", 0, 5))]:
+        check_parity(t2, [x], types, node, proj=[0])
+
+
+def test_capacity_gate(ctx):
+    """Algorithm 1: the exact count is always returned; only the first
+    `capacity` ascending rows are written; capacity == count passes (strict '>')."""
+    rng = np.random.default_rng(5)
+    types = [INT32, DICT8]
+    cols, pools = random_table(rng, types, 100_000)
+    t = register(ctx, cols, types)
+    node = Or(Cmp(">", 0, 0), In(1, (1, 2, 255)))
+    prog = encode(node, types)
+    full = oracle.count(cols, types, prog)
+    for cap in [0, 1, 17, 8191, full // 2, full, full + 100]:
+        sentinel = torch.full((max(cap, 1) + 64,), -7, dtype=torch.int32, device=ctx.device)
+        outc = torch.full((max(cap, 1) + 64,), 99, dtype=torch.uint8, device=ctx.device)
+        res = t.pushdown(prog, project=[1], capacity=cap, out=(sentinel, [outc]))
+        assert res.count == full and res.local_count == full
+        assert res.gated == (full > cap)
+        check_parity(t, cols, types, node, proj=[1], capacity=cap)
+        # nothing written past the capacity
+        assert (sentinel[cap:].cpu() == -7).all()
+        assert (outc[cap:].cpu() == 99).all()
+
+
+def test_shard_loop_offsets(ctx):
+    """Register contiguous shards with their global offsets: counts add up, row ids
+    are global, and the concatenation equals the unsharded result."""
+    n = 300_007
+    T = configs.gen_lineitem(n)
+    cols = [c.numpy() for c in T.columns]
+    probes = configs.lineitem_probes(T)
+    cuts = [0, 77_777, 77_778, 200_000, n]
+    for name, node in probes.items():
+        prog = encode(node, T.types)
+        want_c, want_ids, _ = oracle.pushdown(cols, T.types, prog)
+        total, ids = 0, []
+        for s, e in zip(cuts[:-1], cuts[1:]):
+            t = register(ctx, [c[s:e] for c in cols], T.types, row_offset=s, global_rows=n)
+            total += t.count(prog)
+            ids.append(t.pushdown(prog).rowids.cpu().numpy().view(np.uint32))
+        assert total == want_c, name
+        np.testing.assert_array_equal(np.concatenate(ids), want_ids)
+
+
+def test_large_program_block(ctx):
+    """A program at the validator's limits (128 instructions, 512 constants) takes the large
+    parameter block and the interpreter path."""
+    rng = np.random.default_rng(8)
+    instrs = [(0x30, 0, 0, 256), (0x30, 1, 256, 256), (0x41, 0, 0, 0)]
+    k = 0
+    while len(instrs) < 127:
+        instrs += [(0x13 if k % 2 else 0x12, k % 2, int(rng.integers(512)), 0), (0x40 if k % 3 else 0x41, 0, 0, 0)]
+        k += 1
+    instrs.append((0x42, 0, 0, 0))
+    consts = [int(v) for v in rng.integers(-3000, 3000, 512)]
+    prog = encode_raw(instrs, [c & (2**64 - 1) for c in consts])
+    types = [INT32, INT32]
+    x = rng.integers(-3000, 3000, 200_000).astype(np.int32)
+    y = rng.integers(-3000, 3000, 200_000).astype(np.int32)
+    t = register(ctx, [x, y], types)
+    want_c, want_ids, _ = oracle.pushdown([x, y], types, prog)
+    assert t.count(prog) == want_c
+    np.testing.assert_array_equal(t.pushdown(prog).rowids.cpu().numpy().view(np.uint32), want_ids)
+
+
+def test_program_errors_surface(ctx):
+    t = register(ctx, [np.arange(10, dtype=np.int32)], [INT32])
+    with pytest.raises(sel.SelError) as e:
+        t.count(b"SELP\x02\x00")
+    assert e.value.status == 4
+    with pytest.raises(sel.SelError) as e:
+        t.count(encode_raw([(0x10, 0, 0, 0)], [1 << 40]))
+    assert e.value.status == 3
+
+
+def test_alignment_and_size_checks(ctx):
+    x = torch.zeros(100, dtype=torch.int32, device=ctx.device)
+    with pytest.raises(sel.SelError) as e:
+        sel.Table(ctx, ["x"], [INT32], [x[1:]])
+    assert e.value.status == 2
+    with pytest.raises(sel.SelError) as e:
+        sel.Table(ctx, ["x"], [INT32], [x], global_rows=1 << 32)
+    assert e.value.status == 5
+
+
+def test_nccl_single_rank_comm_and_timing(ctx, cuda_device):
+    c = sel.Context(cuda_device)
+    c.set_comm(1, 0, sel.Context.new_unique_id())
+    c.enable_timing(True)
+    T = configs.gen_c2(600_000)
+    cols = [x.numpy() for x in T.columns]
+    t = register(c, cols, T.types)
+    prog = encode(configs.c2_probes()["listing"], T.types)
+    assert t.count(prog) == 100_200
+    assert c.last_kernel_ms() > 0
+    res = t.pushdown(prog, project=[3])
+    assert res.count == 100_200 and res.offset == 0
+    np.testing.assert_array_equal(res.rowids.cpu().numpy().view(np.uint32),
+                                  oracle.pushdown(cols, T.types, prog)[1])
+    c.close()
+
+
+def _closed_form_ids_gpu(T, node, dev):
+    """Closed-form ascending row ids of a C2 predicate, computed on the GPU with torch."""
+    ta, tb, tc, tm = T.meta["tuples"]
+    from helpers import np_mask
+    hit = np_mask(node, [ta.astype(np.int32), tb.astype(np.int32), tc.astype(np.uint8)],
+                  [INT32, INT32, DICT8], len(ta))
+    ends = np.cumsum(tm)
+    starts = ends - tm
+    a, b, _ = T.meta["affine"]
+    parts = []
+    for s, e in zip(starts[hit], ends[hit]):
+        parts.append(torch.arange(int(s), int(e), dtype=torch.int64, device=dev))
+    j = torch.cat(parts)
+    return torch.sort((a * j + b) % T.n_total).values, int(tm[hit].sum())
+
+
+def test_full_size_worked_example(ctx):
+    """BASELINE.json configs[1] at full size (600M rows), in bench.py's launch configuration:
+    exact count 100,200,000 for all encodings, and the push-down row ids / projected
+    columns equal the closed form of the tuple multiset (every one of the 100.2M rows checked)."""
+    dev = ctx.device
+    T = configs.gen_c2(device=dev)
+    t = sel.Table(ctx, ["A", "B", "C", "D"], T.types, [c.data for c in T.columns])
+    for node in configs.c2_probes().values():
+        assert t.count(encode(node, T.types)) == 100_200_000
+    assert t.count(encode(Cmp("=", 0, 2), T.types)) == 120_000_000
+    node = configs.c2_probes()["listing"]
+    want_ids, want_n = _closed_form_ids_gpu(T, node, dev)
+    res = t.pushdown(encode(node, T.types), project=["A", "C", "D"])
+    assert res.count == want_n == 100_200_000
+    got = res.rowids.to(torch.int64) & 0xFFFFFFFF
+    assert torch.equal(got, want_ids)
+    assert bool((res.columns["A"] == 2).all())
+    cc = res.columns["C"]
+    assert bool(((cc == 1) | (cc == 4)).all())
+    assert torch.equal(res.columns["D"], T.col("D").data[got])
+    # the complement partitions the table (count(P) + count(NOT P) = N)
+    assert t.count(encode(Not(node), T.types)) == 600_000_000 - 100_200_000
