@@ -182,11 +182,13 @@ __device__ __forceinline__ uint32_t eval_leaf(const P& p, const DevLeaf& L, uint
     for (int h = 0; h < 2; ++h) {
       uint64_t v[16];
       load_w8_half<TAIL>(col, base, lane, h, nvalid, v);
+      uint32_t mh = 0;
       for (int t = 0; t < L.iv_count; ++t) {
         const uint64_t lo = p.lo[L.iv_begin + t], sp = p.span[L.iv_begin + t];
 #pragma unroll
-        for (int i = 0; i < 16; ++i) m |= (uint32_t)(v[i] - lo <= sp) << (16 * h + i);
+        for (int i = 0; i < 16; ++i) mh |= (v[i] - lo <= sp) ? (1u << i) : 0u;
       }
+      m |= mh << (16 * h);
     }
     return m;
   }
@@ -205,7 +207,7 @@ __device__ __forceinline__ uint32_t eval_leaf(const P& p, const DevLeaf& L, uint
   for (int t = 0; t < L.iv_count; ++t) {
     const uint32_t lo = (uint32_t)p.lo[L.iv_begin + t], sp = (uint32_t)p.span[L.iv_begin + t];
 #pragma unroll
-    for (int i = 0; i < 32; ++i) m |= (uint32_t)(v[i] - lo <= sp) << i;
+    for (int i = 0; i < 32; ++i) m |= (v[i] - lo <= sp) ? (1u << i) : 0u;
   }
   return m;
 }
@@ -290,18 +292,17 @@ __device__ __forceinline__ uint64_t pack_status(uint32_t epoch, uint64_t flag, u
   return ((uint64_t)epoch << 34) | (flag << 32) | value;
 }
 
-template <class P>
-__device__ __forceinline__ void emit_row(const P& p, uint64_t pos, uint64_t row,
-                                         uint32_t* __restrict__ out_ids) {
-  out_ids[pos] = (uint32_t)(p.row_offset + row);
-  for (uint32_t j = 0; j < p.n_proj; ++j) {
-    switch (p.proj_wclass[j]) {
-      case W1: static_cast<uint8_t*>(p.proj_dst[j])[pos] = static_cast<const uint8_t*>(p.proj_src[j])[row]; break;
-      case W2: static_cast<uint16_t*>(p.proj_dst[j])[pos] = static_cast<const uint16_t*>(p.proj_src[j])[row]; break;
-      case W4: static_cast<uint32_t*>(p.proj_dst[j])[pos] = static_cast<const uint32_t*>(p.proj_src[j])[row]; break;
-      default: static_cast<uint64_t*>(p.proj_dst[j])[pos] = static_cast<const uint64_t*>(p.proj_src[j])[row]; break;
-    }
-  }
+// Coalesced write-out of one warp's compacted rows: positions [gbase, gbase + lim) receive the
+// chunk-local rows s_idx[0..lim) (ascending). Stores are consecutive across lanes; gathers read
+// ascending rows of the chunk the warp just evaluated.
+template <class T>
+__device__ __forceinline__ void gather_out(const void* src_v, void* dst_v, uint64_t cbase,
+                                           uint64_t gbase, const uint16_t* s_idx, uint32_t lim,
+                                           int lane) {
+  const T* __restrict__ src = static_cast<const T*>(src_v) + cbase;
+  T* __restrict__ dst = static_cast<T*>(dst_v) + gbase;
+#pragma unroll 4
+  for (uint32_t q = lane; q < lim; q += 32) dst[q] = src[s_idx[q]];
 }
 
 template <class P>
@@ -314,6 +315,7 @@ __global__ void __launch_bounds__(kThreads) pushdown_kernel(
   __shared__ uint64_t s_tile;
   __shared__ uint32_t s_warp_tot[kWarpsPerCta];
   __shared__ uint64_t s_prefix;
+  __shared__ uint16_t s_idx[kWarpsPerCta][kChunkRows];  // 16 KB: compacted chunk-local rows
 
   for (;;) {
     if (threadIdx.x == 0) s_tile = (uint64_t)atomicAdd(ticket, 1ull) - ticket_base;
@@ -362,6 +364,21 @@ __global__ void __launch_bounds__(kThreads) pushdown_kernel(
       agg += t;
     }
 
+    // 2b. stage the chunk-local indices of the selected rows (ascending) in shared memory
+    {
+      uint16_t* my = s_idx[warp];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const uint32_t nib = (m >> (4 * k)) & 0xFu;
+        if (nib == 0) continue;
+        uint32_t pos = stripe_base[k] + (((k < 4 ? e_lo : e_hi) >> (8 * (k & 3))) & 0xFFu);
+        const uint32_t r0 = 4u * (32u * k + lane);
+#pragma unroll
+        for (int e = 0; e < 4; ++e)
+          if (nib & (1u << e)) my[pos++] = (uint16_t)(r0 + e);
+      }
+    }
+
     // 3. decoupled look-back for the tile's exclusive prefix (warp 0)
     if (warp == 0) {
       uint64_t excl = 0;
@@ -397,21 +414,20 @@ __global__ void __launch_bounds__(kThreads) pushdown_kernel(
     const uint64_t tile_prefix = s_prefix;
     if (tile == ntiles - 1 && threadIdx.x == 0) *out_count = tile_prefix + agg;
 
-    // 4. scatter selected rows in ascending order, honouring the capacity gate
-    if (m != 0) {
-      const uint64_t wbase = tile_prefix + woff;
-#pragma unroll
-      for (int k = 0; k < 8; ++k) {
-        const uint32_t nib = (m >> (4 * k)) & 0xFu;
-        if (nib == 0) continue;
-        uint64_t pos = wbase + stripe_base[k] + (((k < 4 ? e_lo : e_hi) >> (8 * (k & 3))) & 0xFFu);
-        const uint64_t row = cbase + 4u * (32u * k + lane);
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          if (nib & (1u << e)) {
-            if (pos < p.capacity) emit_row(p, pos, row + e, out_ids);
-            ++pos;
-          }
+    // 4. coalesced write-out of this warp's slice, honouring the capacity gate
+    const uint64_t gbase = tile_prefix + woff;
+    if (acc != 0 && gbase < p.capacity) {
+      const uint32_t lim = (uint32_t)min((uint64_t)acc, p.capacity - gbase);
+      const uint16_t* my = s_idx[warp];
+      const uint32_t idbase = (uint32_t)(p.row_offset + cbase);
+#pragma unroll 4
+      for (uint32_t q = lane; q < lim; q += 32) out_ids[gbase + q] = idbase + my[q];
+      for (uint32_t j = 0; j < p.n_proj; ++j) {
+        switch (p.proj_wclass[j]) {
+          case W1: gather_out<uint8_t>(p.proj_src[j], p.proj_dst[j], cbase, gbase, my, lim, lane); break;
+          case W2: gather_out<uint16_t>(p.proj_src[j], p.proj_dst[j], cbase, gbase, my, lim, lane); break;
+          case W4: gather_out<uint32_t>(p.proj_src[j], p.proj_dst[j], cbase, gbase, my, lim, lane); break;
+          default: gather_out<uint64_t>(p.proj_src[j], p.proj_dst[j], cbase, gbase, my, lim, lane); break;
         }
       }
     }

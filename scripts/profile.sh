@@ -1,0 +1,14 @@
+#!/bin/bash
+# Run on the GPU box (via gpurun): launch list + one full ncu capture of each probe kernel.
+# Usage: scripts/profile.sh <tag> [bench args...]
+set -u
+TAG=${1:-r1}; shift || true
+ARGS=${*:-"--steps 3 --warmup 3 --no-cpu --no-e2e"}
+mkdir -p gpurun_out
+ncu --metrics gpu__time_duration.sum --clock-control none --csv \
+    --log-file gpurun_out/launches_${TAG}.csv python bench.py $ARGS > gpurun_out/launches_${TAG}.out 2>&1
+for K in pushdown_kernel count_kernel; do
+  ncu --set full --clock-control none --import-source on -k regex:${K} -s 3 -c 1 \
+      -o gpurun_out/prof_${TAG}_${K} -f python bench.py $ARGS > gpurun_out/prof_${TAG}_${K}.out 2>&1
+done
+ls -la gpurun_out
