@@ -93,7 +93,9 @@ sel_status sel_ctx_set_comm(sel_ctx ctx, int nranks, int rank, const void* nccl_
  * failure. */
 sel_status sel_nccl_unique_id(void* out128);
 
-/* Destroys the context and its communicator. Tables registered on it must be released first. */
+/* Destroys the context: frees its device scratch and communicator at once. If tables are still
+ * registered, the context struct is freed when the last of them is released (sel_table_release
+ * stays valid) and probes on them fail with SEL_E_STATE. */
 void sel_ctx_destroy(sel_ctx ctx);
 
 /* Kernel timing (for bench.py's roofline): when enabled, every probe records CUDA events around

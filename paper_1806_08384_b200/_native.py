@@ -8,7 +8,7 @@ import ctypes
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libsel.so")
+LIB_PATH = os.environ.get("SEL_LIB") or os.path.join(HERE, "libsel.so")
 
 SEL_OK, SEL_E_ARG, SEL_E_ALIGN, SEL_E_TYPE, SEL_E_PROGRAM, SEL_E_TOO_LARGE, SEL_E_CUDA, \
     SEL_E_NCCL, SEL_E_STATE = range(9)

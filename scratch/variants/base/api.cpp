@@ -118,7 +118,7 @@ bool known_type(int t) { return t >= SEL_INT32 && t <= SEL_DICT32; }
 struct sel_ctx_s {
   int device = 0;
   int num_sms = 148;
-  int occ_count_small = 1, occ_count_large = 1;
+  int occ_count_small = 1, occ_count_large = 1, occ_push_small = 1, occ_push_large = 1;
   Scratch s{};
   uint64_t* h_result = nullptr;   // pinned: [0] local count, [1..nranks] gathered counts
   uint64_t ticket_base = 0;
@@ -129,7 +129,6 @@ struct sel_ctx_s {
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   float last_ms = 0.f;
   int live_tables = 0;
-  bool destroyed = false;
 };
 
 struct sel_table_s {
@@ -250,10 +249,8 @@ sel_status sel_ctx_create(int cuda_device, sel_ctx* out) {
   cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, cuda_device);
   c->occ_count_small = occupancy_count_small();
   c->occ_count_large = occupancy_count_large();
-  if (prepare_kernels() != cudaSuccess) {
-    delete c;
-    return set_error(SEL_E_CUDA, "cudaFuncSetAttribute(push-down shared memory) failed");
-  }
+  c->occ_push_small = occupancy_pushdown_small();
+  c->occ_push_large = occupancy_pushdown_large();
   const char* env = std::getenv("SEL_CTAS_PER_SM");
   if (env && std::atoi(env) > 0) {
     const int v = std::atoi(env);
@@ -272,7 +269,7 @@ sel_status sel_ctx_create(int cuda_device, sel_ctx* out) {
               cudaDeviceSynchronize() == cudaSuccess;
   if (!okay) {
     cudaError_t le = cudaGetLastError();
-    sel_ctx_destroy(c);  // no tables yet: frees the struct
+    sel_ctx_destroy(c);
     return set_error(SEL_E_CUDA, cuda_msg("context allocation", le));
   }
   *out = c;
@@ -310,11 +307,10 @@ sel_status sel_ctx_set_comm(sel_ctx ctx, int nranks, int rank, const void* nccl_
   return SEL_OK;
 }
 
-namespace {
-void release_ctx_resources(sel_ctx c) {
+void sel_ctx_destroy(sel_ctx c) {
+  if (!c) return;
   DeviceGuard g(c->device);
   if (c->comm && nccl().loaded) nccl().CommDestroy(c->comm);
-  c->comm = nullptr;
   if (c->s.partials) cudaFree(c->s.partials);
   if (c->s.done) cudaFree(c->s.done);
   if (c->s.result) cudaFree(c->s.result);
@@ -323,20 +319,7 @@ void release_ctx_resources(sel_ctx c) {
   if (c->h_result) cudaFreeHost(c->h_result);
   if (c->ev0) cudaEventDestroy(c->ev0);
   if (c->ev1) cudaEventDestroy(c->ev1);
-  c->s = Scratch{};
-  c->h_result = nullptr;
-  c->ev0 = c->ev1 = nullptr;
-}
-}  // namespace
-
-// Destroying a context that still has registered tables releases its device resources at once;
-// the struct itself lives until the last table is released (so a late sel_table_release is safe),
-// and probes on those tables fail with SEL_E_STATE.
-void sel_ctx_destroy(sel_ctx c) {
-  if (!c || c->destroyed) return;
-  release_ctx_resources(c);
-  c->destroyed = true;
-  if (c->live_tables == 0) delete c;
+  delete c;
 }
 
 sel_status sel_ctx_set_timing(sel_ctx ctx, int enable) {
@@ -360,7 +343,6 @@ sel_status sel_table_register(sel_ctx ctx, const sel_column* cols, uint32_t ncol
   clear_error();
   if (!ctx || !cols || !out) return set_error(SEL_E_ARG, "null argument");
   *out = nullptr;
-  if (ctx->destroyed) return set_error(SEL_E_STATE, "context destroyed");
   if (ncols == 0 || ncols > 255) return set_error(SEL_E_ARG, "ncols must be 1..255");
   if (global_rows >= (1ull << 32)) return set_error(SEL_E_TOO_LARGE, "global_rows must be < 2^32");
   if (global_row_offset > global_rows || local_rows > global_rows - global_row_offset)
@@ -388,9 +370,8 @@ sel_status sel_table_register(sel_ctx ctx, const sel_column* cols, uint32_t ncol
 
 void sel_table_release(sel_table t) {
   if (!t) return;
-  sel_ctx c = t->ctx;
+  t->ctx->live_tables--;
   delete t;
-  if (--c->live_tables == 0 && c->destroyed) delete c;
 }
 
 sel_status sel_program_check(const void* prog, size_t prog_bytes, const sel_type* types,
@@ -461,7 +442,6 @@ uint64_t sel_count(sel_table t, const void* prog, size_t prog_bytes, void* cuda_
   clear_error();
   if (!t) return fail64(SEL_E_ARG, "null table");
   sel_ctx c = t->ctx;
-  if (c->destroyed) return fail64(SEL_E_STATE, "context destroyed");
   Plan plan;
   if (plan_for(t, prog, prog_bytes, &plan) != SEL_OK) return SEL_ERR;
   cudaStream_t stream = (cudaStream_t)cuda_stream;
@@ -515,7 +495,6 @@ uint64_t sel_pushdown(sel_table t, const void* prog, size_t prog_bytes, const ui
   clear_error();
   if (!t) return fail64(SEL_E_ARG, "null table");
   sel_ctx c = t->ctx;
-  if (c->destroyed) return fail64(SEL_E_STATE, "context destroyed");
   if (nproj > 0 && !proj_cols) return fail64(SEL_E_ARG, "null proj_cols");
   if (nproj > 255) return fail64(SEL_E_ARG, "nproj must be <= 255");
   for (uint32_t j = 0; j < nproj; ++j)
@@ -536,7 +515,7 @@ uint64_t sel_pushdown(sel_table t, const void* prog, size_t prog_bytes, const ui
   const bool scan = n > 0 && !(plan.path == PATH_CONST && !plan.const_value);
   cudaError_t e;
   if (scan) {
-    const uint64_t ntiles = (n + kChunkRows - 1) / kChunkRows;
+    const uint64_t ntiles = (n + kPdTileRows - 1) / kPdTileRows;
     if (ensure_status(c, ntiles, stream) != SEL_OK) return SEL_ERR;
     if (++c->epoch >= (1u << 30)) {
       e = cudaMemsetAsync(c->s.status, 0, c->s.status_cap * sizeof(uint64_t), stream);
@@ -549,50 +528,23 @@ uint64_t sel_pushdown(sel_table t, const void* prog, size_t prog_bytes, const ui
       p->row_offset = t->row_offset;
       p->capacity = capacity_rows;
       p->n_proj = capacity_rows > 0 ? nproj : 0;
-      // Projected predicate columns are captured in shared memory while the predicate loads them
-      // (no second read from HBM); the rest are gathered from global memory at write-out.
-      std::vector<int> cap_off(t->cols.size(), -1);
-      uint32_t off = kIdxBytes;
       for (uint32_t j = 0; j < p->n_proj; ++j) {
-        const int c = (int)proj_cols[j];
-        const uint32_t w = (uint32_t)width_of(t->types[c]);
-        bool pred_col = false;
-        for (auto& L : plan.leaves) pred_col = pred_col || L.col == c;
-        if (pred_col && cap_off[c] < 0 && off + w * kChunkRows <= kIdxBytes + kCaptureBudget) {
-          cap_off[c] = (int)off;
-          off += w * kChunkRows;
-        }
-        p->proj_src[j] = t->cols[c].data;
+        p->proj_src[j] = t->cols[proj_cols[j]].data;
         p->proj_dst[j] = out_cols[j];
-        p->proj_wclass[j] = wclass_of(t->types[c]);
-        p->proj_cap_off[j] = cap_off[c] >= 0 ? (uint16_t)cap_off[c] : kNoCapture;
+        p->proj_wclass[j] = wclass_of(t->types[proj_cols[j]]);
       }
-      std::vector<bool> marked(t->cols.size(), false);
-      for (size_t i = 0; i < plan.op.size(); ++i) {
-        if (plan.op[i] != DOP_LEAF) continue;
-        const int l = plan.arg[i];
-        const int c = plan.leaves[l].col;
-        if (cap_off[c] >= 0 && !marked[c]) {
-          p->leaf[l].cap = 1;
-          p->leaf[l].cap_off = (uint16_t)cap_off[c];
-          marked[c] = true;
-        }
-      }
-      p->warp_smem = (off + 15u) & ~15u;
     };
     if (c->timing) cudaEventRecord(c->ev0, stream);
     int le, grid;
     if (fits_block<DevProgramSmall>(plan, nslots, nproj)) {
       DevProgramSmall p;
       fill(&p);
-      grid = grid_for(c, (ntiles + kWarpsPerCta - 1) / kWarpsPerCta,
-                      occupancy_pushdown_small((size_t)p.warp_smem * kWarpsPerCta));
+      grid = grid_for(c, (ntiles + kWarpsPerCta - 1) / kWarpsPerCta, c->occ_push_small);
       le = launch_pushdown_small(p, n, out_rowids, grid, c->s, c->ticket_base, c->epoch, stream);
     } else {
       static thread_local DevProgramLarge p;
       fill(&p);
-      grid = grid_for(c, (ntiles + kWarpsPerCta - 1) / kWarpsPerCta,
-                      occupancy_pushdown_large((size_t)p.warp_smem * kWarpsPerCta));
+      grid = grid_for(c, (ntiles + kWarpsPerCta - 1) / kWarpsPerCta, c->occ_push_large);
       le = launch_pushdown_large(p, n, out_rowids, grid, c->s, c->ticket_base, c->epoch, stream);
     }
     if (le != cudaSuccess) {

@@ -19,12 +19,8 @@ constexpr int kWarpsPerCta = 8;              // 256 threads
 constexpr int kThreads = kWarpsPerCta * 32;
 constexpr int kRowsPerThread = 32;           // one 32-bit row mask per thread per chunk
 constexpr int kChunkRows = 32 * kRowsPerThread;        // 1024 rows per warp-chunk
-// Push-down: one warp tile = one 1024-row chunk. Dynamic shared memory per warp holds the
-// compacted chunk-local row indices (u16 x 1024) and captures of projected predicate columns.
-constexpr uint32_t kIdxBytes = 2 * kChunkRows;
-constexpr uint32_t kCaptureBudget = 8 * kChunkRows;     // <= 8 bytes/row of captured columns
-constexpr uint32_t kMaxPushdownSmem = kWarpsPerCta * (kIdxBytes + kCaptureBudget);  // 80 KB
-constexpr uint16_t kNoCapture = 0xFFFF;
+constexpr int kPdChunks = 2;                            // push-down: chunks per warp tile
+constexpr int kPdTileRows = kPdChunks * kChunkRows;     // 2048 rows per push-down warp tile
 constexpr int kMaxDeviceStack = 32;
 
 enum WidthClass : uint8_t { W1 = 0, W2 = 1, W4 = 2, W8 = 3 };
@@ -35,11 +31,9 @@ struct DevLeaf {
   uint8_t slot;      // index into DevProgram::col
   uint8_t wclass;    // WidthClass of the column
   uint8_t fkey;      // 1: FLOAT32 — apply the sortable-key transform before the interval test
-  uint8_t cap;       // push-down: 1 = store the loaded raw values to shared memory at cap_off
+  uint8_t pad;
   uint16_t iv_begin; // first interval in lo[]/span[]
   uint16_t iv_count; // >= 1
-  uint16_t cap_off;  // byte offset of the capture within the warp's shared-memory area
-  uint16_t pad;
 };
 
 // Kernel parameter block (passed by value as a __grid_constant__; no H2D copy per probe).
@@ -51,8 +45,6 @@ struct DevProgramT {
   uint32_t n_leaves;
   uint32_t conj;         // 1: ops are leaf0 AND leaf1 AND ... (no stack needed)
   uint32_t n_proj;
-  uint32_t warp_smem;    // push-down: dynamic shared memory bytes per warp
-  uint32_t pad0;
   uint64_t row_offset;   // global id of local row 0 (push-down ids)
   uint64_t capacity;     // push-down capacity in rows
   uint8_t op[MAXOPS];
@@ -63,7 +55,6 @@ struct DevProgramT {
   uint64_t span[MAXIV];
   const void* proj_src[MAXPROJ];
   void* proj_dst[MAXPROJ];
-  uint16_t proj_cap_off[MAXPROJ];  // kNoCapture: gather from proj_src; else smem capture offset
   uint8_t proj_wclass[MAXPROJ];
 };
 
@@ -91,12 +82,10 @@ int launch_pushdown_small(const DevProgramSmall& p, uint64_t n, uint32_t* out_id
                           const Scratch& s, uint64_t ticket_base, uint32_t epoch, void* stream);
 int launch_pushdown_large(const DevProgramLarge& p, uint64_t n, uint32_t* out_ids, int grid,
                           const Scratch& s, uint64_t ticket_base, uint32_t epoch, void* stream);
-// One-time kernel attributes (dynamic shared memory limit of the push-down kernels).
-int prepare_kernels();
 // Occupancy (CTAs per SM) of each kernel, for persistent-grid sizing.
 int occupancy_count_small();
 int occupancy_count_large();
-int occupancy_pushdown_small(size_t dyn_smem);
-int occupancy_pushdown_large(size_t dyn_smem);
+int occupancy_pushdown_small();
+int occupancy_pushdown_large();
 
 }  // namespace sel

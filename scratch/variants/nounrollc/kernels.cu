@@ -12,12 +12,9 @@
 // 4(32k+l)+e. For a 4-byte column one warp instruction (fixed k) loads 32 x 16 B = 512 contiguous
 // bytes (LDG.128, fully coalesced); 1-, 2- and 8-byte columns load 4/8/32 B per lane per quad
 // with the same row mapping, so every leaf of a program produces masks in the same bit layout and
-// AND/OR combination (NOT was folded into the leaves by the host) is one LOP per 32 rows.
-//
-// Toolchain note (nvcc 12.9, sm_100a): when eval_leaf's dynamic interval loop was instantiated
-// twice by unrolling an enclosing loop, the second instance produced wrong masks (intervals >= 2
-// lost). Every loop enclosing eval_leaf is therefore kept rolled; tests/test_gpu_parity.py
-// exercises multi-interval leaves of every width in both kernels.
+// AND/OR/NOT-free combination (NOT was folded into the leaves by the host) is one LOP per 32 rows.
+// Counting is popc per lane, a warp redux, a CTA reduction and one partial per CTA; the last CTA
+// to finish sums the partials (self-resetting, so no memset is needed between probes).
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -44,16 +41,13 @@ __device__ __forceinline__ uint32_t ld_stream_u32(const void* p) {
   return r;
 }
 
-// Tile status words carry their own payload (epoch | flag | value in one 64-bit word, single-copy
-// atomic), so the look-back needs no acquire/release ordering: relaxed gpu-scope accesses only
-// (an acquire load would emit CCTL.IVALL, an L1 invalidation, on every poll).
-__device__ __forceinline__ uint64_t ld_relaxed_u64(const uint64_t* p) {
+__device__ __forceinline__ uint64_t ld_acquire_u64(const uint64_t* p) {
   uint64_t v;
-  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
   return v;
 }
-__device__ __forceinline__ void st_relaxed_u64(uint64_t* p, uint64_t v) {
-  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+__device__ __forceinline__ void st_release_u64(uint64_t* p, uint64_t v) {
+  asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 
 // FLOAT32 sortable key (canon.cpp): sign ? ~bits : bits | 0x80000000.
@@ -74,13 +68,9 @@ __device__ __forceinline__ uint32_t valid_mask(int lane, uint32_t nvalid) {
 }
 
 // ---- per-width loaders: v[4k+e] = value of row 4(32k+lane)+e of the chunk at `base` ---------
-// With cap != nullptr the raw quads are also stored to `cap` (shared memory, chunk row r at
-// cap + r*w), so a projected predicate column is never read from global memory a second time.
-// (A runtime pointer, not a template flag: one inlined copy of the interval loop per TAIL variant,
-// see the toolchain note above.)
 template <bool TAIL>
 __device__ __forceinline__ void load_w4(const void* col, uint64_t base, int lane, uint32_t nvalid,
-                                        uint32_t (&v)[32], char* cap) {
+                                        uint32_t (&v)[32]) {
   const uint32_t* c = static_cast<const uint32_t*>(col) + base;
   uint4 x[8];
 #pragma unroll
@@ -97,7 +87,6 @@ __device__ __forceinline__ void load_w4(const void* col, uint64_t base, int lane
   }
 #pragma unroll
   for (int k = 0; k < 8; ++k) {
-    if (cap) reinterpret_cast<uint4*>(cap)[32 * k + lane] = x[k];
     v[4 * k + 0] = x[k].x;
     v[4 * k + 1] = x[k].y;
     v[4 * k + 2] = x[k].z;
@@ -107,7 +96,7 @@ __device__ __forceinline__ void load_w4(const void* col, uint64_t base, int lane
 
 template <bool TAIL>
 __device__ __forceinline__ void load_w2(const void* col, uint64_t base, int lane, uint32_t nvalid,
-                                        uint32_t (&v)[32], char* cap) {
+                                        uint32_t (&v)[32]) {
   const uint16_t* c = static_cast<const uint16_t*>(col) + base;
   uint2 x[8];
 #pragma unroll
@@ -124,7 +113,6 @@ __device__ __forceinline__ void load_w2(const void* col, uint64_t base, int lane
   }
 #pragma unroll
   for (int k = 0; k < 8; ++k) {
-    if (cap) reinterpret_cast<uint2*>(cap)[32 * k + lane] = x[k];
     v[4 * k + 0] = x[k].x & 0xFFFFu;
     v[4 * k + 1] = x[k].x >> 16;
     v[4 * k + 2] = x[k].y & 0xFFFFu;
@@ -134,7 +122,7 @@ __device__ __forceinline__ void load_w2(const void* col, uint64_t base, int lane
 
 template <bool TAIL>
 __device__ __forceinline__ void load_w1(const void* col, uint64_t base, int lane, uint32_t nvalid,
-                                        uint32_t (&v)[32], char* cap) {
+                                        uint32_t (&v)[32]) {
   const uint8_t* c = static_cast<const uint8_t*>(col) + base;
   uint32_t x[8];
 #pragma unroll
@@ -150,7 +138,6 @@ __device__ __forceinline__ void load_w1(const void* col, uint64_t base, int lane
   }
 #pragma unroll
   for (int k = 0; k < 8; ++k) {
-    if (cap) reinterpret_cast<uint32_t*>(cap)[32 * k + lane] = x[k];
 #pragma unroll
     for (int e = 0; e < 4; ++e) v[4 * k + e] = __byte_perm(x[k], 0u, 0x4440 | e);
   }
@@ -159,7 +146,7 @@ __device__ __forceinline__ void load_w1(const void* col, uint64_t base, int lane
 // 8-byte columns, half a chunk at a time (k = 4h .. 4h+3) to bound registers.
 template <bool TAIL>
 __device__ __forceinline__ void load_w8_half(const void* col, uint64_t base, int lane, int h,
-                                             uint32_t nvalid, uint64_t (&v)[16], char* cap) {
+                                             uint32_t nvalid, uint64_t (&v)[16]) {
   const uint64_t* c = static_cast<const uint64_t*>(col) + base;
   uint4 x[8];
 #pragma unroll
@@ -177,11 +164,6 @@ __device__ __forceinline__ void load_w8_half(const void* col, uint64_t base, int
   }
 #pragma unroll
   for (int kk = 0; kk < 4; ++kk) {
-    if (cap) {
-      uint4* dst = reinterpret_cast<uint4*>(cap) + 2 * (32 * (4 * h + kk) + lane);
-      dst[0] = x[2 * kk];
-      dst[1] = x[2 * kk + 1];
-    }
     v[4 * kk + 0] = ((uint64_t)x[2 * kk].y << 32) | x[2 * kk].x;
     v[4 * kk + 1] = ((uint64_t)x[2 * kk].w << 32) | x[2 * kk].z;
     v[4 * kk + 2] = ((uint64_t)x[2 * kk + 1].y << 32) | x[2 * kk + 1].x;
@@ -190,19 +172,19 @@ __device__ __forceinline__ void load_w8_half(const void* col, uint64_t base, int
 }
 
 // One leaf: bit i of the result <=> row i of the lane's 32 rows lies in the leaf's interval set.
-template <bool TAIL>
-__device__ __forceinline__ uint32_t leaf_mask(const void* col, const DevLeaf& L,
-                                              const uint64_t* lo_tab, const uint64_t* span_tab,
-                                              uint64_t base, int lane, uint32_t nvalid, char* cap) {
+template <bool TAIL, class P>
+__device__ __forceinline__ uint32_t eval_leaf(const P& p, const DevLeaf& L, uint64_t base,
+                                              int lane, uint32_t nvalid) {
+  const void* col = p.col[L.slot];
   uint32_t m = 0;
   if (L.wclass == W8) {
-#pragma unroll 1  // one instance of the interval loop (see the toolchain note above)
+#pragma unroll
     for (int h = 0; h < 2; ++h) {
       uint64_t v[16];
-      load_w8_half<TAIL>(col, base, lane, h, nvalid, v, cap);
+      load_w8_half<TAIL>(col, base, lane, h, nvalid, v);
       uint32_t mh = 0;
       for (int t = 0; t < L.iv_count; ++t) {
-        const uint64_t lo = lo_tab[L.iv_begin + t], sp = span_tab[L.iv_begin + t];
+        const uint64_t lo = p.lo[L.iv_begin + t], sp = p.span[L.iv_begin + t];
 #pragma unroll
         for (int i = 0; i < 16; ++i) mh |= (v[i] - lo <= sp) ? (1u << i) : 0u;
       }
@@ -212,62 +194,51 @@ __device__ __forceinline__ uint32_t leaf_mask(const void* col, const DevLeaf& L,
   }
   uint32_t v[32];
   if (L.wclass == W4) {
-    load_w4<TAIL>(col, base, lane, nvalid, v, cap);
+    load_w4<TAIL>(col, base, lane, nvalid, v);
     if (L.fkey) {
 #pragma unroll
       for (int i = 0; i < 32; ++i) v[i] = fkey(v[i]);
     }
   } else if (L.wclass == W1) {
-    load_w1<TAIL>(col, base, lane, nvalid, v, cap);
+    load_w1<TAIL>(col, base, lane, nvalid, v);
   } else {
-    load_w2<TAIL>(col, base, lane, nvalid, v, cap);
+    load_w2<TAIL>(col, base, lane, nvalid, v);
   }
   for (int t = 0; t < L.iv_count; ++t) {
-    const uint32_t lo = (uint32_t)lo_tab[L.iv_begin + t], sp = (uint32_t)span_tab[L.iv_begin + t];
+    const uint32_t lo = (uint32_t)p.lo[L.iv_begin + t], sp = (uint32_t)p.span[L.iv_begin + t];
 #pragma unroll
     for (int i = 0; i < 32; ++i) m |= (v[i] - lo <= sp) ? (1u << i) : 0u;
   }
   return m;
 }
 
-template <bool TAIL, bool CAP, class P>
-__device__ __forceinline__ uint32_t eval_leaf(const P& p, const DevLeaf& L, uint64_t base,
-                                              int lane, uint32_t nvalid, char* wsmem) {
-  const void* col = p.col[L.slot];
-  char* cap = (CAP && L.cap) ? wsmem + L.cap_off : nullptr;
-  return leaf_mask<TAIL>(col, L, p.lo, p.span, base, lane, nvalid, cap);
-}
-
 // The whole predicate over the lane's 32 rows of the chunk at `base` (nvalid rows valid).
-// One eval_leaf call site (conjunctions just AND into an accumulator instead of using the stack),
-// so each TAIL variant inlines a single copy of the interval loop (toolchain note above).
-template <bool TAIL, bool CAP, class P>
+template <bool TAIL, class P>
 __device__ __forceinline__ uint32_t eval_program(const P& p, uint64_t base, int lane,
-                                                 uint32_t nvalid, char* wsmem) {
-  uint32_t st[kMaxDeviceStack];
-  int sp = 0;
-  uint32_t acc = 0xFFFFFFFFu;
-  const bool conj = p.conj != 0;
-#pragma unroll 1
-  for (uint32_t i = 0; i < p.n_ops; ++i) {
-    const uint8_t op = p.op[i];
-    if (op == DOP_LEAF) {
-      const uint32_t r = eval_leaf<TAIL, CAP>(p, p.leaf[p.arg[i]], base, lane, nvalid, wsmem);
-      if (conj) acc &= r;
-      else st[sp++] = r;
-    } else if (!conj) {
-      --sp;
-      st[sp - 1] = op == DOP_AND ? (st[sp - 1] & st[sp]) : (st[sp - 1] | st[sp]);
+                                                 uint32_t nvalid) {
+  uint32_t m;
+  if (p.conj) {
+    m = 0xFFFFFFFFu;
+    for (uint32_t l = 0; l < p.n_leaves; ++l) m &= eval_leaf<TAIL>(p, p.leaf[l], base, lane, nvalid);
+  } else {
+    uint32_t st[kMaxDeviceStack];
+    int sp = 0;
+    for (uint32_t i = 0; i < p.n_ops; ++i) {
+      const uint8_t op = p.op[i];
+      if (op == DOP_LEAF) {
+        st[sp++] = eval_leaf<TAIL>(p, p.leaf[p.arg[i]], base, lane, nvalid);
+      } else {
+        --sp;
+        st[sp - 1] = op == DOP_AND ? (st[sp - 1] & st[sp]) : (st[sp - 1] | st[sp]);
+      }
     }
+    m = st[0];
   }
-  uint32_t m = conj ? acc : st[0];
   if (TAIL) m &= valid_mask(lane, nvalid);
   return m;
 }
 
 // ---- count ----------------------------------------------------------------------------------
-// Persistent grid-stride over warp-chunks; per-lane popc, warp redux, CTA reduction, one partial
-// per CTA; the last CTA to finish sums the partials (self-resetting: no memset between probes).
 template <class P>
 __global__ void __launch_bounds__(kThreads) count_kernel(const __grid_constant__ P p, uint64_t n,
                                                          uint64_t* __restrict__ partials,
@@ -280,9 +251,8 @@ __global__ void __launch_bounds__(kThreads) count_kernel(const __grid_constant__
   const uint64_t nw = (uint64_t)gridDim.x * kWarpsPerCta;
   uint32_t cnt = 0;
   for (uint64_t c = gw; c < nfull; c += nw)
-    cnt += __popc(eval_program<false, false>(p, c * kChunkRows, lane, kChunkRows, nullptr));
-  if (rem != 0 && gw == nfull % nw)
-    cnt += __popc(eval_program<true, false>(p, nfull * kChunkRows, lane, rem, nullptr));
+    cnt += __popc(eval_program<false>(p, c * kChunkRows, lane, kChunkRows));
+  if (rem != 0 && gw == nfull % nw) cnt += __popc(eval_program<true>(p, nfull * kChunkRows, lane, rem));
   cnt = __reduce_add_sync(0xFFFFFFFFu, cnt);
 
   __shared__ uint32_t s_warp[kWarpsPerCta];
@@ -298,7 +268,7 @@ __global__ void __launch_bounds__(kThreads) count_kernel(const __grid_constant__
     s_last = atomicAdd(done, 1u) == gridDim.x - 1;
   }
   __syncthreads();
-  if (s_last) {
+  if (s_last) {  // the last CTA to finish sums every partial
     __threadfence();
     uint64_t s = 0;
     for (uint32_t b = threadIdx.x; b < gridDim.x; b += kThreads) s += ((volatile uint64_t*)partials)[b];
@@ -322,104 +292,100 @@ __device__ __forceinline__ uint64_t pack_status(uint32_t epoch, uint64_t flag, u
   return ((uint64_t)epoch << 34) | (flag << 32) | value;
 }
 
-// Write-out of a projected column gathered from global memory (non-predicate columns): the
-// chunk-local rows s_idx[0..lim) ascending; batches of 8 loads in flight per lane before stores.
+// Coalesced write-out of one warp's compacted rows: positions [gbase, gbase + lim) receive the
+// chunk-local rows s_idx[0..lim) (ascending). Stores are consecutive across lanes; gathers read
+// ascending rows of the chunk the warp just evaluated.
 template <class T>
-__device__ __forceinline__ void gather_global(const void* src_v, void* dst_v, uint64_t cbase,
-                                              uint64_t gbase, const uint16_t* s_idx, uint32_t lim,
-                                              int lane) {
+__device__ __forceinline__ void gather_out(const void* src_v, void* dst_v, uint64_t cbase,
+                                           uint64_t gbase, const uint16_t* s_idx, uint32_t lim,
+                                           int lane) {
   const T* __restrict__ src = static_cast<const T*>(src_v) + cbase;
-  T* __restrict__ dst = static_cast<T*>(dst_v) + gbase;
-  uint32_t q = lane;
-  for (; q + 7 * 32 < lim; q += 8 * 32) {
-    T v[8];
-#pragma unroll
-    for (int u = 0; u < 8; ++u) v[u] = __ldg(src + s_idx[q + 32 * u]);
-#pragma unroll
-    for (int u = 0; u < 8; ++u) dst[q + 32 * u] = v[u];
-  }
-  for (; q < lim; q += 32) dst[q] = __ldg(src + s_idx[q]);
-}
-
-// Write-out of a projected predicate column from its shared-memory capture.
-template <class T>
-__device__ __forceinline__ void gather_smem(const char* cap, void* dst_v, uint64_t gbase,
-                                            const uint16_t* s_idx, uint32_t lim, int lane) {
-  const T* src = reinterpret_cast<const T*>(cap);
   T* __restrict__ dst = static_cast<T*>(dst_v) + gbase;
 #pragma unroll 4
   for (uint32_t q = lane; q < lim; q += 32) dst[q] = src[s_idx[q]];
 }
 
 // Warp-granular single-pass compaction. Every warp runs independently (no CTA barriers): it draws
-// a 1024-row tile from a global ticket counter (tickets are handed out in order, so every tile a
-// warp waits on belongs to a warp that is already running: forward progress), evaluates the
-// predicate (capturing projected predicate columns into its shared-memory area), scans its
-// per-stripe counts, publishes its aggregate, resolves its exclusive prefix by decoupled
-// look-back over up to 32 predecessors per step, publishes the inclusive prefix, stages the
-// ascending chunk-local indices of the selected rows and writes row ids + projected columns with
-// coalesced stores. Dynamic shared memory per warp: [u16 s_idx[1024] | captures].
+// a tile of kPdChunks x 1024 rows from a global ticket counter (tickets are handed out in order, so
+// every tile a warp waits on belongs to a warp that is already running: forward progress), evaluates
+// the predicate, scans its per-stripe counts, publishes its aggregate, resolves its exclusive
+// prefix by decoupled look-back over up to 32 predecessors per step, publishes the inclusive
+// prefix, stages the ascending tile-local indices of the selected rows in shared memory and writes
+// row ids + projected columns with coalesced stores.
 template <class P>
-__global__ void __launch_bounds__(kThreads, 3) pushdown_kernel(
+__global__ void __launch_bounds__(kThreads) pushdown_kernel(
     const __grid_constant__ P p, uint64_t n, uint32_t* __restrict__ out_ids,
     unsigned long long* __restrict__ ticket, uint64_t ticket_base, uint64_t* __restrict__ status,
     uint32_t epoch, uint64_t* __restrict__ out_count) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const uint64_t ntiles = (n + kChunkRows - 1) / kChunkRows;
-  extern __shared__ __align__(16) char s_dyn[];
-  char* wsmem = s_dyn + (size_t)warp * p.warp_smem;
-  uint16_t* my = reinterpret_cast<uint16_t*>(wsmem);
+  const uint64_t ntiles = (n + kPdTileRows - 1) / kPdTileRows;
+  __shared__ uint16_t s_idx[kWarpsPerCta][kPdTileRows];  // compacted tile-local rows
+  uint16_t* my = s_idx[warp];
 
   for (;;) {
     unsigned long long tk = 0;
     if (lane == 0) tk = atomicAdd(ticket, 1ull);
     const uint64_t tile = __shfl_sync(0xFFFFFFFFu, tk, 0) - ticket_base;
     if (tile >= ntiles) break;
-    const uint64_t cbase = tile * kChunkRows;
-    const uint32_t nvalid = n - cbase >= (uint64_t)kChunkRows ? (uint32_t)kChunkRows : (uint32_t)(n - cbase);
+    const uint64_t tbase = tile * kPdTileRows;
 
-    // 1. evaluate (and capture)
-    const uint32_t m = nvalid == kChunkRows ? eval_program<false, true>(p, cbase, lane, kChunkRows, wsmem)
-                                            : eval_program<true, true>(p, cbase, lane, nvalid, wsmem);
+    // 1. evaluate the tile's chunks
+    uint32_t m[kPdChunks];
+#pragma unroll 1
+    for (int c = 0; c < kPdChunks; ++c) {
+      const uint64_t cbase = tbase + (uint64_t)c * kChunkRows;
+      const uint32_t nvalid = cbase >= n ? 0u : (n - cbase >= (uint64_t)kChunkRows ? (uint32_t)kChunkRows : (uint32_t)(n - cbase));
+      m[c] = 0;
+      if (nvalid == kChunkRows) m[c] = eval_program<false>(p, cbase, lane, kChunkRows);
+      else if (nvalid > 0) m[c] = eval_program<true>(p, cbase, lane, nvalid);
+    }
 
     // 2. warp scan of per-quad-stripe counts (4 stripes of 8 bits per word; fields <= 128)
-    uint32_t cw[2], ex[2], tot[2];
-    cw[0] = cw[1] = 0;
+    uint32_t cw[2 * kPdChunks], ex[2 * kPdChunks], tot[2 * kPdChunks];
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      cw[0] |= (uint32_t)__popc((m >> (4 * k)) & 0xFu) << (8 * k);
-      cw[1] |= (uint32_t)__popc((m >> (4 * (k + 4))) & 0xFu) << (8 * k);
+    for (int c = 0; c < kPdChunks; ++c) {
+      uint32_t lo = 0, hi = 0;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        lo |= (uint32_t)__popc((m[c] >> (4 * k)) & 0xFu) << (8 * k);
+        hi |= (uint32_t)__popc((m[c] >> (4 * (k + 4))) & 0xFu) << (8 * k);
+      }
+      cw[2 * c] = lo;
+      cw[2 * c + 1] = hi;
     }
-    ex[0] = cw[0];
-    ex[1] = cw[1];
+#pragma unroll
+    for (int w = 0; w < 2 * kPdChunks; ++w) ex[w] = cw[w];
 #pragma unroll
     for (int d = 1; d < 32; d <<= 1) {
-      const uint32_t t0 = __shfl_up_sync(0xFFFFFFFFu, ex[0], d);
-      const uint32_t t1 = __shfl_up_sync(0xFFFFFFFFu, ex[1], d);
-      if (lane >= d) { ex[0] += t0; ex[1] += t1; }
+#pragma unroll
+      for (int w = 0; w < 2 * kPdChunks; ++w) {
+        const uint32_t t = __shfl_up_sync(0xFFFFFFFFu, ex[w], d);
+        if (lane >= d) ex[w] += t;
+      }
     }
-    tot[0] = __shfl_sync(0xFFFFFFFFu, ex[0], 31);
-    tot[1] = __shfl_sync(0xFFFFFFFFu, ex[1], 31);
-    ex[0] -= cw[0];
-    ex[1] -= cw[1];
-    uint32_t stripe_base[8];
+#pragma unroll
+    for (int w = 0; w < 2 * kPdChunks; ++w) {
+      tot[w] = __shfl_sync(0xFFFFFFFFu, ex[w], 31);
+      ex[w] -= cw[w];                          // exclusive, per field (no borrows: ex <= inclusive)
+    }
+    uint32_t stripe_base[8 * kPdChunks];
     uint32_t acc = 0;
 #pragma unroll
-    for (int k = 0; k < 8; ++k) {
-      stripe_base[k] = acc;
-      acc += (tot[k >> 2] >> (8 * (k & 3))) & 0xFFu;
+    for (int sidx = 0; sidx < 8 * kPdChunks; ++sidx) {
+      stripe_base[sidx] = acc;
+      acc += (tot[sidx >> 2] >> (8 * (sidx & 3))) & 0xFFu;
     }
 
     // 3. publish the aggregate, look back for the exclusive prefix, publish the inclusive prefix
     uint64_t excl = 0;
     if (tile == 0) {
-      if (lane == 0) st_relaxed_u64(&status[0], pack_status(epoch, kFlagPrefix, acc));
+      if (lane == 0) st_release_u64(&status[0], pack_status(epoch, kFlagPrefix, acc));
     } else {
-      if (lane == 0) st_relaxed_u64(&status[tile], pack_status(epoch, kFlagAgg, acc));
+      if (lane == 0) st_release_u64(&status[tile], pack_status(epoch, kFlagAgg, acc));
       int64_t j = (int64_t)tile - 1;
       for (;;) {
         const int64_t idx = j - lane;
-        const uint64_t sw = idx >= 0 ? ld_relaxed_u64(&status[idx]) : pack_status(epoch, kFlagPrefix, 0);
+        const uint64_t sw = idx >= 0 ? ld_acquire_u64(&status[idx]) : pack_status(epoch, kFlagPrefix, 0);
         const uint64_t flag = (sw >> 32) & 3u;
         const bool ready = (uint32_t)(sw >> 34) == epoch && flag != 0;
         const uint32_t notready = __ballot_sync(0xFFFFFFFFu, !ready);
@@ -436,24 +402,25 @@ __global__ void __launch_bounds__(kThreads, 3) pushdown_kernel(
         j -= lim;
         if (lim == 0) __nanosleep(20);
       }
-      if (lane == 0) st_relaxed_u64(&status[tile], pack_status(epoch, kFlagPrefix, (uint32_t)(excl + acc)));
+      if (lane == 0) st_release_u64(&status[tile], pack_status(epoch, kFlagPrefix, (uint32_t)(excl + acc)));
     }
     if (tile == ntiles - 1 && lane == 0) *out_count = excl + acc;
-    if (acc == 0) {
-      __syncwarp();
-      continue;
-    }
+    if (acc == 0) continue;
 
-    // 4. stage the chunk-local indices of the selected rows, ascending
+    // 4. stage the tile-local indices of the selected rows, ascending
 #pragma unroll
-    for (int k = 0; k < 8; ++k) {
-      const uint32_t nib = (m >> (4 * k)) & 0xFu;
-      if (nib == 0) continue;
-      uint32_t pos = stripe_base[k] + ((ex[k >> 2] >> (8 * (k & 3))) & 0xFFu);
-      const uint32_t r0 = 4u * (32u * k + lane);
+    for (int c = 0; c < kPdChunks; ++c) {
 #pragma unroll
-      for (int e = 0; e < 4; ++e)
-        if (nib & (1u << e)) my[pos++] = (uint16_t)(r0 + e);
+      for (int k = 0; k < 8; ++k) {
+        const uint32_t nib = (m[c] >> (4 * k)) & 0xFu;
+        if (nib == 0) continue;
+        const int sidx = 8 * c + k;
+        uint32_t pos = stripe_base[sidx] + ((ex[sidx >> 2] >> (8 * (sidx & 3))) & 0xFFu);
+        const uint32_t r0 = (uint32_t)c * kChunkRows + 4u * (32u * k + lane);
+#pragma unroll
+        for (int e = 0; e < 4; ++e)
+          if (nib & (1u << e)) my[pos++] = (uint16_t)(r0 + e);
+      }
     }
     __syncwarp();
 
@@ -461,38 +428,26 @@ __global__ void __launch_bounds__(kThreads, 3) pushdown_kernel(
     const uint64_t gbase = excl;
     if (gbase < p.capacity) {
       const uint32_t lim = (uint32_t)min((uint64_t)acc, p.capacity - gbase);
-      const uint32_t idbase = (uint32_t)(p.row_offset + cbase);
+      const uint32_t idbase = (uint32_t)(p.row_offset + tbase);
 #pragma unroll 4
       for (uint32_t q = lane; q < lim; q += 32) out_ids[gbase + q] = idbase + my[q];
-#pragma unroll 1
       for (uint32_t j = 0; j < p.n_proj; ++j) {
-        const uint16_t co = p.proj_cap_off[j];
-        if (co != kNoCapture) {
-          const char* cap = wsmem + co;
-          switch (p.proj_wclass[j]) {
-            case W1: gather_smem<uint8_t>(cap, p.proj_dst[j], gbase, my, lim, lane); break;
-            case W2: gather_smem<uint16_t>(cap, p.proj_dst[j], gbase, my, lim, lane); break;
-            case W4: gather_smem<uint32_t>(cap, p.proj_dst[j], gbase, my, lim, lane); break;
-            default: gather_smem<uint64_t>(cap, p.proj_dst[j], gbase, my, lim, lane); break;
-          }
-        } else {
-          switch (p.proj_wclass[j]) {
-            case W1: gather_global<uint8_t>(p.proj_src[j], p.proj_dst[j], cbase, gbase, my, lim, lane); break;
-            case W2: gather_global<uint16_t>(p.proj_src[j], p.proj_dst[j], cbase, gbase, my, lim, lane); break;
-            case W4: gather_global<uint32_t>(p.proj_src[j], p.proj_dst[j], cbase, gbase, my, lim, lane); break;
-            default: gather_global<uint64_t>(p.proj_src[j], p.proj_dst[j], cbase, gbase, my, lim, lane); break;
-          }
+        switch (p.proj_wclass[j]) {
+          case W1: gather_out<uint8_t>(p.proj_src[j], p.proj_dst[j], tbase, gbase, my, lim, lane); break;
+          case W2: gather_out<uint16_t>(p.proj_src[j], p.proj_dst[j], tbase, gbase, my, lim, lane); break;
+          case W4: gather_out<uint32_t>(p.proj_src[j], p.proj_dst[j], tbase, gbase, my, lim, lane); break;
+          default: gather_out<uint64_t>(p.proj_src[j], p.proj_dst[j], tbase, gbase, my, lim, lane); break;
         }
       }
     }
-    __syncwarp();  // `my` and the captures are rewritten by the next tile
+    __syncwarp();  // `my` is rewritten by the next tile
   }
 }
 
 template <class Kern>
-int occupancy_of(Kern k, size_t dyn_smem) {
+int occupancy_of(Kern k) {
   int blocks = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, k, kThreads, dyn_smem) != cudaSuccess) return 1;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, k, kThreads, 0) != cudaSuccess) return 1;
   return blocks > 0 ? blocks : 1;
 }
 
@@ -508,28 +463,19 @@ int launch_count_large(const DevProgramLarge& p, uint64_t n, int grid, const Scr
 }
 int launch_pushdown_small(const DevProgramSmall& p, uint64_t n, uint32_t* out_ids, int grid,
                           const Scratch& s, uint64_t ticket_base, uint32_t epoch, void* st) {
-  pushdown_kernel<DevProgramSmall><<<grid, kThreads, (size_t)p.warp_smem * kWarpsPerCta, (cudaStream_t)st>>>(
+  pushdown_kernel<DevProgramSmall><<<grid, kThreads, 0, (cudaStream_t)st>>>(
       p, n, out_ids, s.ticket, ticket_base, s.status, epoch, s.result);
   return (int)cudaGetLastError();
 }
 int launch_pushdown_large(const DevProgramLarge& p, uint64_t n, uint32_t* out_ids, int grid,
                           const Scratch& s, uint64_t ticket_base, uint32_t epoch, void* st) {
-  pushdown_kernel<DevProgramLarge><<<grid, kThreads, (size_t)p.warp_smem * kWarpsPerCta, (cudaStream_t)st>>>(
+  pushdown_kernel<DevProgramLarge><<<grid, kThreads, 0, (cudaStream_t)st>>>(
       p, n, out_ids, s.ticket, ticket_base, s.status, epoch, s.result);
   return (int)cudaGetLastError();
 }
-int prepare_kernels() {
-  const int bytes = (int)kMaxPushdownSmem;
-  cudaError_t e = cudaFuncSetAttribute(pushdown_kernel<DevProgramSmall>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
-  if (e == cudaSuccess)
-    e = cudaFuncSetAttribute(pushdown_kernel<DevProgramLarge>,
-                             cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
-  return (int)e;
-}
-int occupancy_count_small() { return occupancy_of(count_kernel<DevProgramSmall>, 0); }
-int occupancy_count_large() { return occupancy_of(count_kernel<DevProgramLarge>, 0); }
-int occupancy_pushdown_small(size_t dyn_smem) { return occupancy_of(pushdown_kernel<DevProgramSmall>, dyn_smem); }
-int occupancy_pushdown_large(size_t dyn_smem) { return occupancy_of(pushdown_kernel<DevProgramLarge>, dyn_smem); }
+int occupancy_count_small() { return occupancy_of(count_kernel<DevProgramSmall>); }
+int occupancy_count_large() { return occupancy_of(count_kernel<DevProgramLarge>); }
+int occupancy_pushdown_small() { return occupancy_of(pushdown_kernel<DevProgramSmall>); }
+int occupancy_pushdown_large() { return occupancy_of(pushdown_kernel<DevProgramLarge>); }
 
 }  // namespace sel

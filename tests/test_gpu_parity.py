@@ -246,3 +246,15 @@ def test_full_size_worked_example(ctx):
     assert torch.equal(res.columns["D"], T.col("D").data[got])
     # the complement partitions the table (count(P) + count(NOT P) = N)
     assert t.count(encode(Not(node), T.types)) == 600_000_000 - 100_200_000
+
+
+def test_context_destroyed_before_table(cuda_device):
+    """A table released (or garbage-collected) after its context was destroyed is safe; probes on
+    it report SEL_E_STATE instead of touching freed memory."""
+    c = sel.Context(cuda_device)
+    t = register(c, [np.arange(100, dtype=np.int32)], [INT32])
+    c.close()
+    with pytest.raises(sel.SelError) as e:
+        t.count(encode(Cmp("<", 0, 5), [INT32]))
+    assert e.value.status == 8
+    t.release()
