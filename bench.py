@@ -74,16 +74,30 @@ def shard(n, world, rank):
     return n * rank // world, n * (rank + 1) // world
 
 
-def algo_bytes(table, prog_cols, proj, local_count):
-    """SURVEY §8d algorithmic bytes: count = rows x sum of distinct predicate-column widths (+8 B
-    result); push-down = the count bytes + selected x (non-predicate projected widths) read +
-    selected x (4 + projected widths) written."""
+def algo_bytes(table, prog_cols, proj, local_count, pushdown_path=0):
+    """Algorithmic bytes.
+    step  = what COUNT + push-down must move once (e.g. C2: 5.4 GB scan + 0.40 GB of D
+            read + 1.303 GB written = 7.10 GB): rows x distinct predicate widths + selected x
+            non-predicate projected widths + selected x (4 + projected widths) + 8 B count.
+            Implementation-independent: the same figure divides both arms' step times.
+    count kernel = rows x distinct predicate widths + 8 B.
+    push-down kernel, by the path it took:
+      single pass (0): the count scan + selected x non-predicate projected widths + writes;
+      from a kept selection (1): the selection (rows/8 + 2 B per 1024 rows) + selected x all
+                       projected widths + writes — it evaluates nothing, so no predicate column
+                       is charged."""
     w = [c.width for c in table.columns]
-    scan = table.n_rows * sum(w[c] for c in prog_cols)
+    n = table.n_rows
+    scan = n * sum(w[c] for c in prog_cols)
     count_b = scan + 8
-    gather = local_count * sum(w[c] for c in set(proj) if c not in prog_cols)
     write = local_count * (4 + sum(w[c] for c in proj))
-    return count_b, scan + gather + write
+    single = scan + local_count * sum(w[c] for c in set(proj) if c not in prog_cols) + write
+    if pushdown_path == 1:
+        selection = n // 8 + 2 * ((n + 1023) // 1024)
+        push_b = selection + local_count * sum(w[c] for c in proj) + write
+    else:
+        push_b = single
+    return count_b, push_b, single + 8
 
 
 def prog_columns(node):
@@ -169,18 +183,17 @@ def ncu_traffic(kernel, config):
 
 # ---- the oracle as baseline / reference arm ------------------------------------------------------
 
-def cpu_baseline(host_cols, types, prog, proj, n_sample, per_row_count_b, per_row_scan_b,
-                 selected_frac, proj_w, nthreads):
+def cpu_baseline(host_cols, table_like, prog, proj, prog_cols, nthreads):
+    """The oracle as it stands on a bounded sample: count on all host threads, push-down on one."""
     import oracle
-    cols = [c[:n_sample] for c in host_cols]
     t0 = time.perf_counter()
-    cnt = oracle.count_mt(cols, types, prog, nthreads)
+    cnt = oracle.count_mt(host_cols, table_like.types, prog, nthreads)
     t1 = time.perf_counter()
-    c2, ids, outs = oracle.pushdown(cols, types, prog, proj=proj)
+    c2, ids, outs = oracle.pushdown(host_cols, table_like.types, prog, proj=proj)
     t2 = time.perf_counter()
     assert c2 == cnt
-    by = n_sample * per_row_count_b + n_sample * per_row_scan_b + cnt * proj_w
-    return by, t2 - t0, t1 - t0, t2 - t1, cnt
+    _, _, step_b = algo_bytes(table_like, prog_cols, proj, cnt, 0)
+    return step_b, t2 - t0, t1 - t0, t2 - t1, cnt
 
 
 def run_reference(args):
@@ -211,8 +224,7 @@ def run_reference(args):
     for _ in range(args.steps):
         dt, cnt = step()
         times.append(dt)
-    cb, pb = algo_bytes(T, pc, proj, cnt)
-    total = cb + pb
+    cb, pb, total = algo_bytes(T, pc, proj, cnt, 0)
     ms = 1000 * sum(times) / len(times)
     value = total / (ms / 1000) / 1e9
     line = {"metric": METRIC, "value": round(value, 3), "unit": "GB/s", "impl": "reference",
@@ -277,7 +289,7 @@ def run_ours(args):
 
     def step(record):
         t0 = time.perf_counter()
-        c = table.count(prog)
+        c = table.count(prog, keep_selection=True)
         k1 = ctx.last_kernel_ms()
         t1 = time.perf_counter()
         r = table.pushdown(prog, project=proj_names, capacity=local_count, out=(out_ids, out_cols))
@@ -306,8 +318,9 @@ def run_ours(args):
     if world > 1:
         dist.barrier()
     dev_ms = ev0.elapsed_time(ev1)
-    cb, pb = algo_bytes(T, pc, proj, local_count)
-    my_bytes = cb + pb
+    pd_path = ctx.last_pushdown_path()
+    cb, pb, step_b = algo_bytes(T, pc, proj, local_count, pd_path)
+    my_bytes = step_b
     t = torch.tensor([dev_ms, my_bytes, cb, pb, statistics.mean(count_ms), statistics.mean(push_ms)],
                      dtype=torch.float64, device=dev)
     if world > 1:
@@ -342,7 +355,7 @@ def run_ours(args):
         def e2e_step():
             for d, h in zip(dcols, host):
                 d.copy_(h, non_blocking=True)
-            c = table.count(prog)
+            c = table.count(prog, keep_selection=True)
             r = table.pushdown(prog, project=proj_names, capacity=local_count, out=(out_ids, out_cols))
             h_ids.copy_(out_ids, non_blocking=True)
             for h, o in zip(h_cols, out_cols):
@@ -373,16 +386,24 @@ def run_ours(args):
             {1: np.int32, 2: np.int64, 3: np.float32, 4: np.int32, 5: np.uint8, 6: np.uint16,
              7: np.uint32}[c.ctype]) for c in T.columns]
         ns = len(host_cols[0])
-        w = [c.width for c in T.columns]
-        scan_w = sum(w[c] for c in pc)
-        proj_w = 4 + sum(w[c] for c in proj) + sum(w[c] for c in set(proj) if c not in pc)
         nthreads = os.cpu_count() or 1
-        by, dt, t_cnt, t_push, cnt = cpu_baseline(host_cols, T.types, prog, proj, ns, scan_w, scan_w,
-                                                  None, proj_w, nthreads)
+        sample_table = type("S", (), {})()
+        sample_table.columns, sample_table.n_rows, sample_table.types = T.columns, ns, T.types
+        by, dt, t_cnt, t_push, cnt = cpu_baseline(host_cols, sample_table, prog, proj, pc, nthreads)
         cpu = {"value": round(by / dt / 1e9, 3), "unit": "GB/s", "cores": nthreads, "kind": "oracle",
                "sample": f"first {ns} of {n} rows; count on {nthreads} threads ({t_cnt:.2f} s), "
                          f"push-down on 1 thread ({t_push:.2f} s)"}
 
+    push_name = "pushdown_sel_kernel" if pd_path == 1 else "pushdown_kernel"
+    roof_count = {"bound": "hbm", "achieved": round(count_gbs, 2), "peak": hbm, "unit": "GB/s",
+                  "frac": round(count_gbs / hbm, 4), "traffic": ncu_traffic("count_kernel", args.config),
+                  "kernel": "count_kernel", "ms": round(count_k, 4),
+                  "algorithmic_bytes_per_launch": int(cb), "peak_source": peak_note}
+    roof_push = {"bound": "hbm", "achieved": round(push_gbs, 2), "peak": hbm, "unit": "GB/s",
+                 "frac": round(push_gbs / hbm, 4), "traffic": ncu_traffic(push_name, args.config),
+                 "kernel": push_name, "ms": round(push_k, 4),
+                 "algorithmic_bytes_per_launch": int(pb), "peak_source": peak_note}
+    roof_dom = roof_push if push_k >= count_k else roof_count
     if rank == 0:
         line = {
             "metric": METRIC, "value": round(value_gbs, 3), "unit": "GB/s",
@@ -398,18 +419,12 @@ def run_ours(args):
                            "count_probe_min": round(min(count_lat), 4),
                            "pushdown_probe_median": round(statistics.median(push_lat), 4),
                            "count_kernel": round(count_k, 4), "pushdown_kernel": round(push_k, 4)},
-            "roofline": {"bound": "hbm", "achieved": round(push_gbs, 2), "peak": hbm, "unit": "GB/s",
-                         "frac": round(push_gbs / hbm, 4),
-                         "traffic": ncu_traffic("pushdown_kernel", args.config),
-                         "kernel": "pushdown_kernel", "peak_source": peak_note,
-                         "algorithmic_bytes_per_launch": int(pb)},
-            "roofline_count": {"bound": "hbm", "achieved": round(count_gbs, 2), "peak": hbm,
-                               "unit": "GB/s", "frac": round(count_gbs / hbm, 4),
-                               "traffic": ncu_traffic("count_kernel", args.config),
-                               "algorithmic_bytes_per_launch": int(cb)},
+            "roofline": roof_dom,
+            "roofline_kernels": {"count_kernel": roof_count, push_name: roof_push},
+            "pushdown_path": pd_path,
             "clocks": clk.summary(),
             "e2e": e2e,
-            "gpu_launches": 2 * args.steps,
+            "gpu_launches": (3 if pd_path == 1 else 2) * args.steps,
             "cpu_baseline": cpu,
         }
         print(json.dumps(line), flush=True)

@@ -127,6 +127,18 @@ void sel_table_release(sel_table table);
  * Returns the count, or SEL_ERR (SEL_E_ARG, SEL_E_PROGRAM, SEL_E_TYPE, SEL_E_CUDA, SEL_E_NCCL). */
 uint64_t sel_count(sel_table table, const void* prog, size_t prog_bytes, void* cuda_stream);
 
+/* sel_count_ex: sel_count with flags.
+ *   SEL_KEEP_SELECTION: the probe also keeps its selection in the context's scratch (the local row
+ *   mask, 1 bit per row, plus per-1024-row counts: n/8 + n/512 bytes). A following sel_pushdown of
+ *   the SAME table with byte-identical program bytes then materialises from it without
+ *   re-evaluating the predicate (materialise right after the count, reusing the scan
+ *   just done on the GPU; Algorithm 1 always counts before it executes). The
+ *   kept selection stays valid until the next SEL_KEEP_SELECTION probe on this context or the
+ *   release of the table; the columns must not change in between (the registration contract). */
+#define SEL_KEEP_SELECTION 1u
+uint64_t sel_count_ex(sel_table table, const void* prog, size_t prog_bytes, uint32_t flags,
+                      void* cuda_stream);
+
 /* sel_pushdown: materialise sigma_P pi_proj(R) for the local shard.
  *   out_rowids : device uint32[capacity_rows], receives GLOBAL row ids (global_row_offset + i)
  *                of the selected local rows in ascending order.
@@ -147,6 +159,12 @@ uint64_t sel_pushdown(sel_table table, const void* prog, size_t prog_bytes,
                       const uint32_t* proj_cols, uint32_t nproj, uint32_t* out_rowids,
                       void* const* out_cols, uint64_t capacity_rows, uint64_t* out_local_count,
                       uint64_t* out_global_offset, void* cuda_stream);
+
+/* Which path the context's last sel_pushdown took: 1 = from a kept selection (no predicate
+ * evaluation, no look-back), 0 = single pass (evaluate + decoupled look-back), -1 = no kernel ran
+ * (empty shard or constant-false program). Set SEL_PUSHDOWN_PATH=single in the environment to
+ * force the single pass. */
+int sel_ctx_last_pushdown_path(sel_ctx ctx);
 
 /* Validate a program against column types without running it (host only; no GPU needed).
  * Returns SEL_OK or the status sel_count would report for it. */

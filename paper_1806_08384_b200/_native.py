@@ -13,6 +13,7 @@ LIB_PATH = os.environ.get("SEL_LIB") or os.path.join(HERE, "libsel.so")
 SEL_OK, SEL_E_ARG, SEL_E_ALIGN, SEL_E_TYPE, SEL_E_PROGRAM, SEL_E_TOO_LARGE, SEL_E_CUDA, \
     SEL_E_NCCL, SEL_E_STATE = range(9)
 SEL_ERR = (1 << 64) - 1
+SEL_KEEP_SELECTION = 1
 STATUS_NAMES = {0: "SEL_OK", 1: "SEL_E_ARG", 2: "SEL_E_ALIGN", 3: "SEL_E_TYPE",
                 4: "SEL_E_PROGRAM", 5: "SEL_E_TOO_LARGE", 6: "SEL_E_CUDA", 7: "SEL_E_NCCL",
                 8: "SEL_E_STATE"}
@@ -20,7 +21,8 @@ STATUS_NAMES = {0: "SEL_OK", 1: "SEL_E_ARG", 2: "SEL_E_ALIGN", 3: "SEL_E_TYPE",
 # Every symbol include/sel.h declares (tests check the library exports exactly these).
 EXPORTS = ["sel_ctx_create", "sel_ctx_set_comm", "sel_nccl_unique_id", "sel_ctx_destroy",
            "sel_ctx_set_timing", "sel_ctx_last_kernel_ms", "sel_table_register",
-           "sel_table_release", "sel_count", "sel_pushdown", "sel_program_check",
+           "sel_table_release", "sel_count", "sel_count_ex", "sel_pushdown",
+           "sel_ctx_last_pushdown_path", "sel_program_check",
            "sel_program_path", "sel_program_plan_json", "sel_last_error",
            "sel_last_error_message", "sel_abi_version"]
 
@@ -59,6 +61,8 @@ def lib() -> ctypes.CDLL:
                                      ctypes.POINTER(vp)]),
         "sel_table_release": (None, [vp]),
         "sel_count": (u64, [vp, ctypes.c_char_p, sz, vp]),
+        "sel_count_ex": (u64, [vp, ctypes.c_char_p, sz, u32, vp]),
+        "sel_ctx_last_pushdown_path": (i32, [vp]),
         "sel_pushdown": (u64, [vp, ctypes.c_char_p, sz, vp, u32, vp, vp, u64,
                                ctypes.POINTER(u64), ctypes.POINTER(u64), vp]),
         "sel_program_check": (i32, [ctypes.c_char_p, sz, vp, u32]),

@@ -57,6 +57,10 @@ class Context:
     def enable_timing(self, on: bool = True) -> None:
         check(lib().sel_ctx_set_timing(self._h, 1 if on else 0))
 
+    def last_pushdown_path(self) -> int:
+        """1: the last pushdown materialised from a kept selection; 0: single pass; -1: none."""
+        return int(lib().sel_ctx_last_pushdown_path(self._h))
+
     def last_kernel_ms(self) -> float:
         ms = ctypes.c_float(0.0)
         check(lib().sel_ctx_last_kernel_ms(self._h, ctypes.byref(ms)))
@@ -144,10 +148,13 @@ class Table:
             return bytes(pred)
         return compile_predicate(pred, self.schema)
 
-    def count(self, pred, stream=None) -> int:
-        """Exact |sigma_P(R)| (Listing 3.1); global over ranks."""
+    def count(self, pred, stream=None, keep_selection: bool = False) -> int:
+        """Exact |sigma_P(R)| (Listing 3.1); global over ranks. With
+        keep_selection the probe keeps its selection so that a following pushdown() of the same
+        predicate materialises without re-evaluating it."""
         prog = self.program(pred)
-        r = lib().sel_count(self._h, prog, len(prog), _stream_ptr(stream, self.ctx.device))
+        r = lib().sel_count_ex(self._h, prog, len(prog), _native.SEL_KEEP_SELECTION if keep_selection else 0,
+                               _stream_ptr(stream, self.ctx.device))
         if r == SEL_ERR:
             raise last_error()
         return int(r)
@@ -182,8 +189,10 @@ class Table:
         return PushdownResult(rowids[:k], cols, int(r), int(local.value), int(off.value))
 
     def _local_count(self, prog: bytes, stream) -> int:
+        # Algorithm 1's order: count first (keeping the selection for the materialisation)
+        c = self.count(prog, stream, keep_selection=True)
         if self.ctx.nranks == 1:
-            return self.count(prog, stream)
+            return c
         # local count of this shard: a push-down with capacity 0 returns it without writing
         local = ctypes.c_uint64(0)
         r = lib().sel_pushdown(self._h, prog, len(prog), None, 0, None, None, 0,

@@ -130,6 +130,13 @@ struct sel_ctx_s {
   float last_ms = 0.f;
   int live_tables = 0;
   bool destroyed = false;
+  // kept selection (sel_count_ex + SEL_KEEP_SELECTION)
+  SelectionBufs sel{};
+  uint64_t sel_cap_chunks = 0;
+  sel_table kept_table = nullptr;
+  std::string kept_prog;
+  int last_pd_path = -1;
+  bool force_single = false;
 };
 
 struct sel_table_s {
@@ -226,6 +233,26 @@ sel_status ensure_status(sel_ctx c, uint64_t ntiles, cudaStream_t stream) {
   return SEL_OK;
 }
 
+sel_status ensure_selection(sel_ctx c, uint64_t nchunks) {
+  if (c->sel_cap_chunks >= nchunks) return SEL_OK;
+  if (c->sel.bits) cudaFree(c->sel.bits);
+  if (c->sel.chunk_cnt) cudaFree(c->sel.chunk_cnt);
+  if (c->sel.sb_sum) cudaFree(c->sel.sb_sum);
+  if (c->sel.sb_prefix) cudaFree(c->sel.sb_prefix);
+  c->sel = SelectionBufs{};
+  c->sel_cap_chunks = 0;
+  c->kept_table = nullptr;
+  const uint64_t cap = std::max<uint64_t>(nchunks, 1024);
+  const uint64_t nsb = (cap + kSbChunks - 1) / kSbChunks;
+  cudaError_t e = cudaMalloc(&c->sel.bits, cap * 32 * sizeof(uint32_t));
+  if (e == cudaSuccess) e = cudaMalloc(&c->sel.chunk_cnt, cap * sizeof(uint16_t));
+  if (e == cudaSuccess) e = cudaMalloc(&c->sel.sb_sum, nsb * sizeof(uint32_t));
+  if (e == cudaSuccess) e = cudaMalloc(&c->sel.sb_prefix, nsb * sizeof(uint32_t));
+  if (e != cudaSuccess) return set_error(SEL_E_CUDA, cuda_msg("cudaMalloc(selection)", e));
+  c->sel_cap_chunks = cap;
+  return SEL_OK;
+}
+
 }  // namespace
 
 // ---- ABI -------------------------------------------------------------------------------------------
@@ -254,6 +281,8 @@ sel_status sel_ctx_create(int cuda_device, sel_ctx* out) {
     delete c;
     return set_error(SEL_E_CUDA, "cudaFuncSetAttribute(push-down shared memory) failed");
   }
+  const char* pp = std::getenv("SEL_PUSHDOWN_PATH");
+  c->force_single = pp && std::strcmp(pp, "single") == 0;
   const char* env = std::getenv("SEL_CTAS_PER_SM");
   if (env && std::atoi(env) > 0) {
     const int v = std::atoi(env);
@@ -321,6 +350,13 @@ void release_ctx_resources(sel_ctx c) {
   if (c->s.ticket) cudaFree(c->s.ticket);
   if (c->s.status) cudaFree(c->s.status);
   if (c->h_result) cudaFreeHost(c->h_result);
+  if (c->sel.bits) cudaFree(c->sel.bits);
+  if (c->sel.chunk_cnt) cudaFree(c->sel.chunk_cnt);
+  if (c->sel.sb_sum) cudaFree(c->sel.sb_sum);
+  if (c->sel.sb_prefix) cudaFree(c->sel.sb_prefix);
+  c->sel = SelectionBufs{};
+  c->sel_cap_chunks = 0;
+  c->kept_table = nullptr;
   if (c->ev0) cudaEventDestroy(c->ev0);
   if (c->ev1) cudaEventDestroy(c->ev1);
   c->s = Scratch{};
@@ -389,6 +425,7 @@ sel_status sel_table_register(sel_ctx ctx, const sel_column* cols, uint32_t ncol
 void sel_table_release(sel_table t) {
   if (!t) return;
   sel_ctx c = t->ctx;
+  if (c->kept_table == t) c->kept_table = nullptr;
   delete t;
   if (--c->live_tables == 0 && c->destroyed) delete c;
 }
@@ -458,7 +495,15 @@ long sel_program_plan_json(const void* prog, size_t prog_bytes, const sel_type* 
 }
 
 uint64_t sel_count(sel_table t, const void* prog, size_t prog_bytes, void* cuda_stream) {
+  return sel_count_ex(t, prog, prog_bytes, 0u, cuda_stream);
+}
+
+int sel_ctx_last_pushdown_path(sel_ctx ctx) { return ctx ? ctx->last_pd_path : -1; }
+
+uint64_t sel_count_ex(sel_table t, const void* prog, size_t prog_bytes, uint32_t flags,
+                      void* cuda_stream) {
   clear_error();
+  if (flags & ~SEL_KEEP_SELECTION) return fail64(SEL_E_ARG, "unknown flags");
   if (!t) return fail64(SEL_E_ARG, "null table");
   sel_ctx c = t->ctx;
   if (c->destroyed) return fail64(SEL_E_STATE, "context destroyed");
@@ -472,6 +517,7 @@ uint64_t sel_count(sel_table t, const void* prog, size_t prog_bytes, void* cuda_
   const bool scan = n > 0 && plan.path != PATH_CONST;
   uint64_t local = 0;
   if (!scan) local = plan.path == PATH_CONST && plan.const_value ? n : 0;
+  if ((flags & SEL_KEEP_SELECTION) && !scan) c->kept_table = nullptr;
   if (!scan && !c->comm) return local;
 
   cudaError_t e;
@@ -479,16 +525,25 @@ uint64_t sel_count(sel_table t, const void* prog, size_t prog_bytes, void* cuda_
     const uint64_t nchunks = (n + kChunkRows - 1) / kChunkRows;
     const uint64_t units = (nchunks + kWarpsPerCta - 1) / kWarpsPerCta;
     const size_t nslots = count_slots(plan);
+    const SelectionBufs* keep = nullptr;
+    if (flags & SEL_KEEP_SELECTION) {
+      if (ensure_selection(c, nchunks) != SEL_OK) return SEL_ERR;
+      const uint64_t nsb = (nchunks + kSbChunks - 1) / kSbChunks;
+      e = cudaMemsetAsync(c->sel.sb_sum, 0, nsb * sizeof(uint32_t), stream);
+      if (e != cudaSuccess) return fail64(SEL_E_CUDA, cuda_msg("cudaMemsetAsync(selection)", e));
+      keep = &c->sel;
+      c->kept_table = nullptr;  // valid again only once this probe has completed
+    }
     if (c->timing) cudaEventRecord(c->ev0, stream);
     int le;
     if (fits_block<DevProgramSmall>(plan, nslots, 0)) {
       DevProgramSmall p;
       pack(plan, t, &p);
-      le = launch_count_small(p, n, grid_for(c, units, c->occ_count_small), c->s, stream);
+      le = launch_count_small(p, n, grid_for(c, units, c->occ_count_small), c->s, keep, stream);
     } else {
       static thread_local DevProgramLarge p;
       pack(plan, t, &p);
-      le = launch_count_large(p, n, grid_for(c, units, c->occ_count_large), c->s, stream);
+      le = launch_count_large(p, n, grid_for(c, units, c->occ_count_large), c->s, keep, stream);
     }
     if (le != cudaSuccess) return fail64(SEL_E_CUDA, cuda_msg("count kernel launch", (cudaError_t)le));
     if (c->timing) cudaEventRecord(c->ev1, stream);
@@ -505,6 +560,10 @@ uint64_t sel_count(sel_table t, const void* prog, size_t prog_bytes, void* cuda_
   if (e == cudaSuccess) e = cudaStreamSynchronize(stream);
   if (e != cudaSuccess) return fail64(SEL_E_CUDA, cuda_msg("count result", e));
   if (scan && c->timing) cudaEventElapsedTime(&c->last_ms, c->ev0, c->ev1);
+  if (scan && (flags & SEL_KEEP_SELECTION)) {
+    c->kept_table = t;
+    c->kept_prog.assign(static_cast<const char*>(prog), prog_bytes);
+  }
   return c->h_result[0];
 }
 
@@ -534,6 +593,7 @@ uint64_t sel_pushdown(sel_table t, const void* prog, size_t prog_bytes, const ui
   c->last_ms = 0.f;
   const uint64_t n = t->local_rows;
   const bool scan = n > 0 && !(plan.path == PATH_CONST && !plan.const_value);
+  c->last_pd_path = -1;
   cudaError_t e;
   if (scan) {
     const uint64_t ntiles = (n + kChunkRows - 1) / kChunkRows;
@@ -580,9 +640,40 @@ uint64_t sel_pushdown(sel_table t, const void* prog, size_t prog_bytes, const ui
       }
       p->warp_smem = (off + 15u) & ~15u;
     };
+    const bool from_sel = !c->force_single && c->kept_table == t &&
+                          c->kept_prog.size() == prog_bytes &&
+                          std::memcmp(c->kept_prog.data(), prog, prog_bytes) == 0;
     if (c->timing) cudaEventRecord(c->ev0, stream);
     int le, grid;
-    if (fits_block<DevProgramSmall>(plan, nslots, nproj)) {
+    if (from_sel) {
+      // Materialise from the kept selection: gathers only, every projection from global memory.
+      auto fill_sel = [&](auto* p) {
+        std::memset(p, 0, sizeof(*p));
+        p->row_offset = t->row_offset;
+        p->capacity = capacity_rows;
+        p->n_proj = capacity_rows > 0 ? nproj : 0;
+        for (uint32_t j = 0; j < p->n_proj; ++j) {
+          p->proj_src[j] = t->cols[proj_cols[j]].data;
+          p->proj_dst[j] = out_cols[j];
+          p->proj_wclass[j] = wclass_of(t->types[proj_cols[j]]);
+          p->proj_cap_off[j] = kNoCapture;
+        }
+      };
+      const uint64_t units = (ntiles + kWarpsPerCta - 1) / kWarpsPerCta;
+      if (nproj <= (uint32_t)DevProgramSmall::kMaxProj) {
+        DevProgramSmall p;
+        fill_sel(&p);
+        grid = grid_for(c, units, occupancy_pushdown_sel_small());
+        le = launch_pushdown_sel_small(p, n, out_rowids, grid, c->s, c->sel, stream);
+      } else {
+        static thread_local DevProgramLarge p;
+        fill_sel(&p);
+        grid = grid_for(c, units, occupancy_pushdown_sel_large());
+        le = launch_pushdown_sel_large(p, n, out_rowids, grid, c->s, c->sel, stream);
+      }
+      if (le != cudaSuccess) return fail64(SEL_E_CUDA, cuda_msg("push-down kernel launch", (cudaError_t)le));
+      c->last_pd_path = 1;
+    } else if (fits_block<DevProgramSmall>(plan, nslots, nproj)) {
       DevProgramSmall p;
       fill(&p);
       grid = grid_for(c, (ntiles + kWarpsPerCta - 1) / kWarpsPerCta,
@@ -595,12 +686,15 @@ uint64_t sel_pushdown(sel_table t, const void* prog, size_t prog_bytes, const ui
                       occupancy_pushdown_large((size_t)p.warp_smem * kWarpsPerCta));
       le = launch_pushdown_large(p, n, out_rowids, grid, c->s, c->ticket_base, c->epoch, stream);
     }
-    if (le != cudaSuccess) {
-      cudaMemsetAsync(c->s.ticket, 0, sizeof(unsigned long long), stream);
-      c->ticket_base = 0;
-      return fail64(SEL_E_CUDA, cuda_msg("push-down kernel launch", (cudaError_t)le));
+    if (!from_sel) {
+      if (le != cudaSuccess) {
+        cudaMemsetAsync(c->s.ticket, 0, sizeof(unsigned long long), stream);
+        c->ticket_base = 0;
+        return fail64(SEL_E_CUDA, cuda_msg("push-down kernel launch", (cudaError_t)le));
+      }
+      c->ticket_base += ntiles + (uint64_t)grid * kWarpsPerCta;  // every warp draws one ticket past the last tile
+      c->last_pd_path = 0;
     }
-    c->ticket_base += ntiles + (uint64_t)grid * kWarpsPerCta;  // every warp draws one ticket past the last tile
     if (c->timing) cudaEventRecord(c->ev1, stream);
   } else {
     c->h_result[0] = 0;

@@ -268,21 +268,43 @@ __device__ __forceinline__ uint32_t eval_program(const P& p, uint64_t base, int 
 // ---- count ----------------------------------------------------------------------------------
 // Persistent grid-stride over warp-chunks; per-lane popc, warp redux, CTA reduction, one partial
 // per CTA; the last CTA to finish sums the partials (self-resetting: no memset between probes).
-template <class P>
+// KEEP (sel_count_ex with SEL_KEEP_SELECTION): the chunk's row mask (one u32 per lane, 128 B per
+// 1024 rows) and its count are also kept, plus per-64-chunk sums, so that a following push-down
+// of the same predicate materialises from the selection without re-evaluating it (PAPER.md:329:
+// materialise right after the count, reusing the scan already done on the GPU).
+template <bool KEEP>
+__device__ __forceinline__ void keep_chunk(const SelectionBufs& sb, uint64_t c, int lane, uint32_t m) {
+  if (!KEEP) return;
+  sb.bits[c * 32 + lane] = m;
+  const uint32_t cc = __reduce_add_sync(0xFFFFFFFFu, (uint32_t)__popc(m));
+  if (lane == 0) {
+    sb.chunk_cnt[c] = (uint16_t)cc;
+    if (cc) atomicAdd(&sb.sb_sum[c >> kSbShift], cc);
+  }
+}
+
+template <class P, bool KEEP>
 __global__ void __launch_bounds__(kThreads) count_kernel(const __grid_constant__ P p, uint64_t n,
                                                          uint64_t* __restrict__ partials,
                                                          unsigned int* __restrict__ done,
-                                                         uint64_t* __restrict__ out) {
+                                                         uint64_t* __restrict__ out,
+                                                         SelectionBufs sb) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const uint64_t nfull = n / kChunkRows;
   const uint32_t rem = (uint32_t)(n % kChunkRows);
   const uint64_t gw = (uint64_t)blockIdx.x * kWarpsPerCta + warp;
   const uint64_t nw = (uint64_t)gridDim.x * kWarpsPerCta;
   uint32_t cnt = 0;
-  for (uint64_t c = gw; c < nfull; c += nw)
-    cnt += __popc(eval_program<false, false>(p, c * kChunkRows, lane, kChunkRows, nullptr));
-  if (rem != 0 && gw == nfull % nw)
-    cnt += __popc(eval_program<true, false>(p, nfull * kChunkRows, lane, rem, nullptr));
+  for (uint64_t c = gw; c < nfull; c += nw) {
+    const uint32_t m = eval_program<false, false>(p, c * kChunkRows, lane, kChunkRows, nullptr);
+    cnt += __popc(m);
+    keep_chunk<KEEP>(sb, c, lane, m);
+  }
+  if (rem != 0 && gw == nfull % nw) {
+    const uint32_t m = eval_program<true, false>(p, nfull * kChunkRows, lane, rem, nullptr);
+    cnt += __popc(m);
+    keep_chunk<KEEP>(sb, nfull, lane, m);
+  }
   cnt = __reduce_add_sync(0xFFFFFFFFu, cnt);
 
   __shared__ uint32_t s_warp[kWarpsPerCta];
@@ -351,6 +373,74 @@ __device__ __forceinline__ void gather_smem(const char* cap, void* dst_v, uint64
   for (uint32_t q = lane; q < lim; q += 32) dst[q] = src[s_idx[q]];
 }
 
+// Coalesced write-out of one chunk's compacted rows: output positions [gbase, gbase + cnt) receive
+// the chunk-local rows s_idx[0..cnt) (ascending), truncated at the capacity (Algorithm 1's gate).
+template <class P>
+__device__ __forceinline__ void write_out(const P& p, uint64_t cbase, uint64_t gbase, uint32_t cnt,
+                                          const uint16_t* my, const char* wsmem, int lane,
+                                          uint32_t* __restrict__ out_ids) {
+  if (gbase >= p.capacity) return;
+  const uint32_t lim = (uint32_t)min((uint64_t)cnt, p.capacity - gbase);
+  const uint32_t idbase = (uint32_t)(p.row_offset + cbase);
+#pragma unroll 4
+  for (uint32_t q = lane; q < lim; q += 32) out_ids[gbase + q] = idbase + my[q];
+#pragma unroll 1
+  for (uint32_t j = 0; j < p.n_proj; ++j) {
+    const uint16_t co = p.proj_cap_off[j];
+    if (co != kNoCapture) {
+      const char* cap = wsmem + co;
+      switch (p.proj_wclass[j]) {
+        case W1: gather_smem<uint8_t>(cap, p.proj_dst[j], gbase, my, lim, lane); break;
+        case W2: gather_smem<uint16_t>(cap, p.proj_dst[j], gbase, my, lim, lane); break;
+        case W4: gather_smem<uint32_t>(cap, p.proj_dst[j], gbase, my, lim, lane); break;
+        default: gather_smem<uint64_t>(cap, p.proj_dst[j], gbase, my, lim, lane); break;
+      }
+    } else {
+      switch (p.proj_wclass[j]) {
+        case W1: gather_global<uint8_t>(p.proj_src[j], p.proj_dst[j], cbase, gbase, my, lim, lane); break;
+        case W2: gather_global<uint16_t>(p.proj_src[j], p.proj_dst[j], cbase, gbase, my, lim, lane); break;
+        case W4: gather_global<uint32_t>(p.proj_src[j], p.proj_dst[j], cbase, gbase, my, lim, lane); break;
+        default: gather_global<uint64_t>(p.proj_src[j], p.proj_dst[j], cbase, gbase, my, lim, lane); break;
+      }
+    }
+  }
+}
+
+// Stage the chunk-local indices of the rows selected by the lanes' masks, ascending; returns the
+// chunk's count. Positions come from a warp scan of per-quad-stripe popcounts, 4 stripes of 8 bits
+// per word (fields <= 128 never carry).
+__device__ __forceinline__ uint32_t stage_indices(uint32_t m, int lane, uint16_t* my) {
+  uint32_t cw0 = 0, cw1 = 0;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    cw0 |= (uint32_t)__popc((m >> (4 * k)) & 0xFu) << (8 * k);
+    cw1 |= (uint32_t)__popc((m >> (4 * (k + 4))) & 0xFu) << (8 * k);
+  }
+  uint32_t ex0 = cw0, ex1 = cw1;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const uint32_t t0 = __shfl_up_sync(0xFFFFFFFFu, ex0, d);
+    const uint32_t t1 = __shfl_up_sync(0xFFFFFFFFu, ex1, d);
+    if (lane >= d) { ex0 += t0; ex1 += t1; }
+  }
+  const uint32_t tot0 = __shfl_sync(0xFFFFFFFFu, ex0, 31), tot1 = __shfl_sync(0xFFFFFFFFu, ex1, 31);
+  ex0 -= cw0;
+  ex1 -= cw1;
+  uint32_t acc = 0;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    const uint32_t nib = (m >> (4 * k)) & 0xFu;
+    uint32_t pos = acc + (((k < 4 ? ex0 : ex1) >> (8 * (k & 3))) & 0xFFu);
+    acc += ((k < 4 ? tot0 : tot1) >> (8 * (k & 3))) & 0xFFu;
+    if (nib == 0) continue;
+    const uint32_t r0 = 4u * (32u * k + lane);
+#pragma unroll
+    for (int e = 0; e < 4; ++e)
+      if (nib & (1u << e)) my[pos++] = (uint16_t)(r0 + e);
+  }
+  return acc;
+}
+
 // Warp-granular single-pass compaction. Every warp runs independently (no CTA barriers): it draws
 // a 1024-row tile from a global ticket counter (tickets are handed out in order, so every tile a
 // warp waits on belongs to a warp that is already running: forward progress), evaluates the
@@ -382,33 +472,9 @@ __global__ void __launch_bounds__(kThreads, 3) pushdown_kernel(
     const uint32_t m = nvalid == kChunkRows ? eval_program<false, true>(p, cbase, lane, kChunkRows, wsmem)
                                             : eval_program<true, true>(p, cbase, lane, nvalid, wsmem);
 
-    // 2. warp scan of per-quad-stripe counts (4 stripes of 8 bits per word; fields <= 128)
-    uint32_t cw[2], ex[2], tot[2];
-    cw[0] = cw[1] = 0;
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      cw[0] |= (uint32_t)__popc((m >> (4 * k)) & 0xFu) << (8 * k);
-      cw[1] |= (uint32_t)__popc((m >> (4 * (k + 4))) & 0xFu) << (8 * k);
-    }
-    ex[0] = cw[0];
-    ex[1] = cw[1];
-#pragma unroll
-    for (int d = 1; d < 32; d <<= 1) {
-      const uint32_t t0 = __shfl_up_sync(0xFFFFFFFFu, ex[0], d);
-      const uint32_t t1 = __shfl_up_sync(0xFFFFFFFFu, ex[1], d);
-      if (lane >= d) { ex[0] += t0; ex[1] += t1; }
-    }
-    tot[0] = __shfl_sync(0xFFFFFFFFu, ex[0], 31);
-    tot[1] = __shfl_sync(0xFFFFFFFFu, ex[1], 31);
-    ex[0] -= cw[0];
-    ex[1] -= cw[1];
-    uint32_t stripe_base[8];
-    uint32_t acc = 0;
-#pragma unroll
-    for (int k = 0; k < 8; ++k) {
-      stripe_base[k] = acc;
-      acc += (tot[k >> 2] >> (8 * (k & 3))) & 0xFFu;
-    }
+    // 2. stage the chunk-local indices of the selected rows (ascending) and count them
+    const uint32_t acc = stage_indices(m, lane, my);
+    __syncwarp();
 
     // 3. publish the aggregate, look back for the exclusive prefix, publish the inclusive prefix
     uint64_t excl = 0;
@@ -439,53 +505,76 @@ __global__ void __launch_bounds__(kThreads, 3) pushdown_kernel(
       if (lane == 0) st_relaxed_u64(&status[tile], pack_status(epoch, kFlagPrefix, (uint32_t)(excl + acc)));
     }
     if (tile == ntiles - 1 && lane == 0) *out_count = excl + acc;
-    if (acc == 0) {
-      __syncwarp();
-      continue;
-    }
-
-    // 4. stage the chunk-local indices of the selected rows, ascending
-#pragma unroll
-    for (int k = 0; k < 8; ++k) {
-      const uint32_t nib = (m >> (4 * k)) & 0xFu;
-      if (nib == 0) continue;
-      uint32_t pos = stripe_base[k] + ((ex[k >> 2] >> (8 * (k & 3))) & 0xFFu);
-      const uint32_t r0 = 4u * (32u * k + lane);
-#pragma unroll
-      for (int e = 0; e < 4; ++e)
-        if (nib & (1u << e)) my[pos++] = (uint16_t)(r0 + e);
-    }
-    __syncwarp();
-
-    // 5. coalesced write-out of the tile's slice, honouring the capacity gate
-    const uint64_t gbase = excl;
-    if (gbase < p.capacity) {
-      const uint32_t lim = (uint32_t)min((uint64_t)acc, p.capacity - gbase);
-      const uint32_t idbase = (uint32_t)(p.row_offset + cbase);
-#pragma unroll 4
-      for (uint32_t q = lane; q < lim; q += 32) out_ids[gbase + q] = idbase + my[q];
-#pragma unroll 1
-      for (uint32_t j = 0; j < p.n_proj; ++j) {
-        const uint16_t co = p.proj_cap_off[j];
-        if (co != kNoCapture) {
-          const char* cap = wsmem + co;
-          switch (p.proj_wclass[j]) {
-            case W1: gather_smem<uint8_t>(cap, p.proj_dst[j], gbase, my, lim, lane); break;
-            case W2: gather_smem<uint16_t>(cap, p.proj_dst[j], gbase, my, lim, lane); break;
-            case W4: gather_smem<uint32_t>(cap, p.proj_dst[j], gbase, my, lim, lane); break;
-            default: gather_smem<uint64_t>(cap, p.proj_dst[j], gbase, my, lim, lane); break;
-          }
-        } else {
-          switch (p.proj_wclass[j]) {
-            case W1: gather_global<uint8_t>(p.proj_src[j], p.proj_dst[j], cbase, gbase, my, lim, lane); break;
-            case W2: gather_global<uint16_t>(p.proj_src[j], p.proj_dst[j], cbase, gbase, my, lim, lane); break;
-            case W4: gather_global<uint32_t>(p.proj_src[j], p.proj_dst[j], cbase, gbase, my, lim, lane); break;
-            default: gather_global<uint64_t>(p.proj_src[j], p.proj_dst[j], cbase, gbase, my, lim, lane); break;
-          }
-        }
-      }
-    }
+    // 4. coalesced write-out of the tile's slice, honouring the capacity gate
+    if (acc != 0) write_out(p, cbase, excl, acc, my, wsmem, lane, out_ids);
     __syncwarp();  // `my` and the captures are rewritten by the next tile
+  }
+}
+
+
+// ---- push-down from a kept selection ------------------------------------------------------------
+// Exclusive prefix of the per-64-chunk sums kept by the count kernel (one CTA; <= 65536 sums).
+__global__ void __launch_bounds__(1024) superblock_prefix_kernel(const uint32_t* __restrict__ sb_sum,
+                                                                 uint32_t* __restrict__ sb_prefix,
+                                                                 uint32_t nsb, uint64_t* __restrict__ out_count) {
+  const uint32_t t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  const uint32_t per = (nsb + 1023u) / 1024u;
+  const uint32_t b = min(nsb, t * per), e = min(nsb, b + per);
+  uint32_t local = 0;
+  for (uint32_t i = b; i < e; ++i) local += sb_sum[i];
+  uint32_t incl = local;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const uint32_t v = __shfl_up_sync(0xFFFFFFFFu, incl, d);
+    if (lane >= (uint32_t)d) incl += v;
+  }
+  __shared__ uint32_t s_w[32];
+  if (lane == 31) s_w[warp] = incl;
+  __syncthreads();
+  if (warp == 0) {
+    uint32_t w = s_w[lane], wi = w;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const uint32_t v = __shfl_up_sync(0xFFFFFFFFu, wi, d);
+      if (lane >= (uint32_t)d) wi += v;
+    }
+    s_w[lane] = wi - w;
+    if (lane == 31) *out_count = wi;
+  }
+  __syncthreads();
+  uint32_t run = s_w[warp] + incl - local;
+  for (uint32_t i = b; i < e; ++i) {
+    sb_prefix[i] = run;
+    run += sb_sum[i];
+  }
+}
+
+// Grid-stride over chunks; chunks with no selected row are skipped without touching the columns.
+// A chunk's output offset is its superblock prefix plus the counts of the preceding chunks of its
+// superblock (<= 63, one warp-wide 128-byte read). No ticket, no look-back, no predicate.
+template <class P>
+__global__ void __launch_bounds__(kThreads) pushdown_sel_kernel(const __grid_constant__ P p,
+                                                                uint64_t n, SelectionBufs sb,
+                                                                uint32_t* __restrict__ out_ids) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  __shared__ uint16_t s_idx[kWarpsPerCta][kChunkRows];
+  uint16_t* my = s_idx[warp];
+  const uint64_t nchunks = (n + kChunkRows - 1) / kChunkRows;
+  const uint64_t gw = (uint64_t)blockIdx.x * kWarpsPerCta + warp;
+  const uint64_t nw = (uint64_t)gridDim.x * kWarpsPerCta;
+  for (uint64_t c = gw; c < nchunks; c += nw) {
+    const uint32_t cnt = sb.chunk_cnt[c];
+    if (cnt == 0) continue;
+    const uint32_t m = sb.bits[c * 32 + lane];
+    const uint64_t first = (c >> kSbShift) << kSbShift;
+    uint32_t part = 0;
+    if (first + lane < c) part += sb.chunk_cnt[first + lane];
+    if (first + 32 + lane < c) part += sb.chunk_cnt[first + 32 + lane];
+    const uint64_t gbase = (uint64_t)sb.sb_prefix[c >> kSbShift] + __reduce_add_sync(0xFFFFFFFFu, part);
+    stage_indices(m, lane, my);
+    __syncwarp();
+    write_out(p, c * kChunkRows, gbase, cnt, my, nullptr, lane, out_ids);
+    __syncwarp();
   }
 }
 
@@ -498,12 +587,36 @@ int occupancy_of(Kern k, size_t dyn_smem) {
 
 }  // namespace
 
-int launch_count_small(const DevProgramSmall& p, uint64_t n, int grid, const Scratch& s, void* st) {
-  count_kernel<DevProgramSmall><<<grid, kThreads, 0, (cudaStream_t)st>>>(p, n, s.partials, s.done, s.result);
+int launch_count_small(const DevProgramSmall& p, uint64_t n, int grid, const Scratch& s,
+                       const SelectionBufs* keep, void* st) {
+  if (keep)
+    count_kernel<DevProgramSmall, true><<<grid, kThreads, 0, (cudaStream_t)st>>>(p, n, s.partials, s.done, s.result, *keep);
+  else
+    count_kernel<DevProgramSmall, false><<<grid, kThreads, 0, (cudaStream_t)st>>>(p, n, s.partials, s.done, s.result, SelectionBufs{});
   return (int)cudaGetLastError();
 }
-int launch_count_large(const DevProgramLarge& p, uint64_t n, int grid, const Scratch& s, void* st) {
-  count_kernel<DevProgramLarge><<<grid, kThreads, 0, (cudaStream_t)st>>>(p, n, s.partials, s.done, s.result);
+int launch_count_large(const DevProgramLarge& p, uint64_t n, int grid, const Scratch& s,
+                       const SelectionBufs* keep, void* st) {
+  if (keep)
+    count_kernel<DevProgramLarge, true><<<grid, kThreads, 0, (cudaStream_t)st>>>(p, n, s.partials, s.done, s.result, *keep);
+  else
+    count_kernel<DevProgramLarge, false><<<grid, kThreads, 0, (cudaStream_t)st>>>(p, n, s.partials, s.done, s.result, SelectionBufs{});
+  return (int)cudaGetLastError();
+}
+int launch_pushdown_sel_small(const DevProgramSmall& p, uint64_t n, uint32_t* out_ids, int grid,
+                              const Scratch& s, const SelectionBufs& sb, void* st) {
+  const uint64_t nchunks = (n + kChunkRows - 1) / kChunkRows;
+  const uint32_t nsb = (uint32_t)((nchunks + kSbChunks - 1) / kSbChunks);
+  superblock_prefix_kernel<<<1, 1024, 0, (cudaStream_t)st>>>(sb.sb_sum, sb.sb_prefix, nsb, s.result);
+  pushdown_sel_kernel<DevProgramSmall><<<grid, kThreads, 0, (cudaStream_t)st>>>(p, n, sb, out_ids);
+  return (int)cudaGetLastError();
+}
+int launch_pushdown_sel_large(const DevProgramLarge& p, uint64_t n, uint32_t* out_ids, int grid,
+                              const Scratch& s, const SelectionBufs& sb, void* st) {
+  const uint64_t nchunks = (n + kChunkRows - 1) / kChunkRows;
+  const uint32_t nsb = (uint32_t)((nchunks + kSbChunks - 1) / kSbChunks);
+  superblock_prefix_kernel<<<1, 1024, 0, (cudaStream_t)st>>>(sb.sb_sum, sb.sb_prefix, nsb, s.result);
+  pushdown_sel_kernel<DevProgramLarge><<<grid, kThreads, 0, (cudaStream_t)st>>>(p, n, sb, out_ids);
   return (int)cudaGetLastError();
 }
 int launch_pushdown_small(const DevProgramSmall& p, uint64_t n, uint32_t* out_ids, int grid,
@@ -527,8 +640,10 @@ int prepare_kernels() {
                              cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
   return (int)e;
 }
-int occupancy_count_small() { return occupancy_of(count_kernel<DevProgramSmall>, 0); }
-int occupancy_count_large() { return occupancy_of(count_kernel<DevProgramLarge>, 0); }
+int occupancy_count_small() { return occupancy_of(count_kernel<DevProgramSmall, false>, 0); }
+int occupancy_count_large() { return occupancy_of(count_kernel<DevProgramLarge, false>, 0); }
+int occupancy_pushdown_sel_small() { return occupancy_of(pushdown_sel_kernel<DevProgramSmall>, 0); }
+int occupancy_pushdown_sel_large() { return occupancy_of(pushdown_sel_kernel<DevProgramLarge>, 0); }
 int occupancy_pushdown_small(size_t dyn_smem) { return occupancy_of(pushdown_kernel<DevProgramSmall>, dyn_smem); }
 int occupancy_pushdown_large(size_t dyn_smem) { return occupancy_of(pushdown_kernel<DevProgramLarge>, dyn_smem); }
 

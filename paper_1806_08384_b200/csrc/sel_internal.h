@@ -72,6 +72,18 @@ struct DevProgramT {
 using DevProgramSmall = DevProgramT<64, 32, 64, 32, 16>;
 using DevProgramLarge = DevProgramT<256, 128, 1024, 128, 256>;
 
+// A kept selection (sel_count_ex with SEL_KEEP_SELECTION): per chunk of 1024 rows, the 32 lane
+// masks (bit layout of kernels.cu) and the chunk's count; per superblock of 64 chunks, the sum of
+// its counts and (filled by the push-down) its exclusive prefix.
+constexpr int kSbShift = 6;
+constexpr uint64_t kSbChunks = 1ull << kSbShift;
+struct SelectionBufs {
+  uint32_t* bits;        // [nchunks * 32]
+  uint16_t* chunk_cnt;   // [nchunks]
+  uint32_t* sb_sum;      // [nsb], zeroed before the count
+  uint32_t* sb_prefix;   // [nsb]
+};
+
 // Device-side scratch owned by a context.
 struct Scratch {
   uint64_t* partials;      // per-CTA partial counts (count kernel)
@@ -84,9 +96,15 @@ struct Scratch {
 
 // Launch entry points (kernels.cu). Return cudaError_t as int.
 int launch_count_small(const DevProgramSmall& p, uint64_t n, int grid, const Scratch& s,
-                       void* stream);
+                       const SelectionBufs* keep, void* stream);
 int launch_count_large(const DevProgramLarge& p, uint64_t n, int grid, const Scratch& s,
-                       void* stream);
+                       const SelectionBufs* keep, void* stream);
+// Push-down from a kept selection: superblock prefix (writes the local count to s.result[0]) and
+// the compaction/gather kernel.
+int launch_pushdown_sel_small(const DevProgramSmall& p, uint64_t n, uint32_t* out_ids, int grid,
+                              const Scratch& s, const SelectionBufs& sb, void* stream);
+int launch_pushdown_sel_large(const DevProgramLarge& p, uint64_t n, uint32_t* out_ids, int grid,
+                              const Scratch& s, const SelectionBufs& sb, void* stream);
 int launch_pushdown_small(const DevProgramSmall& p, uint64_t n, uint32_t* out_ids, int grid,
                           const Scratch& s, uint64_t ticket_base, uint32_t epoch, void* stream);
 int launch_pushdown_large(const DevProgramLarge& p, uint64_t n, uint32_t* out_ids, int grid,
@@ -97,6 +115,8 @@ int prepare_kernels();
 int occupancy_count_small();
 int occupancy_count_large();
 int occupancy_pushdown_small(size_t dyn_smem);
+int occupancy_pushdown_sel_small();
+int occupancy_pushdown_sel_large();
 int occupancy_pushdown_large(size_t dyn_smem);
 
 }  // namespace sel

@@ -45,18 +45,38 @@ def register(ctx, cols, types, row_offset=0, global_rows=None):
     return sel.Table(ctx, names, types, tens, row_offset=row_offset, global_rows=global_rows)
 
 
+def _invalidate_selection(table):
+    """A keep-selection probe of a constant program drops the context's kept selection."""
+    table.count(encode(Const(True), table.types), keep_selection=True)
+
+
 def check_parity(table, cols, types, node, proj=None, capacity=None, row_offset=0):
+    """Count and BOTH push-down paths vs the oracle: materialised from a kept selection (after a
+    keep-selection count, Algorithm 1's order) and the single pass (evaluate + look-back)."""
     prog = encode(node, types)
-    want_count, want_ids, want_cols = oracle.pushdown(cols, types, prog, proj=proj or [],
+    proj = proj or []
+    want_count, want_ids, want_cols = oracle.pushdown(cols, types, prog, proj=proj,
                                                       capacity=capacity, row_offset=row_offset)
     assert table.count(prog) == want_count, node
-    res = table.pushdown(prog, project=proj or [], capacity=capacity)
-    assert res.count == want_count and res.local_count == want_count
-    got_ids = res.rowids.cpu().numpy().view(np.uint32)
-    np.testing.assert_array_equal(got_ids, want_ids, err_msg=str(node))
-    for j, c in enumerate(proj or []):
-        got = res.columns[c].cpu().numpy().view(want_cols[j].dtype)
-        np.testing.assert_array_equal(got, want_cols[j])
+    cap = want_count if capacity is None else capacity
+    n = table.local_rows
+    for keep in (True, False):
+        if keep:
+            assert table.count(prog, keep_selection=True) == want_count
+        else:
+            _invalidate_selection(table)
+        res = table.pushdown(prog, project=proj, capacity=cap)
+        path = table.ctx.last_pushdown_path()
+        if n > 0 and want_count > 0:
+            # a program folded to a constant never launches the count kernel, so nothing is kept
+            const = sel.program_path(prog, types) == 2
+            assert path == (1 if keep and not const else 0), (keep, path)
+        assert res.count == want_count and res.local_count == want_count
+        got_ids = res.rowids.cpu().numpy().view(np.uint32)
+        np.testing.assert_array_equal(got_ids, want_ids, err_msg=f"keep={keep} {node}")
+        for j, c in enumerate(proj):
+            got = res.columns[c].cpu().numpy().view(want_cols[j].dtype)
+            np.testing.assert_array_equal(got, want_cols[j], err_msg=f"keep={keep} col {c}")
 
 
 def test_worked_example_scaled(ctx):
@@ -119,15 +139,21 @@ def test_capacity_gate(ctx):
     prog = encode(node, types)
     full = oracle.count(cols, types, prog)
     for cap in [0, 1, 17, 8191, full // 2, full, full + 100]:
-        sentinel = torch.full((max(cap, 1) + 64,), -7, dtype=torch.int32, device=ctx.device)
-        outc = torch.full((max(cap, 1) + 64,), 99, dtype=torch.uint8, device=ctx.device)
-        res = t.pushdown(prog, project=[1], capacity=cap, out=(sentinel, [outc]))
-        assert res.count == full and res.local_count == full
-        assert res.gated == (full > cap)
+        for keep in (True, False):
+            if keep:
+                t.count(prog, keep_selection=True)
+            else:
+                _invalidate_selection(t)
+            sentinel = torch.full((max(cap, 1) + 64,), -7, dtype=torch.int32, device=ctx.device)
+            outc = torch.full((max(cap, 1) + 64,), 99, dtype=torch.uint8, device=ctx.device)
+            res = t.pushdown(prog, project=[1], capacity=cap, out=(sentinel, [outc]))
+            assert ctx.last_pushdown_path() == (1 if keep else 0)
+            assert res.count == full and res.local_count == full
+            assert res.gated == (full > cap)
+            # nothing written past the capacity
+            assert (sentinel[cap:].cpu() == -7).all()
+            assert (outc[cap:].cpu() == 99).all()
         check_parity(t, cols, types, node, proj=[1], capacity=cap)
-        # nothing written past the capacity
-        assert (sentinel[cap:].cpu() == -7).all()
-        assert (outc[cap:].cpu() == 99).all()
 
 
 def test_shard_loop_offsets(ctx):
@@ -236,7 +262,8 @@ def test_full_size_worked_example(ctx):
     assert t.count(encode(Cmp("=", 0, 2), T.types)) == 120_000_000
     node = configs.c2_probes()["listing"]
     want_ids, want_n = _closed_form_ids_gpu(T, node, dev)
-    res = t.pushdown(encode(node, T.types), project=["A", "C", "D"])
+    res = t.pushdown(encode(node, T.types), project=["A", "C", "D"])   # count(keep) + materialise
+    assert ctx.last_pushdown_path() == 1
     assert res.count == want_n == 100_200_000
     got = res.rowids.to(torch.int64) & 0xFFFFFFFF
     assert torch.equal(got, want_ids)
@@ -244,6 +271,13 @@ def test_full_size_worked_example(ctx):
     cc = res.columns["C"]
     assert bool(((cc == 1) | (cc == 4)).all())
     assert torch.equal(res.columns["D"], T.col("D").data[got])
+    # the single pass (no kept selection) gives the same bytes
+    _invalidate_selection(t)
+    res2 = t.pushdown(encode(node, T.types), project=["A", "C", "D"], capacity=want_n)
+    assert ctx.last_pushdown_path() == 0
+    assert torch.equal(res2.rowids, res.rowids)
+    for k in "ACD":
+        assert torch.equal(res2.columns[k], res.columns[k])
     # the complement partitions the table (count(P) + count(NOT P) = N)
     assert t.count(encode(Not(node), T.types)) == 600_000_000 - 100_200_000
 
