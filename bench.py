@@ -70,10 +70,6 @@ def workload(name, rows):
             "1e9-row sweep, x < 0.01 N")
 
 
-def shard(n, world, rank):
-    return n * rank // world, n * (rank + 1) // world
-
-
 def algo_bytes(table, prog_cols, proj, local_count, pushdown_path=0):
     """Algorithmic bytes.
     step  = what COUNT + push-down must move once (e.g. C2: 5.4 GB scan + 0.40 GB of D
@@ -261,15 +257,14 @@ def run_ours(args):
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
 
+    from paper_1806_08384_b200 import dist as sdist
     n, gen, node, proj, desc = workload(args.config, args.rows)
-    s, e = shard(n, world, rank)
+    s, e = sdist.shard_range(n, world, rank)
     T = gen(s, e - s, dev)
     torch.cuda.synchronize()
     ctx = sel.Context(dev)
     if world > 1:
-        obj = [sel.Context.new_unique_id() if rank == 0 else None]
-        dist.broadcast_object_list(obj, src=0)
-        ctx.set_comm(world, rank, obj[0])
+        sdist.setup_comm(ctx)
     names = [c.name for c in T.columns]
     table = sel.Table(ctx, names, T.types, [c.data for c in T.columns], row_offset=s, global_rows=n)
     prog = encode(node, T.types)

@@ -1,0 +1,53 @@
+"""Multi-GPU plumbing: one process per GPU, rows sharded contiguously.
+
+Rank r of P owns rows [floor(rN/P), floor((r+1)N/P)) and registers them with
+global_row_offset = floor(rN/P). libsel combines the shards itself over NCCL (one 8-byte
+all-reduce per count, one P x 8-byte all-gather per push-down); torch.distributed is used only
+to hand rank 0's ncclUniqueId to every rank (any backend: gloo or nccl) and for barriers.
+"""
+
+from __future__ import annotations
+
+import torch.distributed as dist
+
+from .api import Context, Table
+
+
+def shard_range(n: int, world: int, rank: int) -> tuple:
+    """Contiguous row range [start, end) of `rank` among `world` ranks."""
+    if world < 1 or not 0 <= rank < world:
+        raise ValueError("bad world/rank")
+    return n * rank // world, n * (rank + 1) // world
+
+
+def broadcast_unique_id(unique_id: bytes | None, group=None) -> bytes:
+    """Rank 0's 128-byte ncclUniqueId delivered to every rank of `group`."""
+    obj = [unique_id if dist.get_rank(group) == 0 else None]
+    dist.broadcast_object_list(obj, src=dist.get_global_rank(group, 0) if group else 0, group=group)
+    uid = obj[0]
+    if not isinstance(uid, (bytes, bytearray)) or len(uid) != 128:
+        raise RuntimeError("bad ncclUniqueId broadcast")
+    return bytes(uid)
+
+
+def setup_comm(ctx: Context, group=None) -> Context:
+    """Make `ctx` one rank of the current torch.distributed group (collective)."""
+    world, rank = dist.get_world_size(group), dist.get_rank(group)
+    uid = broadcast_unique_id(Context.new_unique_id() if rank == 0 else None, group)
+    ctx.set_comm(world, rank, uid)
+    return ctx
+
+
+def exclusive_offset(local_counts, rank: int) -> int:
+    """Position of rank `rank`'s slice in the rank-ordered (= ascending row id) concatenation."""
+    return int(sum(local_counts[:rank]))
+
+
+def register_shard(ctx: Context, names, types, tensors, global_rows: int, dicts=None,
+                   group=None) -> Table:
+    """Register this rank's shard; its row offset follows shard_range."""
+    world, rank = dist.get_world_size(group), dist.get_rank(group)
+    start, end = shard_range(global_rows, world, rank)
+    if tensors and tensors[0].numel() != end - start:
+        raise ValueError(f"rank {rank} holds {tensors[0].numel()} rows, expected {end - start}")
+    return Table(ctx, names, types, tensors, dicts=dicts, row_offset=start, global_rows=global_rows)

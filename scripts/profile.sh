@@ -7,8 +7,10 @@ ARGS=${*:-"--steps 3 --warmup 3 --no-cpu --no-e2e"}
 mkdir -p gpurun_out
 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
     --log-file gpurun_out/launches_${TAG}.csv python bench.py $ARGS > gpurun_out/launches_${TAG}.out 2>&1
-for K in pushdown_kernel count_kernel; do
+for K in count_kernel pushdown_sel_kernel superblock_prefix_kernel; do
   ncu --set full --clock-control none --import-source on -k regex:${K} -s 3 -c 1 \
       -o gpurun_out/prof_${TAG}_${K} -f python bench.py $ARGS > gpurun_out/prof_${TAG}_${K}.out 2>&1
 done
-ls -la gpurun_out
+SEL_PUSHDOWN_PATH=single ncu --set full --clock-control none --import-source on -k regex:'pushdown_kernel' -s 3 -c 1 \
+    -o gpurun_out/prof_${TAG}_pushdown_kernel -f python bench.py $ARGS > gpurun_out/prof_${TAG}_pushdown_kernel.out 2>&1
+ls -la gpurun_out | grep $TAG

@@ -1,0 +1,103 @@
+"""The N > 1 host path on CPU: two processes over gloo (world_size 2, 127.0.0.1).
+
+What runs here is everything of the multi-GPU path that is not a device collective: the
+contiguous sharding, the ncclUniqueId hand-off from rank 0 (produced by libsel's own
+sel_nccl_unique_id, which needs no GPU) and the count / offset combination the library performs
+with NCCL (sum of local counts; exclusive prefix of local counts in rank order). Each rank's
+local probe is the CPU oracle on its shard (tests may use it); the combined result must equal the
+unsharded oracle result: count and the ascending concatenation of row ids.
+"""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, n, q):
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    sys.path.insert(0, root)
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import oracle
+        from paper_1806_08384_b200 import dist as sdist
+        from paper_1806_08384_b200 import Context
+        from selgen import configs, encode
+
+        uid = sdist.broadcast_unique_id(Context.new_unique_id() if rank == 0 else None)
+        ids_all = [None] * world
+        dist.all_gather_object(ids_all, uid)
+        assert all(u == uid for u in ids_all) and len(uid) == 128
+
+        start, end = sdist.shard_range(n, world, rank)
+        T = configs.gen_c2(n, start, end - start)             # this rank's shard only
+        cols = [c.numpy() for c in T.columns]
+        results = {}
+        for name, node in configs.c2_probes().items():
+            prog = encode(node, T.types)
+            local, ids, (d,) = oracle.pushdown(cols, T.types, prog, proj=[3], row_offset=start)
+            total = torch.tensor([local], dtype=torch.int64)
+            dist.all_reduce(total)                                # the count all-reduce (a4)
+            counts = [None] * world
+            dist.all_gather_object(counts, local)                 # the offset all-gather (a7)
+            off = sdist.exclusive_offset(counts, rank)
+            results[name] = (int(total.item()), off, ids, d)
+        q.put((rank, start, end, results))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("n", [600_000, 6_000 * 37])
+def test_two_rank_shards_combine_to_the_unsharded_result(n):
+    import oracle
+    from selgen import configs, encode
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, n, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    out = dict()
+    for _ in range(world):
+        rank, s, e, res = q.get(timeout=300)
+        out[rank] = (s, e, res)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert out[0][0] == 0 and out[0][1] == out[1][0] and out[1][1] == n
+    T = configs.gen_c2(n)
+    cols = [c.numpy() for c in T.columns]
+    for name, node in configs.c2_probes().items():
+        want_c, want_ids, (want_d,) = oracle.pushdown(cols, T.types, encode(node, T.types), proj=[3])
+        tot0, off0, ids0, d0 = out[0][2][name]
+        tot1, off1, ids1, d1 = out[1][2][name]
+        assert tot0 == tot1 == want_c
+        assert off0 == 0 and off1 == len(ids0)
+        np.testing.assert_array_equal(np.concatenate([ids0, ids1]), want_ids)
+        np.testing.assert_array_equal(np.concatenate([d0, d1]), want_d)
+
+
+def test_shard_range_partitions():
+    from paper_1806_08384_b200.dist import shard_range
+    for n in [0, 1, 7, 600_000_000, 2**32 - 1]:
+        for world in [1, 2, 3, 4, 8]:
+            r = [shard_range(n, world, k) for k in range(world)]
+            assert r[0][0] == 0 and r[-1][1] == n
+            assert all(r[k][1] == r[k + 1][0] for k in range(world - 1))
+            assert max(e - s for s, e in r) - min(e - s for s, e in r) <= 1
