@@ -283,22 +283,23 @@ def run_ours(args):
     count_ms, push_ms, count_lat, push_lat = [], [], [], []
 
     def step(record):
+        # Algorithm 1's Execute(compound, isSPD=true, maxSize) with PUSH_DOWN_MAX_SELECTIVITY = 1.0
+        # (the paper's push-down experiments): count (keeping the selection and the
+        # projected predicate columns) -> gate -> materialise, through one C-ABI call.
         t0 = time.perf_counter()
-        c = table.count(prog, keep_selection=True)
-        k1 = ctx.last_kernel_ms()
+        r = table.execute(prog, project=proj_names, max_size=n, capacity=local_count,
+                          out=(out_ids, out_cols))
         t1 = time.perf_counter()
-        r = table.pushdown(prog, project=proj_names, capacity=local_count, out=(out_ids, out_cols))
-        k2 = ctx.last_kernel_ms()
-        t2 = time.perf_counter()
         if record:
+            k1, k2 = ctx.last_times()
             count_ms.append(k1); push_ms.append(k2)
-            count_lat.append(1000 * (t1 - t0)); push_lat.append(1000 * (t2 - t1))
-        return c, r
+            count_lat.append(1000 * (t1 - t0))
+        return r.count, r
 
     ctx.enable_timing(True)
     for _ in range(max(args.warmup, 3)):
         c, r = step(False)
-        assert c == global_count and r.count == global_count
+        assert c == global_count and r.materialized
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
@@ -350,8 +351,9 @@ def run_ours(args):
         def e2e_step():
             for d, h in zip(dcols, host):
                 d.copy_(h, non_blocking=True)
-            c = table.count(prog, keep_selection=True)
-            r = table.pushdown(prog, project=proj_names, capacity=local_count, out=(out_ids, out_cols))
+            r = table.execute(prog, project=proj_names, max_size=n, capacity=local_count,
+                              out=(out_ids, out_cols))
+            c = r.count
             h_ids.copy_(out_ids, non_blocking=True)
             for h, o in zip(h_cols, out_cols):
                 h.copy_(o, non_blocking=True)
@@ -409,11 +411,10 @@ def run_ours(args):
                        "rows_per_gpu": e - s, "selected": global_count,
                        "parallelism": f"row-shard x{world}",
                        "l2": "inputs larger than L2 (no flush needed)",
-                       "step": "sel_count + sel_pushdown (exact-size outputs)"},
-            "latency_ms": {"count_probe_median": round(statistics.median(count_lat), 4),
-                           "count_probe_min": round(min(count_lat), 4),
-                           "pushdown_probe_median": round(statistics.median(push_lat), 4),
-                           "count_kernel": round(count_k, 4), "pushdown_kernel": round(push_k, 4)},
+                       "step": "sel_execute = count (keep selection + projected predicate values) -> gate -> materialise"},
+            "latency_ms": {"execute_median": round(statistics.median(count_lat), 4),
+                           "execute_min": round(min(count_lat), 4),
+                           "count_kernel": round(count_k, 4), "pushdown_kernels": round(push_k, 4)},
             "roofline": roof_dom,
             "roofline_kernels": {"count_kernel": roof_count, push_name: roof_push},
             "pushdown_path": pd_path,

@@ -103,6 +103,9 @@ void sel_ctx_destroy(sel_ctx ctx);
  * main-kernel duration in milliseconds (0 if timing is off). */
 sel_status sel_ctx_set_timing(sel_ctx ctx, int enable);
 sel_status sel_ctx_last_kernel_ms(sel_ctx ctx, float* ms);
+/* Device time of the most recent count probe's kernel and of the most recent push-down's kernels
+ * (ms; 0 if timing is off or none ran). */
+sel_status sel_ctx_last_times(sel_ctx ctx, float* count_ms, float* pushdown_ms);
 
 /* ---- tables --------------------------------------------------------------------------------
  * sel_table_register: records descriptors of `ncols` (1..255) columns that
@@ -132,12 +135,31 @@ uint64_t sel_count(sel_table table, const void* prog, size_t prog_bytes, void* c
  *   mask, 1 bit per row, plus per-1024-row counts: n/8 + n/512 bytes). A following sel_pushdown of
  *   the SAME table with byte-identical program bytes then materialises from it without
  *   re-evaluating the predicate (materialise right after the count, reusing the scan
- *   just done on the GPU; Algorithm 1 always counts before it executes). The
- *   kept selection stays valid until the next SEL_KEEP_SELECTION probe on this context or the
- *   release of the table; the columns must not change in between (the registration contract). */
+ *   just done on the GPU; Algorithm 1 always counts before it executes).
+ *   keep_cols/nkeep (host array, may be NULL/0): the compound's projected columns — Algorithm 1
+ *   knows them before it counts (ExtractPushDown returns conditions and columns, PAPER.md:374,
+ *   408). Those that are predicate columns have their selected values kept too (in row order per
+ *   1024-row chunk; at most 8 columns and 8 bytes per row), so the push-down copies them instead
+ *   of reading them again; the others are gathered by the push-down. The kept selection stays
+ *   valid until the next SEL_KEEP_SELECTION probe on this context or the release of the table;
+ *   the columns must not change in between (the registration contract).
+ *   Errors: as sel_count, plus SEL_E_ARG (unknown flag, keep column index >= ncols). */
 #define SEL_KEEP_SELECTION 1u
 uint64_t sel_count_ex(sel_table table, const void* prog, size_t prog_bytes, uint32_t flags,
-                      void* cuda_stream);
+                      const uint32_t* keep_cols, uint32_t nkeep, void* cuda_stream);
+
+/* sel_execute: Algorithm 1's Execute(compound, isSPD = true, maxSize) in one
+ * call: count with SEL_KEEP_SELECTION (and, with SEL_KEEP_VALUES=1 in the environment, the
+ * projected predicate columns' values), then if the
+ * GLOBAL count > max_size "throw" — *out_materialized = 0, nothing is written, *out_local_count
+ * and *out_global_offset are set to 0 — else materialise exactly like sel_pushdown (from the kept
+ * selection) and set *out_materialized = 1. Returns the global count or SEL_ERR. Arguments as
+ * sel_pushdown; out_materialized may be NULL. */
+uint64_t sel_execute(sel_table table, const void* prog, size_t prog_bytes,
+                     const uint32_t* proj_cols, uint32_t nproj, uint64_t max_size,
+                     uint32_t* out_rowids, void* const* out_cols, uint64_t capacity_rows,
+                     uint64_t* out_local_count, uint64_t* out_global_offset,
+                     int* out_materialized, void* cuda_stream);
 
 /* sel_pushdown: materialise sigma_P pi_proj(R) for the local shard.
  *   out_rowids : device uint32[capacity_rows], receives GLOBAL row ids (global_row_offset + i)

@@ -8,8 +8,9 @@ memory, streams and process groups only.
 
 from ._native import SelError, EXPORTS
 from .predicate import col, TRUE, FALSE, INT32, INT64, FLOAT32, DATE32, DICT8, DICT16, DICT32
-from .api import Context, Table, PushdownResult, program_check, program_path, program_plan
+from .api import (Context, Table, PushdownResult, ExecuteResult, program_check, program_path,
+                  program_plan)
 
 __all__ = ["SelError", "EXPORTS", "col", "TRUE", "FALSE", "INT32", "INT64", "FLOAT32", "DATE32",
-           "DICT8", "DICT16", "DICT32", "Context", "Table", "PushdownResult", "program_check",
+           "DICT8", "DICT16", "DICT32", "Context", "Table", "PushdownResult", "ExecuteResult", "program_check",
            "program_path", "program_plan"]

@@ -57,6 +57,12 @@ class Context:
     def enable_timing(self, on: bool = True) -> None:
         check(lib().sel_ctx_set_timing(self._h, 1 if on else 0))
 
+    def last_times(self) -> tuple:
+        """(count kernel ms, push-down kernels ms) of the most recent probes (timing enabled)."""
+        c, p = ctypes.c_float(0.0), ctypes.c_float(0.0)
+        check(lib().sel_ctx_last_times(self._h, ctypes.byref(c), ctypes.byref(p)))
+        return float(c.value), float(p.value)
+
     def last_pushdown_path(self) -> int:
         """1: the last pushdown materialised from a kept selection; 0: single pass; -1: none."""
         return int(lib().sel_ctx_last_pushdown_path(self._h))
@@ -90,6 +96,11 @@ class PushdownResult:
     def gated(self) -> bool:
         """Algorithm 1's 'count > maxSize' outcome: output truncated."""
         return self.local_count > self.rowids.numel()
+
+
+@dataclass
+class ExecuteResult(PushdownResult):
+    materialized: bool = True     # False: count > max_size, Algorithm 1's "throw" (revert)
 
 
 class Table:
@@ -148,16 +159,52 @@ class Table:
             return bytes(pred)
         return compile_predicate(pred, self.schema)
 
-    def count(self, pred, stream=None, keep_selection: bool = False) -> int:
+    def count(self, pred, stream=None, keep_selection: bool = False, keep_columns=()) -> int:
         """Exact |sigma_P(R)| (Listing 3.1); global over ranks. With
-        keep_selection the probe keeps its selection so that a following pushdown() of the same
+        keep_selection the probe keeps its selection (and the selected values of the projected
+        predicate columns named in keep_columns) so that a following pushdown() of the same
         predicate materialises without re-evaluating it."""
         prog = self.program(pred)
+        keep = self._col_indices(keep_columns)
+        arr = (ctypes.c_uint32 * max(len(keep), 1))(*keep)
         r = lib().sel_count_ex(self._h, prog, len(prog), _native.SEL_KEEP_SELECTION if keep_selection else 0,
-                               _stream_ptr(stream, self.ctx.device))
+                               arr, len(keep), _stream_ptr(stream, self.ctx.device))
         if r == SEL_ERR:
             raise last_error()
         return int(r)
+
+    def _col_indices(self, cols):
+        return [self.names.index(p) if isinstance(p, str) else int(p) for p in cols]
+
+    def execute(self, pred, project: Sequence[str | int] = (), max_size: int | None = None,
+                capacity: int | None = None, stream=None, out=None) -> "ExecuteResult":
+        """Algorithm 1's Execute(compound, isSPD=true, maxSize): count keeping
+        the selection, then "throw" if count > max_size (result.materialized is False, nothing
+        written) else materialise. capacity (rows of the output buffers) defaults to
+        min(max_size, local rows)."""
+        prog = self.program(pred)
+        proj = self._col_indices(project)
+        if max_size is None:
+            max_size = (1 << 64) - 2
+        if capacity is None:
+            capacity = min(int(max_size), self.local_rows)
+        dev = self.ctx.device
+        if out is None:
+            rowids = torch.empty(max(capacity, 1), dtype=torch.int32, device=dev)
+            outs = [torch.empty(max(capacity, 1), dtype=_OUT_DTYPE[self.types[j]], device=dev) for j in proj]
+        else:
+            rowids, outs = out
+        ptrs = (ctypes.c_void_p * max(len(outs), 1))(*[o.data_ptr() for o in outs])
+        pj = (ctypes.c_uint32 * max(len(proj), 1))(*proj)
+        local, off, mat = ctypes.c_uint64(0), ctypes.c_uint64(0), ctypes.c_int(0)
+        r = lib().sel_execute(self._h, prog, len(prog), pj, len(proj), int(max_size), rowids.data_ptr(),
+                              ptrs, capacity, ctypes.byref(local), ctypes.byref(off), ctypes.byref(mat),
+                              _stream_ptr(stream, dev))
+        if r == SEL_ERR:
+            raise last_error()
+        k = min(int(local.value), capacity)
+        cols = {self.names[j] if isinstance(p, str) else j: o[:k] for p, j, o in zip(project, proj, outs)}
+        return ExecuteResult(rowids[:k], cols, int(r), int(local.value), int(off.value), bool(mat.value))
 
     def pushdown(self, pred, project: Sequence[str | int] = (), capacity: int | None = None,
                  stream=None, out=None) -> PushdownResult:
@@ -167,7 +214,7 @@ class Table:
         prog = self.program(pred)
         proj = [self.names.index(p) if isinstance(p, str) else int(p) for p in project]
         if capacity is None:
-            capacity = self._local_count(prog, stream)
+            capacity = self._local_count(prog, stream, proj)
         dev = self.ctx.device
         if out is None:
             rowids = torch.empty(max(capacity, 1), dtype=torch.int32, device=dev)
@@ -188,9 +235,9 @@ class Table:
                 for p, j, o in zip(project, proj, outs)}
         return PushdownResult(rowids[:k], cols, int(r), int(local.value), int(off.value))
 
-    def _local_count(self, prog: bytes, stream) -> int:
+    def _local_count(self, prog: bytes, stream, keep_columns=()) -> int:
         # Algorithm 1's order: count first (keeping the selection for the materialisation)
-        c = self.count(prog, stream, keep_selection=True)
+        c = self.count(prog, stream, keep_selection=True, keep_columns=keep_columns)
         if self.ctx.nranks == 1:
             return c
         # local count of this shard: a push-down with capacity 0 returns it without writing

@@ -135,8 +135,14 @@ struct sel_ctx_s {
   uint64_t sel_cap_chunks = 0;
   sel_table kept_table = nullptr;
   std::string kept_prog;
+  std::vector<int> kept_cols;        // columns with kept values (slot k holds kept_cols[k])
+  void* slot_buf[kMaxKeep] = {};     // value slots, nchunks * 1024 * width bytes each
+  uint64_t slot_cap[kMaxKeep] = {};  // bytes allocated per slot
   int last_pd_path = -1;
   bool force_single = false;
+  bool prefetch = true;
+  bool keep_values = false;
+  float last_count_ms = 0.f, last_push_ms = 0.f;
 };
 
 struct sel_table_s {
@@ -166,6 +172,7 @@ void pack(const Plan& plan, const sel_table_s* t, P* p) {
   uint32_t nslots = 0, iv = 0;
   p->n_ops = (uint32_t)plan.op.size();
   p->n_leaves = (uint32_t)plan.leaves.size();
+  p->prefetch = t->ctx->prefetch ? 1u : 0u;
   p->conj = plan.path != PATH_INTERP ? 1u : 0u;
   for (size_t i = 0; i < plan.op.size(); ++i) {
     p->op[i] = plan.op[i];
@@ -244,12 +251,24 @@ sel_status ensure_selection(sel_ctx c, uint64_t nchunks) {
   c->kept_table = nullptr;
   const uint64_t cap = std::max<uint64_t>(nchunks, 1024);
   const uint64_t nsb = (cap + kSbChunks - 1) / kSbChunks;
+  c->kept_cols.clear();
   cudaError_t e = cudaMalloc(&c->sel.bits, cap * 32 * sizeof(uint32_t));
   if (e == cudaSuccess) e = cudaMalloc(&c->sel.chunk_cnt, cap * sizeof(uint16_t));
   if (e == cudaSuccess) e = cudaMalloc(&c->sel.sb_sum, nsb * sizeof(uint32_t));
   if (e == cudaSuccess) e = cudaMalloc(&c->sel.sb_prefix, nsb * sizeof(uint32_t));
   if (e != cudaSuccess) return set_error(SEL_E_CUDA, cuda_msg("cudaMalloc(selection)", e));
   c->sel_cap_chunks = cap;
+  return SEL_OK;
+}
+
+sel_status ensure_slot(sel_ctx c, int k, uint64_t bytes) {
+  if (c->slot_cap[k] >= bytes) return SEL_OK;
+  if (c->slot_buf[k]) cudaFree(c->slot_buf[k]);
+  c->slot_buf[k] = nullptr;
+  c->slot_cap[k] = 0;
+  cudaError_t e = cudaMalloc(&c->slot_buf[k], bytes);
+  if (e != cudaSuccess) return set_error(SEL_E_CUDA, cuda_msg("cudaMalloc(kept values)", e));
+  c->slot_cap[k] = bytes;
   return SEL_OK;
 }
 
@@ -281,6 +300,10 @@ sel_status sel_ctx_create(int cuda_device, sel_ctx* out) {
     delete c;
     return set_error(SEL_E_CUDA, "cudaFuncSetAttribute(push-down shared memory) failed");
   }
+  const char* pf = std::getenv("SEL_PREFETCH");
+  c->prefetch = pf && std::strcmp(pf, "1") == 0;  // measured: slower for the plain count on C2
+  const char* kv = std::getenv("SEL_KEEP_VALUES");
+  c->keep_values = kv && std::strcmp(kv, "1") == 0;
   const char* pp = std::getenv("SEL_PUSHDOWN_PATH");
   c->force_single = pp && std::strcmp(pp, "single") == 0;
   const char* env = std::getenv("SEL_CTAS_PER_SM");
@@ -357,6 +380,11 @@ void release_ctx_resources(sel_ctx c) {
   c->sel = SelectionBufs{};
   c->sel_cap_chunks = 0;
   c->kept_table = nullptr;
+  for (int k = 0; k < kMaxKeep; ++k) {
+    if (c->slot_buf[k]) cudaFree(c->slot_buf[k]);
+    c->slot_buf[k] = nullptr;
+    c->slot_cap[k] = 0;
+  }
   if (c->ev0) cudaEventDestroy(c->ev0);
   if (c->ev1) cudaEventDestroy(c->ev1);
   c->s = Scratch{};
@@ -495,15 +523,27 @@ long sel_program_plan_json(const void* prog, size_t prog_bytes, const sel_type* 
 }
 
 uint64_t sel_count(sel_table t, const void* prog, size_t prog_bytes, void* cuda_stream) {
-  return sel_count_ex(t, prog, prog_bytes, 0u, cuda_stream);
+  return sel_count_ex(t, prog, prog_bytes, 0u, nullptr, 0u, cuda_stream);
+}
+
+sel_status sel_ctx_last_times(sel_ctx ctx, float* count_ms, float* pushdown_ms) {
+  clear_error();
+  if (!ctx) return set_error(SEL_E_ARG, "null ctx");
+  if (count_ms) *count_ms = ctx->timing ? ctx->last_count_ms : 0.f;
+  if (pushdown_ms) *pushdown_ms = ctx->timing ? ctx->last_push_ms : 0.f;
+  return SEL_OK;
 }
 
 int sel_ctx_last_pushdown_path(sel_ctx ctx) { return ctx ? ctx->last_pd_path : -1; }
 
 uint64_t sel_count_ex(sel_table t, const void* prog, size_t prog_bytes, uint32_t flags,
-                      void* cuda_stream) {
+                      const uint32_t* keep_cols, uint32_t nkeep, void* cuda_stream) {
   clear_error();
   if (flags & ~SEL_KEEP_SELECTION) return fail64(SEL_E_ARG, "unknown flags");
+  if (nkeep > 0 && !keep_cols) return fail64(SEL_E_ARG, "null keep_cols");
+  if (t)
+    for (uint32_t j = 0; j < nkeep; ++j)
+      if (keep_cols[j] >= t->cols.size()) return fail64(SEL_E_ARG, "keep column index out of range");
   if (!t) return fail64(SEL_E_ARG, "null table");
   sel_ctx c = t->ctx;
   if (c->destroyed) return fail64(SEL_E_STATE, "context destroyed");
@@ -526,24 +566,64 @@ uint64_t sel_count_ex(sel_table t, const void* prog, size_t prog_bytes, uint32_t
     const uint64_t units = (nchunks + kWarpsPerCta - 1) / kWarpsPerCta;
     const size_t nslots = count_slots(plan);
     const SelectionBufs* keep = nullptr;
+    std::vector<int> cap_off(t->cols.size(), -1);
     if (flags & SEL_KEEP_SELECTION) {
       if (ensure_selection(c, nchunks) != SEL_OK) return SEL_ERR;
       const uint64_t nsb = (nchunks + kSbChunks - 1) / kSbChunks;
       e = cudaMemsetAsync(c->sel.sb_sum, 0, nsb * sizeof(uint32_t), stream);
       if (e != cudaSuccess) return fail64(SEL_E_CUDA, cuda_msg("cudaMemsetAsync(selection)", e));
-      keep = &c->sel;
       c->kept_table = nullptr;  // valid again only once this probe has completed
+      c->kept_cols.clear();
+      // projected predicate columns: capture while evaluating, keep the selected values
+      uint32_t off = kIdxBytes;
+      for (uint32_t j = 0; j < nkeep && (int)c->kept_cols.size() < kMaxKeep; ++j) {
+        const int col = (int)keep_cols[j];
+        bool pred_col = false;
+        for (auto& L : plan.leaves) pred_col = pred_col || L.col == col;
+        const uint32_t w = (uint32_t)width_of(t->types[col]);
+        if (!pred_col || cap_off[col] >= 0 || off + w * kChunkRows > kIdxBytes + kCaptureBudget) continue;
+        const int k = (int)c->kept_cols.size();
+        if (ensure_slot(c, k, nchunks * (uint64_t)kChunkRows * w) != SEL_OK) return SEL_ERR;
+        cap_off[col] = (int)off;
+        c->sel.keep_col[k] = (uint8_t)col;
+        c->sel.keep_wclass[k] = wclass_of(t->types[col]);
+        c->sel.keep_cap_off[k] = (uint16_t)off;
+        c->sel.keep_slot[k] = c->slot_buf[k];
+        c->kept_cols.push_back(col);
+        off += w * kChunkRows;
+      }
+      c->sel.n_keep = (uint32_t)c->kept_cols.size();
+      c->sel.warp_smem = c->sel.n_keep ? ((off + 15u) & ~15u) : 0u;
+      keep = &c->sel;
     }
+    auto mark_captures = [&](auto* p) {
+      std::vector<bool> marked(t->cols.size(), false);
+      for (size_t i = 0; i < plan.op.size(); ++i) {
+        if (plan.op[i] != DOP_LEAF) continue;
+        const int l = plan.arg[i];
+        const int col = plan.leaves[l].col;
+        if (cap_off[col] >= 0 && !marked[col]) {
+          p->leaf[l].cap = 1;
+          p->leaf[l].cap_off = (uint16_t)cap_off[col];
+          marked[col] = true;
+        }
+      }
+    };
+    const size_t dyn = keep ? (size_t)keep->warp_smem * kWarpsPerCta : 0;
     if (c->timing) cudaEventRecord(c->ev0, stream);
     int le;
     if (fits_block<DevProgramSmall>(plan, nslots, 0)) {
       DevProgramSmall p;
       pack(plan, t, &p);
-      le = launch_count_small(p, n, grid_for(c, units, c->occ_count_small), c->s, keep, stream);
+      mark_captures(&p);
+      const int occ = keep ? occupancy_count_keep_small(dyn) : c->occ_count_small;
+      le = launch_count_small(p, n, grid_for(c, units, occ), c->s, keep, stream);
     } else {
       static thread_local DevProgramLarge p;
       pack(plan, t, &p);
-      le = launch_count_large(p, n, grid_for(c, units, c->occ_count_large), c->s, keep, stream);
+      mark_captures(&p);
+      const int occ = keep ? occupancy_count_keep_large(dyn) : c->occ_count_large;
+      le = launch_count_large(p, n, grid_for(c, units, occ), c->s, keep, stream);
     }
     if (le != cudaSuccess) return fail64(SEL_E_CUDA, cuda_msg("count kernel launch", (cudaError_t)le));
     if (c->timing) cudaEventRecord(c->ev1, stream);
@@ -559,7 +639,10 @@ uint64_t sel_count_ex(sel_table t, const void* prog, size_t prog_bytes, uint32_t
   e = cudaMemcpyAsync(c->h_result, c->s.result, sizeof(uint64_t), cudaMemcpyDeviceToHost, stream);
   if (e == cudaSuccess) e = cudaStreamSynchronize(stream);
   if (e != cudaSuccess) return fail64(SEL_E_CUDA, cuda_msg("count result", e));
-  if (scan && c->timing) cudaEventElapsedTime(&c->last_ms, c->ev0, c->ev1);
+  if (scan && c->timing) {
+    cudaEventElapsedTime(&c->last_ms, c->ev0, c->ev1);
+    c->last_count_ms = c->last_ms;
+  }
   if (scan && (flags & SEL_KEEP_SELECTION)) {
     c->kept_table = t;
     c->kept_prog.assign(static_cast<const char*>(prog), prog_bytes);
@@ -657,6 +740,8 @@ uint64_t sel_pushdown(sel_table t, const void* prog, size_t prog_bytes, const ui
           p->proj_dst[j] = out_cols[j];
           p->proj_wclass[j] = wclass_of(t->types[proj_cols[j]]);
           p->proj_cap_off[j] = kNoCapture;
+          for (size_t k = 0; k < c->kept_cols.size(); ++k)
+            if (c->kept_cols[k] == (int)proj_cols[j]) p->proj_cap_off[j] = (uint16_t)(kKeptBase + k);
         }
       };
       const uint64_t units = (ntiles + kWarpsPerCta - 1) / kWarpsPerCta;
@@ -724,10 +809,36 @@ uint64_t sel_pushdown(sel_table t, const void* prog, size_t prog_bytes, const ui
     }
     local = total = c->h_result[0];
   }
-  if (scan && c->timing) cudaEventElapsedTime(&c->last_ms, c->ev0, c->ev1);
+  if (scan && c->timing) {
+    cudaEventElapsedTime(&c->last_ms, c->ev0, c->ev1);
+    c->last_push_ms = c->last_ms;
+  }
   if (out_local_count) *out_local_count = local;
   if (out_global_offset) *out_global_offset = offset;
   return total;
+}
+
+uint64_t sel_execute(sel_table t, const void* prog, size_t prog_bytes, const uint32_t* proj_cols,
+                     uint32_t nproj, uint64_t max_size, uint32_t* out_rowids,
+                     void* const* out_cols, uint64_t capacity_rows, uint64_t* out_local_count,
+                     uint64_t* out_global_offset, int* out_materialized, void* cuda_stream) {
+  if (out_materialized) *out_materialized = 0;
+  if (out_local_count) *out_local_count = 0;
+  if (out_global_offset) *out_global_offset = 0;
+  // Execute(isSPD): gamma_COUNT over the compound, keeping what the materialisation reuses.
+  // Kept values of projected predicate columns are opt-in (SEL_KEEP_VALUES=1): on C2 the extra
+  // per-row compaction in the count costs more than the re-read it saves.
+  const bool keep_values = t && t->ctx->keep_values;
+  const uint64_t count = sel_count_ex(t, prog, prog_bytes, SEL_KEEP_SELECTION,
+                                      keep_values ? proj_cols : nullptr, keep_values ? nproj : 0u,
+                                      cuda_stream);
+  if (count == SEL_ERR) return SEL_ERR;
+  if (count > max_size) return count;  // "throw exception": revert, nothing written
+  const uint64_t r = sel_pushdown(t, prog, prog_bytes, proj_cols, nproj, out_rowids, out_cols,
+                                  capacity_rows, out_local_count, out_global_offset, cuda_stream);
+  if (r == SEL_ERR) return SEL_ERR;
+  if (out_materialized) *out_materialized = 1;
+  return r;
 }
 
 }  // extern "C"

@@ -56,6 +56,22 @@ __device__ __forceinline__ void st_relaxed_u64(uint64_t* p, uint64_t v) {
   asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 
+// TMA bulk prefetch of [p, p + bytes) into L2 (bytes multiple of 16, p 16-byte aligned).
+__device__ __forceinline__ void prefetch_l2(const void* p, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+}
+
+// Prefetch every predicate column of chunk `c` into L2 (issued by one lane a chunk ahead).
+template <class P>
+__device__ __forceinline__ void prefetch_chunk(const P& p, uint64_t c) {
+#pragma unroll 1
+  for (uint32_t l = 0; l < p.n_leaves; ++l) {
+    const DevLeaf& L = p.leaf[l];
+    const uint32_t w = 1u << L.wclass;
+    prefetch_l2(static_cast<const char*>(p.col[L.slot]) + c * kChunkRows * w, kChunkRows * w);
+  }
+}
+
 // FLOAT32 sortable key (canon.cpp): sign ? ~bits : bits | 0x80000000.
 __device__ __forceinline__ uint32_t fkey(uint32_t b) {
   return b ^ ((uint32_t)((int32_t)b >> 31) | 0x80000000u);
@@ -265,79 +281,6 @@ __device__ __forceinline__ uint32_t eval_program(const P& p, uint64_t base, int 
   return m;
 }
 
-// ---- count ----------------------------------------------------------------------------------
-// Persistent grid-stride over warp-chunks; per-lane popc, warp redux, CTA reduction, one partial
-// per CTA; the last CTA to finish sums the partials (self-resetting: no memset between probes).
-// KEEP (sel_count_ex with SEL_KEEP_SELECTION): the chunk's row mask (one u32 per lane, 128 B per
-// 1024 rows) and its count are also kept, plus per-64-chunk sums, so that a following push-down
-// of the same predicate materialises from the selection without re-evaluating it (PAPER.md:329:
-// materialise right after the count, reusing the scan already done on the GPU).
-template <bool KEEP>
-__device__ __forceinline__ void keep_chunk(const SelectionBufs& sb, uint64_t c, int lane, uint32_t m) {
-  if (!KEEP) return;
-  sb.bits[c * 32 + lane] = m;
-  const uint32_t cc = __reduce_add_sync(0xFFFFFFFFu, (uint32_t)__popc(m));
-  if (lane == 0) {
-    sb.chunk_cnt[c] = (uint16_t)cc;
-    if (cc) atomicAdd(&sb.sb_sum[c >> kSbShift], cc);
-  }
-}
-
-template <class P, bool KEEP>
-__global__ void __launch_bounds__(kThreads) count_kernel(const __grid_constant__ P p, uint64_t n,
-                                                         uint64_t* __restrict__ partials,
-                                                         unsigned int* __restrict__ done,
-                                                         uint64_t* __restrict__ out,
-                                                         SelectionBufs sb) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const uint64_t nfull = n / kChunkRows;
-  const uint32_t rem = (uint32_t)(n % kChunkRows);
-  const uint64_t gw = (uint64_t)blockIdx.x * kWarpsPerCta + warp;
-  const uint64_t nw = (uint64_t)gridDim.x * kWarpsPerCta;
-  uint32_t cnt = 0;
-  for (uint64_t c = gw; c < nfull; c += nw) {
-    const uint32_t m = eval_program<false, false>(p, c * kChunkRows, lane, kChunkRows, nullptr);
-    cnt += __popc(m);
-    keep_chunk<KEEP>(sb, c, lane, m);
-  }
-  if (rem != 0 && gw == nfull % nw) {
-    const uint32_t m = eval_program<true, false>(p, nfull * kChunkRows, lane, rem, nullptr);
-    cnt += __popc(m);
-    keep_chunk<KEEP>(sb, nfull, lane, m);
-  }
-  cnt = __reduce_add_sync(0xFFFFFFFFu, cnt);
-
-  __shared__ uint32_t s_warp[kWarpsPerCta];
-  __shared__ bool s_last;
-  if (lane == 0) s_warp[warp] = cnt;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    uint64_t s = 0;
-#pragma unroll
-    for (int w = 0; w < kWarpsPerCta; ++w) s += s_warp[w];
-    partials[blockIdx.x] = s;
-    __threadfence();
-    s_last = atomicAdd(done, 1u) == gridDim.x - 1;
-  }
-  __syncthreads();
-  if (s_last) {
-    __threadfence();
-    uint64_t s = 0;
-    for (uint32_t b = threadIdx.x; b < gridDim.x; b += kThreads) s += ((volatile uint64_t*)partials)[b];
-    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xFFFFFFFFu, s, o);
-    __shared__ uint64_t s_sum[kWarpsPerCta];
-    if (lane == 0) s_sum[warp] = s;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      uint64_t t = 0;
-#pragma unroll
-      for (int w = 0; w < kWarpsPerCta; ++w) t += s_sum[w];
-      *out = t;
-      *done = 0u;
-    }
-  }
-}
-
 // ---- push-down ------------------------------------------------------------------------------
 constexpr uint64_t kFlagAgg = 1, kFlagPrefix = 2;
 __device__ __forceinline__ uint64_t pack_status(uint32_t epoch, uint64_t flag, uint32_t value) {
@@ -375,10 +318,21 @@ __device__ __forceinline__ void gather_smem(const char* cap, void* dst_v, uint64
 
 // Coalesced write-out of one chunk's compacted rows: output positions [gbase, gbase + cnt) receive
 // the chunk-local rows s_idx[0..cnt) (ascending), truncated at the capacity (Algorithm 1's gate).
+template <class T>
+__device__ __forceinline__ void copy_slot(const void* slot_v, void* dst_v, uint64_t cbase,
+                                          uint64_t gbase, uint32_t lim, int lane) {
+  const T* __restrict__ src = static_cast<const T*>(slot_v) + cbase;
+  T* __restrict__ dst = static_cast<T*>(dst_v) + gbase;
+#pragma unroll 4
+  for (uint32_t q = lane; q < lim; q += 32) dst[q] = src[q];
+}
+
+// proj_cap_off >= kKeptBase: projection j comes from kept slot (proj_cap_off - kKeptBase).
 template <class P>
 __device__ __forceinline__ void write_out(const P& p, uint64_t cbase, uint64_t gbase, uint32_t cnt,
                                           const uint16_t* my, const char* wsmem, int lane,
-                                          uint32_t* __restrict__ out_ids) {
+                                          uint32_t* __restrict__ out_ids,
+                                          const SelectionBufs* kept = nullptr) {
   if (gbase >= p.capacity) return;
   const uint32_t lim = (uint32_t)min((uint64_t)cnt, p.capacity - gbase);
   const uint32_t idbase = (uint32_t)(p.row_offset + cbase);
@@ -387,7 +341,15 @@ __device__ __forceinline__ void write_out(const P& p, uint64_t cbase, uint64_t g
 #pragma unroll 1
   for (uint32_t j = 0; j < p.n_proj; ++j) {
     const uint16_t co = p.proj_cap_off[j];
-    if (co != kNoCapture) {
+    if (kept && co != kNoCapture) {
+      const void* slot = kept->keep_slot[co - kKeptBase];
+      switch (p.proj_wclass[j]) {
+        case W1: copy_slot<uint8_t>(slot, p.proj_dst[j], cbase, gbase, lim, lane); break;
+        case W2: copy_slot<uint16_t>(slot, p.proj_dst[j], cbase, gbase, lim, lane); break;
+        case W4: copy_slot<uint32_t>(slot, p.proj_dst[j], cbase, gbase, lim, lane); break;
+        default: copy_slot<uint64_t>(slot, p.proj_dst[j], cbase, gbase, lim, lane); break;
+      }
+    } else if (co != kNoCapture) {
       const char* cap = wsmem + co;
       switch (p.proj_wclass[j]) {
         case W1: gather_smem<uint8_t>(cap, p.proj_dst[j], gbase, my, lim, lane); break;
@@ -439,6 +401,105 @@ __device__ __forceinline__ uint32_t stage_indices(uint32_t m, int lane, uint16_t
       if (nib & (1u << e)) my[pos++] = (uint16_t)(r0 + e);
   }
   return acc;
+}
+
+// ---- count ----------------------------------------------------------------------------------
+// Persistent grid-stride over warp-chunks; per-lane popc, warp redux, CTA reduction, one partial
+// per CTA; the last CTA to finish sums the partials (self-resetting: no memset between probes).
+// KEEP (sel_count_ex with SEL_KEEP_SELECTION): the chunk's row mask (one u32 per lane, 128 B per
+// 1024 rows) and its count are also kept, plus per-64-chunk sums, so that a following push-down
+// of the same predicate materialises from the selection without re-evaluating it (PAPER.md:329:
+// materialise right after the count, reusing the scan already done on the GPU). With kept value
+// columns (the compound's projected predicate columns, known before the count: ExtractPushDown
+// returns conditions AND columns) the values loaded for the predicate are
+// captured in shared memory and the chunk's selected ones written, compacted, to its slot.
+template <class P, bool KEEP>
+__device__ __forceinline__ void keep_chunk(const SelectionBufs& sb, uint64_t c, int lane, uint32_t m,
+                                           char* wsmem) {
+  if (!KEEP) return;
+  sb.bits[c * 32 + lane] = m;
+  uint32_t cc;
+  if (sb.n_keep) {
+    uint16_t* my = reinterpret_cast<uint16_t*>(wsmem);
+    cc = stage_indices(m, lane, my);
+    __syncwarp();
+#pragma unroll 1
+    for (uint32_t k = 0; k < sb.n_keep; ++k) {
+      const char* cap = wsmem + sb.keep_cap_off[k];
+      switch (sb.keep_wclass[k]) {
+        case W1: gather_smem<uint8_t>(cap, sb.keep_slot[k], c * kChunkRows, my, cc, lane); break;
+        case W2: gather_smem<uint16_t>(cap, sb.keep_slot[k], c * kChunkRows, my, cc, lane); break;
+        case W4: gather_smem<uint32_t>(cap, sb.keep_slot[k], c * kChunkRows, my, cc, lane); break;
+        default: gather_smem<uint64_t>(cap, sb.keep_slot[k], c * kChunkRows, my, cc, lane); break;
+      }
+    }
+    __syncwarp();
+  } else {
+    cc = __reduce_add_sync(0xFFFFFFFFu, (uint32_t)__popc(m));
+  }
+  if (lane == 0) {
+    sb.chunk_cnt[c] = (uint16_t)cc;
+    if (cc) atomicAdd(&sb.sb_sum[c >> kSbShift], cc);
+  }
+}
+
+template <class P, bool KEEP>
+__global__ void __launch_bounds__(kThreads, 4) count_kernel(const __grid_constant__ P p, uint64_t n,
+                                                         uint64_t* __restrict__ partials,
+                                                         unsigned int* __restrict__ done,
+                                                         uint64_t* __restrict__ out,
+                                                         SelectionBufs sb) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const uint64_t nfull = n / kChunkRows;
+  const uint32_t rem = (uint32_t)(n % kChunkRows);
+  const uint64_t gw = (uint64_t)blockIdx.x * kWarpsPerCta + warp;
+  const uint64_t nw = (uint64_t)gridDim.x * kWarpsPerCta;
+  extern __shared__ __align__(16) char s_dyn[];
+  char* wsmem = KEEP ? s_dyn + (size_t)warp * sb.warp_smem : nullptr;
+  uint32_t cnt = 0;
+  if (lane == 0 && p.prefetch && gw < nfull) prefetch_chunk(p, gw);
+  for (uint64_t c = gw; c < nfull; c += nw) {
+    if (lane == 0 && p.prefetch && c + nw < nfull) prefetch_chunk(p, c + nw);
+    const uint32_t m = eval_program<false, KEEP>(p, c * kChunkRows, lane, kChunkRows, wsmem);
+    cnt += __popc(m);
+    keep_chunk<P, KEEP>(sb, c, lane, m, wsmem);
+  }
+  if (rem != 0 && gw == nfull % nw) {
+    const uint32_t m = eval_program<true, KEEP>(p, nfull * kChunkRows, lane, rem, wsmem);
+    cnt += __popc(m);
+    keep_chunk<P, KEEP>(sb, nfull, lane, m, wsmem);
+  }
+  cnt = __reduce_add_sync(0xFFFFFFFFu, cnt);
+
+  __shared__ uint32_t s_warp[kWarpsPerCta];
+  __shared__ bool s_last;
+  if (lane == 0) s_warp[warp] = cnt;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint64_t s = 0;
+#pragma unroll
+    for (int w = 0; w < kWarpsPerCta; ++w) s += s_warp[w];
+    partials[blockIdx.x] = s;
+    __threadfence();
+    s_last = atomicAdd(done, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (s_last) {
+    __threadfence();
+    uint64_t s = 0;
+    for (uint32_t b = threadIdx.x; b < gridDim.x; b += kThreads) s += ((volatile uint64_t*)partials)[b];
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xFFFFFFFFu, s, o);
+    __shared__ uint64_t s_sum[kWarpsPerCta];
+    if (lane == 0) s_sum[warp] = s;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      uint64_t t = 0;
+#pragma unroll
+      for (int w = 0; w < kWarpsPerCta; ++w) t += s_sum[w];
+      *out = t;
+      *done = 0u;
+    }
+  }
 }
 
 // Warp-granular single-pass compaction. Every warp runs independently (no CTA barriers): it draws
@@ -553,7 +614,7 @@ __global__ void __launch_bounds__(1024) superblock_prefix_kernel(const uint32_t*
 // A chunk's output offset is its superblock prefix plus the counts of the preceding chunks of its
 // superblock (<= 63, one warp-wide 128-byte read). No ticket, no look-back, no predicate.
 template <class P>
-__global__ void __launch_bounds__(kThreads) pushdown_sel_kernel(const __grid_constant__ P p,
+__global__ void __launch_bounds__(kThreads, 6) pushdown_sel_kernel(const __grid_constant__ P p,
                                                                 uint64_t n, SelectionBufs sb,
                                                                 uint32_t* __restrict__ out_ids) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -573,7 +634,7 @@ __global__ void __launch_bounds__(kThreads) pushdown_sel_kernel(const __grid_con
     const uint64_t gbase = (uint64_t)sb.sb_prefix[c >> kSbShift] + __reduce_add_sync(0xFFFFFFFFu, part);
     stage_indices(m, lane, my);
     __syncwarp();
-    write_out(p, c * kChunkRows, gbase, cnt, my, nullptr, lane, out_ids);
+    write_out(p, c * kChunkRows, gbase, cnt, my, nullptr, lane, out_ids, &sb);
     __syncwarp();
   }
 }
@@ -590,7 +651,7 @@ int occupancy_of(Kern k, size_t dyn_smem) {
 int launch_count_small(const DevProgramSmall& p, uint64_t n, int grid, const Scratch& s,
                        const SelectionBufs* keep, void* st) {
   if (keep)
-    count_kernel<DevProgramSmall, true><<<grid, kThreads, 0, (cudaStream_t)st>>>(p, n, s.partials, s.done, s.result, *keep);
+    count_kernel<DevProgramSmall, true><<<grid, kThreads, (size_t)keep->warp_smem * kWarpsPerCta, (cudaStream_t)st>>>(p, n, s.partials, s.done, s.result, *keep);
   else
     count_kernel<DevProgramSmall, false><<<grid, kThreads, 0, (cudaStream_t)st>>>(p, n, s.partials, s.done, s.result, SelectionBufs{});
   return (int)cudaGetLastError();
@@ -598,7 +659,7 @@ int launch_count_small(const DevProgramSmall& p, uint64_t n, int grid, const Scr
 int launch_count_large(const DevProgramLarge& p, uint64_t n, int grid, const Scratch& s,
                        const SelectionBufs* keep, void* st) {
   if (keep)
-    count_kernel<DevProgramLarge, true><<<grid, kThreads, 0, (cudaStream_t)st>>>(p, n, s.partials, s.done, s.result, *keep);
+    count_kernel<DevProgramLarge, true><<<grid, kThreads, (size_t)keep->warp_smem * kWarpsPerCta, (cudaStream_t)st>>>(p, n, s.partials, s.done, s.result, *keep);
   else
     count_kernel<DevProgramLarge, false><<<grid, kThreads, 0, (cudaStream_t)st>>>(p, n, s.partials, s.done, s.result, SelectionBufs{});
   return (int)cudaGetLastError();
@@ -638,9 +699,17 @@ int prepare_kernels() {
   if (e == cudaSuccess)
     e = cudaFuncSetAttribute(pushdown_kernel<DevProgramLarge>,
                              cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(count_kernel<DevProgramSmall, true>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(count_kernel<DevProgramLarge, true>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
   return (int)e;
 }
 int occupancy_count_small() { return occupancy_of(count_kernel<DevProgramSmall, false>, 0); }
+int occupancy_count_keep_small(size_t dyn) { return occupancy_of(count_kernel<DevProgramSmall, true>, dyn); }
+int occupancy_count_keep_large(size_t dyn) { return occupancy_of(count_kernel<DevProgramLarge, true>, dyn); }
 int occupancy_count_large() { return occupancy_of(count_kernel<DevProgramLarge, false>, 0); }
 int occupancy_pushdown_sel_small() { return occupancy_of(pushdown_sel_kernel<DevProgramSmall>, 0); }
 int occupancy_pushdown_sel_large() { return occupancy_of(pushdown_sel_kernel<DevProgramLarge>, 0); }

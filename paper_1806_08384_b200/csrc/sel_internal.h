@@ -25,6 +25,7 @@ constexpr uint32_t kIdxBytes = 2 * kChunkRows;
 constexpr uint32_t kCaptureBudget = 8 * kChunkRows;     // <= 8 bytes/row of captured columns
 constexpr uint32_t kMaxPushdownSmem = kWarpsPerCta * (kIdxBytes + kCaptureBudget);  // 80 KB
 constexpr uint16_t kNoCapture = 0xFFFF;
+constexpr uint16_t kKeptBase = 0xFF00;  // push-down from a selection: proj_cap_off = kKeptBase + slot
 constexpr int kMaxDeviceStack = 32;
 
 enum WidthClass : uint8_t { W1 = 0, W2 = 1, W4 = 2, W8 = 3 };
@@ -52,7 +53,7 @@ struct DevProgramT {
   uint32_t conj;         // 1: ops are leaf0 AND leaf1 AND ... (no stack needed)
   uint32_t n_proj;
   uint32_t warp_smem;    // push-down: dynamic shared memory bytes per warp
-  uint32_t pad0;
+  uint32_t prefetch;     // 1: L2 bulk-prefetch each warp's next chunk (SEL_PREFETCH=0 disables)
   uint64_t row_offset;   // global id of local row 0 (push-down ids)
   uint64_t capacity;     // push-down capacity in rows
   uint8_t op[MAXOPS];
@@ -77,11 +78,20 @@ using DevProgramLarge = DevProgramT<256, 128, 1024, 128, 256>;
 // its counts and (filled by the push-down) its exclusive prefix.
 constexpr int kSbShift = 6;
 constexpr uint64_t kSbChunks = 1ull << kSbShift;
+constexpr int kMaxKeep = 8;
 struct SelectionBufs {
   uint32_t* bits;        // [nchunks * 32]
   uint16_t* chunk_cnt;   // [nchunks]
   uint32_t* sb_sum;      // [nsb], zeroed before the count
   uint32_t* sb_prefix;   // [nsb]
+  // Kept values of projected predicate columns: chunk c's selected values, compacted in row
+  // order, at keep_slot[k] + c * 1024 * width (written by the count, copied by the push-down).
+  uint32_t n_keep;
+  uint32_t warp_smem;            // count kernel: dynamic shared memory per warp (0 without keep)
+  uint8_t keep_col[kMaxKeep];    // table column index (host bookkeeping)
+  uint8_t keep_wclass[kMaxKeep];
+  uint16_t keep_cap_off[kMaxKeep];
+  void* keep_slot[kMaxKeep];
 };
 
 // Device-side scratch owned by a context.
@@ -95,6 +105,8 @@ struct Scratch {
 };
 
 // Launch entry points (kernels.cu). Return cudaError_t as int.
+// keep != nullptr: also keep the selection (and, with keep->n_keep > 0, the selected values of
+// projected predicate columns; the leaves carry the capture offsets and keep->warp_smem is set).
 int launch_count_small(const DevProgramSmall& p, uint64_t n, int grid, const Scratch& s,
                        const SelectionBufs* keep, void* stream);
 int launch_count_large(const DevProgramLarge& p, uint64_t n, int grid, const Scratch& s,
@@ -114,6 +126,8 @@ int prepare_kernels();
 // Occupancy (CTAs per SM) of each kernel, for persistent-grid sizing.
 int occupancy_count_small();
 int occupancy_count_large();
+int occupancy_count_keep_small(size_t dyn_smem);
+int occupancy_count_keep_large(size_t dyn_smem);
 int occupancy_pushdown_small(size_t dyn_smem);
 int occupancy_pushdown_sel_small();
 int occupancy_pushdown_sel_large();

@@ -51,8 +51,11 @@ def _invalidate_selection(table):
 
 
 def check_parity(table, cols, types, node, proj=None, capacity=None, row_offset=0):
-    """Count and BOTH push-down paths vs the oracle: materialised from a kept selection (after a
-    keep-selection count, Algorithm 1's order) and the single pass (evaluate + look-back)."""
+    """Count and every materialisation path vs the oracle:
+       kept  — count keeping the selection AND the projected predicate columns' values, then
+               push-down (Algorithm 1's order; what sel_execute does);
+       sel   — count keeping only the selection, push-down gathers every projected column;
+       single— no kept selection: single pass (evaluate + decoupled look-back)."""
     prog = encode(node, types)
     proj = proj or []
     want_count, want_ids, want_cols = oracle.pushdown(cols, types, prog, proj=proj,
@@ -60,8 +63,11 @@ def check_parity(table, cols, types, node, proj=None, capacity=None, row_offset=
     assert table.count(prog) == want_count, node
     cap = want_count if capacity is None else capacity
     n = table.local_rows
-    for keep in (True, False):
-        if keep:
+    const = sel.program_path(prog, types) == 2
+    for mode in ("kept", "sel", "single"):
+        if mode == "kept":
+            assert table.count(prog, keep_selection=True, keep_columns=proj) == want_count
+        elif mode == "sel":
             assert table.count(prog, keep_selection=True) == want_count
         else:
             _invalidate_selection(table)
@@ -69,14 +75,13 @@ def check_parity(table, cols, types, node, proj=None, capacity=None, row_offset=
         path = table.ctx.last_pushdown_path()
         if n > 0 and want_count > 0:
             # a program folded to a constant never launches the count kernel, so nothing is kept
-            const = sel.program_path(prog, types) == 2
-            assert path == (1 if keep and not const else 0), (keep, path)
+            assert path == (0 if mode == "single" or const else 1), (mode, path)
         assert res.count == want_count and res.local_count == want_count
         got_ids = res.rowids.cpu().numpy().view(np.uint32)
-        np.testing.assert_array_equal(got_ids, want_ids, err_msg=f"keep={keep} {node}")
+        np.testing.assert_array_equal(got_ids, want_ids, err_msg=f"{mode} {node}")
         for j, c in enumerate(proj):
             got = res.columns[c].cpu().numpy().view(want_cols[j].dtype)
-            np.testing.assert_array_equal(got, want_cols[j], err_msg=f"keep={keep} col {c}")
+            np.testing.assert_array_equal(got, want_cols[j], err_msg=f"{mode} col {c}")
 
 
 def test_worked_example_scaled(ctx):
@@ -262,8 +267,9 @@ def test_full_size_worked_example(ctx):
     assert t.count(encode(Cmp("=", 0, 2), T.types)) == 120_000_000
     node = configs.c2_probes()["listing"]
     want_ids, want_n = _closed_form_ids_gpu(T, node, dev)
-    res = t.pushdown(encode(node, T.types), project=["A", "C", "D"])   # count(keep) + materialise
-    assert ctx.last_pushdown_path() == 1
+    res = t.execute(encode(node, T.types), project=["A", "C", "D"], max_size=600_000_000,
+                    capacity=100_200_000)       # bench.py's step: Execute(isSPD) = count + materialise
+    assert res.materialized and ctx.last_pushdown_path() == 1
     assert res.count == want_n == 100_200_000
     got = res.rowids.to(torch.int64) & 0xFFFFFFFF
     assert torch.equal(got, want_ids)
@@ -292,3 +298,31 @@ def test_context_destroyed_before_table(cuda_device):
         t.count(encode(Cmp("<", 0, 5), [INT32]))
     assert e.value.status == 8
     t.release()
+
+
+def test_execute_gate(ctx):
+    """sel_execute = Algorithm 1's Execute(compound, isSPD=true, maxSize):
+    count > maxSize "throws" (nothing materialised, buffers untouched); count <= maxSize (strict
+    '>', so maxSize == count passes) materialises exactly the oracle's rows and values."""
+    n = 600_000
+    T = configs.gen_c2(n)
+    cols = [c.numpy() for c in T.columns]
+    t = register(ctx, cols, T.types)
+    node = configs.c2_probes()["listing"]
+    prog = encode(node, T.types)
+    want_c, want_ids, want_cols = oracle.pushdown(cols, T.types, prog, proj=configs.C2_PROJECT)
+    for max_size in (0, want_c - 1):
+        ids = torch.full((want_c,), -7, dtype=torch.int32, device=ctx.device)
+        outs = [torch.full((want_c,), 5, dtype=d, device=ctx.device) for d in (torch.int32, torch.uint8, torch.int32)]
+        r = t.execute(prog, project=configs.C2_PROJECT, max_size=max_size, capacity=want_c, out=(ids, outs))
+        assert r.count == want_c and not r.materialized and r.rowids.numel() == 0
+        assert bool((ids == -7).all()) and all(bool((o == 5).all()) for o in outs)
+    for max_size in (want_c, n):
+        r = t.execute(prog, project=configs.C2_PROJECT, max_size=max_size)
+        assert r.materialized and r.count == want_c and ctx.last_pushdown_path() == 1
+        np.testing.assert_array_equal(r.rowids.cpu().numpy().view(np.uint32), want_ids)
+        for j, c in enumerate(configs.C2_PROJECT):
+            np.testing.assert_array_equal(r.columns[c].cpu().numpy().view(want_cols[j].dtype), want_cols[j])
+    # a selection that matches nothing: count 0 passes any gate (0 > 0 is false), writes nothing
+    r = t.execute(encode(Cmp("=", 0, 99), T.types), project=[3], max_size=0, capacity=4)
+    assert r.materialized and r.count == 0 and r.rowids.numel() == 0
