@@ -35,7 +35,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="c2", choices=["c2", "c3", "c4", "c5"])
+    ap.add_argument("--config", default="c2", choices=["c1", "c2", "c3", "c4", "c5"])
     ap.add_argument("--rows", type=int, default=0, help="override global rows (testing only)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
@@ -46,20 +46,23 @@ def parse():
 # ---- workloads ---------------------------------------------------------------------------------
 
 def workload(name, rows):
-    """(generator(row_start, row_count, device) -> Table, program AST, projection, description)."""
+    """(global rows, generator(row_start, row_count, device) -> Table, program AST, projection,
+    description). BASELINE.json configs: c1..c5; the bench line is c2."""
     from selgen import configs
     if name == "c2":
         n = rows or configs.C2_ROWS
         return (n, lambda s, c, d: configs.gen_c2(n, s, c, device=d),
                 configs.c2_probes()["listing"], configs.C2_PROJECT,
                 "worked example R (PAPER.md:55-64): 600M rows, Listing 3.1 COUNT + push-down of A,C,D")
-    if name == "c3":
-        n = rows or 300_000_000
-        cols = ["l_orderkey", "l_discount", "l_extendedprice", "l_returnflag", "l_shipdate"]
+    if name in ("c1", "c3"):
+        n = rows or (60_000 if name == "c1" else 300_000_000)
+        cols = ["l_orderkey", "l_discount", "l_extendedprice", "l_returnflag", "l_shipdate", "l_shipmode"]
         def gen(s, c, d):
             return configs.gen_lineitem(n, s, c, device=d, columns=cols)
-        probe = configs.lineitem_probes(gen(0, 16, "cpu"))["q10"]
-        return n, gen, probe, [0, 2, 1], "TPC-H SF-50 lineitem, Q10-style predicate"
+        probes = configs.lineitem_probes(gen(0, 16, "cpu"))
+        if name == "c1":
+            return n, gen, probes["listing1"], [0], "TPC-H SF-0.01 lineitem, Listing 1.1 mapped"
+        return n, gen, probes["q10"], [0, 2, 1], "TPC-H SF-50 lineitem, Q10-style predicate"
     if name == "c4":
         n = rows or 480_000_000
         return (n, lambda s, c, d: configs.gen_lineorder(n, s, c, device=d),

@@ -744,7 +744,8 @@ uint64_t sel_pushdown(sel_table t, const void* prog, size_t prog_bytes, const ui
             if (c->kept_cols[k] == (int)proj_cols[j]) p->proj_cap_off[j] = (uint16_t)(kKeptBase + k);
         }
       };
-      const uint64_t units = (ntiles + kWarpsPerCta - 1) / kWarpsPerCta;
+      const uint64_t nblocks = (ntiles + kSelBlockChunks - 1) / kSelBlockChunks;
+      const uint64_t units = (nblocks + kWarpsPerCta - 1) / kWarpsPerCta;
       if (nproj <= (uint32_t)DevProgramSmall::kMaxProj) {
         DevProgramSmall p;
         fill_sel(&p);

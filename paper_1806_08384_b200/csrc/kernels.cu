@@ -610,31 +610,148 @@ __global__ void __launch_bounds__(1024) superblock_prefix_kernel(const uint32_t*
   }
 }
 
-// Grid-stride over chunks; chunks with no selected row are skipped without touching the columns.
-// A chunk's output offset is its superblock prefix plus the counts of the preceding chunks of its
-// superblock (<= 63, one warp-wide 128-byte read). No ticket, no look-back, no predicate.
+// Stage the rows selected by the lanes' masks of one chunk at my[base..], as block-relative row
+// numbers (row_base + chunk-local row), ascending; same scan as stage_indices.
+__device__ __forceinline__ void stage_rows(uint32_t m, int lane, uint16_t* my, uint32_t base,
+                                           uint32_t row_base) {
+  uint32_t cw0 = 0, cw1 = 0;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    cw0 |= (uint32_t)__popc((m >> (4 * k)) & 0xFu) << (8 * k);
+    cw1 |= (uint32_t)__popc((m >> (4 * (k + 4))) & 0xFu) << (8 * k);
+  }
+  uint32_t ex0 = cw0, ex1 = cw1;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const uint32_t t0 = __shfl_up_sync(0xFFFFFFFFu, ex0, d);
+    const uint32_t t1 = __shfl_up_sync(0xFFFFFFFFu, ex1, d);
+    if (lane >= d) { ex0 += t0; ex1 += t1; }
+  }
+  const uint32_t tot0 = __shfl_sync(0xFFFFFFFFu, ex0, 31), tot1 = __shfl_sync(0xFFFFFFFFu, ex1, 31);
+  ex0 -= cw0;
+  ex1 -= cw1;
+  uint32_t acc = base;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    const uint32_t nib = (m >> (4 * k)) & 0xFu;
+    uint32_t pos = acc + (((k < 4 ? ex0 : ex1) >> (8 * (k & 3))) & 0xFFu);
+    acc += ((k < 4 ? tot0 : tot1) >> (8 * (k & 3))) & 0xFFu;
+    if (nib == 0) continue;
+    const uint32_t r0 = row_base + 4u * (32u * k + lane);
+#pragma unroll
+    for (int e = 0; e < 4; ++e)
+      if (nib & (1u << e)) my[pos++] = (uint16_t)(r0 + e);
+  }
+}
+
+// Flush `k` staged rows (block-relative, ascending) to output positions [gbase, gbase + k): row
+// ids and the projections gathered from global memory (kept-value projections were copied per
+// chunk while staging).
 template <class P>
-__global__ void __launch_bounds__(kThreads, 6) pushdown_sel_kernel(const __grid_constant__ P p,
-                                                                uint64_t n, SelectionBufs sb,
-                                                                uint32_t* __restrict__ out_ids) {
+__device__ __forceinline__ void flush_rows(const P& p, uint64_t bbase, uint64_t gbase, uint32_t k,
+                                           const uint16_t* my, int lane,
+                                           uint32_t* __restrict__ out_ids) {
+  if (gbase >= p.capacity || k == 0) return;
+  const uint32_t lim = (uint32_t)min((uint64_t)k, p.capacity - gbase);
+  const uint32_t idbase = (uint32_t)(p.row_offset + bbase);
+#pragma unroll 4
+  for (uint32_t q = lane; q < lim; q += 32) out_ids[gbase + q] = idbase + my[q];
+#pragma unroll 1
+  for (uint32_t j = 0; j < p.n_proj; ++j) {
+    if (p.proj_cap_off[j] != kNoCapture) continue;
+    switch (p.proj_wclass[j]) {
+      case W1: gather_global<uint8_t>(p.proj_src[j], p.proj_dst[j], bbase, gbase, my, lim, lane); break;
+      case W2: gather_global<uint16_t>(p.proj_src[j], p.proj_dst[j], bbase, gbase, my, lim, lane); break;
+      case W4: gather_global<uint32_t>(p.proj_src[j], p.proj_dst[j], bbase, gbase, my, lim, lane); break;
+      default: gather_global<uint64_t>(p.proj_src[j], p.proj_dst[j], bbase, gbase, my, lim, lane); break;
+    }
+  }
+}
+
+// Copy chunk c's kept values of the projections that have them to output positions [pos, pos+cnt).
+template <class P>
+__device__ __forceinline__ void copy_kept(const P& p, const SelectionBufs& sb, uint64_t c,
+                                          uint64_t pos, uint32_t cnt, int lane) {
+  if (pos >= p.capacity) return;
+  const uint32_t lim = (uint32_t)min((uint64_t)cnt, p.capacity - pos);
+#pragma unroll 1
+  for (uint32_t j = 0; j < p.n_proj; ++j) {
+    const uint16_t co = p.proj_cap_off[j];
+    if (co == kNoCapture) continue;
+    const void* slot = sb.keep_slot[co - kKeptBase];
+    switch (p.proj_wclass[j]) {
+      case W1: copy_slot<uint8_t>(slot, p.proj_dst[j], c * kChunkRows, pos, lim, lane); break;
+      case W2: copy_slot<uint16_t>(slot, p.proj_dst[j], c * kChunkRows, pos, lim, lane); break;
+      case W4: copy_slot<uint32_t>(slot, p.proj_dst[j], c * kChunkRows, pos, lim, lane); break;
+      default: copy_slot<uint64_t>(slot, p.proj_dst[j], c * kChunkRows, pos, lim, lane); break;
+    }
+  }
+}
+
+#ifndef SEL_BLOCK_CHUNKS
+#define SEL_BLOCK_CHUNKS 2
+#endif
+#ifndef SEL_STAGE_CAP
+#define SEL_STAGE_CAP 1024
+#endif
+#ifndef SEL_PD_MINB
+#define SEL_PD_MINB 8
+#endif
+constexpr int kBlockChunks = SEL_BLOCK_CHUNKS;         // chunks per warp block
+constexpr uint32_t kStageCap = SEL_STAGE_CAP;          // staged rows per warp before a flush
+
+// Warp blocks of 4 contiguous chunks, grid-stride. All of a block's metadata — its 4 chunk counts,
+// the lane's 4 mask words and the counts of the preceding chunks of its 64-chunk superblock —
+// are independent loads issued together (one round trip). The block's output base is the
+// superblock prefix plus that partial sum; empty chunks are skipped without touching any column;
+// the selected rows of the block are staged and flushed with batched gathers into one contiguous
+// output range. No ticket, no look-back, no predicate evaluation.
+template <class P>
+__global__ void __launch_bounds__(kThreads, SEL_PD_MINB) pushdown_sel_kernel(const __grid_constant__ P p,
+                                                                   uint64_t n, SelectionBufs sb,
+                                                                   uint32_t* __restrict__ out_ids) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  __shared__ uint16_t s_idx[kWarpsPerCta][kChunkRows];
-  uint16_t* my = s_idx[warp];
+  __shared__ uint16_t s_stage[kWarpsPerCta][kStageCap];
+  uint16_t* my = s_stage[warp];
   const uint64_t nchunks = (n + kChunkRows - 1) / kChunkRows;
+  const uint64_t nblocks = (nchunks + kBlockChunks - 1) / kBlockChunks;
   const uint64_t gw = (uint64_t)blockIdx.x * kWarpsPerCta + warp;
   const uint64_t nw = (uint64_t)gridDim.x * kWarpsPerCta;
-  for (uint64_t c = gw; c < nchunks; c += nw) {
-    const uint32_t cnt = sb.chunk_cnt[c];
-    if (cnt == 0) continue;
-    const uint32_t m = sb.bits[c * 32 + lane];
-    const uint64_t first = (c >> kSbShift) << kSbShift;
+  for (uint64_t blk = gw; blk < nblocks; blk += nw) {
+    const uint64_t c0 = blk * kBlockChunks;
+    const uint64_t first = (c0 >> kSbShift) << kSbShift;
+    // --- metadata, all loads independent ---
+    const uint32_t cntv = (lane < kBlockChunks && c0 + lane < nchunks) ? sb.chunk_cnt[c0 + lane] : 0u;
+    uint32_t m[kBlockChunks];
+#pragma unroll
+    for (int g = 0; g < kBlockChunks; ++g) m[g] = c0 + g < nchunks ? sb.bits[(c0 + g) * 32 + lane] : 0u;
     uint32_t part = 0;
-    if (first + lane < c) part += sb.chunk_cnt[first + lane];
-    if (first + 32 + lane < c) part += sb.chunk_cnt[first + 32 + lane];
-    const uint64_t gbase = (uint64_t)sb.sb_prefix[c >> kSbShift] + __reduce_add_sync(0xFFFFFFFFu, part);
-    stage_indices(m, lane, my);
+    if (first + lane < c0) part += sb.chunk_cnt[first + lane];
+    if (first + 32 + lane < c0) part += sb.chunk_cnt[first + 32 + lane];
+    const uint32_t sbp = sb.sb_prefix[c0 >> kSbShift];
+    // --- offsets ---
+    const uint32_t total = __reduce_add_sync(0xFFFFFFFFu, cntv);
+    if (total == 0) continue;
+    uint64_t gbase = (uint64_t)sbp + __reduce_add_sync(0xFFFFFFFFu, part);
+    const uint64_t bbase = c0 * kChunkRows;
+    uint32_t staged = 0;
+#pragma unroll
+    for (int g = 0; g < kBlockChunks; ++g) {
+      const uint32_t cg = __shfl_sync(0xFFFFFFFFu, cntv, g);
+      if (cg == 0) continue;
+      if (staged + cg > kStageCap) {
+        __syncwarp();
+        flush_rows(p, bbase, gbase, staged, my, lane, out_ids);
+        __syncwarp();
+        gbase += staged;
+        staged = 0;
+      }
+      if (sb.n_keep) copy_kept(p, sb, c0 + g, gbase + staged, cg, lane);
+      stage_rows(m[g], lane, my, staged, (uint32_t)g * kChunkRows);
+      staged += cg;
+    }
     __syncwarp();
-    write_out(p, c * kChunkRows, gbase, cnt, my, nullptr, lane, out_ids, &sb);
+    flush_rows(p, bbase, gbase, staged, my, lane, out_ids);
     __syncwarp();
   }
 }

@@ -76,6 +76,10 @@ using DevProgramLarge = DevProgramT<256, 128, 1024, 128, 256>;
 // A kept selection (sel_count_ex with SEL_KEEP_SELECTION): per chunk of 1024 rows, the 32 lane
 // masks (bit layout of kernels.cu) and the chunk's count; per superblock of 64 chunks, the sum of
 // its counts and (filled by the push-down) its exclusive prefix.
+#ifndef SEL_BLOCK_CHUNKS
+#define SEL_BLOCK_CHUNKS 2
+#endif
+constexpr int kSelBlockChunks = SEL_BLOCK_CHUNKS;   // push-down from a selection: chunks per warp block
 constexpr int kSbShift = 6;
 constexpr uint64_t kSbChunks = 1ull << kSbShift;
 constexpr int kMaxKeep = 8;
