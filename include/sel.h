@@ -188,6 +188,15 @@ uint64_t sel_pushdown(sel_table table, const void* prog, size_t prog_bytes,
  * force the single pass. */
 int sel_ctx_last_pushdown_path(sel_ctx ctx);
 
+/* sel_count_batch: exact counts of nprog (1..32) programs over the table in
+ * ONE scan — each referenced column is read once per chunk and each distinct leaf (same column and
+ * same canonical interval set, across programs) evaluated once. out_counts: host array of nprog,
+ * global over ranks (one all-reduce of nprog u64). Limits after canonicalisation: <= 32 distinct
+ * leaves, <= 32 columns, <= 1024 intervals, <= 512 postfix ops in total (else SEL_E_ARG).
+ * Errors: as sel_count. Blocks until the counts are on the host. */
+sel_status sel_count_batch(sel_table table, const void* const* progs, const size_t* prog_bytes,
+                           uint32_t nprog, uint64_t* out_counts, void* cuda_stream);
+
 /* Validate a program against column types without running it (host only; no GPU needed).
  * Returns SEL_OK or the status sel_count would report for it. */
 sel_status sel_program_check(const void* prog, size_t prog_bytes, const sel_type* types,

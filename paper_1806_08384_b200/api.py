@@ -173,6 +173,19 @@ class Table:
             raise last_error()
         return int(r)
 
+    def count_batch(self, preds, stream=None) -> list:
+        """Exact counts of several predicates in ONE scan: each column read
+        once, each distinct leaf evaluated once; e.g. the worked example's four leaves and their
+        conjunction (PAPER.md:64, 88)."""
+        progs = [self.program(p) for p in preds]
+        bufs = [ctypes.create_string_buffer(b, len(b)) for b in progs]
+        ptrs = (ctypes.c_void_p * len(progs))(*[ctypes.addressof(b) for b in bufs])
+        lens = (ctypes.c_size_t * len(progs))(*[len(b) for b in progs])
+        out = (ctypes.c_uint64 * len(progs))()
+        check(lib().sel_count_batch(self._h, ptrs, lens, len(progs), out,
+                                    _stream_ptr(stream, self.ctx.device)))
+        return [int(x) for x in out]
+
     def _col_indices(self, cols):
         return [self.names.index(p) if isinstance(p, str) else int(p) for p in cols]
 

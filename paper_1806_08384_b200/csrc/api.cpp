@@ -5,6 +5,7 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <map>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -817,6 +818,111 @@ uint64_t sel_pushdown(sel_table t, const void* prog, size_t prog_bytes, const ui
   if (out_local_count) *out_local_count = local;
   if (out_global_offset) *out_global_offset = offset;
   return total;
+}
+
+sel_status sel_count_batch(sel_table t, const void* const* progs, const size_t* prog_bytes,
+                           uint32_t nprog, uint64_t* out_counts, void* cuda_stream) {
+  clear_error();
+  if (!t || !progs || !prog_bytes || !out_counts) return set_error(SEL_E_ARG, "null argument");
+  if (nprog == 0 || nprog > (uint32_t)kBatchMaxProgs) return set_error(SEL_E_ARG, "nprog must be 1..32");
+  sel_ctx c = t->ctx;
+  if (c->destroyed) return set_error(SEL_E_STATE, "context destroyed");
+  std::vector<Plan> plans(nprog);
+  for (uint32_t k = 0; k < nprog; ++k)
+    if (plan_for(t, progs[k], prog_bytes[k], &plans[k]) != SEL_OK) return g_status;
+  // distinct leaves, grouped by column (first-appearance order)
+  std::vector<int> col_order;
+  std::map<int, std::vector<std::vector<Interval>>> by_col;
+  auto leaf_key = [&](const PlanLeaf& L) -> std::pair<int, int> {
+    auto& lst = by_col[L.col];
+    if (lst.empty()) col_order.push_back(L.col);
+    for (size_t i = 0; i < lst.size(); ++i) {
+      if (lst[i].size() == L.iv.size() &&
+          std::equal(lst[i].begin(), lst[i].end(), L.iv.begin(),
+                     [](const Interval& x, const Interval& y) { return x.lo == y.lo && x.hi == y.hi; }))
+        return {L.col, (int)i};
+    }
+    lst.push_back(L.iv);
+    return {L.col, (int)lst.size() - 1};
+  };
+  std::vector<std::vector<std::pair<int, int>>> prog_leaf(nprog);
+  for (uint32_t k = 0; k < nprog; ++k)
+    for (auto& L : plans[k].leaves) prog_leaf[k].push_back(leaf_key(L));
+  static thread_local BatchProgram bp;
+  std::memset(&bp, 0, sizeof(bp));
+  std::map<std::pair<int, int>, int> leaf_id;
+  uint32_t nl = 0, niv = 0;
+  for (int col : col_order) {
+    if (bp.n_cols >= (uint32_t)kBatchMaxCols) return set_error(SEL_E_ARG, "batch exceeds 32 columns");
+    BatchColumn& C = bp.col[bp.n_cols++];
+    const int type = t->types[col];
+    C.data = t->cols[col].data;
+    C.wclass = wclass_of(type);
+    C.fkey = type == SEL_FLOAT32 ? 1 : 0;
+    C.leaf_begin = (uint16_t)nl;
+    const uint64_t bias = key_sign_bias(type);
+    auto& lst = by_col[col];
+    for (size_t i = 0; i < lst.size(); ++i) {
+      if (nl >= (uint32_t)kBatchMaxLeaves) return set_error(SEL_E_ARG, "batch exceeds 32 distinct leaves");
+      if (niv + lst[i].size() > 1024) return set_error(SEL_E_ARG, "batch exceeds 1024 intervals");
+      leaf_id[{col, (int)i}] = (int)nl;
+      bp.leaf_iv_begin[nl] = (uint16_t)niv;
+      bp.leaf_iv_count[nl] = (uint16_t)lst[i].size();
+      for (const Interval& x : lst[i]) {
+        bp.lo[niv] = x.lo ^ bias;
+        bp.span[niv] = x.hi - x.lo;
+        ++niv;
+      }
+      ++nl;
+    }
+    C.leaf_count = (uint16_t)(nl - C.leaf_begin);
+  }
+  bp.n_leaves = nl;
+  uint32_t nop = 0;
+  std::vector<bool> host_zero(nprog, false);
+  for (uint32_t k = 0; k < nprog; ++k) {
+    const Plan& P = plans[k];
+    if (P.path == PATH_CONST && !P.const_value) { host_zero[k] = true; continue; }  // FALSE: 0
+    if (nop + P.op.size() + 1 > sizeof(bp.op)) return set_error(SEL_E_ARG, "batch exceeds 512 ops");
+    for (size_t i = 0; i < P.op.size(); ++i) {
+      bp.op[nop] = P.op[i];
+      bp.arg[nop] = P.op[i] == DOP_LEAF ? (uint8_t)leaf_id[prog_leaf[k][P.arg[i]]] : 0;
+      ++nop;
+    }
+    bp.op[nop] = DOP_EMIT;   // TRUE (no ops) emits the all-ones mask
+    bp.arg[nop] = (uint8_t)k;
+    ++nop;
+  }
+  bp.n_ops = nop;
+  bp.n_progs = nprog;
+  cudaStream_t stream = (cudaStream_t)cuda_stream;
+  DeviceGuard g(c->device);
+  if (!g.ok) return set_error(SEL_E_CUDA, "cudaSetDevice failed");
+  const uint64_t n = t->local_rows;
+  uint64_t* d_out = c->s.result + 1;
+  cudaError_t e = cudaMemsetAsync(d_out, 0, nprog * sizeof(uint64_t), stream);
+  if (e != cudaSuccess) return set_error(SEL_E_CUDA, cuda_msg("cudaMemsetAsync(batch)", e));
+  if (n > 0 && nop > 0) {
+    const uint64_t nchunks = (n + kChunkRows - 1) / kChunkRows;
+    const uint64_t units = (nchunks + kWarpsPerCta - 1) / kWarpsPerCta;
+    if (c->timing) cudaEventRecord(c->ev0, stream);
+    const int le = launch_count_batch(bp, n, grid_for(c, units, occupancy_count_batch()), d_out, stream);
+    if (le != cudaSuccess) return set_error(SEL_E_CUDA, cuda_msg("batch kernel launch", (cudaError_t)le));
+    if (c->timing) cudaEventRecord(c->ev1, stream);
+  }
+  if (c->comm) {
+    ncclResult_t r = nccl().AllReduce(d_out, d_out, nprog, ncclUint64, ncclSum, c->comm, stream);
+    if (r != ncclSuccess) return set_error(SEL_E_NCCL, nccl_msg("ncclAllReduce(batch)", r));
+  }
+  e = cudaMemcpyAsync(c->h_result + 1, d_out, nprog * sizeof(uint64_t), cudaMemcpyDeviceToHost, stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(stream);
+  if (e != cudaSuccess) return set_error(SEL_E_CUDA, cuda_msg("batch result", e));
+  if (n > 0 && nop > 0 && c->timing) {
+    cudaEventElapsedTime(&c->last_ms, c->ev0, c->ev1);
+    c->last_count_ms = c->last_ms;
+  }
+  for (uint32_t k = 0; k < nprog; ++k) out_counts[k] = c->h_result[1 + k];  // FALSE programs stay 0
+  return SEL_OK;
 }
 
 uint64_t sel_execute(sel_table t, const void* prog, size_t prog_bytes, const uint32_t* proj_cols,

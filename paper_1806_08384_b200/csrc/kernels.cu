@@ -756,6 +756,113 @@ __global__ void __launch_bounds__(kThreads, SEL_PD_MINB) pushdown_sel_kernel(con
   }
 }
 
+
+// ---- batch of programs over one scan -------------------------------------
+// Every column of the batch is loaded once per chunk; each distinct leaf on it is evaluated once
+// into the warp's leaf-mask table (shared memory, one u32 per lane per leaf); each program's
+// postfix then runs over leaf masks and DOP_EMIT(k) adds the warp's popcount to program k's
+// counter. One instance of the interval loop per TAIL variant (toolchain note above).
+template <bool TAIL>
+__device__ __forceinline__ void batch_column(const BatchProgram& p, const BatchColumn& C,
+                                             uint64_t base, int lane, uint32_t nvalid,
+                                             uint32_t* lm /* [leaf][32] */) {
+  if (C.wclass == W8) {
+#pragma unroll 1
+    for (int h = 0; h < 2; ++h) {
+      uint64_t v[16];
+      load_w8_half<TAIL>(C.data, base, lane, h, nvalid, v, nullptr);
+#pragma unroll 1
+      for (uint32_t l = C.leaf_begin; l < (uint32_t)C.leaf_begin + C.leaf_count; ++l) {
+        uint32_t mh = 0;
+#pragma unroll 1
+        for (int t = 0; t < p.leaf_iv_count[l]; ++t) {
+          const uint64_t lo = p.lo[p.leaf_iv_begin[l] + t], sp = p.span[p.leaf_iv_begin[l] + t];
+#pragma unroll
+          for (int i = 0; i < 16; ++i) mh |= (v[i] - lo <= sp) ? (1u << i) : 0u;
+        }
+        if (h == 0) lm[l * 32 + lane] = mh;
+        else lm[l * 32 + lane] |= mh << 16;
+      }
+    }
+    return;
+  }
+  uint32_t v[32];
+  if (C.wclass == W4) {
+    load_w4<TAIL>(C.data, base, lane, nvalid, v, nullptr);
+    if (C.fkey) {
+#pragma unroll
+      for (int i = 0; i < 32; ++i) v[i] = fkey(v[i]);
+    }
+  } else if (C.wclass == W1) {
+    load_w1<TAIL>(C.data, base, lane, nvalid, v, nullptr);
+  } else {
+    load_w2<TAIL>(C.data, base, lane, nvalid, v, nullptr);
+  }
+#pragma unroll 1
+  for (uint32_t l = C.leaf_begin; l < (uint32_t)C.leaf_begin + C.leaf_count; ++l) {
+    uint32_t m = 0;
+#pragma unroll 1
+    for (int t = 0; t < p.leaf_iv_count[l]; ++t) {
+      const uint32_t lo = (uint32_t)p.lo[p.leaf_iv_begin[l] + t];
+      const uint32_t sp = (uint32_t)p.span[p.leaf_iv_begin[l] + t];
+#pragma unroll
+      for (int i = 0; i < 32; ++i) m |= (v[i] - lo <= sp) ? (1u << i) : 0u;
+    }
+    lm[l * 32 + lane] = m;
+  }
+}
+
+template <bool TAIL>
+__device__ __forceinline__ void batch_chunk(const BatchProgram& p, uint64_t base, int lane,
+                                            uint32_t nvalid, uint32_t* lm, uint32_t* cnt /* [k] */) {
+#pragma unroll 1
+  for (uint32_t c = 0; c < p.n_cols; ++c) batch_column<TAIL>(p, p.col[c], base, lane, nvalid, lm);
+  __syncwarp();
+  const uint32_t valid = TAIL ? valid_mask(lane, nvalid) : 0xFFFFFFFFu;
+  uint32_t st[kMaxDeviceStack];
+  int sp = 0;
+#pragma unroll 1
+  for (uint32_t i = 0; i < p.n_ops; ++i) {
+    const uint8_t op = p.op[i];
+    if (op == DOP_LEAF) {
+      st[sp++] = lm[p.arg[i] * 32 + lane];
+    } else if (op == DOP_EMIT) {
+      const uint32_t m = sp > 0 ? st[--sp] : 0xFFFFFFFFu;    // an empty program is TRUE
+      const uint32_t c = __reduce_add_sync(0xFFFFFFFFu, (uint32_t)__popc(m & valid));
+      if (lane == 0) cnt[p.arg[i]] += c;
+      sp = 0;
+    } else {
+      --sp;
+      st[sp - 1] = op == DOP_AND ? (st[sp - 1] & st[sp]) : (st[sp - 1] | st[sp]);
+    }
+  }
+  __syncwarp();
+}
+
+__global__ void __launch_bounds__(kThreads) count_batch_kernel(const __grid_constant__ BatchProgram p,
+                                                               uint64_t n, uint64_t* __restrict__ out) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  __shared__ uint32_t s_lm[kWarpsPerCta][kBatchMaxLeaves * 32];
+  __shared__ uint32_t s_cnt[kWarpsPerCta][kBatchMaxProgs];
+  for (int k = lane; k < kBatchMaxProgs; k += 32) s_cnt[warp][k] = 0;
+  __syncwarp();
+  const uint64_t nfull = n / kChunkRows;
+  const uint32_t rem = (uint32_t)(n % kChunkRows);
+  const uint64_t gw = (uint64_t)blockIdx.x * kWarpsPerCta + warp;
+  const uint64_t nw = (uint64_t)gridDim.x * kWarpsPerCta;
+  for (uint64_t c = gw; c < nfull; c += nw)
+    batch_chunk<false>(p, c * kChunkRows, lane, kChunkRows, s_lm[warp], s_cnt[warp]);
+  if (rem != 0 && gw == nfull % nw)
+    batch_chunk<true>(p, nfull * kChunkRows, lane, rem, s_lm[warp], s_cnt[warp]);
+  __syncthreads();
+  for (uint32_t k = threadIdx.x; k < p.n_progs; k += kThreads) {
+    uint64_t s = 0;
+#pragma unroll
+    for (int w = 0; w < kWarpsPerCta; ++w) s += s_cnt[w][k];
+    if (s) atomicAdd(reinterpret_cast<unsigned long long*>(out + k), (unsigned long long)s);
+  }
+}
+
 template <class Kern>
 int occupancy_of(Kern k, size_t dyn_smem) {
   int blocks = 0;
@@ -824,6 +931,11 @@ int prepare_kernels() {
                              cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
   return (int)e;
 }
+int launch_count_batch(const BatchProgram& p, uint64_t n, int grid, uint64_t* out, void* st) {
+  count_batch_kernel<<<grid, kThreads, 0, (cudaStream_t)st>>>(p, n, out);
+  return (int)cudaGetLastError();
+}
+int occupancy_count_batch() { return occupancy_of(count_batch_kernel, 0); }
 int occupancy_count_small() { return occupancy_of(count_kernel<DevProgramSmall, false>, 0); }
 int occupancy_count_keep_small(size_t dyn) { return occupancy_of(count_kernel<DevProgramSmall, true>, dyn); }
 int occupancy_count_keep_large(size_t dyn) { return occupancy_of(count_kernel<DevProgramLarge, true>, dyn); }

@@ -73,6 +73,32 @@ struct DevProgramT {
 using DevProgramSmall = DevProgramT<64, 32, 64, 32, 16>;
 using DevProgramLarge = DevProgramT<256, 128, 1024, 128, 256>;
 
+// Batch of programs over one scan (sel_count_batch): distinct leaves of all
+// programs grouped by column (each column loaded once per chunk, each leaf evaluated once into a
+// shared-memory leaf-mask table), then each program's postfix over leaf masks, DOP_EMIT(k) ending
+// program k.
+constexpr int kBatchMaxLeaves = 32, kBatchMaxProgs = 32, kBatchMaxCols = 32;
+constexpr uint8_t DOP_EMIT = 3;
+struct BatchColumn {
+  const void* data;
+  uint8_t wclass, fkey;
+  uint16_t leaf_begin, leaf_count;  // its leaves are [leaf_begin, leaf_begin + leaf_count)
+  uint16_t pad;
+};
+struct BatchProgram {
+  uint32_t n_cols, n_leaves, n_ops, n_progs;
+  BatchColumn col[kBatchMaxCols];
+  uint16_t leaf_iv_begin[kBatchMaxLeaves];
+  uint16_t leaf_iv_count[kBatchMaxLeaves];
+  uint8_t op[512];
+  uint8_t arg[512];
+  uint64_t lo[1024];
+  uint64_t span[1024];
+};
+int launch_count_batch(const BatchProgram& p, uint64_t n, int grid, uint64_t* out_counts,
+                       void* stream);
+int occupancy_count_batch();
+
 // A kept selection (sel_count_ex with SEL_KEEP_SELECTION): per chunk of 1024 rows, the 32 lane
 // masks (bit layout of kernels.cu) and the chunk's count; per superblock of 64 chunks, the sum of
 // its counts and (filled by the push-down) its exclusive prefix.
