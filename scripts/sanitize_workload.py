@@ -1,0 +1,34 @@
+"""Small-size exercise of every kernel path (count, selection push-down, single pass, kept values,
+batch) for compute-sanitizer; see scripts/sanitize.sh."""
+import sys
+sys.path.insert(0, '.'); sys.path.insert(0, 'tests')
+import numpy as np, torch
+import oracle, paper_1806_08384_b200 as sel
+from selgen import configs, encode
+from selgen.program import *
+from helpers import random_table
+dev = torch.device('cuda:0')
+ctx = sel.Context(dev)
+for n in [5, 1025, 70_001]:
+    rng = np.random.default_rng(n)
+    types = [INT32, DICT8, INT64, FLOAT32, DICT16]
+    cols, pools = random_table(rng, types, n)
+    view = {INT32: np.int32, INT64: np.int64, FLOAT32: np.float32, DICT8: np.uint8, DICT16: np.int16}
+    t = sel.Table(ctx, [f"c{i}" for i in range(5)], types,
+                  [torch.from_numpy(np.ascontiguousarray(c).view(view[ty]).copy()).to(dev) for c, ty in zip(cols, types)])
+    for _ in range(4):
+        node = random_program(rng, types, pools, max_depth=3)
+        prog = encode(node, types)
+        want = oracle.pushdown(cols, types, prog, proj=[0, 1, 2])
+        c = t.count(prog)
+        r1 = t.execute(prog, project=[0, 1, 2], max_size=n)                  # selection path
+        t.count(encode(Const(True), types), keep_selection=True)
+        r2 = t.pushdown(prog, project=[0, 1, 2], capacity=max(want[0], 1))    # single pass
+        t.count(prog, keep_selection=True, keep_columns=[0, 1, 2])
+        r3 = t.pushdown(prog, project=[0, 1, 2], capacity=max(want[0], 1))    # kept values
+        b = t.count_batch([prog, encode(Not(node), types)])
+        assert c == want[0] == r1.count == r2.count == r3.count and b[0] + b[1] == n
+        for r in (r1, r2, r3):
+            assert np.array_equal(r.rowids.cpu().numpy().view(np.uint32), want[1])
+torch.cuda.synchronize()
+print("sanitize workload ok")
