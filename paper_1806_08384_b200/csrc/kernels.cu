@@ -23,6 +23,10 @@
 
 #include "sel_internal.h"
 
+#ifndef SEL_SB_ATOMICS
+#define SEL_SB_ATOMICS 1   // 0: superblock sums by a separate kernel (measured equal, one more launch)
+#endif
+
 namespace sel {
 namespace {
 
@@ -439,7 +443,9 @@ __device__ __forceinline__ void keep_chunk(const SelectionBufs& sb, uint64_t c, 
   }
   if (lane == 0) {
     sb.chunk_cnt[c] = (uint16_t)cc;
+#if SEL_SB_ATOMICS
     if (cc) atomicAdd(&sb.sb_sum[c >> kSbShift], cc);
+#endif
   }
 }
 
@@ -574,6 +580,25 @@ __global__ void __launch_bounds__(kThreads, 3) pushdown_kernel(
 
 
 // ---- push-down from a kept selection ------------------------------------------------------------
+#if !SEL_SB_ATOMICS
+// Per-64-chunk sums of the kept chunk counts (one warp per superblock, 2 counts per lane).
+__global__ void __launch_bounds__(kThreads) superblock_sum_kernel(const uint16_t* __restrict__ cnt,
+                                                                  uint64_t nchunks,
+                                                                  uint32_t* __restrict__ sb_sum) {
+  const int lane = threadIdx.x & 31;
+  const uint64_t nsb = (nchunks + kSbChunks - 1) / kSbChunks;
+  const uint64_t w = (uint64_t)blockIdx.x * kWarpsPerCta + (threadIdx.x >> 5);
+  const uint64_t nw = (uint64_t)gridDim.x * kWarpsPerCta;
+  for (uint64_t sb = w; sb < nsb; sb += nw) {
+    const uint64_t c = sb * kSbChunks + lane;
+    uint32_t v = (c < nchunks ? cnt[c] : 0u) + (c + 32 < nchunks ? cnt[c + 32] : 0u);
+    v = __reduce_add_sync(0xFFFFFFFFu, v);
+    if (lane == 0) sb_sum[sb] = v;
+  }
+}
+
+#endif
+
 // Exclusive prefix of the per-64-chunk sums kept by the count kernel (one CTA; <= 65536 sums).
 __global__ void __launch_bounds__(1024) superblock_prefix_kernel(const uint32_t* __restrict__ sb_sum,
                                                                  uint32_t* __restrict__ sb_prefix,
@@ -892,6 +917,10 @@ int launch_pushdown_sel_small(const DevProgramSmall& p, uint64_t n, uint32_t* ou
                               const Scratch& s, const SelectionBufs& sb, void* st) {
   const uint64_t nchunks = (n + kChunkRows - 1) / kChunkRows;
   const uint32_t nsb = (uint32_t)((nchunks + kSbChunks - 1) / kSbChunks);
+#if !SEL_SB_ATOMICS
+  superblock_sum_kernel<<<(unsigned)(nsb < 148ull * 16 * kWarpsPerCta ? (nsb + kWarpsPerCta - 1) / kWarpsPerCta : 148ull * 16), kThreads, 0,
+                          (cudaStream_t)st>>>(sb.chunk_cnt, nchunks, sb.sb_sum);
+#endif
   superblock_prefix_kernel<<<1, 1024, 0, (cudaStream_t)st>>>(sb.sb_sum, sb.sb_prefix, nsb, s.result);
   pushdown_sel_kernel<DevProgramSmall><<<grid, kThreads, 0, (cudaStream_t)st>>>(p, n, sb, out_ids);
   return (int)cudaGetLastError();
@@ -900,6 +929,10 @@ int launch_pushdown_sel_large(const DevProgramLarge& p, uint64_t n, uint32_t* ou
                               const Scratch& s, const SelectionBufs& sb, void* st) {
   const uint64_t nchunks = (n + kChunkRows - 1) / kChunkRows;
   const uint32_t nsb = (uint32_t)((nchunks + kSbChunks - 1) / kSbChunks);
+#if !SEL_SB_ATOMICS
+  superblock_sum_kernel<<<(unsigned)(nsb < 148ull * 16 * kWarpsPerCta ? (nsb + kWarpsPerCta - 1) / kWarpsPerCta : 148ull * 16), kThreads, 0,
+                          (cudaStream_t)st>>>(sb.chunk_cnt, nchunks, sb.sb_sum);
+#endif
   superblock_prefix_kernel<<<1, 1024, 0, (cudaStream_t)st>>>(sb.sb_sum, sb.sb_prefix, nsb, s.result);
   pushdown_sel_kernel<DevProgramLarge><<<grid, kThreads, 0, (cudaStream_t)st>>>(p, n, sb, out_ids);
   return (int)cudaGetLastError();
