@@ -464,7 +464,7 @@ def run_ours(args):
                        "rows_per_gpu": e - s, "selected": global_count,
                        "parallelism": f"row-shard x{world}",
                        "l2": "inputs larger than L2 (no flush needed)",
-                       "step": "sel_execute = count (keep selection + projected predicate values) -> gate -> materialise"},
+                       "step": "sel_execute = count (keeping the selection) -> gate -> materialise"},
             "latency_ms": {"execute_median": round(statistics.median(count_lat), 4),
                            "execute_min": round(min(count_lat), 4),
                            "count_kernel": round(count_k, 4), "pushdown_kernels": round(push_k, 4)},

@@ -417,11 +417,24 @@ __device__ __forceinline__ uint32_t stage_indices(uint32_t m, int lane, uint16_t
 // columns (the compound's projected predicate columns, known before the count: ExtractPushDown
 // returns conditions AND columns) the values loaded for the predicate are
 // captured in shared memory and the chunk's selected ones written, compacted, to its slot.
+// Quad layout (bit 4k+e of lane l = row 4(32k+l)+e) -> row-major (bit b of lane L = row 32L+b):
+// lane L = 4k + j gathers nibble k of lanes 8j..8j+7 (row 128k + 32j + 4i + e = 32L + 4i + e).
+__device__ __forceinline__ uint32_t to_row_major(uint32_t m, int lane) {
+  const int k = lane >> 2, j = lane & 3;
+  uint32_t t = 0;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const uint32_t v = __shfl_sync(0xFFFFFFFFu, m, 8 * j + i);
+    t |= ((v >> (4 * k)) & 0xFu) << (4 * i);
+  }
+  return t;
+}
+
 template <class P, bool KEEP>
 __device__ __forceinline__ void keep_chunk(const SelectionBufs& sb, uint64_t c, int lane, uint32_t m,
                                            char* wsmem) {
   if (!KEEP) return;
-  sb.bits[c * 32 + lane] = m;
+  sb.bits[c * 32 + lane] = to_row_major(m, lane);   // the push-down stages from row-major masks
   uint32_t cc;
   if (sb.n_keep) {
     uint16_t* my = reinterpret_cast<uint16_t*>(wsmem);
@@ -635,37 +648,24 @@ __global__ void __launch_bounds__(1024) superblock_prefix_kernel(const uint32_t*
   }
 }
 
-// Stage the rows selected by the lanes' masks of one chunk at my[base..], as block-relative row
-// numbers (row_base + chunk-local row), ascending; same scan as stage_indices.
-__device__ __forceinline__ void stage_rows(uint32_t m, int lane, uint16_t* my, uint32_t base,
-                                           uint32_t row_base) {
-  uint32_t cw0 = 0, cw1 = 0;
-#pragma unroll
-  for (int k = 0; k < 4; ++k) {
-    cw0 |= (uint32_t)__popc((m >> (4 * k)) & 0xFu) << (8 * k);
-    cw1 |= (uint32_t)__popc((m >> (4 * (k + 4))) & 0xFu) << (8 * k);
-  }
-  uint32_t ex0 = cw0, ex1 = cw1;
+// Stage the rows of one chunk from its ROW-MAJOR kept masks (lane L: rows 32L..32L+31) at
+// my[base..] as block-relative rows, ascending: one warp scan of per-lane popcounts, then each lane
+// walks its set bits.
+__device__ __forceinline__ void stage_rows_rm(uint32_t t, int lane, uint16_t* my, uint32_t base,
+                                              uint32_t row_base) {
+  const uint32_t c = (uint32_t)__popc(t);
+  uint32_t incl = c;
 #pragma unroll
   for (int d = 1; d < 32; d <<= 1) {
-    const uint32_t t0 = __shfl_up_sync(0xFFFFFFFFu, ex0, d);
-    const uint32_t t1 = __shfl_up_sync(0xFFFFFFFFu, ex1, d);
-    if (lane >= d) { ex0 += t0; ex1 += t1; }
+    const uint32_t v = __shfl_up_sync(0xFFFFFFFFu, incl, d);
+    if (lane >= d) incl += v;
   }
-  const uint32_t tot0 = __shfl_sync(0xFFFFFFFFu, ex0, 31), tot1 = __shfl_sync(0xFFFFFFFFu, ex1, 31);
-  ex0 -= cw0;
-  ex1 -= cw1;
-  uint32_t acc = base;
-#pragma unroll
-  for (int k = 0; k < 8; ++k) {
-    const uint32_t nib = (m >> (4 * k)) & 0xFu;
-    uint32_t pos = acc + (((k < 4 ? ex0 : ex1) >> (8 * (k & 3))) & 0xFFu);
-    acc += ((k < 4 ? tot0 : tot1) >> (8 * (k & 3))) & 0xFFu;
-    if (nib == 0) continue;
-    const uint32_t r0 = row_base + 4u * (32u * k + lane);
-#pragma unroll
-    for (int e = 0; e < 4; ++e)
-      if (nib & (1u << e)) my[pos++] = (uint16_t)(r0 + e);
+  uint32_t pos = base + incl - c;
+  const uint32_t r0 = row_base + 32u * lane;
+  while (t) {
+    const uint32_t b = (uint32_t)(__ffs(t) - 1);
+    t &= t - 1;
+    my[pos++] = (uint16_t)(r0 + b);
   }
 }
 
@@ -772,7 +772,7 @@ __global__ void __launch_bounds__(kThreads, SEL_PD_MINB) pushdown_sel_kernel(con
         staged = 0;
       }
       if (sb.n_keep) copy_kept(p, sb, c0 + g, gbase + staged, cg, lane);
-      stage_rows(m[g], lane, my, staged, (uint32_t)g * kChunkRows);
+      stage_rows_rm(m[g], lane, my, staged, (uint32_t)g * kChunkRows);
       staged += cg;
     }
     __syncwarp();

@@ -99,8 +99,9 @@ int launch_count_batch(const BatchProgram& p, uint64_t n, int grid, uint64_t* ou
                        void* stream);
 int occupancy_count_batch();
 
-// A kept selection (sel_count_ex with SEL_KEEP_SELECTION): per chunk of 1024 rows, the 32 lane
-// masks (bit layout of kernels.cu) and the chunk's count; per superblock of 64 chunks, the sum of
+// A kept selection (sel_count_ex with SEL_KEEP_SELECTION): per chunk of 1024 rows, 32 row-major
+// mask words (word L, bit b = row 32L + b of the chunk) and the chunk's count; per superblock of
+// 64 chunks, the sum of
 // its counts and (filled by the push-down) its exclusive prefix.
 #ifndef SEL_BLOCK_CHUNKS
 #define SEL_BLOCK_CHUNKS 2
