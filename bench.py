@@ -436,8 +436,17 @@ def run_ours(args):
         return int(torch.unique_consecutive(ids64 // (32 // width)).numel())
     write_b = local_count * (4 + sum(w_all[j] for j in proj))
     if pd_path == 1:
+        # projected predicate columns whose values the count kept (sel_execute's default, within
+        # 8 B/row) are copied contiguously from their slots: count x width, not sectors
+        kept, budget = set(), 8
+        if os.environ.get("SEL_KEEP_VALUES", "1") != "0":
+            for j in proj:
+                if j in pc and j not in kept and w_all[j] <= budget:
+                    kept.add(j)
+                    budget -= w_all[j]
         pb_sector = (T.n_rows // 8 + 2 * ((T.n_rows + 1023) // 1024)
-                     + sum(32 * sectors(w_all[j]) for j in set(proj)) + write_b)
+                     + sum(local_count * w_all[j] for j in kept)
+                     + sum(32 * sectors(w_all[j]) for j in set(proj) if j not in kept) + write_b)
     else:
         pb_sector = (T.n_rows * sum(w_all[j] for j in pc)
                      + sum(32 * sectors(w_all[j]) for j in set(proj) if j not in pc) + write_b)

@@ -149,8 +149,8 @@ uint64_t sel_count_ex(sel_table table, const void* prog, size_t prog_bytes, uint
                       const uint32_t* keep_cols, uint32_t nkeep, void* cuda_stream);
 
 /* sel_execute: Algorithm 1's Execute(compound, isSPD = true, maxSize) in one
- * call: count with SEL_KEEP_SELECTION (and, with SEL_KEEP_VALUES=1 in the environment, the
- * projected predicate columns' values), then if the
+ * call: count with SEL_KEEP_SELECTION and the projected predicate columns' values (environment
+ * SEL_KEEP_VALUES=0: the selection only), then if the
  * GLOBAL count > max_size "throw" — *out_materialized = 0, nothing is written, *out_local_count
  * and *out_global_offset are set to 0 — else materialise exactly like sel_pushdown (from the kept
  * selection) and set *out_materialized = 1. Returns the global count or SEL_ERR. Arguments as

@@ -141,8 +141,8 @@ struct sel_ctx_s {
   uint64_t slot_cap[kMaxKeep] = {};  // bytes allocated per slot
   int last_pd_path = -1;
   bool force_single = false;
-  bool prefetch = true;
-  bool keep_values = false;
+  int prefetch_mode = -1;   // -1 auto, 0 off, 1 on
+  bool keep_values = true;
   float last_count_ms = 0.f, last_push_ms = 0.f;
 };
 
@@ -173,7 +173,7 @@ void pack(const Plan& plan, const sel_table_s* t, P* p) {
   uint32_t nslots = 0, iv = 0;
   p->n_ops = (uint32_t)plan.op.size();
   p->n_leaves = (uint32_t)plan.leaves.size();
-  p->prefetch = t->ctx->prefetch ? 1u : 0u;
+  p->prefetch = t->ctx->prefetch_mode == 1 ? 1u : 0u;
   p->conj = plan.path != PATH_INTERP ? 1u : 0u;
   for (size_t i = 0; i < plan.op.size(); ++i) {
     p->op[i] = plan.op[i];
@@ -301,10 +301,12 @@ sel_status sel_ctx_create(int cuda_device, sel_ctx* out) {
     delete c;
     return set_error(SEL_E_CUDA, "cudaFuncSetAttribute(push-down shared memory) failed");
   }
+  // L2 bulk prefetch of the next chunk: measured to help the count that keeps values (extra
+  // per-chunk compaction) and to hurt the plain streaming count; SEL_PREFETCH=0/1 forces it.
   const char* pf = std::getenv("SEL_PREFETCH");
-  c->prefetch = pf && std::strcmp(pf, "1") == 0;  // measured: slower for the plain count on C2
+  c->prefetch_mode = pf ? (std::strcmp(pf, "1") == 0 ? 1 : 0) : -1;
   const char* kv = std::getenv("SEL_KEEP_VALUES");
-  c->keep_values = kv && std::strcmp(kv, "1") == 0;
+  c->keep_values = !(kv && std::strcmp(kv, "0") == 0);
   const char* pp = std::getenv("SEL_PUSHDOWN_PATH");
   c->force_single = pp && std::strcmp(pp, "single") == 0;
   const char* env = std::getenv("SEL_CTAS_PER_SM");
@@ -617,12 +619,14 @@ uint64_t sel_count_ex(sel_table t, const void* prog, size_t prog_bytes, uint32_t
       DevProgramSmall p;
       pack(plan, t, &p);
       mark_captures(&p);
+      if (c->prefetch_mode < 0) p.prefetch = (keep && keep->n_keep) ? 1u : 0u;
       const int occ = keep ? occupancy_count_keep_small(dyn) : c->occ_count_small;
       le = launch_count_small(p, n, grid_for(c, units, occ), c->s, keep, stream);
     } else {
       static thread_local DevProgramLarge p;
       pack(plan, t, &p);
       mark_captures(&p);
+      if (c->prefetch_mode < 0) p.prefetch = (keep && keep->n_keep) ? 1u : 0u;
       const int occ = keep ? occupancy_count_keep_large(dyn) : c->occ_count_large;
       le = launch_count_large(p, n, grid_for(c, units, occ), c->s, keep, stream);
     }
@@ -932,9 +936,9 @@ uint64_t sel_execute(sel_table t, const void* prog, size_t prog_bytes, const uin
   if (out_materialized) *out_materialized = 0;
   if (out_local_count) *out_local_count = 0;
   if (out_global_offset) *out_global_offset = 0;
-  // Execute(isSPD): gamma_COUNT over the compound, keeping what the materialisation reuses.
-  // Kept values of projected predicate columns are opt-in (SEL_KEEP_VALUES=1): on C2 the extra
-  // per-row compaction in the count costs more than the re-read it saves.
+  // Execute(isSPD): gamma_COUNT over the compound, keeping what the materialisation reuses: the
+  // selection and the projected predicate columns' values (SEL_KEEP_VALUES=0 keeps the selection
+  // only; DESIGN.md §6 has both measured).
   const bool keep_values = t && t->ctx->keep_values;
   const uint64_t count = sel_count_ex(t, prog, prog_bytes, SEL_KEEP_SELECTION,
                                       keep_values ? proj_cols : nullptr, keep_values ? nproj : 0u,

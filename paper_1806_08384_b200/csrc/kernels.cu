@@ -417,6 +417,27 @@ __device__ __forceinline__ uint32_t stage_indices(uint32_t m, int lane, uint16_t
 // columns (the compound's projected predicate columns, known before the count: ExtractPushDown
 // returns conditions AND columns) the values loaded for the predicate are
 // captured in shared memory and the chunk's selected ones written, compacted, to its slot.
+// Stage the rows of one chunk from its ROW-MAJOR kept masks (lane L: rows 32L..32L+31) at
+// my[base..] as block-relative rows, ascending: one warp scan of per-lane popcounts, then each lane
+// walks its set bits.
+__device__ __forceinline__ void stage_rows_rm(uint32_t t, int lane, uint16_t* my, uint32_t base,
+                                              uint32_t row_base) {
+  const uint32_t c = (uint32_t)__popc(t);
+  uint32_t incl = c;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const uint32_t v = __shfl_up_sync(0xFFFFFFFFu, incl, d);
+    if (lane >= d) incl += v;
+  }
+  uint32_t pos = base + incl - c;
+  const uint32_t r0 = row_base + 32u * lane;
+  while (t) {
+    const uint32_t b = (uint32_t)(__ffs(t) - 1);
+    t &= t - 1;
+    my[pos++] = (uint16_t)(r0 + b);
+  }
+}
+
 // Quad layout (bit 4k+e of lane l = row 4(32k+l)+e) -> row-major (bit b of lane L = row 32L+b):
 // lane L = 4k + j gathers nibble k of lanes 8j..8j+7 (row 128k + 32j + 4i + e = 32L + 4i + e).
 __device__ __forceinline__ uint32_t to_row_major(uint32_t m, int lane) {
@@ -434,11 +455,13 @@ template <class P, bool KEEP>
 __device__ __forceinline__ void keep_chunk(const SelectionBufs& sb, uint64_t c, int lane, uint32_t m,
                                            char* wsmem) {
   if (!KEEP) return;
-  sb.bits[c * 32 + lane] = to_row_major(m, lane);   // the push-down stages from row-major masks
+  const uint32_t t = to_row_major(m, lane);          // the push-down stages from row-major masks
+  sb.bits[c * 32 + lane] = t;
   uint32_t cc;
   if (sb.n_keep) {
     uint16_t* my = reinterpret_cast<uint16_t*>(wsmem);
-    cc = stage_indices(m, lane, my);
+    stage_rows_rm(t, lane, my, 0u, 0u);
+    cc = __reduce_add_sync(0xFFFFFFFFu, (uint32_t)__popc(t));
     __syncwarp();
 #pragma unroll 1
     for (uint32_t k = 0; k < sb.n_keep; ++k) {
@@ -645,27 +668,6 @@ __global__ void __launch_bounds__(1024) superblock_prefix_kernel(const uint32_t*
   for (uint32_t i = b; i < e; ++i) {
     sb_prefix[i] = run;
     run += sb_sum[i];
-  }
-}
-
-// Stage the rows of one chunk from its ROW-MAJOR kept masks (lane L: rows 32L..32L+31) at
-// my[base..] as block-relative rows, ascending: one warp scan of per-lane popcounts, then each lane
-// walks its set bits.
-__device__ __forceinline__ void stage_rows_rm(uint32_t t, int lane, uint16_t* my, uint32_t base,
-                                              uint32_t row_base) {
-  const uint32_t c = (uint32_t)__popc(t);
-  uint32_t incl = c;
-#pragma unroll
-  for (int d = 1; d < 32; d <<= 1) {
-    const uint32_t v = __shfl_up_sync(0xFFFFFFFFu, incl, d);
-    if (lane >= d) incl += v;
-  }
-  uint32_t pos = base + incl - c;
-  const uint32_t r0 = row_base + 32u * lane;
-  while (t) {
-    const uint32_t b = (uint32_t)(__ffs(t) - 1);
-    t &= t - 1;
-    my[pos++] = (uint16_t)(r0 + b);
   }
 }
 

@@ -52,7 +52,7 @@ def single():
     return ctx.last_times()[1]
 
 
-print('prefetch', os.environ.get('SEL_PREFETCH', '1'))
+print('prefetch', os.environ.get('SEL_PREFETCH', 'auto'))
 print('plain count        %.3f ms' % med(plain))
 km = [keep_mask() for _ in range(12)][3:]
 print('keep mask   count  %.3f  pushdown %.3f' % (statistics.median(x[0] for x in km), statistics.median(x[1] for x in km)))
