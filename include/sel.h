@@ -197,6 +197,14 @@ int sel_ctx_last_pushdown_path(sel_ctx ctx);
 sel_status sel_count_batch(sel_table table, const void* const* progs, const size_t* prog_bytes,
                            uint32_t nprog, uint64_t* out_counts, void* cuda_stream);
 
+/* sel_count_sampled: the exact count over a BLOCK SAMPLE of the table —
+ * the 1024-row chunks c with c mod stride == phase (stride >= 1, phase < stride; stride 1 is the
+ * whole table) — for the sampling estimator |sigma(R')| * |R| / |R'| of PAPER.md:199-203, shown
+ * beside the exact probe. *out_sample_rows (may be NULL) receives |R'|. Global over ranks.
+ * Returns the sample's count or SEL_ERR (SEL_E_ARG for a bad stride/phase; as sel_count). */
+uint64_t sel_count_sampled(sel_table table, const void* prog, size_t prog_bytes, uint32_t stride,
+                           uint32_t phase, uint64_t* out_sample_rows, void* cuda_stream);
+
 /* Validate a program against column types without running it (host only; no GPU needed).
  * Returns SEL_OK or the status sel_count would report for it. */
 sel_status sel_program_check(const void* prog, size_t prog_bytes, const sel_type* types,

@@ -186,6 +186,19 @@ class Table:
                                     _stream_ptr(stream, self.ctx.device)))
         return [int(x) for x in out]
 
+    def count_sampled(self, pred, stride: int, phase: int = 0, stream=None) -> tuple:
+        """Exact count over the block sample of chunks c = phase (mod stride) (SURVEY §8f NEXT(4));
+        returns (sample count, sample rows, estimate = count * rows / sample rows) — the sampling
+        estimator of PAPER.md:199-203, to set beside the exact probe."""
+        prog = self.program(pred)
+        rows = ctypes.c_uint64(0)
+        r = lib().sel_count_sampled(self._h, prog, len(prog), int(stride), int(phase),
+                                    ctypes.byref(rows), _stream_ptr(stream, self.ctx.device))
+        if r == SEL_ERR:
+            raise last_error()
+        est = r * self.global_rows / rows.value if rows.value else 0.0
+        return int(r), int(rows.value), est
+
     def _col_indices(self, cols):
         return [self.names.index(p) if isinstance(p, str) else int(p) for p in cols]
 

@@ -174,6 +174,8 @@ void pack(const Plan& plan, const sel_table_s* t, P* p) {
   p->n_ops = (uint32_t)plan.op.size();
   p->n_leaves = (uint32_t)plan.leaves.size();
   p->prefetch = t->ctx->prefetch_mode == 1 ? 1u : 0u;
+  p->chunk_stride = 1;
+  p->chunk_phase = 0;
   p->conj = plan.path != PATH_INTERP ? 1u : 0u;
   for (size_t i = 0; i < plan.op.size(); ++i) {
     p->op[i] = plan.op[i];
@@ -822,6 +824,63 @@ uint64_t sel_pushdown(sel_table t, const void* prog, size_t prog_bytes, const ui
   if (out_local_count) *out_local_count = local;
   if (out_global_offset) *out_global_offset = offset;
   return total;
+}
+
+uint64_t sel_count_sampled(sel_table t, const void* prog, size_t prog_bytes, uint32_t stride,
+                           uint32_t phase, uint64_t* out_sample_rows, void* cuda_stream) {
+  clear_error();
+  if (!t) return fail64(SEL_E_ARG, "null table");
+  if (stride == 0 || phase >= stride) return fail64(SEL_E_ARG, "need stride >= 1 and phase < stride");
+  sel_ctx c = t->ctx;
+  if (c->destroyed) return fail64(SEL_E_STATE, "context destroyed");
+  Plan plan;
+  if (plan_for(t, prog, prog_bytes, &plan) != SEL_OK) return SEL_ERR;
+  cudaStream_t stream = (cudaStream_t)cuda_stream;
+  DeviceGuard g(c->device);
+  if (!g.ok) return fail64(SEL_E_CUDA, "cudaSetDevice failed");
+  const uint64_t n = t->local_rows;
+  const uint64_t nfull = n / kChunkRows, rem = n % kChunkRows;
+  const uint64_t ns_full = nfull > phase ? (nfull - phase + stride - 1) / stride : 0;
+  const bool tail = rem != 0 && nfull >= phase && (nfull - phase) % stride == 0;
+  const uint64_t sample_rows = ns_full * kChunkRows + (tail ? rem : 0);
+  const bool scan = sample_rows > 0 && plan.path != PATH_CONST;
+  uint64_t local = scan ? 0 : (plan.path == PATH_CONST && plan.const_value ? sample_rows : 0);
+  cudaError_t e;
+  if (scan) {
+    const uint64_t units = (ns_full + 1 + kWarpsPerCta - 1) / kWarpsPerCta;
+    const size_t nslots = count_slots(plan);
+    int le;
+    if (fits_block<DevProgramSmall>(plan, nslots, 0)) {
+      DevProgramSmall p;
+      pack(plan, t, &p);
+      p.chunk_stride = stride;
+      p.chunk_phase = phase;
+      le = launch_count_small(p, n, grid_for(c, units, c->occ_count_small), c->s, nullptr, stream);
+    } else {
+      static thread_local DevProgramLarge p;
+      pack(plan, t, &p);
+      p.chunk_stride = stride;
+      p.chunk_phase = phase;
+      le = launch_count_large(p, n, grid_for(c, units, c->occ_count_large), c->s, nullptr, stream);
+    }
+    if (le != cudaSuccess) return fail64(SEL_E_CUDA, cuda_msg("sampled count launch", (cudaError_t)le));
+  } else {
+    c->h_result[0] = local;
+    e = cudaMemcpyAsync(c->s.result, c->h_result, sizeof(uint64_t), cudaMemcpyHostToDevice, stream);
+    if (e != cudaSuccess) return fail64(SEL_E_CUDA, cuda_msg("cudaMemcpyAsync", e));
+  }
+  c->h_result[1] = sample_rows;
+  e = cudaMemcpyAsync(c->s.result + 1, c->h_result + 1, sizeof(uint64_t), cudaMemcpyHostToDevice, stream);
+  if (e != cudaSuccess) return fail64(SEL_E_CUDA, cuda_msg("cudaMemcpyAsync", e));
+  if (c->comm) {
+    ncclResult_t r = nccl().AllReduce(c->s.result, c->s.result, 2, ncclUint64, ncclSum, c->comm, stream);
+    if (r != ncclSuccess) return fail64(SEL_E_NCCL, nccl_msg("ncclAllReduce(sampled)", r));
+  }
+  e = cudaMemcpyAsync(c->h_result, c->s.result, 2 * sizeof(uint64_t), cudaMemcpyDeviceToHost, stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(stream);
+  if (e != cudaSuccess) return fail64(SEL_E_CUDA, cuda_msg("sampled count result", e));
+  if (out_sample_rows) *out_sample_rows = c->h_result[1];
+  return c->h_result[0];
 }
 
 sel_status sel_count_batch(sel_table t, const void* const* progs, const size_t* prog_bytes,

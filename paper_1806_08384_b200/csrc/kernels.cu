@@ -244,8 +244,13 @@ __device__ __forceinline__ uint32_t leaf_mask(const void* col, const DevLeaf& L,
   }
   for (int t = 0; t < L.iv_count; ++t) {
     const uint32_t lo = (uint32_t)lo_tab[L.iv_begin + t], sp = (uint32_t)span_tab[L.iv_begin + t];
+    if (sp == 0) {            // an equality (=, IN value): one compare per row
 #pragma unroll
-    for (int i = 0; i < 32; ++i) m |= (v[i] - lo <= sp) ? (1u << i) : 0u;
+      for (int i = 0; i < 32; ++i) m |= (v[i] == lo) ? (1u << i) : 0u;
+    } else {
+#pragma unroll
+      for (int i = 0; i < 32; ++i) m |= (v[i] - lo <= sp) ? (1u << i) : 0u;
+    }
   }
   return m;
 }
@@ -499,14 +504,20 @@ __global__ void __launch_bounds__(kThreads, 4) count_kernel(const __grid_constan
   extern __shared__ __align__(16) char s_dyn[];
   char* wsmem = KEEP ? s_dyn + (size_t)warp * sb.warp_smem : nullptr;
   uint32_t cnt = 0;
-  if (lane == 0 && p.prefetch && gw < nfull) prefetch_chunk(p, gw);
-  for (uint64_t c = gw; c < nfull; c += nw) {
-    if (lane == 0 && p.prefetch && c + nw < nfull) prefetch_chunk(p, c + nw);
+  // Chunks scanned: c = phase + s * stride (stride 1, phase 0: every chunk). A stride > 1 is the
+  // block sample of sel_count_sampled; keeping a selection needs stride 1.
+  const uint64_t stride = p.chunk_stride, phase = p.chunk_phase;
+  const uint64_t ns_full = nfull > phase ? (nfull - phase + stride - 1) / stride : 0;
+  const bool tail_sampled = rem != 0 && nfull >= phase && (nfull - phase) % stride == 0;
+  if (lane == 0 && p.prefetch && gw < ns_full) prefetch_chunk(p, phase + gw * stride);
+  for (uint64_t s = gw; s < ns_full; s += nw) {
+    const uint64_t c = phase + s * stride;
+    if (lane == 0 && p.prefetch && s + nw < ns_full) prefetch_chunk(p, c + nw * stride);
     const uint32_t m = eval_program<false, KEEP>(p, c * kChunkRows, lane, kChunkRows, wsmem);
     cnt += __popc(m);
     keep_chunk<P, KEEP>(sb, c, lane, m, wsmem);
   }
-  if (rem != 0 && gw == nfull % nw) {
+  if (tail_sampled && gw == ns_full % nw) {
     const uint32_t m = eval_program<true, KEEP>(p, nfull * kChunkRows, lane, rem, wsmem);
     cnt += __popc(m);
     keep_chunk<P, KEEP>(sb, nfull, lane, m, wsmem);

@@ -54,6 +54,9 @@ struct DevProgramT {
   uint32_t n_proj;
   uint32_t warp_smem;    // push-down: dynamic shared memory bytes per warp
   uint32_t prefetch;     // 1: L2 bulk-prefetch each warp's next chunk (SEL_PREFETCH=0 disables)
+  uint32_t chunk_stride; // count kernel: scan chunks phase, phase + stride, ... (1: all)
+  uint32_t chunk_phase;
+  uint32_t pad1;
   uint64_t row_offset;   // global id of local row 0 (push-down ids)
   uint64_t capacity;     // push-down capacity in rows
   uint8_t op[MAXOPS];
