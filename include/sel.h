@@ -75,6 +75,7 @@ typedef struct {
 
 typedef struct sel_ctx_s* sel_ctx;
 typedef struct sel_table_s* sel_table;
+typedef struct sel_prepared_s* sel_prepared;
 
 /* ---- contexts ------------------------------------------------------------------------------
  * sel_ctx_create: binds to `cuda_device` (the caller's current device is not changed on return).
@@ -161,6 +162,28 @@ uint64_t sel_execute(sel_table table, const void* prog, size_t prog_bytes,
                      uint64_t* out_local_count, uint64_t* out_global_offset,
                      int* out_materialized, void* cuda_stream);
 
+/* Prepared executes: the same Execute with every argument fixed, validated and canonicalised
+ * once and — on one rank, for a program that scans — its device work (count keeping the
+ * selection, device-side gate, materialisation, result copies) captured into a CUDA graph, so
+ * that a repeated probe (the optimizer re-estimating) costs one graph launch
+ * and one synchronisation. The graph reads the columns' CURRENT contents at every run.
+ * sel_prepare_execute: arguments as sel_execute (host arrays are copied; device buffers must
+ * stay valid while prepared). Errors: as sel_execute's validation (SEL_E_ARG, SEL_E_PROGRAM,
+ * SEL_E_TYPE, SEL_E_STATE), SEL_E_CUDA (capture).
+ * sel_prepared_execute: one Execute on `cuda_stream`, blocking; outputs and return as
+ * sel_execute. A run after the context reallocated its scratch (a probe of a larger table) or
+ * after the bitmap registry changed re-captures first (SEL_E_ARG if a bitmap id the program
+ * uses is no longer registered). SEL_E_STATE if the table was released.
+ * sel_prepared_release: frees the handle (NULL is a no-op); release it before its context. */
+sel_status sel_prepare_execute(sel_table table, const void* prog, size_t prog_bytes,
+                               const uint32_t* proj_cols, uint32_t nproj, uint64_t max_size,
+                               uint32_t* out_rowids, void* const* out_cols,
+                               uint64_t capacity_rows, sel_prepared* out);
+uint64_t sel_prepared_execute(sel_prepared prepared, uint64_t* out_local_count,
+                              uint64_t* out_global_offset, int* out_materialized,
+                              void* cuda_stream);
+void sel_prepared_release(sel_prepared prepared);
+
 /* sel_pushdown: materialise sigma_P pi_proj(R) for the local shard.
  *   out_rowids : device uint32[capacity_rows], receives GLOBAL row ids (global_row_offset + i)
  *                of the selected local rows in ascending order.
@@ -192,10 +215,19 @@ int sel_ctx_last_pushdown_path(sel_ctx ctx);
  * ONE scan — each referenced column is read once per chunk and each distinct leaf (same column and
  * same canonical interval set, across programs) evaluated once. out_counts: host array of nprog,
  * global over ranks (one all-reduce of nprog u64). Limits after canonicalisation: <= 32 distinct
- * leaves, <= 32 columns, <= 1024 intervals, <= 512 postfix ops in total (else SEL_E_ARG).
+ * leaves, <= 32 columns, <= 1024 intervals, <= 512 postfix ops in total, no IN_BITMAP leaves
+ * (else SEL_E_ARG).
  * Errors: as sel_count. Blocks until the counts are on the host. */
 sel_status sel_count_batch(sel_table table, const void* const* progs, const size_t* prog_bytes,
                            uint32_t nprog, uint64_t* out_counts, void* cuda_stream);
+
+/* Bitmaps for IN_BITMAP leaves: `words` is a DEVICE array of
+ * ceil(nbits/64) uint64 (16-byte aligned, caller-owned, alive and unmodified while registered);
+ * bit i (word i/64, bit i%64) = key i is in the set. nbits < 2^31. Ids are small integers, valid
+ * for the context until released. Errors: SEL_E_ARG, SEL_E_ALIGN, SEL_E_TOO_LARGE (too many). */
+sel_status sel_bitmap_register(sel_ctx ctx, const uint64_t* words, uint64_t nbits,
+                               uint32_t* out_id);
+sel_status sel_bitmap_release(sel_ctx ctx, uint32_t id);
 
 /* sel_count_sampled: the exact count over a BLOCK SAMPLE of the table —
  * the 1024-row chunks c with c mod stride == phase (stride >= 1, phase < stride; stride 1 is the
@@ -253,6 +285,10 @@ int sel_abi_version(void);
  *   0x13 LE  push v <= k[a]    0x14 GE push v >= k[a]   (b must be 0)
  *   0x20 BETWEEN               push k[a] <= v && v <= k[b]  (inclusive; empty if k[a] > k[b])
  *   0x30 IN                    push v == k[a] || ... || v == k[a+b-1]   (1 <= b <= 256)
+ *   0x31 IN_BITMAP             push 0 <= v < nbits(a) && bit v of bitmap a is set, where a is an
+ *                              id from sel_bitmap_register (b must be 0; integer columns only) —
+ *                              a dimension-derived key set pushed onto a foreign key (SURVEY §8f
+ *                              NEXT(3); e.g. SSB `s_region = 1` as a set of lo_suppkey values)
  *   0x40 AND, 0x41 OR          pop y, pop x, push x AND/OR y      (col, a, b must be 0)
  *   0x42 NOT                   pop x, push NOT x                  (col, a, b must be 0)
  * Comparisons use the column type's order: signed for INT32/INT64/DATE32, unsigned for DICT*,
@@ -266,12 +302,14 @@ int sel_abi_version(void);
  *   2. For each instruction in order:
  *      a. reserved != 0, unknown op                                          -> SEL_E_PROGRAM
  *      b. TRUE/FALSE/AND/OR/NOT with col, a or b nonzero                      -> SEL_E_PROGRAM
- *      c. comparison/BETWEEN/IN: col >= ncols; EQ..GE with b != 0 or a >= n_consts;
- *         BETWEEN with a or b >= n_consts; IN with b == 0, b > 256 or a + b > n_consts
- *                                                                             -> SEL_E_PROGRAM
+ *      c. comparison/BETWEEN/IN/IN_BITMAP: col >= ncols; EQ..GE with b != 0 or a >= n_consts;
+ *         BETWEEN with a or b >= n_consts; IN with b == 0, b > 256 or a + b > n_consts;
+ *         IN_BITMAP with b != 0                                               -> SEL_E_PROGRAM
  *      d. stack underflow (AND/OR need 2, NOT needs 1), or depth after the instruction > 16
  *                                                                             -> SEL_E_PROGRAM
- *      e. a referenced constant slot not representable in the column's type   -> SEL_E_TYPE
+ *      e. a referenced constant slot not representable in the column's type, or
+ *         IN_BITMAP on a FLOAT32 column                                       -> SEL_E_TYPE
+ *   (whether an IN_BITMAP id is registered is checked by the probe: SEL_E_ARG)
  *   3. stack depth after the last instruction != 1                            -> SEL_E_PROGRAM
  * Maximum program size: 12 + 8 * (128 + 512) = 5,132 bytes.
  */

@@ -56,6 +56,13 @@ def _load():
         L.oracle_pushdown.restype = u64
         L.oracle_pushdown.argtypes = [vp, vp, ctypes.c_uint32, u64, ctypes.c_char_p, sz, vp,
                                       ctypes.c_uint32, u64, vp, vp, u64, ip]
+        L.oracle_count_bm.restype = u64
+        L.oracle_count_bm.argtypes = [vp, vp, ctypes.c_uint32, u64, ctypes.c_char_p, sz, vp, vp,
+                                      ctypes.c_uint32, ip]
+        L.oracle_pushdown_bm.restype = u64
+        L.oracle_pushdown_bm.argtypes = [vp, vp, ctypes.c_uint32, u64, ctypes.c_char_p, sz, vp,
+                                         ctypes.c_uint32, u64, vp, vp, u64, vp, vp,
+                                         ctypes.c_uint32, ip]
         _lib = L
     return _lib
 
@@ -86,12 +93,24 @@ def check(prog: bytes, types: Sequence[int]) -> int:
     return int(_load().oracle_check(prog, len(prog), tys.ctypes.data, len(types)))
 
 
-def count(columns: Sequence, types: Sequence[int], prog: bytes) -> int:
-    """count(T, P): rows of T (numpy columns) satisfying program P."""
+def _bitmaps(bitmaps):
+    """[(uint64 words, nbits), ...] -> ctypes arrays for the IN_BITMAP key sets (id = index)."""
+    bitmaps = list(bitmaps or [])
+    words = [np.ascontiguousarray(w, dtype=np.uint64) for w, _ in bitmaps]
+    wp = (ctypes.c_void_p * max(len(words), 1))(*[w.ctypes.data for w in words])
+    nb = np.asarray([int(nbits) for _, nbits in bitmaps] or [0], dtype=np.uint64)
+    return words, wp, nb, len(bitmaps)
+
+
+def count(columns: Sequence, types: Sequence[int], prog: bytes, bitmaps=None) -> int:
+    """count(T, P): rows of T (numpy columns) satisfying program P; `bitmaps` are the key sets
+    of IN_BITMAP leaves as [(uint64 words, nbits), ...] (id = position)."""
     arrs, ptrs, tys = _marshal(columns, types)
     n = len(arrs[0]) if arrs else 0
     st = ctypes.c_int(0)
-    r = _load().oracle_count(ptrs, tys.ctypes.data, len(arrs), n, prog, len(prog), ctypes.byref(st))
+    keep, wp, nb, k = _bitmaps(bitmaps)
+    r = _load().oracle_count_bm(ptrs, tys.ctypes.data, len(arrs), n, prog, len(prog), wp,
+                                nb.ctypes.data, k, ctypes.byref(st))
     if st.value != 0:
         raise OracleError(st.value)
     return int(r)
@@ -110,7 +129,7 @@ def count_mt(columns: Sequence, types: Sequence[int], prog: bytes, nthreads: int
 
 
 def pushdown(columns: Sequence, types: Sequence[int], prog: bytes, proj: Sequence[int] = (),
-             capacity: int | None = None, row_offset: int = 0):
+             capacity: int | None = None, row_offset: int = 0, bitmaps=None):
     """pushdown(T, P, proj) -> (count, ids[:min(count, capacity)], [projected columns])."""
     arrs, ptrs, tys = _marshal(columns, types)
     n = len(arrs[0]) if arrs else 0
@@ -120,9 +139,11 @@ def pushdown(columns: Sequence, types: Sequence[int], prog: bytes, proj: Sequenc
     optrs = (ctypes.c_void_p * max(len(outs), 1))(*[o.ctypes.data for o in outs])
     pj = np.asarray(list(proj), dtype=np.uint32)
     st = ctypes.c_int(0)
-    r = _load().oracle_pushdown(ptrs, tys.ctypes.data, len(arrs), n, prog, len(prog),
-                                pj.ctypes.data if len(pj) else None, len(pj), row_offset,
-                                ids.ctypes.data, optrs, cap, ctypes.byref(st))
+    keep, wp, nb, k = _bitmaps(bitmaps)
+    r = _load().oracle_pushdown_bm(ptrs, tys.ctypes.data, len(arrs), n, prog, len(prog),
+                                   pj.ctypes.data if len(pj) else None, len(pj), row_offset,
+                                   ids.ctypes.data, optrs, cap, wp, nb.ctypes.data, k,
+                                   ctypes.byref(st))
     if st.value != 0:
         raise OracleError(st.value)
     k = min(int(r), cap)

@@ -32,8 +32,15 @@ enum { O_OK = 0, O_E_ARG = 1, O_E_TYPE = 3, O_E_PROGRAM = 4 };
 enum { T_INT32 = 1, T_INT64 = 2, T_FLOAT32 = 3, T_DATE32 = 4, T_DICT8 = 5, T_DICT16 = 6,
        T_DICT32 = 7 };
 enum { OP_TRUE = 0x01, OP_FALSE = 0x02, OP_EQ = 0x10, OP_LT = 0x11, OP_GT = 0x12, OP_LE = 0x13,
-       OP_GE = 0x14, OP_BETWEEN = 0x20, OP_IN = 0x30, OP_AND = 0x40, OP_OR = 0x41,
-       OP_NOT = 0x42 };
+       OP_GE = 0x14, OP_BETWEEN = 0x20, OP_IN = 0x30, OP_IN_BITMAP = 0x31, OP_AND = 0x40,
+       OP_OR = 0x41, OP_NOT = 0x42 };
+
+/* Key sets of IN_BITMAP leaves: set `id` holds key i iff bit i%64 of words[id][i/64] is set. */
+typedef struct {
+  const uint64_t* const* words;
+  const uint64_t* nbits;
+  uint32_t count;
+} bitmaps_t;
 
 #define MAX_INSTR 128
 #define MAX_CONSTS 512
@@ -102,7 +109,7 @@ int oracle_check_into(const uint8_t* b, size_t len, const int32_t* types, uint32
     switch (op) {
       case OP_TRUE: case OP_FALSE: pops = 0; is_leaf = 0; break;
       case OP_EQ: case OP_LT: case OP_GT: case OP_LE: case OP_GE:
-      case OP_BETWEEN: case OP_IN: pops = 0; is_leaf = 1; break;
+      case OP_BETWEEN: case OP_IN: case OP_IN_BITMAP: pops = 0; is_leaf = 1; break;
       case OP_AND: case OP_OR: pops = 2; is_leaf = 0; break;
       case OP_NOT: pops = 1; is_leaf = 0; break;
       default: return O_E_PROGRAM;
@@ -114,6 +121,8 @@ int oracle_check_into(const uint8_t* b, size_t len, const int32_t* types, uint32
         if (a >= n_consts || bb >= n_consts) return O_E_PROGRAM;
       } else if (op == OP_IN) {
         if (bb == 0 || bb > MAX_IN || a + bb > n_consts) return O_E_PROGRAM;
+      } else if (op == OP_IN_BITMAP) {
+        if (bb != 0) return O_E_PROGRAM;
       } else {
         if (bb != 0 || a >= n_consts) return O_E_PROGRAM;
       }
@@ -128,6 +137,8 @@ int oracle_check_into(const uint8_t* b, size_t len, const int32_t* types, uint32
       } else if (op == OP_IN) {
         for (unsigned j = a; j < a + bb; j++)
           if (!representable(P->k[j], t)) return O_E_TYPE;
+      } else if (op == OP_IN_BITMAP) {
+        if (t == T_FLOAT32) return O_E_TYPE;
       } else {
         if (!representable(P->k[a], t)) return O_E_TYPE;
       }
@@ -211,9 +222,35 @@ static int compare(int op, const void* col, int t, uint64_t i, uint64_t k) {
   return 0;
 }
 
+/* v in key set `id`: 0 <= v < nbits and its bit set; v read in the column's own type. */
+static int in_bitmap(const void* col, int t, uint64_t i, const bitmaps_t* bm, int id) {
+  uint64_t u;
+  switch (t) {
+    case T_INT32:
+    case T_DATE32: {
+      int32_t v = ((const int32_t*)col)[i];
+      if (v < 0) return 0;
+      u = (uint64_t)v;
+      break;
+    }
+    case T_INT64: {
+      int64_t v = ((const int64_t*)col)[i];
+      if (v < 0) return 0;
+      u = (uint64_t)v;
+      break;
+    }
+    case T_DICT8: u = ((const uint8_t*)col)[i]; break;
+    case T_DICT16: u = ((const uint16_t*)col)[i]; break;
+    case T_DICT32: u = ((const uint32_t*)col)[i]; break;
+    default: return 0;
+  }
+  if (u >= bm->nbits[id]) return 0;
+  return (int)((bm->words[id][u / 64] >> (u % 64)) & 1u);
+}
+
 /* P(row i): postfix evaluation on a bool stack (include/sel.h "Opcodes"). */
 static int eval_row(const program_t* P, const void* const* cols, const int32_t* types,
-                    uint64_t i) {
+                    uint64_t i, const bitmaps_t* bm) {
   unsigned char st[MAX_DEPTH];
   int sp = 0;
   for (int n = 0; n < P->n_instr; n++) {
@@ -237,6 +274,9 @@ static int eval_row(const program_t* P, const void* const* cols, const int32_t* 
           if (compare(OP_EQ, cols[in->col], types[in->col], i, P->k[j])) r = 1;
         st[sp++] = (unsigned char)r;
         break;
+      case OP_IN_BITMAP:
+        st[sp++] = (unsigned char)in_bitmap(cols[in->col], types[in->col], i, bm, in->a);
+        break;
       case OP_AND: sp--; st[sp - 1] = (unsigned char)(st[sp - 1] && st[sp]); break;
       case OP_OR: sp--; st[sp - 1] = (unsigned char)(st[sp - 1] || st[sp]); break;
       case OP_NOT: st[sp - 1] = (unsigned char)!st[sp - 1]; break;
@@ -246,28 +286,41 @@ static int eval_row(const program_t* P, const void* const* cols, const int32_t* 
 }
 
 static int prepare(const void* const* cols, const int32_t* types, uint32_t ncols, uint64_t n,
-                   const uint8_t* prog, size_t len, program_t* P) {
+                   const uint8_t* prog, size_t len, program_t* P, const bitmaps_t* bm) {
   if (ncols == 0 || (n > 0 && cols == NULL)) return O_E_ARG;
   for (uint32_t c = 0; c < ncols; c++) {
     if (!known_type(types[c])) return O_E_TYPE;
     if (n > 0 && cols[c] == NULL) return O_E_ARG;
   }
-  return oracle_check_into(prog, len, types, ncols, P);
+  int s = oracle_check_into(prog, len, types, ncols, P);
+  if (s != O_OK) return s;
+  for (int i = 0; i < P->n_instr; i++)   /* an IN_BITMAP id must name a given bitmap */
+    if (P->ins[i].op == OP_IN_BITMAP && (uint32_t)P->ins[i].a >= bm->count) return O_E_ARG;
+  return O_OK;
 }
 
+
 /* count(T, P) over rows [0, n). *status receives the validation status; returns UINT64_MAX
- * on error. */
-uint64_t oracle_count(const void* const* cols, const int32_t* types, uint32_t ncols, uint64_t n,
-                      const uint8_t* prog, size_t len, int* status) {
+ * on error. bm_*: the IN_BITMAP key sets (may be NULL/0). */
+uint64_t oracle_count_bm(const void* const* cols, const int32_t* types, uint32_t ncols,
+                         uint64_t n, const uint8_t* prog, size_t len,
+                         const uint64_t* const* bm_words, const uint64_t* bm_nbits,
+                         uint32_t nbm, int* status) {
+  const bitmaps_t bm = {bm_words, bm_nbits, nbm};
   program_t* P = (program_t*)malloc(sizeof(program_t));
-  int s = prepare(cols, types, ncols, n, prog, len, P);
+  int s = prepare(cols, types, ncols, n, prog, len, P, &bm);
   if (status) *status = s;
   if (s != O_OK) { free(P); return UINT64_MAX; }
   uint64_t count = 0;
   for (uint64_t i = 0; i < n; i++)
-    if (eval_row(P, cols, types, i)) count++;
+    if (eval_row(P, cols, types, i, &bm)) count++;
   free(P);
   return count;
+}
+
+uint64_t oracle_count(const void* const* cols, const int32_t* types, uint32_t ncols, uint64_t n,
+                      const uint8_t* prog, size_t len, int* status) {
+  return oracle_count_bm(cols, types, ncols, n, prog, len, NULL, NULL, 0, status);
 }
 
 static size_t width_of(int t) {
@@ -280,19 +333,22 @@ static size_t width_of(int t) {
 }
 
 /* pushdown(T, P, proj): ascending ids (+ row_offset), gathered projected columns, gate. */
-uint64_t oracle_pushdown(const void* const* cols, const int32_t* types, uint32_t ncols,
-                         uint64_t n, const uint8_t* prog, size_t len, const uint32_t* proj,
-                         uint32_t nproj, uint64_t row_offset, uint32_t* out_ids,
-                         void* const* out_cols, uint64_t capacity, int* status) {
+uint64_t oracle_pushdown_bm(const void* const* cols, const int32_t* types, uint32_t ncols,
+                            uint64_t n, const uint8_t* prog, size_t len, const uint32_t* proj,
+                            uint32_t nproj, uint64_t row_offset, uint32_t* out_ids,
+                            void* const* out_cols, uint64_t capacity,
+                            const uint64_t* const* bm_words, const uint64_t* bm_nbits,
+                            uint32_t nbm, int* status) {
+  const bitmaps_t bm = {bm_words, bm_nbits, nbm};
   program_t* P = (program_t*)malloc(sizeof(program_t));
-  int s = prepare(cols, types, ncols, n, prog, len, P);
+  int s = prepare(cols, types, ncols, n, prog, len, P, &bm);
   for (uint32_t j = 0; s == O_OK && j < nproj; j++)
     if (proj[j] >= ncols) s = O_E_ARG;
   if (status) *status = s;
   if (s != O_OK) { free(P); return UINT64_MAX; }
   uint64_t count = 0;
   for (uint64_t i = 0; i < n; i++) {
-    if (!eval_row(P, cols, types, i)) continue;
+    if (!eval_row(P, cols, types, i, &bm)) continue;
     if (count < capacity) {
       out_ids[count] = (uint32_t)(row_offset + i);
       for (uint32_t j = 0; j < nproj; j++) {
@@ -304,6 +360,14 @@ uint64_t oracle_pushdown(const void* const* cols, const int32_t* types, uint32_t
   }
   free(P);
   return count;
+}
+
+uint64_t oracle_pushdown(const void* const* cols, const int32_t* types, uint32_t ncols,
+                         uint64_t n, const uint8_t* prog, size_t len, const uint32_t* proj,
+                         uint32_t nproj, uint64_t row_offset, uint32_t* out_ids,
+                         void* const* out_cols, uint64_t capacity, int* status) {
+  return oracle_pushdown_bm(cols, types, ncols, n, prog, len, proj, nproj, row_offset, out_ids,
+                            out_cols, capacity, NULL, NULL, 0, status);
 }
 
 /* Row-sharded count over `nthreads` POSIX threads (contiguous shards, summed) — used only to

@@ -23,6 +23,8 @@ EXPORTS = ["sel_ctx_create", "sel_ctx_set_comm", "sel_nccl_unique_id", "sel_ctx_
            "sel_ctx_set_timing", "sel_ctx_last_kernel_ms", "sel_table_register",
            "sel_table_release", "sel_count", "sel_count_ex", "sel_execute", "sel_pushdown",
            "sel_ctx_last_times", "sel_count_batch", "sel_count_sampled",
+           "sel_bitmap_register", "sel_bitmap_release",
+           "sel_prepare_execute", "sel_prepared_execute", "sel_prepared_release",
            "sel_ctx_last_pushdown_path", "sel_program_check",
            "sel_program_path", "sel_program_plan_json", "sel_last_error",
            "sel_last_error_message", "sel_abi_version"]
@@ -67,6 +69,13 @@ def lib() -> ctypes.CDLL:
                               ctypes.POINTER(u64), ctypes.POINTER(u64), ctypes.POINTER(i32), vp]),
         "sel_count_sampled": (u64, [vp, ctypes.c_char_p, sz, u32, u32, ctypes.POINTER(u64), vp]),
         "sel_count_batch": (i32, [vp, vp, vp, u32, ctypes.POINTER(u64), vp]),
+        "sel_bitmap_register": (i32, [vp, vp, u64, ctypes.POINTER(u32)]),
+        "sel_bitmap_release": (i32, [vp, u32]),
+        "sel_prepare_execute": (i32, [vp, ctypes.c_char_p, sz, vp, u32, u64, vp, vp, u64,
+                                      ctypes.POINTER(vp)]),
+        "sel_prepared_execute": (u64, [vp, ctypes.POINTER(u64), ctypes.POINTER(u64),
+                                       ctypes.POINTER(i32), vp]),
+        "sel_prepared_release": (None, [vp]),
         "sel_ctx_last_times": (i32, [vp, ctypes.POINTER(ctypes.c_float), ctypes.POINTER(ctypes.c_float)]),
         "sel_ctx_last_pushdown_path": (i32, [vp]),
         "sel_pushdown": (u64, [vp, ctypes.c_char_p, sz, vp, u32, vp, vp, u64,

@@ -67,6 +67,25 @@ class Context:
         """1: the last pushdown materialised from a kept selection; 0: single pass; -1: none."""
         return int(lib().sel_ctx_last_pushdown_path(self._h))
 
+    def register_bitmap(self, words: torch.Tensor, nbits: int) -> int:
+        """Register a key set for IN_BITMAP leaves (selgen.InSet): `words` is a device tensor of
+        ceil(nbits/64) 64-bit words (bit i = key i), kept alive by this context until
+        release_bitmap. Returns the id programs refer to."""
+        if not words.is_cuda or words.element_size() != 8 or not words.is_contiguous():
+            raise ValueError("bitmap words must be a contiguous 64-bit CUDA tensor")
+        if words.numel() * 64 < nbits:
+            raise ValueError("bitmap shorter than nbits")
+        out = ctypes.c_uint32(0)
+        check(lib().sel_bitmap_register(self._h, ctypes.c_void_p(words.data_ptr()), int(nbits),
+                                        ctypes.byref(out)))
+        self._bitmaps = getattr(self, "_bitmaps", {})
+        self._bitmaps[out.value] = words
+        return int(out.value)
+
+    def release_bitmap(self, bitmap_id: int) -> None:
+        check(lib().sel_bitmap_release(self._h, int(bitmap_id)))
+        getattr(self, "_bitmaps", {}).pop(int(bitmap_id), None)
+
     def last_kernel_ms(self) -> float:
         ms = ctypes.c_float(0.0)
         check(lib().sel_ctx_last_kernel_ms(self._h, ctypes.byref(ms)))
@@ -101,6 +120,71 @@ class PushdownResult:
 @dataclass
 class ExecuteResult(PushdownResult):
     materialized: bool = True     # False: count > max_size, Algorithm 1's "throw" (revert)
+
+
+class PreparedExecute:
+    """A prepared Algorithm 1 Execute (Table.prepare_execute). run() returns the global count;
+    .materialized / .local_count describe the last run and .result() views its output."""
+
+    def __init__(self, table, pred, project, max_size, capacity, stream, out):
+        self.table = table
+        prog = table.program(pred)
+        proj = table._col_indices(project)
+        if max_size is None:
+            max_size = (1 << 64) - 2
+        if capacity is None:
+            capacity = min(int(max_size), table.local_rows)
+        dev = table.ctx.device
+        if out is None:
+            rowids = torch.empty(max(capacity, 1), dtype=torch.int32, device=dev)
+            outs = [torch.empty(max(capacity, 1), dtype=_OUT_DTYPE[table.types[j]], device=dev) for j in proj]
+        else:
+            rowids, outs = out
+        self.rowids, self.outs, self.capacity = rowids, list(outs), int(capacity)
+        self._keys = [table.names[j] if isinstance(p, str) else j for p, j in zip(project, proj)]
+        ptrs = (ctypes.c_void_p * max(len(outs), 1))(*[o.data_ptr() for o in outs])
+        pj = (ctypes.c_uint32 * max(len(proj), 1))(*proj)
+        h = ctypes.c_void_p()
+        check(lib().sel_prepare_execute(table._h, prog, len(prog), pj, len(proj), int(max_size),
+                                        rowids.data_ptr(), ptrs, int(capacity), ctypes.byref(h)))
+        self._h = h
+        self._local, self._off, self._mat = ctypes.c_uint64(0), ctypes.c_uint64(0), ctypes.c_int(0)
+        self._refs = (ctypes.byref(self._local), ctypes.byref(self._off), ctypes.byref(self._mat))
+        self._stream = _stream_ptr(stream, dev)
+        self._fn = lib().sel_prepared_execute
+        self.count = 0
+
+    def run(self, stream=None) -> int:
+        r = self._fn(self._h, *self._refs, self._stream if stream is None else _stream_ptr(stream, self.table.ctx.device))
+        if r == SEL_ERR:
+            raise last_error()
+        self.count = r
+        return r
+
+    @property
+    def materialized(self) -> bool:
+        return bool(self._mat.value)
+
+    @property
+    def local_count(self) -> int:
+        return int(self._local.value)
+
+    def result(self) -> "ExecuteResult":
+        k = min(self.local_count, self.capacity)
+        cols = {key: o[:k] for key, o in zip(self._keys, self.outs)}
+        return ExecuteResult(self.rowids[:k], cols, int(self.count), self.local_count,
+                             int(self._off.value), self.materialized)
+
+    def release(self) -> None:
+        if getattr(self, "_h", None):
+            lib().sel_prepared_release(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.release()
+        except Exception:
+            pass
 
 
 class Table:
@@ -231,6 +315,12 @@ class Table:
         k = min(int(local.value), capacity)
         cols = {self.names[j] if isinstance(p, str) else j: o[:k] for p, j, o in zip(project, proj, outs)}
         return ExecuteResult(rowids[:k], cols, int(r), int(local.value), int(off.value), bool(mat.value))
+
+    def prepare_execute(self, pred, project: Sequence[str | int] = (), max_size: int | None = None,
+                        capacity: int | None = None, stream=None, out=None) -> "PreparedExecute":
+        """execute() with every argument fixed: validated once and captured into a CUDA graph
+        (include/sel.h sel_prepare_execute); each .run() is one graph launch + one sync."""
+        return PreparedExecute(self, pred, project, max_size, capacity, stream, out)
 
     def pushdown(self, pred, project: Sequence[str | int] = (), capacity: int | None = None,
                  stream=None, out=None) -> PushdownResult:

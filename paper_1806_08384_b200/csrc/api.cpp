@@ -121,13 +121,14 @@ struct sel_ctx_s {
   int num_sms = 148;
   int occ_count_small = 1, occ_count_large = 1;
   Scratch s{};
-  uint64_t* h_result = nullptr;   // pinned: [0] local count, [1..nranks] gathered counts
+  uint64_t* h_result = nullptr;   // pinned mirror of Scratch::result (kResultSlots)
   uint64_t ticket_base = 0;
   uint32_t epoch = 0;
   ncclComm_t comm = nullptr;
   int nranks = 1, rank = 0;
   bool timing = false;
-  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;   // count kernel
+  cudaEvent_t ev2 = nullptr, ev3 = nullptr;   // push-down kernels (sel_execute times both)
   float last_ms = 0.f;
   int live_tables = 0;
   bool destroyed = false;
@@ -144,6 +145,14 @@ struct sel_ctx_s {
   int prefetch_mode = -1;   // -1 auto, 0 off, 1 on
   bool keep_values = true;
   float last_count_ms = 0.f, last_push_ms = 0.f;
+  // IN_BITMAP key sets (sel_bitmap_register): id -> device words / nbits; words null = free id
+  std::vector<const uint64_t*> bm_words;
+  std::vector<uint64_t> bm_nbits;
+  // generations: bumped when device buffers are reallocated / the bitmap registry changes, so
+  // that prepared executes (captured CUDA graphs) re-capture instead of using stale pointers
+  uint64_t alloc_gen = 0, bm_gen = 0;
+  cudaStream_t cap_stream = nullptr;  // stream-capture source for prepared executes
+  bool capturing = false;             // timing events become graph event-record nodes
 };
 
 struct sel_table_s {
@@ -151,12 +160,29 @@ struct sel_table_s {
   std::vector<sel_column> cols;
   std::vector<int> types;
   uint64_t local_rows, row_offset, global_rows;
+  std::vector<sel_prepared> prepared;  // orphaned (table = nullptr) when the table is released
+};
+
+struct sel_prepared_s {
+  sel_table t = nullptr;
+  std::string prog;
+  std::vector<uint32_t> proj;
+  std::vector<void*> out_cols;
+  uint32_t* out_rowids = nullptr;
+  uint64_t max_size = 0, capacity = 0;
+  bool graph = false;                 // false: each run is a plain sel_execute
+  cudaGraphExec_t exec = nullptr;
+  uint64_t alloc_gen = ~0ull, bm_gen = ~0ull;
+  bool timing = false;
+  ncclComm_t comm = nullptr;
+  std::vector<int> kept_cols;         // the kept selection a run leaves in the context
+  SelectionBufs sel{};
 };
 
 namespace {
 
 constexpr int kMaxGrid = 148 * 32;
-constexpr int kMaxRanks = 1024;
+constexpr size_t kMaxBitmaps = 65536;  // ids fit the instruction's u16 `a`
 
 template <class P>
 bool fits_block(const Plan& plan, size_t nslots, uint32_t nproj) {
@@ -193,6 +219,14 @@ void pack(const Plan& plan, const sel_table_s* t, P* p) {
     d.wclass = wclass_of(type);
     d.fkey = type == SEL_FLOAT32 ? 1 : 0;
     d.iv_begin = (uint16_t)iv;
+    if (L.bitmap >= 0) {  // IN_BITMAP: one table entry = (words pointer, nbits)
+      d.iv_count = 1;
+      d.pad = (uint16_t)(kLeafBitmap | (L.negate ? kLeafNegate : 0));
+      p->lo[iv] = (uint64_t)(uintptr_t)t->ctx->bm_words[L.bitmap];
+      p->span[iv] = t->ctx->bm_nbits[L.bitmap];
+      ++iv;
+      continue;
+    }
     d.iv_count = (uint16_t)L.iv.size();
     const uint64_t bias = key_sign_bias(type);
     for (const Interval& x : L.iv) {
@@ -215,6 +249,10 @@ sel_status plan_for(sel_table t, const void* prog, size_t bytes, Plan* plan) {
   std::string msg;
   const int st = decode_program(prog, bytes, t->types.data(), (uint32_t)t->types.size(), &P, &msg);
   if (st != SEL_OK) return set_error((sel_status)st, msg);
+  const sel_ctx c = t->ctx;
+  for (const Instr& in : P.ins)
+    if (in.op == 0x31 && (in.a >= c->bm_words.size() || c->bm_words[in.a] == nullptr))
+      return set_error(SEL_E_ARG, "IN_BITMAP id " + std::to_string(in.a) + " is not registered");
   plan_program(P, t->types.data(), plan);
   if (plan->max_depth > kMaxDeviceStack)
     return set_error(SEL_E_PROGRAM, "program too deep after canonicalisation");
@@ -252,6 +290,7 @@ sel_status ensure_selection(sel_ctx c, uint64_t nchunks) {
   c->sel = SelectionBufs{};
   c->sel_cap_chunks = 0;
   c->kept_table = nullptr;
+  ++c->alloc_gen;
   const uint64_t cap = std::max<uint64_t>(nchunks, 1024);
   const uint64_t nsb = (cap + kSbChunks - 1) / kSbChunks;
   c->kept_cols.clear();
@@ -266,6 +305,7 @@ sel_status ensure_selection(sel_ctx c, uint64_t nchunks) {
 
 sel_status ensure_slot(sel_ctx c, int k, uint64_t bytes) {
   if (c->slot_cap[k] >= bytes) return SEL_OK;
+  ++c->alloc_gen;
   if (c->slot_buf[k]) cudaFree(c->slot_buf[k]);
   c->slot_buf[k] = nullptr;
   c->slot_cap[k] = 0;
@@ -319,13 +359,15 @@ sel_status sel_ctx_create(int cuda_device, sel_ctx* out) {
   }
   bool okay = cudaMalloc(&c->s.partials, kMaxGrid * sizeof(uint64_t)) == cudaSuccess &&
               cudaMalloc(&c->s.done, sizeof(unsigned int)) == cudaSuccess &&
-              cudaMalloc(&c->s.result, (1 + kMaxRanks) * sizeof(uint64_t)) == cudaSuccess &&
+              cudaMalloc(&c->s.result, kResultSlots * sizeof(uint64_t)) == cudaSuccess &&
               cudaMalloc(&c->s.ticket, sizeof(unsigned long long)) == cudaSuccess &&
-              cudaMallocHost(&c->h_result, (1 + kMaxRanks) * sizeof(uint64_t)) == cudaSuccess &&
+              cudaMallocHost(&c->h_result, kResultSlots * sizeof(uint64_t)) == cudaSuccess &&
               cudaMemset(c->s.done, 0, sizeof(unsigned int)) == cudaSuccess &&
               cudaMemset(c->s.ticket, 0, sizeof(unsigned long long)) == cudaSuccess &&
-              cudaMemset(c->s.result, 0, (1 + kMaxRanks) * sizeof(uint64_t)) == cudaSuccess &&
+              cudaMemset(c->s.result, 0, kResultSlots * sizeof(uint64_t)) == cudaSuccess &&
               cudaEventCreate(&c->ev0) == cudaSuccess && cudaEventCreate(&c->ev1) == cudaSuccess &&
+              cudaEventCreate(&c->ev2) == cudaSuccess && cudaEventCreate(&c->ev3) == cudaSuccess &&
+              cudaStreamCreateWithFlags(&c->cap_stream, cudaStreamNonBlocking) == cudaSuccess &&
               cudaDeviceSynchronize() == cudaSuccess;
   if (!okay) {
     cudaError_t le = cudaGetLastError();
@@ -392,9 +434,13 @@ void release_ctx_resources(sel_ctx c) {
   }
   if (c->ev0) cudaEventDestroy(c->ev0);
   if (c->ev1) cudaEventDestroy(c->ev1);
+  if (c->ev2) cudaEventDestroy(c->ev2);
+  if (c->ev3) cudaEventDestroy(c->ev3);
+  if (c->cap_stream) cudaStreamDestroy(c->cap_stream);
+  c->cap_stream = nullptr;
   c->s = Scratch{};
   c->h_result = nullptr;
-  c->ev0 = c->ev1 = nullptr;
+  c->ev0 = c->ev1 = c->ev2 = c->ev3 = nullptr;
 }
 }  // namespace
 
@@ -459,6 +505,7 @@ void sel_table_release(sel_table t) {
   if (!t) return;
   sel_ctx c = t->ctx;
   if (c->kept_table == t) c->kept_table = nullptr;
+  for (sel_prepared q : t->prepared) q->t = nullptr;
   delete t;
   if (--c->live_tables == 0 && c->destroyed) delete c;
 }
@@ -513,6 +560,12 @@ long sel_program_plan_json(const void* prog, size_t prog_bytes, const sel_type* 
       lo += (i ? ", " : "") + std::to_string(L.iv[i].lo ^ bias);
       sp += (i ? ", " : "") + std::to_string(L.iv[i].hi - L.iv[i].lo);
     }
+    if (L.bitmap >= 0) {
+      js += (l ? ", " : "") + std::string("{\"col\": ") + std::to_string(L.col) +
+            ", \"wclass\": " + std::to_string(wclass_of(type)) + ", \"bitmap\": " +
+            std::to_string(L.bitmap) + ", \"negate\": " + (L.negate ? "true" : "false") + "}";
+      continue;
+    }
     js += (l ? ", " : "") + std::string("{\"col\": ") + std::to_string(L.col) +
           ", \"wclass\": " + std::to_string(wclass_of(type)) +
           ", \"fkey\": " + (type == SEL_FLOAT32 ? "1" : "0") + ", \"lo\": [" + lo +
@@ -525,6 +578,40 @@ long sel_program_plan_json(const void* prog, size_t prog_bytes, const sel_type* 
     buf[n] = '\0';
   }
   return (long)js.size();
+}
+
+sel_status sel_bitmap_register(sel_ctx c, const uint64_t* words, uint64_t nbits, uint32_t* out_id) {
+  clear_error();
+  if (!c || !words || !out_id) return set_error(SEL_E_ARG, "null argument");
+  if (c->destroyed) return set_error(SEL_E_STATE, "context destroyed");
+  if (nbits == 0 || nbits >= (1ull << 31)) return set_error(SEL_E_ARG, "nbits must be 1..2^31-1");
+  if (reinterpret_cast<uintptr_t>(words) % 16 != 0)
+    return set_error(SEL_E_ALIGN, "bitmap words must be 16-byte aligned");
+  size_t id = 0;
+  while (id < c->bm_words.size() && c->bm_words[id] != nullptr) ++id;
+  if (id >= kMaxBitmaps) return set_error(SEL_E_TOO_LARGE, "too many registered bitmaps");
+  if (id == c->bm_words.size()) {
+    c->bm_words.push_back(nullptr);
+    c->bm_nbits.push_back(0);
+  }
+  c->bm_words[id] = words;
+  c->bm_nbits[id] = nbits;
+  c->kept_table = nullptr;  // a kept selection may have used a previous set under this id
+  ++c->bm_gen;
+  *out_id = (uint32_t)id;
+  return SEL_OK;
+}
+
+sel_status sel_bitmap_release(sel_ctx c, uint32_t id) {
+  clear_error();
+  if (!c) return set_error(SEL_E_ARG, "null ctx");
+  if (id >= c->bm_words.size() || c->bm_words[id] == nullptr)
+    return set_error(SEL_E_ARG, "bitmap id not registered");
+  c->bm_words[id] = nullptr;
+  c->bm_nbits[id] = 0;
+  c->kept_table = nullptr;
+  ++c->bm_gen;
+  return SEL_OK;
 }
 
 uint64_t sel_count(sel_table t, const void* prog, size_t prog_bytes, void* cuda_stream) {
@@ -540,6 +627,199 @@ sel_status sel_ctx_last_times(sel_ctx ctx, float* count_ms, float* pushdown_ms) 
 }
 
 int sel_ctx_last_pushdown_path(sel_ctx ctx) { return ctx ? ctx->last_pd_path : -1; }
+
+}  // extern "C"
+
+namespace {
+
+// Timing event on `s`; inside a stream capture it must be an external event-record node (a plain
+// record would only express a dependency within the capture).
+void record(sel_ctx c, cudaEvent_t ev, cudaStream_t s) {
+  if (c->capturing) cudaEventRecordWithFlags(ev, s, cudaEventRecordExternal);
+  else cudaEventRecord(ev, s);
+}
+
+// The projected predicate columns whose selected values a keeping count stores (<= kMaxKeep,
+// within the warp's capture budget) with their shared-memory capture offsets; *off advances.
+std::vector<std::pair<int, uint32_t>> choose_kept(sel_table t, const Plan& plan,
+                                                  const uint32_t* keep_cols, uint32_t nkeep,
+                                                  uint32_t* off) {
+  std::vector<std::pair<int, uint32_t>> chosen;
+  for (uint32_t j = 0; j < nkeep && (int)chosen.size() < kMaxKeep; ++j) {
+    const int col = (int)keep_cols[j];
+    bool pred_col = false, dup = false;
+    for (auto& L : plan.leaves) pred_col = pred_col || L.col == col;
+    for (auto& ck : chosen) dup = dup || ck.first == col;
+    const uint32_t w = (uint32_t)width_of(t->types[col]);
+    if (!pred_col || dup || *off + w * kChunkRows > kIdxBytes + kCaptureBudget) continue;
+    chosen.emplace_back(col, *off);
+    *off += w * kChunkRows;
+  }
+  return chosen;
+}
+
+// Device memory a keeping count of t needs (selection + kept-value slots); allocates only when
+// the context's buffers are too small (bumping alloc_gen, which invalidates captured graphs).
+sel_status reserve_selection(sel_table t, uint64_t nchunks,
+                             const std::vector<std::pair<int, uint32_t>>& chosen) {
+  sel_ctx c = t->ctx;
+  if (ensure_selection(c, nchunks) != SEL_OK) return g_status;
+  for (size_t k = 0; k < chosen.size(); ++k) {
+    const uint64_t w = (uint64_t)width_of(t->types[chosen[k].first]);
+    if (ensure_slot(c, (int)k, nchunks * (uint64_t)kChunkRows * w) != SEL_OK) return g_status;
+  }
+  return SEL_OK;
+}
+
+// Enqueue the count of `plan` over t's shard on `stream`: the count kernel
+// (keeping the selection with SEL_KEEP_SELECTION) writes the local count to *d_out, then the
+// 8-byte all-reduce makes it global in place. Nothing waits for the host.
+sel_status enqueue_count(sel_table t, const Plan& plan, uint32_t flags, const uint32_t* keep_cols,
+                         uint32_t nkeep, cudaStream_t stream, uint64_t* d_out) {
+  sel_ctx c = t->ctx;
+  const uint64_t n = t->local_rows;
+  const bool scan = n > 0 && plan.path != PATH_CONST;
+  cudaError_t e;
+  if (scan) {
+    const uint64_t nchunks = (n + kChunkRows - 1) / kChunkRows;
+    const uint64_t units = (nchunks + kWarpsPerCta - 1) / kWarpsPerCta;
+    const size_t nslots = count_slots(plan);
+    const SelectionBufs* keep = nullptr;
+    std::vector<int> cap_off(t->cols.size(), -1);
+    if (flags & SEL_KEEP_SELECTION) {
+      if (ensure_selection(c, nchunks) != SEL_OK) return g_status;
+      const uint64_t nsb = (nchunks + kSbChunks - 1) / kSbChunks;
+      e = cudaMemsetAsync(c->sel.sb_sum, 0, nsb * sizeof(uint32_t), stream);
+      if (e != cudaSuccess) return set_error(SEL_E_CUDA, cuda_msg("cudaMemsetAsync(selection)", e));
+      c->kept_table = nullptr;  // valid again only once this probe has completed
+      c->kept_cols.clear();
+      // projected predicate columns: capture while evaluating, keep the selected values
+      uint32_t off = kIdxBytes;
+      const auto chosen = choose_kept(t, plan, keep_cols, nkeep, &off);
+      if (reserve_selection(t, nchunks, chosen) != SEL_OK) return g_status;
+      for (const auto& ck : chosen) {
+        const int col = ck.first, k = (int)c->kept_cols.size();
+        cap_off[col] = (int)ck.second;
+        c->sel.keep_col[k] = (uint8_t)col;
+        c->sel.keep_wclass[k] = wclass_of(t->types[col]);
+        c->sel.keep_cap_off[k] = (uint16_t)ck.second;
+        c->sel.keep_slot[k] = c->slot_buf[k];
+        c->kept_cols.push_back(col);
+      }
+      c->sel.n_keep = (uint32_t)c->kept_cols.size();
+      c->sel.warp_smem = c->sel.n_keep ? ((off + 15u) & ~15u) : 0u;
+      keep = &c->sel;
+    }
+    auto mark_captures = [&](auto* p) {
+      std::vector<bool> marked(t->cols.size(), false);
+      for (size_t i = 0; i < plan.op.size(); ++i) {
+        if (plan.op[i] != DOP_LEAF) continue;
+        const int l = plan.arg[i];
+        const int col = plan.leaves[l].col;
+        if (cap_off[col] >= 0 && !marked[col]) {
+          p->leaf[l].cap = 1;
+          p->leaf[l].cap_off = (uint16_t)cap_off[col];
+          marked[col] = true;
+        }
+      }
+    };
+    const size_t dyn = keep ? (size_t)keep->warp_smem * kWarpsPerCta : 0;
+    Scratch s = c->s;
+    s.result = d_out;
+    if (c->timing) record(c, c->ev0, stream);
+    int le;
+    if (fits_block<DevProgramSmall>(plan, nslots, 0)) {
+      DevProgramSmall p;
+      pack(plan, t, &p);
+      mark_captures(&p);
+      if (c->prefetch_mode < 0) p.prefetch = (keep && keep->n_keep) ? 1u : 0u;
+      const int occ = keep ? occupancy_count_keep_small(dyn) : c->occ_count_small;
+      le = launch_count_small(p, n, grid_for(c, units, occ), s, keep, stream);
+    } else {
+      static thread_local DevProgramLarge p;
+      pack(plan, t, &p);
+      mark_captures(&p);
+      if (c->prefetch_mode < 0) p.prefetch = (keep && keep->n_keep) ? 1u : 0u;
+      const int occ = keep ? occupancy_count_keep_large(dyn) : c->occ_count_large;
+      le = launch_count_large(p, n, grid_for(c, units, occ), s, keep, stream);
+    }
+    if (le != cudaSuccess) return set_error(SEL_E_CUDA, cuda_msg("count kernel launch", (cudaError_t)le));
+    if (c->timing) record(c, c->ev1, stream);
+  } else {
+    uint64_t* h = c->h_result + (d_out - c->s.result);
+    *h = plan.path == PATH_CONST && plan.const_value ? n : 0;
+    e = cudaMemcpyAsync(d_out, h, sizeof(uint64_t), cudaMemcpyHostToDevice, stream);
+    if (e != cudaSuccess) return set_error(SEL_E_CUDA, cuda_msg("cudaMemcpyAsync", e));
+  }
+  if (c->comm) {  // SURVEY §8a a4: one 8-byte all-reduce on the probe stream
+    ncclResult_t r = nccl().AllReduce(d_out, d_out, 1, ncclUint64, ncclSum, c->comm, stream);
+    if (r != ncclSuccess) return set_error(SEL_E_NCCL, nccl_msg("ncclAllReduce", r));
+  }
+  return SEL_OK;
+}
+
+// Enqueue the materialisation from the kept selection (pushdown_sel): every
+// projection gathered from global memory or copied from its kept-value slot. gate: write nothing
+// when the global count in Scratch::result[kGateSlot] exceeds gate_max (sel_execute).
+sel_status enqueue_pushdown_sel(sel_table t, const uint32_t* proj_cols, uint32_t nproj,
+                                uint32_t* out_rowids, void* const* out_cols, uint64_t capacity_rows,
+                                bool gate, uint64_t gate_max, cudaStream_t stream) {
+  sel_ctx c = t->ctx;
+  const uint64_t n = t->local_rows;
+  const uint64_t ntiles = (n + kChunkRows - 1) / kChunkRows;
+  auto fill_sel = [&](auto* p) {
+    std::memset(p, 0, sizeof(*p));
+    p->row_offset = t->row_offset;
+    p->capacity = capacity_rows;
+    p->gate = gate ? 1u : 0u;
+    p->gate_max = gate_max;
+    p->n_proj = capacity_rows > 0 ? nproj : 0;
+    for (uint32_t j = 0; j < p->n_proj; ++j) {
+      p->proj_src[j] = t->cols[proj_cols[j]].data;
+      p->proj_dst[j] = out_cols[j];
+      p->proj_wclass[j] = wclass_of(t->types[proj_cols[j]]);
+      p->proj_cap_off[j] = kNoCapture;
+      for (size_t k = 0; k < c->kept_cols.size(); ++k)
+        if (c->kept_cols[k] == (int)proj_cols[j]) p->proj_cap_off[j] = (uint16_t)(kKeptBase + k);
+    }
+  };
+  const uint64_t nblocks = (ntiles + kSelBlockChunks - 1) / kSelBlockChunks;
+  const uint64_t units = (nblocks + kWarpsPerCta - 1) / kWarpsPerCta;
+  int le;
+  if (nproj <= (uint32_t)DevProgramSmall::kMaxProj) {
+    DevProgramSmall p;
+    fill_sel(&p);
+    le = launch_pushdown_sel_small(p, n, out_rowids, grid_for(c, units, occupancy_pushdown_sel_small()),
+                                   c->s, c->sel, stream);
+  } else {
+    static thread_local DevProgramLarge p;
+    fill_sel(&p);
+    le = launch_pushdown_sel_large(p, n, out_rowids, grid_for(c, units, occupancy_pushdown_sel_large()),
+                                   c->s, c->sel, stream);
+  }
+  if (le != cudaSuccess) return set_error(SEL_E_CUDA, cuda_msg("push-down kernel launch", (cudaError_t)le));
+  c->last_pd_path = 1;
+  return SEL_OK;
+}
+
+sel_status check_projection(sel_table t, const uint32_t* proj_cols, uint32_t nproj,
+                            uint32_t* out_rowids, void* const* out_cols, uint64_t capacity_rows) {
+  if (nproj > 0 && !proj_cols) return set_error(SEL_E_ARG, "null proj_cols");
+  if (nproj > 255) return set_error(SEL_E_ARG, "nproj must be <= 255");
+  for (uint32_t j = 0; j < nproj; ++j)
+    if (proj_cols[j] >= t->cols.size()) return set_error(SEL_E_ARG, "projection index out of range");
+  if (capacity_rows > 0) {
+    if (!out_rowids) return set_error(SEL_E_ARG, "null out_rowids with capacity > 0");
+    if (nproj > 0 && !out_cols) return set_error(SEL_E_ARG, "null out_cols with capacity > 0");
+    for (uint32_t j = 0; j < nproj; ++j)
+      if (!out_cols[j]) return set_error(SEL_E_ARG, "null out_cols entry with capacity > 0");
+  }
+  return SEL_OK;
+}
+
+}  // namespace
+
+extern "C" {
 
 uint64_t sel_count_ex(sel_table t, const void* prog, size_t prog_bytes, uint32_t flags,
                       const uint32_t* keep_cols, uint32_t nkeep, void* cuda_stream) {
@@ -560,90 +840,10 @@ uint64_t sel_count_ex(sel_table t, const void* prog, size_t prog_bytes, uint32_t
   c->last_ms = 0.f;
   const uint64_t n = t->local_rows;
   const bool scan = n > 0 && plan.path != PATH_CONST;
-  uint64_t local = 0;
-  if (!scan) local = plan.path == PATH_CONST && plan.const_value ? n : 0;
   if ((flags & SEL_KEEP_SELECTION) && !scan) c->kept_table = nullptr;
-  if (!scan && !c->comm) return local;
-
-  cudaError_t e;
-  if (scan) {
-    const uint64_t nchunks = (n + kChunkRows - 1) / kChunkRows;
-    const uint64_t units = (nchunks + kWarpsPerCta - 1) / kWarpsPerCta;
-    const size_t nslots = count_slots(plan);
-    const SelectionBufs* keep = nullptr;
-    std::vector<int> cap_off(t->cols.size(), -1);
-    if (flags & SEL_KEEP_SELECTION) {
-      if (ensure_selection(c, nchunks) != SEL_OK) return SEL_ERR;
-      const uint64_t nsb = (nchunks + kSbChunks - 1) / kSbChunks;
-      e = cudaMemsetAsync(c->sel.sb_sum, 0, nsb * sizeof(uint32_t), stream);
-      if (e != cudaSuccess) return fail64(SEL_E_CUDA, cuda_msg("cudaMemsetAsync(selection)", e));
-      c->kept_table = nullptr;  // valid again only once this probe has completed
-      c->kept_cols.clear();
-      // projected predicate columns: capture while evaluating, keep the selected values
-      uint32_t off = kIdxBytes;
-      for (uint32_t j = 0; j < nkeep && (int)c->kept_cols.size() < kMaxKeep; ++j) {
-        const int col = (int)keep_cols[j];
-        bool pred_col = false;
-        for (auto& L : plan.leaves) pred_col = pred_col || L.col == col;
-        const uint32_t w = (uint32_t)width_of(t->types[col]);
-        if (!pred_col || cap_off[col] >= 0 || off + w * kChunkRows > kIdxBytes + kCaptureBudget) continue;
-        const int k = (int)c->kept_cols.size();
-        if (ensure_slot(c, k, nchunks * (uint64_t)kChunkRows * w) != SEL_OK) return SEL_ERR;
-        cap_off[col] = (int)off;
-        c->sel.keep_col[k] = (uint8_t)col;
-        c->sel.keep_wclass[k] = wclass_of(t->types[col]);
-        c->sel.keep_cap_off[k] = (uint16_t)off;
-        c->sel.keep_slot[k] = c->slot_buf[k];
-        c->kept_cols.push_back(col);
-        off += w * kChunkRows;
-      }
-      c->sel.n_keep = (uint32_t)c->kept_cols.size();
-      c->sel.warp_smem = c->sel.n_keep ? ((off + 15u) & ~15u) : 0u;
-      keep = &c->sel;
-    }
-    auto mark_captures = [&](auto* p) {
-      std::vector<bool> marked(t->cols.size(), false);
-      for (size_t i = 0; i < plan.op.size(); ++i) {
-        if (plan.op[i] != DOP_LEAF) continue;
-        const int l = plan.arg[i];
-        const int col = plan.leaves[l].col;
-        if (cap_off[col] >= 0 && !marked[col]) {
-          p->leaf[l].cap = 1;
-          p->leaf[l].cap_off = (uint16_t)cap_off[col];
-          marked[col] = true;
-        }
-      }
-    };
-    const size_t dyn = keep ? (size_t)keep->warp_smem * kWarpsPerCta : 0;
-    if (c->timing) cudaEventRecord(c->ev0, stream);
-    int le;
-    if (fits_block<DevProgramSmall>(plan, nslots, 0)) {
-      DevProgramSmall p;
-      pack(plan, t, &p);
-      mark_captures(&p);
-      if (c->prefetch_mode < 0) p.prefetch = (keep && keep->n_keep) ? 1u : 0u;
-      const int occ = keep ? occupancy_count_keep_small(dyn) : c->occ_count_small;
-      le = launch_count_small(p, n, grid_for(c, units, occ), c->s, keep, stream);
-    } else {
-      static thread_local DevProgramLarge p;
-      pack(plan, t, &p);
-      mark_captures(&p);
-      if (c->prefetch_mode < 0) p.prefetch = (keep && keep->n_keep) ? 1u : 0u;
-      const int occ = keep ? occupancy_count_keep_large(dyn) : c->occ_count_large;
-      le = launch_count_large(p, n, grid_for(c, units, occ), c->s, keep, stream);
-    }
-    if (le != cudaSuccess) return fail64(SEL_E_CUDA, cuda_msg("count kernel launch", (cudaError_t)le));
-    if (c->timing) cudaEventRecord(c->ev1, stream);
-  } else {
-    c->h_result[0] = local;
-    e = cudaMemcpyAsync(c->s.result, c->h_result, sizeof(uint64_t), cudaMemcpyHostToDevice, stream);
-    if (e != cudaSuccess) return fail64(SEL_E_CUDA, cuda_msg("cudaMemcpyAsync", e));
-  }
-  if (c->comm) {  // SURVEY §8a a4: one 8-byte all-reduce on the probe stream
-    ncclResult_t r = nccl().AllReduce(c->s.result, c->s.result, 1, ncclUint64, ncclSum, c->comm, stream);
-    if (r != ncclSuccess) return fail64(SEL_E_NCCL, nccl_msg("ncclAllReduce", r));
-  }
-  e = cudaMemcpyAsync(c->h_result, c->s.result, sizeof(uint64_t), cudaMemcpyDeviceToHost, stream);
+  if (!scan && !c->comm) return plan.path == PATH_CONST && plan.const_value ? n : 0;
+  if (enqueue_count(t, plan, flags, keep_cols, nkeep, stream, c->s.result) != SEL_OK) return SEL_ERR;
+  cudaError_t e = cudaMemcpyAsync(c->h_result, c->s.result, sizeof(uint64_t), cudaMemcpyDeviceToHost, stream);
   if (e == cudaSuccess) e = cudaStreamSynchronize(stream);
   if (e != cudaSuccess) return fail64(SEL_E_CUDA, cuda_msg("count result", e));
   if (scan && c->timing) {
@@ -665,16 +865,8 @@ uint64_t sel_pushdown(sel_table t, const void* prog, size_t prog_bytes, const ui
   if (!t) return fail64(SEL_E_ARG, "null table");
   sel_ctx c = t->ctx;
   if (c->destroyed) return fail64(SEL_E_STATE, "context destroyed");
-  if (nproj > 0 && !proj_cols) return fail64(SEL_E_ARG, "null proj_cols");
-  if (nproj > 255) return fail64(SEL_E_ARG, "nproj must be <= 255");
-  for (uint32_t j = 0; j < nproj; ++j)
-    if (proj_cols[j] >= t->cols.size()) return fail64(SEL_E_ARG, "projection index out of range");
-  if (capacity_rows > 0) {
-    if (!out_rowids) return fail64(SEL_E_ARG, "null out_rowids with capacity > 0");
-    if (nproj > 0 && !out_cols) return fail64(SEL_E_ARG, "null out_cols with capacity > 0");
-    for (uint32_t j = 0; j < nproj; ++j)
-      if (!out_cols[j]) return fail64(SEL_E_ARG, "null out_cols entry with capacity > 0");
-  }
+  if (check_projection(t, proj_cols, nproj, out_rowids, out_cols, capacity_rows) != SEL_OK)
+    return SEL_ERR;
   Plan plan;
   if (plan_for(t, prog, prog_bytes, &plan) != SEL_OK) return SEL_ERR;
   cudaStream_t stream = (cudaStream_t)cuda_stream;
@@ -736,36 +928,10 @@ uint64_t sel_pushdown(sel_table t, const void* prog, size_t prog_bytes, const ui
     if (c->timing) cudaEventRecord(c->ev0, stream);
     int le, grid;
     if (from_sel) {
-      // Materialise from the kept selection: gathers only, every projection from global memory.
-      auto fill_sel = [&](auto* p) {
-        std::memset(p, 0, sizeof(*p));
-        p->row_offset = t->row_offset;
-        p->capacity = capacity_rows;
-        p->n_proj = capacity_rows > 0 ? nproj : 0;
-        for (uint32_t j = 0; j < p->n_proj; ++j) {
-          p->proj_src[j] = t->cols[proj_cols[j]].data;
-          p->proj_dst[j] = out_cols[j];
-          p->proj_wclass[j] = wclass_of(t->types[proj_cols[j]]);
-          p->proj_cap_off[j] = kNoCapture;
-          for (size_t k = 0; k < c->kept_cols.size(); ++k)
-            if (c->kept_cols[k] == (int)proj_cols[j]) p->proj_cap_off[j] = (uint16_t)(kKeptBase + k);
-        }
-      };
-      const uint64_t nblocks = (ntiles + kSelBlockChunks - 1) / kSelBlockChunks;
-      const uint64_t units = (nblocks + kWarpsPerCta - 1) / kWarpsPerCta;
-      if (nproj <= (uint32_t)DevProgramSmall::kMaxProj) {
-        DevProgramSmall p;
-        fill_sel(&p);
-        grid = grid_for(c, units, occupancy_pushdown_sel_small());
-        le = launch_pushdown_sel_small(p, n, out_rowids, grid, c->s, c->sel, stream);
-      } else {
-        static thread_local DevProgramLarge p;
-        fill_sel(&p);
-        grid = grid_for(c, units, occupancy_pushdown_sel_large());
-        le = launch_pushdown_sel_large(p, n, out_rowids, grid, c->s, c->sel, stream);
-      }
-      if (le != cudaSuccess) return fail64(SEL_E_CUDA, cuda_msg("push-down kernel launch", (cudaError_t)le));
-      c->last_pd_path = 1;
+      if (enqueue_pushdown_sel(t, proj_cols, nproj, out_rowids, out_cols, capacity_rows, false, 0,
+                               stream) != SEL_OK)
+        return SEL_ERR;
+      le = cudaSuccess;
     } else if (fits_block<DevProgramSmall>(plan, nslots, nproj)) {
       DevProgramSmall p;
       fill(&p);
@@ -891,8 +1057,11 @@ sel_status sel_count_batch(sel_table t, const void* const* progs, const size_t* 
   sel_ctx c = t->ctx;
   if (c->destroyed) return set_error(SEL_E_STATE, "context destroyed");
   std::vector<Plan> plans(nprog);
-  for (uint32_t k = 0; k < nprog; ++k)
+  for (uint32_t k = 0; k < nprog; ++k) {
     if (plan_for(t, progs[k], prog_bytes[k], &plans[k]) != SEL_OK) return g_status;
+    for (auto& L : plans[k].leaves)
+      if (L.bitmap >= 0) return set_error(SEL_E_ARG, "IN_BITMAP leaves are not batched");
+  }
   // distinct leaves, grouped by column (first-appearance order)
   std::vector<int> col_order;
   std::map<int, std::vector<std::vector<Interval>>> by_col;
@@ -992,23 +1161,236 @@ uint64_t sel_execute(sel_table t, const void* prog, size_t prog_bytes, const uin
                      uint32_t nproj, uint64_t max_size, uint32_t* out_rowids,
                      void* const* out_cols, uint64_t capacity_rows, uint64_t* out_local_count,
                      uint64_t* out_global_offset, int* out_materialized, void* cuda_stream) {
+  clear_error();
   if (out_materialized) *out_materialized = 0;
   if (out_local_count) *out_local_count = 0;
   if (out_global_offset) *out_global_offset = 0;
+  if (!t) return fail64(SEL_E_ARG, "null table");
+  sel_ctx c = t->ctx;
+  if (c->destroyed) return fail64(SEL_E_STATE, "context destroyed");
+  if (check_projection(t, proj_cols, nproj, out_rowids, out_cols, capacity_rows) != SEL_OK)
+    return SEL_ERR;
+  Plan plan;
+  if (plan_for(t, prog, prog_bytes, &plan) != SEL_OK) return SEL_ERR;
   // Execute(isSPD): gamma_COUNT over the compound, keeping what the materialisation reuses: the
   // selection and the projected predicate columns' values (SEL_KEEP_VALUES=0 keeps the selection
   // only; DESIGN.md §6 has both measured).
-  const bool keep_values = t && t->ctx->keep_values;
-  const uint64_t count = sel_count_ex(t, prog, prog_bytes, SEL_KEEP_SELECTION,
-                                      keep_values ? proj_cols : nullptr, keep_values ? nproj : 0u,
-                                      cuda_stream);
-  if (count == SEL_ERR) return SEL_ERR;
-  if (count > max_size) return count;  // "throw exception": revert, nothing written
-  const uint64_t r = sel_pushdown(t, prog, prog_bytes, proj_cols, nproj, out_rowids, out_cols,
-                                  capacity_rows, out_local_count, out_global_offset, cuda_stream);
-  if (r == SEL_ERR) return SEL_ERR;
+  const uint32_t nkeep = c->keep_values ? nproj : 0u;
+  const bool scan = t->local_rows > 0 && plan.path != PATH_CONST;
+  if (!scan || c->force_single) {  // host-side gate: count, then (maybe) the push-down
+    const uint64_t count = sel_count_ex(t, prog, prog_bytes, SEL_KEEP_SELECTION, proj_cols, nkeep,
+                                        cuda_stream);
+    if (count == SEL_ERR) return SEL_ERR;
+    if (count > max_size) return count;  // "throw exception": nothing written
+    const uint64_t r = sel_pushdown(t, prog, prog_bytes, proj_cols, nproj, out_rowids, out_cols,
+                                    capacity_rows, out_local_count, out_global_offset, cuda_stream);
+    if (r == SEL_ERR) return SEL_ERR;
+    if (out_materialized) *out_materialized = 1;
+    return r;
+  }
+  // Device-side gate (PAPER.md:393-400 in one stream, one host synchronisation): count keeping
+  // the selection -> global count into result[kGateSlot] (all-reduce) -> the push-down kernels
+  // read it and write nothing if count > maxSize -> per-rank counts -> one D2H.
+  cudaStream_t stream = (cudaStream_t)cuda_stream;
+  DeviceGuard g(c->device);
+  if (!g.ok) return fail64(SEL_E_CUDA, "cudaSetDevice failed");
+  c->last_ms = 0.f;
+  c->last_pd_path = -1;
+  if (enqueue_count(t, plan, SEL_KEEP_SELECTION, proj_cols, nkeep, stream,
+                    c->s.result + kGateSlot) != SEL_OK)
+    return SEL_ERR;
+  if (c->timing) cudaEventRecord(c->ev2, stream);
+  if (enqueue_pushdown_sel(t, proj_cols, nproj, out_rowids, out_cols, capacity_rows, true, max_size,
+                           stream) != SEL_OK)
+    return SEL_ERR;
+  if (c->timing) cudaEventRecord(c->ev3, stream);
+  cudaError_t e = cudaMemcpyAsync(c->h_result + kGateSlot, c->s.result + kGateSlot,
+                                  sizeof(uint64_t), cudaMemcpyDeviceToHost, stream);
+  if (c->comm) {  // all-gather the per-rank counts
+    ncclResult_t r = nccl().AllGather(c->s.result, c->s.result + 1, 1, ncclUint64, c->comm, stream);
+    if (r != ncclSuccess) return fail64(SEL_E_NCCL, nccl_msg("ncclAllGather", r));
+    if (e == cudaSuccess)
+      e = cudaMemcpyAsync(c->h_result + 1, c->s.result + 1, c->nranks * sizeof(uint64_t),
+                          cudaMemcpyDeviceToHost, stream);
+  } else if (e == cudaSuccess) {
+    e = cudaMemcpyAsync(c->h_result, c->s.result, sizeof(uint64_t), cudaMemcpyDeviceToHost, stream);
+  }
+  if (e == cudaSuccess) e = cudaStreamSynchronize(stream);
+  if (e != cudaSuccess) return fail64(SEL_E_CUDA, cuda_msg("execute result", e));
+  c->kept_table = t;
+  c->kept_prog.assign(static_cast<const char*>(prog), prog_bytes);
+  if (c->timing) {
+    cudaEventElapsedTime(&c->last_count_ms, c->ev0, c->ev1);
+    cudaEventElapsedTime(&c->last_push_ms, c->ev2, c->ev3);
+    c->last_ms = c->last_push_ms;
+  }
+  const uint64_t count = c->h_result[kGateSlot];
+  if (count > max_size) return count;  // "throw exception": nothing written
+  uint64_t local = c->h_result[0], offset = 0;
+  if (c->comm) {
+    for (int r2 = 0; r2 < c->rank; ++r2) offset += c->h_result[1 + r2];
+    local = c->h_result[1 + c->rank];
+  }
+  if (out_local_count) *out_local_count = local;
+  if (out_global_offset) *out_global_offset = offset;
   if (out_materialized) *out_materialized = 1;
-  return r;
+  return count;
 }
 
 }  // extern "C"
+
+namespace {
+
+// (Re)build a prepared execute: plan (validating bitmap ids), reserve device memory outside the
+// capture, then capture the one-synchronisation Execute sequence of sel_execute into a graph.
+sel_status capture_prepared(sel_prepared q) {
+  sel_table t = q->t;
+  sel_ctx c = t->ctx;
+  if (q->exec) cudaGraphExecDestroy(q->exec);
+  q->exec = nullptr;
+  q->graph = false;
+  Plan plan;
+  if (plan_for(t, q->prog.data(), q->prog.size(), &plan) != SEL_OK) return g_status;
+  q->alloc_gen = c->alloc_gen;
+  q->bm_gen = c->bm_gen;
+  q->timing = c->timing;
+  q->comm = c->comm;
+  if (t->local_rows == 0 || plan.path == PATH_CONST || c->comm || c->force_single) return SEL_OK;
+  DeviceGuard g(c->device);
+  if (!g.ok) return set_error(SEL_E_CUDA, "cudaSetDevice failed");
+  const uint32_t nproj = (uint32_t)q->proj.size();
+  const uint32_t nkeep = c->keep_values ? nproj : 0u;
+  const uint32_t* proj = nproj ? q->proj.data() : nullptr;
+  void* const* outs = nproj ? q->out_cols.data() : nullptr;
+  const uint64_t nchunks = (t->local_rows + kChunkRows - 1) / kChunkRows;
+  uint32_t off = kIdxBytes;
+  if (reserve_selection(t, nchunks, choose_kept(t, plan, proj, nkeep, &off)) != SEL_OK) return g_status;
+  q->alloc_gen = c->alloc_gen;
+  cudaStream_t s = c->cap_stream;
+  cudaError_t e = cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal);
+  if (e != cudaSuccess) return set_error(SEL_E_CUDA, cuda_msg("cudaStreamBeginCapture", e));
+  c->capturing = true;
+  sel_status st = enqueue_count(t, plan, SEL_KEEP_SELECTION, proj, nkeep, s, c->s.result + kGateSlot);
+  if (st == SEL_OK && c->timing) record(c, c->ev2, s);
+  if (st == SEL_OK)
+    st = enqueue_pushdown_sel(t, proj, nproj, q->out_rowids, outs, q->capacity, true, q->max_size, s);
+  if (st == SEL_OK && c->timing) record(c, c->ev3, s);
+  if (st == SEL_OK) {
+    e = cudaMemcpyAsync(c->h_result + kGateSlot, c->s.result + kGateSlot, sizeof(uint64_t),
+                        cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess)
+      e = cudaMemcpyAsync(c->h_result, c->s.result, sizeof(uint64_t), cudaMemcpyDeviceToHost, s);
+    if (e != cudaSuccess) st = set_error(SEL_E_CUDA, cuda_msg("cudaMemcpyAsync (capture)", e));
+  }
+  c->capturing = false;
+  cudaGraph_t graph = nullptr;
+  e = cudaStreamEndCapture(s, &graph);
+  if (st == SEL_OK && e != cudaSuccess) st = set_error(SEL_E_CUDA, cuda_msg("cudaStreamEndCapture", e));
+  if (st == SEL_OK) {
+    e = cudaGraphInstantiate(&q->exec, graph, 0);
+    if (e != cudaSuccess) {
+      q->exec = nullptr;
+      st = set_error(SEL_E_CUDA, cuda_msg("cudaGraphInstantiate", e));
+    }
+  }
+  if (graph) cudaGraphDestroy(graph);
+  c->kept_table = nullptr;  // the capture only configured the kept-selection bookkeeping
+  q->kept_cols = c->kept_cols;
+  q->sel = c->sel;
+  q->graph = st == SEL_OK;
+  return st;
+}
+
+}  // namespace
+
+extern "C" {
+
+sel_status sel_prepare_execute(sel_table t, const void* prog, size_t prog_bytes,
+                               const uint32_t* proj_cols, uint32_t nproj, uint64_t max_size,
+                               uint32_t* out_rowids, void* const* out_cols,
+                               uint64_t capacity_rows, sel_prepared* out) {
+  clear_error();
+  if (!out) return set_error(SEL_E_ARG, "null out");
+  *out = nullptr;
+  if (!t) return set_error(SEL_E_ARG, "null table");
+  if (!prog) return set_error(SEL_E_PROGRAM, "program shorter than its header");
+  if (t->ctx->destroyed) return set_error(SEL_E_STATE, "context destroyed");
+  if (check_projection(t, proj_cols, nproj, out_rowids, out_cols, capacity_rows) != SEL_OK)
+    return g_status;
+  sel_prepared q = new sel_prepared_s();
+  q->t = t;
+  q->prog.assign(static_cast<const char*>(prog), prog_bytes);
+  q->proj.assign(proj_cols, proj_cols + nproj);
+  if (out_cols) q->out_cols.assign(out_cols, out_cols + nproj);
+  else q->out_cols.assign(nproj, nullptr);
+  q->out_rowids = out_rowids;
+  q->max_size = max_size;
+  q->capacity = capacity_rows;
+  if (capture_prepared(q) != SEL_OK) {
+    const sel_status st = g_status;
+    if (q->exec) cudaGraphExecDestroy(q->exec);
+    delete q;
+    return st;
+  }
+  t->prepared.push_back(q);
+  *out = q;
+  return SEL_OK;
+}
+
+uint64_t sel_prepared_execute(sel_prepared q, uint64_t* out_local_count,
+                              uint64_t* out_global_offset, int* out_materialized,
+                              void* cuda_stream) {
+  clear_error();
+  if (out_materialized) *out_materialized = 0;
+  if (out_local_count) *out_local_count = 0;
+  if (out_global_offset) *out_global_offset = 0;
+  if (!q) return fail64(SEL_E_ARG, "null prepared execute");
+  if (!q->t) return fail64(SEL_E_STATE, "table released");
+  sel_table t = q->t;
+  sel_ctx c = t->ctx;
+  if (c->destroyed) return fail64(SEL_E_STATE, "context destroyed");
+  if (q->alloc_gen != c->alloc_gen || q->bm_gen != c->bm_gen || q->timing != c->timing ||
+      q->comm != c->comm) {
+    if (capture_prepared(q) != SEL_OK) return SEL_ERR;
+  }
+  if (!q->graph)
+    return sel_execute(t, q->prog.data(), q->prog.size(), q->proj.empty() ? nullptr : q->proj.data(),
+                       (uint32_t)q->proj.size(), q->max_size, q->out_rowids,
+                       q->out_cols.empty() ? nullptr : q->out_cols.data(), q->capacity,
+                       out_local_count, out_global_offset, out_materialized, cuda_stream);
+  DeviceGuard g(c->device);
+  if (!g.ok) return fail64(SEL_E_CUDA, "cudaSetDevice failed");
+  cudaStream_t stream = (cudaStream_t)cuda_stream;
+  c->kept_table = nullptr;
+  cudaError_t e = cudaGraphLaunch(q->exec, stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(stream);
+  if (e != cudaSuccess) return fail64(SEL_E_CUDA, cuda_msg("prepared execute", e));
+  c->kept_table = t;
+  c->kept_prog = q->prog;
+  c->kept_cols = q->kept_cols;
+  c->sel = q->sel;
+  c->last_pd_path = 1;
+  if (c->timing) {
+    cudaEventElapsedTime(&c->last_count_ms, c->ev0, c->ev1);
+    cudaEventElapsedTime(&c->last_push_ms, c->ev2, c->ev3);
+    c->last_ms = c->last_push_ms;
+  }
+  const uint64_t count = c->h_result[kGateSlot];
+  if (count > q->max_size) return count;  // "throw exception"
+  if (out_local_count) *out_local_count = c->h_result[0];
+  if (out_materialized) *out_materialized = 1;
+  return count;
+}
+
+void sel_prepared_release(sel_prepared q) {
+  if (!q) return;
+  if (q->t) {
+    auto& v = q->t->prepared;
+    v.erase(std::remove(v.begin(), v.end(), q), v.end());
+  }
+  if (q->exec) cudaGraphExecDestroy(q->exec);
+  delete q;
+}
+
+}  // extern "C"
+

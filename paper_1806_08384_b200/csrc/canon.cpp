@@ -30,8 +30,8 @@ enum : int { S_OK = 0, S_E_TYPE = 3, S_E_PROGRAM = 4 };
 enum : int { T_INT32 = 1, T_INT64 = 2, T_FLOAT32 = 3, T_DATE32 = 4, T_DICT8 = 5, T_DICT16 = 6,
              T_DICT32 = 7 };
 enum : uint8_t { OP_TRUE = 0x01, OP_FALSE = 0x02, OP_EQ = 0x10, OP_LT = 0x11, OP_GT = 0x12,
-                 OP_LE = 0x13, OP_GE = 0x14, OP_BETWEEN = 0x20, OP_IN = 0x30, OP_AND = 0x40,
-                 OP_OR = 0x41, OP_NOT = 0x42 };
+                 OP_LE = 0x13, OP_GE = 0x14, OP_BETWEEN = 0x20, OP_IN = 0x30,
+                 OP_IN_BITMAP = 0x31, OP_AND = 0x40, OP_OR = 0x41, OP_NOT = 0x42 };
 
 constexpr size_t kHeader = 12, kSlot = 8;
 constexpr unsigned kMaxInstr = 128, kMaxConsts = 512, kMaxDepth = 16, kMaxIn = 256;
@@ -45,7 +45,7 @@ inline uint64_t le64(const uint8_t* p) {
 
 bool is_leaf_op(uint8_t op) {
   return op == OP_EQ || op == OP_LT || op == OP_GT || op == OP_LE || op == OP_GE ||
-         op == OP_BETWEEN || op == OP_IN;
+         op == OP_BETWEEN || op == OP_IN || op == OP_IN_BITMAP;
 }
 
 bool fits(int type, uint64_t k) {
@@ -106,6 +106,8 @@ int decode_program(const void* bytes, size_t len, const int* types, uint32_t nco
       } else if (in.op == OP_IN) {
         if (in.b == 0 || in.b > kMaxIn || (unsigned)in.a + in.b > n_consts)
           return fail(S_E_PROGRAM, "IN list out of range" + at);
+      } else if (in.op == OP_IN_BITMAP) {
+        if (in.b != 0) return fail(S_E_PROGRAM, "IN_BITMAP with nonzero b" + at);
       } else if (in.b != 0 || in.a >= n_consts) {
         return fail(S_E_PROGRAM, "comparison constant out of range" + at);
       }
@@ -118,7 +120,9 @@ int decode_program(const void* bytes, size_t len, const int* types, uint32_t nco
       const int t = types[in.col];
       unsigned first = in.a, last = in.a;
       if (in.op == OP_IN) last = in.a + in.b - 1u;
-      if (in.op == OP_BETWEEN) {
+      if (in.op == OP_IN_BITMAP) {
+        if (t == T_FLOAT32) return fail(S_E_TYPE, "IN_BITMAP on a FLOAT32 column" + at);
+      } else if (in.op == OP_BETWEEN) {
         if (!fits(t, out->consts[in.a]) || !fits(t, out->consts[in.b]))
           return fail(S_E_TYPE, "BETWEEN constant not representable in its column" + at);
       } else {
@@ -247,9 +251,10 @@ IvSet cmp_set(int type, uint8_t op, uint64_t c) {
 }
 
 struct Node {
-  enum Kind { LEAF, AND, OR, NOT, CONST } kind;
-  bool value = false;  // CONST
-  int col = -1;        // LEAF
+  enum Kind { LEAF, AND, OR, NOT, CONST, BMLEAF } kind;
+  bool value = false;  // CONST; BMLEAF: negated
+  int col = -1;        // LEAF, BMLEAF
+  int bitmap = -1;     // BMLEAF
   IvSet set;           // LEAF
   std::vector<std::unique_ptr<Node>> kids;
 };
@@ -277,6 +282,13 @@ NodeP simplify(NodeP n, bool negate, const int* types) {
     case Node::CONST: return make_const(n->value != negate);
     case Node::LEAF:
       return make_leaf(n->col, negate ? complement(n->set, key_max(types[n->col])) : n->set, types);
+    case Node::BMLEAF: {  // NOT folds into the key-set test
+      NodeP b(new Node{Node::BMLEAF});
+      b->col = n->col;
+      b->bitmap = n->bitmap;
+      b->value = n->value != negate;
+      return b;
+    }
     case Node::NOT: return simplify(std::move(n->kids[0]), !negate, types);
     default: break;
   }
@@ -325,7 +337,7 @@ NodeP simplify(NodeP n, bool negate, const int* types) {
 
 // Stack slots needed to evaluate a subtree in postfix, children ordered deepest first.
 int need(const Node* n) {
-  if (n->kind == Node::LEAF || n->kind == Node::CONST) return 1;
+  if (n->kind == Node::LEAF || n->kind == Node::CONST || n->kind == Node::BMLEAF) return 1;
   std::vector<int> d;
   for (auto& k : n->kids) d.push_back(need(k.get()));
   std::sort(d.rbegin(), d.rend());
@@ -340,6 +352,16 @@ void emit(const Node* n, Plan* out) {
     out->arg.push_back((uint8_t)out->leaves.size());
     out->leaves.push_back(PlanLeaf{n->col, n->set});
     out->n_intervals += n->set.size();
+    return;
+  }
+  if (n->kind == Node::BMLEAF) {
+    out->op.push_back(DOP_LEAF);
+    out->arg.push_back((uint8_t)out->leaves.size());
+    PlanLeaf L{n->col, {}};
+    L.bitmap = n->bitmap;
+    L.negate = n->value;
+    out->leaves.push_back(L);
+    out->n_intervals += 1;  // its (words, nbits) table entry
     return;
   }
   std::vector<const Node*> kids;
@@ -377,6 +399,13 @@ void plan_program(const Program& prog, const int* types, Plan* out) {
         st.back() = std::move(n);
         break;
       }
+      case OP_IN_BITMAP: {
+        NodeP b(new Node{Node::BMLEAF});
+        b->col = in.col;
+        b->bitmap = in.a;
+        st.push_back(std::move(b));
+        break;
+      }
       default: {
         const int t = types[in.col];
         IvSet s;
@@ -401,10 +430,10 @@ void plan_program(const Program& prog, const int* types, Plan* out) {
   }
   emit(root.get(), out);
   out->max_depth = need(root.get());
-  out->conj = root->kind == Node::LEAF || root->kind == Node::AND;
+  out->conj = root->kind == Node::LEAF || root->kind == Node::BMLEAF || root->kind == Node::AND;
   if (out->conj) {
     for (auto& k : root->kids)
-      if (k->kind != Node::LEAF) out->conj = false;
+      if (k->kind != Node::LEAF && k->kind != Node::BMLEAF) out->conj = false;
   }
   out->path = out->conj ? PATH_CONJ : PATH_INTERP;
 }

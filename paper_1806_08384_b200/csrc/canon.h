@@ -26,6 +26,8 @@ struct Interval {
 struct PlanLeaf {
   int col;
   std::vector<Interval> iv;  // sorted, disjoint, non-adjacent, non-empty, not the full space
+  int bitmap = -1;           // >= 0: an IN_BITMAP leaf on key set `bitmap` (iv unused)
+  bool negate = false;       // IN_BITMAP leaf: NOT(v in set)
 };
 
 struct Plan {

@@ -209,6 +209,22 @@ __device__ __forceinline__ void load_w8_half(const void* col, uint64_t base, int
   }
 }
 
+// IN_BITMAP membership of N raw values: bit i <=> v[i] < nbits and bit v[i]
+// of the key set is set. Raw unsigned compare: negative INT32/INT64 values are >= 2^31 > nbits.
+// The set is small and hot (read-only path, L1/L2 resident); 32-bit words, little-endian layout.
+template <int N, class T>
+__device__ __forceinline__ uint32_t bitmap_test(const T (&v)[N], uint64_t words, uint64_t nbits) {
+  const uint32_t* w = reinterpret_cast<const uint32_t*>(words);
+  uint32_t m = 0;
+#pragma unroll
+  for (int i = 0; i < N; ++i) {
+    const bool in = v[i] < (T)nbits;
+    const uint32_t x = in ? __ldg(w + (uint32_t)(v[i] >> 5)) : 0u;
+    m |= ((x >> ((uint32_t)v[i] & 31u)) & 1u) << i;
+  }
+  return m;
+}
+
 // One leaf: bit i of the result <=> row i of the lane's 32 rows lies in the leaf's interval set.
 template <bool TAIL>
 __device__ __forceinline__ uint32_t leaf_mask(const void* col, const DevLeaf& L,
@@ -221,14 +237,18 @@ __device__ __forceinline__ uint32_t leaf_mask(const void* col, const DevLeaf& L,
       uint64_t v[16];
       load_w8_half<TAIL>(col, base, lane, h, nvalid, v, cap);
       uint32_t mh = 0;
-      for (int t = 0; t < L.iv_count; ++t) {
-        const uint64_t lo = lo_tab[L.iv_begin + t], sp = span_tab[L.iv_begin + t];
+      if (L.pad & kLeafBitmap) {
+        mh = bitmap_test<16>(v, lo_tab[L.iv_begin], span_tab[L.iv_begin]);
+      } else {
+        for (int t = 0; t < L.iv_count; ++t) {
+          const uint64_t lo = lo_tab[L.iv_begin + t], sp = span_tab[L.iv_begin + t];
 #pragma unroll
-        for (int i = 0; i < 16; ++i) mh |= (v[i] - lo <= sp) ? (1u << i) : 0u;
+          for (int i = 0; i < 16; ++i) mh |= (v[i] - lo <= sp) ? (1u << i) : 0u;
+        }
       }
       m |= mh << (16 * h);
     }
-    return m;
+    return (L.pad & kLeafNegate) ? ~m : m;
   }
   uint32_t v[32];
   if (L.wclass == W4) {
@@ -241,6 +261,10 @@ __device__ __forceinline__ uint32_t leaf_mask(const void* col, const DevLeaf& L,
     load_w1<TAIL>(col, base, lane, nvalid, v, cap);
   } else {
     load_w2<TAIL>(col, base, lane, nvalid, v, cap);
+  }
+  if (L.pad & kLeafBitmap) {
+    m = bitmap_test<32>(v, lo_tab[L.iv_begin], span_tab[L.iv_begin]);
+    return (L.pad & kLeafNegate) ? ~m : m;
   }
   for (int t = 0; t < L.iv_count; ++t) {
     const uint32_t lo = (uint32_t)lo_tab[L.iv_begin + t], sp = (uint32_t)span_tab[L.iv_begin + t];
@@ -747,7 +771,9 @@ constexpr uint32_t kStageCap = SEL_STAGE_CAP;          // staged rows per warp b
 template <class P>
 __global__ void __launch_bounds__(kThreads, SEL_PD_MINB) pushdown_sel_kernel(const __grid_constant__ P p,
                                                                    uint64_t n, SelectionBufs sb,
-                                                                   uint32_t* __restrict__ out_ids) {
+                                                                   uint32_t* __restrict__ out_ids,
+                                                                   const uint64_t* __restrict__ gate_count) {
+  if (p.gate && *gate_count > p.gate_max) return;  // Algorithm 1's "throw": nothing written
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   __shared__ uint16_t s_stage[kWarpsPerCta][kStageCap];
   uint16_t* my = s_stage[warp];
@@ -935,7 +961,8 @@ int launch_pushdown_sel_small(const DevProgramSmall& p, uint64_t n, uint32_t* ou
                           (cudaStream_t)st>>>(sb.chunk_cnt, nchunks, sb.sb_sum);
 #endif
   superblock_prefix_kernel<<<1, 1024, 0, (cudaStream_t)st>>>(sb.sb_sum, sb.sb_prefix, nsb, s.result);
-  pushdown_sel_kernel<DevProgramSmall><<<grid, kThreads, 0, (cudaStream_t)st>>>(p, n, sb, out_ids);
+  pushdown_sel_kernel<DevProgramSmall><<<grid, kThreads, 0, (cudaStream_t)st>>>(p, n, sb, out_ids,
+                                                                                s.result + kGateSlot);
   return (int)cudaGetLastError();
 }
 int launch_pushdown_sel_large(const DevProgramLarge& p, uint64_t n, uint32_t* out_ids, int grid,
@@ -947,7 +974,8 @@ int launch_pushdown_sel_large(const DevProgramLarge& p, uint64_t n, uint32_t* ou
                           (cudaStream_t)st>>>(sb.chunk_cnt, nchunks, sb.sb_sum);
 #endif
   superblock_prefix_kernel<<<1, 1024, 0, (cudaStream_t)st>>>(sb.sb_sum, sb.sb_prefix, nsb, s.result);
-  pushdown_sel_kernel<DevProgramLarge><<<grid, kThreads, 0, (cudaStream_t)st>>>(p, n, sb, out_ids);
+  pushdown_sel_kernel<DevProgramLarge><<<grid, kThreads, 0, (cudaStream_t)st>>>(p, n, sb, out_ids,
+                                                                                s.result + kGateSlot);
   return (int)cudaGetLastError();
 }
 int launch_pushdown_small(const DevProgramSmall& p, uint64_t n, uint32_t* out_ids, int grid,

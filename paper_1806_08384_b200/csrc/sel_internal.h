@@ -40,8 +40,10 @@ struct DevLeaf {
   uint16_t iv_begin; // first interval in lo[]/span[]
   uint16_t iv_count; // >= 1
   uint16_t cap_off;  // byte offset of the capture within the warp's shared-memory area
-  uint16_t pad;
+  uint16_t pad;      // kLeafBitmap | kLeafNegate: an IN_BITMAP leaf (lo[iv_begin] = words,
+                     // span[iv_begin] = nbits; the test is v < nbits && bit v set, raw v)
 };
+constexpr uint16_t kLeafBitmap = 1, kLeafNegate = 2;
 
 // Kernel parameter block (passed by value as a __grid_constant__; no H2D copy per probe).
 template <int MAXOPS, int MAXLEAVES, int MAXIV, int MAXSLOTS, int MAXPROJ>
@@ -56,9 +58,11 @@ struct DevProgramT {
   uint32_t prefetch;     // 1: L2 bulk-prefetch each warp's next chunk (SEL_PREFETCH=0 disables)
   uint32_t chunk_stride; // count kernel: scan chunks phase, phase + stride, ... (1: all)
   uint32_t chunk_phase;
-  uint32_t pad1;
+  uint32_t gate;         // push-down from a selection: 1 = write nothing if the global count
+                         // (Scratch::result[kGateSlot]) exceeds gate_max (Algorithm 1's throw)
   uint64_t row_offset;   // global id of local row 0 (push-down ids)
   uint64_t capacity;     // push-down capacity in rows
+  uint64_t gate_max;
   uint8_t op[MAXOPS];
   uint8_t arg[MAXOPS];   // leaf index for DOP_LEAF
   DevLeaf leaf[MAXLEAVES];
@@ -127,6 +131,12 @@ struct SelectionBufs {
   uint16_t keep_cap_off[kMaxKeep];
   void* keep_slot[kMaxKeep];
 };
+
+// Result slots: [0] local count, [1 .. kMaxRanks] gathered per-rank counts / batch counts,
+// [kGateSlot] the global count sel_execute's device-side gate reads.
+constexpr int kMaxRanks = 1024;
+constexpr int kGateSlot = 1 + kMaxRanks;
+constexpr int kResultSlots = 2 + kMaxRanks;
 
 // Device-side scratch owned by a context.
 struct Scratch {

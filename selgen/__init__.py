@@ -10,7 +10,7 @@ byte-identical columns on the CPU (tests) and on a CUDA device (bench, large GPU
 """
 
 from .hashing import splitmix64, derive_seed, h32, uniform_int
-from .program import (Cmp, Between, In, And, Or, Not, Const, F32Bits, encode, encode_raw,
+from .program import (Cmp, Between, In, InSet, And, Or, Not, Const, F32Bits, encode, encode_raw,
                       random_program, INT32, INT64, FLOAT32, DATE32, DICT8, DICT16, DICT32,
                       TYPE_WIDTH, TYPE_NAMES)
 from .tables import Column, Table
@@ -18,7 +18,7 @@ from . import configs
 
 __all__ = [
     "splitmix64", "derive_seed", "h32", "uniform_int",
-    "Cmp", "Between", "In", "And", "Or", "Not", "Const", "F32Bits", "encode", "encode_raw",
+    "Cmp", "Between", "In", "InSet", "And", "Or", "Not", "Const", "F32Bits", "encode", "encode_raw",
     "random_program", "INT32", "INT64", "FLOAT32", "DATE32", "DICT8", "DICT16", "DICT32",
     "TYPE_WIDTH", "TYPE_NAMES", "Column", "Table", "configs",
 ]

@@ -23,7 +23,7 @@ TYPE_NAMES = {INT32: "INT32", INT64: "INT64", FLOAT32: "FLOAT32", DATE32: "DATE3
 # Opcodes (include/sel.h).
 OP_TRUE, OP_FALSE = 0x01, 0x02
 OP_EQ, OP_LT, OP_GT, OP_LE, OP_GE = 0x10, 0x11, 0x12, 0x13, 0x14
-OP_BETWEEN, OP_IN = 0x20, 0x30
+OP_BETWEEN, OP_IN, OP_IN_BITMAP = 0x20, 0x30, 0x31
 OP_AND, OP_OR, OP_NOT = 0x40, 0x41, 0x42
 CMP_OPS = {"=": OP_EQ, "<": OP_LT, ">": OP_GT, "<=": OP_LE, ">=": OP_GE}
 
@@ -58,6 +58,13 @@ class Between:
 class In:
     col: int
     values: tuple
+
+
+@dataclass(frozen=True)
+class InSet:
+    """Membership in a registered key set (IN_BITMAP); `bitmap` is its id."""
+    col: int
+    bitmap: int
 
 
 @dataclass(frozen=True)
@@ -117,6 +124,8 @@ def _walk(node, types, instrs, consts):
         for v in node.values:
             consts.append(encode_const(v, types[node.col]))
         instrs.append((OP_IN, node.col, first, len(node.values)))
+    elif isinstance(node, InSet):
+        instrs.append((OP_IN_BITMAP, node.col, node.bitmap, 0))
     elif isinstance(node, (And, Or)):
         _walk(node.l, types, instrs, consts)
         _walk(node.r, types, instrs, consts)
@@ -181,14 +190,17 @@ def _pick_value(rng, ctype, pool):
 
 
 def random_program(rng, types: Sequence[int], pools: Sequence | None = None, max_depth: int = 3,
-                   in_max: int = 6):
+                   in_max: int = 6, n_bitmaps: int = 0):
     """A random AST of depth ≤ max_depth over columns with `types`. pools[c] (optional) lists
-    values that occur in column c, so that constants hit data boundaries often."""
+    values that occur in column c, so that constants hit data boundaries often. With n_bitmaps,
+    some leaves on integer columns are InSet(col, id < n_bitmaps)."""
     ncols = len(types)
 
     def leaf():
         c = int(rng.integers(ncols))
         pool = pools[c] if pools is not None else None
+        if n_bitmaps and types[c] != FLOAT32 and rng.random() < 0.2:
+            return InSet(c, int(rng.integers(n_bitmaps)))
         r = rng.random()
         if r < 0.04:
             return Const(bool(rng.integers(2)))

@@ -9,7 +9,7 @@ import struct
 
 import numpy as np
 
-from selgen.program import (Cmp, Between, In, And, Or, Not, Const, F32Bits, INT32, INT64, FLOAT32,
+from selgen.program import (Cmp, Between, In, InSet, And, Or, Not, Const, F32Bits, INT32, INT64, FLOAT32,
                             DATE32, DICT8, DICT16, DICT32)
 
 NP_DTYPE = {INT32: np.int32, INT64: np.int64, FLOAT32: np.float32, DATE32: np.int32,
@@ -71,9 +71,42 @@ def _c(v, t):
 
 # ---- NumPy renderer -------------------------------------------------------------------------
 
-def np_mask(node, cols, types, n):
+def bitmap_keys(words, nbits):
+    """The key set of a bitmap given as uint64 words."""
+    bits = np.unpackbits(np.asarray(words, dtype=np.uint64).view(np.uint8), bitorder="little")
+    return np.flatnonzero(bits[:nbits])
+
+
+def make_bitmap(keys, nbits):
+    """(uint64 words, nbits) with exactly `keys` (all < nbits) set."""
+    bits = np.zeros(((nbits + 63) // 64) * 64, dtype=np.uint8)
+    keys = np.asarray(list(keys), dtype=np.int64)
+    bits[keys] = 1
+    return np.packbits(bits, bitorder="little").view(np.uint64).copy(), int(nbits)
+
+
+def random_bitmaps(rng, pools):
+    """Key sets for InSet leaves that hit the data: boundaries 0, nbits-1, nbits; non-negative
+    pool values; an empty set; DICT8/DICT16 code-space edges."""
+    nonneg = sorted({int(v) for p in pools for v in p if isinstance(v, (int, np.integer)) and v >= 0})
+    out = [make_bitmap([0], 1), make_bitmap([], 64)]
+    keys = [k for k in range(256) if rng.random() < 0.5] + [255]
+    out.append(make_bitmap(keys, 256))
+    keys = [v for v in nonneg if v < 1001 and rng.random() < 0.6] + [1000]
+    keys += [int(k) for k in rng.integers(0, 1001, 50)]
+    out.append(make_bitmap(keys, 1001))
+    keys = [v for v in nonneg if v < 65543 and rng.random() < 0.6] + [65535, 65536, 65542]
+    keys += [int(k) for k in rng.integers(0, 65543, 300)]
+    out.append(make_bitmap(keys, 65543))
+    return out
+
+
+def np_mask(node, cols, types, n, bitmaps=None):
     if isinstance(node, Const):
         return np.full(n, bool(node.value))
+    if isinstance(node, InSet):
+        keys = bitmap_keys(*bitmaps[node.bitmap])
+        return np.isin(cols[node.col].astype(np.int64), keys.astype(np.int64))
     if isinstance(node, Cmp):
         a = cols[node.col]
         c = NP_DTYPE[types[node.col]](_c(node.value, types[node.col]))
@@ -90,19 +123,25 @@ def np_mask(node, cols, types, n):
             m |= a == NP_DTYPE[t](_c(v, t))
         return m
     if isinstance(node, And):
-        return np_mask(node.l, cols, types, n) & np_mask(node.r, cols, types, n)
+        return np_mask(node.l, cols, types, n, bitmaps) & np_mask(node.r, cols, types, n, bitmaps)
     if isinstance(node, Or):
-        return np_mask(node.l, cols, types, n) | np_mask(node.r, cols, types, n)
+        return np_mask(node.l, cols, types, n, bitmaps) | np_mask(node.r, cols, types, n, bitmaps)
     if isinstance(node, Not):
-        return ~np_mask(node.x, cols, types, n)
+        return ~np_mask(node.x, cols, types, n, bitmaps)
     raise TypeError(node)
 
 
 # ---- SQLite renderer ------------------------------------------------------------------------
 
-def sql_where(node, types, params):
+def sql_where(node, types, params, bitmaps=None):
     if isinstance(node, Const):
         return "1" if node.value else "0"
+    if isinstance(node, InSet):
+        keys = [int(k) for k in bitmap_keys(*bitmaps[node.bitmap])]
+        if not keys:
+            return "0"
+        params += keys
+        return f"(c{node.col} IN ({', '.join('?' * len(keys))}))"
     if isinstance(node, Cmp):
         params.append(_c(node.value, types[node.col]))
         return f"(c{node.col} {node.op} ?)"
@@ -113,11 +152,11 @@ def sql_where(node, types, params):
         params += [_c(v, types[node.col]) for v in node.values]
         return f"(c{node.col} IN ({', '.join('?' * len(node.values))}))"
     if isinstance(node, And):
-        return f"({sql_where(node.l, types, params)} AND {sql_where(node.r, types, params)})"
+        return f"({sql_where(node.l, types, params, bitmaps)} AND {sql_where(node.r, types, params, bitmaps)})"
     if isinstance(node, Or):
-        return f"({sql_where(node.l, types, params)} OR {sql_where(node.r, types, params)})"
+        return f"({sql_where(node.l, types, params, bitmaps)} OR {sql_where(node.r, types, params, bitmaps)})"
     if isinstance(node, Not):
-        return f"(NOT {sql_where(node.x, types, params)})"
+        return f"(NOT {sql_where(node.x, types, params, bitmaps)})"
     raise TypeError(node)
 
 
@@ -130,7 +169,7 @@ class SqliteTable:
         self.db.executemany(f"INSERT INTO t VALUES ({', '.join('?' * len(types))})", rows)
         self.types = types
 
-    def ids(self, node):
+    def ids(self, node, bitmaps=None):
         params = []
-        w = sql_where(node, self.types, params)
+        w = sql_where(node, self.types, params, bitmaps)
         return [r[0] for r in self.db.execute(f"SELECT rowid - 1 FROM t WHERE {w} ORDER BY rowid", params)]

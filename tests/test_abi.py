@@ -90,13 +90,21 @@ _U = {INT32: np.uint32, DATE32: np.uint32, FLOAT32: np.uint32, DICT32: np.uint32
       DICT8: np.uint8, DICT16: np.uint16}
 
 
-def emulate_plan(plan, cols, types, n):
+def emulate_plan(plan, cols, types, n, bitmaps=None):
     if plan["path"] == 2:
         return np.full(n, plan["const"])
     masks = []
     for L in plan["leaves"]:
         c = L["col"]
         raw = cols[c].view(_U[types[c]]).astype(np.uint64)
+        if "bitmap" in L:   # raw unsigned value < nbits and its bit set (kernels.cu bitmap_test)
+            words, nbits = bitmaps[L["bitmap"]]
+            inr = raw < np.uint64(nbits)
+            k = np.where(inr, raw, np.uint64(0)).astype(np.int64)
+            bit = (words[k >> 6] >> (k & 63).astype(np.uint64)) & np.uint64(1)
+            m = inr & (bit == 1)
+            masks.append(~m if L["negate"] else m)
+            continue
         if L["fkey"]:
             sign = (raw >> np.uint64(31)) & np.uint64(1)
             raw = raw ^ np.where(sign == 1, np.uint64(0xFFFFFFFF), np.uint64(0x80000000))
@@ -135,6 +143,32 @@ def test_plan_is_exact_vs_oracle(types):
             _, want, _ = oracle.pushdown(cols, types, prog)
             np.testing.assert_array_equal(got, want, err_msg=str(node))
     assert paths == {0, 1, 2}
+
+
+@pytest.mark.parametrize("types", [[INT32, DICT8, INT64], [DICT16, DATE32, DICT32, FLOAT32]])
+def test_plan_inset_exact_vs_oracle(types):
+    """IN_BITMAP leaves through the canonicaliser: NOT folds into the leaf's negate flag, the leaf
+    is never merged with interval leaves, and the plan selects exactly the oracle's rows."""
+    from helpers import random_bitmaps
+    rng = np.random.default_rng(sum(types) + 17)
+    n = 2000
+    cols, pools = random_table(rng, types, n)
+    for c, t in enumerate(types):
+        if t != FLOAT32:
+            small = rng.integers(0, 256 if t == DICT8 else 1100, n)
+            cols[c] = np.where(rng.random(n) < 0.5, small.astype(cols[c].dtype), cols[c])
+    bms = random_bitmaps(rng, pools)
+    negated = 0
+    with np.errstate(over="ignore"):
+        for _ in range(300):
+            node = random_program(rng, types, pools, max_depth=4, n_bitmaps=len(bms))
+            prog = encode(node, types)
+            plan = sel.program_plan(prog, types)
+            negated += sum(1 for L in plan.get("leaves", []) if L.get("negate"))
+            got = np.flatnonzero(emulate_plan(plan, cols, types, n, bms))
+            _, want, _ = oracle.pushdown(cols, types, prog, bitmaps=bms)
+            np.testing.assert_array_equal(got, want, err_msg=str(node))
+    assert negated > 0
 
 
 def test_plan_paths_of_the_paper_predicates():

@@ -326,3 +326,17 @@ def test_execute_gate(ctx):
     # a selection that matches nothing: count 0 passes any gate (0 > 0 is false), writes nothing
     r = t.execute(encode(Cmp("=", 0, 99), T.types), project=[3], max_size=0, capacity=4)
     assert r.materialized and r.count == 0 and r.rowids.numel() == 0
+    # a gated execute still keeps its selection: a push-down of the same program reuses it
+    r = t.execute(prog, project=[3], max_size=0, capacity=want_c)
+    assert not r.materialized and r.count == want_c
+    p = t.pushdown(prog, project=[3], capacity=want_c)
+    assert ctx.last_pushdown_path() == 1 and p.count == want_c
+    np.testing.assert_array_equal(p.rowids.cpu().numpy().view(np.uint32), want_ids)
+    # both kernels of the one-synchronisation execute are timed
+    ctx.enable_timing(True)
+    try:
+        r = t.execute(prog, project=configs.C2_PROJECT, max_size=n)
+        c_ms, p_ms = ctx.last_times()
+        assert r.materialized and c_ms > 0 and p_ms > 0
+    finally:
+        ctx.enable_timing(False)

@@ -1,0 +1,161 @@
+"""Prepared executes (include/sel.h sel_prepare_execute / sel_prepared_execute): Algorithm 1's
+Execute captured once into a CUDA graph and replayed. Every run must equal a
+fresh sel_execute and the oracle — including after the columns change in place, after the
+context reallocates its scratch, after the bitmap registry changes, with timing toggled, and on
+the non-graph cases (constant programs, empty tables)."""
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import paper_1806_08384_b200 as sel
+from selgen import configs
+from selgen.program import Cmp, InSet, And, Const, encode, random_program, INT32, DICT8, INT64
+
+from helpers import random_table, make_bitmap
+from test_gpu_parity import register
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def pctx(cuda_device):
+    c = sel.Context(cuda_device)
+    yield c
+    c.close()
+
+
+def _check(q, cols, types, prog, proj):
+    want_c, want_ids, want_cols = oracle.pushdown(cols, types, prog, proj=proj)
+    assert q.run() == want_c
+    assert q.materialized and q.local_count == want_c
+    r = q.result()
+    np.testing.assert_array_equal(r.rowids.cpu().numpy().view(np.uint32), want_ids)
+    for j, c in enumerate(proj):
+        np.testing.assert_array_equal(r.columns[c].cpu().numpy().view(want_cols[j].dtype), want_cols[j])
+    return want_c
+
+
+def test_prepared_parity_and_live_columns(pctx):
+    n = 600_000
+    T = configs.gen_c2(n)
+    cols = [c.numpy().copy() for c in T.columns]
+    t = register(pctx, cols, T.types)
+    prog = encode(configs.c2_probes()["listing"], T.types)
+    proj = configs.C2_PROJECT
+    q = t.prepare_execute(prog, project=proj, max_size=n)
+    for _ in range(3):
+        c = _check(q, cols, T.types, prog, proj)
+    assert c == 100_200
+    assert pctx.last_pushdown_path() == 1
+    # the graph reads the columns' current contents: change B in place, run again
+    b = t.tensors[1]
+    b[::7] = 1500                                     # inside (1000, 2001)
+    cols[1] = b.cpu().numpy().copy()
+    c2 = _check(q, cols, T.types, prog, proj)
+    assert c2 > c
+    # the run left its selection kept: a push-down of the same program reuses it
+    p = t.pushdown(prog, project=[3], capacity=c2)
+    assert pctx.last_pushdown_path() == 1 and p.count == c2
+    # the same table through a fresh execute agrees
+    r = t.execute(prog, project=proj, max_size=n)
+    np.testing.assert_array_equal(r.rowids.cpu().numpy(), q.result().rowids.cpu().numpy())
+    q.release()
+    t.release()
+
+
+def test_prepared_gate_writes_nothing(pctx):
+    n = 300_000
+    T = configs.gen_c2(n)
+    cols = [c.numpy() for c in T.columns]
+    t = register(pctx, cols, T.types)
+    prog = encode(configs.c2_probes()["listing"], T.types)
+    want = oracle.count(cols, T.types, prog)
+    ids = torch.full((want,), -7, dtype=torch.int32, device=pctx.device)
+    outs = [torch.full((want,), 5, dtype=d, device=pctx.device) for d in (torch.int32, torch.uint8, torch.int32)]
+    q = t.prepare_execute(prog, project=configs.C2_PROJECT, max_size=want - 1, capacity=want,
+                          out=(ids, outs))
+    for _ in range(2):
+        assert q.run() == want and not q.materialized and q.local_count == 0
+        assert bool((ids == -7).all()) and all(bool((o == 5).all()) for o in outs)
+    q2 = t.prepare_execute(prog, project=configs.C2_PROJECT, max_size=want, capacity=want,
+                           out=(ids, outs))
+    assert q2.run() == want and q2.materialized
+    assert not bool((ids == -7).any())
+    q.release()
+    q2.release()
+    t.release()
+
+
+def test_prepared_recaptures_after_realloc_and_timing(pctx):
+    rng = np.random.default_rng(11)
+    types = [INT32, DICT8, INT64]
+    small_cols, pools = random_table(rng, types, 5000)
+    t_small = register(pctx, small_cols, types)
+    node = random_program(rng, types, pools, max_depth=3)
+    while sel.program_path(encode(node, types), types) == 2:
+        node = random_program(rng, types, pools, max_depth=3)
+    prog = encode(node, types)
+    q = t_small.prepare_execute(prog, project=[0, 2], max_size=5000)
+    _check(q, small_cols, types, prog, [0, 2])
+    # a keeping probe of a much larger table reallocates the context's selection buffers
+    big_cols, _ = random_table(rng, types, 3_000_000)
+    t_big = register(pctx, big_cols, types)
+    assert t_big.count(prog, keep_selection=True, keep_columns=[0, 2]) == oracle.count(big_cols, types, prog)
+    _check(q, small_cols, types, prog, [0, 2])      # re-captured against the new buffers
+    pctx.enable_timing(True)
+    try:
+        _check(q, small_cols, types, prog, [0, 2])
+        c_ms, p_ms = pctx.last_times()
+        assert c_ms > 0 and p_ms > 0
+    finally:
+        pctx.enable_timing(False)
+    _check(q, small_cols, types, prog, [0, 2])
+    q.release()
+    t_big.release()
+    t_small.release()
+
+
+def test_prepared_bitmap_registry_and_release(pctx):
+    n = 50_000
+    x = (np.arange(n) % 1000).astype(np.int32)
+    y = (np.arange(n) % 7).astype(np.uint8)
+    t = register(pctx, [x, y], [INT32, DICT8])
+    w1 = torch.from_numpy(make_bitmap(range(0, 1000, 3), 1000)[0].view(np.int64).copy()).to(pctx.device)
+    bid = pctx.register_bitmap(w1, 1000)
+    prog = encode(And(InSet(0, bid), Cmp("<", 1, 4)), [INT32, DICT8])
+    q = t.prepare_execute(prog, project=[0], max_size=n)
+    want1 = int((((x % 3) == 0) & (y < 4)).sum())
+    assert q.run() == want1 and q.materialized
+    pctx.release_bitmap(bid)
+    with pytest.raises(sel.SelError) as e:
+        q.run()
+    assert e.value.status == 1
+    w2 = torch.from_numpy(make_bitmap(range(0, 1000, 5), 1000)[0].view(np.int64).copy()).to(pctx.device)
+    assert pctx.register_bitmap(w2, 1000) == bid
+    want2 = int((((x % 5) == 0) & (y < 4)).sum())
+    assert q.run() == want2
+    np.testing.assert_array_equal(q.result().columns[0].cpu().numpy() % 5, 0)
+    pctx.release_bitmap(bid)
+    t.release()
+    with pytest.raises(sel.SelError) as e:
+        q.run()
+    assert e.value.status == 8
+    q.release()
+
+
+def test_prepared_non_graph_cases(pctx):
+    x = np.arange(10_000, dtype=np.int32)
+    t = register(pctx, [x], [INT32])
+    q_true = t.prepare_execute(encode(Const(True), [INT32]), project=[0], max_size=10_000)
+    assert q_true.run() == 10_000 and q_true.materialized
+    np.testing.assert_array_equal(q_true.result().columns[0].cpu().numpy(), x)
+    q_false = t.prepare_execute(encode(Const(False), [INT32]), project=[0], max_size=0)
+    assert q_false.run() == 0 and q_false.materialized
+    with pytest.raises(sel.SelError) as e:
+        t.prepare_execute(b"nope", max_size=1)
+    assert e.value.status == 4
+    q_true.release()
+    q_false.release()
+    t.release()

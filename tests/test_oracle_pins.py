@@ -23,10 +23,10 @@ import pytest
 import oracle
 from oracle import ast_eval
 from selgen import configs
-from selgen.program import (Cmp, Between, In, And, Or, Not, Const, F32Bits, encode, encode_raw,
+from selgen.program import (Cmp, Between, In, InSet, And, Or, Not, Const, F32Bits, encode, encode_raw,
                             random_program, INT32, INT64, FLOAT32, DATE32, DICT8, DICT16, DICT32)
 
-from helpers import random_table, np_mask, SqliteTable
+from helpers import random_table, np_mask, SqliteTable, random_bitmaps, make_bitmap
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 ALL_TYPES = [INT32, INT64, FLOAT32, DATE32, DICT8, DICT16, DICT32]
@@ -60,6 +60,57 @@ def test_p1_sqlite_numpy(types):
         assert got_count == len(want_np) == len(want_sql), node
         np.testing.assert_array_equal(ids, want_np)
         np.testing.assert_array_equal(ids, want_sql)
+
+
+@pytest.mark.parametrize("types", [
+    [INT32, DICT8, INT64],
+    [DICT16, DATE32, DICT32, FLOAT32],
+])
+def test_p1_inset_sqlite_numpy(types):
+    """IN_BITMAP leaves: membership of the value in a registered key set is
+    SQL `col IN (keys...)` and np.isin, under AND/OR/NOT with every other leaf kind."""
+    rng = np.random.default_rng(sum(types) * 131)
+    n = 3000
+    cols, pools = random_table(rng, types, n)
+    for c, t in enumerate(types):   # small non-negative values, so that the key sets hit rows
+        if t != FLOAT32:
+            small = rng.integers(0, 256 if t == DICT8 else 1100, n)
+            cols[c] = np.where(rng.random(n) < 0.5, small.astype(cols[c].dtype), cols[c])
+            pools[c] = list(pools[c]) + [int(v) for v in small[:20]]
+    bms = random_bitmaps(rng, pools)
+    sq = SqliteTable(cols, types)
+    seen_nonempty = 0
+    for trial in range(60):
+        node = random_program(rng, types, pools, max_depth=3, n_bitmaps=len(bms))
+        prog = encode(node, types)
+        got = oracle.count(cols, types, prog, bitmaps=bms)
+        c, ids, _ = oracle.pushdown(cols, types, prog, bitmaps=bms)
+        want_np = np.flatnonzero(np_mask(node, cols, types, n, bms))
+        want_sql = np.asarray(sq.ids(node, bms), dtype=np.int64)
+        assert got == c == len(want_np) == len(want_sql), node
+        np.testing.assert_array_equal(ids, want_np)
+        np.testing.assert_array_equal(ids, want_sql)
+        seen_nonempty += 0 < got < n
+    assert seen_nonempty > 10
+
+
+def test_p1_inset_edges():
+    """v < nbits boundary, negative values never members (also under NOT), the empty set, and an
+    id that is not among the supplied sets (SEL_E_ARG)."""
+    x = np.array([-2**31, -1, 0, 1, 62, 63, 64, 65, 99, 100, 2**31 - 1], dtype=np.int32)
+    bm = [make_bitmap([0, 63, 64, 99], 100), make_bitmap([], 1)]
+    prog = encode(InSet(0, 0), [INT32])
+    assert oracle.pushdown([x], [INT32], prog, bitmaps=bm)[1].tolist() == [2, 5, 6, 8]
+    notp = encode(Not(InSet(0, 0)), [INT32])
+    assert oracle.pushdown([x], [INT32], notp, bitmaps=bm)[1].tolist() == [0, 1, 3, 4, 7, 9, 10]
+    assert oracle.count([x], [INT32], encode(InSet(0, 1), [INT32]), bitmaps=bm) == 0
+    y = np.array([-1, 0, 99, 100, 2**40], dtype=np.int64)
+    assert oracle.pushdown([y], [INT64], prog, bitmaps=bm)[1].tolist() == [1, 2]
+    with pytest.raises(oracle.OracleError) as e:
+        oracle.count([x], [INT32], encode(InSet(0, 2), [INT32]), bitmaps=bm)
+    assert e.value.status == 1
+    with pytest.raises(oracle.OracleError):
+        oracle.count([x], [INT32], prog)
 
 
 def test_p1_float_nan_and_signed_zero_numpy():
@@ -376,6 +427,17 @@ VALIDATOR_CASES = [
     ("prog_then_type", encode_raw([_leaf(op=0x15), _leaf(a=0)], [300]), [DICT8], E_PROG),
     ("depth_then_type", encode_raw([(0x40, 0, 0, 0), _leaf(a=0)], [300]), [DICT8], E_PROG),
     ("unknown_coltype", encode_raw([_leaf()], [5]), [9], E_TYPE),
+    # IN_BITMAP (0x31): a = set id (checked by the probe, not the validator), b must be 0
+    ("inbm_ok", encode_raw([(0x31, 0, 7, 0)], []), [INT32], E_OK),
+    ("inbm_d8_ok", encode_raw([(0x31, 0, 65535, 0)], []), [DICT8], E_OK),
+    ("inbm_i64_ok", encode_raw([(0x31, 0, 0, 0), (0x42, 0, 0, 0)], []), [INT64], E_OK),
+    ("inbm_b", encode_raw([(0x31, 0, 0, 1)], []), [INT32], E_PROG),
+    ("inbm_col", encode_raw([(0x31, 1, 0, 0)], []), [INT32], E_PROG),
+    ("inbm_f32", encode_raw([(0x31, 0, 0, 0)], []), [FLOAT32], E_TYPE),
+    ("inbm_f32_then_b", encode_raw([(0x31, 0, 0, 0), (0x31, 0, 0, 1), (0x40, 0, 0, 0)], []),
+     [FLOAT32], E_TYPE),
+    ("inbm_b_then_f32", encode_raw([(0x31, 0, 0, 1), (0x31, 0, 0, 0), (0x40, 0, 0, 0)], []),
+     [FLOAT32], E_PROG),
 ]
 
 

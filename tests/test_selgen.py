@@ -85,3 +85,12 @@ def test_program_encoding_layout():
     assert p[36:44] == b"\xff" * 8                        # -1 sign-extended
     f = encode(Cmp("<", 0, -0.0), [FLOAT32])
     assert f[-8:] == bytes([0, 0, 0, 0x80, 0, 0, 0, 0])  # binary32 bits, high word zero
+
+
+def test_inset_encoding_layout():
+    """IN_BITMAP instruction: op 0x31, col, a = set id, b = 0, no constants (include/sel.h)."""
+    from selgen.program import InSet
+    b = encode(Not(InSet(1, 513)), [INT32, DICT16])
+    assert b[:4] == b"SELP" and b[6:8] == b"\x02\x00" and b[8:10] == b"\x00\x00"
+    assert b[12:20] == bytes([0x31, 1, 0x01, 0x02, 0, 0, 0, 0])
+    assert b[20:28] == bytes([0x42, 0, 0, 0, 0, 0, 0, 0]) and len(b) == 28
