@@ -35,7 +35,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="c2", choices=["c1", "c2", "c3", "c4", "c5"])
+    ap.add_argument("--config", default="c2", choices=["c1", "c2", "c3", "c4", "c5", "c6"])
     ap.add_argument("--rows", type=int, default=0, help="override global rows (testing only)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-graph", action="store_true",
@@ -49,8 +49,15 @@ def parse():
 
 def workload(name, rows):
     """(global rows, generator(row_start, row_count, device) -> Table, program AST, projection,
-    description). BASELINE.json configs: c1..c5; the bench line is c2."""
+    description). BASELINE.json configs: c1..c5; the bench line is c2. c6 (NEXT(3))
+    also needs key sets: see key_sets()."""
     from selgen import configs
+    if name == "c6":
+        n = rows or configs.ssb_sizes(80)["lineorder"]
+        node, _ = configs.q2_probes(80)["q2.1"]
+        return (n, lambda s, c, d: configs.gen_lineorder_q2(n, 80, s, c, device=d), node, [0, 1, 3],
+                "SSB SF-80 lineorder, Q2.1 semijoin probe: lo_partkey IN {p_category = 12} AND "
+                "lo_suppkey IN {s_region = 1} (PAPER.md:719-729), push-down of orderdate, partkey, revenue")
     if name == "c2":
         n = rows or configs.C2_ROWS
         return (n, lambda s, c, d: configs.gen_c2(n, s, c, device=d),
@@ -73,6 +80,14 @@ def workload(name, rows):
     return (n, lambda s, c, d: configs.gen_sweep(n, s, c, device=d),
             configs.sweep_probe(configs.sweep_threshold(n, 0.01)), [1],
             "1e9-row sweep, x < 0.01 N")
+
+
+def key_sets(name):
+    """The IN_BITMAP key sets of a workload ([(uint64 words, nbits)], ids = positions), or []."""
+    if name != "c6":
+        return []
+    from selgen import configs
+    return configs.q2_probes(80)["q2.1"][1]
 
 
 def algo_bytes(table, prog_cols, proj, local_count, pushdown_path=0):
@@ -102,8 +117,8 @@ def algo_bytes(table, prog_cols, proj, local_count, pushdown_path=0):
 
 
 def prog_columns(node):
-    from selgen.program import Cmp, Between, In, And, Or, Not
-    if isinstance(node, (Cmp, Between, In)):
+    from selgen.program import Cmp, Between, In, InSet, And, Or, Not
+    if isinstance(node, (Cmp, Between, In, InSet)):
         return {node.col}
     if isinstance(node, (And, Or)):
         return prog_columns(node.l) | prog_columns(node.r)
@@ -184,13 +199,13 @@ def ncu_traffic(kernel, config):
 
 # ---- the oracle as baseline / reference arm ------------------------------------------------------
 
-def cpu_baseline(host_cols, table_like, prog, proj, prog_cols, nthreads):
+def cpu_baseline(host_cols, table_like, prog, proj, prog_cols, nthreads, bitmaps=None):
     """The oracle as it stands on a bounded sample: count on all host threads, push-down on one."""
     import oracle
     t0 = time.perf_counter()
-    cnt = oracle.count_mt(host_cols, table_like.types, prog, nthreads)
+    cnt = oracle.count_mt(host_cols, table_like.types, prog, nthreads, bitmaps=bitmaps)
     t1 = time.perf_counter()
-    c2, ids, outs = oracle.pushdown(host_cols, table_like.types, prog, proj=proj)
+    c2, ids, outs = oracle.pushdown(host_cols, table_like.types, prog, proj=proj, bitmaps=bitmaps)
     t2 = time.perf_counter()
     assert c2 == cnt
     _, _, step_b = algo_bytes(table_like, prog_cols, proj, cnt, 0)
@@ -206,6 +221,7 @@ def run_reference(args):
     if rank != 0:
         return
     n, gen, node, proj, desc = workload(args.config, args.rows)
+    bms = key_sets(args.config)
     sample = min(n, 12_000_000)
     T = gen(0, sample, "cpu")
     cols = [c.numpy() for c in T.columns]
@@ -215,8 +231,8 @@ def run_reference(args):
     w = [c.width for c in T.columns]
     def step():
         t0 = time.perf_counter()
-        cnt = oracle.count_mt(cols, T.types, prog, nthreads)
-        c2, ids, outs = oracle.pushdown(cols, T.types, prog, proj=proj)
+        cnt = oracle.count_mt(cols, T.types, prog, nthreads, bitmaps=bms)
+        c2, ids, outs = oracle.pushdown(cols, T.types, prog, proj=proj, bitmaps=bms)
         return time.perf_counter() - t0, cnt
     for _ in range(args.warmup):
         step()
@@ -270,6 +286,11 @@ def run_ours(args):
     ctx = sel.Context(dev)
     if world > 1:
         sdist.setup_comm(ctx)
+    bms = key_sets(args.config)   # NEXT(3) key sets (c6), registered once like the table
+    bm_dev = []
+    for words, nbits in bms:
+        bm_dev.append(torch.from_numpy(words.view(np.int64).copy()).to(dev))
+        assert ctx.register_bitmap(bm_dev[-1], nbits) == len(bm_dev) - 1
     names = [c.name for c in T.columns]
     table = sel.Table(ctx, names, T.types, [c.data for c in T.columns], row_offset=s, global_rows=n)
     prog = encode(node, T.types)
@@ -421,7 +442,8 @@ def run_ours(args):
         e2e = {"value": round(agg_bytes / (e_step / 1000) / 1e9, 3), "unit": "GB/s",
                "ms_per_step": round(e_step, 3), "h2d_bytes_per_step": int(h2d),
                "d2h_bytes_per_step": int(d2h), "steps": args.e2e_steps,
-               "mode": "pipelined across steps (H2D of step i+1 || probe + D2H of step i), pinned host memory"}
+               "mode": "pipelined across steps (H2D of step i+1 || probe + D2H of step i), pinned host memory"
+                       + ("; key sets resident (registered once)" if bms else "")}
         tabs[1].release()
 
     cpu = None
@@ -433,7 +455,8 @@ def run_ours(args):
         nthreads = os.cpu_count() or 1
         sample_table = type("S", (), {})()
         sample_table.columns, sample_table.n_rows, sample_table.types = T.columns, ns, T.types
-        by, dt, t_cnt, t_push, cnt = cpu_baseline(host_cols, sample_table, prog, proj, pc, nthreads)
+        by, dt, t_cnt, t_push, cnt = cpu_baseline(host_cols, sample_table, prog, proj, pc, nthreads,
+                                                  bitmaps=bms)
         cpu = {"value": round(by / dt / 1e9, 3), "unit": "GB/s", "cores": nthreads, "kind": "oracle",
                "sample": f"first {ns} of {n} rows; count on {nthreads} threads ({t_cnt:.2f} s), "
                          f"push-down on 1 thread ({t_push:.2f} s)"}

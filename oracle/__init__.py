@@ -56,6 +56,9 @@ def _load():
         L.oracle_pushdown.restype = u64
         L.oracle_pushdown.argtypes = [vp, vp, ctypes.c_uint32, u64, ctypes.c_char_p, sz, vp,
                                       ctypes.c_uint32, u64, vp, vp, u64, ip]
+        L.oracle_count_mt_bm.restype = u64
+        L.oracle_count_mt_bm.argtypes = [vp, vp, ctypes.c_uint32, u64, ctypes.c_char_p, sz,
+                                         ctypes.c_int, vp, vp, ctypes.c_uint32, ip]
         L.oracle_count_bm.restype = u64
         L.oracle_count_bm.argtypes = [vp, vp, ctypes.c_uint32, u64, ctypes.c_char_p, sz, vp, vp,
                                       ctypes.c_uint32, ip]
@@ -116,13 +119,15 @@ def count(columns: Sequence, types: Sequence[int], prog: bytes, bitmaps=None) ->
     return int(r)
 
 
-def count_mt(columns: Sequence, types: Sequence[int], prog: bytes, nthreads: int) -> int:
+def count_mt(columns: Sequence, types: Sequence[int], prog: bytes, nthreads: int,
+             bitmaps=None) -> int:
     """Same count, row-sharded over nthreads host threads (for timing on all cores)."""
     arrs, ptrs, tys = _marshal(columns, types)
     n = len(arrs[0]) if arrs else 0
     st = ctypes.c_int(0)
-    r = _load().oracle_count_mt(ptrs, tys.ctypes.data, len(arrs), n, prog, len(prog), nthreads,
-                                ctypes.byref(st))
+    keep, wp, nb, k = _bitmaps(bitmaps)
+    r = _load().oracle_count_mt_bm(ptrs, tys.ctypes.data, len(arrs), n, prog, len(prog), nthreads,
+                                   wp, nb.ctypes.data, k, ctypes.byref(st))
     if st.value != 0:
         raise OracleError(st.value)
     return int(r)

@@ -379,7 +379,11 @@ typedef struct {
   uint64_t begin, end;
   const uint8_t* prog;
   size_t len;
+  const uint64_t* const* bm_words;
+  const uint64_t* bm_nbits;
+  uint32_t nbm;
   uint64_t result;
+  int status;
   const void* shifted[256];
 } shard_t;
 
@@ -388,14 +392,16 @@ static void* shard_main(void* arg) {
   for (uint32_t c = 0; c < s->ncols; c++)
     s->shifted[c] = (const char*)s->cols[c] + s->begin * width_of(s->types[c]);
   int st;
-  s->result = oracle_count(s->shifted, s->types, s->ncols, s->end - s->begin, s->prog, s->len,
-                           &st);
+  s->result = oracle_count_bm(s->shifted, s->types, s->ncols, s->end - s->begin, s->prog, s->len,
+                              s->bm_words, s->bm_nbits, s->nbm, &st);
+  s->status = st;
   return NULL;
 }
 
-uint64_t oracle_count_mt(const void* const* cols, const int32_t* types, uint32_t ncols,
-                         uint64_t n, const uint8_t* prog, size_t len, int nthreads,
-                         int* status) {
+uint64_t oracle_count_mt_bm(const void* const* cols, const int32_t* types, uint32_t ncols,
+                            uint64_t n, const uint8_t* prog, size_t len, int nthreads,
+                            const uint64_t* const* bm_words, const uint64_t* bm_nbits,
+                            uint32_t nbm, int* status) {
   int s = oracle_check(prog, len, types, ncols);
   if (status) *status = s;
   if (s != O_OK) return UINT64_MAX;
@@ -408,14 +414,29 @@ uint64_t oracle_count_mt(const void* const* cols, const int32_t* types, uint32_t
     sh[t].begin = n * (uint64_t)t / (uint64_t)nthreads;
     sh[t].end = n * (uint64_t)(t + 1) / (uint64_t)nthreads;
     sh[t].prog = prog; sh[t].len = len;
+    sh[t].bm_words = bm_words; sh[t].bm_nbits = bm_nbits; sh[t].nbm = nbm;
     pthread_create(&th[t], NULL, shard_main, &sh[t]);
   }
   uint64_t total = 0;
+  int failed = O_OK;
   for (int t = 0; t < nthreads; t++) {
     pthread_join(th[t], NULL);
+    if (sh[t].status != O_OK) failed = sh[t].status;   /* e.g. an unknown IN_BITMAP id */
     total += sh[t].result;
+  }
+  if (failed != O_OK) {
+    if (status) *status = failed;
+    free(sh);
+    free(th);
+    return UINT64_MAX;
   }
   free(sh);
   free(th);
   return total;
+}
+
+uint64_t oracle_count_mt(const void* const* cols, const int32_t* types, uint32_t ncols,
+                         uint64_t n, const uint8_t* prog, size_t len, int nthreads,
+                         int* status) {
+  return oracle_count_mt_bm(cols, types, ncols, n, prog, len, nthreads, NULL, NULL, 0, status);
 }

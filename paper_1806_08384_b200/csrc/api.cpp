@@ -196,6 +196,8 @@ template <class P>
 void pack(const Plan& plan, const sel_table_s* t, P* p) {
   std::memset(p, 0, sizeof(P));
   std::vector<int> slot_of(t->cols.size(), -1);
+  std::vector<int> bm_ids;
+  std::vector<uint32_t> bm_off;
   uint32_t nslots = 0, iv = 0;
   p->n_ops = (uint32_t)plan.op.size();
   p->n_leaves = (uint32_t)plan.leaves.size();
@@ -219,11 +221,21 @@ void pack(const Plan& plan, const sel_table_s* t, P* p) {
     d.wclass = wclass_of(type);
     d.fkey = type == SEL_FLOAT32 ? 1 : 0;
     d.iv_begin = (uint16_t)iv;
-    if (L.bitmap >= 0) {  // IN_BITMAP: one table entry = (words pointer, nbits)
+    if (L.bitmap >= 0) {  // IN_BITMAP: one table entry = (words pointer, nbits | smem offset)
       d.iv_count = 1;
       d.pad = (uint16_t)(kLeafBitmap | (L.negate ? kLeafNegate : 0));
+      const uint64_t nbits = t->ctx->bm_nbits[L.bitmap];
+      uint32_t off = p->bm_bytes;
+      for (size_t q = 0; q < bm_ids.size(); ++q)
+        if (bm_ids[q] == L.bitmap) off = bm_off[q];
+      if (off == p->bm_bytes) {  // first leaf on this set: lay it out (16-byte aligned)
+        bm_ids.push_back(L.bitmap);
+        bm_off.push_back(off);
+        const uint64_t bytes = ((nbits + 127) / 128) * 16;
+        p->bm_bytes = (uint32_t)std::min<uint64_t>(off + bytes, 0xFFFFFFFFull);
+      }
       p->lo[iv] = (uint64_t)(uintptr_t)t->ctx->bm_words[L.bitmap];
-      p->span[iv] = t->ctx->bm_nbits[L.bitmap];
+      p->span[iv] = nbits | ((uint64_t)off << 32);
       ++iv;
       continue;
     }
@@ -235,6 +247,57 @@ void pack(const Plan& plan, const sel_table_s* t, P* p) {
       ++iv;
     }
   }
+}
+
+// Stage key sets in the count kernel's shared memory, smallest first, while they fit beside `dyn`
+// bytes of warp areas (a staged lookup costs ~conflict-degree cycles per warp; a global one an
+// L1 wavefront per distinct 128-byte line). Staged sets are re-laid out contiguously.
+template <class P>
+void choose_bitmap_staging(P* p, size_t dyn) {
+  p->bm_smem = 0;
+  if (p->bm_bytes == 0) return;
+  struct Set { uint64_t words; uint32_t nbits, bytes, off; };
+  std::vector<Set> sets;
+  for (uint32_t l = 0; l < p->n_leaves; ++l) {
+    const DevLeaf& L = p->leaf[l];
+    if (!(L.pad & kLeafBitmap)) continue;
+    const uint64_t w = p->lo[L.iv_begin];
+    bool seen = false;
+    for (auto& s : sets) seen = seen || s.words == w;
+    if (!seen) {
+      const uint32_t nb = (uint32_t)p->span[L.iv_begin];
+      sets.push_back({w, nb, (uint32_t)(((uint64_t)nb + 127) / 128 * 16), 0xFFFFFFFFu});
+    }
+  }
+  std::sort(sets.begin(), sets.end(), [](const Set& x, const Set& y) { return x.bytes < y.bytes; });
+  uint32_t used = 0;
+  for (auto& s : sets) {
+    if (dyn + used + s.bytes > kMaxCountSmem) break;
+    s.off = used;
+    used += s.bytes;
+  }
+  for (uint32_t l = 0; l < p->n_leaves; ++l) {
+    DevLeaf& L = p->leaf[l];
+    if (!(L.pad & kLeafBitmap)) continue;
+    for (auto& s : sets) {
+      if (s.words != p->lo[L.iv_begin] || s.off == 0xFFFFFFFFu) continue;
+      L.pad |= kLeafStaged;
+      p->span[L.iv_begin] = s.nbits | ((uint64_t)s.off << 32);
+    }
+  }
+  p->bm_smem = used;
+}
+
+// Shared-memory bytes of the distinct key sets a plan's IN_BITMAP leaves use.
+uint64_t plan_bitmap_bytes(sel_ctx c, const Plan& plan) {
+  std::vector<int> ids;
+  uint64_t total = 0;
+  for (auto& L : plan.leaves) {
+    if (L.bitmap < 0 || std::find(ids.begin(), ids.end(), L.bitmap) != ids.end()) continue;
+    ids.push_back(L.bitmap);
+    total += (c->bm_nbits[L.bitmap] + 127) / 128 * 16;
+  }
+  return total;
 }
 
 size_t count_slots(const Plan& plan) {
@@ -695,7 +758,15 @@ sel_status enqueue_count(sel_table t, const Plan& plan, uint32_t flags, const ui
       c->kept_cols.clear();
       // projected predicate columns: capture while evaluating, keep the selected values
       uint32_t off = kIdxBytes;
-      const auto chosen = choose_kept(t, plan, keep_cols, nkeep, &off);
+      auto chosen = choose_kept(t, plan, keep_cols, nkeep, &off);
+      // Key sets staged in shared memory save far more than kept values do: when both do not
+      // fit, keep no values (the push-down then gathers those columns).
+      const uint64_t bmb = plan_bitmap_bytes(c, plan);
+      if (!chosen.empty() && bmb > 0 && bmb <= kMaxCountSmem &&
+          (uint64_t)((off + 15u) & ~15u) * kWarpsPerCta + bmb > kMaxCountSmem) {
+        chosen.clear();
+        off = kIdxBytes;
+      }
       if (reserve_selection(t, nchunks, chosen) != SEL_OK) return g_status;
       for (const auto& ck : chosen) {
         const int col = ck.first, k = (int)c->kept_cols.size();
@@ -732,15 +803,19 @@ sel_status enqueue_count(sel_table t, const Plan& plan, uint32_t flags, const ui
       DevProgramSmall p;
       pack(plan, t, &p);
       mark_captures(&p);
-      if (c->prefetch_mode < 0) p.prefetch = (keep && keep->n_keep) ? 1u : 0u;
-      const int occ = keep ? occupancy_count_keep_small(dyn) : c->occ_count_small;
+      choose_bitmap_staging(&p, dyn);
+      if (c->prefetch_mode < 0) p.prefetch = ((keep && keep->n_keep) || p.bm_smem) ? 1u : 0u;
+      const int occ = keep ? occupancy_count_keep_small(dyn + p.bm_smem)
+                           : (p.bm_smem ? occupancy_count_dyn_small(p.bm_smem) : c->occ_count_small);
       le = launch_count_small(p, n, grid_for(c, units, occ), s, keep, stream);
     } else {
       static thread_local DevProgramLarge p;
       pack(plan, t, &p);
       mark_captures(&p);
-      if (c->prefetch_mode < 0) p.prefetch = (keep && keep->n_keep) ? 1u : 0u;
-      const int occ = keep ? occupancy_count_keep_large(dyn) : c->occ_count_large;
+      choose_bitmap_staging(&p, dyn);
+      if (c->prefetch_mode < 0) p.prefetch = ((keep && keep->n_keep) || p.bm_smem) ? 1u : 0u;
+      const int occ = keep ? occupancy_count_keep_large(dyn + p.bm_smem)
+                           : (p.bm_smem ? occupancy_count_dyn_large(p.bm_smem) : c->occ_count_large);
       le = launch_count_large(p, n, grid_for(c, units, occ), s, keep, stream);
     }
     if (le != cudaSuccess) return set_error(SEL_E_CUDA, cuda_msg("count kernel launch", (cudaError_t)le));
@@ -1021,13 +1096,17 @@ uint64_t sel_count_sampled(sel_table t, const void* prog, size_t prog_bytes, uin
       pack(plan, t, &p);
       p.chunk_stride = stride;
       p.chunk_phase = phase;
-      le = launch_count_small(p, n, grid_for(c, units, c->occ_count_small), c->s, nullptr, stream);
+      choose_bitmap_staging(&p, 0);
+      const int occ = p.bm_smem ? occupancy_count_dyn_small(p.bm_smem) : c->occ_count_small;
+      le = launch_count_small(p, n, grid_for(c, units, occ), c->s, nullptr, stream);
     } else {
       static thread_local DevProgramLarge p;
       pack(plan, t, &p);
       p.chunk_stride = stride;
       p.chunk_phase = phase;
-      le = launch_count_large(p, n, grid_for(c, units, c->occ_count_large), c->s, nullptr, stream);
+      choose_bitmap_staging(&p, 0);
+      const int occ = p.bm_smem ? occupancy_count_dyn_large(p.bm_smem) : c->occ_count_large;
+      le = launch_count_large(p, n, grid_for(c, units, occ), c->s, nullptr, stream);
     }
     if (le != cudaSuccess) return fail64(SEL_E_CUDA, cuda_msg("sampled count launch", (cudaError_t)le));
   } else {

@@ -225,11 +225,34 @@ __device__ __forceinline__ uint32_t bitmap_test(const T (&v)[N], uint64_t words,
   return m;
 }
 
+// The same test against a copy of the set staged in shared memory at shared address `sw`
+// (count kernel, p.bm_smem): random 4-byte LDS cost ~conflict-degree cycles per warp instead of
+// one L1 wavefront per distinct 128-byte line.
+__device__ __forceinline__ uint32_t lds_u32(uint32_t saddr) {
+  uint32_t v;
+  asm("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(saddr));
+  return v;
+}
+template <int N, class T>
+__device__ __forceinline__ uint32_t bitmap_test_smem(const T (&v)[N], uint32_t sw, uint32_t nbits) {
+  uint32_t m = 0;
+#pragma unroll
+  for (int i = 0; i < N; ++i) {
+    const bool in = v[i] < (T)nbits;
+    const uint32_t x = in ? lds_u32(sw + 4u * (uint32_t)(v[i] >> 5)) : 0u;
+    m |= ((x >> ((uint32_t)v[i] & 31u)) & 1u) << i;
+  }
+  return m;
+}
+
 // One leaf: bit i of the result <=> row i of the lane's 32 rows lies in the leaf's interval set.
+// bm_sbase: shared address of the staged key sets, or kNoStage (global lookups).
+constexpr uint32_t kNoStage = 0xFFFFFFFFu;
 template <bool TAIL>
 __device__ __forceinline__ uint32_t leaf_mask(const void* col, const DevLeaf& L,
                                               const uint64_t* lo_tab, const uint64_t* span_tab,
-                                              uint64_t base, int lane, uint32_t nvalid, char* cap) {
+                                              uint64_t base, int lane, uint32_t nvalid, char* cap,
+                                              uint32_t bm_sbase) {
   uint32_t m = 0;
   if (L.wclass == W8) {
 #pragma unroll 1  // one instance of the interval loop (see the toolchain note above)
@@ -238,7 +261,10 @@ __device__ __forceinline__ uint32_t leaf_mask(const void* col, const DevLeaf& L,
       load_w8_half<TAIL>(col, base, lane, h, nvalid, v, cap);
       uint32_t mh = 0;
       if (L.pad & kLeafBitmap) {
-        mh = bitmap_test<16>(v, lo_tab[L.iv_begin], span_tab[L.iv_begin]);
+        const uint64_t sp = span_tab[L.iv_begin];
+        mh = (bm_sbase != kNoStage && (L.pad & kLeafStaged))
+                 ? bitmap_test_smem<16>(v, bm_sbase + (uint32_t)(sp >> 32), (uint32_t)sp)
+                 : bitmap_test<16>(v, lo_tab[L.iv_begin], (uint32_t)sp);
       } else {
         for (int t = 0; t < L.iv_count; ++t) {
           const uint64_t lo = lo_tab[L.iv_begin + t], sp = span_tab[L.iv_begin + t];
@@ -263,7 +289,10 @@ __device__ __forceinline__ uint32_t leaf_mask(const void* col, const DevLeaf& L,
     load_w2<TAIL>(col, base, lane, nvalid, v, cap);
   }
   if (L.pad & kLeafBitmap) {
-    m = bitmap_test<32>(v, lo_tab[L.iv_begin], span_tab[L.iv_begin]);
+    const uint64_t sp = span_tab[L.iv_begin];
+    m = (bm_sbase != kNoStage && (L.pad & kLeafStaged))
+            ? bitmap_test_smem<32>(v, bm_sbase + (uint32_t)(sp >> 32), (uint32_t)sp)
+            : bitmap_test<32>(v, lo_tab[L.iv_begin], (uint32_t)sp);
     return (L.pad & kLeafNegate) ? ~m : m;
   }
   for (int t = 0; t < L.iv_count; ++t) {
@@ -281,10 +310,11 @@ __device__ __forceinline__ uint32_t leaf_mask(const void* col, const DevLeaf& L,
 
 template <bool TAIL, bool CAP, class P>
 __device__ __forceinline__ uint32_t eval_leaf(const P& p, const DevLeaf& L, uint64_t base,
-                                              int lane, uint32_t nvalid, char* wsmem) {
+                                              int lane, uint32_t nvalid, char* wsmem,
+                                              uint32_t bm_sbase) {
   const void* col = p.col[L.slot];
   char* cap = (CAP && L.cap) ? wsmem + L.cap_off : nullptr;
-  return leaf_mask<TAIL>(col, L, p.lo, p.span, base, lane, nvalid, cap);
+  return leaf_mask<TAIL>(col, L, p.lo, p.span, base, lane, nvalid, cap, bm_sbase);
 }
 
 // The whole predicate over the lane's 32 rows of the chunk at `base` (nvalid rows valid).
@@ -292,7 +322,8 @@ __device__ __forceinline__ uint32_t eval_leaf(const P& p, const DevLeaf& L, uint
 // so each TAIL variant inlines a single copy of the interval loop (toolchain note above).
 template <bool TAIL, bool CAP, class P>
 __device__ __forceinline__ uint32_t eval_program(const P& p, uint64_t base, int lane,
-                                                 uint32_t nvalid, char* wsmem) {
+                                                 uint32_t nvalid, char* wsmem,
+                                                 uint32_t bm_sbase = kNoStage) {
   uint32_t st[kMaxDeviceStack];
   int sp = 0;
   uint32_t acc = 0xFFFFFFFFu;
@@ -301,7 +332,7 @@ __device__ __forceinline__ uint32_t eval_program(const P& p, uint64_t base, int 
   for (uint32_t i = 0; i < p.n_ops; ++i) {
     const uint8_t op = p.op[i];
     if (op == DOP_LEAF) {
-      const uint32_t r = eval_leaf<TAIL, CAP>(p, p.leaf[p.arg[i]], base, lane, nvalid, wsmem);
+      const uint32_t r = eval_leaf<TAIL, CAP>(p, p.leaf[p.arg[i]], base, lane, nvalid, wsmem, bm_sbase);
       if (conj) acc &= r;
       else st[sp++] = r;
     } else if (!conj) {
@@ -528,6 +559,24 @@ __global__ void __launch_bounds__(kThreads, 4) count_kernel(const __grid_constan
   extern __shared__ __align__(16) char s_dyn[];
   char* wsmem = KEEP ? s_dyn + (size_t)warp * sb.warp_smem : nullptr;
   uint32_t cnt = 0;
+  // Stage the program's key sets in shared memory (after the warps' areas), once per CTA.
+  uint32_t bm_sbase = kNoStage;
+  if (p.bm_smem) {
+    char* area = s_dyn + (KEEP ? (size_t)kWarpsPerCta * sb.warp_smem : 0);
+#pragma unroll 1
+    for (uint32_t l = 0; l < p.n_leaves; ++l) {
+      const DevLeaf& L = p.leaf[l];
+      if (!(L.pad & kLeafStaged)) continue;
+      const uint64_t sp = p.span[L.iv_begin];
+      const uint64_t* src = reinterpret_cast<const uint64_t*>(p.lo[L.iv_begin]);
+      uint64_t* dst = reinterpret_cast<uint64_t*>(area + (uint32_t)(sp >> 32));
+      const uint32_t nwords = ((uint32_t)sp + 63u) >> 6;
+#pragma unroll 8
+      for (uint32_t i = threadIdx.x; i < nwords; i += kThreads) dst[i] = __ldg(src + i);
+    }
+    __syncthreads();
+    bm_sbase = (uint32_t)__cvta_generic_to_shared(area);
+  }
   // Chunks scanned: c = phase + s * stride (stride 1, phase 0: every chunk). A stride > 1 is the
   // block sample of sel_count_sampled; keeping a selection needs stride 1.
   const uint64_t stride = p.chunk_stride, phase = p.chunk_phase;
@@ -537,12 +586,12 @@ __global__ void __launch_bounds__(kThreads, 4) count_kernel(const __grid_constan
   for (uint64_t s = gw; s < ns_full; s += nw) {
     const uint64_t c = phase + s * stride;
     if (lane == 0 && p.prefetch && s + nw < ns_full) prefetch_chunk(p, c + nw * stride);
-    const uint32_t m = eval_program<false, KEEP>(p, c * kChunkRows, lane, kChunkRows, wsmem);
+    const uint32_t m = eval_program<false, KEEP>(p, c * kChunkRows, lane, kChunkRows, wsmem, bm_sbase);
     cnt += __popc(m);
     keep_chunk<P, KEEP>(sb, c, lane, m, wsmem);
   }
   if (tail_sampled && gw == ns_full % nw) {
-    const uint32_t m = eval_program<true, KEEP>(p, nfull * kChunkRows, lane, rem, wsmem);
+    const uint32_t m = eval_program<true, KEEP>(p, nfull * kChunkRows, lane, rem, wsmem, bm_sbase);
     cnt += __popc(m);
     keep_chunk<P, KEEP>(sb, nfull, lane, m, wsmem);
   }
@@ -939,17 +988,17 @@ int occupancy_of(Kern k, size_t dyn_smem) {
 int launch_count_small(const DevProgramSmall& p, uint64_t n, int grid, const Scratch& s,
                        const SelectionBufs* keep, void* st) {
   if (keep)
-    count_kernel<DevProgramSmall, true><<<grid, kThreads, (size_t)keep->warp_smem * kWarpsPerCta, (cudaStream_t)st>>>(p, n, s.partials, s.done, s.result, *keep);
+    count_kernel<DevProgramSmall, true><<<grid, kThreads, (size_t)keep->warp_smem * kWarpsPerCta + p.bm_smem, (cudaStream_t)st>>>(p, n, s.partials, s.done, s.result, *keep);
   else
-    count_kernel<DevProgramSmall, false><<<grid, kThreads, 0, (cudaStream_t)st>>>(p, n, s.partials, s.done, s.result, SelectionBufs{});
+    count_kernel<DevProgramSmall, false><<<grid, kThreads, p.bm_smem, (cudaStream_t)st>>>(p, n, s.partials, s.done, s.result, SelectionBufs{});
   return (int)cudaGetLastError();
 }
 int launch_count_large(const DevProgramLarge& p, uint64_t n, int grid, const Scratch& s,
                        const SelectionBufs* keep, void* st) {
   if (keep)
-    count_kernel<DevProgramLarge, true><<<grid, kThreads, (size_t)keep->warp_smem * kWarpsPerCta, (cudaStream_t)st>>>(p, n, s.partials, s.done, s.result, *keep);
+    count_kernel<DevProgramLarge, true><<<grid, kThreads, (size_t)keep->warp_smem * kWarpsPerCta + p.bm_smem, (cudaStream_t)st>>>(p, n, s.partials, s.done, s.result, *keep);
   else
-    count_kernel<DevProgramLarge, false><<<grid, kThreads, 0, (cudaStream_t)st>>>(p, n, s.partials, s.done, s.result, SelectionBufs{});
+    count_kernel<DevProgramLarge, false><<<grid, kThreads, p.bm_smem, (cudaStream_t)st>>>(p, n, s.partials, s.done, s.result, SelectionBufs{});
   return (int)cudaGetLastError();
 }
 int launch_pushdown_sel_small(const DevProgramSmall& p, uint64_t n, uint32_t* out_ids, int grid,
@@ -997,12 +1046,19 @@ int prepare_kernels() {
   if (e == cudaSuccess)
     e = cudaFuncSetAttribute(pushdown_kernel<DevProgramLarge>,
                              cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  const int cbytes = (int)kMaxCountSmem;  // warp areas + staged key sets
   if (e == cudaSuccess)
     e = cudaFuncSetAttribute(count_kernel<DevProgramSmall, true>,
-                             cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, cbytes);
   if (e == cudaSuccess)
     e = cudaFuncSetAttribute(count_kernel<DevProgramLarge, true>,
-                             cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, cbytes);
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(count_kernel<DevProgramSmall, false>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, cbytes);
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(count_kernel<DevProgramLarge, false>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, cbytes);
   return (int)e;
 }
 int launch_count_batch(const BatchProgram& p, uint64_t n, int grid, uint64_t* out, void* st) {
@@ -1014,6 +1070,8 @@ int occupancy_count_small() { return occupancy_of(count_kernel<DevProgramSmall, 
 int occupancy_count_keep_small(size_t dyn) { return occupancy_of(count_kernel<DevProgramSmall, true>, dyn); }
 int occupancy_count_keep_large(size_t dyn) { return occupancy_of(count_kernel<DevProgramLarge, true>, dyn); }
 int occupancy_count_large() { return occupancy_of(count_kernel<DevProgramLarge, false>, 0); }
+int occupancy_count_dyn_small(size_t dyn) { return occupancy_of(count_kernel<DevProgramSmall, false>, dyn); }
+int occupancy_count_dyn_large(size_t dyn) { return occupancy_of(count_kernel<DevProgramLarge, false>, dyn); }
 int occupancy_pushdown_sel_small() { return occupancy_of(pushdown_sel_kernel<DevProgramSmall>, 0); }
 int occupancy_pushdown_sel_large() { return occupancy_of(pushdown_sel_kernel<DevProgramLarge>, 0); }
 int occupancy_pushdown_small(size_t dyn_smem) { return occupancy_of(pushdown_kernel<DevProgramSmall>, dyn_smem); }

@@ -41,9 +41,9 @@ struct DevLeaf {
   uint16_t iv_count; // >= 1
   uint16_t cap_off;  // byte offset of the capture within the warp's shared-memory area
   uint16_t pad;      // kLeafBitmap | kLeafNegate: an IN_BITMAP leaf (lo[iv_begin] = words,
-                     // span[iv_begin] = nbits; the test is v < nbits && bit v set, raw v)
+                     // span[iv_begin] = nbits | smem offset << 32; test: v < nbits && bit v, raw v)
 };
-constexpr uint16_t kLeafBitmap = 1, kLeafNegate = 2;
+constexpr uint16_t kLeafBitmap = 1, kLeafNegate = 2, kLeafStaged = 4;  // staged: in shared memory
 
 // Kernel parameter block (passed by value as a __grid_constant__; no H2D copy per probe).
 template <int MAXOPS, int MAXLEAVES, int MAXIV, int MAXSLOTS, int MAXPROJ>
@@ -60,6 +60,9 @@ struct DevProgramT {
   uint32_t chunk_phase;
   uint32_t gate;         // push-down from a selection: 1 = write nothing if the global count
                          // (Scratch::result[kGateSlot]) exceeds gate_max (Algorithm 1's throw)
+  uint32_t bm_bytes;     // IN_BITMAP key sets: total bytes (16-byte aligned each)
+  uint32_t bm_smem;      // count kernel: bytes of the sets staged in shared memory (leaves with
+                         // kLeafStaged; offset = span[iv_begin] >> 32), 0 = none
   uint64_t row_offset;   // global id of local row 0 (push-down ids)
   uint64_t capacity;     // push-down capacity in rows
   uint64_t gate_max;
@@ -172,6 +175,9 @@ int occupancy_count_small();
 int occupancy_count_large();
 int occupancy_count_keep_small(size_t dyn_smem);
 int occupancy_count_keep_large(size_t dyn_smem);
+int occupancy_count_dyn_small(size_t dyn_smem);   // plain count with staged key sets
+int occupancy_count_dyn_large(size_t dyn_smem);
+constexpr uint32_t kMaxCountSmem = 200 * 1024;    // dynamic shared memory cap of the count kernel
 int occupancy_pushdown_small(size_t dyn_smem);
 int occupancy_pushdown_sel_small();
 int occupancy_pushdown_sel_large();

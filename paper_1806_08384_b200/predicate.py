@@ -72,6 +72,12 @@ class _In(Expr):
 
 
 @dataclass(eq=False)
+class _InSet(Expr):
+    name: str
+    bitmap: int
+
+
+@dataclass(eq=False)
 class _And(Expr):
     l: Expr
     r: Expr
@@ -123,6 +129,11 @@ class Col:
 
     def isin(self, values):
         return _In(self.name, tuple(values))
+
+    def in_set(self, bitmap_id: int):
+        """Membership in a key set registered with Context.register_bitmap (IN_BITMAP, 0x31):
+        e.g. lo_partkey IN {p_partkey : p_category = 12} as a semijoin filter."""
+        return _InSet(self.name, int(bitmap_id))
 
 
 def col(name: str) -> Col:
@@ -187,6 +198,8 @@ class _Writer:
                 return
             k = self.const_slot(self.value(e.name, e.value), t)
             self.instrs.append((_OPS[e.op], c, k, 0))
+        elif isinstance(e, _InSet):
+            self.instrs.append((0x31, self.index[e.name], e.bitmap, 0))
         elif isinstance(e, _Between):
             c = self.index[e.name]
             t = self.schema[c][1]

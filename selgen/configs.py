@@ -22,7 +22,7 @@ import numpy as np
 import torch
 
 from .hashing import derive_seed, h32, splitmix64, uniform_int
-from .program import (Cmp, Between, In, And, Or, Const, INT32, INT64, DATE32, DICT8)
+from .program import (Cmp, Between, In, InSet, And, Or, Const, INT32, INT64, DATE32, DICT8)
 from .tables import Column, Table, to_storage, STORAGE_DTYPE
 
 EPOCH = _dt.date(1970, 1, 1)
@@ -273,6 +273,79 @@ def lineorder_probes():
         "q3.1": Between(od, 19920101, 19971231),
         "q3.4": Between(od, 19971201, 19971231),
         "q4.2": Or(Between(od, 19970101, 19971231), Between(od, 19980101, 19981231)),
+    }
+
+
+# ------------------------------------------------------------------------------------------
+# C6: SSB Q2.x-shaped semijoin probes. The paper's SSB
+# queries use integer-coded dimension attributes (p_category = 12, s_region = 1, p_brand1 in
+# 2221..2228). Dimension sizes follow the SSB convention: part 200,000 x floor(1 + log2 SF),
+# supplier 2,000 x SF. p_category = mfgr*10 + category (mfgr, category in 1..5), p_brand1 =
+# p_category*100 + brand (brand in 1..40), s_region in 0..4, all by seeded hash of the key.
+# The dimension selections become key sets over lo_partkey / lo_suppkey (the fact-table probe is
+# the hot path; building the sets is the join side, out of scope, done here as input prep).
+
+LINEORDER_Q2_COLS = ["lo_orderdate", "lo_partkey", "lo_suppkey", "lo_revenue"]
+
+
+def ssb_sizes(sf: int) -> dict:
+    return {"lineorder": 6_000_000 * sf, "part": 200_000 * int(math.floor(1 + math.log2(sf))),
+            "supplier": 2_000 * sf}
+
+
+def gen_lineorder_q2(n_total: int, sf: int, row_start: int = 0, row_count: int | None = None,
+                     device="cpu", chunk: int = DEFAULT_CHUNK) -> Table:
+    if row_count is None:
+        row_count = n_total - row_start
+    dev = torch.device(device)
+    keys = _datekeys(dev)
+    sz = ssb_sizes(sf)
+    out = {n: _alloc(INT32, row_count, dev) for n in LINEORDER_Q2_COLS}
+    sd = {n: derive_seed("lineorder_q2", n) for n in LINEORDER_Q2_COLS}
+    for s, e in _chunks(row_start, row_count, chunk):
+        i = torch.arange(s, e, dtype=torch.int64, device=dev)
+        o, p = s - row_start, e - row_start
+        out["lo_orderdate"][o:p] = keys[uniform_int(sd["lo_orderdate"], i >> 2, 0, keys.numel() - 1)].to(torch.int32)
+        out["lo_partkey"][o:p] = uniform_int(sd["lo_partkey"], i, 1, sz["part"]).to(torch.int32)
+        out["lo_suppkey"][o:p] = uniform_int(sd["lo_suppkey"], i, 1, sz["supplier"]).to(torch.int32)
+        out["lo_revenue"][o:p] = uniform_int(sd["lo_revenue"], i, 100, 10_000_000).to(torch.int32)
+    cols = [Column(n, INT32, out[n]) for n in LINEORDER_Q2_COLS]
+    return Table("lineorder_q2", cols, row_count, row_start, n_total)
+
+
+def ssb_dimensions(sf: int) -> dict:
+    """Integer-coded dimension attributes indexed by key (index 0 unused): p_category, p_brand1,
+    s_region (numpy int64)."""
+    sz = ssb_sizes(sf)
+    pk = torch.arange(sz["part"] + 1, dtype=torch.int64)
+    sk = torch.arange(sz["supplier"] + 1, dtype=torch.int64)
+    mfgr = uniform_int(derive_seed("part", "mfgr"), pk, 1, 5)
+    cat = uniform_int(derive_seed("part", "category"), pk, 1, 5)
+    brand = uniform_int(derive_seed("part", "brand"), pk, 1, 40)
+    p_category = mfgr * 10 + cat
+    return {"p_category": p_category.numpy(), "p_brand1": (p_category * 100 + brand).numpy(),
+            "s_region": uniform_int(derive_seed("supplier", "region"), sk, 0, 4).numpy()}
+
+
+def key_set(mask: np.ndarray) -> tuple:
+    """(uint64 words, nbits) of the keys k with mask[k] (k = 0 .. len(mask)-1)."""
+    nb = len(mask)
+    bits = np.zeros(((nb + 63) // 64) * 64, dtype=np.uint8)
+    bits[:nb] = mask[:nb] != 0
+    bits[0] = 0                                                   # key 0 is not a key
+    return np.packbits(bits, bitorder="little").view(np.uint64).copy(), nb
+
+
+def q2_probes(sf: int):
+    """{name: (AST over LINEORDER_Q2_COLS with key-set ids 0 and 1, [part set, supplier set])}
+    for SSB Q2.1-Q2.3."""
+    dims = ssb_dimensions(sf)
+    pc, pb, sr = dims["p_category"], dims["p_brand1"], dims["s_region"]
+    node = And(InSet(1, 0), InSet(2, 1))
+    return {
+        "q2.1": (node, [key_set(pc == 12), key_set(sr == 1)]),
+        "q2.2": (node, [key_set((pb >= 2221) & (pb <= 2228)), key_set(sr == 2)]),
+        "q2.3": (node, [key_set(pb == 2239), key_set(sr == 3)]),
     }
 
 

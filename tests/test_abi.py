@@ -19,7 +19,7 @@ import pytest
 import oracle
 import paper_1806_08384_b200 as sel
 from paper_1806_08384_b200 import _native, col
-from selgen.program import (Cmp, Between, In, And, Or, Not, Const, encode, encode_raw,
+from selgen.program import (InSet, Cmp, Between, In, And, Or, Not, Const, encode, encode_raw,
                             random_program, INT32, INT64, FLOAT32, DATE32, DICT8, DICT16, DICT32)
 
 from helpers import random_table
@@ -195,6 +195,7 @@ def test_builder_bytes_match_generator():
         (col("C") == "zz", Const(False)),
         (col("C") < "c", Cmp("<", 2, 2)),
         (col("C") <= "bb", Cmp("<=", 2, 1)),
+        (col("B").in_set(3) & ~col("C").in_set(0), And(InSet(1, 3), Not(InSet(2, 0)))),
     ]
     for expr, node in cases:
         assert sel.predicate.compile_predicate(expr, schema) == encode(node, types)

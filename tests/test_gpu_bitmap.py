@@ -191,3 +191,38 @@ def test_bitmap_star_join_semijoin(bctx):
         t.release()
     finally:
         release(bctx, ids)
+
+
+def test_bitmap_staged_and_global_sets_together(bctx):
+    """A key set too large for the count kernel's shared memory (2^21 bits = 256 KB, looked up in
+    global memory) beside small staged ones, in one program, with kept values competing for the
+    same shared memory; also through the block-sampled count."""
+    n = 200_000
+    rng = np.random.default_rng(21)
+    big_n = 1 << 21
+    a = rng.integers(0, big_n + 5000, n).astype(np.int32)
+    b = rng.integers(0, 70_000, n).astype(np.uint32)
+    c = rng.integers(0, 256, n).astype(np.uint8)
+    big = make_bitmap(np.flatnonzero(rng.random(big_n) < 0.3), big_n)
+    small = make_bitmap(np.flatnonzero(rng.random(70_000) < 0.5), 70_000)
+    tiny = make_bitmap(range(0, 256, 3), 256)
+    bms = [big, small, tiny]
+    ids = upload(bctx, bms)
+    assert ids == [0, 1, 2]
+    try:
+        types = [INT32, DICT32, DICT8]
+        cols = [a, b, c]
+        t = register(bctx, cols, types)
+        for node in (And(InSet(0, 0), InSet(1, 1)),
+                     Or(And(InSet(0, 0), Not(InSet(2, 2))), InSet(1, 1)),
+                     And(Not(InSet(0, 0)), And(InSet(1, 1), InSet(2, 2)))):
+            parity(t, cols, types, node, bms, [0, 1, 2])
+            prog = encode(node, types)
+            got, rows, _ = t.count_sampled(prog, 3, 1)
+            chunk = np.arange(n) // 1024
+            keep = (chunk % 3) == 1
+            assert rows == int(keep.sum())
+            assert got == oracle.count([x[keep] for x in cols], types, prog, bitmaps=bms)
+        t.release()
+    finally:
+        release(bctx, ids)

@@ -457,3 +457,20 @@ def test_validator_max_size_program():
     assert oracle.check(prog, [INT32]) == E_OK
     x = np.arange(-5, 600, dtype=np.int32)
     assert oracle.count([x], [INT32], prog) == int(((x < 0) | (x > 511)).sum())
+
+
+def test_count_mt_matches_count():
+    """The threaded count bench.py times (oracle_count_mt[_bm]) is the same count: shards of any
+    size (incl. empty ones), every thread count, with key sets, and errors propagate."""
+    rng = np.random.default_rng(404)
+    types = [INT32, DICT8, INT64, FLOAT32]
+    cols, pools = random_table(rng, types, 1001)
+    bms = random_bitmaps(rng, pools)
+    for _ in range(20):
+        prog = encode(random_program(rng, types, pools, max_depth=3, n_bitmaps=len(bms)), types)
+        want = oracle.count(cols, types, prog, bitmaps=bms)
+        for nt in (1, 3, 8, 2000):
+            assert oracle.count_mt(cols, types, prog, nt, bitmaps=bms) == want
+    with pytest.raises(oracle.OracleError) as e:
+        oracle.count_mt(cols, types, encode(InSet(0, 9), types), 4, bitmaps=bms)
+    assert e.value.status == 1
