@@ -153,6 +153,7 @@ struct sel_ctx_s {
   uint64_t alloc_gen = 0, bm_gen = 0;
   cudaStream_t cap_stream = nullptr;  // stream-capture source for prepared executes
   bool capturing = false;             // timing events become graph event-record nodes
+  int count_nw = 0;                   // SEL_COUNT_NW: 8 forces 8-warp count CTAs
 };
 
 struct sel_table_s {
@@ -288,6 +289,15 @@ void choose_bitmap_staging(P* p, size_t dyn) {
   p->bm_smem = used;
 }
 
+// Warps per count CTA: when staged key sets leave room for a single 8-warp CTA per SM, run one
+// 32-warp CTA instead (4x the loads in flight; the sets are staged once per SM either way).
+// Needs no per-warp areas (no kept values). SEL_COUNT_NW=8 disables it.
+template <class P>
+int pick_count_warps(sel_ctx c, const P& p, size_t dyn, int occ8) {
+  if (!p.bm_smem || dyn != 0 || occ8 > 1 || c->count_nw == kWarpsPerCta) return kWarpsPerCta;
+  return 32;
+}
+
 // Shared-memory bytes of the distinct key sets a plan's IN_BITMAP leaves use.
 uint64_t plan_bitmap_bytes(sel_ctx c, const Plan& plan) {
   std::vector<int> ids;
@@ -412,6 +422,8 @@ sel_status sel_ctx_create(int cuda_device, sel_ctx* out) {
   c->prefetch_mode = pf ? (std::strcmp(pf, "1") == 0 ? 1 : 0) : -1;
   const char* kv = std::getenv("SEL_KEEP_VALUES");
   c->keep_values = !(kv && std::strcmp(kv, "0") == 0);
+  const char* cnw = std::getenv("SEL_COUNT_NW");
+  c->count_nw = cnw ? std::atoi(cnw) : 0;
   const char* pp = std::getenv("SEL_PUSHDOWN_PATH");
   c->force_single = pp && std::strcmp(pp, "single") == 0;
   const char* env = std::getenv("SEL_CTAS_PER_SM");
@@ -807,7 +819,9 @@ sel_status enqueue_count(sel_table t, const Plan& plan, uint32_t flags, const ui
       if (c->prefetch_mode < 0) p.prefetch = ((keep && keep->n_keep) || p.bm_smem) ? 1u : 0u;
       const int occ = keep ? occupancy_count_keep_small(dyn + p.bm_smem)
                            : (p.bm_smem ? occupancy_count_dyn_small(p.bm_smem) : c->occ_count_small);
-      le = launch_count_small(p, n, grid_for(c, units, occ), s, keep, stream);
+      const int nw = pick_count_warps(c, p, dyn, occ);
+      le = launch_count_small(p, n, grid_for(c, nw == kWarpsPerCta ? units : (nchunks + nw - 1) / nw,
+                                             nw == kWarpsPerCta ? occ : 1), s, keep, stream, nw);
     } else {
       static thread_local DevProgramLarge p;
       pack(plan, t, &p);
@@ -816,7 +830,9 @@ sel_status enqueue_count(sel_table t, const Plan& plan, uint32_t flags, const ui
       if (c->prefetch_mode < 0) p.prefetch = ((keep && keep->n_keep) || p.bm_smem) ? 1u : 0u;
       const int occ = keep ? occupancy_count_keep_large(dyn + p.bm_smem)
                            : (p.bm_smem ? occupancy_count_dyn_large(p.bm_smem) : c->occ_count_large);
-      le = launch_count_large(p, n, grid_for(c, units, occ), s, keep, stream);
+      const int nw = pick_count_warps(c, p, dyn, occ);
+      le = launch_count_large(p, n, grid_for(c, nw == kWarpsPerCta ? units : (nchunks + nw - 1) / nw,
+                                             nw == kWarpsPerCta ? occ : 1), s, keep, stream, nw);
     }
     if (le != cudaSuccess) return set_error(SEL_E_CUDA, cuda_msg("count kernel launch", (cudaError_t)le));
     if (c->timing) record(c, c->ev1, stream);
@@ -1098,7 +1114,9 @@ uint64_t sel_count_sampled(sel_table t, const void* prog, size_t prog_bytes, uin
       p.chunk_phase = phase;
       choose_bitmap_staging(&p, 0);
       const int occ = p.bm_smem ? occupancy_count_dyn_small(p.bm_smem) : c->occ_count_small;
-      le = launch_count_small(p, n, grid_for(c, units, occ), c->s, nullptr, stream);
+      const int nw = pick_count_warps(c, p, 0, occ);
+      le = launch_count_small(p, n, grid_for(c, nw == kWarpsPerCta ? units : (ns_full + nw) / nw,
+                                             nw == kWarpsPerCta ? occ : 1), c->s, nullptr, stream, nw);
     } else {
       static thread_local DevProgramLarge p;
       pack(plan, t, &p);
@@ -1106,7 +1124,9 @@ uint64_t sel_count_sampled(sel_table t, const void* prog, size_t prog_bytes, uin
       p.chunk_phase = phase;
       choose_bitmap_staging(&p, 0);
       const int occ = p.bm_smem ? occupancy_count_dyn_large(p.bm_smem) : c->occ_count_large;
-      le = launch_count_large(p, n, grid_for(c, units, occ), c->s, nullptr, stream);
+      const int nw = pick_count_warps(c, p, 0, occ);
+      le = launch_count_large(p, n, grid_for(c, nw == kWarpsPerCta ? units : (ns_full + nw) / nw,
+                                             nw == kWarpsPerCta ? occ : 1), c->s, nullptr, stream, nw);
     }
     if (le != cudaSuccess) return fail64(SEL_E_CUDA, cuda_msg("sampled count launch", (cudaError_t)le));
   } else {

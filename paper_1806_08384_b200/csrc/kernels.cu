@@ -545,8 +545,9 @@ __device__ __forceinline__ void keep_chunk(const SelectionBufs& sb, uint64_t c, 
   }
 }
 
-template <class P, bool KEEP>
-__global__ void __launch_bounds__(kThreads, 4) count_kernel(const __grid_constant__ P p, uint64_t n,
+// NW warps per CTA: 8 normally; 32 when staged key sets leave room for one CTA per SM only.
+template <class P, bool KEEP, int NW>
+__global__ void __launch_bounds__(NW * 32, NW == kWarpsPerCta ? 4 : 1) count_kernel(const __grid_constant__ P p, uint64_t n,
                                                          uint64_t* __restrict__ partials,
                                                          unsigned int* __restrict__ done,
                                                          uint64_t* __restrict__ out,
@@ -554,15 +555,15 @@ __global__ void __launch_bounds__(kThreads, 4) count_kernel(const __grid_constan
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const uint64_t nfull = n / kChunkRows;
   const uint32_t rem = (uint32_t)(n % kChunkRows);
-  const uint64_t gw = (uint64_t)blockIdx.x * kWarpsPerCta + warp;
-  const uint64_t nw = (uint64_t)gridDim.x * kWarpsPerCta;
+  const uint64_t gw = (uint64_t)blockIdx.x * NW + warp;
+  const uint64_t nw = (uint64_t)gridDim.x * NW;
   extern __shared__ __align__(16) char s_dyn[];
   char* wsmem = KEEP ? s_dyn + (size_t)warp * sb.warp_smem : nullptr;
   uint32_t cnt = 0;
   // Stage the program's key sets in shared memory (after the warps' areas), once per CTA.
   uint32_t bm_sbase = kNoStage;
   if (p.bm_smem) {
-    char* area = s_dyn + (KEEP ? (size_t)kWarpsPerCta * sb.warp_smem : 0);
+    char* area = s_dyn + (KEEP ? (size_t)NW * sb.warp_smem : 0);
 #pragma unroll 1
     for (uint32_t l = 0; l < p.n_leaves; ++l) {
       const DevLeaf& L = p.leaf[l];
@@ -572,7 +573,7 @@ __global__ void __launch_bounds__(kThreads, 4) count_kernel(const __grid_constan
       uint64_t* dst = reinterpret_cast<uint64_t*>(area + (uint32_t)(sp >> 32));
       const uint32_t nwords = ((uint32_t)sp + 63u) >> 6;
 #pragma unroll 8
-      for (uint32_t i = threadIdx.x; i < nwords; i += kThreads) dst[i] = __ldg(src + i);
+      for (uint32_t i = threadIdx.x; i < nwords; i += (NW * 32)) dst[i] = __ldg(src + i);
     }
     __syncthreads();
     bm_sbase = (uint32_t)__cvta_generic_to_shared(area);
@@ -597,14 +598,14 @@ __global__ void __launch_bounds__(kThreads, 4) count_kernel(const __grid_constan
   }
   cnt = __reduce_add_sync(0xFFFFFFFFu, cnt);
 
-  __shared__ uint32_t s_warp[kWarpsPerCta];
+  __shared__ uint32_t s_warp[NW];
   __shared__ bool s_last;
   if (lane == 0) s_warp[warp] = cnt;
   __syncthreads();
   if (threadIdx.x == 0) {
     uint64_t s = 0;
 #pragma unroll
-    for (int w = 0; w < kWarpsPerCta; ++w) s += s_warp[w];
+    for (int w = 0; w < NW; ++w) s += s_warp[w];
     partials[blockIdx.x] = s;
     __threadfence();
     s_last = atomicAdd(done, 1u) == gridDim.x - 1;
@@ -613,15 +614,15 @@ __global__ void __launch_bounds__(kThreads, 4) count_kernel(const __grid_constan
   if (s_last) {
     __threadfence();
     uint64_t s = 0;
-    for (uint32_t b = threadIdx.x; b < gridDim.x; b += kThreads) s += ((volatile uint64_t*)partials)[b];
+    for (uint32_t b = threadIdx.x; b < gridDim.x; b += (NW * 32)) s += ((volatile uint64_t*)partials)[b];
     for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xFFFFFFFFu, s, o);
-    __shared__ uint64_t s_sum[kWarpsPerCta];
+    __shared__ uint64_t s_sum[NW];
     if (lane == 0) s_sum[warp] = s;
     __syncthreads();
     if (threadIdx.x == 0) {
       uint64_t t = 0;
 #pragma unroll
-      for (int w = 0; w < kWarpsPerCta; ++w) t += s_sum[w];
+      for (int w = 0; w < NW; ++w) t += s_sum[w];
       *out = t;
       *done = 0u;
     }
@@ -977,29 +978,38 @@ __global__ void __launch_bounds__(kThreads) count_batch_kernel(const __grid_cons
 }
 
 template <class Kern>
-int occupancy_of(Kern k, size_t dyn_smem) {
+int occupancy_of(Kern k, size_t dyn_smem, int threads = kThreads) {
   int blocks = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, k, kThreads, dyn_smem) != cudaSuccess) return 1;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, k, threads, dyn_smem) != cudaSuccess) return 1;
   return blocks > 0 ? blocks : 1;
 }
 
 }  // namespace
 
-int launch_count_small(const DevProgramSmall& p, uint64_t n, int grid, const Scratch& s,
-                       const SelectionBufs* keep, void* st) {
-  if (keep)
-    count_kernel<DevProgramSmall, true><<<grid, kThreads, (size_t)keep->warp_smem * kWarpsPerCta + p.bm_smem, (cudaStream_t)st>>>(p, n, s.partials, s.done, s.result, *keep);
-  else
-    count_kernel<DevProgramSmall, false><<<grid, kThreads, p.bm_smem, (cudaStream_t)st>>>(p, n, s.partials, s.done, s.result, SelectionBufs{});
+template <class P>
+int launch_count_t(const P& p, uint64_t n, int grid, const Scratch& s, const SelectionBufs* keep,
+                   int nw, void* st) {
+  cudaStream_t stream = (cudaStream_t)st;
+  if (nw == 32) {
+    if (keep)
+      count_kernel<P, true, 32><<<grid, 32 * 32, (size_t)keep->warp_smem * 32 + p.bm_smem, stream>>>(p, n, s.partials, s.done, s.result, *keep);
+    else
+      count_kernel<P, false, 32><<<grid, 32 * 32, p.bm_smem, stream>>>(p, n, s.partials, s.done, s.result, SelectionBufs{});
+  } else {
+    if (keep)
+      count_kernel<P, true, kWarpsPerCta><<<grid, kThreads, (size_t)keep->warp_smem * kWarpsPerCta + p.bm_smem, stream>>>(p, n, s.partials, s.done, s.result, *keep);
+    else
+      count_kernel<P, false, kWarpsPerCta><<<grid, kThreads, p.bm_smem, stream>>>(p, n, s.partials, s.done, s.result, SelectionBufs{});
+  }
   return (int)cudaGetLastError();
 }
+int launch_count_small(const DevProgramSmall& p, uint64_t n, int grid, const Scratch& s,
+                       const SelectionBufs* keep, void* st, int nw) {
+  return launch_count_t(p, n, grid, s, keep, nw, st);
+}
 int launch_count_large(const DevProgramLarge& p, uint64_t n, int grid, const Scratch& s,
-                       const SelectionBufs* keep, void* st) {
-  if (keep)
-    count_kernel<DevProgramLarge, true><<<grid, kThreads, (size_t)keep->warp_smem * kWarpsPerCta + p.bm_smem, (cudaStream_t)st>>>(p, n, s.partials, s.done, s.result, *keep);
-  else
-    count_kernel<DevProgramLarge, false><<<grid, kThreads, p.bm_smem, (cudaStream_t)st>>>(p, n, s.partials, s.done, s.result, SelectionBufs{});
-  return (int)cudaGetLastError();
+                       const SelectionBufs* keep, void* st, int nw) {
+  return launch_count_t(p, n, grid, s, keep, nw, st);
 }
 int launch_pushdown_sel_small(const DevProgramSmall& p, uint64_t n, uint32_t* out_ids, int grid,
                               const Scratch& s, const SelectionBufs& sb, void* st) {
@@ -1047,18 +1057,16 @@ int prepare_kernels() {
     e = cudaFuncSetAttribute(pushdown_kernel<DevProgramLarge>,
                              cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
   const int cbytes = (int)kMaxCountSmem;  // warp areas + staged key sets
-  if (e == cudaSuccess)
-    e = cudaFuncSetAttribute(count_kernel<DevProgramSmall, true>,
-                             cudaFuncAttributeMaxDynamicSharedMemorySize, cbytes);
-  if (e == cudaSuccess)
-    e = cudaFuncSetAttribute(count_kernel<DevProgramLarge, true>,
-                             cudaFuncAttributeMaxDynamicSharedMemorySize, cbytes);
-  if (e == cudaSuccess)
-    e = cudaFuncSetAttribute(count_kernel<DevProgramSmall, false>,
-                             cudaFuncAttributeMaxDynamicSharedMemorySize, cbytes);
-  if (e == cudaSuccess)
-    e = cudaFuncSetAttribute(count_kernel<DevProgramLarge, false>,
-                             cudaFuncAttributeMaxDynamicSharedMemorySize, cbytes);
+  const void* counts[] = {(const void*)count_kernel<DevProgramSmall, true, kWarpsPerCta>,
+                          (const void*)count_kernel<DevProgramLarge, true, kWarpsPerCta>,
+                          (const void*)count_kernel<DevProgramSmall, false, kWarpsPerCta>,
+                          (const void*)count_kernel<DevProgramLarge, false, kWarpsPerCta>,
+                          (const void*)count_kernel<DevProgramSmall, true, 32>,
+                          (const void*)count_kernel<DevProgramLarge, true, 32>,
+                          (const void*)count_kernel<DevProgramSmall, false, 32>,
+                          (const void*)count_kernel<DevProgramLarge, false, 32>};
+  for (const void* f : counts)
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, cbytes);
   return (int)e;
 }
 int launch_count_batch(const BatchProgram& p, uint64_t n, int grid, uint64_t* out, void* st) {
@@ -1066,12 +1074,12 @@ int launch_count_batch(const BatchProgram& p, uint64_t n, int grid, uint64_t* ou
   return (int)cudaGetLastError();
 }
 int occupancy_count_batch() { return occupancy_of(count_batch_kernel, 0); }
-int occupancy_count_small() { return occupancy_of(count_kernel<DevProgramSmall, false>, 0); }
-int occupancy_count_keep_small(size_t dyn) { return occupancy_of(count_kernel<DevProgramSmall, true>, dyn); }
-int occupancy_count_keep_large(size_t dyn) { return occupancy_of(count_kernel<DevProgramLarge, true>, dyn); }
-int occupancy_count_large() { return occupancy_of(count_kernel<DevProgramLarge, false>, 0); }
-int occupancy_count_dyn_small(size_t dyn) { return occupancy_of(count_kernel<DevProgramSmall, false>, dyn); }
-int occupancy_count_dyn_large(size_t dyn) { return occupancy_of(count_kernel<DevProgramLarge, false>, dyn); }
+int occupancy_count_small() { return occupancy_of(count_kernel<DevProgramSmall, false, kWarpsPerCta>, 0); }
+int occupancy_count_keep_small(size_t dyn) { return occupancy_of(count_kernel<DevProgramSmall, true, kWarpsPerCta>, dyn); }
+int occupancy_count_keep_large(size_t dyn) { return occupancy_of(count_kernel<DevProgramLarge, true, kWarpsPerCta>, dyn); }
+int occupancy_count_large() { return occupancy_of(count_kernel<DevProgramLarge, false, kWarpsPerCta>, 0); }
+int occupancy_count_dyn_small(size_t dyn) { return occupancy_of(count_kernel<DevProgramSmall, false, kWarpsPerCta>, dyn); }
+int occupancy_count_dyn_large(size_t dyn) { return occupancy_of(count_kernel<DevProgramLarge, false, kWarpsPerCta>, dyn); }
 int occupancy_pushdown_sel_small() { return occupancy_of(pushdown_sel_kernel<DevProgramSmall>, 0); }
 int occupancy_pushdown_sel_large() { return occupancy_of(pushdown_sel_kernel<DevProgramLarge>, 0); }
 int occupancy_pushdown_small(size_t dyn_smem) { return occupancy_of(pushdown_kernel<DevProgramSmall>, dyn_smem); }

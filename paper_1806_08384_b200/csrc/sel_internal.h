@@ -154,10 +154,12 @@ struct Scratch {
 // Launch entry points (kernels.cu). Return cudaError_t as int.
 // keep != nullptr: also keep the selection (and, with keep->n_keep > 0, the selected values of
 // projected predicate columns; the leaves carry the capture offsets and keep->warp_smem is set).
+// nw: warps per CTA, kWarpsPerCta or 32 (one 1024-thread CTA per SM when staged key sets fill
+// the shared memory; keep->warp_smem must then be 0).
 int launch_count_small(const DevProgramSmall& p, uint64_t n, int grid, const Scratch& s,
-                       const SelectionBufs* keep, void* stream);
+                       const SelectionBufs* keep, void* stream, int nw = kWarpsPerCta);
 int launch_count_large(const DevProgramLarge& p, uint64_t n, int grid, const Scratch& s,
-                       const SelectionBufs* keep, void* stream);
+                       const SelectionBufs* keep, void* stream, int nw = kWarpsPerCta);
 // Push-down from a kept selection: superblock prefix (writes the local count to s.result[0]) and
 // the compaction/gather kernel.
 int launch_pushdown_sel_small(const DevProgramSmall& p, uint64_t n, uint32_t* out_ids, int grid,

@@ -3,7 +3,9 @@
 # Usage: scripts/profile.sh <tag> [bench args...]
 set -u
 TAG=${1:-r1}; shift || true
-ARGS=${*:-"--steps 3 --warmup 3 --no-cpu --no-e2e"}
+# --no-graph: ncu does not attribute kernels replayed inside the prepared CUDA graph; the kernels
+# and their launch configuration are the same.
+ARGS=${*:-"--steps 3 --warmup 3 --no-cpu --no-e2e --no-graph"}
 mkdir -p gpurun_out
 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
     --log-file gpurun_out/launches_${TAG}.csv python bench.py $ARGS > gpurun_out/launches_${TAG}.out 2>&1

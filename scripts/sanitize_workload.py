@@ -30,5 +30,31 @@ for n in [5, 1025, 70_001]:
         assert c == want[0] == r1.count == r2.count == r3.count and b[0] + b[1] == n
         for r in (r1, r2, r3):
             assert np.array_equal(r.rowids.cpu().numpy().view(np.uint32), want[1])
+# IN_BITMAP leaves: a staged small set and a global (too large to stage) set; prepared executes;
+# the block-sampled count
+from helpers import make_bitmap
+for n in [1025, 70_001]:
+    rng = np.random.default_rng(7 + n)
+    a = rng.integers(0, (1 << 21) + 100, n).astype(np.int32)
+    b = rng.integers(0, 3000, n).astype(np.int32)
+    big = make_bitmap(np.flatnonzero(rng.random(1 << 21) < 0.3), 1 << 21)
+    small = make_bitmap(np.flatnonzero(rng.random(3000) < 0.5), 3000)
+    ids = [ctx.register_bitmap(torch.from_numpy(w.view(np.int64).copy()).to(dev), nb) for w, nb in (big, small)]
+    t = sel.Table(ctx, ["a", "b"], [INT32, INT32], [torch.from_numpy(a).to(dev), torch.from_numpy(b).to(dev)])
+    for node in (And(InSet(0, ids[0]), InSet(1, ids[1])), Or(Not(InSet(0, ids[0])), Cmp("<", 1, 100))):
+        prog = encode(node, [INT32, INT32])
+        want = oracle.pushdown([a, b], [INT32, INT32], prog, proj=[0, 1], bitmaps=[big, small])
+        r1 = t.execute(prog, project=[0, 1], max_size=n)
+        q = t.prepare_execute(prog, project=[0, 1], max_size=n)
+        assert q.run() == want[0] == r1.count
+        assert np.array_equal(q.result().rowids.cpu().numpy().view(np.uint32), want[1])
+        q.release()
+        t.count(encode(Const(True), [INT32, INT32]), keep_selection=True)
+        r2 = t.pushdown(prog, project=[0, 1], capacity=max(want[0], 1))       # single pass, global sets
+        assert np.array_equal(r2.rowids.cpu().numpy().view(np.uint32), want[1])
+        assert t.count_sampled(prog, 3, 1)[1] > 0
+    t.release()
+    for i in ids:
+        ctx.release_bitmap(i)
 torch.cuda.synchronize()
 print("sanitize workload ok")

@@ -226,3 +226,43 @@ def test_bitmap_staged_and_global_sets_together(bctx):
         t.release()
     finally:
         release(bctx, ids)
+
+
+def test_bitmap_large_staged_set_32_warp_count(bctx):
+    """A staged key set large enough (150 KB) that only one CTA fits per SM: the count runs
+    32-warp CTAs (pick_count_warps). Plain count, keeping count (kept values yield to the set),
+    execute, prepared execute and the block-sampled count all match the oracle; ragged size."""
+    n = 1_000_003
+    rng = np.random.default_rng(33)
+    nb = 1_200_000
+    k = rng.integers(0, nb + 1000, n).astype(np.int32)
+    s = rng.integers(0, 40_000, n).astype(np.int32)
+    v = rng.integers(-10**6, 10**6, n).astype(np.int64)
+    bms = [make_bitmap(np.flatnonzero(rng.random(nb) < 0.04), nb),
+           make_bitmap(np.flatnonzero(rng.random(40_000) < 0.2), 40_000)]
+    ids = upload(bctx, bms)
+    assert ids == [0, 1]
+    try:
+        types = [INT32, INT32, INT64]
+        cols = [k, s, v]
+        t = register(bctx, cols, types)
+        for node in (And(InSet(0, 0), InSet(1, 1)), Or(InSet(0, 0), Not(InSet(1, 1))),
+                     And(InSet(0, 0), Cmp(">", 2, 0))):
+            parity(t, cols, types, node, bms, [0, 2])
+            prog = encode(node, types)
+            want_c, want_ids, want_cols = oracle.pushdown(cols, types, prog, proj=[0, 2], bitmaps=bms)
+            r = t.execute(prog, project=[0, 2], max_size=n)
+            assert r.materialized and r.count == want_c
+            np.testing.assert_array_equal(r.rowids.cpu().numpy().view(np.uint32), want_ids)
+            np.testing.assert_array_equal(r.columns[2].cpu().numpy(), want_cols[1])
+            q = t.prepare_execute(prog, project=[0, 2], max_size=n)
+            assert q.run() == want_c
+            np.testing.assert_array_equal(q.result().rowids.cpu().numpy().view(np.uint32), want_ids)
+            q.release()
+            got, rows, _ = t.count_sampled(prog, 5, 2)
+            keep = (np.arange(n) // 1024) % 5 == 2
+            assert rows == int(keep.sum())
+            assert got == oracle.count([x[keep] for x in cols], types, prog, bitmaps=bms)
+        t.release()
+    finally:
+        release(bctx, ids)
