@@ -35,19 +35,25 @@ def _stale() -> bool:
     return any(os.path.getmtime(f) > t for f in SOURCES + HEADERS)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not _stale():
+def build(force: bool = False, verbose: bool = False, out: str = LIB, defines=()) -> str:
+    """Build libsel.so. `out`/`defines` (-DNAME=VALUE tuning macros, e.g. SEL_GATHER_BATCH) build
+    an A/B variant elsewhere; load it with SEL_LIB=<path>. The product is the default build."""
+    if out == LIB and not defines and not force and not _stale():
         return LIB
     nccl_inc, nccl_lib = _nccl_dirs()
     cmd = ["nvcc", *ARCH, "-O3", "-lineinfo", "-std=c++17", "-shared", "-cudart", "static",
            "-Xcompiler", "-fPIC", "-Xptxas", "-v" if verbose else "-O3",
-           "-I", os.path.join(ROOT, "include"), "-I", nccl_inc,
-           f'-DSEL_NCCL_FALLBACK="{nccl_lib}"', *SOURCES, "-o", LIB + ".tmp", "-ldl"]
+           "-I", os.path.join(ROOT, "include"), "-I", nccl_inc, *[f"-D{d}" for d in defines],
+           f'-DSEL_NCCL_FALLBACK="{nccl_lib}"', *SOURCES, "-o", out + ".tmp", "-ldl"]
     subprocess.run(cmd, check=True)
-    os.replace(LIB + ".tmp", LIB)
-    return LIB
+    os.replace(out + ".tmp", out)
+    return out
 
 
 if __name__ == "__main__":
     import sys
-    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))
+    args = sys.argv[1:]
+    defs = [a[2:] for a in args if a.startswith("-D")]
+    outs = [a[6:] for a in args if a.startswith("--out=")]
+    print(build(force="--force" in args, verbose="-v" in args, out=outs[0] if outs else LIB,
+                defines=defs))

@@ -353,19 +353,23 @@ __device__ __forceinline__ uint64_t pack_status(uint32_t epoch, uint64_t flag, u
 
 // Write-out of a projected column gathered from global memory (non-predicate columns): the
 // chunk-local rows s_idx[0..lim) ascending; batches of 8 loads in flight per lane before stores.
+#ifndef SEL_GATHER_BATCH
+#define SEL_GATHER_BATCH 8   // loads in flight per lane (A/B: 4 equal, 16 slower on C2)
+#endif
 template <class T>
 __device__ __forceinline__ void gather_global(const void* src_v, void* dst_v, uint64_t cbase,
                                               uint64_t gbase, const uint16_t* s_idx, uint32_t lim,
                                               int lane) {
+  constexpr int B = SEL_GATHER_BATCH;
   const T* __restrict__ src = static_cast<const T*>(src_v) + cbase;
   T* __restrict__ dst = static_cast<T*>(dst_v) + gbase;
   uint32_t q = lane;
-  for (; q + 7 * 32 < lim; q += 8 * 32) {
-    T v[8];
+  for (; q + (B - 1) * 32 < lim; q += B * 32) {
+    T v[B];
 #pragma unroll
-    for (int u = 0; u < 8; ++u) v[u] = __ldg(src + s_idx[q + 32 * u]);
+    for (int u = 0; u < B; ++u) v[u] = __ldg(src + s_idx[q + 32 * u]);
 #pragma unroll
-    for (int u = 0; u < 8; ++u) dst[q + 32 * u] = v[u];
+    for (int u = 0; u < B; ++u) dst[q + 32 * u] = v[u];
   }
   for (; q < lim; q += 32) dst[q] = __ldg(src + s_idx[q]);
 }
