@@ -38,6 +38,7 @@ def parse():
     ap.add_argument("--config", default="c2", choices=["c1", "c2", "c3", "c4", "c5", "c6"])
     ap.add_argument("--rows", type=int, default=0, help="override global rows (testing only)")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-read-peak", action="store_true")
     ap.add_argument("--no-graph", action="store_true",
                     help="time table.execute() per step instead of the prepared (graph) execute")
     ap.add_argument("--no-cpu", action="store_true")
@@ -90,7 +91,18 @@ def key_sets(name):
     return configs.q2_probes(80)["q2.1"][1]
 
 
-def algo_bytes(table, prog_cols, proj, local_count, pushdown_path=0):
+def const_columns(prog, types):
+    """Columns the program pins to one value (a conjunction with a single-point leaf on them):
+    the push-down fills those projections instead of reading them."""
+    import paper_1806_08384_b200 as sel
+    plan = sel.program_plan(prog, types)
+    if plan["path"] != 1:
+        return set()
+    return {L["col"] for L in plan["leaves"]
+            if "bitmap" not in L and len(L["lo"]) == 1 and L["span"] == [0]}
+
+
+def algo_bytes(table, prog_cols, proj, local_count, pushdown_path=0, consts=()):
     """Algorithmic bytes.
     step  = what COUNT + push-down must move once (e.g. C2: 5.4 GB scan + 0.40 GB of D
             read + 1.303 GB written = 7.10 GB): rows x distinct predicate widths + selected x
@@ -101,7 +113,7 @@ def algo_bytes(table, prog_cols, proj, local_count, pushdown_path=0):
       single pass (0): the count scan + selected x non-predicate projected widths + writes;
       from a kept selection (1): the selection (rows/8 + 2 B per 1024 rows) + selected x all
                        projected widths + writes — it evaluates nothing, so no predicate column
-                       is charged."""
+                       is charged; columns pinned to a constant (`consts`) are filled, not read."""
     w = [c.width for c in table.columns]
     n = table.n_rows
     scan = n * sum(w[c] for c in prog_cols)
@@ -110,7 +122,7 @@ def algo_bytes(table, prog_cols, proj, local_count, pushdown_path=0):
     single = scan + local_count * sum(w[c] for c in set(proj) if c not in prog_cols) + write
     if pushdown_path == 1:
         selection = n // 8 + 2 * ((n + 1023) // 1024)
-        push_b = selection + local_count * sum(w[c] for c in proj) + write
+        push_b = selection + local_count * sum(w[c] for c in proj if c not in consts) + write
     else:
         push_b = single
     return count_b, push_b, single + 8
@@ -353,7 +365,8 @@ def run_ours(args):
         dist.barrier()
     dev_ms = ev0.elapsed_time(ev1)
     pd_path = ctx.last_pushdown_path()
-    cb, pb, step_b = algo_bytes(T, pc, proj, local_count, pd_path)
+    consts = const_columns(prog, T.types)
+    cb, pb, step_b = algo_bytes(T, pc, proj, local_count, pd_path, consts)
     my_bytes = step_b
     t = torch.tensor([dev_ms, my_bytes, cb, pb, statistics.mean(count_ms), statistics.mean(push_ms)],
                      dtype=torch.float64, device=dev)
@@ -376,6 +389,37 @@ def run_ours(args):
     count_k = statistics.mean(count_ms)
     push_gbs = pb / (push_k / 1000) / 1e9
     count_gbs = cb / (count_k / 1000) / 1e9
+
+    # ---- probe latency: host clock around the public call, >= 50 warm reps ----
+    def _stats(xs):
+        xs = sorted(xs)
+        return {"min": round(xs[0], 4), "median": round(statistics.median(xs), 4),
+                "p99": round(xs[min(len(xs) - 1, int(0.99 * len(xs)))], 4), "reps": len(xs)}
+    ctx.enable_timing(False)
+    for _ in range(5):
+        table.count(prog)
+    count_probe = []
+    for _ in range(max(50, args.steps)):
+        t0 = time.perf_counter()
+        table.count(prog)
+        count_probe.append(1000 * (time.perf_counter() - t0))
+    count_probe_stats = _stats(count_probe)
+
+    # ---- read-only streaming reference measured in this run (SURVEY §8(d) peak iii) ----
+    read_peak = None
+    if world == 1 and not args.no_read_peak:
+        buf = torch.ones(1 << 31, dtype=torch.float32, device=dev)   # 8 GiB
+        for _ in range(3):
+            buf.sum()
+        ra, rb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ra.record()
+        for _ in range(5):
+            buf.sum()
+        rb.record()
+        torch.cuda.synchronize()
+        read_peak = round(5 * buf.numel() * 4 / (ra.elapsed_time(rb) / 1000) / 1e9, 1)
+        del buf
+        torch.cuda.empty_cache()
 
     # ---- e2e: the same step through the public API from pinned host buffers ----
     e2e = None
@@ -478,12 +522,13 @@ def run_ours(args):
         kept, budget = set(), 8
         if os.environ.get("SEL_KEEP_VALUES", "1") != "0":
             for j in proj:
-                if j in pc and j not in kept and w_all[j] <= budget:
+                if j in pc and j not in kept and j not in consts and w_all[j] <= budget:
                     kept.add(j)
                     budget -= w_all[j]
         pb_sector = (T.n_rows // 8 + 2 * ((T.n_rows + 1023) // 1024)
                      + sum(local_count * w_all[j] for j in kept)
-                     + sum(32 * sectors(w_all[j]) for j in set(proj) if j not in kept) + write_b)
+                     + sum(32 * sectors(w_all[j]) for j in set(proj) if j not in kept and j not in consts)
+                     + write_b)
     else:
         pb_sector = (T.n_rows * sum(w_all[j] for j in pc)
                      + sum(32 * sectors(w_all[j]) for j in set(proj) if j not in pc) + write_b)
@@ -499,6 +544,10 @@ def run_ours(args):
                  "sector_bytes_per_launch": int(pb_sector),
                  "achieved_sector": round(push_sector_gbs, 2),
                  "frac_sector": round(push_sector_gbs / hbm, 4)}
+    for r in (roof_count, roof_push):   # the same achieved rate against SURVEY §8(d)'s other peaks
+        r["frac_nominal_8tbs"] = round(r["achieved"] / 8000.0, 4)
+        if read_peak:
+            r["frac_read_stream"] = round(r["achieved"] / read_peak, 4)
     roof_dom = roof_push if push_k >= count_k else roof_count
     if rank == 0:
         line = {
@@ -515,8 +564,12 @@ def run_ours(args):
                                                  ", prepared once and replayed as a CUDA graph"))},
             "latency_ms": {"execute_median": round(statistics.median(count_lat), 4),
                            "execute_min": round(min(count_lat), 4),
+                           "execute_p99": _stats(count_lat)["p99"],
+                           "count_probe": count_probe_stats,
                            "count_kernel": round(count_k, 4), "pushdown_kernels": round(push_k, 4)},
             "roofline": roof_dom,
+            "read_stream_gbs": read_peak,
+            "read_stream_note": "torch float32 sum over 8 GiB, this run (SURVEY 8(d) peak iii)",
             "roofline_kernels": {"count_kernel": roof_count, push_name: roof_push},
             "pushdown_path": pd_path,
             "clocks": clk.summary(),

@@ -714,14 +714,49 @@ void record(sel_ctx c, cudaEvent_t ev, cudaStream_t s) {
   else cudaEventRecord(ev, s);
 }
 
+// Columns whose value is the same in every selected row: in a conjunction of leaves, a leaf whose
+// key-space set is one point {k} pins its column to the single raw bit pattern that maps to k
+// (exact: the key maps are bijections, and -0/+0 are two keys so x = 0.0 is never a point).
+// Returns (column, raw bits) pairs; the push-down fills them instead of keeping or gathering.
+std::vector<std::pair<int, uint64_t>> const_columns(sel_table t, const Plan& plan) {
+  std::vector<std::pair<int, uint64_t>> out;
+  if (plan.path != PATH_CONJ) return out;
+  for (const PlanLeaf& L : plan.leaves) {
+    if (L.bitmap >= 0 || L.iv.size() != 1 || L.iv[0].lo != L.iv[0].hi) continue;
+    const int type = t->types[L.col];
+    const uint64_t k = L.iv[0].lo;
+    uint64_t raw;
+    if (type == SEL_FLOAT32) {
+      const uint32_t x = (uint32_t)k;
+      raw = (x & 0x80000000u) ? (x ^ 0x80000000u) : (~x & 0xFFFFFFFFu);
+    } else {
+      const int w = width_of(type);
+      raw = (k ^ key_sign_bias(type)) & (w == 8 ? ~0ull : ((1ull << (8 * w)) - 1));
+    }
+    out.emplace_back(L.col, raw);
+  }
+  return out;
+}
+
+bool is_const_col(const std::vector<std::pair<int, uint64_t>>& cc, int col, uint64_t* raw) {
+  for (auto& x : cc)
+    if (x.first == col) {
+      if (raw) *raw = x.second;
+      return true;
+    }
+  return false;
+}
+
 // The projected predicate columns whose selected values a keeping count stores (<= kMaxKeep,
 // within the warp's capture budget) with their shared-memory capture offsets; *off advances.
 std::vector<std::pair<int, uint32_t>> choose_kept(sel_table t, const Plan& plan,
                                                   const uint32_t* keep_cols, uint32_t nkeep,
                                                   uint32_t* off) {
   std::vector<std::pair<int, uint32_t>> chosen;
+  const auto consts = const_columns(t, plan);   // filled by the push-down, never kept
   for (uint32_t j = 0; j < nkeep && (int)chosen.size() < kMaxKeep; ++j) {
     const int col = (int)keep_cols[j];
+    if (is_const_col(consts, col, nullptr)) continue;
     bool pred_col = false, dup = false;
     for (auto& L : plan.leaves) pred_col = pred_col || L.col == col;
     for (auto& ck : chosen) dup = dup || ck.first == col;
@@ -852,10 +887,12 @@ sel_status enqueue_count(sel_table t, const Plan& plan, uint32_t flags, const ui
 // Enqueue the materialisation from the kept selection (pushdown_sel): every
 // projection gathered from global memory or copied from its kept-value slot. gate: write nothing
 // when the global count in Scratch::result[kGateSlot] exceeds gate_max (sel_execute).
-sel_status enqueue_pushdown_sel(sel_table t, const uint32_t* proj_cols, uint32_t nproj,
-                                uint32_t* out_rowids, void* const* out_cols, uint64_t capacity_rows,
-                                bool gate, uint64_t gate_max, cudaStream_t stream) {
+sel_status enqueue_pushdown_sel(sel_table t, const Plan& plan, const uint32_t* proj_cols,
+                                uint32_t nproj, uint32_t* out_rowids, void* const* out_cols,
+                                uint64_t capacity_rows, bool gate, uint64_t gate_max,
+                                cudaStream_t stream) {
   sel_ctx c = t->ctx;
+  const auto consts = const_columns(t, plan);
   const uint64_t n = t->local_rows;
   const uint64_t ntiles = (n + kChunkRows - 1) / kChunkRows;
   auto fill_sel = [&](auto* p) {
@@ -870,8 +907,15 @@ sel_status enqueue_pushdown_sel(sel_table t, const uint32_t* proj_cols, uint32_t
       p->proj_dst[j] = out_cols[j];
       p->proj_wclass[j] = wclass_of(t->types[proj_cols[j]]);
       p->proj_cap_off[j] = kNoCapture;
-      for (size_t k = 0; k < c->kept_cols.size(); ++k)
-        if (c->kept_cols[k] == (int)proj_cols[j]) p->proj_cap_off[j] = (uint16_t)(kKeptBase + k);
+      uint64_t raw = 0;
+      if (is_const_col(consts, (int)proj_cols[j], &raw)) {
+        p->proj_cap_off[j] = kConstProj;
+        p->proj_src[j] = reinterpret_cast<const void*>((uintptr_t)raw);
+      } else {
+        for (size_t k = 0; k < c->kept_cols.size(); ++k)
+          if (c->kept_cols[k] == (int)proj_cols[j]) p->proj_cap_off[j] = (uint16_t)(kKeptBase + k);
+      }
+      if (p->proj_cap_off[j] != kNoCapture) ++p->n_direct;
     }
   };
   const uint64_t nblocks = (ntiles + kSelBlockChunks - 1) / kSelBlockChunks;
@@ -986,9 +1030,18 @@ uint64_t sel_pushdown(sel_table t, const void* prog, size_t prog_bytes, const ui
       // (no second read from HBM); the rest are gathered from global memory at write-out.
       std::vector<int> cap_off(t->cols.size(), -1);
       uint32_t off = kIdxBytes;
+      const auto consts = const_columns(t, plan);
       for (uint32_t j = 0; j < p->n_proj; ++j) {
         const int c = (int)proj_cols[j];
         const uint32_t w = (uint32_t)width_of(t->types[c]);
+        uint64_t raw = 0;
+        if (is_const_col(consts, c, &raw)) {   // a fill: no capture, no gather
+          p->proj_src[j] = reinterpret_cast<const void*>((uintptr_t)raw);
+          p->proj_dst[j] = out_cols[j];
+          p->proj_wclass[j] = wclass_of(t->types[c]);
+          p->proj_cap_off[j] = kConstProj;
+          continue;
+        }
         bool pred_col = false;
         for (auto& L : plan.leaves) pred_col = pred_col || L.col == c;
         if (pred_col && cap_off[c] < 0 && off + w * kChunkRows <= kIdxBytes + kCaptureBudget) {
@@ -1019,8 +1072,8 @@ uint64_t sel_pushdown(sel_table t, const void* prog, size_t prog_bytes, const ui
     if (c->timing) cudaEventRecord(c->ev0, stream);
     int le, grid;
     if (from_sel) {
-      if (enqueue_pushdown_sel(t, proj_cols, nproj, out_rowids, out_cols, capacity_rows, false, 0,
-                               stream) != SEL_OK)
+      if (enqueue_pushdown_sel(t, plan, proj_cols, nproj, out_rowids, out_cols, capacity_rows, false,
+                               0, stream) != SEL_OK)
         return SEL_ERR;
       le = cudaSuccess;
     } else if (fits_block<DevProgramSmall>(plan, nslots, nproj)) {
@@ -1299,8 +1352,8 @@ uint64_t sel_execute(sel_table t, const void* prog, size_t prog_bytes, const uin
                     c->s.result + kGateSlot) != SEL_OK)
     return SEL_ERR;
   if (c->timing) cudaEventRecord(c->ev2, stream);
-  if (enqueue_pushdown_sel(t, proj_cols, nproj, out_rowids, out_cols, capacity_rows, true, max_size,
-                           stream) != SEL_OK)
+  if (enqueue_pushdown_sel(t, plan, proj_cols, nproj, out_rowids, out_cols, capacity_rows, true,
+                           max_size, stream) != SEL_OK)
     return SEL_ERR;
   if (c->timing) cudaEventRecord(c->ev3, stream);
   cudaError_t e = cudaMemcpyAsync(c->h_result + kGateSlot, c->s.result + kGateSlot,
@@ -1372,7 +1425,8 @@ sel_status capture_prepared(sel_prepared q) {
   sel_status st = enqueue_count(t, plan, SEL_KEEP_SELECTION, proj, nkeep, s, c->s.result + kGateSlot);
   if (st == SEL_OK && c->timing) record(c, c->ev2, s);
   if (st == SEL_OK)
-    st = enqueue_pushdown_sel(t, proj, nproj, q->out_rowids, outs, q->capacity, true, q->max_size, s);
+    st = enqueue_pushdown_sel(t, plan, proj, nproj, q->out_rowids, outs, q->capacity, true,
+                              q->max_size, s);
   if (st == SEL_OK && c->timing) record(c, c->ev3, s);
   if (st == SEL_OK) {
     e = cudaMemcpyAsync(c->h_result + kGateSlot, c->s.result + kGateSlot, sizeof(uint64_t),

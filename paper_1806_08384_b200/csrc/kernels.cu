@@ -395,6 +395,26 @@ __device__ __forceinline__ void copy_slot(const void* slot_v, void* dst_v, uint6
   for (uint32_t q = lane; q < lim; q += 32) dst[q] = src[q];
 }
 
+// Output positions [gbase, gbase + lim) of a constant projection receive its value.
+template <class T>
+__device__ __forceinline__ void fill_const(uint64_t bits, void* dst_v, uint64_t gbase, uint32_t lim,
+                                           int lane) {
+  T* __restrict__ dst = static_cast<T*>(dst_v) + gbase;
+  const T v = (T)bits;
+#pragma unroll 4
+  for (uint32_t q = lane; q < lim; q += 32) dst[q] = v;
+}
+__device__ __forceinline__ void fill_proj(uint8_t wclass, const void* bits, void* dst, uint64_t gbase,
+                                          uint32_t lim, int lane) {
+  const uint64_t b = (uint64_t)(uintptr_t)bits;
+  switch (wclass) {
+    case W1: fill_const<uint8_t>(b, dst, gbase, lim, lane); break;
+    case W2: fill_const<uint16_t>(b, dst, gbase, lim, lane); break;
+    case W4: fill_const<uint32_t>(b, dst, gbase, lim, lane); break;
+    default: fill_const<uint64_t>(b, dst, gbase, lim, lane); break;
+  }
+}
+
 // proj_cap_off >= kKeptBase: projection j comes from kept slot (proj_cap_off - kKeptBase).
 template <class P>
 __device__ __forceinline__ void write_out(const P& p, uint64_t cbase, uint64_t gbase, uint32_t cnt,
@@ -409,7 +429,9 @@ __device__ __forceinline__ void write_out(const P& p, uint64_t cbase, uint64_t g
 #pragma unroll 1
   for (uint32_t j = 0; j < p.n_proj; ++j) {
     const uint16_t co = p.proj_cap_off[j];
-    if (kept && co != kNoCapture) {
+    if (co == kConstProj) {
+      fill_proj(p.proj_wclass[j], p.proj_src[j], p.proj_dst[j], gbase, lim, lane);
+    } else if (kept && co != kNoCapture) {
       const void* slot = kept->keep_slot[co - kKeptBase];
       switch (p.proj_wclass[j]) {
         case W1: copy_slot<uint8_t>(slot, p.proj_dst[j], cbase, gbase, lim, lane); break;
@@ -794,6 +816,10 @@ __device__ __forceinline__ void copy_kept(const P& p, const SelectionBufs& sb, u
   for (uint32_t j = 0; j < p.n_proj; ++j) {
     const uint16_t co = p.proj_cap_off[j];
     if (co == kNoCapture) continue;
+    if (co == kConstProj) {
+      fill_proj(p.proj_wclass[j], p.proj_src[j], p.proj_dst[j], pos, lim, lane);
+      continue;
+    }
     const void* slot = sb.keep_slot[co - kKeptBase];
     switch (p.proj_wclass[j]) {
       case W1: copy_slot<uint8_t>(slot, p.proj_dst[j], c * kChunkRows, pos, lim, lane); break;
@@ -864,7 +890,7 @@ __global__ void __launch_bounds__(kThreads, SEL_PD_MINB) pushdown_sel_kernel(con
         gbase += staged;
         staged = 0;
       }
-      if (sb.n_keep) copy_kept(p, sb, c0 + g, gbase + staged, cg, lane);
+      if (p.n_direct) copy_kept(p, sb, c0 + g, gbase + staged, cg, lane);  // kept / constant
       stage_rows_rm(m[g], lane, my, staged, (uint32_t)g * kChunkRows);
       staged += cg;
     }

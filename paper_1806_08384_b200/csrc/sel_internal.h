@@ -26,6 +26,9 @@ constexpr uint32_t kCaptureBudget = 8 * kChunkRows;     // <= 8 bytes/row of cap
 constexpr uint32_t kMaxPushdownSmem = kWarpsPerCta * (kIdxBytes + kCaptureBudget);  // 80 KB
 constexpr uint16_t kNoCapture = 0xFFFF;
 constexpr uint16_t kKeptBase = 0xFF00;  // push-down from a selection: proj_cap_off = kKeptBase + slot
+// proj_cap_off = kConstProj: every selected row has the same value in this column (the
+// conjunction pins it with a single-value leaf), raw bits in (uintptr_t)proj_src: a fill.
+constexpr uint16_t kConstProj = 0xFFFE;
 constexpr int kMaxDeviceStack = 32;
 
 enum WidthClass : uint8_t { W1 = 0, W2 = 1, W4 = 2, W8 = 3 };
@@ -63,6 +66,7 @@ struct DevProgramT {
   uint32_t bm_bytes;     // IN_BITMAP key sets: total bytes (16-byte aligned each)
   uint32_t bm_smem;      // count kernel: bytes of the sets staged in shared memory (leaves with
                          // kLeafStaged; offset = span[iv_begin] >> 32), 0 = none
+  uint32_t n_direct;     // push-down from a selection: projections that are kept or constant
   uint64_t row_offset;   // global id of local row 0 (push-down ids)
   uint64_t capacity;     // push-down capacity in rows
   uint64_t gate_max;

@@ -340,3 +340,47 @@ def test_execute_gate(ctx):
         assert r.materialized and c_ms > 0 and p_ms > 0
     finally:
         ctx.enable_timing(False)
+
+
+def test_constant_projections(ctx):
+    """A conjunction pins a column with a single-value leaf: the push-down fills that projection
+    instead of keeping or gathering it. Every type (negative INT32/INT64, FLOAT32 of either sign,
+    DICT8/16 codes) through execute, both push-down paths and a prepared execute; x = 0.0 is two
+    keys (-0, +0) and must still gather the real bits."""
+    n = 300_017
+    rng = np.random.default_rng(8)
+    a = rng.choice(np.array([-5, 3, 7], dtype=np.int32), n)
+    b = rng.choice(np.array([-(2**40), 1, 2**50], dtype=np.int64), n)
+    f = rng.choice(np.array([-1.5, 1.5, 0.0, -0.0], dtype=np.float32), n)
+    d8 = rng.integers(0, 4, n).astype(np.uint8)
+    d16 = rng.choice(np.array([0, 65535], dtype=np.uint16), n)
+    cols = [a, b, f, d8, d16]
+    types = [INT32, INT64, FLOAT32, DICT8, DICT16]
+    t = register(ctx, cols, types)
+    progs = [
+        And(And(Cmp("=", 0, -5), Cmp("=", 1, -(2**40))), Cmp("=", 2, -1.5)),
+        And(And(Cmp("=", 2, 1.5), Cmp("=", 4, 65535)), Cmp("<", 3, 3)),
+        And(Cmp("=", 2, 0.0), Cmp("=", 3, 2)),                     # f: -0 and +0 both selected
+        And(In(0, (7,)), Between(1, 1, 1)),
+    ]
+    proj = [0, 1, 2, 3, 4]
+    for node in progs:
+        plan = sel.program_plan(encode(node, types), types)
+        assert plan["path"] == 1
+        check_parity(t, cols, types, node, proj=proj)
+        prog = encode(node, types)
+        want_c, want_ids, want_cols = oracle.pushdown(cols, types, prog, proj=proj)
+        for r in (t.execute(prog, project=proj, max_size=n),):
+            assert r.materialized and r.count == want_c
+            for j in proj:
+                np.testing.assert_array_equal(r.columns[j].cpu().numpy().view(want_cols[j].dtype), want_cols[j])
+        q = t.prepare_execute(prog, project=proj, max_size=n)
+        assert q.run() == want_c
+        res = q.result()
+        for j in proj:
+            np.testing.assert_array_equal(res.columns[j].cpu().numpy().view(want_cols[j].dtype), want_cols[j])
+        q.release()
+    # x = 0.0 selects both zeros: the projected bits are not a constant
+    _, _, wc = oracle.pushdown(cols, types, encode(progs[2], types), proj=[2])
+    assert len(set(wc[0].view(np.uint32).tolist())) == 2
+    t.release()
