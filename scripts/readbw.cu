@@ -1,3 +1,5 @@
+// readbw.cu — read-only HBM streaming microbenchmark (LDG.128 and TMA bulk rings) behind the
+// 7,389 / 7,204 GB/s figures in DESIGN.md §6. Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 readbw.cu
 // Read-only streaming bandwidth microbenchmark (scratch, not product): how fast can a B200 stream
 // a large buffer with LDG.128 (and with cp.async.bulk into shared memory)?
 #include <cstdio>

@@ -1,3 +1,6 @@
+// Attempted minimal standalone repro of the nvcc 12.9 / sm_100a miscompile described in
+// DESIGN.md §9 (two inlined copies of the dynamic interval loop). This reduced form compiles
+// correctly; the hazard only reproduced inside the full kernel. Kept as the record of the attempt.
 #include <stdint.h>
 struct Leaf { uint8_t slot, wclass, fkey, pad; uint16_t iv_begin, iv_count; };
 struct P { uint32_t n_leaves; Leaf leaf[4]; const void* col[4]; uint64_t lo[8]; uint64_t span[8]; };
