@@ -25,7 +25,7 @@ EXPORTS = ["sel_ctx_create", "sel_ctx_set_comm", "sel_nccl_unique_id", "sel_ctx_
            "sel_ctx_last_times", "sel_count_batch", "sel_count_sampled",
            "sel_bitmap_register", "sel_bitmap_release",
            "sel_prepare_execute", "sel_prepared_execute", "sel_prepared_release",
-           "sel_ctx_last_pushdown_path", "sel_program_check",
+           "sel_ctx_last_pushdown_path", "sel_ctx_set_pushdown_path", "sel_program_check",
            "sel_program_path", "sel_program_plan_json", "sel_last_error",
            "sel_last_error_message", "sel_abi_version"]
 
@@ -78,6 +78,7 @@ def lib() -> ctypes.CDLL:
         "sel_prepared_release": (None, [vp]),
         "sel_ctx_last_times": (i32, [vp, ctypes.POINTER(ctypes.c_float), ctypes.POINTER(ctypes.c_float)]),
         "sel_ctx_last_pushdown_path": (i32, [vp]),
+        "sel_ctx_set_pushdown_path": (i32, [vp, i32]),
         "sel_pushdown": (u64, [vp, ctypes.c_char_p, sz, vp, u32, vp, vp, u64,
                                ctypes.POINTER(u64), ctypes.POINTER(u64), vp]),
         "sel_program_check": (i32, [ctypes.c_char_p, sz, vp, u32]),

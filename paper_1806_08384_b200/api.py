@@ -64,8 +64,14 @@ class Context:
         return float(c.value), float(p.value)
 
     def last_pushdown_path(self) -> int:
-        """1: the last pushdown materialised from a kept selection; 0: single pass; -1: none."""
+        """1: the last pushdown materialised from a kept selection; 2: two passes inside the call
+        (keeping count, then 1's materialisation); 0: single pass; -1: none."""
         return int(lib().sel_ctx_last_pushdown_path(self._h))
+
+    def set_pushdown_path(self, mode: int) -> None:
+        """Path of a pushdown without a matching kept selection: -1 automatic (two passes at
+        >= 2^22 local rows), 0 always the single pass, 2 always two passes (include/sel.h)."""
+        check(lib().sel_ctx_set_pushdown_path(self._h, int(mode)))
 
     def register_bitmap(self, words: torch.Tensor, nbits: int) -> int:
         """Register a key set for IN_BITMAP leaves (selgen.InSet): `words` is a device tensor of

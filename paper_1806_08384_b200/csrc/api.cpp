@@ -142,6 +142,9 @@ struct sel_ctx_s {
   uint64_t slot_cap[kMaxKeep] = {};  // bytes allocated per slot
   int last_pd_path = -1;
   bool force_single = false;
+  // sel_pushdown without a kept selection: two passes (keeping count -> materialise from it) at
+  // >= two_pass_min_rows local rows, else the single pass (SEL_PUSHDOWN_PATH=single|two forces)
+  uint64_t two_pass_min_rows = 1ull << 22;
   int prefetch_mode = -1;   // -1 auto, 0 off, 1 on
   bool keep_values = true;
   float last_count_ms = 0.f, last_push_ms = 0.f;
@@ -426,6 +429,10 @@ sel_status sel_ctx_create(int cuda_device, sel_ctx* out) {
   c->count_nw = cnw ? std::atoi(cnw) : 0;
   const char* pp = std::getenv("SEL_PUSHDOWN_PATH");
   c->force_single = pp && std::strcmp(pp, "single") == 0;
+  if (pp && std::strcmp(pp, "two") == 0) c->two_pass_min_rows = 0;
+  const char* tpm = std::getenv("SEL_TWO_PASS_MIN_ROWS");
+  if (tpm && !c->force_single && !(pp && std::strcmp(pp, "two") == 0))
+    c->two_pass_min_rows = std::strtoull(tpm, nullptr, 10);
   const char* env = std::getenv("SEL_CTAS_PER_SM");
   if (env && std::atoi(env) > 0) {
     const int v = std::atoi(env);
@@ -534,6 +541,15 @@ sel_status sel_ctx_set_timing(sel_ctx ctx, int enable) {
   if (!ctx) return set_error(SEL_E_ARG, "null ctx");
   ctx->timing = enable != 0;
   ctx->last_ms = 0.f;
+  return SEL_OK;
+}
+
+sel_status sel_ctx_set_pushdown_path(sel_ctx ctx, int mode) {
+  clear_error();
+  if (!ctx) return set_error(SEL_E_ARG, "null ctx");
+  if (mode != -1 && mode != 0 && mode != 2) return set_error(SEL_E_ARG, "mode must be -1, 0 or 2");
+  ctx->force_single = mode == 0;
+  ctx->two_pass_min_rows = mode == 2 ? 0 : (mode == 0 ? ~0ull : (1ull << 22));
   return SEL_OK;
 }
 
@@ -785,7 +801,8 @@ sel_status reserve_selection(sel_table t, uint64_t nchunks,
 // (keeping the selection with SEL_KEEP_SELECTION) writes the local count to *d_out, then the
 // 8-byte all-reduce makes it global in place. Nothing waits for the host.
 sel_status enqueue_count(sel_table t, const Plan& plan, uint32_t flags, const uint32_t* keep_cols,
-                         uint32_t nkeep, cudaStream_t stream, uint64_t* d_out) {
+                         uint32_t nkeep, cudaStream_t stream, uint64_t* d_out,
+                         bool allreduce = true) {
   sel_ctx c = t->ctx;
   const uint64_t n = t->local_rows;
   const bool scan = n > 0 && plan.path != PATH_CONST;
@@ -877,7 +894,7 @@ sel_status enqueue_count(sel_table t, const Plan& plan, uint32_t flags, const ui
     e = cudaMemcpyAsync(d_out, h, sizeof(uint64_t), cudaMemcpyHostToDevice, stream);
     if (e != cudaSuccess) return set_error(SEL_E_CUDA, cuda_msg("cudaMemcpyAsync", e));
   }
-  if (c->comm) {  // one 8-byte all-reduce on the probe stream
+  if (c->comm && allreduce) {  // one 8-byte all-reduce on the probe stream
     ncclResult_t r = nccl().AllReduce(d_out, d_out, 1, ncclUint64, ncclSum, c->comm, stream);
     if (r != ncclSuccess) return set_error(SEL_E_NCCL, nccl_msg("ncclAllReduce", r));
   }
@@ -1012,6 +1029,7 @@ uint64_t sel_pushdown(sel_table t, const void* prog, size_t prog_bytes, const ui
   const bool scan = n > 0 && !(plan.path == PATH_CONST && !plan.const_value);
   c->last_pd_path = -1;
   cudaError_t e;
+  bool two_pass = false;
   if (scan) {
     const uint64_t ntiles = (n + kChunkRows - 1) / kChunkRows;
     if (ensure_status(c, ntiles, stream) != SEL_OK) return SEL_ERR;
@@ -1069,9 +1087,25 @@ uint64_t sel_pushdown(sel_table t, const void* prog, size_t prog_bytes, const ui
     const bool from_sel = !c->force_single && c->kept_table == t &&
                           c->kept_prog.size() == prog_bytes &&
                           std::memcmp(c->kept_prog.data(), prog, prog_bytes) == 0;
+    // No kept selection: large shards take two passes — the count keeping the selection and the
+    // projected predicate columns' values, then the materialisation from it (Algorithm 1's
+    // count-then-execute order, without the gate) — instead of the single
+    // pass, whose decoupled look-back waits dominate at this size.
+    two_pass = !from_sel && !c->force_single && n >= c->two_pass_min_rows &&
+               plan.path != PATH_CONST;  // TRUE runs no count kernel: nothing would be kept
     if (c->timing) cudaEventRecord(c->ev0, stream);
     int le, grid;
-    if (from_sel) {
+    if (two_pass) {
+      if (enqueue_count(t, plan, SEL_KEEP_SELECTION, proj_cols, c->keep_values ? nproj : 0u, stream,
+                        c->s.result + kGateSlot, false) != SEL_OK)
+        return SEL_ERR;
+      if (c->timing) cudaEventRecord(c->ev2, stream);
+      if (enqueue_pushdown_sel(t, plan, proj_cols, nproj, out_rowids, out_cols, capacity_rows, false,
+                               0, stream) != SEL_OK)
+        return SEL_ERR;
+      c->last_pd_path = 2;
+      le = cudaSuccess;
+    } else if (from_sel) {
       if (enqueue_pushdown_sel(t, plan, proj_cols, nproj, out_rowids, out_cols, capacity_rows, false,
                                0, stream) != SEL_OK)
         return SEL_ERR;
@@ -1089,7 +1123,7 @@ uint64_t sel_pushdown(sel_table t, const void* prog, size_t prog_bytes, const ui
                       occupancy_pushdown_large((size_t)p.warp_smem * kWarpsPerCta));
       le = launch_pushdown_large(p, n, out_rowids, grid, c->s, c->ticket_base, c->epoch, stream);
     }
-    if (!from_sel) {
+    if (!from_sel && !two_pass) {
       if (le != cudaSuccess) {
         cudaMemsetAsync(c->s.ticket, 0, sizeof(unsigned long long), stream);
         c->ticket_base = 0;
@@ -1130,6 +1164,14 @@ uint64_t sel_pushdown(sel_table t, const void* prog, size_t prog_bytes, const ui
   if (scan && c->timing) {
     cudaEventElapsedTime(&c->last_ms, c->ev0, c->ev1);
     c->last_push_ms = c->last_ms;
+    if (two_pass) {  // last_times: (keeping count, materialisation); last_ms: the whole call
+      cudaEventElapsedTime(&c->last_count_ms, c->ev0, c->ev2);
+      cudaEventElapsedTime(&c->last_push_ms, c->ev2, c->ev1);
+    }
+  }
+  if (two_pass) {  // the selection this call kept serves a following push-down of the program
+    c->kept_table = t;
+    c->kept_prog.assign(static_cast<const char*>(prog), prog_bytes);
   }
   if (out_local_count) *out_local_count = local;
   if (out_global_offset) *out_global_offset = offset;

@@ -55,7 +55,8 @@ def check_parity(table, cols, types, node, proj=None, capacity=None, row_offset=
        kept  — count keeping the selection AND the projected predicate columns' values, then
                push-down (Algorithm 1's order; what sel_execute does);
        sel   — count keeping only the selection, push-down gathers every projected column;
-       single— no kept selection: single pass (evaluate + decoupled look-back)."""
+       single— no kept selection: single pass (evaluate + decoupled look-back);
+       two   — no kept selection: two passes inside the call (keeping count, then materialise)."""
     prog = encode(node, types)
     proj = proj or []
     want_count, want_ids, want_cols = oracle.pushdown(cols, types, prog, proj=proj,
@@ -64,18 +65,23 @@ def check_parity(table, cols, types, node, proj=None, capacity=None, row_offset=
     cap = want_count if capacity is None else capacity
     n = table.local_rows
     const = sel.program_path(prog, types) == 2
-    for mode in ("kept", "sel", "single"):
+    for mode in ("kept", "sel", "single", "two"):
         if mode == "kept":
             assert table.count(prog, keep_selection=True, keep_columns=proj) == want_count
         elif mode == "sel":
             assert table.count(prog, keep_selection=True) == want_count
         else:
             _invalidate_selection(table)
-        res = table.pushdown(prog, project=proj, capacity=cap)
+            table.ctx.set_pushdown_path(0 if mode == "single" else 2)
+        try:
+            res = table.pushdown(prog, project=proj, capacity=cap)
+        finally:
+            table.ctx.set_pushdown_path(-1)
         path = table.ctx.last_pushdown_path()
         if n > 0 and want_count > 0:
             # a program folded to a constant never launches the count kernel, so nothing is kept
-            assert path == (0 if mode == "single" or const else 1), (mode, path)
+            want_path = 0 if mode == "single" or const else (2 if mode == "two" else 1)
+            assert path == want_path, (mode, path)
         assert res.count == want_count and res.local_count == want_count
         got_ids = res.rowids.cpu().numpy().view(np.uint32)
         np.testing.assert_array_equal(got_ids, want_ids, err_msg=f"{mode} {node}")
@@ -144,15 +150,19 @@ def test_capacity_gate(ctx):
     prog = encode(node, types)
     full = oracle.count(cols, types, prog)
     for cap in [0, 1, 17, 8191, full // 2, full, full + 100]:
-        for keep in (True, False):
-            if keep:
+        for path in (1, 0, 2):
+            if path == 1:
                 t.count(prog, keep_selection=True)
             else:
                 _invalidate_selection(t)
+                ctx.set_pushdown_path(path)
             sentinel = torch.full((max(cap, 1) + 64,), -7, dtype=torch.int32, device=ctx.device)
             outc = torch.full((max(cap, 1) + 64,), 99, dtype=torch.uint8, device=ctx.device)
-            res = t.pushdown(prog, project=[1], capacity=cap, out=(sentinel, [outc]))
-            assert ctx.last_pushdown_path() == (1 if keep else 0)
+            try:
+                res = t.pushdown(prog, project=[1], capacity=cap, out=(sentinel, [outc]))
+            finally:
+                ctx.set_pushdown_path(-1)
+            assert ctx.last_pushdown_path() == path
             assert res.count == full and res.local_count == full
             assert res.gated == (full > cap)
             # nothing written past the capacity
@@ -277,13 +287,21 @@ def test_full_size_worked_example(ctx):
     cc = res.columns["C"]
     assert bool(((cc == 1) | (cc == 4)).all())
     assert torch.equal(res.columns["D"], T.col("D").data[got])
-    # the single pass (no kept selection) gives the same bytes
-    _invalidate_selection(t)
-    res2 = t.pushdown(encode(node, T.types), project=["A", "C", "D"], capacity=want_n)
-    assert ctx.last_pushdown_path() == 0
-    assert torch.equal(res2.rowids, res.rowids)
-    for k in "ACD":
-        assert torch.equal(res2.columns[k], res.columns[k])
+    # a plain sel_pushdown (no kept selection) gives the same bytes: at this size it takes two
+    # passes by default (2); forced, the single pass (0)
+    for mode, want_path in ((-1, 2), (0, 0)):
+        _invalidate_selection(t)
+        ctx.set_pushdown_path(mode)
+        try:
+            res2 = t.pushdown(encode(node, T.types), project=["A", "C", "D"], capacity=want_n)
+        finally:
+            ctx.set_pushdown_path(-1)
+        assert ctx.last_pushdown_path() == want_path
+        assert res2.count == want_n
+        assert torch.equal(res2.rowids, res.rowids)
+        for k in "ACD":
+            assert torch.equal(res2.columns[k], res.columns[k])
+        del res2
     # the complement partitions the table (count(P) + count(NOT P) = N)
     assert t.count(encode(Not(node), T.types)) == 600_000_000 - 100_200_000
 
