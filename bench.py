@@ -517,10 +517,10 @@ def run_ours(args):
         return int(torch.unique_consecutive(ids64 // (32 // width)).numel())
     write_b = local_count * (4 + sum(w_all[j] for j in proj))
     if pd_path == 1:
-        # projected predicate columns whose values the count kept (sel_execute's default, within
+        # projected predicate columns whose values the count kept (SEL_KEEP_VALUES=1, within
         # 8 B/row) are copied contiguously from their slots: count x width, not sectors
         kept, budget = set(), 8
-        if os.environ.get("SEL_KEEP_VALUES", "1") != "0":
+        if os.environ.get("SEL_KEEP_VALUES", "0") == "1":
             for j in proj:
                 if j in pc and j not in kept and j not in consts and w_all[j] <= budget:
                     kept.add(j)

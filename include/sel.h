@@ -150,8 +150,8 @@ uint64_t sel_count_ex(sel_table table, const void* prog, size_t prog_bytes, uint
                       const uint32_t* keep_cols, uint32_t nkeep, void* cuda_stream);
 
 /* sel_execute: Algorithm 1's Execute(compound, isSPD = true, maxSize) in one
- * call: count with SEL_KEEP_SELECTION and the projected predicate columns' values (environment
- * SEL_KEEP_VALUES=0: the selection only), then if the
+ * call: count with SEL_KEEP_SELECTION (environment SEL_KEEP_VALUES=1: also keeping the projected
+ * predicate columns' values, as sel_count_ex's keep_cols), then if the
  * GLOBAL count > max_size "throw" — *out_materialized = 0, nothing is written, *out_local_count
  * and *out_global_offset are set to 0 — else materialise exactly like sel_pushdown (from the kept
  * selection) and set *out_materialized = 1. Returns the global count or SEL_ERR. Arguments as
@@ -261,7 +261,11 @@ int sel_program_path(const void* prog, size_t prog_bytes, const sel_type* types,
 /* The canonical plan the device would execute, as JSON, for host-side inspection and tests:
  *   {"path": p, "const": b, "max_depth": d,
  *    "ops": [[opcode, arg], ...],              opcode 0 = leaf(arg), 1 = AND, 2 = OR (postfix)
- *    "leaves": [{"col": c, "wclass": w, "fkey": f, "lo": [...], "span": [...]}, ...]}
+ *    "leaves": [{"col": c, "wclass": w, "fkey": f, "lo": [...], "span": [...]}, ...],
+ *    "fast": [k, ...]}                          the count kernel's fast-path leaf kinds, one per
+ *                                               leaf (0 point/4 B, 1 interval/4 B, 2 <= 4
+ *                                               intervals/4 B, 3 interval/8 B, 4 <= 4 points/1 B),
+ *                                               or [] when the interpreter runs the program
  * lo/span are the packed device values: a row value v (its raw bits, zero-extended; FLOAT32
  * first mapped through the sortable key) lies in the leaf iff ((v - lo) mod 2^W) <= span for
  * some interval, W = 64 for 8-byte columns and 32 otherwise. Writes at most `cap` bytes

@@ -145,8 +145,9 @@ struct sel_ctx_s {
   // sel_pushdown without a kept selection: two passes (keeping count -> materialise from it) at
   // >= two_pass_min_rows local rows, else the single pass (SEL_PUSHDOWN_PATH=single|two forces)
   uint64_t two_pass_min_rows = 1ull << 22;
+  bool fast_enabled = true;  // count fast path (SEL_FAST=0: interpreter only)
   int prefetch_mode = -1;   // -1 auto, 0 off, 1 on
-  bool keep_values = true;
+  bool keep_values = false;  // SEL_KEEP_VALUES=1: executes also keep projected predicate values
   float last_count_ms = 0.f, last_push_ms = 0.f;
   // IN_BITMAP key sets (sel_bitmap_register): id -> device words / nbits; words null = free id
   std::vector<const uint64_t*> bm_words;
@@ -193,6 +194,53 @@ bool fits_block(const Plan& plan, size_t nslots, uint32_t nproj) {
   return plan.op.size() <= (size_t)P::kMaxOps && plan.leaves.size() <= (size_t)P::kMaxLeaves &&
          plan.n_intervals <= (size_t)P::kMaxIv && nslots <= (size_t)P::kMaxSlots &&
          nproj <= (uint32_t)P::kMaxProj;
+}
+
+// Count fast path (sel_internal.h FastKind): a conjunction of 1..4 leaves, each a point or
+// interval(s) on a 4-byte column, one interval on an 8-byte column, or up to 4 points on a
+// 1-byte column. Anything else (FLOAT32 keys, 2-byte columns, key sets, OR/NOT structure, wider
+// sets) runs the interpreter. Returns the number of fast leaves (0 = interpreter); fills kind[]
+// and, for FK_S1 leaves, the byte-replicated point keys. SEL_FAST=0 disables it (pack()).
+int fast_kinds(const Plan& plan, const int* types, uint8_t (&kind)[kMaxFastLeaves],
+               uint32_t (&pts)[kMaxFastLeaves][4], uint8_t (&npts)[kMaxFastLeaves]) {
+  if (plan.path != PATH_CONJ || plan.leaves.empty() || plan.leaves.size() > (size_t)kMaxFastLeaves)
+    return 0;
+  for (size_t i = 0; i < plan.op.size(); ++i)   // a conjunction evaluates leaves in index order
+    if (plan.op[i] == DOP_LEAF && plan.arg[i] >= plan.leaves.size()) return 0;
+  for (size_t l = 0; l < plan.leaves.size(); ++l) {
+    const PlanLeaf& L = plan.leaves[l];
+    const int type = types[L.col];
+    if (L.bitmap >= 0 || type == SEL_FLOAT32 || L.iv.empty()) return 0;
+    const uint8_t w = wclass_of(type);
+    npts[l] = 0;
+    if (w == W4) {
+      if (L.iv.size() == 1) kind[l] = L.iv[0].lo == L.iv[0].hi ? FK_E4 : FK_R4;
+      else if (L.iv.size() <= 4) kind[l] = FK_S4;
+      else return 0;
+    } else if (w == W8) {
+      if (L.iv.size() != 1) return 0;
+      kind[l] = FK_R8;
+    } else if (w == W1) {
+      uint64_t n = 0;
+      for (const Interval& x : L.iv) n += x.hi - x.lo + 1;
+      if (n > 4) return 0;
+      uint32_t k = 0;
+      for (const Interval& x : L.iv)
+        for (uint64_t v = x.lo; v <= x.hi; ++v) pts[l][k++] = (uint32_t)v * 0x01010101u;
+      npts[l] = (uint8_t)n;
+      kind[l] = FK_S1;
+    } else {
+      return 0;
+    }
+  }
+  return (int)plan.leaves.size();
+}
+
+template <class P>
+void classify_fast(const Plan& plan, const sel_table_s* t, P* p) {
+  p->fast_n = 0;
+  if (!t->ctx->fast_enabled) return;
+  p->fast_n = (uint32_t)fast_kinds(plan, t->types.data(), p->fast_kind, p->fast_pts, p->fast_npts);
 }
 
 // Plan -> kernel parameter block. TRUE (PATH_CONST with value true) packs as an empty conjunction.
@@ -251,6 +299,7 @@ void pack(const Plan& plan, const sel_table_s* t, P* p) {
       ++iv;
     }
   }
+  classify_fast(plan, t, p);
 }
 
 // Stage key sets in the count kernel's shared memory, smallest first, while they fit beside `dyn`
@@ -424,7 +473,9 @@ sel_status sel_ctx_create(int cuda_device, sel_ctx* out) {
   const char* pf = std::getenv("SEL_PREFETCH");
   c->prefetch_mode = pf ? (std::strcmp(pf, "1") == 0 ? 1 : 0) : -1;
   const char* kv = std::getenv("SEL_KEEP_VALUES");
-  c->keep_values = !(kv && std::strcmp(kv, "0") == 0);
+  c->keep_values = kv && std::strcmp(kv, "1") == 0;
+  const char* fe = std::getenv("SEL_FAST");
+  c->fast_enabled = !(fe && std::strcmp(fe, "0") == 0);
   const char* cnw = std::getenv("SEL_COUNT_NW");
   c->count_nw = cnw ? std::atoi(cnw) : 0;
   const char* pp = std::getenv("SEL_PUSHDOWN_PATH");
@@ -662,6 +713,11 @@ long sel_program_plan_json(const void* prog, size_t prog_bytes, const sel_type* 
           ", \"fkey\": " + (type == SEL_FLOAT32 ? "1" : "0") + ", \"lo\": [" + lo +
           "], \"span\": [" + sp + "]}";
   }
+  js += "], \"fast\": [";
+  uint8_t kind[kMaxFastLeaves], npts[kMaxFastLeaves];
+  uint32_t pts[kMaxFastLeaves][4];
+  const int nf = fast_kinds(plan, ty.data(), kind, pts, npts);
+  for (int l = 0; l < nf; ++l) js += (l ? ", " : "") + std::to_string(kind[l]);
   js += "]}";
   if (buf && cap > 0) {
     const size_t n = std::min(cap - 1, js.size());
@@ -869,8 +925,9 @@ sel_status enqueue_count(sel_table t, const Plan& plan, uint32_t flags, const ui
       mark_captures(&p);
       choose_bitmap_staging(&p, dyn);
       if (c->prefetch_mode < 0) p.prefetch = ((keep && keep->n_keep) || p.bm_smem) ? 1u : 0u;
-      const int occ = keep ? occupancy_count_keep_small(dyn + p.bm_smem)
-                           : (p.bm_smem ? occupancy_count_dyn_small(p.bm_smem) : c->occ_count_small);
+      int occ = keep ? occupancy_count_keep_small(dyn + p.bm_smem)
+                     : (p.bm_smem ? occupancy_count_dyn_small(p.bm_smem) : c->occ_count_small);
+      if (p.fast_n && !p.bm_smem) occ = occupancy_count_fast((int)p.fast_n, keep != nullptr, dyn);
       const int nw = pick_count_warps(c, p, dyn, occ);
       le = launch_count_small(p, n, grid_for(c, nw == kWarpsPerCta ? units : (nchunks + nw - 1) / nw,
                                              nw == kWarpsPerCta ? occ : 1), s, keep, stream, nw);
@@ -1208,7 +1265,8 @@ uint64_t sel_count_sampled(sel_table t, const void* prog, size_t prog_bytes, uin
       p.chunk_stride = stride;
       p.chunk_phase = phase;
       choose_bitmap_staging(&p, 0);
-      const int occ = p.bm_smem ? occupancy_count_dyn_small(p.bm_smem) : c->occ_count_small;
+      int occ = p.bm_smem ? occupancy_count_dyn_small(p.bm_smem) : c->occ_count_small;
+      if (p.fast_n && !p.bm_smem) occ = occupancy_count_fast((int)p.fast_n, false, 0);
       const int nw = pick_count_warps(c, p, 0, occ);
       le = launch_count_small(p, n, grid_for(c, nw == kWarpsPerCta ? units : (ns_full + nw) / nw,
                                              nw == kWarpsPerCta ? occ : 1), c->s, nullptr, stream, nw);
@@ -1367,8 +1425,8 @@ uint64_t sel_execute(sel_table t, const void* prog, size_t prog_bytes, const uin
   Plan plan;
   if (plan_for(t, prog, prog_bytes, &plan) != SEL_OK) return SEL_ERR;
   // Execute(isSPD): gamma_COUNT over the compound, keeping what the materialisation reuses: the
-  // selection and the projected predicate columns' values (SEL_KEEP_VALUES=0 keeps the selection
-  // only; DESIGN.md §6 has both measured).
+  // selection (SEL_KEEP_VALUES=1: also the projected predicate columns' values — measured equal
+  // or slower on every config).
   const uint32_t nkeep = c->keep_values ? nproj : 0u;
   const bool scan = t->local_rows > 0 && plan.path != PATH_CONST;
   if (!scan || c->force_single) {  // host-side gate: count, then (maybe) the push-down

@@ -34,6 +34,14 @@ constexpr int kMaxDeviceStack = 32;
 enum WidthClass : uint8_t { W1 = 0, W2 = 1, W4 = 2, W8 = 3 };
 enum DevOpcode : uint8_t { DOP_LEAF = 0, DOP_AND = 1, DOP_OR = 2 };
 enum Path : int { PATH_INTERP = 0, PATH_CONJ = 1, PATH_CONST = 2 };
+// Leaf kinds of the count kernel's conjunctive fast path (width in bytes, key-space test):
+//   FK_E4  4-byte column, one point           v == lo
+//   FK_R4  4-byte column, one interval        v - lo <= span
+//   FK_S4  4-byte column, 2..4 intervals      OR of the above
+//   FK_R8  8-byte column, one interval        v - lo <= span (64-bit)
+//   FK_S1  1-byte column, 1..4 points         SWAR byte compare, 4 rows per instruction group
+enum FastKind : uint8_t { FK_E4 = 0, FK_R4 = 1, FK_S4 = 2, FK_R8 = 3, FK_S1 = 4 };
+constexpr int kMaxFastLeaves = 4;
 
 struct DevLeaf {
   uint8_t slot;      // index into DevProgram::col
@@ -67,6 +75,15 @@ struct DevProgramT {
   uint32_t bm_smem;      // count kernel: bytes of the sets staged in shared memory (leaves with
                          // kLeafStaged; offset = span[iv_begin] >> 32), 0 = none
   uint32_t n_direct;     // push-down from a selection: projections that are kept or constant
+  // Count kernel fast path (template-specialised conjunctive forms): when
+  // fast_n > 0 the program is leaf 0 AND ... AND leaf fast_n-1 and leaf s has kind fast_kind[s]
+  // (FastKind); the kernel instantiated for fast_n evaluates it as straight-line code with the
+  // leaf parameters hoisted out of the chunk loop. FK_S1 compares against fast_pts[s][0..npts)
+  // (the point keys, each byte-replicated).
+  uint32_t fast_n;
+  uint8_t fast_kind[4];
+  uint8_t fast_npts[4];
+  uint32_t fast_pts[4][4];
   uint64_t row_offset;   // global id of local row 0 (push-down ids)
   uint64_t capacity;     // push-down capacity in rows
   uint64_t gate_max;
@@ -180,6 +197,7 @@ int prepare_kernels();
 int occupancy_count_small();
 int occupancy_count_large();
 int occupancy_count_keep_small(size_t dyn_smem);
+int occupancy_count_fast(int fast_n, bool keep, size_t dyn_smem);  // fast path (small block)
 int occupancy_count_keep_large(size_t dyn_smem);
 int occupancy_count_dyn_small(size_t dyn_smem);   // plain count with staged key sets
 int occupancy_count_dyn_large(size_t dyn_smem);
