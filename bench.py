@@ -43,6 +43,9 @@ def parse():
                     help="time table.execute() per step instead of the prepared (graph) execute")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=8)
+    ap.add_argument("--comm1", action="store_true",
+                    help="testing: give the N=1 context a one-rank NCCL communicator (the N>1 "
+                         "collectives on the step's critical path, without peers)")
     return ap.parse_args()
 
 
@@ -298,6 +301,8 @@ def run_ours(args):
     ctx = sel.Context(dev)
     if world > 1:
         sdist.setup_comm(ctx)
+    elif args.comm1:
+        ctx.set_comm(1, 0, sel.Context.new_unique_id())
     bms = key_sets(args.config)   # NEXT(3) key sets (c6), registered once like the table
     bm_dev = []
     for words, nbits in bms:

@@ -163,8 +163,10 @@ uint64_t sel_execute(sel_table table, const void* prog, size_t prog_bytes,
                      int* out_materialized, void* cuda_stream);
 
 /* Prepared executes: the same Execute with every argument fixed, validated and canonicalised
- * once and — on one rank, for a program that scans — its device work (count keeping the
- * selection, device-side gate, materialisation, result copies) captured into a CUDA graph, so
+ * once and — for a program that scans a non-empty shard — its device work (count keeping the
+ * selection, device-side gate, materialisation, result copies; with a communicator also the
+ * count all-reduce and the all-gather of per-rank counts, NCCL operations being capturable;
+ * environment SEL_GRAPH_COMM=0 leaves those uncaptured) captured into a CUDA graph, so
  * that a repeated probe (the optimizer re-estimating) costs one graph launch
  * and one synchronisation. The graph reads the columns' CURRENT contents at every run.
  * sel_prepare_execute: arguments as sel_execute (host arrays are copied; device buffers must

@@ -146,6 +146,7 @@ struct sel_ctx_s {
   // >= two_pass_min_rows local rows, else the single pass (SEL_PUSHDOWN_PATH=single|two forces)
   uint64_t two_pass_min_rows = 1ull << 22;
   bool fast_enabled = true;  // count fast path (SEL_FAST=0: interpreter only)
+  bool graph_comm = true;    // prepared executes with a communicator are captured (SEL_GRAPH_COMM=0: not)
   int prefetch_mode = -1;   // -1 auto, 0 off, 1 on
   bool keep_values = false;  // SEL_KEEP_VALUES=1: executes also keep projected predicate values
   float last_count_ms = 0.f, last_push_ms = 0.f;
@@ -474,6 +475,8 @@ sel_status sel_ctx_create(int cuda_device, sel_ctx* out) {
   c->prefetch_mode = pf ? (std::strcmp(pf, "1") == 0 ? 1 : 0) : -1;
   const char* kv = std::getenv("SEL_KEEP_VALUES");
   c->keep_values = kv && std::strcmp(kv, "1") == 0;
+  const char* gc = std::getenv("SEL_GRAPH_COMM");
+  c->graph_comm = !(gc && std::strcmp(gc, "0") == 0);
   const char* fe = std::getenv("SEL_FAST");
   c->fast_enabled = !(fe && std::strcmp(fe, "0") == 0);
   const char* cnw = std::getenv("SEL_COUNT_NW");
@@ -1011,6 +1014,25 @@ sel_status enqueue_pushdown_sel(sel_table t, const Plan& plan, const uint32_t* p
   return SEL_OK;
 }
 
+// All-gather a per-rank count into result[1..nranks] and its pinned mirror,
+// blocking (used where a rank has nothing of its own to enqueue but must match the collectives of
+// the others).
+sel_status gather_counts(sel_ctx c, uint64_t local, void* cuda_stream) {
+  cudaStream_t stream = (cudaStream_t)cuda_stream;
+  DeviceGuard g(c->device);
+  if (!g.ok) return set_error(SEL_E_CUDA, "cudaSetDevice failed");
+  c->h_result[0] = local;
+  cudaError_t e = cudaMemcpyAsync(c->s.result, c->h_result, sizeof(uint64_t), cudaMemcpyHostToDevice, stream);
+  if (e != cudaSuccess) return set_error(SEL_E_CUDA, cuda_msg("cudaMemcpyAsync", e));
+  ncclResult_t r = nccl().AllGather(c->s.result, c->s.result + 1, 1, ncclUint64, c->comm, stream);
+  if (r != ncclSuccess) return set_error(SEL_E_NCCL, nccl_msg("ncclAllGather", r));
+  e = cudaMemcpyAsync(c->h_result + 1, c->s.result + 1, c->nranks * sizeof(uint64_t),
+                      cudaMemcpyDeviceToHost, stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(stream);
+  if (e != cudaSuccess) return set_error(SEL_E_CUDA, cuda_msg("all-gather result", e));
+  return SEL_OK;
+}
+
 sel_status check_projection(sel_table t, const uint32_t* proj_cols, uint32_t nproj,
                             uint32_t* out_rowids, void* const* out_cols, uint64_t capacity_rows) {
   if (nproj > 0 && !proj_cols) return set_error(SEL_E_ARG, "null proj_cols");
@@ -1433,7 +1455,13 @@ uint64_t sel_execute(sel_table t, const void* prog, size_t prog_bytes, const uin
     const uint64_t count = sel_count_ex(t, prog, prog_bytes, SEL_KEEP_SELECTION, proj_cols, nkeep,
                                         cuda_stream);
     if (count == SEL_ERR) return SEL_ERR;
-    if (count > max_size) return count;  // "throw exception": nothing written
+    if (count > max_size) {  // "throw exception": nothing written
+      // Every rank issues the same collectives per Execute (all-reduce, then all-gather; the
+      // device-gated path below all-gathers also when gated), so a rank on this path (empty
+      // shard) matches ranks on the other.
+      if (c->comm && gather_counts(c, 0, cuda_stream) != SEL_OK) return SEL_ERR;
+      return count;
+    }
     const uint64_t r = sel_pushdown(t, prog, prog_bytes, proj_cols, nproj, out_rowids, out_cols,
                                     capacity_rows, out_local_count, out_global_offset, cuda_stream);
     if (r == SEL_ERR) return SEL_ERR;
@@ -1507,7 +1535,11 @@ sel_status capture_prepared(sel_prepared q) {
   q->bm_gen = c->bm_gen;
   q->timing = c->timing;
   q->comm = c->comm;
-  if (t->local_rows == 0 || plan.path == PATH_CONST || c->comm || c->force_single) return SEL_OK;
+  // With a communicator the two collectives are captured too (NCCL operations are capturable);
+  // SEL_GRAPH_COMM=0 keeps those executes uncaptured.
+  if (t->local_rows == 0 || plan.path == PATH_CONST || c->force_single ||
+      (c->comm && !c->graph_comm))
+    return SEL_OK;
   DeviceGuard g(c->device);
   if (!g.ok) return set_error(SEL_E_CUDA, "cudaSetDevice failed");
   const uint32_t nproj = (uint32_t)q->proj.size();
@@ -1531,9 +1563,16 @@ sel_status capture_prepared(sel_prepared q) {
   if (st == SEL_OK) {
     e = cudaMemcpyAsync(c->h_result + kGateSlot, c->s.result + kGateSlot, sizeof(uint64_t),
                         cudaMemcpyDeviceToHost, s);
-    if (e == cudaSuccess)
+    if (c->comm) {  // SURVEY §8a a7, as sel_execute: all-gather the per-rank counts
+      ncclResult_t r = nccl().AllGather(c->s.result, c->s.result + 1, 1, ncclUint64, c->comm, s);
+      if (r != ncclSuccess) st = set_error(SEL_E_NCCL, nccl_msg("ncclAllGather (capture)", r));
+      if (e == cudaSuccess)
+        e = cudaMemcpyAsync(c->h_result + 1, c->s.result + 1, c->nranks * sizeof(uint64_t),
+                            cudaMemcpyDeviceToHost, s);
+    } else if (e == cudaSuccess) {
       e = cudaMemcpyAsync(c->h_result, c->s.result, sizeof(uint64_t), cudaMemcpyDeviceToHost, s);
-    if (e != cudaSuccess) st = set_error(SEL_E_CUDA, cuda_msg("cudaMemcpyAsync (capture)", e));
+    }
+    if (st == SEL_OK && e != cudaSuccess) st = set_error(SEL_E_CUDA, cuda_msg("cudaMemcpyAsync (capture)", e));
   }
   c->capturing = false;
   cudaGraph_t graph = nullptr;
@@ -1630,7 +1669,13 @@ uint64_t sel_prepared_execute(sel_prepared q, uint64_t* out_local_count,
   }
   const uint64_t count = c->h_result[kGateSlot];
   if (count > q->max_size) return count;  // "throw exception"
-  if (out_local_count) *out_local_count = c->h_result[0];
+  uint64_t local = c->h_result[0], offset = 0;
+  if (q->comm) {
+    for (int r2 = 0; r2 < c->rank; ++r2) offset += c->h_result[1 + r2];
+    local = c->h_result[1 + c->rank];
+  }
+  if (out_local_count) *out_local_count = local;
+  if (out_global_offset) *out_global_offset = offset;
   if (out_materialized) *out_materialized = 1;
   return count;
 }

@@ -159,3 +159,37 @@ def test_prepared_non_graph_cases(pctx):
     q_true.release()
     q_false.release()
     t.release()
+
+
+def test_prepared_with_single_rank_communicator(cuda_device):
+    """With a (one-rank) NCCL communicator the prepared Execute captures the count all-reduce and
+    the all-gather of per-rank counts into its graph; results, offset and the gate are unchanged.
+    The host-gated path (constant program) issues the same collectives."""
+    c = sel.Context(cuda_device)
+    c.set_comm(1, 0, sel.Context.new_unique_id())
+    n = 600_000
+    T = configs.gen_c2(n)
+    cols = [x.numpy() for x in T.columns]
+    t = register(c, cols, T.types)
+    prog = encode(configs.c2_probes()["listing"], T.types)
+    proj = configs.C2_PROJECT
+    q = t.prepare_execute(prog, project=proj, max_size=n)
+    for _ in range(3):
+        assert _check(q, cols, T.types, prog, proj) == 100_200
+        assert q.result().offset == 0
+    gated = t.prepare_execute(prog, project=proj, max_size=100_199, capacity=16)
+    assert gated.run() == 100_200 and not gated.materialized
+    for node in (Const(True), Const(False)):
+        p = encode(node, T.types)
+        qc = t.prepare_execute(p, project=[3], max_size=n if node.value else 0)
+        want = n if node.value else 0
+        assert qc.run() == want
+        qc.release()
+        r = t.execute(p, project=[3], max_size=0)           # host-gated, gated: all-gather too
+        assert r.count == want and r.materialized == (want == 0)
+    # collectives still line up: a plain count afterwards
+    assert t.count(prog) == 100_200
+    for h in (q, gated):
+        h.release()
+    t.release()
+    c.close()
