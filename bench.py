@@ -270,7 +270,7 @@ def run_reference(args):
                              "sample": f"first {sample} rows of the workload; count on {nthreads} threads (oracle_count_mt), push-down single-threaded (oracle_pushdown)"},
             "e2e": {"value": round(value, 3), "unit": "GB/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
-    print(json.dumps(line), flush=True)
+    emit(line)
 
 
 # ---- our arm ---------------------------------------------------------------------------------------
@@ -567,6 +567,7 @@ def run_ours(args):
                        "step": ("sel_execute = count (keeping the selection) -> device-side gate -> "
                                 "materialise" + (", per table.execute()" if prepared is None else
                                                  ", prepared once and replayed as a CUDA graph"))},
+            "rows_per_s": round(n / (ms_per_step / 1000)),
             "latency_ms": {"execute_median": round(statistics.median(count_lat), 4),
                            "execute_min": round(min(count_lat), 4),
                            "execute_p99": _stats(count_lat)["p99"],
@@ -582,7 +583,7 @@ def run_ours(args):
             "gpu_launches": (3 if pd_path == 1 else 2) * args.steps,
             "cpu_baseline": cpu,
         }
-        print(json.dumps(line), flush=True)
+        emit(line)
     if prepared is not None:
         prepared.release()
     table.release()
@@ -591,7 +592,20 @@ def run_ours(args):
         dist.destroy_process_group()
 
 
+_JSON_FD = None
+
+
+def emit(line):
+    """The bench line, alone on the real stdout (native libraries such as NCCL print banners to
+    fd 1; main() points fd 1 at stderr for the run)."""
+    os.write(_JSON_FD if _JSON_FD is not None else 1, (json.dumps(line) + "\n").encode())
+
+
 def main():
+    global _JSON_FD
+    sys.stdout.flush()
+    _JSON_FD = os.dup(1)
+    os.dup2(2, 1)
     args = parse()
     if args.impl == "reference":
         run_reference(args)

@@ -155,7 +155,9 @@ uint64_t sel_count_ex(sel_table table, const void* prog, size_t prog_bytes, uint
  * GLOBAL count > max_size "throw" — *out_materialized = 0, nothing is written, *out_local_count
  * and *out_global_offset are set to 0 — else materialise exactly like sel_pushdown (from the kept
  * selection) and set *out_materialized = 1. Returns the global count or SEL_ERR. Arguments as
- * sel_pushdown; out_materialized may be NULL. */
+ * sel_pushdown; out_materialized may be NULL. With a communicator the call issues exactly one
+ * collective, gated or not: an all-gather of the per-rank counts, whose sum is the global count
+ * the gate compares and whose exclusive prefix is *out_global_offset (every rank must call it). */
 uint64_t sel_execute(sel_table table, const void* prog, size_t prog_bytes,
                      const uint32_t* proj_cols, uint32_t nproj, uint64_t max_size,
                      uint32_t* out_rowids, void* const* out_cols, uint64_t capacity_rows,

@@ -967,7 +967,7 @@ sel_status enqueue_count(sel_table t, const Plan& plan, uint32_t flags, const ui
 sel_status enqueue_pushdown_sel(sel_table t, const Plan& plan, const uint32_t* proj_cols,
                                 uint32_t nproj, uint32_t* out_rowids, void* const* out_cols,
                                 uint64_t capacity_rows, bool gate, uint64_t gate_max,
-                                cudaStream_t stream) {
+                                cudaStream_t stream, int gate_ranks = 0) {
   sel_ctx c = t->ctx;
   const auto consts = const_columns(t, plan);
   const uint64_t n = t->local_rows;
@@ -1002,12 +1002,12 @@ sel_status enqueue_pushdown_sel(sel_table t, const Plan& plan, const uint32_t* p
     DevProgramSmall p;
     fill_sel(&p);
     le = launch_pushdown_sel_small(p, n, out_rowids, grid_for(c, units, occupancy_pushdown_sel_small()),
-                                   c->s, c->sel, stream);
+                                   c->s, c->sel, stream, gate_ranks);
   } else {
     static thread_local DevProgramLarge p;
     fill_sel(&p);
     le = launch_pushdown_sel_large(p, n, out_rowids, grid_for(c, units, occupancy_pushdown_sel_large()),
-                                   c->s, c->sel, stream);
+                                   c->s, c->sel, stream, gate_ranks);
   }
   if (le != cudaSuccess) return set_error(SEL_E_CUDA, cuda_msg("push-down kernel launch", (cudaError_t)le));
   c->last_pd_path = 1;
@@ -1031,6 +1031,57 @@ sel_status gather_counts(sel_ctx c, uint64_t local, void* cuda_stream) {
   if (e == cudaSuccess) e = cudaStreamSynchronize(stream);
   if (e != cudaSuccess) return set_error(SEL_E_CUDA, cuda_msg("all-gather result", e));
   return SEL_OK;
+}
+
+// The device work of a device-gated Execute on `stream` (sel_execute, prepared executes): count
+// keeping the selection (local count -> result[kGateSlot]); with a communicator the all-gather of
+// the per-rank counts into result[1..nranks] (the prefix kernel then sums them into
+// result[kGateSlot]); the gated materialisation; D2H copies of result[kGateSlot] and of the
+// per-rank counts (result[1..nranks]) or the local count (result[0]).
+sel_status enqueue_execute(sel_table t, const Plan& plan, const uint32_t* proj, uint32_t nproj,
+                           uint32_t nkeep, uint64_t max_size, uint32_t* out_rowids,
+                           void* const* outs, uint64_t capacity, cudaStream_t s) {
+  sel_ctx c = t->ctx;
+  sel_status st = enqueue_count(t, plan, SEL_KEEP_SELECTION, proj, nkeep, s, c->s.result + kGateSlot,
+                                false);
+  if (st != SEL_OK) return st;
+  if (c->comm) {  // SURVEY §8a a4 + a7 in one collective
+    ncclResult_t r = nccl().AllGather(c->s.result + kGateSlot, c->s.result + 1, 1, ncclUint64,
+                                      c->comm, s);
+    if (r != ncclSuccess) return set_error(SEL_E_NCCL, nccl_msg("ncclAllGather", r));
+  }
+  if (c->timing) record(c, c->ev2, s);
+  st = enqueue_pushdown_sel(t, plan, proj, nproj, out_rowids, outs, capacity, true, max_size, s,
+                            c->comm ? c->nranks : 0);
+  if (st != SEL_OK) return st;
+  if (c->timing) record(c, c->ev3, s);
+  cudaError_t e = cudaMemcpyAsync(c->h_result + kGateSlot, c->s.result + kGateSlot, sizeof(uint64_t),
+                                  cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess) {
+    if (c->comm)
+      e = cudaMemcpyAsync(c->h_result + 1, c->s.result + 1, c->nranks * sizeof(uint64_t),
+                          cudaMemcpyDeviceToHost, s);
+    else
+      e = cudaMemcpyAsync(c->h_result, c->s.result, sizeof(uint64_t), cudaMemcpyDeviceToHost, s);
+  }
+  if (e != cudaSuccess) return set_error(SEL_E_CUDA, cuda_msg("cudaMemcpyAsync (execute)", e));
+  return SEL_OK;
+}
+
+// Outputs of a completed device-gated Execute from the pinned result mirror.
+uint64_t execute_outputs(sel_ctx c, uint64_t max_size, uint64_t* out_local_count,
+                         uint64_t* out_global_offset, int* out_materialized) {
+  const uint64_t count = c->h_result[kGateSlot];
+  if (count > max_size) return count;  // "throw exception" (PAPER.md:396-397): nothing written
+  uint64_t local = c->h_result[0], offset = 0;
+  if (c->comm) {
+    for (int r2 = 0; r2 < c->rank; ++r2) offset += c->h_result[1 + r2];
+    local = c->h_result[1 + c->rank];
+  }
+  if (out_local_count) *out_local_count = local;
+  if (out_global_offset) *out_global_offset = offset;
+  if (out_materialized) *out_materialized = 1;
+  return count;
 }
 
 sel_status check_projection(sel_table t, const uint32_t* proj_cols, uint32_t nproj,
@@ -1088,11 +1139,16 @@ uint64_t sel_count_ex(sel_table t, const void* prog, size_t prog_bytes, uint32_t
   return c->h_result[0];
 }
 
-uint64_t sel_pushdown(sel_table t, const void* prog, size_t prog_bytes, const uint32_t* proj_cols,
-                      uint32_t nproj, uint32_t* out_rowids, void* const* out_cols,
-                      uint64_t capacity_rows, uint64_t* out_local_count,
-                      uint64_t* out_global_offset, void* cuda_stream) {
-  clear_error();
+}  // extern "C"
+
+namespace {
+
+// sel_pushdown's body. collective = false: no all-gather — the local count is returned (and
+// *out_global_offset left 0); sel_execute's host-gated path has gathered the counts already.
+uint64_t pushdown_impl(sel_table t, const void* prog, size_t prog_bytes, const uint32_t* proj_cols,
+                       uint32_t nproj, uint32_t* out_rowids, void* const* out_cols,
+                       uint64_t capacity_rows, uint64_t* out_local_count,
+                       uint64_t* out_global_offset, void* cuda_stream, bool collective) {
   if (!t) return fail64(SEL_E_ARG, "null table");
   sel_ctx c = t->ctx;
   if (c->destroyed) return fail64(SEL_E_STATE, "context destroyed");
@@ -1214,13 +1270,13 @@ uint64_t sel_pushdown(sel_table t, const void* prog, size_t prog_bytes, const ui
     if (c->timing) cudaEventRecord(c->ev1, stream);
   } else {
     c->h_result[0] = 0;
-    if (c->comm) {
+    if (c->comm && collective) {
       e = cudaMemcpyAsync(c->s.result, c->h_result, sizeof(uint64_t), cudaMemcpyHostToDevice, stream);
       if (e != cudaSuccess) return fail64(SEL_E_CUDA, cuda_msg("cudaMemcpyAsync", e));
     }
   }
   uint64_t local = 0, offset = 0, total = 0;
-  if (c->comm) {  // all-gather the per-rank counts, exclusive scan on the host
+  if (c->comm && collective) {  // all-gather the per-rank counts, exclusive scan on the host
     ncclResult_t r = nccl().AllGather(c->s.result, c->s.result + 1, 1, ncclUint64, c->comm, stream);
     if (r != ncclSuccess) return fail64(SEL_E_NCCL, nccl_msg("ncclAllGather", r));
     e = cudaMemcpyAsync(c->h_result + 1, c->s.result + 1, c->nranks * sizeof(uint64_t),
@@ -1255,6 +1311,19 @@ uint64_t sel_pushdown(sel_table t, const void* prog, size_t prog_bytes, const ui
   if (out_local_count) *out_local_count = local;
   if (out_global_offset) *out_global_offset = offset;
   return total;
+}
+
+}  // namespace
+
+extern "C" {
+
+uint64_t sel_pushdown(sel_table t, const void* prog, size_t prog_bytes, const uint32_t* proj_cols,
+                      uint32_t nproj, uint32_t* out_rowids, void* const* out_cols,
+                      uint64_t capacity_rows, uint64_t* out_local_count,
+                      uint64_t* out_global_offset, void* cuda_stream) {
+  clear_error();
+  return pushdown_impl(t, prog, prog_bytes, proj_cols, nproj, out_rowids, out_cols, capacity_rows,
+                       out_local_count, out_global_offset, cuda_stream, true);
 }
 
 uint64_t sel_count_sampled(sel_table t, const void* prog, size_t prog_bytes, uint32_t stride,
@@ -1449,53 +1518,64 @@ uint64_t sel_execute(sel_table t, const void* prog, size_t prog_bytes, const uin
   // Execute(isSPD): gamma_COUNT over the compound, keeping what the materialisation reuses: the
   // selection (SEL_KEEP_VALUES=1: also the projected predicate columns' values — measured equal
   // or slower on every config).
+  // With a communicator every Execute issues exactly one collective, an all-gather of the
+  // per-rank counts (their sum is the global count the gate compares; their exclusive prefix
+  // the rank's offset), on both paths below, so ranks on different paths stay matched.
   const uint32_t nkeep = c->keep_values ? nproj : 0u;
   const bool scan = t->local_rows > 0 && plan.path != PATH_CONST;
   if (!scan || c->force_single) {  // host-side gate: count, then (maybe) the push-down
-    const uint64_t count = sel_count_ex(t, prog, prog_bytes, SEL_KEEP_SELECTION, proj_cols, nkeep,
-                                        cuda_stream);
-    if (count == SEL_ERR) return SEL_ERR;
-    if (count > max_size) {  // "throw exception": nothing written
-      // Every rank issues the same collectives per Execute (all-reduce, then all-gather; the
-      // device-gated path below all-gathers also when gated), so a rank on this path (empty
-      // shard) matches ranks on the other.
-      if (c->comm && gather_counts(c, 0, cuda_stream) != SEL_OK) return SEL_ERR;
-      return count;
+    uint64_t local;
+    if (c->comm) {
+      local = scan ? 0 : (plan.path == PATH_CONST && plan.const_value ? t->local_rows : 0);
+      if (scan) {
+        cudaStream_t stream = (cudaStream_t)cuda_stream;
+        DeviceGuard g(c->device);
+        if (!g.ok) return fail64(SEL_E_CUDA, "cudaSetDevice failed");
+        if (enqueue_count(t, plan, SEL_KEEP_SELECTION, proj_cols, nkeep, stream, c->s.result,
+                          false) != SEL_OK)
+          return SEL_ERR;
+        cudaError_t e = cudaMemcpyAsync(c->h_result, c->s.result, sizeof(uint64_t),
+                                        cudaMemcpyDeviceToHost, stream);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(stream);
+        if (e != cudaSuccess) return fail64(SEL_E_CUDA, cuda_msg("count result", e));
+        local = c->h_result[0];
+        c->kept_table = t;
+        c->kept_prog.assign(static_cast<const char*>(prog), prog_bytes);
+      }
+      if (gather_counts(c, local, cuda_stream) != SEL_OK) return SEL_ERR;
+    } else {
+      local = sel_count_ex(t, prog, prog_bytes, SEL_KEEP_SELECTION, proj_cols, nkeep, cuda_stream);
+      if (local == SEL_ERR) return SEL_ERR;
     }
-    const uint64_t r = sel_pushdown(t, prog, prog_bytes, proj_cols, nproj, out_rowids, out_cols,
-                                    capacity_rows, out_local_count, out_global_offset, cuda_stream);
+    uint64_t count = local, offset = 0;
+    if (c->comm) {
+      count = 0;
+      for (int r2 = 0; r2 < c->nranks; ++r2) {
+        if (r2 < c->rank) offset += c->h_result[1 + r2];
+        count += c->h_result[1 + r2];
+      }
+    }
+    if (count > max_size) return count;  // "throw exception": nothing written
+    const uint64_t r = pushdown_impl(t, prog, prog_bytes, proj_cols, nproj, out_rowids, out_cols,
+                                     capacity_rows, out_local_count, nullptr, cuda_stream, false);
     if (r == SEL_ERR) return SEL_ERR;
+    if (out_global_offset) *out_global_offset = offset;
     if (out_materialized) *out_materialized = 1;
-    return r;
+    return count;
   }
   // Device-side gate (PAPER.md:393-400 in one stream, one host synchronisation): count keeping
-  // the selection -> global count into result[kGateSlot] (all-reduce) -> the push-down kernels
-  // read it and write nothing if count > maxSize -> per-rank counts -> one D2H.
+  // the selection -> global count into result[kGateSlot] (without a communicator the count
+  // itself; with one, the sum of the all-gathered per-rank counts) -> the push-down kernels
+  // read it and write nothing if count > maxSize -> one D2H.
   cudaStream_t stream = (cudaStream_t)cuda_stream;
   DeviceGuard g(c->device);
   if (!g.ok) return fail64(SEL_E_CUDA, "cudaSetDevice failed");
   c->last_ms = 0.f;
   c->last_pd_path = -1;
-  if (enqueue_count(t, plan, SEL_KEEP_SELECTION, proj_cols, nkeep, stream,
-                    c->s.result + kGateSlot) != SEL_OK)
-    return SEL_ERR;
-  if (c->timing) cudaEventRecord(c->ev2, stream);
-  if (enqueue_pushdown_sel(t, plan, proj_cols, nproj, out_rowids, out_cols, capacity_rows, true,
-                           max_size, stream) != SEL_OK)
-    return SEL_ERR;
-  if (c->timing) cudaEventRecord(c->ev3, stream);
-  cudaError_t e = cudaMemcpyAsync(c->h_result + kGateSlot, c->s.result + kGateSlot,
-                                  sizeof(uint64_t), cudaMemcpyDeviceToHost, stream);
-  if (c->comm) {  // all-gather the per-rank counts
-    ncclResult_t r = nccl().AllGather(c->s.result, c->s.result + 1, 1, ncclUint64, c->comm, stream);
-    if (r != ncclSuccess) return fail64(SEL_E_NCCL, nccl_msg("ncclAllGather", r));
-    if (e == cudaSuccess)
-      e = cudaMemcpyAsync(c->h_result + 1, c->s.result + 1, c->nranks * sizeof(uint64_t),
-                          cudaMemcpyDeviceToHost, stream);
-  } else if (e == cudaSuccess) {
-    e = cudaMemcpyAsync(c->h_result, c->s.result, sizeof(uint64_t), cudaMemcpyDeviceToHost, stream);
-  }
-  if (e == cudaSuccess) e = cudaStreamSynchronize(stream);
+  sel_status st = enqueue_execute(t, plan, proj_cols, nproj, nkeep, max_size, out_rowids, out_cols,
+                                  capacity_rows, stream);
+  if (st != SEL_OK) return SEL_ERR;
+  cudaError_t e = cudaStreamSynchronize(stream);
   if (e != cudaSuccess) return fail64(SEL_E_CUDA, cuda_msg("execute result", e));
   c->kept_table = t;
   c->kept_prog.assign(static_cast<const char*>(prog), prog_bytes);
@@ -1504,17 +1584,7 @@ uint64_t sel_execute(sel_table t, const void* prog, size_t prog_bytes, const uin
     cudaEventElapsedTime(&c->last_push_ms, c->ev2, c->ev3);
     c->last_ms = c->last_push_ms;
   }
-  const uint64_t count = c->h_result[kGateSlot];
-  if (count > max_size) return count;  // "throw exception" (PAPER.md:396-397): nothing written
-  uint64_t local = c->h_result[0], offset = 0;
-  if (c->comm) {
-    for (int r2 = 0; r2 < c->rank; ++r2) offset += c->h_result[1 + r2];
-    local = c->h_result[1 + c->rank];
-  }
-  if (out_local_count) *out_local_count = local;
-  if (out_global_offset) *out_global_offset = offset;
-  if (out_materialized) *out_materialized = 1;
-  return count;
+  return execute_outputs(c, max_size, out_local_count, out_global_offset, out_materialized);
 }
 
 }  // extern "C"
@@ -1554,26 +1624,8 @@ sel_status capture_prepared(sel_prepared q) {
   cudaError_t e = cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal);
   if (e != cudaSuccess) return set_error(SEL_E_CUDA, cuda_msg("cudaStreamBeginCapture", e));
   c->capturing = true;
-  sel_status st = enqueue_count(t, plan, SEL_KEEP_SELECTION, proj, nkeep, s, c->s.result + kGateSlot);
-  if (st == SEL_OK && c->timing) record(c, c->ev2, s);
-  if (st == SEL_OK)
-    st = enqueue_pushdown_sel(t, plan, proj, nproj, q->out_rowids, outs, q->capacity, true,
-                              q->max_size, s);
-  if (st == SEL_OK && c->timing) record(c, c->ev3, s);
-  if (st == SEL_OK) {
-    e = cudaMemcpyAsync(c->h_result + kGateSlot, c->s.result + kGateSlot, sizeof(uint64_t),
-                        cudaMemcpyDeviceToHost, s);
-    if (c->comm) {  // SURVEY §8a a7, as sel_execute: all-gather the per-rank counts
-      ncclResult_t r = nccl().AllGather(c->s.result, c->s.result + 1, 1, ncclUint64, c->comm, s);
-      if (r != ncclSuccess) st = set_error(SEL_E_NCCL, nccl_msg("ncclAllGather (capture)", r));
-      if (e == cudaSuccess)
-        e = cudaMemcpyAsync(c->h_result + 1, c->s.result + 1, c->nranks * sizeof(uint64_t),
-                            cudaMemcpyDeviceToHost, s);
-    } else if (e == cudaSuccess) {
-      e = cudaMemcpyAsync(c->h_result, c->s.result, sizeof(uint64_t), cudaMemcpyDeviceToHost, s);
-    }
-    if (st == SEL_OK && e != cudaSuccess) st = set_error(SEL_E_CUDA, cuda_msg("cudaMemcpyAsync (capture)", e));
-  }
+  sel_status st = enqueue_execute(t, plan, proj, nproj, nkeep, q->max_size, q->out_rowids, outs,
+                                  q->capacity, s);
   c->capturing = false;
   cudaGraph_t graph = nullptr;
   e = cudaStreamEndCapture(s, &graph);
@@ -1667,17 +1719,7 @@ uint64_t sel_prepared_execute(sel_prepared q, uint64_t* out_local_count,
     cudaEventElapsedTime(&c->last_push_ms, c->ev2, c->ev3);
     c->last_ms = c->last_push_ms;
   }
-  const uint64_t count = c->h_result[kGateSlot];
-  if (count > q->max_size) return count;  // "throw exception"
-  uint64_t local = c->h_result[0], offset = 0;
-  if (q->comm) {
-    for (int r2 = 0; r2 < c->rank; ++r2) offset += c->h_result[1 + r2];
-    local = c->h_result[1 + c->rank];
-  }
-  if (out_local_count) *out_local_count = local;
-  if (out_global_offset) *out_global_offset = offset;
-  if (out_materialized) *out_materialized = 1;
-  return count;
+  return execute_outputs(c, q->max_size, out_local_count, out_global_offset, out_materialized);
 }
 
 void sel_prepared_release(sel_prepared q) {

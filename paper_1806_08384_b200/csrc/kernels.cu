@@ -886,10 +886,19 @@ __global__ void __launch_bounds__(kThreads) superblock_sum_kernel(const uint16_t
 #endif
 
 // Exclusive prefix of the per-64-chunk sums kept by the count kernel (one CTA; <= 65536 sums).
+// gate_ranks > 0 (sel_execute with a communicator): result[1..gate_ranks] holds the all-gathered
+// per-rank counts; their sum, the global count, is written to result[kGateSlot] for the gate of
+// the push-down kernel that follows (one collective per Execute instead of two).
 __global__ void __launch_bounds__(1024) superblock_prefix_kernel(const uint32_t* __restrict__ sb_sum,
                                                                  uint32_t* __restrict__ sb_prefix,
-                                                                 uint32_t nsb, uint64_t* __restrict__ out_count) {
+                                                                 uint32_t nsb, uint64_t* __restrict__ out_count,
+                                                                 int gate_ranks) {
   const uint32_t t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  if (gate_ranks > 0 && t == 0) {
+    uint64_t g = 0;
+    for (int r = 0; r < gate_ranks; ++r) g += out_count[1 + r];
+    out_count[kGateSlot] = g;
+  }
   const uint32_t per = (nsb + 1023u) / 1024u;
   const uint32_t b = min(nsb, t * per), e = min(nsb, b + per);
   uint32_t local = 0;
@@ -1205,27 +1214,29 @@ int launch_count_large(const DevProgramLarge& p, uint64_t n, int grid, const Scr
   return launch_count_t(p, n, grid, s, keep, nw, st);
 }
 int launch_pushdown_sel_small(const DevProgramSmall& p, uint64_t n, uint32_t* out_ids, int grid,
-                              const Scratch& s, const SelectionBufs& sb, void* st) {
+                              const Scratch& s, const SelectionBufs& sb, void* st, int gate_ranks) {
   const uint64_t nchunks = (n + kChunkRows - 1) / kChunkRows;
   const uint32_t nsb = (uint32_t)((nchunks + kSbChunks - 1) / kSbChunks);
 #if !SEL_SB_ATOMICS
   superblock_sum_kernel<<<(unsigned)(nsb < 148ull * 16 * kWarpsPerCta ? (nsb + kWarpsPerCta - 1) / kWarpsPerCta : 148ull * 16), kThreads, 0,
                           (cudaStream_t)st>>>(sb.chunk_cnt, nchunks, sb.sb_sum);
 #endif
-  superblock_prefix_kernel<<<1, 1024, 0, (cudaStream_t)st>>>(sb.sb_sum, sb.sb_prefix, nsb, s.result);
+  superblock_prefix_kernel<<<1, 1024, 0, (cudaStream_t)st>>>(sb.sb_sum, sb.sb_prefix, nsb, s.result,
+                                                               gate_ranks);
   pushdown_sel_kernel<DevProgramSmall><<<grid, kThreads, 0, (cudaStream_t)st>>>(p, n, sb, out_ids,
                                                                                 s.result + kGateSlot);
   return (int)cudaGetLastError();
 }
 int launch_pushdown_sel_large(const DevProgramLarge& p, uint64_t n, uint32_t* out_ids, int grid,
-                              const Scratch& s, const SelectionBufs& sb, void* st) {
+                              const Scratch& s, const SelectionBufs& sb, void* st, int gate_ranks) {
   const uint64_t nchunks = (n + kChunkRows - 1) / kChunkRows;
   const uint32_t nsb = (uint32_t)((nchunks + kSbChunks - 1) / kSbChunks);
 #if !SEL_SB_ATOMICS
   superblock_sum_kernel<<<(unsigned)(nsb < 148ull * 16 * kWarpsPerCta ? (nsb + kWarpsPerCta - 1) / kWarpsPerCta : 148ull * 16), kThreads, 0,
                           (cudaStream_t)st>>>(sb.chunk_cnt, nchunks, sb.sb_sum);
 #endif
-  superblock_prefix_kernel<<<1, 1024, 0, (cudaStream_t)st>>>(sb.sb_sum, sb.sb_prefix, nsb, s.result);
+  superblock_prefix_kernel<<<1, 1024, 0, (cudaStream_t)st>>>(sb.sb_sum, sb.sb_prefix, nsb, s.result,
+                                                               gate_ranks);
   pushdown_sel_kernel<DevProgramLarge><<<grid, kThreads, 0, (cudaStream_t)st>>>(p, n, sb, out_ids,
                                                                                 s.result + kGateSlot);
   return (int)cudaGetLastError();

@@ -181,12 +181,15 @@ int launch_count_small(const DevProgramSmall& p, uint64_t n, int grid, const Scr
                        const SelectionBufs* keep, void* stream, int nw = kWarpsPerCta);
 int launch_count_large(const DevProgramLarge& p, uint64_t n, int grid, const Scratch& s,
                        const SelectionBufs* keep, void* stream, int nw = kWarpsPerCta);
-// Push-down from a kept selection: superblock prefix (writes the local count to s.result[0]) and
-// the compaction/gather kernel.
+// Push-down from a kept selection: superblock prefix (writes the local count to s.result[0]; with
+// gate_ranks > 0 also s.result[kGateSlot] = sum of the gathered s.result[1..gate_ranks]) and the
+// compaction/gather kernel.
 int launch_pushdown_sel_small(const DevProgramSmall& p, uint64_t n, uint32_t* out_ids, int grid,
-                              const Scratch& s, const SelectionBufs& sb, void* stream);
+                              const Scratch& s, const SelectionBufs& sb, void* stream,
+                              int gate_ranks = 0);
 int launch_pushdown_sel_large(const DevProgramLarge& p, uint64_t n, uint32_t* out_ids, int grid,
-                              const Scratch& s, const SelectionBufs& sb, void* stream);
+                              const Scratch& s, const SelectionBufs& sb, void* stream,
+                              int gate_ranks = 0);
 int launch_pushdown_small(const DevProgramSmall& p, uint64_t n, uint32_t* out_ids, int grid,
                           const Scratch& s, uint64_t ticket_base, uint32_t epoch, void* stream);
 int launch_pushdown_large(const DevProgramLarge& p, uint64_t n, uint32_t* out_ids, int grid,
