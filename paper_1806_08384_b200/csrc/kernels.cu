@@ -701,7 +701,10 @@ __device__ __forceinline__ void keep_chunk(const SelectionBufs& sb, uint64_t c, 
 // NW warps per CTA: 8 normally; 32 when staged key sets leave room for one CTA per SM only.
 // FASTN > 0: the program is a conjunction of FASTN fast-path leaves (p.fast_n == FASTN).
 template <class P, bool KEEP, int NW, int FASTN = 0>
-__global__ void __launch_bounds__(NW * 32, NW == kWarpsPerCta ? 4 : 1) count_kernel(const __grid_constant__ P p, uint64_t n,
+#ifndef SEL_FAST_MINB
+#define SEL_FAST_MINB 3   // fast path: <= 85 registers (A/B: 2-6; 3 best on C2, C4, C5)
+#endif
+__global__ void __launch_bounds__(NW * 32, NW == kWarpsPerCta ? (FASTN ? SEL_FAST_MINB : 4) : 1) count_kernel(const __grid_constant__ P p, uint64_t n,
                                                          uint64_t* __restrict__ partials,
                                                          unsigned int* __restrict__ done,
                                                          uint64_t* __restrict__ out,

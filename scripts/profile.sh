@@ -13,6 +13,9 @@ for K in count_kernel pushdown_sel_kernel superblock_prefix_kernel; do
   ncu --set full --clock-control none --import-source on -k regex:${K} -s 3 -c 1 \
       -o gpurun_out/prof_${TAG}_${K} -f python bench.py $ARGS > gpurun_out/prof_${TAG}_${K}.out 2>&1
 done
+# the count kernel through the interpreter instead of the fast path (fast path vs interpreter)
+SEL_FAST=0 ncu --set full --clock-control none --import-source on -k regex:count_kernel -s 3 -c 1 \
+    -o gpurun_out/prof_${TAG}_count_interp -f python bench.py $ARGS > gpurun_out/prof_${TAG}_count_interp.out 2>&1
 SEL_PUSHDOWN_PATH=single ncu --set full --clock-control none --import-source on -k regex:'pushdown_kernel' -s 3 -c 1 \
     -o gpurun_out/prof_${TAG}_pushdown_kernel -f python bench.py $ARGS > gpurun_out/prof_${TAG}_pushdown_kernel.out 2>&1
 ls -la gpurun_out | grep $TAG
