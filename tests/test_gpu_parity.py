@@ -402,3 +402,22 @@ def test_constant_projections(ctx):
     _, _, wc = oracle.pushdown(cols, types, encode(progs[2], types), proj=[2])
     assert len(set(wc[0].view(np.uint32).tolist())) == 2
     t.release()
+
+
+def test_selection_chunk_densities(ctx):
+    """Kept selections whose per-chunk counts span empty, 1, sector and warp boundaries
+    (15/16/17, 31/32/33, 63/64/65), dense and full chunks, and a ragged tail; every
+    materialisation path."""
+    rng = np.random.default_rng(64)
+    ks = [0, 1, 2, 15, 16, 17, 31, 32, 33, 48, 63, 64, 65, 100, 511, 1023, 1024, 0, 64, 7]
+    n = 1024 * len(ks) - 300                                     # the last chunk is ragged
+    x = np.zeros(n, np.int32)
+    for c, k in enumerate(ks):
+        lo, hi = 1024 * c, min(n, 1024 * c + 1024)
+        pick = rng.choice(hi - lo, size=min(k, hi - lo), replace=False)
+        x[lo + pick] = 1
+    y = rng.integers(-1000, 1000, n).astype(np.int32)
+    types = [INT32, INT32]
+    t = register(ctx, [x, y], types)
+    for node in [Cmp("=", 0, 1), And(Cmp("=", 0, 1), Cmp(">", 1, 0)), Cmp("=", 0, 0)]:
+        check_parity(t, [x, y], types, node, proj=[1, 0])
