@@ -20,6 +20,7 @@ using namespace sel;
 
 // ---- thread-local error state ----------------------------------------------------------------
 namespace {
+constexpr uint64_t kTwoPassMinRows = 1ull << 21;  // sel_pushdown: two passes from here
 thread_local sel_status g_status = SEL_OK;
 thread_local std::string g_message;
 
@@ -144,7 +145,7 @@ struct sel_ctx_s {
   bool force_single = false;
   // sel_pushdown without a kept selection: two passes (keeping count -> materialise from it) at
   // >= two_pass_min_rows local rows, else the single pass (SEL_PUSHDOWN_PATH=single|two forces)
-  uint64_t two_pass_min_rows = 1ull << 22;
+  uint64_t two_pass_min_rows = kTwoPassMinRows;
   bool fast_enabled = true;  // count fast path (SEL_FAST=0: interpreter only)
   bool graph_comm = true;    // prepared executes with a communicator are captured (SEL_GRAPH_COMM=0: not)
   int prefetch_mode = -1;   // -1 auto, 0 off, 1 on
@@ -603,7 +604,7 @@ sel_status sel_ctx_set_pushdown_path(sel_ctx ctx, int mode) {
   if (!ctx) return set_error(SEL_E_ARG, "null ctx");
   if (mode != -1 && mode != 0 && mode != 2) return set_error(SEL_E_ARG, "mode must be -1, 0 or 2");
   ctx->force_single = mode == 0;
-  ctx->two_pass_min_rows = mode == 2 ? 0 : (mode == 0 ? ~0ull : (1ull << 22));
+  ctx->two_pass_min_rows = mode == 2 ? 0 : (mode == 0 ? ~0ull : kTwoPassMinRows);
   return SEL_OK;
 }
 
