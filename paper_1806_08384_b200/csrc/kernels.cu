@@ -982,7 +982,7 @@ __device__ __forceinline__ void copy_kept(const P& p, const SelectionBufs& sb, u
 }
 
 #ifndef SEL_BLOCK_CHUNKS
-#define SEL_BLOCK_CHUNKS 2
+#define SEL_BLOCK_CHUNKS 4
 #endif
 #ifndef SEL_STAGE_CAP
 #define SEL_STAGE_CAP 1024

@@ -135,7 +135,7 @@ int occupancy_count_batch();
 // 64 chunks, the sum of
 // its counts and (filled by the push-down) its exclusive prefix.
 #ifndef SEL_BLOCK_CHUNKS
-#define SEL_BLOCK_CHUNKS 2
+#define SEL_BLOCK_CHUNKS 4   // A/B 2/4/8: 4 best (C5 push-down 0.233 -> 0.206 ms, C3 0.240 -> 0.232, C2 equal)
 #endif
 constexpr int kSelBlockChunks = SEL_BLOCK_CHUNKS;   // push-down from a selection: chunks per warp block
 constexpr int kSbShift = 6;
