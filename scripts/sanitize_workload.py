@@ -56,5 +56,35 @@ for n in [1025, 70_001]:
     t.release()
     for i in ids:
         ctx.release_bitmap(i)
+# conjunctive fast path (count kernel FASTN = 1..4) through count, execute and the two-pass
+# push-down; a one-rank communicator (the Execute's all-gather, captured in a prepared graph)
+sys.path.insert(0, 'tests')
+from test_gpu_fastpath import TYPES as FT, fast_conjunction
+cctx = sel.Context(dev)
+cctx.set_comm(1, 0, sel.Context.new_unique_id())
+for n in [1025, 70_001]:
+    rng = np.random.default_rng(11 + n)
+    cols, pools = random_table(rng, FT, n)
+    view = {INT32: np.int32, DATE32: np.int32, DICT32: np.int32, INT64: np.int64, DICT8: np.uint8}
+    tens = [torch.from_numpy(np.ascontiguousarray(c).view(view[ty]).copy()).to(dev) for c, ty in zip(cols, FT)]
+    for cx in (ctx, cctx):
+        t = sel.Table(cx, [f"c{i}" for i in range(len(FT))], FT, tens)
+        for _ in range(6):
+            node = fast_conjunction(rng, pools)
+            prog = encode(node, FT)
+            want = oracle.pushdown(cols, FT, prog, proj=[0, 3, 4])
+            assert t.count(prog) == want[0]
+            r1 = t.execute(prog, project=[0, 3, 4], max_size=n)
+            cx.set_pushdown_path(2)
+            t.count(encode(Const(True), FT), keep_selection=True)
+            r2 = t.pushdown(prog, project=[0, 3, 4], capacity=max(want[0], 1))   # two passes
+            cx.set_pushdown_path(-1)
+            q = t.prepare_execute(prog, project=[0, 3, 4], max_size=n)
+            assert q.run() == want[0]
+            for r in (r1, r2, q.result()):
+                assert np.array_equal(r.rowids.cpu().numpy().view(np.uint32), want[1])
+            q.release()
+        t.release()
+cctx.close()
 torch.cuda.synchronize()
 print("sanitize workload ok")
