@@ -46,6 +46,13 @@ def parse():
     ap.add_argument("--comm1", action="store_true",
                     help="testing: give the N=1 context a one-rank NCCL communicator (the N>1 "
                          "collectives on the step's critical path, without peers)")
+    ap.add_argument("--same-device", action="store_true",
+                    help="testing: every rank on cuda:0 (torch.distributed over gloo; the ranks "
+                         "time-slice one GPU, so timings are meaningless) to exercise the N > 1 "
+                         "path on a one-GPU box")
+    ap.add_argument("--peers1", action="store_true",
+                    help="testing: give the N=1 context a one-rank peer exchange (the N>1 "
+                         "exchange on the step's critical path)")
     return ap.parse_args()
 
 
@@ -203,8 +210,11 @@ def measured_peaks():
         return {}
 
 
-def ncu_traffic(kernel, config):
-    """dram__bytes_read.sum + dram__bytes_write.sum per launch from the committed ncu capture."""
+def ncu_traffic(kernel, config, applies=True):
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch from the committed ncu capture
+    (captured at N = 1 on the full table: null for other launch shapes)."""
+    if not applies:
+        return None
     try:
         d = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))
         return d.get(config, {}).get(kernel)
@@ -275,6 +285,51 @@ def run_reference(args):
 
 # ---- our arm ---------------------------------------------------------------------------------------
 
+_GLOO = False
+
+
+def _red_dev(dev):
+    """Device of the small tensors reduced over torch.distributed (CPU under --same-device/gloo)."""
+    return "cpu" if _GLOO else dev
+
+
+def setup_exchange(ctx, sel, sdist, dist, dev):
+    """Cross-rank combination for N > 1: the library's own exchange over peer memory
+    (CUDA IPC + NVLink stores, fused into the push-down's prefix kernel; include/sel.h
+    sel_ctx_set_peers) when every rank can map every other rank's buffer — tried first on a
+    throw-away context, agreed by all ranks — else NCCL. SEL_XCHG=nccl forces NCCL."""
+    import torch
+    ok = os.environ.get("SEL_XCHG", "peers") != "nccl"
+    why = "SEL_XCHG=nccl"
+    if ok:
+        # every rank reaches each collective below whatever fails locally (no rank left waiting)
+        mapped = False
+        try:
+            h = ctx.peer_handle()
+        except Exception as ex:  # noqa: BLE001 - any failure falls back to NCCL on every rank
+            h, ok, why = None, False, f"peers unavailable: {type(ex).__name__}: {ex}"
+        handles = [None] * dist.get_world_size()
+        dist.all_gather_object(handles, h)
+        if ok and all(x is not None for x in handles):
+            try:
+                ctx.set_peers(len(handles), dist.get_rank(), handles)
+                mapped = True
+            except Exception as ex:  # noqa: BLE001
+                ok, why = False, f"peers unavailable: {type(ex).__name__}: {ex}"
+        else:
+            ok = False
+        flag = torch.tensor([1 if ok else 0], dtype=torch.int32, device=_red_dev(dev))
+        dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+        ok = bool(flag.item())
+        if not ok and mapped:
+            ctx.drop_peers()
+            why = why if why != "SEL_XCHG=nccl" else "a rank could not map the peers' buffers"
+    if ok:
+        return "peers (CUDA IPC, NVLink release stores, fused into the prefix kernel)"
+    sdist.setup_comm(ctx)
+    return f"nccl ({why})"
+
+
 def run_ours(args):
     import numpy as np
     import torch
@@ -288,10 +343,17 @@ def run_ours(args):
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
     if world != args.gpus:
         args.gpus = world
+    global _GLOO
+    if args.same_device:
+        local_rank = 0
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if args.same_device:
+            _GLOO = True
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
 
     from paper_1806_08384_b200 import dist as sdist
     n, gen, node, proj, desc = workload(args.config, args.rows)
@@ -299,10 +361,15 @@ def run_ours(args):
     T = gen(s, e - s, dev)
     torch.cuda.synchronize()
     ctx = sel.Context(dev)
+    xchg = None
     if world > 1:
-        sdist.setup_comm(ctx)
+        xchg = setup_exchange(ctx, sel, sdist, dist, dev)
     elif args.comm1:
         ctx.set_comm(1, 0, sel.Context.new_unique_id())
+        xchg = "nccl (one rank)"
+    elif args.peers1:
+        ctx.set_peers(1, 0, [ctx.peer_handle()])
+        xchg = "peers (one rank)"
     bms = key_sets(args.config)   # NEXT(3) key sets (c6), registered once like the table
     bm_dev = []
     for words, nbits in bms:
@@ -374,7 +441,7 @@ def run_ours(args):
     cb, pb, step_b = algo_bytes(T, pc, proj, local_count, pd_path, consts)
     my_bytes = step_b
     t = torch.tensor([dev_ms, my_bytes, cb, pb, statistics.mean(count_ms), statistics.mean(push_ms)],
-                     dtype=torch.float64, device=dev)
+                     dtype=torch.float64, device=_red_dev(dev))
     if world > 1:
         tmax = t.clone(); dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
         tsum = t.clone(); dist.all_reduce(tsum, op=dist.ReduceOp.SUM)
@@ -484,7 +551,7 @@ def run_ours(args):
         eb.record(s_out)
         torch.cuda.synchronize()
         assert all(c == global_count for c in counts)
-        e_ms = torch.tensor([ea.elapsed_time(eb)], dtype=torch.float64, device=dev)
+        e_ms = torch.tensor([ea.elapsed_time(eb)], dtype=torch.float64, device=_red_dev(dev))
         if world > 1:
             dist.all_reduce(e_ms, op=dist.ReduceOp.MAX)
         e_step = float(e_ms[0]) / args.e2e_steps
@@ -538,12 +605,12 @@ def run_ours(args):
         pb_sector = (T.n_rows * sum(w_all[j] for j in pc)
                      + sum(32 * sectors(w_all[j]) for j in set(proj) if j not in pc) + write_b)
     roof_count = {"bound": "hbm", "achieved": round(count_gbs, 2), "peak": hbm, "unit": "GB/s",
-                  "frac": round(count_gbs / hbm, 4), "traffic": ncu_traffic("count_kernel", args.config),
+                  "frac": round(count_gbs / hbm, 4), "traffic": ncu_traffic("count_kernel", args.config, world == 1 and not args.rows),
                   "kernel": "count_kernel", "ms": round(count_k, 4),
                   "algorithmic_bytes_per_launch": int(cb), "peak_source": peak_note}
     push_sector_gbs = pb_sector / (push_k / 1000) / 1e9
     roof_push = {"bound": "hbm", "achieved": round(push_gbs, 2), "peak": hbm, "unit": "GB/s",
-                 "frac": round(push_gbs / hbm, 4), "traffic": ncu_traffic(push_name, args.config),
+                 "frac": round(push_gbs / hbm, 4), "traffic": ncu_traffic(push_name, args.config, world == 1 and not args.rows),
                  "kernel": push_name, "ms": round(push_k, 4),
                  "algorithmic_bytes_per_launch": int(pb), "peak_source": peak_note,
                  "sector_bytes_per_launch": int(pb_sector),
@@ -563,6 +630,7 @@ def run_ours(args):
             "config": {"workload": f"{args.config}: {desc}", "global_rows": n,
                        "rows_per_gpu": e - s, "selected": global_count,
                        "parallelism": f"row-shard x{world}",
+                       "exchange": xchg,
                        "l2": "inputs larger than L2 (no flush needed)",
                        "step": ("sel_execute = count (keeping the selection) -> device-side gate -> "
                                 "materialise" + (", per table.execute()" if prepared is None else
@@ -587,6 +655,10 @@ def run_ours(args):
     if prepared is not None:
         prepared.release()
     table.release()
+    if world > 1:
+        if ctx.nranks > 1 and xchg and xchg.startswith("peers"):
+            ctx.drop_peers()          # every rank unmaps before any rank frees its buffer
+        dist.barrier()
     ctx.close()
     if world > 1:
         dist.destroy_process_group()

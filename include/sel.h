@@ -90,6 +90,32 @@ sel_status sel_ctx_create(int cuda_device, sel_ctx* out);
  * (already set). */
 sel_status sel_ctx_set_comm(sel_ctx ctx, int nranks, int rank, const void* nccl_unique_id);
 
+/* Cross-rank exchange over peer memory, without NCCL ("a one-shot peer write of each
+ * rank's count into a symmetric buffer over NVLink plus a flag"). Each rank owns a small
+ * symmetric buffer that every other rank maps through CUDA IPC; an exchange stores the rank's
+ * counts (epoch-tagged) into every rank's buffer with system-scope release stores over
+ * NVLink/NVSwitch and waits (acquire loads) until all ranks' values of that epoch arrived.
+ * Once set, EVERY cross-rank combination of the context uses it instead of NCCL: sel_count's
+ * sum, sel_pushdown's offsets, sel_count_batch / sel_count_sampled's sums, and sel_execute's
+ * one exchange per call — which runs inside the push-down's prefix kernel, fused with the
+ * materialisation it gates, also in prepared (graph) executes. A communicator is then not
+ * needed; if one is set as well, its nranks/rank must agree.
+ * sel_ctx_peer_handle: allocates the context's buffer (on first call) and writes its 64-byte
+ *   CUDA IPC handle to out64 (host memory), to be shared out of band (torch.distributed).
+ *   Errors: SEL_E_ARG, SEL_E_STATE (context destroyed), SEL_E_CUDA.
+ * sel_ctx_set_peers: `handles` = nranks consecutive 64-byte handles, rank r's at 64*r (this
+ *   rank's own entry is ignored). 1 <= nranks <= 32; the ranks may share a device (IPC maps
+ *   a buffer of the same GPU too). Collective in effect: every rank must call it and then
+ *   issue the same sequence of probes. A wait longer than ~10 s (a rank missing) makes the
+ *   call fail with SEL_E_STATE instead of hanging.
+ *   nranks == 0 drops the peers again (unmaps the others' buffers; handles may be NULL) — e.g.
+ *   when not every rank could map every buffer and all fall back to a communicator; every rank
+ *   should drop its peers before any rank destroys its context.
+ *   Errors: SEL_E_ARG (bad ranks, disagreeing with the communicator), SEL_E_STATE (already
+ *   set, or no handle exported yet), SEL_E_CUDA (cudaIpcOpenMemHandle failed). */
+sel_status sel_ctx_peer_handle(sel_ctx ctx, void* out64);
+sel_status sel_ctx_set_peers(sel_ctx ctx, int nranks, int rank, const void* handles);
+
 /* Writes a fresh 128-byte ncclUniqueId into `out128` (call on rank 0 only). SEL_E_NCCL on
  * failure. */
 sel_status sel_nccl_unique_id(void* out128);

@@ -20,6 +20,7 @@ STATUS_NAMES = {0: "SEL_OK", 1: "SEL_E_ARG", 2: "SEL_E_ALIGN", 3: "SEL_E_TYPE",
 
 # Every symbol include/sel.h declares (tests check the library exports exactly these).
 EXPORTS = ["sel_ctx_create", "sel_ctx_set_comm", "sel_nccl_unique_id", "sel_ctx_destroy",
+           "sel_ctx_peer_handle", "sel_ctx_set_peers",
            "sel_ctx_set_timing", "sel_ctx_last_kernel_ms", "sel_table_register",
            "sel_table_release", "sel_count", "sel_count_ex", "sel_execute", "sel_pushdown",
            "sel_ctx_last_times", "sel_count_batch", "sel_count_sampled",
@@ -56,6 +57,8 @@ def lib() -> ctypes.CDLL:
     sig = {
         "sel_ctx_create": (i32, [i32, ctypes.POINTER(vp)]),
         "sel_ctx_set_comm": (i32, [vp, i32, i32, vp]),
+        "sel_ctx_peer_handle": (i32, [vp, vp]),
+        "sel_ctx_set_peers": (i32, [vp, i32, i32, vp]),
         "sel_nccl_unique_id": (i32, [vp]),
         "sel_ctx_destroy": (None, [vp]),
         "sel_ctx_set_timing": (i32, [vp, i32]),

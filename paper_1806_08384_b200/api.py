@@ -54,6 +54,26 @@ class Context:
         check(lib().sel_ctx_set_comm(self._h, nranks, rank, buf))
         self.nranks, self.rank = nranks, rank
 
+    def peer_handle(self) -> bytes:
+        """This rank's 64-byte CUDA IPC handle of its exchange buffer (include/sel.h)."""
+        buf = ctypes.create_string_buffer(64)
+        check(lib().sel_ctx_peer_handle(self._h, buf))
+        return buf.raw
+
+    def set_peers(self, nranks: int, rank: int, handles) -> None:
+        """Exchange counts over peer memory with the ranks whose handles are given (one per rank,
+        in rank order): the library's own collective, replacing NCCL for every combination."""
+        handles = [bytes(h) for h in handles]
+        if len(handles) != nranks or any(len(h) != 64 for h in handles):
+            raise ValueError("need nranks 64-byte handles")
+        buf = ctypes.create_string_buffer(b"".join(handles), 64 * nranks)
+        check(lib().sel_ctx_set_peers(self._h, nranks, rank, buf))
+        self.nranks, self.rank = nranks, rank
+
+    def drop_peers(self) -> None:
+        """Unmap the other ranks' exchange buffers (every rank before any rank closes)."""
+        check(lib().sel_ctx_set_peers(self._h, 0, 0, None))
+
     def enable_timing(self, on: bool = True) -> None:
         check(lib().sel_ctx_set_timing(self._h, 1 if on else 0))
 

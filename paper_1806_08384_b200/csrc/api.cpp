@@ -160,6 +160,14 @@ struct sel_ctx_s {
   cudaStream_t cap_stream = nullptr;  // stream-capture source for prepared executes
   bool capturing = false;             // timing events become graph event-record nodes
   int count_nw = 0;                   // SEL_COUNT_NW: 8 forces 8-warp count CTAs
+  // the library's own exchange over peer memory (sel_ctx_set_peers; sel_internal.h PeerXchg)
+  bool peers = false;
+  uint64_t* peer_buf = nullptr;       // this rank's symmetric buffer (exported by CUDA IPC)
+  uint64_t** peer_ptrs = nullptr;     // device array of the n buffers as mapped here
+  std::vector<void*> peer_opened;     // IPC mappings to close
+  uint32_t* peer_epoch = nullptr;     // device exchange counter
+  uint32_t* h_peer_err = nullptr;     // host-mapped timeout flag
+  PeerXchg xg{};
 };
 
 struct sel_table_s {
@@ -190,6 +198,19 @@ namespace {
 
 constexpr int kMaxGrid = 148 * 32;
 constexpr size_t kMaxBitmaps = 65536;  // ids fit the instruction's u16 `a`
+
+// Cross-rank combination needed: a communicator (NCCL) or peers (the library's own exchange).
+bool multi(sel_ctx c) { return c->comm != nullptr || c->peers; }
+
+// After a synchronisation that followed peer exchanges: a timed-out wait (a rank missing) is an
+// error of the call (the flag is reset).
+sel_status peer_status(sel_ctx c) {
+  if (c->peers && c->h_peer_err && *(volatile uint32_t*)c->h_peer_err) {
+    *(volatile uint32_t*)c->h_peer_err = 0;
+    return set_error(SEL_E_STATE, "peer exchange timed out (a rank did not take part)");
+  }
+  return SEL_OK;
+}
 
 template <class P>
 bool fits_block(const Plan& plan, size_t nslots, uint32_t nproj) {
@@ -532,6 +553,8 @@ sel_status sel_ctx_set_comm(sel_ctx ctx, int nranks, int rank, const void* nccl_
   if (!ctx || !nccl_unique_id || nranks < 1 || nranks > kMaxRanks || rank < 0 || rank >= nranks)
     return set_error(SEL_E_ARG, "bad communicator arguments");
   if (ctx->comm) return set_error(SEL_E_STATE, "communicator already set");
+  if (ctx->peers && (ctx->nranks != nranks || ctx->rank != rank))
+    return set_error(SEL_E_ARG, "communicator ranks differ from the peers'");
   NcclApi& n = nccl();
   if (!n.loaded) return set_error(SEL_E_NCCL, n.error);
   DeviceGuard g(ctx->device);
@@ -546,11 +569,107 @@ sel_status sel_ctx_set_comm(sel_ctx ctx, int nranks, int rank, const void* nccl_
   return SEL_OK;
 }
 
+sel_status sel_ctx_peer_handle(sel_ctx ctx, void* out64) {
+  clear_error();
+  if (!ctx || !out64) return set_error(SEL_E_ARG, "null argument");
+  if (ctx->destroyed) return set_error(SEL_E_STATE, "context destroyed");
+  DeviceGuard g(ctx->device);
+  if (!g.ok) return set_error(SEL_E_CUDA, "cudaSetDevice failed");
+  if (!ctx->peer_buf) {
+    const size_t bytes = 2 * (size_t)kMaxPeers * kMaxXchgVals * sizeof(uint64_t);
+    cudaError_t e = cudaMalloc(&ctx->peer_buf, bytes);
+    if (e == cudaSuccess) e = cudaMemset(ctx->peer_buf, 0, bytes);
+    if (e == cudaSuccess) e = cudaMalloc(&ctx->peer_epoch, sizeof(uint32_t));
+    if (e == cudaSuccess) e = cudaMemset(ctx->peer_epoch, 0, sizeof(uint32_t));
+    if (e == cudaSuccess) e = cudaHostAlloc(&ctx->h_peer_err, sizeof(uint32_t), cudaHostAllocMapped);
+    if (e == cudaSuccess) *ctx->h_peer_err = 0;
+    if (e == cudaSuccess) e = cudaDeviceSynchronize();
+    if (e != cudaSuccess) return set_error(SEL_E_CUDA, cuda_msg("peer buffer", e));
+  }
+  cudaIpcMemHandle_t h;
+  cudaError_t e = cudaIpcGetMemHandle(&h, ctx->peer_buf);
+  if (e != cudaSuccess) return set_error(SEL_E_CUDA, cuda_msg("cudaIpcGetMemHandle", e));
+  static_assert(sizeof(h) == 64, "cudaIpcMemHandle_t is 64 bytes");
+  std::memcpy(out64, &h, sizeof(h));
+  return SEL_OK;
+}
+
+sel_status sel_ctx_set_peers(sel_ctx ctx, int nranks, int rank, const void* handles) {
+  clear_error();
+  if (ctx && nranks == 0) {  // drop the peers: unmap the others' buffers, keep this rank's
+    DeviceGuard g(ctx->device);
+    for (void* p : ctx->peer_opened) cudaIpcCloseMemHandle(p);
+    ctx->peer_opened.clear();
+    if (ctx->peer_ptrs) cudaFree(ctx->peer_ptrs);
+    ctx->peer_ptrs = nullptr;
+    ctx->xg = PeerXchg{};
+    if (ctx->peers && !ctx->comm) ctx->nranks = 1, ctx->rank = 0;
+    ctx->peers = false;
+    ++ctx->alloc_gen;
+    return SEL_OK;
+  }
+  if (!ctx || !handles || nranks < 1 || nranks > kMaxPeers || rank < 0 || rank >= nranks)
+    return set_error(SEL_E_ARG, "bad peer arguments");
+  if (ctx->peers) return set_error(SEL_E_STATE, "peers already set");
+  if (!ctx->peer_buf) return set_error(SEL_E_STATE, "export this rank's handle (sel_ctx_peer_handle) first");
+  if (ctx->comm && (ctx->nranks != nranks || ctx->rank != rank))
+    return set_error(SEL_E_ARG, "peer ranks differ from the communicator's");
+  DeviceGuard g(ctx->device);
+  if (!g.ok) return set_error(SEL_E_CUDA, "cudaSetDevice failed");
+  std::vector<uint64_t*> ptrs(nranks, nullptr);
+  std::vector<void*> opened;
+  cudaError_t e = cudaSuccess;
+  for (int r = 0; r < nranks && e == cudaSuccess; ++r) {
+    if (r == rank) {
+      ptrs[r] = ctx->peer_buf;
+      continue;
+    }
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, static_cast<const char*>(handles) + 64 * (size_t)r, sizeof(h));
+    void* p = nullptr;
+    e = cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess);
+    if (e == cudaSuccess) {
+      opened.push_back(p);
+      ptrs[r] = static_cast<uint64_t*>(p);
+    }
+  }
+  uint64_t** dptrs = nullptr;
+  if (e == cudaSuccess) e = cudaMalloc(&dptrs, nranks * sizeof(uint64_t*));
+  if (e == cudaSuccess)
+    e = cudaMemcpy(dptrs, ptrs.data(), nranks * sizeof(uint64_t*), cudaMemcpyHostToDevice);
+  uint32_t* derr = nullptr;
+  if (e == cudaSuccess) e = cudaHostGetDevicePointer(reinterpret_cast<void**>(&derr), ctx->h_peer_err, 0);
+  if (e != cudaSuccess) {
+    for (void* p : opened) cudaIpcCloseMemHandle(p);
+    if (dptrs) cudaFree(dptrs);
+    return set_error(SEL_E_CUDA, cuda_msg("opening the peers' buffers", e));
+  }
+  ctx->peer_opened = opened;
+  ctx->peer_ptrs = dptrs;
+  ctx->xg = PeerXchg{dptrs, ctx->peer_buf, ctx->peer_epoch, derr, nranks, rank};
+  ctx->peers = true;
+  ctx->nranks = nranks;
+  ctx->rank = rank;
+  ++ctx->alloc_gen;   // prepared executes re-capture with the exchange
+  return SEL_OK;
+}
+
 namespace {
 void release_ctx_resources(sel_ctx c) {
   DeviceGuard g(c->device);
   if (c->comm && nccl().loaded) nccl().CommDestroy(c->comm);
   c->comm = nullptr;
+  for (void* p : c->peer_opened) cudaIpcCloseMemHandle(p);
+  c->peer_opened.clear();
+  if (c->peer_ptrs) cudaFree(c->peer_ptrs);
+  if (c->peer_buf) cudaFree(c->peer_buf);
+  if (c->peer_epoch) cudaFree(c->peer_epoch);
+  if (c->h_peer_err) cudaFreeHost(c->h_peer_err);
+  c->peer_ptrs = nullptr;
+  c->peer_buf = nullptr;
+  c->peer_epoch = nullptr;
+  c->h_peer_err = nullptr;
+  c->peers = false;
   if (c->s.partials) cudaFree(c->s.partials);
   if (c->s.done) cudaFree(c->s.done);
   if (c->s.result) cudaFree(c->s.result);
@@ -955,7 +1074,10 @@ sel_status enqueue_count(sel_table t, const Plan& plan, uint32_t flags, const ui
     e = cudaMemcpyAsync(d_out, h, sizeof(uint64_t), cudaMemcpyHostToDevice, stream);
     if (e != cudaSuccess) return set_error(SEL_E_CUDA, cuda_msg("cudaMemcpyAsync", e));
   }
-  if (c->comm && allreduce) {  // one 8-byte all-reduce on the probe stream
+  if (c->peers && allreduce) {  // SURVEY §8a a4 over peer memory: the sum of the exchanged counts
+    const int le = launch_peer_exchange(c->xg, d_out, 1, nullptr, d_out, stream);
+    if (le != cudaSuccess) return set_error(SEL_E_CUDA, cuda_msg("peer exchange", (cudaError_t)le));
+  } else if (c->comm && allreduce) {  // one 8-byte all-reduce on the probe stream
     ncclResult_t r = nccl().AllReduce(d_out, d_out, 1, ncclUint64, ncclSum, c->comm, stream);
     if (r != ncclSuccess) return set_error(SEL_E_NCCL, nccl_msg("ncclAllReduce", r));
   }
@@ -968,7 +1090,8 @@ sel_status enqueue_count(sel_table t, const Plan& plan, uint32_t flags, const ui
 sel_status enqueue_pushdown_sel(sel_table t, const Plan& plan, const uint32_t* proj_cols,
                                 uint32_t nproj, uint32_t* out_rowids, void* const* out_cols,
                                 uint64_t capacity_rows, bool gate, uint64_t gate_max,
-                                cudaStream_t stream, int gate_ranks = 0) {
+                                cudaStream_t stream, int gate_ranks = 0,
+                                const PeerXchg* xg = nullptr) {
   sel_ctx c = t->ctx;
   const auto consts = const_columns(t, plan);
   const uint64_t n = t->local_rows;
@@ -1003,12 +1126,12 @@ sel_status enqueue_pushdown_sel(sel_table t, const Plan& plan, const uint32_t* p
     DevProgramSmall p;
     fill_sel(&p);
     le = launch_pushdown_sel_small(p, n, out_rowids, grid_for(c, units, occupancy_pushdown_sel_small()),
-                                   c->s, c->sel, stream, gate_ranks);
+                                   c->s, c->sel, stream, gate_ranks, xg);
   } else {
     static thread_local DevProgramLarge p;
     fill_sel(&p);
     le = launch_pushdown_sel_large(p, n, out_rowids, grid_for(c, units, occupancy_pushdown_sel_large()),
-                                   c->s, c->sel, stream, gate_ranks);
+                                   c->s, c->sel, stream, gate_ranks, xg);
   }
   if (le != cudaSuccess) return set_error(SEL_E_CUDA, cuda_msg("push-down kernel launch", (cudaError_t)le));
   c->last_pd_path = 1;
@@ -1025,13 +1148,18 @@ sel_status gather_counts(sel_ctx c, uint64_t local, void* cuda_stream) {
   c->h_result[0] = local;
   cudaError_t e = cudaMemcpyAsync(c->s.result, c->h_result, sizeof(uint64_t), cudaMemcpyHostToDevice, stream);
   if (e != cudaSuccess) return set_error(SEL_E_CUDA, cuda_msg("cudaMemcpyAsync", e));
-  ncclResult_t r = nccl().AllGather(c->s.result, c->s.result + 1, 1, ncclUint64, c->comm, stream);
-  if (r != ncclSuccess) return set_error(SEL_E_NCCL, nccl_msg("ncclAllGather", r));
+  if (c->peers) {
+    const int le = launch_peer_exchange(c->xg, c->s.result, 1, c->s.result + 1, nullptr, stream);
+    if (le != cudaSuccess) return set_error(SEL_E_CUDA, cuda_msg("peer exchange", (cudaError_t)le));
+  } else {
+    ncclResult_t r = nccl().AllGather(c->s.result, c->s.result + 1, 1, ncclUint64, c->comm, stream);
+    if (r != ncclSuccess) return set_error(SEL_E_NCCL, nccl_msg("ncclAllGather", r));
+  }
   e = cudaMemcpyAsync(c->h_result + 1, c->s.result + 1, c->nranks * sizeof(uint64_t),
                       cudaMemcpyDeviceToHost, stream);
   if (e == cudaSuccess) e = cudaStreamSynchronize(stream);
   if (e != cudaSuccess) return set_error(SEL_E_CUDA, cuda_msg("all-gather result", e));
-  return SEL_OK;
+  return peer_status(c);
 }
 
 // The device work of a device-gated Execute on `stream` (sel_execute, prepared executes): count
@@ -1046,20 +1174,21 @@ sel_status enqueue_execute(sel_table t, const Plan& plan, const uint32_t* proj, 
   sel_status st = enqueue_count(t, plan, SEL_KEEP_SELECTION, proj, nkeep, s, c->s.result + kGateSlot,
                                 false);
   if (st != SEL_OK) return st;
-  if (c->comm) {  // SURVEY §8a a4 + a7 in one collective
+  if (c->comm && !c->peers) {  // SURVEY §8a a4 + a7 in one collective
     ncclResult_t r = nccl().AllGather(c->s.result + kGateSlot, c->s.result + 1, 1, ncclUint64,
                                       c->comm, s);
     if (r != ncclSuccess) return set_error(SEL_E_NCCL, nccl_msg("ncclAllGather", r));
   }
   if (c->timing) record(c, c->ev2, s);
+  // with peers the exchange runs inside the prefix kernel, right before the gated push-down
   st = enqueue_pushdown_sel(t, plan, proj, nproj, out_rowids, outs, capacity, true, max_size, s,
-                            c->comm ? c->nranks : 0);
+                            c->comm && !c->peers ? c->nranks : 0, c->peers ? &c->xg : nullptr);
   if (st != SEL_OK) return st;
   if (c->timing) record(c, c->ev3, s);
   cudaError_t e = cudaMemcpyAsync(c->h_result + kGateSlot, c->s.result + kGateSlot, sizeof(uint64_t),
                                   cudaMemcpyDeviceToHost, s);
   if (e == cudaSuccess) {
-    if (c->comm)
+    if (multi(c))
       e = cudaMemcpyAsync(c->h_result + 1, c->s.result + 1, c->nranks * sizeof(uint64_t),
                           cudaMemcpyDeviceToHost, s);
     else
@@ -1075,7 +1204,7 @@ uint64_t execute_outputs(sel_ctx c, uint64_t max_size, uint64_t* out_local_count
   const uint64_t count = c->h_result[kGateSlot];
   if (count > max_size) return count;  // "throw exception": nothing written
   uint64_t local = c->h_result[0], offset = 0;
-  if (c->comm) {
+  if (multi(c)) {
     for (int r2 = 0; r2 < c->rank; ++r2) offset += c->h_result[1 + r2];
     local = c->h_result[1 + c->rank];
   }
@@ -1124,11 +1253,12 @@ uint64_t sel_count_ex(sel_table t, const void* prog, size_t prog_bytes, uint32_t
   const uint64_t n = t->local_rows;
   const bool scan = n > 0 && plan.path != PATH_CONST;
   if ((flags & SEL_KEEP_SELECTION) && !scan) c->kept_table = nullptr;
-  if (!scan && !c->comm) return plan.path == PATH_CONST && plan.const_value ? n : 0;
+  if (!scan && !multi(c)) return plan.path == PATH_CONST && plan.const_value ? n : 0;
   if (enqueue_count(t, plan, flags, keep_cols, nkeep, stream, c->s.result) != SEL_OK) return SEL_ERR;
   cudaError_t e = cudaMemcpyAsync(c->h_result, c->s.result, sizeof(uint64_t), cudaMemcpyDeviceToHost, stream);
   if (e == cudaSuccess) e = cudaStreamSynchronize(stream);
   if (e != cudaSuccess) return fail64(SEL_E_CUDA, cuda_msg("count result", e));
+  if (peer_status(c) != SEL_OK) return SEL_ERR;
   if (scan && c->timing) {
     cudaEventElapsedTime(&c->last_ms, c->ev0, c->ev1);
     c->last_count_ms = c->last_ms;
@@ -1271,19 +1401,25 @@ uint64_t pushdown_impl(sel_table t, const void* prog, size_t prog_bytes, const u
     if (c->timing) cudaEventRecord(c->ev1, stream);
   } else {
     c->h_result[0] = 0;
-    if (c->comm && collective) {
+    if (multi(c) && collective) {
       e = cudaMemcpyAsync(c->s.result, c->h_result, sizeof(uint64_t), cudaMemcpyHostToDevice, stream);
       if (e != cudaSuccess) return fail64(SEL_E_CUDA, cuda_msg("cudaMemcpyAsync", e));
     }
   }
   uint64_t local = 0, offset = 0, total = 0;
-  if (c->comm && collective) {  // all-gather the per-rank counts, exclusive scan on the host
-    ncclResult_t r = nccl().AllGather(c->s.result, c->s.result + 1, 1, ncclUint64, c->comm, stream);
-    if (r != ncclSuccess) return fail64(SEL_E_NCCL, nccl_msg("ncclAllGather", r));
+  if (multi(c) && collective) {  // all-gather the per-rank counts, exclusive scan on the host
+    if (c->peers) {
+      const int le2 = launch_peer_exchange(c->xg, c->s.result, 1, c->s.result + 1, nullptr, stream);
+      if (le2 != cudaSuccess) return fail64(SEL_E_CUDA, cuda_msg("peer exchange", (cudaError_t)le2));
+    } else {
+      ncclResult_t r = nccl().AllGather(c->s.result, c->s.result + 1, 1, ncclUint64, c->comm, stream);
+      if (r != ncclSuccess) return fail64(SEL_E_NCCL, nccl_msg("ncclAllGather", r));
+    }
     e = cudaMemcpyAsync(c->h_result + 1, c->s.result + 1, c->nranks * sizeof(uint64_t),
                         cudaMemcpyDeviceToHost, stream);
     if (e == cudaSuccess) e = cudaStreamSynchronize(stream);
     if (e != cudaSuccess) return fail64(SEL_E_CUDA, cuda_msg("push-down result", e));
+    if (peer_status(c) != SEL_OK) return SEL_ERR;
     for (int r2 = 0; r2 < c->nranks; ++r2) {
       if (r2 < c->rank) offset += c->h_result[1 + r2];
       total += c->h_result[1 + r2];
@@ -1382,13 +1518,17 @@ uint64_t sel_count_sampled(sel_table t, const void* prog, size_t prog_bytes, uin
   c->h_result[1] = sample_rows;
   e = cudaMemcpyAsync(c->s.result + 1, c->h_result + 1, sizeof(uint64_t), cudaMemcpyHostToDevice, stream);
   if (e != cudaSuccess) return fail64(SEL_E_CUDA, cuda_msg("cudaMemcpyAsync", e));
-  if (c->comm) {
+  if (c->peers) {
+    const int le2 = launch_peer_exchange(c->xg, c->s.result, 2, nullptr, c->s.result, stream);
+    if (le2 != cudaSuccess) return fail64(SEL_E_CUDA, cuda_msg("peer exchange", (cudaError_t)le2));
+  } else if (c->comm) {
     ncclResult_t r = nccl().AllReduce(c->s.result, c->s.result, 2, ncclUint64, ncclSum, c->comm, stream);
     if (r != ncclSuccess) return fail64(SEL_E_NCCL, nccl_msg("ncclAllReduce(sampled)", r));
   }
   e = cudaMemcpyAsync(c->h_result, c->s.result, 2 * sizeof(uint64_t), cudaMemcpyDeviceToHost, stream);
   if (e == cudaSuccess) e = cudaStreamSynchronize(stream);
   if (e != cudaSuccess) return fail64(SEL_E_CUDA, cuda_msg("sampled count result", e));
+  if (peer_status(c) != SEL_OK) return SEL_ERR;
   if (out_sample_rows) *out_sample_rows = c->h_result[1];
   return c->h_result[0];
 }
@@ -1486,13 +1626,17 @@ sel_status sel_count_batch(sel_table t, const void* const* progs, const size_t* 
     if (le != cudaSuccess) return set_error(SEL_E_CUDA, cuda_msg("batch kernel launch", (cudaError_t)le));
     if (c->timing) cudaEventRecord(c->ev1, stream);
   }
-  if (c->comm) {
+  if (c->peers) {
+    const int le2 = launch_peer_exchange(c->xg, d_out, (int)nprog, nullptr, d_out, stream);
+    if (le2 != cudaSuccess) return set_error(SEL_E_CUDA, cuda_msg("peer exchange", (cudaError_t)le2));
+  } else if (c->comm) {
     ncclResult_t r = nccl().AllReduce(d_out, d_out, nprog, ncclUint64, ncclSum, c->comm, stream);
     if (r != ncclSuccess) return set_error(SEL_E_NCCL, nccl_msg("ncclAllReduce(batch)", r));
   }
   e = cudaMemcpyAsync(c->h_result + 1, d_out, nprog * sizeof(uint64_t), cudaMemcpyDeviceToHost, stream);
   if (e == cudaSuccess) e = cudaStreamSynchronize(stream);
   if (e != cudaSuccess) return set_error(SEL_E_CUDA, cuda_msg("batch result", e));
+  if (peer_status(c) != SEL_OK) return g_status;
   if (n > 0 && nop > 0 && c->timing) {
     cudaEventElapsedTime(&c->last_ms, c->ev0, c->ev1);
     c->last_count_ms = c->last_ms;
@@ -1526,7 +1670,7 @@ uint64_t sel_execute(sel_table t, const void* prog, size_t prog_bytes, const uin
   const bool scan = t->local_rows > 0 && plan.path != PATH_CONST;
   if (!scan || c->force_single) {  // host-side gate: count, then (maybe) the push-down
     uint64_t local;
-    if (c->comm) {
+    if (multi(c)) {
       local = scan ? 0 : (plan.path == PATH_CONST && plan.const_value ? t->local_rows : 0);
       if (scan) {
         cudaStream_t stream = (cudaStream_t)cuda_stream;
@@ -1549,7 +1693,7 @@ uint64_t sel_execute(sel_table t, const void* prog, size_t prog_bytes, const uin
       if (local == SEL_ERR) return SEL_ERR;
     }
     uint64_t count = local, offset = 0;
-    if (c->comm) {
+    if (multi(c)) {
       count = 0;
       for (int r2 = 0; r2 < c->nranks; ++r2) {
         if (r2 < c->rank) offset += c->h_result[1 + r2];
@@ -1578,6 +1722,7 @@ uint64_t sel_execute(sel_table t, const void* prog, size_t prog_bytes, const uin
   if (st != SEL_OK) return SEL_ERR;
   cudaError_t e = cudaStreamSynchronize(stream);
   if (e != cudaSuccess) return fail64(SEL_E_CUDA, cuda_msg("execute result", e));
+  if (peer_status(c) != SEL_OK) return SEL_ERR;
   c->kept_table = t;
   c->kept_prog.assign(static_cast<const char*>(prog), prog_bytes);
   if (c->timing) {
@@ -1710,6 +1855,7 @@ uint64_t sel_prepared_execute(sel_prepared q, uint64_t* out_local_count,
   cudaError_t e = cudaGraphLaunch(q->exec, stream);
   if (e == cudaSuccess) e = cudaStreamSynchronize(stream);
   if (e != cudaSuccess) return fail64(SEL_E_CUDA, cuda_msg("prepared execute", e));
+  if (peer_status(c) != SEL_OK) return SEL_ERR;
   c->kept_table = t;
   c->kept_prog = q->prog;
   c->kept_cols = q->kept_cols;

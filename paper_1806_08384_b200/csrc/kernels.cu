@@ -889,14 +889,87 @@ __global__ void __launch_bounds__(kThreads) superblock_sum_kernel(const uint16_t
 #endif
 
 // Exclusive prefix of the per-64-chunk sums kept by the count kernel (one CTA; <= 65536 sums).
+// ---- peer exchange (sel_internal.h PeerXchg) -------------------------------------------------
+__device__ __forceinline__ void st_release_sys(uint64_t* p, uint64_t v) {
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ uint64_t ld_acquire_sys(const uint64_t* p) {
+  uint64_t v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ uint64_t globaltimer_ns() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+
+// Run by all threads of ONE CTA (blockDim.x >= 32); see PeerXchg.
+__device__ void peer_gather_block(const PeerXchg& x, const uint64_t* src, int k, uint64_t* out,
+                                  uint64_t* sums) {
+  __shared__ uint32_t s_e;
+  __shared__ uint64_t s_v[kMaxXchgVals];
+  __shared__ uint64_t s_got[kMaxPeers * kMaxXchgVals];
+  const int t = threadIdx.x;
+  if (t == 0) {
+    s_e = *x.epoch + 1u;
+    *x.epoch = s_e;
+  }
+  if (t < k) s_v[t] = src[t];
+  __syncthreads();
+  const uint64_t e = s_e;
+  const uint32_t half = (s_e & 1u) * kMaxPeers * kMaxXchgVals;
+  // write my k values into row `rank` of every rank's buffer
+  for (int i = t; i < x.n * k; i += blockDim.x) {
+    const int r = i / k, j = i - r * k;
+    st_release_sys(x.peers[r] + half + x.rank * kMaxXchgVals + j, (e << 32) | (s_v[j] & 0xFFFFFFFFull));
+  }
+  // wait for every rank's row in my buffer
+  for (int i = t; i < x.n * k; i += blockDim.x) {
+    const int r = i / k, j = i - r * k;
+    const uint64_t* slot = x.mine + half + r * kMaxXchgVals + j;
+    uint64_t w = ld_acquire_sys(slot);
+    if ((w >> 32) != e) {
+      const uint64_t t0 = globaltimer_ns();
+      while (((w = ld_acquire_sys(slot)) >> 32) != e) {
+        if (globaltimer_ns() - t0 > 10000000000ull) {  // ~10 s: a rank is missing
+          atomicExch(x.err, 1u);
+          w = 0;
+          break;
+        }
+        __nanosleep(64);
+      }
+    }
+    s_got[i] = w & 0xFFFFFFFFull;
+  }
+  __syncthreads();
+  if (out)
+    for (int i = t; i < x.n * k; i += blockDim.x) out[i] = s_got[i];
+  if (sums && t < k) {
+    uint64_t acc = 0;
+    for (int r = 0; r < x.n; ++r) acc += s_got[r * k + t];
+    sums[t] = acc;
+  }
+  __syncthreads();
+}
+
+__global__ void __launch_bounds__(256) peer_exchange_kernel(const PeerXchg x, const uint64_t* src,
+                                                            int k, uint64_t* out, uint64_t* sums) {
+  peer_gather_block(x, src, k, out, sums);
+}
+
 // gate_ranks > 0 (sel_execute with a communicator): result[1..gate_ranks] holds the all-gathered
 // per-rank counts; their sum, the global count, is written to result[kGateSlot] for the gate of
 // the push-down kernel that follows (one collective per Execute instead of two).
+// With peers (xg.n > 0; sel_execute over peer memory) the exchange of the local count in
+// out_count[kGateSlot] runs first, fused here: gathered into out_count[1..n], summed into
+// out_count[kGateSlot].
 __global__ void __launch_bounds__(1024) superblock_prefix_kernel(const uint32_t* __restrict__ sb_sum,
                                                                  uint32_t* __restrict__ sb_prefix,
                                                                  uint32_t nsb, uint64_t* __restrict__ out_count,
-                                                                 int gate_ranks) {
+                                                                 int gate_ranks, const PeerXchg xg) {
   const uint32_t t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  if (xg.n > 0) peer_gather_block(xg, out_count + kGateSlot, 1, out_count + 1, out_count + kGateSlot);
   if (gate_ranks > 0 && t == 0) {
     uint64_t g = 0;
     for (int r = 0; r < gate_ranks; ++r) g += out_count[1 + r];
@@ -1217,7 +1290,9 @@ int launch_count_large(const DevProgramLarge& p, uint64_t n, int grid, const Scr
   return launch_count_t(p, n, grid, s, keep, nw, st);
 }
 int launch_pushdown_sel_small(const DevProgramSmall& p, uint64_t n, uint32_t* out_ids, int grid,
-                              const Scratch& s, const SelectionBufs& sb, void* st, int gate_ranks) {
+                              const Scratch& s, const SelectionBufs& sb, void* st, int gate_ranks,
+                              const PeerXchg* xg) {
+  const PeerXchg none{};
   const uint64_t nchunks = (n + kChunkRows - 1) / kChunkRows;
   const uint32_t nsb = (uint32_t)((nchunks + kSbChunks - 1) / kSbChunks);
 #if !SEL_SB_ATOMICS
@@ -1225,13 +1300,15 @@ int launch_pushdown_sel_small(const DevProgramSmall& p, uint64_t n, uint32_t* ou
                           (cudaStream_t)st>>>(sb.chunk_cnt, nchunks, sb.sb_sum);
 #endif
   superblock_prefix_kernel<<<1, 1024, 0, (cudaStream_t)st>>>(sb.sb_sum, sb.sb_prefix, nsb, s.result,
-                                                               gate_ranks);
+                                                               gate_ranks, xg ? *xg : none);
   pushdown_sel_kernel<DevProgramSmall><<<grid, kThreads, 0, (cudaStream_t)st>>>(p, n, sb, out_ids,
                                                                                 s.result + kGateSlot);
   return (int)cudaGetLastError();
 }
 int launch_pushdown_sel_large(const DevProgramLarge& p, uint64_t n, uint32_t* out_ids, int grid,
-                              const Scratch& s, const SelectionBufs& sb, void* st, int gate_ranks) {
+                              const Scratch& s, const SelectionBufs& sb, void* st, int gate_ranks,
+                              const PeerXchg* xg) {
+  const PeerXchg none{};
   const uint64_t nchunks = (n + kChunkRows - 1) / kChunkRows;
   const uint32_t nsb = (uint32_t)((nchunks + kSbChunks - 1) / kSbChunks);
 #if !SEL_SB_ATOMICS
@@ -1239,7 +1316,7 @@ int launch_pushdown_sel_large(const DevProgramLarge& p, uint64_t n, uint32_t* ou
                           (cudaStream_t)st>>>(sb.chunk_cnt, nchunks, sb.sb_sum);
 #endif
   superblock_prefix_kernel<<<1, 1024, 0, (cudaStream_t)st>>>(sb.sb_sum, sb.sb_prefix, nsb, s.result,
-                                                               gate_ranks);
+                                                               gate_ranks, xg ? *xg : none);
   pushdown_sel_kernel<DevProgramLarge><<<grid, kThreads, 0, (cudaStream_t)st>>>(p, n, sb, out_ids,
                                                                                 s.result + kGateSlot);
   return (int)cudaGetLastError();
@@ -1293,6 +1370,11 @@ int occupancy_count_fast(int fast_n, bool keep, size_t dyn) {
     case 8: return occupancy_of(count_kernel<DevProgramSmall, false, kWarpsPerCta, 4>, dyn);
     default: return occupancy_of(count_kernel<DevProgramSmall, true, kWarpsPerCta, 4>, dyn);
   }
+}
+int launch_peer_exchange(const PeerXchg& x, const uint64_t* src, int k, uint64_t* out,
+                         uint64_t* sums, void* st) {
+  peer_exchange_kernel<<<1, 256, 0, (cudaStream_t)st>>>(x, src, k, out, sums);
+  return (int)cudaGetLastError();
 }
 int launch_count_batch(const BatchProgram& p, uint64_t n, int grid, uint64_t* out, void* st) {
   count_batch_kernel<<<grid, kThreads, 0, (cudaStream_t)st>>>(p, n, out);

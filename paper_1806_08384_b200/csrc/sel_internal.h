@@ -172,6 +172,30 @@ struct Scratch {
   uint64_t status_cap;     // entries in status
 };
 
+// The library's own exchange over peer memory (sel_ctx_set_peers; SURVEY §8e "a one-shot peer
+// write of each rank's count into a symmetric buffer over NVLink plus a flag"). Every rank owns a
+// symmetric buffer `mine` of 2 x kMaxPeers x kMaxXchgVals u64 (two halves by exchange parity)
+// that every peer maps (CUDA IPC). An exchange of k values: the rank bumps its device epoch e,
+// stores (e << 32 | value) for each value into half e&1, row `rank`, of EVERY rank's buffer
+// (P2P stores over NVLink, release at system scope), then waits until all n rows of its own
+// half e&1 carry epoch e (acquire loads). Values are < 2^32 (per-rank counts). A rank can run at
+// most one exchange ahead of another (it cannot finish e+1 before every rank has written e+1,
+// which each does only after finishing e), so the parity halves never mix two exchanges. A wait
+// that exceeds ~10 s sets *err (host-mapped) and gives up instead of hanging.
+constexpr int kMaxPeers = 32;
+constexpr int kMaxXchgVals = 32;
+struct PeerXchg {
+  uint64_t* const* peers;  // device array [n]: rank r's buffer as mapped here (peers[rank] = mine)
+  uint64_t* mine;
+  uint32_t* epoch;         // device counter, bumped once per exchange
+  uint32_t* err;           // host-mapped flag: nonzero after a timed-out wait
+  int n, rank;
+};
+// Gather k (<= kMaxXchgVals) values src[0..k) of every rank: out[r * k + j] = rank r's src[j]
+// (out may be null); sums[j] = sum over ranks (sums may be null). One CTA, on `stream`.
+int launch_peer_exchange(const PeerXchg& x, const uint64_t* src, int k, uint64_t* out,
+                         uint64_t* sums, void* stream);
+
 // Launch entry points (kernels.cu). Return cudaError_t as int.
 // keep != nullptr: also keep the selection (and, with keep->n_keep > 0, the selected values of
 // projected predicate columns; the leaves carry the capture offsets and keep->warp_smem is set).
@@ -184,12 +208,14 @@ int launch_count_large(const DevProgramLarge& p, uint64_t n, int grid, const Scr
 // Push-down from a kept selection: superblock prefix (writes the local count to s.result[0]; with
 // gate_ranks > 0 also s.result[kGateSlot] = sum of the gathered s.result[1..gate_ranks]) and the
 // compaction/gather kernel.
+// xg != nullptr (sel_execute with peers): the prefix kernel first runs the peer exchange of the
+// local count in s.result[kGateSlot] (gathered into s.result[1..n], the sum into kGateSlot).
 int launch_pushdown_sel_small(const DevProgramSmall& p, uint64_t n, uint32_t* out_ids, int grid,
                               const Scratch& s, const SelectionBufs& sb, void* stream,
-                              int gate_ranks = 0);
+                              int gate_ranks = 0, const PeerXchg* xg = nullptr);
 int launch_pushdown_sel_large(const DevProgramLarge& p, uint64_t n, uint32_t* out_ids, int grid,
                               const Scratch& s, const SelectionBufs& sb, void* stream,
-                              int gate_ranks = 0);
+                              int gate_ranks = 0, const PeerXchg* xg = nullptr);
 int launch_pushdown_small(const DevProgramSmall& p, uint64_t n, uint32_t* out_ids, int grid,
                           const Scratch& s, uint64_t ticket_base, uint32_t epoch, void* stream);
 int launch_pushdown_large(const DevProgramLarge& p, uint64_t n, uint32_t* out_ids, int grid,

@@ -38,6 +38,17 @@ def setup_comm(ctx: Context, group=None) -> Context:
     return ctx
 
 
+def setup_peers(ctx: Context, group=None) -> Context:
+    """Make `ctx` one rank of the current group over peer memory (collective): every rank's
+    exchange-buffer IPC handle is all-gathered through torch.distributed and mapped by every
+    other rank (include/sel.h sel_ctx_set_peers)."""
+    world, rank = dist.get_world_size(group), dist.get_rank(group)
+    handles = [None] * world
+    dist.all_gather_object(handles, ctx.peer_handle(), group=group)
+    ctx.set_peers(world, rank, handles)
+    return ctx
+
+
 def exclusive_offset(local_counts, rank: int) -> int:
     """Position of rank `rank`'s slice in the rank-ordered (= ascending row id) concatenation."""
     return int(sum(local_counts[:rank]))
