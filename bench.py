@@ -112,7 +112,22 @@ def const_columns(prog, types):
             if "bitmap" not in L and len(L["lo"]) == 1 and L["span"] == [0]}
 
 
-def algo_bytes(table, prog_cols, proj, local_count, pushdown_path=0, consts=()):
+def coded_columns(prog, types, proj):
+    """Projected columns pinned to two values by a fast-path 1-byte leaf: the keeping count keeps
+    one code bit per row for them and the push-down never reads them."""
+    import os as _os
+    import paper_1806_08384_b200 as sel
+    if _os.environ.get("SEL_CODED", "1") == "0":
+        return set()
+    plan = sel.program_plan(prog, types)
+    for L, kind in zip(plan["leaves"], plan.get("fast") or []):
+        pts = sum(sp + 1 for sp in L["span"])
+        if kind == 4 and pts == 2 and L["col"] in proj:
+            return {L["col"]}
+    return set()
+
+
+def algo_bytes(table, prog_cols, proj, local_count, pushdown_path=0, consts=(), coded=()):
     """Algorithmic bytes.
     step  = what COUNT + push-down must move once (e.g. C2: 5.4 GB scan + 0.40 GB of D
             read + 1.303 GB written = 7.10 GB): rows x distinct predicate widths + selected x
@@ -132,7 +147,8 @@ def algo_bytes(table, prog_cols, proj, local_count, pushdown_path=0, consts=()):
     single = scan + local_count * sum(w[c] for c in set(proj) if c not in prog_cols) + write
     if pushdown_path == 1:
         selection = n // 8 + 2 * ((n + 1023) // 1024)
-        push_b = selection + local_count * sum(w[c] for c in proj if c not in consts) + write
+        push_b = (selection + len(coded) * (n // 8)
+                  + local_count * sum(w[c] for c in proj if c not in consts and c not in coded) + write)
     else:
         push_b = single
     return count_b, push_b, single + 8
@@ -438,7 +454,8 @@ def run_ours(args):
     dev_ms = ev0.elapsed_time(ev1)
     pd_path = ctx.last_pushdown_path()
     consts = const_columns(prog, T.types)
-    cb, pb, step_b = algo_bytes(T, pc, proj, local_count, pd_path, consts)
+    coded = coded_columns(prog, T.types, proj) if pd_path == 1 else set()
+    cb, pb, step_b = algo_bytes(T, pc, proj, local_count, pd_path, consts, coded)
     my_bytes = step_b
     t = torch.tensor([dev_ms, my_bytes, cb, pb, statistics.mean(count_ms), statistics.mean(push_ms)],
                      dtype=torch.float64, device=_red_dev(dev))
@@ -598,8 +615,10 @@ def run_ours(args):
                     kept.add(j)
                     budget -= w_all[j]
         pb_sector = (T.n_rows // 8 + 2 * ((T.n_rows + 1023) // 1024)
+                     + len(coded) * (T.n_rows // 8)
                      + sum(local_count * w_all[j] for j in kept)
-                     + sum(32 * sectors(w_all[j]) for j in set(proj) if j not in kept and j not in consts)
+                     + sum(32 * sectors(w_all[j]) for j in set(proj)
+                           if j not in kept and j not in consts and j not in coded)
                      + write_b)
     else:
         pb_sector = (T.n_rows * sum(w_all[j] for j in pc)

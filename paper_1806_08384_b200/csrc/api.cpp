@@ -147,6 +147,7 @@ struct sel_ctx_s {
   // >= two_pass_min_rows local rows, else the single pass (SEL_PUSHDOWN_PATH=single|two forces)
   uint64_t two_pass_min_rows = kTwoPassMinRows;
   bool fast_enabled = true;  // count fast path (SEL_FAST=0: interpreter only)
+  bool code_enabled = true;  // coded projections (SEL_CODED=0: gather them)
   bool graph_comm = true;    // prepared executes with a communicator are captured (SEL_GRAPH_COMM=0: not)
   int prefetch_mode = -1;   // -1 auto, 0 off, 1 on
   bool keep_values = false;  // SEL_KEEP_VALUES=1: executes also keep projected predicate values
@@ -262,6 +263,7 @@ int fast_kinds(const Plan& plan, const int* types, uint8_t (&kind)[kMaxFastLeave
 template <class P>
 void classify_fast(const Plan& plan, const sel_table_s* t, P* p) {
   p->fast_n = 0;
+  p->fast_code = -1;
   if (!t->ctx->fast_enabled) return;
   p->fast_n = (uint32_t)fast_kinds(plan, t->types.data(), p->fast_kind, p->fast_pts, p->fast_npts);
 }
@@ -432,10 +434,12 @@ sel_status ensure_status(sel_ctx c, uint64_t ntiles, cudaStream_t stream) {
 sel_status ensure_selection(sel_ctx c, uint64_t nchunks) {
   if (c->sel_cap_chunks >= nchunks) return SEL_OK;
   if (c->sel.bits) cudaFree(c->sel.bits);
+  if (c->sel.which) cudaFree(c->sel.which);
   if (c->sel.chunk_cnt) cudaFree(c->sel.chunk_cnt);
   if (c->sel.sb_sum) cudaFree(c->sel.sb_sum);
   if (c->sel.sb_prefix) cudaFree(c->sel.sb_prefix);
   c->sel = SelectionBufs{};
+  c->sel.code_col = -1;
   c->sel_cap_chunks = 0;
   c->kept_table = nullptr;
   ++c->alloc_gen;
@@ -443,6 +447,7 @@ sel_status ensure_selection(sel_ctx c, uint64_t nchunks) {
   const uint64_t nsb = (cap + kSbChunks - 1) / kSbChunks;
   c->kept_cols.clear();
   cudaError_t e = cudaMalloc(&c->sel.bits, cap * 32 * sizeof(uint32_t));
+  if (e == cudaSuccess) e = cudaMalloc(&c->sel.which, cap * 32 * sizeof(uint32_t));
   if (e == cudaSuccess) e = cudaMalloc(&c->sel.chunk_cnt, cap * sizeof(uint16_t));
   if (e == cudaSuccess) e = cudaMalloc(&c->sel.sb_sum, nsb * sizeof(uint32_t));
   if (e == cudaSuccess) e = cudaMalloc(&c->sel.sb_prefix, nsb * sizeof(uint32_t));
@@ -497,6 +502,8 @@ sel_status sel_ctx_create(int cuda_device, sel_ctx* out) {
   c->prefetch_mode = pf ? (std::strcmp(pf, "1") == 0 ? 1 : 0) : -1;
   const char* kv = std::getenv("SEL_KEEP_VALUES");
   c->keep_values = kv && std::strcmp(kv, "1") == 0;
+  const char* cd = std::getenv("SEL_CODED");
+  c->code_enabled = !(cd && std::strcmp(cd, "0") == 0);
   const char* gc = std::getenv("SEL_GRAPH_COMM");
   c->graph_comm = !(gc && std::strcmp(gc, "0") == 0);
   const char* fe = std::getenv("SEL_FAST");
@@ -677,6 +684,7 @@ void release_ctx_resources(sel_ctx c) {
   if (c->s.status) cudaFree(c->s.status);
   if (c->h_result) cudaFreeHost(c->h_result);
   if (c->sel.bits) cudaFree(c->sel.bits);
+  if (c->sel.which) cudaFree(c->sel.which);
   if (c->sel.chunk_cnt) cudaFree(c->sel.chunk_cnt);
   if (c->sel.sb_sum) cudaFree(c->sel.sb_sum);
   if (c->sel.sb_prefix) cudaFree(c->sel.sb_prefix);
@@ -979,9 +987,13 @@ sel_status reserve_selection(sel_table t, uint64_t nchunks,
 // Enqueue the count of `plan` over t's shard on `stream`: the count kernel
 // (keeping the selection with SEL_KEEP_SELECTION) writes the local count to *d_out, then the
 // 8-byte all-reduce makes it global in place. Nothing waits for the host.
+// code_cols (a keeping count without kept values): projected columns the materialisation will
+// write; one pinned by a two-point 1-byte leaf of the fast path gets its per-row code bit kept
+// (SelectionBufs::which) so that the push-down never reads it (kCodedProj).
 sel_status enqueue_count(sel_table t, const Plan& plan, uint32_t flags, const uint32_t* keep_cols,
                          uint32_t nkeep, cudaStream_t stream, uint64_t* d_out,
-                         bool allreduce = true) {
+                         bool allreduce = true, const uint32_t* code_cols = nullptr,
+                         uint32_t ncode = 0) {
   sel_ctx c = t->ctx;
   const uint64_t n = t->local_rows;
   const bool scan = n > 0 && plan.path != PATH_CONST;
@@ -1047,6 +1059,22 @@ sel_status enqueue_count(sel_table t, const Plan& plan, uint32_t flags, const ui
       pack(plan, t, &p);
       mark_captures(&p);
       choose_bitmap_staging(&p, dyn);
+      if (keep) {
+        c->sel.code_col = -1;
+        if (keep->n_keep == 0 && p.fast_n > 0 && c->code_enabled) {
+          for (uint32_t s2 = 0; s2 < p.fast_n && c->sel.code_col < 0; ++s2) {
+            if (p.fast_kind[s2] != FK_S1 || p.fast_npts[s2] != 2) continue;
+            const int col = plan.leaves[s2].col;
+            for (uint32_t j = 0; j < ncode; ++j) {
+              if ((int)code_cols[j] != col) continue;
+              p.fast_code = (int32_t)s2;
+              c->sel.code_col = col;
+              c->sel.code_pts = (p.fast_pts[s2][0] & 0xFFu) | ((p.fast_pts[s2][1] & 0xFFu) << 8);
+              break;
+            }
+          }
+        }
+      }
       if (c->prefetch_mode < 0) p.prefetch = ((keep && keep->n_keep) || p.bm_smem) ? 1u : 0u;
       int occ = keep ? occupancy_count_keep_small(dyn + p.bm_smem)
                      : (p.bm_smem ? occupancy_count_dyn_small(p.bm_smem) : c->occ_count_small);
@@ -1059,6 +1087,7 @@ sel_status enqueue_count(sel_table t, const Plan& plan, uint32_t flags, const ui
       pack(plan, t, &p);
       mark_captures(&p);
       choose_bitmap_staging(&p, dyn);
+      if (keep) c->sel.code_col = -1;
       if (c->prefetch_mode < 0) p.prefetch = ((keep && keep->n_keep) || p.bm_smem) ? 1u : 0u;
       const int occ = keep ? occupancy_count_keep_large(dyn + p.bm_smem)
                            : (p.bm_smem ? occupancy_count_dyn_large(p.bm_smem) : c->occ_count_large);
@@ -1112,6 +1141,11 @@ sel_status enqueue_pushdown_sel(sel_table t, const Plan& plan, const uint32_t* p
       if (is_const_col(consts, (int)proj_cols[j], &raw)) {
         p->proj_cap_off[j] = kConstProj;
         p->proj_src[j] = reinterpret_cast<const void*>((uintptr_t)raw);
+      } else if (c->sel.code_col >= 0 && c->sel.code_col == (int)proj_cols[j]) {
+        p->proj_cap_off[j] = kCodedProj;   // from the kept code bits (enqueue_count)
+        p->proj_src[j] = reinterpret_cast<const void*>((uintptr_t)c->sel.code_pts);
+        p->coded = 1;
+        continue;
       } else {
         for (size_t k = 0; k < c->kept_cols.size(); ++k)
           if (c->kept_cols[k] == (int)proj_cols[j]) p->proj_cap_off[j] = (uint16_t)(kKeptBase + k);
@@ -1172,7 +1206,7 @@ sel_status enqueue_execute(sel_table t, const Plan& plan, const uint32_t* proj, 
                            void* const* outs, uint64_t capacity, cudaStream_t s) {
   sel_ctx c = t->ctx;
   sel_status st = enqueue_count(t, plan, SEL_KEEP_SELECTION, proj, nkeep, s, c->s.result + kGateSlot,
-                                false);
+                                false, proj, nproj);
   if (st != SEL_OK) return st;
   if (c->comm && !c->peers) {  // SURVEY §8a a4 + a7 in one collective
     ncclResult_t r = nccl().AllGather(c->s.result + kGateSlot, c->s.result + 1, 1, ncclUint64,
@@ -1363,7 +1397,7 @@ uint64_t pushdown_impl(sel_table t, const void* prog, size_t prog_bytes, const u
     int le, grid;
     if (two_pass) {
       if (enqueue_count(t, plan, SEL_KEEP_SELECTION, proj_cols, c->keep_values ? nproj : 0u, stream,
-                        c->s.result + kGateSlot, false) != SEL_OK)
+                        c->s.result + kGateSlot, false, proj_cols, nproj) != SEL_OK)
         return SEL_ERR;
       if (c->timing) cudaEventRecord(c->ev2, stream);
       if (enqueue_pushdown_sel(t, plan, proj_cols, nproj, out_rowids, out_cols, capacity_rows, false,
@@ -1677,7 +1711,7 @@ uint64_t sel_execute(sel_table t, const void* prog, size_t prog_bytes, const uin
         DeviceGuard g(c->device);
         if (!g.ok) return fail64(SEL_E_CUDA, "cudaSetDevice failed");
         if (enqueue_count(t, plan, SEL_KEEP_SELECTION, proj_cols, nkeep, stream, c->s.result,
-                          false) != SEL_OK)
+                          false, proj_cols, nproj) != SEL_OK)
           return SEL_ERR;
         cudaError_t e = cudaMemcpyAsync(c->h_result, c->s.result, sizeof(uint64_t),
                                         cudaMemcpyDeviceToHost, stream);

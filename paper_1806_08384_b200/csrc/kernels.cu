@@ -368,20 +368,53 @@ __device__ __forceinline__ uint32_t s1_nibble(uint32_t x, const uint32_t (&pts)[
   return ((hit & 0x80808080u) * 0x00204081u) >> 28;   // byte e's high bit -> bit e
 }
 
+// The coded leaf (p.fast_code; two points) also returns which rows matched point 1 (*wm).
+__device__ __forceinline__ uint32_t s1_zero_bytes(uint32_t x, uint32_t pt) {
+  const uint32_t d = x ^ pt;
+  return ~(((d & 0x7F7F7F7Fu) + 0x7F7F7F7Fu) | d);
+}
+__device__ __forceinline__ uint32_t s1_gather_nibble(uint32_t h) {
+  return ((h & 0x80808080u) * 0x00204081u) >> 28;
+}
+
 template <bool CAP>
 __device__ __forceinline__ uint32_t fast_s1(const void* col, uint64_t base, int lane,
-                                            const uint32_t (&pts)[4], int npts, char* cap) {
+                                            const uint32_t (&pts)[4], int npts, char* cap,
+                                            uint32_t* wm) {
   const uint8_t* c = static_cast<const uint8_t*>(col) + base;
   uint32_t x[8];
 #pragma unroll
   for (int k = 0; k < 8; ++k) x[k] = ld_stream_u32(c + 4u * (32u * k + lane));
   uint32_t m = 0;
+  if (wm) {
+    uint32_t w = 0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      if (CAP && cap) reinterpret_cast<uint32_t*>(cap)[32 * k + lane] = x[k];
+      const uint32_t z1 = s1_zero_bytes(x[k], pts[1]);
+      m |= s1_gather_nibble(s1_zero_bytes(x[k], pts[0]) | z1) << (4 * k);
+      w |= s1_gather_nibble(z1) << (4 * k);
+    }
+    *wm = w;
+    return m;
+  }
 #pragma unroll
   for (int k = 0; k < 8; ++k) {
     if (CAP && cap) reinterpret_cast<uint32_t*>(cap)[32 * k + lane] = x[k];
     m |= s1_nibble(x[k], pts, npts) << (4 * k);
   }
   return m;
+}
+
+// The coded leaf's point-1 matches over a partial (tail) chunk, for keep_chunk.
+__device__ __forceinline__ uint32_t which_tail(const void* col, uint64_t base, int lane,
+                                               uint32_t nvalid, uint32_t pt1) {
+  uint32_t v[32];
+  load_w1<true>(col, base, lane, nvalid, v, nullptr);
+  uint32_t m = 0;
+#pragma unroll
+  for (int i = 0; i < 32; ++i) m |= (v[i] == pt1) ? (1u << i) : 0u;
+  return m & valid_mask(lane, nvalid);
 }
 
 // 4-byte column: one point (E4), one interval (R4) or 2..4 intervals (S4, n = iv_count).
@@ -429,7 +462,8 @@ __device__ __forceinline__ uint32_t fast_r8(const void* col, uint64_t base, int 
 }
 
 template <int FASTN, bool CAP, class P>
-__device__ __forceinline__ uint32_t eval_fast(const P& p, uint64_t base, int lane, char* wsmem) {
+__device__ __forceinline__ uint32_t eval_fast(const P& p, uint64_t base, int lane, char* wsmem,
+                                              uint32_t* wm) {
   uint32_t acc = 0xFFFFFFFFu;
 #pragma unroll
   for (int s = 0; s < FASTN; ++s) {
@@ -444,7 +478,10 @@ __device__ __forceinline__ uint32_t eval_fast(const P& p, uint64_t base, int lan
       case FK_R4: r = fast_w4<FK_R4, CAP>(col, base, lane, lo, sp, 1, cap); break;
       case FK_S4: r = fast_w4<FK_S4, CAP>(col, base, lane, lo, sp, L.iv_count, cap); break;
       case FK_R8: r = fast_r8<CAP>(col, base, lane, lo[0], sp[0], cap); break;
-      default: r = fast_s1<CAP>(col, base, lane, p.fast_pts[s], p.fast_npts[s], cap); break;
+      default:
+        r = fast_s1<CAP>(col, base, lane, p.fast_pts[s], p.fast_npts[s], cap,
+                         p.fast_code == s ? wm : nullptr);
+        break;
     }
     acc &= r;
   }
@@ -472,7 +509,7 @@ __device__ __forceinline__ uint64_t pack_status(uint32_t epoch, uint64_t flag, u
 #ifndef SEL_GATHER_BATCH
 #define SEL_GATHER_BATCH 8   // loads in flight per lane (A/B: 4 equal, 16 slower on C2)
 #endif
-template <class T>
+template <class T, bool MASK = false>
 __device__ __forceinline__ void gather_global(const void* src_v, void* dst_v, uint64_t cbase,
                                               uint64_t gbase, const uint16_t* s_idx, uint32_t lim,
                                               int lane) {
@@ -483,11 +520,11 @@ __device__ __forceinline__ void gather_global(const void* src_v, void* dst_v, ui
   for (; q + (B - 1) * 32 < lim; q += B * 32) {
     T v[B];
 #pragma unroll
-    for (int u = 0; u < B; ++u) v[u] = __ldg(src + s_idx[q + 32 * u]);
+    for (int u = 0; u < B; ++u) v[u] = __ldg(src + (MASK ? (s_idx[q + 32 * u] & (kCodeBit - 1u)) : s_idx[q + 32 * u]));
 #pragma unroll
     for (int u = 0; u < B; ++u) dst[q + 32 * u] = v[u];
   }
-  for (; q < lim; q += 32) dst[q] = __ldg(src + s_idx[q]);
+  for (; q < lim; q += 32) dst[q] = __ldg(src + (MASK ? (s_idx[q] & (kCodeBit - 1u)) : s_idx[q]));
 }
 
 // Write-out of a projected predicate column from its shared-memory capture.
@@ -640,6 +677,25 @@ __device__ __forceinline__ void stage_rows_rm(uint32_t t, int lane, uint16_t* my
   }
 }
 
+// stage_rows_rm carrying each row's code bit (row-major word w of the coded leaf) in kCodeBit.
+__device__ __forceinline__ void stage_rows_rm_coded(uint32_t t, uint32_t w, int lane, uint16_t* my,
+                                                    uint32_t base, uint32_t row_base) {
+  const uint32_t c = (uint32_t)__popc(t);
+  uint32_t incl = c;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const uint32_t v = __shfl_up_sync(0xFFFFFFFFu, incl, d);
+    if (lane >= d) incl += v;
+  }
+  uint32_t pos = base + incl - c;
+  const uint32_t r0 = row_base + 32u * lane;
+  while (t) {
+    const uint32_t b = (uint32_t)(__ffs(t) - 1);
+    t &= t - 1;
+    my[pos++] = (uint16_t)((r0 + b) | (((w >> b) & 1u) ? kCodeBit : 0u));
+  }
+}
+
 // Quad layout (bit 4k+e of lane l = row 4(32k+l)+e) -> row-major (bit b of lane L = row 32L+b):
 // lane L = 4k + j gathers nibble k of lanes 8j..8j+7 (row 128k + 32j + 4i + e = 32L + 4i + e).
 __device__ __forceinline__ uint32_t to_row_major(uint32_t m, int lane) {
@@ -653,10 +709,18 @@ __device__ __forceinline__ uint32_t to_row_major(uint32_t m, int lane) {
   return t;
 }
 
+__device__ __forceinline__ void st_evict_last(uint32_t* p, uint32_t v) {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+  asm volatile("st.global.L2::cache_hint.u32 [%0], %1, %2;" ::"l"(p), "r"(v), "l"(pol) : "memory");
+}
+
+// coded: also keep the coded leaf's point-1 matches (wm, the count's quad layout) row-major.
 template <class P, bool KEEP>
 __device__ __forceinline__ void keep_chunk(const SelectionBufs& sb, uint64_t c, int lane, uint32_t m,
-                                           char* wsmem) {
+                                           char* wsmem, uint32_t wm = 0u, bool coded = false) {
   if (!KEEP) return;
+  if (coded) st_evict_last(sb.which + c * 32 + lane, to_row_major(wm, lane));
   const uint32_t t = to_row_major(m, lane);          // the push-down stages from row-major masks
   if (sb.n_keep) {
     sb.bits[c * 32 + lane] = t;
@@ -665,10 +729,7 @@ __device__ __forceinline__ void keep_chunk(const SelectionBufs& sb, uint64_t c, 
     // being written back while the scan streams its columns (measured: C5 count 0.638 -> 0.629
     // ms, C4 push-down 0.176 -> 0.160 ms). With kept values the slots compete for L2 and the
     // policy hurt (C2 0.913 -> 0.968 ms), so it is not used there.
-    uint64_t pol;
-    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
-    asm volatile("st.global.L2::cache_hint.u32 [%0], %1, %2;" ::"l"(sb.bits + c * 32 + lane), "r"(t),
-                 "l"(pol) : "memory");
+    st_evict_last(sb.bits + c * 32 + lane, t);
   }
   uint32_t cc;
   if (sb.n_keep) {
@@ -745,9 +806,10 @@ __global__ void __launch_bounds__(NW * 32, NW == kWarpsPerCta ? (FASTN ? SEL_FAS
     for (uint64_t s = gw; s < ns_full; s += nw) {
       const uint64_t c = phase + s * stride;
       if (lane == 0 && p.prefetch && s + nw < ns_full) prefetch_chunk_fast<FASTN>(p, c + nw * stride);
-      const uint32_t m = eval_fast<FASTN, KEEP>(p, c * kChunkRows, lane, wsmem);
+      uint32_t wm = 0;
+      const uint32_t m = eval_fast<FASTN, KEEP>(p, c * kChunkRows, lane, wsmem, &wm);
       cnt += __popc(m);
-      keep_chunk<P, KEEP>(sb, c, lane, m, wsmem);
+      keep_chunk<P, KEEP>(sb, c, lane, m, wsmem, wm, KEEP && p.fast_code >= 0);
     }
   } else {
     if (lane == 0 && p.prefetch && gw < ns_full) prefetch_chunk(p, phase + gw * stride);
@@ -762,7 +824,13 @@ __global__ void __launch_bounds__(NW * 32, NW == kWarpsPerCta ? (FASTN ? SEL_FAS
   if (tail_sampled && gw == ns_full % nw) {
     const uint32_t m = eval_program<true, KEEP>(p, nfull * kChunkRows, lane, rem, wsmem, bm_sbase);
     cnt += __popc(m);
-    keep_chunk<P, KEEP>(sb, nfull, lane, m, wsmem);
+    uint32_t wm = 0;
+    const bool coded = KEEP && FASTN > 0 && p.fast_code >= 0;
+    if (coded) {
+      const int s = p.fast_code;
+      wm = which_tail(p.col[p.leaf[s].slot], nfull * kChunkRows, lane, rem, p.fast_pts[s][1] & 0xFFu);
+    }
+    keep_chunk<P, KEEP>(sb, nfull, lane, m, wsmem, wm, coded);
   }
   cnt = __reduce_add_sync(0xFFFFFFFFu, cnt);
 
@@ -1009,7 +1077,7 @@ __global__ void __launch_bounds__(1024) superblock_prefix_kernel(const uint32_t*
 // Flush `k` staged rows (block-relative, ascending) to output positions [gbase, gbase + k): row
 // ids and the projections gathered from global memory (kept-value projections were copied per
 // chunk while staging).
-template <class P>
+template <bool CODED, class P>
 __device__ __forceinline__ void flush_rows(const P& p, uint64_t bbase, uint64_t gbase, uint32_t k,
                                            const uint16_t* my, int lane,
                                            uint32_t* __restrict__ out_ids) {
@@ -1017,15 +1085,23 @@ __device__ __forceinline__ void flush_rows(const P& p, uint64_t bbase, uint64_t 
   const uint32_t lim = (uint32_t)min((uint64_t)k, p.capacity - gbase);
   const uint32_t idbase = (uint32_t)(p.row_offset + bbase);
 #pragma unroll 4
-  for (uint32_t q = lane; q < lim; q += 32) out_ids[gbase + q] = idbase + my[q];
+  for (uint32_t q = lane; q < lim; q += 32)
+    out_ids[gbase + q] = idbase + (CODED ? (my[q] & (kCodeBit - 1u)) : my[q]);
 #pragma unroll 1
   for (uint32_t j = 0; j < p.n_proj; ++j) {
+    if (CODED && p.proj_cap_off[j] == kCodedProj) {   // the value from the row's code bit, nothing read
+      const uint32_t pts = (uint32_t)(uintptr_t)p.proj_src[j];
+      uint8_t* __restrict__ dst = static_cast<uint8_t*>(p.proj_dst[j]) + gbase;
+#pragma unroll 4
+      for (uint32_t q = lane; q < lim; q += 32) dst[q] = (uint8_t)(pts >> ((my[q] & kCodeBit) ? 8 : 0));
+      continue;
+    }
     if (p.proj_cap_off[j] != kNoCapture) continue;
     switch (p.proj_wclass[j]) {
-      case W1: gather_global<uint8_t>(p.proj_src[j], p.proj_dst[j], bbase, gbase, my, lim, lane); break;
-      case W2: gather_global<uint16_t>(p.proj_src[j], p.proj_dst[j], bbase, gbase, my, lim, lane); break;
-      case W4: gather_global<uint32_t>(p.proj_src[j], p.proj_dst[j], bbase, gbase, my, lim, lane); break;
-      default: gather_global<uint64_t>(p.proj_src[j], p.proj_dst[j], bbase, gbase, my, lim, lane); break;
+      case W1: gather_global<uint8_t, CODED>(p.proj_src[j], p.proj_dst[j], bbase, gbase, my, lim, lane); break;
+      case W2: gather_global<uint16_t, CODED>(p.proj_src[j], p.proj_dst[j], bbase, gbase, my, lim, lane); break;
+      case W4: gather_global<uint32_t, CODED>(p.proj_src[j], p.proj_dst[j], bbase, gbase, my, lim, lane); break;
+      default: gather_global<uint64_t, CODED>(p.proj_src[j], p.proj_dst[j], bbase, gbase, my, lim, lane); break;
     }
   }
 }
@@ -1039,7 +1115,7 @@ __device__ __forceinline__ void copy_kept(const P& p, const SelectionBufs& sb, u
 #pragma unroll 1
   for (uint32_t j = 0; j < p.n_proj; ++j) {
     const uint16_t co = p.proj_cap_off[j];
-    if (co == kNoCapture) continue;
+    if (co == kNoCapture || co == kCodedProj) continue;
     if (co == kConstProj) {
       fill_proj(p.proj_wclass[j], p.proj_src[j], p.proj_dst[j], pos, lim, lane);
       continue;
@@ -1064,6 +1140,7 @@ __device__ __forceinline__ void copy_kept(const P& p, const SelectionBufs& sb, u
 #define SEL_PD_MINB 8
 #endif
 constexpr int kBlockChunks = SEL_BLOCK_CHUNKS;         // chunks per warp block
+static_assert(kBlockChunks * kChunkRows <= kCodeBit, "staged rows must leave the code bit free");
 constexpr uint32_t kStageCap = SEL_STAGE_CAP;          // staged rows per warp before a flush
 
 // Warp blocks of 4 contiguous chunks, grid-stride. All of a block's metadata — its 4 chunk counts,
@@ -1072,7 +1149,7 @@ constexpr uint32_t kStageCap = SEL_STAGE_CAP;          // staged rows per warp b
 // superblock prefix plus that partial sum; empty chunks are skipped without touching any column;
 // the selected rows of the block are staged and flushed with batched gathers into one contiguous
 // output range. No ticket, no look-back, no predicate evaluation.
-template <class P>
+template <class P, bool CODED>
 __global__ void __launch_bounds__(kThreads, SEL_PD_MINB) pushdown_sel_kernel(const __grid_constant__ P p,
                                                                    uint64_t n, SelectionBufs sb,
                                                                    uint32_t* __restrict__ out_ids,
@@ -1097,6 +1174,8 @@ __global__ void __launch_bounds__(kThreads, SEL_PD_MINB) pushdown_sel_kernel(con
     // replacement order once read (one 128-byte line per chunk)
     if (sb.n_keep == 0 && lane < kBlockChunks && c0 + lane < nchunks)
       asm volatile("applypriority.global.L2::evict_normal [%0], 128;" ::"l"(sb.bits + (c0 + lane) * 32) : "memory");
+    if (CODED && lane < kBlockChunks && c0 + lane < nchunks)
+      asm volatile("applypriority.global.L2::evict_normal [%0], 128;" ::"l"(sb.which + (c0 + lane) * 32) : "memory");
     uint32_t part = 0;
     if (first + lane < c0) part += sb.chunk_cnt[first + lane];
     if (first + 32 + lane < c0) part += sb.chunk_cnt[first + 32 + lane];
@@ -1113,17 +1192,20 @@ __global__ void __launch_bounds__(kThreads, SEL_PD_MINB) pushdown_sel_kernel(con
       if (cg == 0) continue;
       if (staged + cg > kStageCap) {
         __syncwarp();
-        flush_rows(p, bbase, gbase, staged, my, lane, out_ids);
+        flush_rows<CODED>(p, bbase, gbase, staged, my, lane, out_ids);
         __syncwarp();
         gbase += staged;
         staged = 0;
       }
       if (p.n_direct) copy_kept(p, sb, c0 + g, gbase + staged, cg, lane);  // kept / constant
-      stage_rows_rm(m[g], lane, my, staged, (uint32_t)g * kChunkRows);
+      if (CODED)   // the coded leaf's word, read when the chunk is staged (L2: stored evict_last)
+        stage_rows_rm_coded(m[g], sb.which[(c0 + g) * 32 + lane], lane, my, staged, (uint32_t)g * kChunkRows);
+      else
+        stage_rows_rm(m[g], lane, my, staged, (uint32_t)g * kChunkRows);
       staged += cg;
     }
     __syncwarp();
-    flush_rows(p, bbase, gbase, staged, my, lane, out_ids);
+    flush_rows<CODED>(p, bbase, gbase, staged, my, lane, out_ids);
     __syncwarp();
   }
 }
@@ -1301,7 +1383,11 @@ int launch_pushdown_sel_small(const DevProgramSmall& p, uint64_t n, uint32_t* ou
 #endif
   superblock_prefix_kernel<<<1, 1024, 0, (cudaStream_t)st>>>(sb.sb_sum, sb.sb_prefix, nsb, s.result,
                                                                gate_ranks, xg ? *xg : none);
-  pushdown_sel_kernel<DevProgramSmall><<<grid, kThreads, 0, (cudaStream_t)st>>>(p, n, sb, out_ids,
+  if (p.coded)
+    pushdown_sel_kernel<DevProgramSmall, true><<<grid, kThreads, 0, (cudaStream_t)st>>>(p, n, sb, out_ids,
+                                                                                s.result + kGateSlot);
+  else
+    pushdown_sel_kernel<DevProgramSmall, false><<<grid, kThreads, 0, (cudaStream_t)st>>>(p, n, sb, out_ids,
                                                                                 s.result + kGateSlot);
   return (int)cudaGetLastError();
 }
@@ -1317,7 +1403,11 @@ int launch_pushdown_sel_large(const DevProgramLarge& p, uint64_t n, uint32_t* ou
 #endif
   superblock_prefix_kernel<<<1, 1024, 0, (cudaStream_t)st>>>(sb.sb_sum, sb.sb_prefix, nsb, s.result,
                                                                gate_ranks, xg ? *xg : none);
-  pushdown_sel_kernel<DevProgramLarge><<<grid, kThreads, 0, (cudaStream_t)st>>>(p, n, sb, out_ids,
+  if (p.coded)
+    pushdown_sel_kernel<DevProgramLarge, true><<<grid, kThreads, 0, (cudaStream_t)st>>>(p, n, sb, out_ids,
+                                                                                s.result + kGateSlot);
+  else
+    pushdown_sel_kernel<DevProgramLarge, false><<<grid, kThreads, 0, (cudaStream_t)st>>>(p, n, sb, out_ids,
                                                                                 s.result + kGateSlot);
   return (int)cudaGetLastError();
 }
@@ -1387,8 +1477,8 @@ int occupancy_count_keep_large(size_t dyn) { return occupancy_of(count_kernel<De
 int occupancy_count_large() { return occupancy_of(count_kernel<DevProgramLarge, false, kWarpsPerCta>, 0); }
 int occupancy_count_dyn_small(size_t dyn) { return occupancy_of(count_kernel<DevProgramSmall, false, kWarpsPerCta>, dyn); }
 int occupancy_count_dyn_large(size_t dyn) { return occupancy_of(count_kernel<DevProgramLarge, false, kWarpsPerCta>, dyn); }
-int occupancy_pushdown_sel_small() { return occupancy_of(pushdown_sel_kernel<DevProgramSmall>, 0); }
-int occupancy_pushdown_sel_large() { return occupancy_of(pushdown_sel_kernel<DevProgramLarge>, 0); }
+int occupancy_pushdown_sel_small() { return occupancy_of(pushdown_sel_kernel<DevProgramSmall, false>, 0); }
+int occupancy_pushdown_sel_large() { return occupancy_of(pushdown_sel_kernel<DevProgramLarge, false>, 0); }
 int occupancy_pushdown_small(size_t dyn_smem) { return occupancy_of(pushdown_kernel<DevProgramSmall>, dyn_smem); }
 int occupancy_pushdown_large(size_t dyn_smem) { return occupancy_of(pushdown_kernel<DevProgramLarge>, dyn_smem); }
 

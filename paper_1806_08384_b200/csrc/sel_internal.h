@@ -29,6 +29,12 @@ constexpr uint16_t kKeptBase = 0xFF00;  // push-down from a selection: proj_cap_
 // proj_cap_off = kConstProj: every selected row has the same value in this column (the
 // conjunction pins it with a single-value leaf), raw bits in (uintptr_t)proj_src: a fill.
 constexpr uint16_t kConstProj = 0xFFFE;
+// proj_cap_off = kCodedProj (push-down from a selection): the conjunction pins the column to two
+// values (a 1-byte IN of two points) and the keeping count recorded, per row, which one matched
+// (SelectionBufs::which); the staged row numbers carry that bit (kCodeBit) and the value is
+// (uintptr_t)proj_src >> (8 * bit) & 0xFF — the column is never read by the push-down.
+constexpr uint16_t kCodedProj = 0xFFFD;
+constexpr uint16_t kCodeBit = 1u << 12;          // staged block-relative rows are < 4096
 constexpr int kMaxDeviceStack = 32;
 
 enum WidthClass : uint8_t { W1 = 0, W2 = 1, W4 = 2, W8 = 3 };
@@ -75,12 +81,14 @@ struct DevProgramT {
   uint32_t bm_smem;      // count kernel: bytes of the sets staged in shared memory (leaves with
                          // kLeafStaged; offset = span[iv_begin] >> 32), 0 = none
   uint32_t n_direct;     // push-down from a selection: projections that are kept or constant
+  uint32_t coded;        // push-down from a selection: a projection is kCodedProj
   // Count kernel fast path (template-specialised conjunctive forms): when
   // fast_n > 0 the program is leaf 0 AND ... AND leaf fast_n-1 and leaf s has kind fast_kind[s]
   // (FastKind); the kernel instantiated for fast_n evaluates it as straight-line code with the
   // leaf parameters hoisted out of the chunk loop. FK_S1 compares against fast_pts[s][0..npts)
   // (the point keys, each byte-replicated).
   uint32_t fast_n;
+  int32_t fast_code;     // keeping count: slot whose point-1 matches are kept as `which`, or -1
   uint8_t fast_kind[4];
   uint8_t fast_npts[4];
   uint32_t fast_pts[4][4];
@@ -143,6 +151,9 @@ constexpr uint64_t kSbChunks = 1ull << kSbShift;
 constexpr int kMaxKeep = 8;
 struct SelectionBufs {
   uint32_t* bits;        // [nchunks * 32]
+  uint32_t* which;       // [nchunks * 32] row-major: row matched point 1 of the coded leaf
+  int32_t code_col;      // table column coded by `which` (host bookkeeping), -1 = none
+  uint32_t code_pts;     // its two raw byte values: point 0 | point 1 << 8
   uint16_t* chunk_cnt;   // [nchunks]
   uint32_t* sb_sum;      // [nsb], zeroed before the count
   uint32_t* sb_prefix;   // [nsb]
