@@ -238,7 +238,7 @@ uint64_t sel_pushdown(sel_table table, const void* prog, size_t prog_bytes,
 /* Which path the context's last sel_pushdown took: 1 = from a kept selection (no predicate
  * evaluation, no look-back), 2 = two passes inside the call (a count keeping the selection and
  * the projected predicate columns' values, then path 1's materialisation; taken without a kept
- * selection when the shard has >= 2^21 rows), 0 = single pass (evaluate + decoupled look-back;
+ * selection when the shard has >= 3·2^20 rows), 0 = single pass (evaluate + decoupled look-back;
  * smaller shards), -1 = no kernel ran (empty shard or constant-false program). Environment, read
  * at sel_ctx_create: SEL_PUSHDOWN_PATH=single forces the single pass, =two the two passes;
  * SEL_TWO_PASS_MIN_ROWS=<n> moves the threshold. Path 2 leaves its selection kept, so a repeated
@@ -246,7 +246,7 @@ uint64_t sel_pushdown(sel_table table, const void* prog, size_t prog_bytes,
 int sel_ctx_last_pushdown_path(sel_ctx ctx);
 
 /* Choose the path sel_pushdown takes when no kept selection matches (overrides the environment
- * above): mode -1 = automatic (two passes at >= 2^21 local rows, else the single pass), 0 = always
+ * above): mode -1 = automatic (two passes at >= 3·2^20 local rows, else the single pass), 0 = always
  * the single pass (also for sel_execute, which then gates on the host: count, then single pass),
  * 2 = always two passes. A matching kept selection is used in every mode but 0.
  * Errors: SEL_E_ARG (null ctx, other mode). */

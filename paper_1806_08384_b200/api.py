@@ -90,7 +90,7 @@ class Context:
 
     def set_pushdown_path(self, mode: int) -> None:
         """Path of a pushdown without a matching kept selection: -1 automatic (two passes at
-        >= 2^21 local rows), 0 always the single pass, 2 always two passes (include/sel.h)."""
+        >= 3·2^20 local rows), 0 always the single pass, 2 always two passes (include/sel.h)."""
         check(lib().sel_ctx_set_pushdown_path(self._h, int(mode)))
 
     def register_bitmap(self, words: torch.Tensor, nbits: int) -> int:

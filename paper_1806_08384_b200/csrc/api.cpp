@@ -20,7 +20,7 @@ using namespace sel;
 
 // ---- thread-local error state ----------------------------------------------------------------
 namespace {
-constexpr uint64_t kTwoPassMinRows = 1ull << 21;  // sel_pushdown: two passes from here
+constexpr uint64_t kTwoPassMinRows = 3ull << 20;  // sel_pushdown: two passes from here
 thread_local sel_status g_status = SEL_OK;
 thread_local std::string g_message;
 
