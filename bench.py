@@ -330,6 +330,15 @@ def setup_exchange(ctx, sel, sdist, dist, dev):
             try:
                 ctx.set_peers(len(handles), dist.get_rank(), handles)
                 mapped = True
+                # one real exchange: a count over a one-row table on every rank must see all ranks
+                from selgen.program import Const, encode, INT32
+                one = torch.zeros(1, dtype=torch.int32, device=dev)
+                probe = sel.Table(ctx, ["x"], [INT32], [one], row_offset=dist.get_rank(),
+                                  global_rows=dist.get_world_size())
+                got = probe.count(encode(Const(True), [INT32]))
+                probe.release()
+                if got != dist.get_world_size():
+                    ok, why = False, f"peer exchange counted {got} of {dist.get_world_size()}"
             except Exception as ex:  # noqa: BLE001
                 ok, why = False, f"peers unavailable: {type(ex).__name__}: {ex}"
         else:
