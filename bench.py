@@ -664,6 +664,7 @@ def run_ours(args):
                                 "materialise" + (", per table.execute()" if prepared is None else
                                                  ", prepared once and replayed as a CUDA graph"))},
             "rows_per_s": round(n / (ms_per_step / 1000)),
+            "step_frac_aggregate_hbm": round(value_gbs / (world * hbm), 4),
             "latency_ms": {"execute_median": round(statistics.median(count_lat), 4),
                            "execute_min": round(min(count_lat), 4),
                            "execute_p99": _stats(count_lat)["p99"],
