@@ -62,12 +62,14 @@ sys.path.insert(0, 'tests')
 from test_gpu_fastpath import TYPES as FT, fast_conjunction
 cctx = sel.Context(dev)
 cctx.set_comm(1, 0, sel.Context.new_unique_id())
+pctx = sel.Context(dev)                                  # one-rank peer-memory exchange
+pctx.set_peers(1, 0, [pctx.peer_handle()])
 for n in [1025, 70_001]:
     rng = np.random.default_rng(11 + n)
     cols, pools = random_table(rng, FT, n)
     view = {INT32: np.int32, DATE32: np.int32, DICT32: np.int32, INT64: np.int64, DICT8: np.uint8}
     tens = [torch.from_numpy(np.ascontiguousarray(c).view(view[ty]).copy()).to(dev) for c, ty in zip(cols, FT)]
-    for cx in (ctx, cctx):
+    for cx in (ctx, cctx, pctx):
         t = sel.Table(cx, [f"c{i}" for i in range(len(FT))], FT, tens)
         for _ in range(6):
             node = fast_conjunction(rng, pools)
@@ -86,5 +88,21 @@ for n in [1025, 70_001]:
             q.release()
         t.release()
 cctx.close()
+pctx.drop_peers()
+pctx.close()
+# coded projection (C2's C IN (1, 4) projected) through execute, prepared execute, two passes
+T = configs.gen_c2(60_000, device=dev)
+t = sel.Table(ctx, ["A", "B", "C", "D"], T.types, [c.data for c in T.columns])
+host = [c.numpy() for c in configs.gen_c2(60_000).columns]
+prog = encode(configs.c2_probes()["listing"], T.types)
+want = oracle.pushdown(host, T.types, prog, proj=[0, 2, 3])
+r1 = t.execute(prog, project=[0, 2, 3], max_size=60_000)
+q = t.prepare_execute(prog, project=[0, 2, 3], max_size=60_000)
+assert q.run() == want[0] == r1.count
+for r in (r1, q.result()):
+    assert np.array_equal(r.rowids.cpu().numpy().view(np.uint32), want[1])
+    assert np.array_equal(r.columns[2].cpu().numpy(), want[2][1])
+q.release()
+t.release()
 torch.cuda.synchronize()
 print("sanitize workload ok")
