@@ -1219,14 +1219,19 @@ sel_status enqueue_execute(sel_table t, const Plan& plan, const uint32_t* proj, 
                             c->comm && !c->peers ? c->nranks : 0, c->peers ? &c->xg : nullptr);
   if (st != SEL_OK) return st;
   if (c->timing) record(c, c->ev3, s);
-  cudaError_t e = cudaMemcpyAsync(c->h_result + kGateSlot, c->s.result + kGateSlot, sizeof(uint64_t),
-                                  cudaMemcpyDeviceToHost, s);
-  if (e == cudaSuccess) {
-    if (multi(c))
-      e = cudaMemcpyAsync(c->h_result + 1, c->s.result + 1, c->nranks * sizeof(uint64_t),
+  // one copy: the prefix kernel mirrored the words read back right below the gate slot
+  const int nr = multi(c) ? c->nranks : 0;
+  cudaError_t e;
+  if (nr <= kMirrorMax) {
+    const int lo = kGateSlot - (nr > 0 ? nr : 1);
+    e = cudaMemcpyAsync(c->h_result + lo, c->s.result + lo, (kGateSlot + 1 - lo) * sizeof(uint64_t),
+                        cudaMemcpyDeviceToHost, s);
+  } else {
+    e = cudaMemcpyAsync(c->h_result + kGateSlot, c->s.result + kGateSlot, sizeof(uint64_t),
+                        cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess)
+      e = cudaMemcpyAsync(c->h_result + 1, c->s.result + 1, nr * sizeof(uint64_t),
                           cudaMemcpyDeviceToHost, s);
-    else
-      e = cudaMemcpyAsync(c->h_result, c->s.result, sizeof(uint64_t), cudaMemcpyDeviceToHost, s);
   }
   if (e != cudaSuccess) return set_error(SEL_E_CUDA, cuda_msg("cudaMemcpyAsync (execute)", e));
   return SEL_OK;
@@ -1237,10 +1242,12 @@ uint64_t execute_outputs(sel_ctx c, uint64_t max_size, uint64_t* out_local_count
                          uint64_t* out_global_offset, int* out_materialized) {
   const uint64_t count = c->h_result[kGateSlot];
   if (count > max_size) return count;  // "throw exception": nothing written
-  uint64_t local = c->h_result[0], offset = 0;
-  if (multi(c)) {
-    for (int r2 = 0; r2 < c->rank; ++r2) offset += c->h_result[1 + r2];
-    local = c->h_result[1 + c->rank];
+  const int nr = multi(c) ? c->nranks : 0;
+  uint64_t local = c->h_result[kGateSlot - 1], offset = 0;   // the mirrors (enqueue_execute)
+  if (nr > 0) {
+    const uint64_t* v = c->h_result + (nr <= kMirrorMax ? kGateSlot - nr : 1);
+    for (int r2 = 0; r2 < c->rank; ++r2) offset += v[r2];
+    local = v[c->rank];
   }
   if (out_local_count) *out_local_count = local;
   if (out_global_offset) *out_global_offset = offset;

@@ -1032,6 +1032,10 @@ __global__ void __launch_bounds__(256) peer_exchange_kernel(const PeerXchg x, co
 // With peers (xg.n > 0; sel_execute over peer memory) the exchange of the local count in
 // out_count[kGateSlot] runs first, fused here: gathered into out_count[1..n], summed into
 // out_count[kGateSlot].
+// The result words the host reads back are mirrored right below result[kGateSlot] so that one
+// copy fetches them (kMirrorMax ranks at most): the gathered per-rank counts at
+// [kGateSlot - nr, kGateSlot), or, without ranks, the local count at kGateSlot - 1. The
+// superblock sums stay: a kept selection serves any number of push-downs.
 __global__ void __launch_bounds__(1024) superblock_prefix_kernel(const uint32_t* __restrict__ sb_sum,
                                                                  uint32_t* __restrict__ sb_prefix,
                                                                  uint32_t nsb, uint64_t* __restrict__ out_count,
@@ -1043,6 +1047,8 @@ __global__ void __launch_bounds__(1024) superblock_prefix_kernel(const uint32_t*
     for (int r = 0; r < gate_ranks; ++r) g += out_count[1 + r];
     out_count[kGateSlot] = g;
   }
+  const int nr = xg.n > 0 ? xg.n : gate_ranks;
+  if (nr > 0 && nr <= kMirrorMax && (int)t < nr) out_count[kGateSlot - nr + t] = out_count[1 + t];
   const uint32_t per = (nsb + 1023u) / 1024u;
   const uint32_t b = min(nsb, t * per), e = min(nsb, b + per);
   uint32_t local = 0;
@@ -1064,7 +1070,10 @@ __global__ void __launch_bounds__(1024) superblock_prefix_kernel(const uint32_t*
       if (lane >= (uint32_t)d) wi += v;
     }
     s_w[lane] = wi - w;
-    if (lane == 31) *out_count = wi;
+    if (lane == 31) {
+      *out_count = wi;
+      if (nr == 0) out_count[kGateSlot - 1] = wi;
+    }
   }
   __syncthreads();
   uint32_t run = s_w[warp] + incl - local;

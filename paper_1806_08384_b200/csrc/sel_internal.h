@@ -172,6 +172,7 @@ struct SelectionBufs {
 constexpr int kMaxRanks = 1024;
 constexpr int kGateSlot = 1 + kMaxRanks;
 constexpr int kResultSlots = 2 + kMaxRanks;
+constexpr int kMirrorMax = 512;  // read-back mirror below kGateSlot (superblock_prefix_kernel)
 
 // Device-side scratch owned by a context.
 struct Scratch {

@@ -447,3 +447,28 @@ def test_exactness_1000_random_cases(ctx):
         got = res.columns[proj[0]].cpu().numpy().view(want_cols[0].dtype)
         np.testing.assert_array_equal(got, want_cols[0], err_msg=f"case {case}")
         t.release()
+
+
+def test_kept_selection_serves_repeated_pushdowns(ctx):
+    """A kept selection is not consumed: any number of push-downs (and executes' own selections)
+    materialise the same rows (regression: the superblock sums must survive the prefix scan)."""
+    T = configs.gen_c2(600_000)
+    cols = [c.numpy() for c in T.columns]
+    t = register(ctx, cols, T.types)
+    prog = encode(configs.c2_probes()["listing"], T.types)
+    want_c, want_ids, want_cols = oracle.pushdown(cols, T.types, prog, proj=[2, 3])
+    runs = []
+    t.count(prog, keep_selection=True)
+    runs += [t.pushdown(prog, project=[2, 3]) for _ in range(3)]
+    runs.append(t.execute(prog, project=[2, 3], max_size=600_000))
+    runs += [t.pushdown(prog, project=[2, 3]) for _ in range(2)]
+    q = t.prepare_execute(prog, project=[2, 3], max_size=600_000)
+    q.run()
+    runs.append(q.result())
+    runs += [t.pushdown(prog, project=[2, 3]) for _ in range(2)]
+    for r in runs:
+        assert r.count == want_c
+        np.testing.assert_array_equal(r.rowids.cpu().numpy().view(np.uint32), want_ids)
+        for j, c in enumerate([2, 3]):
+            np.testing.assert_array_equal(r.columns[c].cpu().numpy().view(want_cols[j].dtype), want_cols[j])
+    q.release()
