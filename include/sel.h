@@ -157,6 +157,17 @@ void sel_table_release(sel_table table);
  * Returns the count, or SEL_ERR (SEL_E_ARG, SEL_E_PROGRAM, SEL_E_TYPE, SEL_E_CUDA, SEL_E_NCCL). */
 uint64_t sel_count(sel_table table, const void* prog, size_t prog_bytes, void* cuda_stream);
 
+/* sel_count_async: the same count, enqueued on `cuda_stream` WITHOUT waiting: the global count
+ * (uint64) lands in the DEVICE word *d_out when the stream reaches it (with peers or a
+ * communicator after the exchange, also enqueued). No host synchronisation, so the call can be
+ * captured into a caller's CUDA graph or several probes pipelined ("an async variant
+ * that writes the count to a device pointer"). The context's scratch is reused by every probe:
+ * enqueue a context's asynchronous and blocking probes on ONE stream (or synchronise between
+ * streams). Keeps no selection. Errors (validation, launch): as sel_count, returned at once;
+ * kernel faults surface at the caller's next synchronisation. */
+sel_status sel_count_async(sel_table table, const void* prog, size_t prog_bytes, uint64_t* d_out,
+                           void* cuda_stream);
+
 /* sel_count_ex: sel_count with flags.
  *   SEL_KEEP_SELECTION: the probe also keeps its selection in the context's scratch (the local row
  *   mask, 1 bit per row, plus per-1024-row counts: n/8 + n/512 bytes). A following sel_pushdown of

@@ -283,6 +283,17 @@ class Table:
             raise last_error()
         return int(r)
 
+    def count_async(self, pred, out: torch.Tensor, stream=None) -> torch.Tensor:
+        """Enqueue the count without waiting: the global count lands in `out` (a one-element
+        int64 CUDA tensor) when `stream` reaches it — capturable into a CUDA graph
+        (include/sel.h sel_count_async). Enqueue a context's probes on one stream."""
+        if not out.is_cuda or out.dtype != torch.int64 or out.numel() < 1:
+            raise ValueError("out must be a CUDA int64 tensor")
+        prog = self.program(pred)
+        check(lib().sel_count_async(self._h, prog, len(prog), out.data_ptr(),
+                                    _stream_ptr(stream, self.ctx.device)))
+        return out
+
     def count_batch(self, preds, stream=None) -> list:
         """Exact counts of several predicates in ONE scan: each column read
         once, each distinct leaf evaluated once; e.g. the worked example's four leaves and their

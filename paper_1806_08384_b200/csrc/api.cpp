@@ -896,6 +896,7 @@ uint64_t sel_count(sel_table t, const void* prog, size_t prog_bytes, void* cuda_
   return sel_count_ex(t, prog, prog_bytes, 0u, nullptr, 0u, cuda_stream);
 }
 
+
 sel_status sel_ctx_last_times(sel_ctx ctx, float* count_ms, float* pushdown_ms) {
   clear_error();
   if (!ctx) return set_error(SEL_E_ARG, "null ctx");
@@ -1309,6 +1310,33 @@ uint64_t sel_count_ex(sel_table t, const void* prog, size_t prog_bytes, uint32_t
     c->kept_prog.assign(static_cast<const char*>(prog), prog_bytes);
   }
   return c->h_result[0];
+}
+
+sel_status sel_count_async(sel_table t, const void* prog, size_t prog_bytes, uint64_t* d_out,
+                           void* cuda_stream) {
+  clear_error();
+  if (!t || !d_out) return set_error(SEL_E_ARG, "null argument");
+  sel_ctx c = t->ctx;
+  if (c->destroyed) return set_error(SEL_E_STATE, "context destroyed");
+  Plan plan;
+  if (plan_for(t, prog, prog_bytes, &plan) != SEL_OK) return g_status;
+  cudaStream_t stream = (cudaStream_t)cuda_stream;
+  DeviceGuard g(c->device);
+  if (!g.ok) return set_error(SEL_E_CUDA, "cudaSetDevice failed");
+  const uint64_t n = t->local_rows;
+  if (n == 0 || plan.path == PATH_CONST) {  // no scan: the local value by a device-side store
+    const int le = launch_set_u64(d_out, plan.path == PATH_CONST && plan.const_value ? n : 0, stream);
+    if (le != cudaSuccess) return set_error(SEL_E_CUDA, cuda_msg("launch", (cudaError_t)le));
+    if (c->peers) {
+      const int le2 = launch_peer_exchange(c->xg, d_out, 1, nullptr, d_out, stream);
+      if (le2 != cudaSuccess) return set_error(SEL_E_CUDA, cuda_msg("peer exchange", (cudaError_t)le2));
+    } else if (c->comm) {
+      ncclResult_t r = nccl().AllReduce(d_out, d_out, 1, ncclUint64, ncclSum, c->comm, stream);
+      if (r != ncclSuccess) return set_error(SEL_E_NCCL, nccl_msg("ncclAllReduce", r));
+    }
+    return SEL_OK;
+  }
+  return enqueue_count(t, plan, 0u, nullptr, 0u, stream, d_out);
 }
 
 }  // extern "C"

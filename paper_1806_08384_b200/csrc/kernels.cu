@@ -1470,6 +1470,11 @@ int occupancy_count_fast(int fast_n, bool keep, size_t dyn) {
     default: return occupancy_of(count_kernel<DevProgramSmall, true, kWarpsPerCta, 4>, dyn);
   }
 }
+__global__ void set_u64_kernel(uint64_t* p, uint64_t v) { *p = v; }
+int launch_set_u64(uint64_t* p, uint64_t v, void* st) {
+  set_u64_kernel<<<1, 1, 0, (cudaStream_t)st>>>(p, v);
+  return (int)cudaGetLastError();
+}
 int launch_peer_exchange(const PeerXchg& x, const uint64_t* src, int k, uint64_t* out,
                          uint64_t* sums, void* st) {
   peer_exchange_kernel<<<1, 256, 0, (cudaStream_t)st>>>(x, src, k, out, sums);

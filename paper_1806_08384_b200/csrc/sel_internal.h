@@ -208,6 +208,9 @@ struct PeerXchg {
 int launch_peer_exchange(const PeerXchg& x, const uint64_t* src, int k, uint64_t* out,
                          uint64_t* sums, void* stream);
 
+// *p = v on `stream` (one thread; sel_count_async's constant and empty cases).
+int launch_set_u64(uint64_t* p, uint64_t v, void* stream);
+
 // Launch entry points (kernels.cu). Return cudaError_t as int.
 // keep != nullptr: also keep the selection (and, with keep->n_keep > 0, the selected values of
 // projected predicate columns; the leaves carry the capture offsets and keep->warp_smem is set).

@@ -472,3 +472,48 @@ def test_kept_selection_serves_repeated_pushdowns(ctx):
         for j, c in enumerate([2, 3]):
             np.testing.assert_array_equal(r.columns[c].cpu().numpy().view(want_cols[j].dtype), want_cols[j])
     q.release()
+
+
+def test_count_async_and_user_graph_capture(ctx, cuda_device):
+    """sel_count_async: no host synchronisation; the count lands in a device word — also when the
+    call is captured into the caller's own CUDA graph (torch.cuda.graph) and replayed after the
+    column changed in place; constant programs and an empty table; a one-rank peer context."""
+    T = configs.gen_c2(600_000)
+    cols = [c.numpy().copy() for c in T.columns]
+    types = T.types
+    for cx in (ctx, None):
+        if cx is None:
+            cx = sel.Context(cuda_device)
+            cx.set_peers(1, 0, [cx.peer_handle()])
+        t = register(cx, cols, types)
+        prog = encode(configs.c2_probes()["listing"], types)
+        out = torch.zeros(4, dtype=torch.int64, device=cx.device)
+        s = torch.cuda.Stream(cx.device)
+        with torch.cuda.stream(s):
+            t.count_async(prog, out[0:1], stream=s)
+            t.count_async(encode(Const(True), types), out[1:2], stream=s)
+            t.count_async(encode(Const(False), types), out[2:3], stream=s)
+        s.synchronize()
+        assert out[:3].tolist() == [100_200, 600_000, 0]
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=s):
+            t.count_async(prog, out[3:4], stream=s)
+        out[3] = -1
+        g.replay()
+        torch.cuda.synchronize()
+        assert int(out[3]) == 100_200
+        t.tensors[0].fill_(2)                                # every row has A = 2 now
+        g.replay()
+        torch.cuda.synchronize()
+        want = oracle.count([np.full(600_000, 2, np.int32)] + cols[1:], types, prog)
+        assert int(out[3]) == want
+        del g
+        t.release()
+        if cx is not ctx:
+            cx.drop_peers()
+            cx.close()
+    e = register(ctx, [np.zeros(0, np.int32)], [INT32])
+    o = torch.full((1,), -1, dtype=torch.int64, device=ctx.device)
+    e.count_async(encode(Cmp("=", 0, 1), [INT32]), o)
+    torch.cuda.synchronize()
+    assert int(o) == 0
