@@ -87,7 +87,9 @@ sel_status sel_ctx_create(int cuda_device, sel_ctx* out);
  * rank 0 produced with sel_nccl_unique_id and broadcast out of band (torch.distributed).
  * Collective: every rank must call it. NCCL is loaded with dlopen("libnccl.so.2") on first use.
  * nranks == 1 is allowed (a one-rank communicator). Errors: SEL_E_ARG, SEL_E_NCCL, SEL_E_STATE
- * (already set). */
+ * (already set). Failure detection: while a probe waits for its stream the library polls
+ * ncclCommGetAsyncError; an asynchronous NCCL error (a rank died) aborts the communicator and
+ * fails the probe with SEL_E_NCCL instead of hanging, and every later probe of the context too. */
 sel_status sel_ctx_set_comm(sel_ctx ctx, int nranks, int rank, const void* nccl_unique_id);
 
 /* Cross-rank exchange over peer memory, without NCCL ("a one-shot peer write of each

@@ -10,6 +10,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "sel.h"
@@ -37,9 +38,14 @@ uint64_t fail64(sel_status st, const std::string& msg) {
   set_error(st, msg);
   return SEL_ERR;
 }
+// sync_stream's report of a failed communicator (not a CUDA code).
+constexpr cudaError_t kNcclAsyncFailed = (cudaError_t)0x7FFF0001;
 std::string cuda_msg(const char* what, cudaError_t e) {
+  if (e == kNcclAsyncFailed)
+    return std::string(what) + ": NCCL asynchronous error (a rank failed; communicator aborted)";
   return std::string(what) + ": " + cudaGetErrorName(e) + " (" + cudaGetErrorString(e) + ")";
 }
+sel_status sync_code(cudaError_t e) { return e == kNcclAsyncFailed ? SEL_E_NCCL : SEL_E_CUDA; }
 
 struct DeviceGuard {
   int prev = -1;
@@ -65,6 +71,8 @@ struct NcclApi {
                             cudaStream_t) = nullptr;
   ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
   const char* (*GetErrorString)(ncclResult_t) = nullptr;
+  ncclResult_t (*CommGetAsyncError)(ncclComm_t, ncclResult_t*) = nullptr;  // optional
+  ncclResult_t (*CommAbort)(ncclComm_t) = nullptr;                         // optional
 };
 
 NcclApi& nccl() {
@@ -84,6 +92,8 @@ NcclApi& nccl() {
     a.AllGather = (decltype(a.AllGather))dlsym(h, "ncclAllGather");
     a.CommDestroy = (decltype(a.CommDestroy))dlsym(h, "ncclCommDestroy");
     a.GetErrorString = (decltype(a.GetErrorString))dlsym(h, "ncclGetErrorString");
+    a.CommGetAsyncError = (decltype(a.CommGetAsyncError))dlsym(h, "ncclCommGetAsyncError");
+    a.CommAbort = (decltype(a.CommAbort))dlsym(h, "ncclCommAbort");
     a.loaded = a.GetUniqueId && a.CommInitRank && a.AllReduce && a.AllGather && a.CommDestroy &&
                a.GetErrorString;
     if (!a.loaded) a.error = "libnccl.so.2 lacks a required symbol";
@@ -162,6 +172,7 @@ struct sel_ctx_s {
   bool capturing = false;             // timing events become graph event-record nodes
   int count_nw = 0;                   // SEL_COUNT_NW: 8 forces 8-warp count CTAs
   // the library's own exchange over peer memory (sel_ctx_set_peers; sel_internal.h PeerXchg)
+  bool comm_failed = false;          // an asynchronous NCCL error aborted the communicator
   bool peers = false;
   uint64_t* peer_buf = nullptr;       // this rank's symmetric buffer (exported by CUDA IPC)
   uint64_t** peer_ptrs = nullptr;     // device array of the n buffers as mapped here
@@ -202,6 +213,26 @@ constexpr size_t kMaxBitmaps = 65536;  // ids fit the instruction's u16 `a`
 
 // Cross-rank combination needed: a communicator (NCCL) or peers (the library's own exchange).
 bool multi(sel_ctx c) { return c->comm != nullptr || c->peers; }
+
+// Wait for stream `s`. With a communicator, poll instead of blocking so that an asynchronous NCCL
+// failure (a rank died) aborts the communicator and fails the call instead of hanging
+// (SURVEY §5 failure detection; the peer exchange bounds its own waits).
+cudaError_t sync_stream(sel_ctx c, cudaStream_t s) {
+  if (!c->comm || !nccl().CommGetAsyncError) return cudaStreamSynchronize(s);
+  for (unsigned spin = 0;; ++spin) {
+    const cudaError_t q = cudaStreamQuery(s);
+    if (q != cudaErrorNotReady) return q;
+    ncclResult_t st = ncclSuccess;
+    if (nccl().CommGetAsyncError(c->comm, &st) == ncclSuccess && st != ncclSuccess &&
+        st != ncclInProgress) {
+      if (nccl().CommAbort) nccl().CommAbort(c->comm);
+      c->comm = nullptr;
+      c->comm_failed = true;   // every later probe of this context fails (plan_for)
+      return kNcclAsyncFailed;
+    }
+    if (spin > 64) std::this_thread::yield();
+  }
+}
 
 // After a synchronisation that followed peer exchanges: a timed-out wait (a rank missing) is an
 // error of the call (the flag is reset).
@@ -395,6 +426,8 @@ size_t count_slots(const Plan& plan) {
 }
 
 sel_status plan_for(sel_table t, const void* prog, size_t bytes, Plan* plan) {
+  if (t->ctx->comm_failed)
+    return set_error(SEL_E_NCCL, "the communicator failed earlier (a rank was lost); context unusable");
   Program P;
   std::string msg;
   const int st = decode_program(prog, bytes, t->types.data(), (uint32_t)t->types.size(), &P, &msg);
@@ -416,8 +449,8 @@ int grid_for(sel_ctx c, uint64_t units, int occ) {
 
 sel_status ensure_status(sel_ctx c, uint64_t ntiles, cudaStream_t stream) {
   if (c->s.status_cap >= ntiles) return SEL_OK;
-  cudaError_t e = cudaStreamSynchronize(stream);
-  if (e != cudaSuccess) return set_error(SEL_E_CUDA, cuda_msg("cudaStreamSynchronize", e));
+  cudaError_t e = sync_stream(c, stream);
+  if (e != cudaSuccess) return set_error(sync_code(e), cuda_msg("cudaStreamSynchronize", e));
   if (c->s.status) cudaFree(c->s.status);
   c->s.status = nullptr;
   c->s.status_cap = 0;
@@ -1192,8 +1225,8 @@ sel_status gather_counts(sel_ctx c, uint64_t local, void* cuda_stream) {
   }
   e = cudaMemcpyAsync(c->h_result + 1, c->s.result + 1, c->nranks * sizeof(uint64_t),
                       cudaMemcpyDeviceToHost, stream);
-  if (e == cudaSuccess) e = cudaStreamSynchronize(stream);
-  if (e != cudaSuccess) return set_error(SEL_E_CUDA, cuda_msg("all-gather result", e));
+  if (e == cudaSuccess) e = sync_stream(c, stream);
+  if (e != cudaSuccess) return set_error(sync_code(e), cuda_msg("all-gather result", e));
   return peer_status(c);
 }
 
@@ -1298,8 +1331,8 @@ uint64_t sel_count_ex(sel_table t, const void* prog, size_t prog_bytes, uint32_t
   if (!scan && !multi(c)) return plan.path == PATH_CONST && plan.const_value ? n : 0;
   if (enqueue_count(t, plan, flags, keep_cols, nkeep, stream, c->s.result) != SEL_OK) return SEL_ERR;
   cudaError_t e = cudaMemcpyAsync(c->h_result, c->s.result, sizeof(uint64_t), cudaMemcpyDeviceToHost, stream);
-  if (e == cudaSuccess) e = cudaStreamSynchronize(stream);
-  if (e != cudaSuccess) return fail64(SEL_E_CUDA, cuda_msg("count result", e));
+  if (e == cudaSuccess) e = sync_stream(c, stream);
+  if (e != cudaSuccess) return fail64(sync_code(e), cuda_msg("count result", e));
   if (peer_status(c) != SEL_OK) return SEL_ERR;
   if (scan && c->timing) {
     cudaEventElapsedTime(&c->last_ms, c->ev0, c->ev1);
@@ -1486,8 +1519,8 @@ uint64_t pushdown_impl(sel_table t, const void* prog, size_t prog_bytes, const u
     }
     e = cudaMemcpyAsync(c->h_result + 1, c->s.result + 1, c->nranks * sizeof(uint64_t),
                         cudaMemcpyDeviceToHost, stream);
-    if (e == cudaSuccess) e = cudaStreamSynchronize(stream);
-    if (e != cudaSuccess) return fail64(SEL_E_CUDA, cuda_msg("push-down result", e));
+    if (e == cudaSuccess) e = sync_stream(c, stream);
+    if (e != cudaSuccess) return fail64(sync_code(e), cuda_msg("push-down result", e));
     if (peer_status(c) != SEL_OK) return SEL_ERR;
     for (int r2 = 0; r2 < c->nranks; ++r2) {
       if (r2 < c->rank) offset += c->h_result[1 + r2];
@@ -1497,8 +1530,8 @@ uint64_t pushdown_impl(sel_table t, const void* prog, size_t prog_bytes, const u
   } else {
     if (scan) {
       e = cudaMemcpyAsync(c->h_result, c->s.result, sizeof(uint64_t), cudaMemcpyDeviceToHost, stream);
-      if (e == cudaSuccess) e = cudaStreamSynchronize(stream);
-      if (e != cudaSuccess) return fail64(SEL_E_CUDA, cuda_msg("push-down result", e));
+      if (e == cudaSuccess) e = sync_stream(c, stream);
+      if (e != cudaSuccess) return fail64(sync_code(e), cuda_msg("push-down result", e));
     }
     local = total = c->h_result[0];
   }
@@ -1595,8 +1628,8 @@ uint64_t sel_count_sampled(sel_table t, const void* prog, size_t prog_bytes, uin
     if (r != ncclSuccess) return fail64(SEL_E_NCCL, nccl_msg("ncclAllReduce(sampled)", r));
   }
   e = cudaMemcpyAsync(c->h_result, c->s.result, 2 * sizeof(uint64_t), cudaMemcpyDeviceToHost, stream);
-  if (e == cudaSuccess) e = cudaStreamSynchronize(stream);
-  if (e != cudaSuccess) return fail64(SEL_E_CUDA, cuda_msg("sampled count result", e));
+  if (e == cudaSuccess) e = sync_stream(c, stream);
+  if (e != cudaSuccess) return fail64(sync_code(e), cuda_msg("sampled count result", e));
   if (peer_status(c) != SEL_OK) return SEL_ERR;
   if (out_sample_rows) *out_sample_rows = c->h_result[1];
   return c->h_result[0];
@@ -1703,8 +1736,8 @@ sel_status sel_count_batch(sel_table t, const void* const* progs, const size_t* 
     if (r != ncclSuccess) return set_error(SEL_E_NCCL, nccl_msg("ncclAllReduce(batch)", r));
   }
   e = cudaMemcpyAsync(c->h_result + 1, d_out, nprog * sizeof(uint64_t), cudaMemcpyDeviceToHost, stream);
-  if (e == cudaSuccess) e = cudaStreamSynchronize(stream);
-  if (e != cudaSuccess) return set_error(SEL_E_CUDA, cuda_msg("batch result", e));
+  if (e == cudaSuccess) e = sync_stream(c, stream);
+  if (e != cudaSuccess) return set_error(sync_code(e), cuda_msg("batch result", e));
   if (peer_status(c) != SEL_OK) return g_status;
   if (n > 0 && nop > 0 && c->timing) {
     cudaEventElapsedTime(&c->last_ms, c->ev0, c->ev1);
@@ -1750,8 +1783,8 @@ uint64_t sel_execute(sel_table t, const void* prog, size_t prog_bytes, const uin
           return SEL_ERR;
         cudaError_t e = cudaMemcpyAsync(c->h_result, c->s.result, sizeof(uint64_t),
                                         cudaMemcpyDeviceToHost, stream);
-        if (e == cudaSuccess) e = cudaStreamSynchronize(stream);
-        if (e != cudaSuccess) return fail64(SEL_E_CUDA, cuda_msg("count result", e));
+        if (e == cudaSuccess) e = sync_stream(c, stream);
+        if (e != cudaSuccess) return fail64(sync_code(e), cuda_msg("count result", e));
         local = c->h_result[0];
         c->kept_table = t;
         c->kept_prog.assign(static_cast<const char*>(prog), prog_bytes);
@@ -1789,8 +1822,8 @@ uint64_t sel_execute(sel_table t, const void* prog, size_t prog_bytes, const uin
   sel_status st = enqueue_execute(t, plan, proj_cols, nproj, nkeep, max_size, out_rowids, out_cols,
                                   capacity_rows, stream);
   if (st != SEL_OK) return SEL_ERR;
-  cudaError_t e = cudaStreamSynchronize(stream);
-  if (e != cudaSuccess) return fail64(SEL_E_CUDA, cuda_msg("execute result", e));
+  cudaError_t e = sync_stream(c, stream);
+  if (e != cudaSuccess) return fail64(sync_code(e), cuda_msg("execute result", e));
   if (peer_status(c) != SEL_OK) return SEL_ERR;
   c->kept_table = t;
   c->kept_prog.assign(static_cast<const char*>(prog), prog_bytes);
@@ -1922,8 +1955,8 @@ uint64_t sel_prepared_execute(sel_prepared q, uint64_t* out_local_count,
   cudaStream_t stream = (cudaStream_t)cuda_stream;
   c->kept_table = nullptr;
   cudaError_t e = cudaGraphLaunch(q->exec, stream);
-  if (e == cudaSuccess) e = cudaStreamSynchronize(stream);
-  if (e != cudaSuccess) return fail64(SEL_E_CUDA, cuda_msg("prepared execute", e));
+  if (e == cudaSuccess) e = sync_stream(c, stream);
+  if (e != cudaSuccess) return fail64(sync_code(e), cuda_msg("prepared execute", e));
   if (peer_status(c) != SEL_OK) return SEL_ERR;
   c->kept_table = t;
   c->kept_prog = q->prog;
