@@ -253,6 +253,17 @@ def cpu_baseline(host_cols, table_like, prog, proj, prog_cols, nthreads, bitmaps
     return step_b, t2 - t0, t1 - t0, t2 - t1, cnt
 
 
+def cpu_model():
+    """The host CPU model (each CPU record states the model and the thread count)."""
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
+
+
 def run_reference(args):
     """--impl reference: the CPU oracle as it stands, on the host cores, on a bounded sample."""
     import numpy as np
@@ -292,7 +303,7 @@ def run_reference(args):
             "config": {"workload": f"{args.config}: {desc}", "global_rows": n,
                        "sample_rows": sample},
             "cpu_baseline": {"value": round(value, 3), "unit": "GB/s", "cores": nthreads,
-                             "kind": "oracle",
+                             "kind": "oracle", "cpu_model": cpu_model(),
                              "sample": f"first {sample} rows of the workload; count on {nthreads} threads (oracle_count_mt), push-down single-threaded (oracle_pushdown)"},
             "e2e": {"value": round(value, 3), "unit": "GB/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
@@ -610,6 +621,7 @@ def run_ours(args):
         by, dt, t_cnt, t_push, cnt = cpu_baseline(host_cols, sample_table, prog, proj, pc, nthreads,
                                                   bitmaps=bms)
         cpu = {"value": round(by / dt / 1e9, 3), "unit": "GB/s", "cores": nthreads, "kind": "oracle",
+               "cpu_model": cpu_model(),
                "sample": f"first {ns} of {n} rows; count on {nthreads} threads ({t_cnt:.2f} s), "
                          f"push-down on 1 thread ({t_push:.2f} s)"}
 
