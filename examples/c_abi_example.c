@@ -117,6 +117,15 @@ int main(void) {
   printf("execute: materialised %llu ascending ids; gate at maxSize = count - 1 -> reverted\n",
          (unsigned long long)want);
 
+  /* the asynchronous count: lands in a device word, no host synchronisation in the call */
+  uint64_t* dcount;
+  uint64_t hcount = 0;
+  cudaMalloc((void**)&dcount, sizeof(uint64_t));
+  CHECK(sel_count_async(t, prog, len, dcount, NULL));
+  cudaMemcpy(&hcount, dcount, sizeof(uint64_t), cudaMemcpyDeviceToHost);   /* synchronises */
+  if (hcount != want) return 6;
+  cudaFree(dcount);
+
   /* error path: a malformed program */
   const uint8_t bad[4] = {'S', 'E', 'L', 'P'};
   if (sel_count(t, bad, sizeof bad, NULL) != SEL_ERR || sel_last_error() != SEL_E_PROGRAM) return 6;
