@@ -35,7 +35,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="c2", choices=["c1", "c2", "c3", "c4", "c5", "c6"])
+    ap.add_argument("--config", default="c2", choices=["c0", "c1", "c2", "c3", "c4", "c5", "c6"])
     ap.add_argument("--rows", type=int, default=0, help="override global rows (testing only)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-read-peak", action="store_true")
@@ -69,6 +69,12 @@ def workload(name, rows):
         return (n, lambda s, c, d: configs.gen_lineorder_q2(n, 80, s, c, device=d), node, [0, 1, 3],
                 "SSB SF-80 lineorder, Q2.1 semijoin probe: lo_partkey IN {p_category = 12} AND "
                 "lo_suppkey IN {s_region = 1} (PAPER.md:719-729), push-down of orderdate, partkey, revenue")
+    if name == "c0":   # SURVEY §8d optional context: TPC-H SF-50 orders
+        n = rows or 75_000_000
+        return (n, lambda s, c, d: configs.gen_orders(n, s, c, device=d),
+                configs.orders_probes()["q5_orderdate"], [0, 1],
+                "TPC-H SF-50 orders (75M rows), Q5's o_orderdate one-year range (PAPER.md:698-699; "
+                "15.2% of orders, PAPER.md:646), push-down of o_orderkey, o_custkey")
     if name == "c2":
         n = rows or configs.C2_ROWS
         return (n, lambda s, c, d: configs.gen_c2(n, s, c, device=d),
