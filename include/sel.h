@@ -291,6 +291,22 @@ sel_status sel_bitmap_release(sel_ctx ctx, uint32_t id);
 uint64_t sel_count_sampled(sel_table table, const void* prog, size_t prog_bytes, uint32_t stride,
                            uint32_t phase, uint64_t* out_sample_rows, void* cuda_stream);
 
+/* sel_histogram (a synopsis baseline beside the exact probe): an EQUI-DEPTH
+ * histogram of column `col` over the same block sample as sel_count_sampled
+ * (chunks c mod stride == phase; stride 1 = every row), local shard only. The sample's m values
+ * are sorted (CUB radix sort on the device) and cut into nbuckets (1..65536) buckets of
+ * positions [floor(b m / B), floor((b+1) m / B)); bucket b reports its lowest and highest value
+ * (out_lo/out_hi, the column's values as int64), its rows (out_rows) and its number of distinct
+ * values V(b) (out_distinct) — host arrays of nbuckets; an empty bucket (m < B) reports
+ * lo = hi = 0, rows = distinct = 0. *out_sample_rows (may be NULL) = m. The
+ * paper's equality estimate |sigma_{A=x}(R)| = D / V(b_x), D = T(R) / B, is host arithmetic over
+ * these (Python: paper_1806_08384_b200.equi_depth_estimate).
+ * Errors: SEL_E_ARG (bad stride/phase/nbuckets/column), SEL_E_TYPE (not INT32/DATE32/DICT*),
+ * SEL_E_TOO_LARGE (a sample of >= 2^31 rows), SEL_E_CUDA. */
+sel_status sel_histogram(sel_table table, uint32_t col, uint32_t stride, uint32_t phase,
+                         uint32_t nbuckets, int64_t* out_lo, int64_t* out_hi, uint64_t* out_rows,
+                         uint64_t* out_distinct, uint64_t* out_sample_rows, void* cuda_stream);
+
 /* Validate a program against column types without running it (host only; no GPU needed).
  * Returns SEL_OK or the status sel_count would report for it. */
 sel_status sel_program_check(const void* prog, size_t prog_bytes, const sel_type* types,

@@ -9,8 +9,8 @@ memory, streams and process groups only.
 from ._native import SelError, EXPORTS
 from .predicate import col, TRUE, FALSE, INT32, INT64, FLOAT32, DATE32, DICT8, DICT16, DICT32
 from .api import (Context, Table, PushdownResult, ExecuteResult, program_check, program_path,
-                  program_plan)
+                  program_plan, equi_depth_estimate)
 
 __all__ = ["SelError", "EXPORTS", "col", "TRUE", "FALSE", "INT32", "INT64", "FLOAT32", "DATE32",
            "DICT8", "DICT16", "DICT32", "Context", "Table", "PushdownResult", "ExecuteResult", "program_check",
-           "program_path", "program_plan"]
+           "program_path", "program_plan", "equi_depth_estimate"]

@@ -23,7 +23,7 @@ EXPORTS = ["sel_ctx_create", "sel_ctx_set_comm", "sel_nccl_unique_id", "sel_ctx_
            "sel_ctx_peer_handle", "sel_ctx_set_peers",
            "sel_ctx_set_timing", "sel_ctx_last_kernel_ms", "sel_table_register",
            "sel_table_release", "sel_count", "sel_count_async", "sel_count_ex", "sel_execute", "sel_pushdown",
-           "sel_ctx_last_times", "sel_count_batch", "sel_count_sampled",
+           "sel_ctx_last_times", "sel_count_batch", "sel_count_sampled", "sel_histogram",
            "sel_bitmap_register", "sel_bitmap_release",
            "sel_prepare_execute", "sel_prepared_execute", "sel_prepared_release",
            "sel_ctx_last_pushdown_path", "sel_ctx_set_pushdown_path", "sel_program_check",
@@ -69,6 +69,7 @@ def lib() -> ctypes.CDLL:
         "sel_count": (u64, [vp, ctypes.c_char_p, sz, vp]),
         "sel_count_ex": (u64, [vp, ctypes.c_char_p, sz, u32, vp, u32, vp]),
         "sel_count_async": (i32, [vp, ctypes.c_char_p, sz, vp, vp]),
+        "sel_histogram": (i32, [vp, u32, u32, u32, u32, vp, vp, vp, vp, vp, vp]),
         "sel_execute": (u64, [vp, ctypes.c_char_p, sz, vp, u32, u64, vp, vp, u64,
                               ctypes.POINTER(u64), ctypes.POINTER(u64), ctypes.POINTER(i32), vp]),
         "sel_count_sampled": (u64, [vp, ctypes.c_char_p, sz, u32, u32, ctypes.POINTER(u64), vp]),

@@ -12,6 +12,7 @@ import ctypes
 from dataclasses import dataclass
 from typing import Mapping, Sequence
 
+import numpy as np
 import torch
 
 from . import _native
@@ -294,6 +295,24 @@ class Table:
                                     _stream_ptr(stream, self.ctx.device)))
         return out
 
+    def histogram(self, column, buckets: int = 64, stride: int = 1, phase: int = 0,
+                  stream=None) -> dict:
+        """Equi-depth histogram of an integer column over a block sample (SURVEY §8f NEXT(4);
+        include/sel.h sel_histogram): numpy arrays lo, hi (values), rows, distinct per bucket,
+        and sample_rows. Local shard."""
+        col = self._col_indices([column])[0]
+        lo = np.zeros(buckets, np.int64)
+        hi = np.zeros(buckets, np.int64)
+        rows = np.zeros(buckets, np.uint64)
+        distinct = np.zeros(buckets, np.uint64)
+        m = ctypes.c_uint64(0)
+        ptr = lambda a: a.ctypes.data_as(ctypes.c_void_p)
+        check(lib().sel_histogram(self._h, col, int(stride), int(phase), int(buckets), ptr(lo),
+                                  ptr(hi), ptr(rows), ptr(distinct), ctypes.byref(m),
+                                  _stream_ptr(stream, self.ctx.device)))
+        return {"lo": lo, "hi": hi, "rows": rows, "distinct": distinct,
+                "sample_rows": int(m.value), "table_rows": self.local_rows}
+
     def count_batch(self, preds, stream=None) -> list:
         """Exact counts of several predicates in ONE scan: each column read
         once, each distinct leaf evaluated once; e.g. the worked example's four leaves and their
@@ -422,6 +441,19 @@ def program_check(prog: bytes, types: Sequence[int]) -> int:
 def program_path(prog: bytes, types: Sequence[int]) -> int:
     arr = (ctypes.c_int * max(len(types), 1))(*types)
     return int(lib().sel_program_path(prog, len(prog), arr, len(types)))
+
+
+def equi_depth_estimate(hist: dict, value: int) -> float:
+    """The paper's equi-depth equality estimate: |sigma_{A=x}(R)| = D / V(b_x)
+    with D = T(R) / B, summed over every bucket whose [lo, hi] holds x (a value heavy enough to
+    span buckets — the reading under which the paper's "30/2 + 30/1 + 30/7 = 49.3" follows the
+    formula). A synopsis baseline to set beside the exact count."""
+    d = hist["table_rows"] / len(hist["rows"])
+    est = 0.0
+    for lo, hi, v in zip(hist["lo"], hist["hi"], hist["distinct"]):
+        if v and lo <= value <= hi:
+            est += d / float(v)
+    return est
 
 
 def program_plan(prog: bytes, types: Sequence[int]) -> dict:

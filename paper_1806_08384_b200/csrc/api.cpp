@@ -1565,6 +1565,66 @@ uint64_t sel_pushdown(sel_table t, const void* prog, size_t prog_bytes, const ui
                        out_local_count, out_global_offset, cuda_stream, true);
 }
 
+sel_status sel_histogram(sel_table t, uint32_t col, uint32_t stride, uint32_t phase,
+                         uint32_t nbuckets, int64_t* out_lo, int64_t* out_hi, uint64_t* out_rows,
+                         uint64_t* out_distinct, uint64_t* out_sample_rows, void* cuda_stream) {
+  clear_error();
+  if (!t || !out_lo || !out_hi || !out_rows || !out_distinct) return set_error(SEL_E_ARG, "null argument");
+  if (stride == 0 || phase >= stride) return set_error(SEL_E_ARG, "need stride >= 1 and phase < stride");
+  if (nbuckets < 1 || nbuckets > 65536) return set_error(SEL_E_ARG, "nbuckets must be 1..65536");
+  sel_ctx c = t->ctx;
+  if (c->destroyed) return set_error(SEL_E_STATE, "context destroyed");
+  if (col >= t->cols.size()) return set_error(SEL_E_ARG, "column index out of range");
+  const int type = t->types[col];
+  uint32_t flip;
+  if (type == SEL_INT32 || type == SEL_DATE32) flip = 0x80000000u;
+  else if (type == SEL_DICT8 || type == SEL_DICT16 || type == SEL_DICT32) flip = 0u;
+  else return set_error(SEL_E_TYPE, "histograms take INT32, DATE32 and DICT columns");
+  const uint64_t n = t->local_rows;
+  const uint64_t nchunks = (n + kChunkRows - 1) / kChunkRows;
+  const uint64_t nsamp = nchunks > phase ? (nchunks - phase + stride - 1) / stride : 0;
+  uint64_t m = nsamp * kChunkRows;
+  if (nsamp > 0) {   // the last sampled chunk may be the table's partial tail
+    const uint64_t last = phase + (nsamp - 1) * (uint64_t)stride;
+    m -= kChunkRows - std::min<uint64_t>(kChunkRows, n - last * kChunkRows);
+  }
+  if (m >= (1ull << 31)) return set_error(SEL_E_TOO_LARGE, "sample of 2^31 rows or more");
+  if (out_sample_rows) *out_sample_rows = m;
+  cudaStream_t stream = (cudaStream_t)cuda_stream;
+  DeviceGuard g(c->device);
+  if (!g.ok) return set_error(SEL_E_CUDA, "cudaSetDevice failed");
+  const size_t tb = histogram_temp_bytes(std::max<uint64_t>(m, 1));
+  const size_t kb = std::max<uint64_t>(m, 1) * sizeof(uint32_t);
+  const size_t ob = (size_t)nbuckets * (2 * sizeof(uint32_t) + 2 * sizeof(uint64_t));
+  char* buf = nullptr;
+  cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&buf), 2 * kb + tb + ob + 64, stream);
+  if (e != cudaSuccess) return set_error(SEL_E_CUDA, cuda_msg("cudaMallocAsync(histogram)", e));
+  uint32_t* keys = reinterpret_cast<uint32_t*>(buf);
+  uint32_t* sorted = keys + kb / sizeof(uint32_t);
+  uint64_t* rows = reinterpret_cast<uint64_t*>(buf + ((2 * kb + 7) & ~size_t(7)));
+  uint64_t* distinct = rows + nbuckets;
+  uint32_t* lo = reinterpret_cast<uint32_t*>(distinct + nbuckets);
+  uint32_t* hi = lo + nbuckets;
+  void* temp = hi + nbuckets + 16;
+  int le = launch_histogram(t->cols[col].data, wclass_of(type), flip, n, stride, phase, nsamp, m,
+                            nbuckets, keys, sorted, temp, tb, lo, hi, rows, distinct, stream);
+  std::vector<uint32_t> hlo(nbuckets), hhi(nbuckets);
+  e = (cudaError_t)le;
+  if (e == cudaSuccess) e = cudaMemcpyAsync(out_rows, rows, nbuckets * sizeof(uint64_t), cudaMemcpyDeviceToHost, stream);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(out_distinct, distinct, nbuckets * sizeof(uint64_t), cudaMemcpyDeviceToHost, stream);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(hlo.data(), lo, nbuckets * sizeof(uint32_t), cudaMemcpyDeviceToHost, stream);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(hhi.data(), hi, nbuckets * sizeof(uint32_t), cudaMemcpyDeviceToHost, stream);
+  cudaFreeAsync(buf, stream);
+  if (e == cudaSuccess) e = sync_stream(c, stream);
+  if (e != cudaSuccess) return set_error(sync_code(e), cuda_msg("histogram", e));
+  for (uint32_t b = 0; b < nbuckets; ++b) {   // keys back to values; an empty bucket reports 0, 0
+    const uint32_t l = hlo[b] ^ flip, h = hhi[b] ^ flip;
+    out_lo[b] = out_rows[b] == 0 ? 0 : (flip ? (int64_t)(int32_t)l : (int64_t)l);
+    out_hi[b] = out_rows[b] == 0 ? 0 : (flip ? (int64_t)(int32_t)h : (int64_t)h);
+  }
+  return SEL_OK;
+}
+
 uint64_t sel_count_sampled(sel_table t, const void* prog, size_t prog_bytes, uint32_t stride,
                            uint32_t phase, uint64_t* out_sample_rows, void* cuda_stream) {
   clear_error();

@@ -23,6 +23,8 @@
 
 #include <type_traits>
 
+#include <cub/device/device_radix_sort.cuh>
+
 #include "sel_internal.h"
 
 #ifndef SEL_SB_ATOMICS
@@ -1470,7 +1472,75 @@ int occupancy_count_fast(int fast_n, bool keep, size_t dyn) {
     default: return occupancy_of(count_kernel<DevProgramSmall, true, kWarpsPerCta, 4>, dyn);
   }
 }
+// ---- equi-depth histogram over a block sample -----------
+// Keys of the sampled chunks (c = phase + s * stride) of a 1/2/4-byte integer column, in the
+// unsigned order of the values (INT32/DATE32: bits ^ 2^31), packed: sampled chunk s at s * 1024
+// (only the last sampled chunk can be partial). One warp per chunk, grid-stride.
+__global__ void __launch_bounds__(kThreads) sample_keys_kernel(const void* col, int wclass,
+                                                               uint32_t flip, uint64_t n,
+                                                               uint64_t stride, uint64_t phase,
+                                                               uint64_t nsamp, uint32_t* keys) {
+  const int lane = threadIdx.x & 31;
+  const uint64_t gw = (uint64_t)blockIdx.x * kWarpsPerCta + (threadIdx.x >> 5);
+  const uint64_t nw = (uint64_t)gridDim.x * kWarpsPerCta;
+  for (uint64_t s = gw; s < nsamp; s += nw) {
+    const uint64_t base = (phase + s * stride) * kChunkRows;
+    const uint32_t rows = (uint32_t)min((uint64_t)kChunkRows, n - base);
+    for (uint32_t i = lane; i < rows; i += 32) {
+      uint32_t v;
+      if (wclass == W4) v = __ldg(static_cast<const uint32_t*>(col) + base + i);
+      else if (wclass == W2) v = __ldg(static_cast<const uint16_t*>(col) + base + i);
+      else v = __ldg(static_cast<const uint8_t*>(col) + base + i);
+      keys[s * kChunkRows + i] = v ^ flip;
+    }
+  }
+}
+
+// Bucket b of B over the m sorted keys: positions [floor(b m / B), floor((b+1) m / B)); its
+// lowest and highest key, row count and number of distinct keys. One warp per bucket.
+__global__ void __launch_bounds__(kThreads) bucket_stats_kernel(const uint32_t* __restrict__ s,
+                                                                uint64_t m, uint32_t nb,
+                                                                uint32_t* lo, uint32_t* hi,
+                                                                uint64_t* rows, uint64_t* distinct) {
+  const int lane = threadIdx.x & 31;
+  const uint64_t b = (uint64_t)blockIdx.x * kWarpsPerCta + (threadIdx.x >> 5);
+  if (b >= nb) return;
+  const uint64_t start = b * m / nb, end = (b + 1) * m / nb;
+  uint64_t changes = 0;
+  for (uint64_t i = start + 1 + lane; i < end; i += 32) changes += s[i] != s[i - 1] ? 1u : 0u;
+  for (int o = 16; o > 0; o >>= 1) changes += __shfl_xor_sync(0xFFFFFFFFu, changes, o);
+  if (lane == 0) {
+    rows[b] = end - start;
+    distinct[b] = end > start ? changes + 1 : 0;
+    lo[b] = end > start ? s[start] : 0u;
+    hi[b] = end > start ? s[end - 1] : 0u;
+  }
+}
+
 __global__ void set_u64_kernel(uint64_t* p, uint64_t v) { *p = v; }
+int launch_histogram(const void* col, int wclass, uint32_t flip, uint64_t n, uint64_t stride,
+                     uint64_t phase, uint64_t nsamp, uint64_t m, uint32_t nb, uint32_t* keys,
+                     uint32_t* sorted, void* temp, size_t temp_bytes, uint32_t* lo, uint32_t* hi,
+                     uint64_t* rows, uint64_t* distinct, void* st) {
+  cudaStream_t stream = (cudaStream_t)st;
+  const uint64_t units = (nsamp + kWarpsPerCta - 1) / kWarpsPerCta;
+  const uint64_t grid = units < 1 ? 1 : (units > 148ull * 16 ? 148ull * 16 : units);
+  sample_keys_kernel<<<(unsigned)grid, kThreads, 0, stream>>>(col, wclass, flip, n, stride, phase,
+                                                              nsamp, keys);
+  cudaError_t e = cudaGetLastError();
+  if (e == cudaSuccess && m > 0)
+    e = cub::DeviceRadixSort::SortKeys(temp, temp_bytes, keys, sorted, (int)m, 0, 32, stream);
+  if (e == cudaSuccess)
+    bucket_stats_kernel<<<(nb + kWarpsPerCta - 1) / kWarpsPerCta, kThreads, 0, stream>>>(
+        m > 0 ? sorted : keys, m, nb, lo, hi, rows, distinct);
+  return e != cudaSuccess ? (int)e : (int)cudaGetLastError();
+}
+size_t histogram_temp_bytes(uint64_t m) {
+  size_t bytes = 0;
+  cub::DeviceRadixSort::SortKeys(nullptr, bytes, (const uint32_t*)nullptr, (uint32_t*)nullptr,
+                                 (int)m, 0, 32);
+  return bytes;
+}
 int launch_set_u64(uint64_t* p, uint64_t v, void* st) {
   set_u64_kernel<<<1, 1, 0, (cudaStream_t)st>>>(p, v);
   return (int)cudaGetLastError();

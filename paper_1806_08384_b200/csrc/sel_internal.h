@@ -208,6 +208,14 @@ struct PeerXchg {
 int launch_peer_exchange(const PeerXchg& x, const uint64_t* src, int k, uint64_t* out,
                          uint64_t* sums, void* stream);
 
+// Equi-depth histogram of a block sample (sel_histogram): sample keys -> radix sort -> bucket
+// statistics, all on `stream`; histogram_temp_bytes sizes the sort's scratch for m keys.
+int launch_histogram(const void* col, int wclass, uint32_t flip, uint64_t n, uint64_t stride,
+                     uint64_t phase, uint64_t nsamp, uint64_t m, uint32_t nb, uint32_t* keys,
+                     uint32_t* sorted, void* temp, size_t temp_bytes, uint32_t* lo, uint32_t* hi,
+                     uint64_t* rows, uint64_t* distinct, void* stream);
+size_t histogram_temp_bytes(uint64_t m);
+
 // *p = v on `stream` (one thread; sel_count_async's constant and empty cases).
 int launch_set_u64(uint64_t* p, uint64_t v, void* stream);
 

@@ -61,3 +61,45 @@ def test_sampling_misses_rare_selections(ctx):
     exact = t.count(common)
     est = t.count_sampled(common, 100, 17)[2]
     assert abs(est - exact) / exact < 0.05                             # broad patterns: fine
+
+
+def test_equi_depth_histogram_parity(ctx):
+    """sel_histogram vs oracle/synopsis.equi_depth over the same block sample:
+    bucket bounds, rows and distinct counts bit-exact, for every integer column type, ragged
+    sizes, several bucket counts, strides and phases; and the equality estimate beside the exact
+    count."""
+    import paper_1806_08384_b200 as sel
+    from oracle import synopsis
+    from helpers import random_table
+    from selgen.program import INT32, DATE32, DICT8, DICT16, DICT32, INT64, FLOAT32, Cmp, encode
+    from test_gpu_parity import register
+    rng = np.random.default_rng(12)
+    types = [INT32, DATE32, DICT8, DICT16, DICT32, INT64, FLOAT32]
+    for n in (1, 1000, 5001, 70_001):
+        cols, _ = random_table(rng, types, n)
+        cols[0] = rng.integers(-3000, 3000, n).astype(np.int32)     # many duplicates per bucket
+        t = register(ctx, cols, types)
+        for j in range(5):
+            for B, stride, phase in ((1, 1, 0), (7, 1, 0), (64, 3, 1), (16, 2, 1)):
+                if phase >= (n + 1023) // 1024:
+                    continue
+                h = t.histogram(j, buckets=B, stride=stride, phase=phase)
+                want = synopsis.equi_depth(synopsis.block_sample(cols[j], stride, phase), B)
+                assert h["sample_rows"] == want["sample_rows"]
+                for k in ("lo", "hi", "rows", "distinct"):
+                    np.testing.assert_array_equal(h[k], want[k], err_msg=f"n={n} col={j} {k}")
+        for j in (5, 6):
+            with pytest.raises(sel.SelError):
+                t.histogram(j)
+        t.release()
+    # the estimate vs the exact probe on a skewed column (the baseline the paper argues against)
+    v = np.concatenate([np.full(90_000, 7, np.int32), rng.integers(0, 1000, 10_000).astype(np.int32)])
+    rng.shuffle(v)
+    t = register(ctx, [v], [INT32])
+    h = t.histogram(0, buckets=16)
+    for x in (7, 500):
+        est = sel.equi_depth_estimate(h, x)
+        assert est == pytest.approx(synopsis.estimate_eq(synopsis.equi_depth(v, 16), x, len(v)))
+        exact = t.count(encode(Cmp("=", 0, x), [INT32]))
+        print(f"x={x}: equi-depth estimate {est:.1f}, exact {exact}")
+    t.release()

@@ -474,3 +474,49 @@ def test_count_mt_matches_count():
     with pytest.raises(oracle.OracleError) as e:
         oracle.count_mt(cols, types, encode(InSet(0, 9), types), 4, bitmaps=bms)
     assert e.value.status == 1
+
+
+# ---- oracle/synopsis.py: the equi-depth histogram baseline ----------------
+
+def test_equi_depth_paper_example_49_3():
+    """"if we try to estimate the selectivity where the attribute involved equals
+    to 16, 30/2 + 30/1 + 30/7 = 49.3": three buckets of depth D = 30 hold 16, with 2, 1 and 7
+    distinct values (DESIGN.md §2 reading: the per-bucket estimates D / V(b) add up)."""
+    from oracle import synopsis
+    values = np.array([10] * 15 + [16] * (15 + 30 + 24) + list(range(17, 23)), np.int32)
+    h = synopsis.equi_depth(values, 3)
+    assert h["rows"].tolist() == [30, 30, 30]
+    assert h["distinct"].tolist() == [2, 1, 7]
+    est = synopsis.estimate_eq(h, 16, len(values))
+    assert round(est, 1) == 49.3 and abs(est - (30 / 2 + 30 / 1 + 30 / 7)) < 1e-12
+    assert synopsis.estimate_eq(h, 11, len(values)) == 15.0       # inside bucket 0 only: D / 2
+    assert synopsis.estimate_eq(h, 99, len(values)) == 0.0        # outside every bucket
+
+
+def test_equi_depth_brute_force_small():
+    from oracle import synopsis
+    rng = np.random.default_rng(3)
+    for _ in range(300):
+        m = int(rng.integers(0, 60))
+        B = int(rng.integers(1, 9))
+        v = rng.integers(-5, 6, m).astype(np.int32)
+        h = synopsis.equi_depth(v, B)
+        s = sorted(v.tolist())
+        assert int(h["rows"].sum()) == m
+        for b in range(B):
+            part = s[b * m // B:(b + 1) * m // B]
+            assert int(h["rows"][b]) == len(part) in (m // B, -(-m // B))
+            assert int(h["distinct"][b]) == len(set(part))
+            if part:
+                assert (h["lo"][b], h["hi"][b]) == (min(part), max(part))
+        # uniform data with one value per bucket: the estimate is exact
+    u = np.repeat(np.arange(8, dtype=np.int32), 5)
+    h = synopsis.equi_depth(u, 8)
+    assert all(synopsis.estimate_eq(h, x, 40) == 5.0 for x in range(8))
+
+
+def test_block_sample_rows():
+    from oracle import synopsis
+    v = np.arange(5000)
+    s = synopsis.block_sample(v, 3, 1)
+    assert s.tolist() == list(range(1024, 2048)) + list(range(4096, 5000))
