@@ -1773,6 +1773,18 @@ sel_status sel_count_batch(sel_table t, const void* const* progs, const size_t* 
   }
   bp.n_ops = nop;
   bp.n_progs = nprog;
+  bp.all_conj = 1;
+  bp.prog_live = 0;
+  for (uint32_t k = 0; k < nprog; ++k) {
+    const Plan& P = plans[k];
+    bp.conj_set[k] = 0;
+    if (host_zero[k]) continue;
+    bp.prog_live |= 1u << k;
+    if (P.path == PATH_CONST) continue;               // TRUE: every row
+    if (P.path != PATH_CONJ) { bp.all_conj = 0; continue; }
+    for (size_t i = 0; i < P.op.size(); ++i)
+      if (P.op[i] == DOP_LEAF) bp.conj_set[k] |= 1u << leaf_id[prog_leaf[k][P.arg[i]]];
+  }
   cudaStream_t stream = (cudaStream_t)cuda_stream;
   DeviceGuard g(c->device);
   if (!g.ok) return set_error(SEL_E_CUDA, "cudaSetDevice failed");

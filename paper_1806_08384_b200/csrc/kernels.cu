@@ -1279,11 +1279,44 @@ __device__ __forceinline__ void batch_column(const BatchProgram& p, const BatchC
 
 template <bool TAIL>
 __device__ __forceinline__ void batch_chunk(const BatchProgram& p, uint64_t base, int lane,
-                                            uint32_t nvalid, uint32_t* lm, uint32_t* cnt /* [k] */) {
+                                            uint32_t nvalid, uint32_t* lm, uint32_t* cnt /* [k] */,
+                                            uint32_t (&acc)[8]) {
 #pragma unroll 1
   for (uint32_t c = 0; c < p.n_cols; ++c) batch_column<TAIL>(p, p.col[c], base, lane, nvalid, lm);
   __syncwarp();
   const uint32_t valid = TAIL ? valid_mask(lane, nvalid) : 0xFFFFFFFFu;
+  if (p.all_conj && p.n_progs <= 8) {   // and up to 8 programs: per-lane counts in registers
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      if (k < (int)p.n_progs && ((p.prog_live >> k) & 1u)) {
+        uint32_t m = valid, bits = p.conj_set[k];
+        while (bits) {
+          const int l = __ffs(bits) - 1;
+          bits &= bits - 1;
+          m &= lm[l * 32 + lane];
+        }
+        acc[k] += (uint32_t)__popc(m);
+      }
+    }
+    __syncwarp();
+    return;
+  }
+  if (p.all_conj) {   // conjunctions: AND each program's leaf masks, no postfix stack
+#pragma unroll 1
+    for (uint32_t k = 0; k < p.n_progs; ++k) {
+      if (!((p.prog_live >> k) & 1u)) continue;
+      uint32_t m = valid, bits = p.conj_set[k];
+      while (bits) {
+        const int l = __ffs(bits) - 1;
+        bits &= bits - 1;
+        m &= lm[l * 32 + lane];
+      }
+      const uint32_t c = __reduce_add_sync(0xFFFFFFFFu, (uint32_t)__popc(m));
+      if (lane == 0) cnt[k] += c;
+    }
+    __syncwarp();
+    return;
+  }
   uint32_t st[kMaxDeviceStack];
   int sp = 0;
 #pragma unroll 1
@@ -1315,10 +1348,16 @@ __global__ void __launch_bounds__(kThreads) count_batch_kernel(const __grid_cons
   const uint32_t rem = (uint32_t)(n % kChunkRows);
   const uint64_t gw = (uint64_t)blockIdx.x * kWarpsPerCta + warp;
   const uint64_t nw = (uint64_t)gridDim.x * kWarpsPerCta;
+  uint32_t acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   for (uint64_t c = gw; c < nfull; c += nw)
-    batch_chunk<false>(p, c * kChunkRows, lane, kChunkRows, s_lm[warp], s_cnt[warp]);
+    batch_chunk<false>(p, c * kChunkRows, lane, kChunkRows, s_lm[warp], s_cnt[warp], acc);
   if (rem != 0 && gw == nfull % nw)
-    batch_chunk<true>(p, nfull * kChunkRows, lane, rem, s_lm[warp], s_cnt[warp]);
+    batch_chunk<true>(p, nfull * kChunkRows, lane, rem, s_lm[warp], s_cnt[warp], acc);
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {   // register counts of the <= 8-program conjunctive path
+    const uint32_t c = __reduce_add_sync(0xFFFFFFFFu, acc[k]);
+    if (lane == 0 && c) s_cnt[warp][k] += c;
+  }
   __syncthreads();
   for (uint32_t k = threadIdx.x; k < p.n_progs; k += kThreads) {
     uint64_t s = 0;

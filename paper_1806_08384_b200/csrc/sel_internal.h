@@ -126,6 +126,11 @@ struct BatchColumn {
 };
 struct BatchProgram {
   uint32_t n_cols, n_leaves, n_ops, n_progs;
+  // every program a conjunction of leaves (or TRUE/FALSE): program k counts the rows in all
+  // leaves of conj_set[k] (bit l = leaf l; 0 = TRUE) when bit k of prog_live is set — no postfix
+  // walk, no stack
+  uint32_t all_conj, prog_live;
+  uint32_t conj_set[kBatchMaxProgs];
   BatchColumn col[kBatchMaxCols];
   uint16_t leaf_iv_begin[kBatchMaxLeaves];
   uint16_t leaf_iv_count[kBatchMaxLeaves];
