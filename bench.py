@@ -672,6 +672,10 @@ def run_ours(args):
                  "sector_bytes_per_launch": int(pb_sector),
                  "achieved_sector": round(push_sector_gbs, 2),
                  "frac_sector": round(push_sector_gbs / hbm, 4)}
+    for r in (roof_count, roof_push):
+        r["ms_source"] = ("mean of the library's CUDA events around the kernel on its stream, over "
+                          "a second pass of the same steps right after the timed region (events "
+                          "inside the timed graph would add ~20 us per step)")
     for r in (roof_count, roof_push):   # the same achieved rate against SURVEY §8(d)'s other peaks
         r["frac_nominal_8tbs"] = round(r["achieved"] / 8000.0, 4)
         if read_peak:
