@@ -101,3 +101,78 @@ def test_shard_range_partitions():
             assert r[0][0] == 0 and r[-1][1] == n
             assert all(r[k][1] == r[k + 1][0] for k in range(world - 1))
             assert max(e - s for s, e in r) - min(e - s for s, e in r) <= 1
+
+
+# ---- bench.py's choice of exchange at N > 1 (setup_exchange): every rank must agree ----------
+
+def _exchange_worker(rank, world, port, scenario, q):
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    sys.path.insert(0, root)
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import bench
+        log = []
+
+        class Ctx:
+            def peer_handle(self):
+                if scenario == "handle" and rank == 1:
+                    raise RuntimeError("no IPC")
+                return bytes([rank]) * 64
+
+            def set_peers(self, n, r, handles):
+                assert len(handles) == n == world and r == rank
+                if scenario == "map" and rank == 0:
+                    raise RuntimeError("cudaIpcOpenMemHandle failed")
+                log.append("mapped")
+
+            def drop_peers(self):
+                log.append("dropped")
+
+        class Probe:
+            def __init__(self, *a, **k):
+                pass
+
+            def count(self, prog):
+                return world - 1 if (scenario == "verify" and rank == 1) else world
+
+            def release(self):
+                pass
+
+        class Sel:
+            Table = Probe
+
+        class SDist:
+            @staticmethod
+            def setup_comm(ctx):
+                log.append("nccl")
+
+        got = bench.setup_exchange(Ctx(), Sel, SDist, dist, "cpu")
+        q.put((rank, got.split(" ")[0], log))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("scenario,want", [("ok", "peers"), ("handle", "nccl"),
+                                           ("map", "nccl"), ("verify", "nccl")])
+def test_setup_exchange_agreement(scenario, want):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_exchange_worker, args=(r, 2, port, scenario, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = sorted(q.get(timeout=120) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert [r[1] for r in res] == [want, want], res
+    for rank, _, log in res:
+        if want == "nccl":
+            assert log[-1] == "nccl"
+            if "mapped" in log:                     # a rank that mapped the others unmaps them
+                assert "dropped" in log
+        else:
+            assert log == ["mapped"]
