@@ -1086,6 +1086,7 @@ sel_status enqueue_count(sel_table t, const Plan& plan, uint32_t flags, const ui
     const size_t dyn = keep ? (size_t)keep->warp_smem * kWarpsPerCta : 0;
     Scratch s = c->s;
     s.result = d_out;
+    s.xg = (c->peers && allreduce) ? c->xg : PeerXchg{};   // the exchange fused into the count
     if (c->timing) record(c, c->ev0, stream);
     int le;
     if (fits_block<DevProgramSmall>(plan, nslots, 0)) {
@@ -1137,10 +1138,10 @@ sel_status enqueue_count(sel_table t, const Plan& plan, uint32_t flags, const ui
     e = cudaMemcpyAsync(d_out, h, sizeof(uint64_t), cudaMemcpyHostToDevice, stream);
     if (e != cudaSuccess) return set_error(SEL_E_CUDA, cuda_msg("cudaMemcpyAsync", e));
   }
-  if (c->peers && allreduce) {  // SURVEY §8a a4 over peer memory: the sum of the exchanged counts
+  if (c->peers && allreduce && !scan) {  // SURVEY §8a a4 over peer memory (a scan fuses it, above)
     const int le = launch_peer_exchange(c->xg, d_out, 1, nullptr, d_out, stream);
     if (le != cudaSuccess) return set_error(SEL_E_CUDA, cuda_msg("peer exchange", (cudaError_t)le));
-  } else if (c->comm && allreduce) {  // one 8-byte all-reduce on the probe stream
+  } else if (c->comm && allreduce && !c->peers) {  // one 8-byte all-reduce on the probe stream
     ncclResult_t r = nccl().AllReduce(d_out, d_out, 1, ncclUint64, ncclSum, c->comm, stream);
     if (r != ncclSuccess) return set_error(SEL_E_NCCL, nccl_msg("ncclAllReduce", r));
   }

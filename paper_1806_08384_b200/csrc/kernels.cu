@@ -69,6 +69,70 @@ __device__ __forceinline__ void prefetch_l2(const void* p, uint32_t bytes) {
   asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
 }
 
+// ---- peer exchange (sel_internal.h PeerXchg) -------------------------------------------------
+__device__ __forceinline__ void st_release_sys(uint64_t* p, uint64_t v) {
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ uint64_t ld_acquire_sys(const uint64_t* p) {
+  uint64_t v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ uint64_t globaltimer_ns() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+
+// Run by all threads of ONE CTA (blockDim.x >= 32); see PeerXchg.
+__device__ void peer_gather_block(const PeerXchg& x, const uint64_t* src, int k, uint64_t* out,
+                                  uint64_t* sums) {
+  __shared__ uint32_t s_e;
+  __shared__ uint64_t s_v[kMaxXchgVals];
+  __shared__ uint64_t s_got[kMaxPeers * kMaxXchgVals];
+  const int t = threadIdx.x;
+  if (t == 0) {
+    s_e = *x.epoch + 1u;
+    *x.epoch = s_e;
+  }
+  if (t < k) s_v[t] = src[t];
+  __syncthreads();
+  const uint64_t e = s_e;
+  const uint32_t half = (s_e & 1u) * kMaxPeers * kMaxXchgVals;
+  // write my k values into row `rank` of every rank's buffer
+  for (int i = t; i < x.n * k; i += blockDim.x) {
+    const int r = i / k, j = i - r * k;
+    st_release_sys(x.peers[r] + half + x.rank * kMaxXchgVals + j, (e << 32) | (s_v[j] & 0xFFFFFFFFull));
+  }
+  // wait for every rank's row in my buffer
+  for (int i = t; i < x.n * k; i += blockDim.x) {
+    const int r = i / k, j = i - r * k;
+    const uint64_t* slot = x.mine + half + r * kMaxXchgVals + j;
+    uint64_t w = ld_acquire_sys(slot);
+    if ((w >> 32) != e) {
+      const uint64_t t0 = globaltimer_ns();
+      while (((w = ld_acquire_sys(slot)) >> 32) != e) {
+        if (globaltimer_ns() - t0 > 10000000000ull) {  // ~10 s: a rank is missing
+          atomicExch(x.err, 1u);
+          w = 0;
+          break;
+        }
+        __nanosleep(64);
+      }
+    }
+    s_got[i] = w & 0xFFFFFFFFull;
+  }
+  __syncthreads();
+  if (out)
+    for (int i = t; i < x.n * k; i += blockDim.x) out[i] = s_got[i];
+  if (sums && t < k) {
+    uint64_t acc = 0;
+    for (int r = 0; r < x.n; ++r) acc += s_got[r * k + t];
+    sums[t] = acc;
+  }
+  __syncthreads();
+}
+
 // Prefetch every predicate column of chunk `c` into L2 (issued by one lane a chunk ahead).
 template <class P>
 __device__ __forceinline__ void prefetch_chunk(const P& p, uint64_t c) {
@@ -771,7 +835,7 @@ __global__ void __launch_bounds__(NW * 32, NW == kWarpsPerCta ? (FASTN ? SEL_FAS
                                                          uint64_t* __restrict__ partials,
                                                          unsigned int* __restrict__ done,
                                                          uint64_t* __restrict__ out,
-                                                         SelectionBufs sb) {
+                                                         SelectionBufs sb, const PeerXchg xg) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const uint64_t nfull = n / kChunkRows;
   const uint32_t rem = (uint32_t)(n % kChunkRows);
@@ -863,6 +927,12 @@ __global__ void __launch_bounds__(NW * 32, NW == kWarpsPerCta ? (FASTN ? SEL_FAS
       for (int w = 0; w < NW; ++w) t += s_sum[w];
       *out = t;
       *done = 0u;
+    }
+    // sel_count with peers: the count's collective fused into the same kernel — the last CTA
+    // exchanges the local count over peer memory and leaves the global sum in *out
+    if (xg.n > 0) {
+      __syncthreads();
+      peer_gather_block(xg, out, 1, nullptr, out);
     }
   }
 }
@@ -959,70 +1029,6 @@ __global__ void __launch_bounds__(kThreads) superblock_sum_kernel(const uint16_t
 #endif
 
 // Exclusive prefix of the per-64-chunk sums kept by the count kernel (one CTA; <= 65536 sums).
-// ---- peer exchange (sel_internal.h PeerXchg) -------------------------------------------------
-__device__ __forceinline__ void st_release_sys(uint64_t* p, uint64_t v) {
-  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
-}
-__device__ __forceinline__ uint64_t ld_acquire_sys(const uint64_t* p) {
-  uint64_t v;
-  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-  return v;
-}
-__device__ __forceinline__ uint64_t globaltimer_ns() {
-  uint64_t t;
-  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
-  return t;
-}
-
-// Run by all threads of ONE CTA (blockDim.x >= 32); see PeerXchg.
-__device__ void peer_gather_block(const PeerXchg& x, const uint64_t* src, int k, uint64_t* out,
-                                  uint64_t* sums) {
-  __shared__ uint32_t s_e;
-  __shared__ uint64_t s_v[kMaxXchgVals];
-  __shared__ uint64_t s_got[kMaxPeers * kMaxXchgVals];
-  const int t = threadIdx.x;
-  if (t == 0) {
-    s_e = *x.epoch + 1u;
-    *x.epoch = s_e;
-  }
-  if (t < k) s_v[t] = src[t];
-  __syncthreads();
-  const uint64_t e = s_e;
-  const uint32_t half = (s_e & 1u) * kMaxPeers * kMaxXchgVals;
-  // write my k values into row `rank` of every rank's buffer
-  for (int i = t; i < x.n * k; i += blockDim.x) {
-    const int r = i / k, j = i - r * k;
-    st_release_sys(x.peers[r] + half + x.rank * kMaxXchgVals + j, (e << 32) | (s_v[j] & 0xFFFFFFFFull));
-  }
-  // wait for every rank's row in my buffer
-  for (int i = t; i < x.n * k; i += blockDim.x) {
-    const int r = i / k, j = i - r * k;
-    const uint64_t* slot = x.mine + half + r * kMaxXchgVals + j;
-    uint64_t w = ld_acquire_sys(slot);
-    if ((w >> 32) != e) {
-      const uint64_t t0 = globaltimer_ns();
-      while (((w = ld_acquire_sys(slot)) >> 32) != e) {
-        if (globaltimer_ns() - t0 > 10000000000ull) {  // ~10 s: a rank is missing
-          atomicExch(x.err, 1u);
-          w = 0;
-          break;
-        }
-        __nanosleep(64);
-      }
-    }
-    s_got[i] = w & 0xFFFFFFFFull;
-  }
-  __syncthreads();
-  if (out)
-    for (int i = t; i < x.n * k; i += blockDim.x) out[i] = s_got[i];
-  if (sums && t < k) {
-    uint64_t acc = 0;
-    for (int r = 0; r < x.n; ++r) acc += s_got[r * k + t];
-    sums[t] = acc;
-  }
-  __syncthreads();
-}
-
 __global__ void __launch_bounds__(256) peer_exchange_kernel(const PeerXchg x, const uint64_t* src,
                                                             int k, uint64_t* out, uint64_t* sums) {
   peer_gather_block(x, src, k, out, sums);
@@ -1380,9 +1386,9 @@ template <int FASTN>
 void launch_count_fast(const DevProgramSmall& p, uint64_t n, int grid, const Scratch& s,
                        const SelectionBufs* keep, cudaStream_t stream) {
   if (keep)
-    count_kernel<DevProgramSmall, true, kWarpsPerCta, FASTN><<<grid, kThreads, (size_t)keep->warp_smem * kWarpsPerCta, stream>>>(p, n, s.partials, s.done, s.result, *keep);
+    count_kernel<DevProgramSmall, true, kWarpsPerCta, FASTN><<<grid, kThreads, (size_t)keep->warp_smem * kWarpsPerCta, stream>>>(p, n, s.partials, s.done, s.result, *keep, s.xg);
   else
-    count_kernel<DevProgramSmall, false, kWarpsPerCta, FASTN><<<grid, kThreads, 0, stream>>>(p, n, s.partials, s.done, s.result, SelectionBufs{});
+    count_kernel<DevProgramSmall, false, kWarpsPerCta, FASTN><<<grid, kThreads, 0, stream>>>(p, n, s.partials, s.done, s.result, SelectionBufs{}, s.xg);
 }
 
 template <class P>
@@ -1402,14 +1408,14 @@ int launch_count_t(const P& p, uint64_t n, int grid, const Scratch& s, const Sel
   }
   if (nw == 32) {
     if (keep)
-      count_kernel<P, true, 32><<<grid, 32 * 32, (size_t)keep->warp_smem * 32 + p.bm_smem, stream>>>(p, n, s.partials, s.done, s.result, *keep);
+      count_kernel<P, true, 32><<<grid, 32 * 32, (size_t)keep->warp_smem * 32 + p.bm_smem, stream>>>(p, n, s.partials, s.done, s.result, *keep, s.xg);
     else
-      count_kernel<P, false, 32><<<grid, 32 * 32, p.bm_smem, stream>>>(p, n, s.partials, s.done, s.result, SelectionBufs{});
+      count_kernel<P, false, 32><<<grid, 32 * 32, p.bm_smem, stream>>>(p, n, s.partials, s.done, s.result, SelectionBufs{}, s.xg);
   } else {
     if (keep)
-      count_kernel<P, true, kWarpsPerCta><<<grid, kThreads, (size_t)keep->warp_smem * kWarpsPerCta + p.bm_smem, stream>>>(p, n, s.partials, s.done, s.result, *keep);
+      count_kernel<P, true, kWarpsPerCta><<<grid, kThreads, (size_t)keep->warp_smem * kWarpsPerCta + p.bm_smem, stream>>>(p, n, s.partials, s.done, s.result, *keep, s.xg);
     else
-      count_kernel<P, false, kWarpsPerCta><<<grid, kThreads, p.bm_smem, stream>>>(p, n, s.partials, s.done, s.result, SelectionBufs{});
+      count_kernel<P, false, kWarpsPerCta><<<grid, kThreads, p.bm_smem, stream>>>(p, n, s.partials, s.done, s.result, SelectionBufs{}, s.xg);
   }
   return (int)cudaGetLastError();
 }

@@ -179,16 +179,6 @@ constexpr int kGateSlot = 1 + kMaxRanks;
 constexpr int kResultSlots = 2 + kMaxRanks;
 constexpr int kMirrorMax = 512;  // read-back mirror below kGateSlot (superblock_prefix_kernel)
 
-// Device-side scratch owned by a context.
-struct Scratch {
-  uint64_t* partials;      // per-CTA partial counts (count kernel)
-  unsigned int* done;      // CTA completion counter, self-resetting
-  uint64_t* result;        // [0] = count of the last probe, [1..] = gathered per-rank counts
-  unsigned long long* ticket;  // monotone tile ticket counter (push-down)
-  uint64_t* status;        // push-down tile status words (epoch | flag | value)
-  uint64_t status_cap;     // entries in status
-};
-
 // The library's own exchange over peer memory (sel_ctx_set_peers; SURVEY §8e "a one-shot peer
 // write of each rank's count into a symmetric buffer over NVLink plus a flag"). Every rank owns a
 // symmetric buffer `mine` of 2 x kMaxPeers x kMaxXchgVals u64 (two halves by exchange parity)
@@ -208,6 +198,19 @@ struct PeerXchg {
   uint32_t* err;           // host-mapped flag: nonzero after a timed-out wait
   int n, rank;
 };
+
+// Device-side scratch owned by a context.
+struct Scratch {
+  uint64_t* partials;      // per-CTA partial counts (count kernel)
+  unsigned int* done;      // CTA completion counter, self-resetting
+  uint64_t* result;        // [0] = count of the last probe, [1..] = gathered per-rank counts
+  unsigned long long* ticket;  // monotone tile ticket counter (push-down)
+  uint64_t* status;        // push-down tile status words (epoch | flag | value)
+  uint64_t status_cap;     // entries in status
+  PeerXchg xg;             // count kernel: n > 0 = its last CTA exchanges the count over peer
+                           // memory and leaves the global sum in *result (sel_count with peers)
+};
+
 // Gather k (<= kMaxXchgVals) values src[0..k) of every rank: out[r * k + j] = rank r's src[j]
 // (out may be null); sums[j] = sum over ranks (sums may be null). One CTA, on `stream`.
 int launch_peer_exchange(const PeerXchg& x, const uint64_t* src, int k, uint64_t* out,
