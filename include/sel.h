@@ -118,6 +118,16 @@ sel_status sel_ctx_set_comm(sel_ctx ctx, int nranks, int rank, const void* nccl_
 sel_status sel_ctx_peer_handle(sel_ctx ctx, void* out64);
 sel_status sel_ctx_set_peers(sel_ctx ctx, int nranks, int rank, const void* handles);
 
+/* Gather to one rank over peer memory ("an optional gather-to-one-rank uses P2P
+ * writes at the offset"). sel_ctx_export_buffer: a 72-byte handle (CUDA IPC handle of the
+ * allocation holding dev_ptr + the 8-byte offset of dev_ptr in it) to hand to other ranks.
+ * sel_ctx_import_buffer: maps such a handle (once per allocation; unmapped by
+ * sel_ctx_set_peers(ctx, 0, ...) or sel_ctx_destroy) and returns the device pointer, usable by
+ * this context's kernels (NVLink/NVSwitch for another GPU's memory). Errors: SEL_E_ARG,
+ * SEL_E_CUDA. The exporter must not free the buffer while it is mapped elsewhere. */
+sel_status sel_ctx_export_buffer(sel_ctx ctx, const void* dev_ptr, void* out_handle72);
+sel_status sel_ctx_import_buffer(sel_ctx ctx, const void* handle72, void** out_dev_ptr);
+
 /* Writes a fresh 128-byte ncclUniqueId into `out128` (call on rank 0 only). SEL_E_NCCL on
  * failure. */
 sel_status sel_nccl_unique_id(void* out128);
@@ -202,6 +212,19 @@ uint64_t sel_execute(sel_table table, const void* prog, size_t prog_bytes,
                      uint32_t* out_rowids, void* const* out_cols, uint64_t capacity_rows,
                      uint64_t* out_local_count, uint64_t* out_global_offset,
                      int* out_materialized, void* cuda_stream);
+
+/* sel_execute_to: sel_execute whose outputs are the GLOBAL result — typically one rank's buffers
+ * mapped by every rank (sel_ctx_import_buffer): each rank writes its selected rows at its offset
+ * (the exclusive prefix of the per-rank counts, computed on the device from the Execute's one
+ * exchange), so the rank-ordered, ascending result assembles in place through P2P stores of the
+ * materialisation kernel itself — no gather step. capacity_rows is the GLOBAL capacity of the
+ * buffers (rows past it are not written). Other arguments, outputs and errors as sel_execute;
+ * every rank must call it. */
+uint64_t sel_execute_to(sel_table table, const void* prog, size_t prog_bytes,
+                        const uint32_t* proj_cols, uint32_t nproj, uint64_t max_size,
+                        uint32_t* out_rowids, void* const* out_cols, uint64_t capacity_rows,
+                        uint64_t* out_local_count, uint64_t* out_global_offset,
+                        int* out_materialized, void* cuda_stream);
 
 /* Prepared executes: the same Execute with every argument fixed, validated and canonicalised
  * once and — for a program that scans a non-empty shard — its device work (count keeping the

@@ -20,7 +20,8 @@ STATUS_NAMES = {0: "SEL_OK", 1: "SEL_E_ARG", 2: "SEL_E_ALIGN", 3: "SEL_E_TYPE",
 
 # Every symbol include/sel.h declares (tests check the library exports exactly these).
 EXPORTS = ["sel_ctx_create", "sel_ctx_set_comm", "sel_nccl_unique_id", "sel_ctx_destroy",
-           "sel_ctx_peer_handle", "sel_ctx_set_peers",
+           "sel_ctx_peer_handle", "sel_ctx_set_peers", "sel_ctx_export_buffer",
+           "sel_ctx_import_buffer", "sel_execute_to",
            "sel_ctx_set_timing", "sel_ctx_last_kernel_ms", "sel_table_register",
            "sel_table_release", "sel_count", "sel_count_async", "sel_count_ex", "sel_execute", "sel_pushdown",
            "sel_ctx_last_times", "sel_count_batch", "sel_count_sampled", "sel_histogram",
@@ -59,6 +60,8 @@ def lib() -> ctypes.CDLL:
         "sel_ctx_set_comm": (i32, [vp, i32, i32, vp]),
         "sel_ctx_peer_handle": (i32, [vp, vp]),
         "sel_ctx_set_peers": (i32, [vp, i32, i32, vp]),
+        "sel_ctx_export_buffer": (i32, [vp, vp, vp]),
+        "sel_ctx_import_buffer": (i32, [vp, vp, ctypes.POINTER(ctypes.c_void_p)]),
         "sel_nccl_unique_id": (i32, [vp]),
         "sel_ctx_destroy": (None, [vp]),
         "sel_ctx_set_timing": (i32, [vp, i32]),
@@ -72,6 +75,8 @@ def lib() -> ctypes.CDLL:
         "sel_histogram": (i32, [vp, u32, u32, u32, u32, vp, vp, vp, vp, vp, vp]),
         "sel_execute": (u64, [vp, ctypes.c_char_p, sz, vp, u32, u64, vp, vp, u64,
                               ctypes.POINTER(u64), ctypes.POINTER(u64), ctypes.POINTER(i32), vp]),
+        "sel_execute_to": (u64, [vp, ctypes.c_char_p, sz, vp, u32, u64, vp, vp, u64,
+                                 ctypes.POINTER(u64), ctypes.POINTER(u64), ctypes.POINTER(i32), vp]),
         "sel_count_sampled": (u64, [vp, ctypes.c_char_p, sz, u32, u32, ctypes.POINTER(u64), vp]),
         "sel_count_batch": (i32, [vp, vp, vp, u32, ctypes.POINTER(u64), vp]),
         "sel_bitmap_register": (i32, [vp, vp, u64, ctypes.POINTER(u32)]),

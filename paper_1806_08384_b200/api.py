@@ -75,6 +75,19 @@ class Context:
         """Unmap the other ranks' exchange buffers (every rank before any rank closes)."""
         check(lib().sel_ctx_set_peers(self._h, 0, 0, None))
 
+    def export_buffer(self, tensor: torch.Tensor) -> bytes:
+        """72-byte handle of a device tensor's memory for other ranks (include/sel.h)."""
+        buf = ctypes.create_string_buffer(72)
+        check(lib().sel_ctx_export_buffer(self._h, ctypes.c_void_p(tensor.data_ptr()), buf))
+        return buf.raw
+
+    def import_buffer(self, handle: bytes) -> int:
+        """Map another rank's exported buffer; returns the device pointer (an int)."""
+        out = ctypes.c_void_p(0)
+        buf = ctypes.create_string_buffer(bytes(handle), 72)
+        check(lib().sel_ctx_import_buffer(self._h, buf, ctypes.byref(out)))
+        return int(out.value)
+
     def enable_timing(self, on: bool = True) -> None:
         check(lib().sel_ctx_set_timing(self._h, 1 if on else 0))
 
@@ -371,6 +384,26 @@ class Table:
         k = min(int(local.value), capacity)
         cols = {self.names[j] if isinstance(p, str) else j: o[:k] for p, j, o in zip(project, proj, outs)}
         return ExecuteResult(rowids[:k], cols, int(r), int(local.value), int(off.value), bool(mat.value))
+
+    def execute_to(self, pred, project: Sequence[str | int], max_size: int, capacity: int,
+                   rowids_ptr: int, col_ptrs: Sequence[int], stream=None) -> tuple:
+        """Execute writing into the GLOBAL result at this rank's offset (include/sel.h
+        sel_execute_to): rowids_ptr / col_ptrs are device pointers of the global output buffers
+        as this context sees them (sel_ctx_import_buffer for another rank's memory); capacity is
+        their global row capacity. Returns (global count, local count, offset, materialized).
+        dist.gather_execute wraps the whole gather-to-one-rank."""
+        prog = self.program(pred)
+        proj = self._col_indices(project)
+        ptrs = (ctypes.c_void_p * max(len(proj), 1))(*[int(x) for x in col_ptrs])
+        pj = (ctypes.c_uint32 * max(len(proj), 1))(*proj)
+        local, off, mat = ctypes.c_uint64(0), ctypes.c_uint64(0), ctypes.c_int(0)
+        r = lib().sel_execute_to(self._h, prog, len(prog), pj, len(proj), int(max_size),
+                                 int(rowids_ptr), ptrs, int(capacity), ctypes.byref(local),
+                                 ctypes.byref(off), ctypes.byref(mat),
+                                 _stream_ptr(stream, self.ctx.device))
+        if r == SEL_ERR:
+            raise last_error()
+        return int(r), int(local.value), int(off.value), bool(mat.value)
 
     def prepare_execute(self, pred, project: Sequence[str | int] = (), max_size: int | None = None,
                         capacity: int | None = None, stream=None, out=None) -> "PreparedExecute":

@@ -179,6 +179,7 @@ struct sel_ctx_s {
   std::vector<void*> peer_opened;     // IPC mappings to close
   uint32_t* peer_epoch = nullptr;     // device exchange counter
   uint32_t* h_peer_err = nullptr;     // host-mapped timeout flag
+  std::map<std::string, void*> imported;  // sel_ctx_import_buffer: IPC handle -> mapped base
   PeerXchg xg{};
 };
 
@@ -634,12 +635,69 @@ sel_status sel_ctx_peer_handle(sel_ctx ctx, void* out64) {
   return SEL_OK;
 }
 
+// The base of the allocation holding `p` (driver API, through the runtime's loaded libcuda).
+static cudaError_t allocation_base(const void* p, uintptr_t* base) {
+  typedef int (*range_fn)(unsigned long long*, size_t*, unsigned long long);
+  static range_fn fn = [] {
+    void* h = dlopen("libcuda.so.1", RTLD_NOW | RTLD_NOLOAD);
+    if (!h) h = dlopen("libcuda.so.1", RTLD_NOW);
+    return h ? (range_fn)dlsym(h, "cuMemGetAddressRange_v2") : (range_fn) nullptr;
+  }();
+  if (!fn) return cudaErrorNotSupported;
+  unsigned long long b = 0;
+  size_t size = 0;
+  if (fn(&b, &size, (unsigned long long)(uintptr_t)p) != 0) return cudaErrorInvalidValue;
+  *base = (uintptr_t)b;
+  return cudaSuccess;
+}
+
+sel_status sel_ctx_export_buffer(sel_ctx ctx, const void* dev_ptr, void* out72) {
+  clear_error();
+  if (!ctx || !dev_ptr || !out72) return set_error(SEL_E_ARG, "null argument");
+  DeviceGuard g(ctx->device);
+  if (!g.ok) return set_error(SEL_E_CUDA, "cudaSetDevice failed");
+  uintptr_t base = 0;
+  cudaError_t e = allocation_base(dev_ptr, &base);
+  cudaIpcMemHandle_t h;
+  if (e == cudaSuccess) e = cudaIpcGetMemHandle(&h, reinterpret_cast<void*>(base));
+  if (e != cudaSuccess) return set_error(SEL_E_CUDA, cuda_msg("exporting the buffer", e));
+  const uint64_t off = (uint64_t)((uintptr_t)dev_ptr - base);
+  std::memcpy(out72, &h, 64);
+  std::memcpy(static_cast<char*>(out72) + 64, &off, 8);
+  return SEL_OK;
+}
+
+sel_status sel_ctx_import_buffer(sel_ctx ctx, const void* handle72, void** out_dev_ptr) {
+  clear_error();
+  if (!ctx || !handle72 || !out_dev_ptr) return set_error(SEL_E_ARG, "null argument");
+  DeviceGuard g(ctx->device);
+  if (!g.ok) return set_error(SEL_E_CUDA, "cudaSetDevice failed");
+  const std::string key(static_cast<const char*>(handle72), 64);
+  uint64_t off = 0;
+  std::memcpy(&off, static_cast<const char*>(handle72) + 64, 8);
+  auto it = ctx->imported.find(key);
+  void* base = nullptr;
+  if (it != ctx->imported.end()) {
+    base = it->second;
+  } else {
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, handle72, 64);
+    cudaError_t e = cudaIpcOpenMemHandle(&base, h, cudaIpcMemLazyEnablePeerAccess);
+    if (e != cudaSuccess) return set_error(SEL_E_CUDA, cuda_msg("cudaIpcOpenMemHandle", e));
+    ctx->imported[key] = base;
+  }
+  *out_dev_ptr = static_cast<char*>(base) + off;
+  return SEL_OK;
+}
+
 sel_status sel_ctx_set_peers(sel_ctx ctx, int nranks, int rank, const void* handles) {
   clear_error();
   if (ctx && nranks == 0) {  // drop the peers: unmap the others' buffers, keep this rank's
     DeviceGuard g(ctx->device);
     for (void* p : ctx->peer_opened) cudaIpcCloseMemHandle(p);
     ctx->peer_opened.clear();
+    for (auto& kv : ctx->imported) cudaIpcCloseMemHandle(kv.second);
+    ctx->imported.clear();
     if (ctx->peer_ptrs) cudaFree(ctx->peer_ptrs);
     ctx->peer_ptrs = nullptr;
     ctx->xg = PeerXchg{};
@@ -701,6 +759,8 @@ void release_ctx_resources(sel_ctx c) {
   c->comm = nullptr;
   for (void* p : c->peer_opened) cudaIpcCloseMemHandle(p);
   c->peer_opened.clear();
+  for (auto& kv : c->imported) cudaIpcCloseMemHandle(kv.second);
+  c->imported.clear();
   if (c->peer_ptrs) cudaFree(c->peer_ptrs);
   if (c->peer_buf) cudaFree(c->peer_buf);
   if (c->peer_epoch) cudaFree(c->peer_epoch);
@@ -1155,7 +1215,7 @@ sel_status enqueue_pushdown_sel(sel_table t, const Plan& plan, const uint32_t* p
                                 uint32_t nproj, uint32_t* out_rowids, void* const* out_cols,
                                 uint64_t capacity_rows, bool gate, uint64_t gate_max,
                                 cudaStream_t stream, int gate_ranks = 0,
-                                const PeerXchg* xg = nullptr) {
+                                const PeerXchg* xg = nullptr, bool global_out = false) {
   sel_ctx c = t->ctx;
   const auto consts = const_columns(t, plan);
   const uint64_t n = t->local_rows;
@@ -1166,6 +1226,7 @@ sel_status enqueue_pushdown_sel(sel_table t, const Plan& plan, const uint32_t* p
     p->capacity = capacity_rows;
     p->gate = gate ? 1u : 0u;
     p->gate_max = gate_max;
+    p->global_out = global_out ? 1u : 0u;
     p->n_proj = capacity_rows > 0 ? nproj : 0;
     for (uint32_t j = 0; j < p->n_proj; ++j) {
       p->proj_src[j] = t->cols[proj_cols[j]].data;
@@ -1195,12 +1256,12 @@ sel_status enqueue_pushdown_sel(sel_table t, const Plan& plan, const uint32_t* p
     DevProgramSmall p;
     fill_sel(&p);
     le = launch_pushdown_sel_small(p, n, out_rowids, grid_for(c, units, occupancy_pushdown_sel_small()),
-                                   c->s, c->sel, stream, gate_ranks, xg);
+                                   c->s, c->sel, stream, gate_ranks, xg, c->rank);
   } else {
     static thread_local DevProgramLarge p;
     fill_sel(&p);
     le = launch_pushdown_sel_large(p, n, out_rowids, grid_for(c, units, occupancy_pushdown_sel_large()),
-                                   c->s, c->sel, stream, gate_ranks, xg);
+                                   c->s, c->sel, stream, gate_ranks, xg, c->rank);
   }
   if (le != cudaSuccess) return set_error(SEL_E_CUDA, cuda_msg("push-down kernel launch", (cudaError_t)le));
   c->last_pd_path = 1;
@@ -1238,7 +1299,8 @@ sel_status gather_counts(sel_ctx c, uint64_t local, void* cuda_stream) {
 // per-rank counts (result[1..nranks]) or the local count (result[0]).
 sel_status enqueue_execute(sel_table t, const Plan& plan, const uint32_t* proj, uint32_t nproj,
                            uint32_t nkeep, uint64_t max_size, uint32_t* out_rowids,
-                           void* const* outs, uint64_t capacity, cudaStream_t s) {
+                           void* const* outs, uint64_t capacity, cudaStream_t s,
+                           bool global_out = false) {
   sel_ctx c = t->ctx;
   sel_status st = enqueue_count(t, plan, SEL_KEEP_SELECTION, proj, nkeep, s, c->s.result + kGateSlot,
                                 false, proj, nproj);
@@ -1251,7 +1313,8 @@ sel_status enqueue_execute(sel_table t, const Plan& plan, const uint32_t* proj, 
   if (c->timing) record(c, c->ev2, s);
   // with peers the exchange runs inside the prefix kernel, right before the gated push-down
   st = enqueue_pushdown_sel(t, plan, proj, nproj, out_rowids, outs, capacity, true, max_size, s,
-                            c->comm && !c->peers ? c->nranks : 0, c->peers ? &c->xg : nullptr);
+                            c->comm && !c->peers ? c->nranks : 0, c->peers ? &c->xg : nullptr,
+                            global_out);
   if (st != SEL_OK) return st;
   if (c->timing) record(c, c->ev3, s);
   // one copy: the prefix kernel mirrored the words read back right below the gate slot
@@ -1820,10 +1883,13 @@ sel_status sel_count_batch(sel_table t, const void* const* progs, const size_t* 
   return SEL_OK;
 }
 
-uint64_t sel_execute(sel_table t, const void* prog, size_t prog_bytes, const uint32_t* proj_cols,
-                     uint32_t nproj, uint64_t max_size, uint32_t* out_rowids,
-                     void* const* out_cols, uint64_t capacity_rows, uint64_t* out_local_count,
-                     uint64_t* out_global_offset, int* out_materialized, void* cuda_stream) {
+// sel_execute and sel_execute_to (global_out: the outputs are the global result; each rank
+// writes at its offset in it).
+static uint64_t execute_impl(sel_table t, const void* prog, size_t prog_bytes,
+                             const uint32_t* proj_cols, uint32_t nproj, uint64_t max_size,
+                             uint32_t* out_rowids, void* const* out_cols, uint64_t capacity_rows,
+                             uint64_t* out_local_count, uint64_t* out_global_offset,
+                             int* out_materialized, void* cuda_stream, bool global_out) {
   clear_error();
   if (out_materialized) *out_materialized = 0;
   if (out_local_count) *out_local_count = 0;
@@ -1876,8 +1942,20 @@ uint64_t sel_execute(sel_table t, const void* prog, size_t prog_bytes, const uin
       }
     }
     if (count > max_size) return count;  // "throw exception": nothing written
-    const uint64_t r = pushdown_impl(t, prog, prog_bytes, proj_cols, nproj, out_rowids, out_cols,
-                                     capacity_rows, out_local_count, nullptr, cuda_stream, false);
+    uint32_t* ids = out_rowids;
+    std::vector<void*> cols(out_cols, out_cols + (out_cols ? nproj : 0));
+    uint64_t cap = capacity_rows;
+    if (global_out && offset > 0) {   // this rank's slice of the global result
+      cap = capacity_rows > offset ? capacity_rows - offset : 0;
+      if (cap > 0) {
+        ids = out_rowids + offset;
+        for (uint32_t j = 0; j < nproj; ++j)
+          cols[j] = static_cast<char*>(cols[j]) + offset * (uint64_t)width_of(t->types[proj_cols[j]]);
+      }
+    }
+    const uint64_t r = pushdown_impl(t, prog, prog_bytes, proj_cols, nproj, ids,
+                                     cols.empty() ? nullptr : cols.data(), cap, out_local_count,
+                                     nullptr, cuda_stream, false);
     if (r == SEL_ERR) return SEL_ERR;
     if (out_global_offset) *out_global_offset = offset;
     if (out_materialized) *out_materialized = 1;
@@ -1893,7 +1971,7 @@ uint64_t sel_execute(sel_table t, const void* prog, size_t prog_bytes, const uin
   c->last_ms = 0.f;
   c->last_pd_path = -1;
   sel_status st = enqueue_execute(t, plan, proj_cols, nproj, nkeep, max_size, out_rowids, out_cols,
-                                  capacity_rows, stream);
+                                  capacity_rows, stream, global_out);
   if (st != SEL_OK) return SEL_ERR;
   cudaError_t e = sync_stream(c, stream);
   if (e != cudaSuccess) return fail64(sync_code(e), cuda_msg("execute result", e));
@@ -1906,6 +1984,24 @@ uint64_t sel_execute(sel_table t, const void* prog, size_t prog_bytes, const uin
     c->last_ms = c->last_push_ms;
   }
   return execute_outputs(c, max_size, out_local_count, out_global_offset, out_materialized);
+}
+
+uint64_t sel_execute(sel_table t, const void* prog, size_t prog_bytes, const uint32_t* proj_cols,
+                     uint32_t nproj, uint64_t max_size, uint32_t* out_rowids,
+                     void* const* out_cols, uint64_t capacity_rows, uint64_t* out_local_count,
+                     uint64_t* out_global_offset, int* out_materialized, void* cuda_stream) {
+  return execute_impl(t, prog, prog_bytes, proj_cols, nproj, max_size, out_rowids, out_cols,
+                      capacity_rows, out_local_count, out_global_offset, out_materialized,
+                      cuda_stream, false);
+}
+
+uint64_t sel_execute_to(sel_table t, const void* prog, size_t prog_bytes, const uint32_t* proj_cols,
+                        uint32_t nproj, uint64_t max_size, uint32_t* out_rowids,
+                        void* const* out_cols, uint64_t capacity_rows, uint64_t* out_local_count,
+                        uint64_t* out_global_offset, int* out_materialized, void* cuda_stream) {
+  return execute_impl(t, prog, prog_bytes, proj_cols, nproj, max_size, out_rowids, out_cols,
+                      capacity_rows, out_local_count, out_global_offset, out_materialized,
+                      cuda_stream, true);
 }
 
 }  // extern "C"

@@ -1047,7 +1047,8 @@ __global__ void __launch_bounds__(256) peer_exchange_kernel(const PeerXchg x, co
 __global__ void __launch_bounds__(1024) superblock_prefix_kernel(const uint32_t* __restrict__ sb_sum,
                                                                  uint32_t* __restrict__ sb_prefix,
                                                                  uint32_t nsb, uint64_t* __restrict__ out_count,
-                                                                 int gate_ranks, const PeerXchg xg) {
+                                                                 int gate_ranks, const PeerXchg xg,
+                                                                 int rank) {
   const uint32_t t = threadIdx.x, lane = t & 31, warp = t >> 5;
   if (xg.n > 0) peer_gather_block(xg, out_count + kGateSlot, 1, out_count + 1, out_count + kGateSlot);
   if (gate_ranks > 0 && t == 0) {
@@ -1057,6 +1058,11 @@ __global__ void __launch_bounds__(1024) superblock_prefix_kernel(const uint32_t*
   }
   const int nr = xg.n > 0 ? xg.n : gate_ranks;
   if (nr > 0 && nr <= kMirrorMax && (int)t < nr) out_count[kGateSlot - nr + t] = out_count[1 + t];
+  if (t == 0) {   // this rank's position in the rank-ordered global result (sel_execute_to)
+    uint64_t off = 0;
+    for (int r = 0; r < rank && r < nr; ++r) off += out_count[1 + r];
+    out_count[kOffsetSlot] = off;
+  }
   const uint32_t per = (nsb + 1023u) / 1024u;
   const uint32_t b = min(nsb, t * per), e = min(nsb, b + per);
   uint32_t local = 0;
@@ -1172,6 +1178,8 @@ __global__ void __launch_bounds__(kThreads, SEL_PD_MINB) pushdown_sel_kernel(con
                                                                    uint32_t* __restrict__ out_ids,
                                                                    const uint64_t* __restrict__ gate_count) {
   if (p.gate && *gate_count > p.gate_max) return;  // Algorithm 1's "throw": nothing written
+  // sel_execute_to: positions in the global result start at this rank's offset (prefix kernel)
+  const uint64_t goff = p.global_out ? gate_count[kOffsetSlot - kGateSlot] : 0ull;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   __shared__ uint16_t s_stage[kWarpsPerCta][kStageCap];
   uint16_t* my = s_stage[warp];
@@ -1200,7 +1208,7 @@ __global__ void __launch_bounds__(kThreads, SEL_PD_MINB) pushdown_sel_kernel(con
     // --- offsets ---
     const uint32_t total = __reduce_add_sync(0xFFFFFFFFu, cntv);
     if (total == 0) continue;
-    uint64_t gbase = (uint64_t)sbp + __reduce_add_sync(0xFFFFFFFFu, part);
+    uint64_t gbase = goff + (uint64_t)sbp + __reduce_add_sync(0xFFFFFFFFu, part);
     const uint64_t bbase = c0 * kChunkRows;
     uint32_t staged = 0;
 #pragma unroll
@@ -1429,7 +1437,7 @@ int launch_count_large(const DevProgramLarge& p, uint64_t n, int grid, const Scr
 }
 int launch_pushdown_sel_small(const DevProgramSmall& p, uint64_t n, uint32_t* out_ids, int grid,
                               const Scratch& s, const SelectionBufs& sb, void* st, int gate_ranks,
-                              const PeerXchg* xg) {
+                              const PeerXchg* xg, int rank) {
   const PeerXchg none{};
   const uint64_t nchunks = (n + kChunkRows - 1) / kChunkRows;
   const uint32_t nsb = (uint32_t)((nchunks + kSbChunks - 1) / kSbChunks);
@@ -1438,7 +1446,7 @@ int launch_pushdown_sel_small(const DevProgramSmall& p, uint64_t n, uint32_t* ou
                           (cudaStream_t)st>>>(sb.chunk_cnt, nchunks, sb.sb_sum);
 #endif
   superblock_prefix_kernel<<<1, 1024, 0, (cudaStream_t)st>>>(sb.sb_sum, sb.sb_prefix, nsb, s.result,
-                                                               gate_ranks, xg ? *xg : none);
+                                                               gate_ranks, xg ? *xg : none, rank);
   if (p.coded)
     pushdown_sel_kernel<DevProgramSmall, true><<<grid, kThreads, 0, (cudaStream_t)st>>>(p, n, sb, out_ids,
                                                                                 s.result + kGateSlot);
@@ -1449,7 +1457,7 @@ int launch_pushdown_sel_small(const DevProgramSmall& p, uint64_t n, uint32_t* ou
 }
 int launch_pushdown_sel_large(const DevProgramLarge& p, uint64_t n, uint32_t* out_ids, int grid,
                               const Scratch& s, const SelectionBufs& sb, void* st, int gate_ranks,
-                              const PeerXchg* xg) {
+                              const PeerXchg* xg, int rank) {
   const PeerXchg none{};
   const uint64_t nchunks = (n + kChunkRows - 1) / kChunkRows;
   const uint32_t nsb = (uint32_t)((nchunks + kSbChunks - 1) / kSbChunks);
@@ -1458,7 +1466,7 @@ int launch_pushdown_sel_large(const DevProgramLarge& p, uint64_t n, uint32_t* ou
                           (cudaStream_t)st>>>(sb.chunk_cnt, nchunks, sb.sb_sum);
 #endif
   superblock_prefix_kernel<<<1, 1024, 0, (cudaStream_t)st>>>(sb.sb_sum, sb.sb_prefix, nsb, s.result,
-                                                               gate_ranks, xg ? *xg : none);
+                                                               gate_ranks, xg ? *xg : none, rank);
   if (p.coded)
     pushdown_sel_kernel<DevProgramLarge, true><<<grid, kThreads, 0, (cudaStream_t)st>>>(p, n, sb, out_ids,
                                                                                 s.result + kGateSlot);

@@ -82,6 +82,8 @@ struct DevProgramT {
                          // kLeafStaged; offset = span[iv_begin] >> 32), 0 = none
   uint32_t n_direct;     // push-down from a selection: projections that are kept or constant
   uint32_t coded;        // push-down from a selection: a projection is kCodedProj
+  uint32_t global_out;   // push-down from a selection: the outputs are the GLOBAL result
+                         // (sel_execute_to): positions start at Scratch::result[kOffsetSlot]
   // Count kernel fast path (template-specialised conjunctive forms): when
   // fast_n > 0 the program is leaf 0 AND ... AND leaf fast_n-1 and leaf s has kind fast_kind[s]
   // (FastKind); the kernel instantiated for fast_n evaluates it as straight-line code with the
@@ -176,7 +178,8 @@ struct SelectionBufs {
 // [kGateSlot] the global count sel_execute's device-side gate reads.
 constexpr int kMaxRanks = 1024;
 constexpr int kGateSlot = 1 + kMaxRanks;
-constexpr int kResultSlots = 2 + kMaxRanks;
+constexpr int kOffsetSlot = 2 + kMaxRanks;   // this rank's global output offset (sel_execute_to)
+constexpr int kResultSlots = 3 + kMaxRanks;
 constexpr int kMirrorMax = 512;  // read-back mirror below kGateSlot (superblock_prefix_kernel)
 
 // The library's own exchange over peer memory (sel_ctx_set_peers; SURVEY §8e "a one-shot peer
@@ -241,12 +244,14 @@ int launch_count_large(const DevProgramLarge& p, uint64_t n, int grid, const Scr
 // compaction/gather kernel.
 // xg != nullptr (sel_execute with peers): the prefix kernel first runs the peer exchange of the
 // local count in s.result[kGateSlot] (gathered into s.result[1..n], the sum into kGateSlot).
+// rank: this rank (for the offset of sel_execute_to: the sum of the gathered counts of the ranks
+// before it, written to s.result[kOffsetSlot]).
 int launch_pushdown_sel_small(const DevProgramSmall& p, uint64_t n, uint32_t* out_ids, int grid,
                               const Scratch& s, const SelectionBufs& sb, void* stream,
-                              int gate_ranks = 0, const PeerXchg* xg = nullptr);
+                              int gate_ranks = 0, const PeerXchg* xg = nullptr, int rank = 0);
 int launch_pushdown_sel_large(const DevProgramLarge& p, uint64_t n, uint32_t* out_ids, int grid,
                               const Scratch& s, const SelectionBufs& sb, void* stream,
-                              int gate_ranks = 0, const PeerXchg* xg = nullptr);
+                              int gate_ranks = 0, const PeerXchg* xg = nullptr, int rank = 0);
 int launch_pushdown_small(const DevProgramSmall& p, uint64_t n, uint32_t* out_ids, int grid,
                           const Scratch& s, uint64_t ticket_base, uint32_t epoch, void* stream);
 int launch_pushdown_large(const DevProgramLarge& p, uint64_t n, uint32_t* out_ids, int grid,

@@ -49,6 +49,45 @@ def setup_peers(ctx: Context, group=None) -> Context:
     return ctx
 
 
+def gather_execute(table: Table, pred, project, max_size: int, root: int = 0, group=None):
+    """Algorithm 1's Execute over the sharded table with the result gathered on rank `root`
+    (SURVEY §8e's optional gather-to-one-rank): the root allocates the global outputs
+    (min(max_size, global rows) rows), every rank maps them (CUDA IPC over NVLink/NVSwitch) and
+    its materialisation kernel writes its rows straight into them at its offset
+    (include/sel.h sel_execute_to). Collective. Returns (global count, materialized, and on the
+    root the rowids tensor and the {column: tensor} of the whole ascending result; None
+    elsewhere)."""
+    import torch
+    ctx = table.ctx
+    rank = dist.get_rank(group)
+    proj = table._col_indices(project)
+    cap = int(min(max_size, table.global_rows))
+    out = None
+    handles = None
+    if rank == root:
+        from .api import _OUT_DTYPE
+        dev = ctx.device
+        out = (torch.empty(max(cap, 1), dtype=torch.int32, device=dev),
+               [torch.empty(max(cap, 1), dtype=_OUT_DTYPE[table.types[j]], device=dev) for j in proj])
+        handles = [ctx.export_buffer(out[0])] + [ctx.export_buffer(t) for t in out[1]]
+    obj = [handles]
+    dist.broadcast_object_list(obj, src=dist.get_global_rank(group, root) if group else root,
+                               group=group)
+    handles = obj[0]
+    if rank == root:
+        ptrs = [out[0].data_ptr()] + [t.data_ptr() for t in out[1]]
+    else:
+        ptrs = [ctx.import_buffer(h) for h in handles]
+    count, _, _, mat = table.execute_to(pred, project, max_size, cap, ptrs[0], ptrs[1:])
+    torch.cuda.synchronize(ctx.device)
+    dist.barrier(group)          # every rank's stores are complete before the root reads
+    if rank != root:
+        return count, mat, None, None
+    k = min(count, cap) if mat else 0
+    keys = [table.names[j] if isinstance(p, str) else j for p, j in zip(project, proj)]
+    return count, mat, out[0][:k], {key: t[:k] for key, t in zip(keys, out[1])}
+
+
 def exclusive_offset(local_counts, rank: int) -> int:
     """Position of rank `rank`'s slice in the rank-ordered (= ascending row id) concatenation."""
     return int(sum(local_counts[:rank]))

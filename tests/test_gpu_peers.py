@@ -70,6 +70,22 @@ def _worker(rank, world, port, n_global, out_path):
         r["sampled"] = t.count_sampled(prog, 3, 1)[:2]
         rec.append(r)
     r_batch = t.count_batch(progs[:5])
+    # gather to one rank: every rank's materialisation writes into the root's buffers (P2P)
+    keep_alive = []
+    for i, prog in enumerate(progs):
+        root = i % world
+        cnt, mat, ids, cols = sdist.gather_execute(t, prog, ["C", "D"], max_size=n_global, root=root)
+        keep_alive.append((ids, cols))
+        if rank == root:
+            want_c, want_ids, want_cols = oracle.pushdown(host, types, prog, proj=[2, 3])
+            assert cnt == want_c and mat, ("gather", i)
+            np.testing.assert_array_equal(ids.cpu().numpy().view(np.uint32), want_ids)
+            np.testing.assert_array_equal(cols["C"].cpu().numpy(), want_cols[0])
+            np.testing.assert_array_equal(cols["D"].cpu().numpy(), want_cols[1])
+    cnt, mat, ids, cols = sdist.gather_execute(t, progs[0], ["D"], max_size=0, root=0)
+    keep_alive.append((ids, cols))
+    want0 = oracle.count(host, types, progs[0])
+    assert cnt == want0 and mat == (want0 == 0)
     torch.cuda.synchronize()
     gathered = [None] * world
     dist.all_gather_object(gathered, (rec, r_batch, s, e))
