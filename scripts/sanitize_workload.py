@@ -103,6 +103,12 @@ for r in (r1, q.result()):
     assert np.array_equal(r.rowids.cpu().numpy().view(np.uint32), want[1])
     assert np.array_equal(r.columns[2].cpu().numpy(), want[2][1])
 q.release()
+# sel_execute_to into the context's own buffers (offset 0)
+ids = torch.empty(want[0], dtype=torch.int32, device=dev)
+cd = [torch.empty(want[0], dtype=c.dtype, device=dev) for c in (T.columns[0].data, T.columns[2].data, T.columns[3].data)]
+cnt, loc, off, mat = t.execute_to(prog, [0, 2, 3], 60_000, want[0], ids.data_ptr(), [x.data_ptr() for x in cd])
+assert cnt == want[0] and mat and off == 0
+assert np.array_equal(ids.cpu().numpy().view(np.uint32), want[1])
 t.release()
 torch.cuda.synchronize()
 print("sanitize workload ok")
