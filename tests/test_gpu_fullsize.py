@@ -116,3 +116,19 @@ def test_c5_sweep_1e9_closed_form(ctx):
             got = res.rowids.to(torch.int64) & 0xFFFFFFFF
             assert torch.equal(got, want), s
             assert torch.equal(res.columns["y"], T.col("y").data[got])
+
+
+def test_c0_orders_sf50_paper_probes(ctx):
+    """C0 (SURVEY §8d optional context): TPC-H SF-50 orders, 75M rows, with the paper's Table 5.1 /
+    5.2 probes — `o_orderkey = 1` selects exactly one row and `o_orderkey >= 1` every row
+     — the Listing 5.3 attribute sweep and Q5's one-year range (15.2 % of
+    orders), on sampled windows and properties."""
+    T = configs.gen_orders(75_000_000, device=ctx.device)
+    probes = configs.orders_probes()
+    t = sel.Table(ctx, [c.name for c in T.columns], T.types, [c.data for c in T.columns])
+    assert t.count(encode(probes["l5.1"], T.types)) == 1
+    assert t.count(encode(probes["l5.2"], T.types)) == 75_000_000
+    q5 = t.count(encode(probes["q5_orderdate"], T.types))
+    assert abs(q5 / 75_000_000 - 365 / 2406) < 0.002
+    t.release()
+    check_large(ctx, T, {k: probes[k] for k in ("attr2", "attr4", "q5_orderdate")}, [0, 1], 50)
