@@ -128,7 +128,8 @@ def coded_columns(prog, types, proj):
     plan = sel.program_plan(prog, types)
     for L, kind in zip(plan["leaves"], plan.get("fast") or []):
         pts = sum(sp + 1 for sp in L["span"])
-        if kind == 4 and pts == 2 and L["col"] in proj:
+        two_points = (kind == 4 and pts == 2) or (kind == 2 and L["span"] == [0, 0])
+        if two_points and L["col"] in proj:
             return {L["col"]}
     return set()
 

@@ -1158,13 +1158,20 @@ sel_status enqueue_count(sel_table t, const Plan& plan, uint32_t flags, const ui
         c->sel.code_col = -1;
         if (keep->n_keep == 0 && p.fast_n > 0 && c->code_enabled) {
           for (uint32_t s2 = 0; s2 < p.fast_n && c->sel.code_col < 0; ++s2) {
-            if (p.fast_kind[s2] != FK_S1 || p.fast_npts[s2] != 2) continue;
+            const DevLeaf& L = p.leaf[s2];
+            const bool s1 = p.fast_kind[s2] == FK_S1 && p.fast_npts[s2] == 2;
+            const bool s4 = p.fast_kind[s2] == FK_S4 && L.iv_count == 2 &&
+                            p.span[L.iv_begin] == 0 && p.span[L.iv_begin + 1] == 0;
+            if (!s1 && !s4) continue;
             const int col = plan.leaves[s2].col;
             for (uint32_t j = 0; j < ncode; ++j) {
               if ((int)code_cols[j] != col) continue;
               p.fast_code = (int32_t)s2;
               c->sel.code_col = col;
-              c->sel.code_pts = (p.fast_pts[s2][0] & 0xFFu) | ((p.fast_pts[s2][1] & 0xFFu) << 8);
+              c->sel.code_pts =
+                  s1 ? (uint64_t)((p.fast_pts[s2][0] & 0xFFu) | ((p.fast_pts[s2][1] & 0xFFu) << 8))
+                     : ((uint64_t)(uint32_t)p.lo[L.iv_begin] |
+                        ((uint64_t)(uint32_t)p.lo[L.iv_begin + 1] << 32));
               break;
             }
           }

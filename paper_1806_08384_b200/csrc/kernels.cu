@@ -474,9 +474,10 @@ __device__ __forceinline__ uint32_t fast_s1(const void* col, uint64_t base, int 
 
 // The coded leaf's point-1 matches over a partial (tail) chunk, for keep_chunk.
 __device__ __forceinline__ uint32_t which_tail(const void* col, uint64_t base, int lane,
-                                               uint32_t nvalid, uint32_t pt1) {
+                                               uint32_t nvalid, uint32_t pt1, bool w4) {
   uint32_t v[32];
-  load_w1<true>(col, base, lane, nvalid, v, nullptr);
+  if (w4) load_w4<true>(col, base, lane, nvalid, v, nullptr);
+  else load_w1<true>(col, base, lane, nvalid, v, nullptr);
   uint32_t m = 0;
 #pragma unroll
   for (int i = 0; i < 32; ++i) m |= (v[i] == pt1) ? (1u << i) : 0u;
@@ -484,13 +485,25 @@ __device__ __forceinline__ uint32_t which_tail(const void* col, uint64_t base, i
 }
 
 // 4-byte column: one point (E4), one interval (R4) or 2..4 intervals (S4, n = iv_count).
+// The coded leaf (S4 with two points) also returns which rows matched point 1 (*wm).
 template <int KIND, bool CAP>
 __device__ __forceinline__ uint32_t fast_w4(const void* col, uint64_t base, int lane,
                                             const uint64_t* lo, const uint64_t* span, int n,
-                                            char* cap) {
+                                            char* cap, uint32_t* wm = nullptr) {
   uint32_t v[32];
   load_w4<false>(col, base, lane, kChunkRows, v, CAP ? cap : nullptr);
   uint32_t m = 0;
+  if (KIND == FK_S4 && wm) {   // two points
+    const uint32_t a = (uint32_t)lo[0], b = (uint32_t)lo[1];
+    uint32_t m1 = 0;
+#pragma unroll
+    for (int i = 0; i < 32; ++i) {
+      m |= (v[i] == a) ? (1u << i) : 0u;
+      m1 |= (v[i] == b) ? (1u << i) : 0u;
+    }
+    *wm = m1;
+    return m | m1;
+  }
   if (KIND == FK_E4) {
     const uint32_t a = (uint32_t)lo[0];
 #pragma unroll
@@ -542,7 +555,10 @@ __device__ __forceinline__ uint32_t eval_fast(const P& p, uint64_t base, int lan
     switch (p.fast_kind[s]) {
       case FK_E4: r = fast_w4<FK_E4, CAP>(col, base, lane, lo, sp, 1, cap); break;
       case FK_R4: r = fast_w4<FK_R4, CAP>(col, base, lane, lo, sp, 1, cap); break;
-      case FK_S4: r = fast_w4<FK_S4, CAP>(col, base, lane, lo, sp, L.iv_count, cap); break;
+      case FK_S4:
+        r = fast_w4<FK_S4, CAP>(col, base, lane, lo, sp, L.iv_count, cap,
+                                p.fast_code == s ? wm : nullptr);
+        break;
       case FK_R8: r = fast_r8<CAP>(col, base, lane, lo[0], sp[0], cap); break;
       default:
         r = fast_s1<CAP>(col, base, lane, p.fast_pts[s], p.fast_npts[s], cap,
@@ -894,7 +910,9 @@ __global__ void __launch_bounds__(NW * 32, NW == kWarpsPerCta ? (FASTN ? SEL_FAS
     const bool coded = KEEP && FASTN > 0 && p.fast_code >= 0;
     if (coded) {
       const int s = p.fast_code;
-      wm = which_tail(p.col[p.leaf[s].slot], nfull * kChunkRows, lane, rem, p.fast_pts[s][1] & 0xFFu);
+      const bool w4 = p.fast_kind[s] == FK_S4;
+      const uint32_t pt1 = w4 ? (uint32_t)p.lo[p.leaf[s].iv_begin + 1] : (p.fast_pts[s][1] & 0xFFu);
+      wm = which_tail(p.col[p.leaf[s].slot], nfull * kChunkRows, lane, rem, pt1, w4);
     }
     keep_chunk<P, KEEP>(sb, nfull, lane, m, wsmem, wm, coded);
   }
@@ -1113,10 +1131,16 @@ __device__ __forceinline__ void flush_rows(const P& p, uint64_t bbase, uint64_t 
 #pragma unroll 1
   for (uint32_t j = 0; j < p.n_proj; ++j) {
     if (CODED && p.proj_cap_off[j] == kCodedProj) {   // the value from the row's code bit, nothing read
-      const uint32_t pts = (uint32_t)(uintptr_t)p.proj_src[j];
-      uint8_t* __restrict__ dst = static_cast<uint8_t*>(p.proj_dst[j]) + gbase;
+      const uint64_t pts = (uint64_t)(uintptr_t)p.proj_src[j];
+      if (p.proj_wclass[j] == W1) {
+        uint8_t* __restrict__ dst = static_cast<uint8_t*>(p.proj_dst[j]) + gbase;
 #pragma unroll 4
-      for (uint32_t q = lane; q < lim; q += 32) dst[q] = (uint8_t)(pts >> ((my[q] & kCodeBit) ? 8 : 0));
+        for (uint32_t q = lane; q < lim; q += 32) dst[q] = (uint8_t)(pts >> ((my[q] & kCodeBit) ? 8 : 0));
+      } else {
+        uint32_t* __restrict__ dst = static_cast<uint32_t*>(p.proj_dst[j]) + gbase;
+#pragma unroll 4
+        for (uint32_t q = lane; q < lim; q += 32) dst[q] = (uint32_t)(pts >> ((my[q] & kCodeBit) ? 32 : 0));
+      }
       continue;
     }
     if (p.proj_cap_off[j] != kNoCapture) continue;

@@ -30,9 +30,10 @@ constexpr uint16_t kKeptBase = 0xFF00;  // push-down from a selection: proj_cap_
 // conjunction pins it with a single-value leaf), raw bits in (uintptr_t)proj_src: a fill.
 constexpr uint16_t kConstProj = 0xFFFE;
 // proj_cap_off = kCodedProj (push-down from a selection): the conjunction pins the column to two
-// values (a 1-byte IN of two points) and the keeping count recorded, per row, which one matched
-// (SelectionBufs::which); the staged row numbers carry that bit (kCodeBit) and the value is
-// (uintptr_t)proj_src >> (8 * bit) & 0xFF — the column is never read by the push-down.
+// values (an IN of two points on a 1- or 4-byte column) and the keeping count recorded, per row,
+// which one matched (SelectionBufs::which); the staged row numbers carry that bit (kCodeBit) and
+// the value is (uintptr_t)proj_src >> (w * bit), w = 8 or 32 — the column is never read by the
+// push-down.
 constexpr uint16_t kCodedProj = 0xFFFD;
 constexpr uint16_t kCodeBit = 1u << 12;          // staged block-relative rows are < 4096
 constexpr int kMaxDeviceStack = 32;
@@ -160,7 +161,8 @@ struct SelectionBufs {
   uint32_t* bits;        // [nchunks * 32]
   uint32_t* which;       // [nchunks * 32] row-major: row matched point 1 of the coded leaf
   int32_t code_col;      // table column coded by `which` (host bookkeeping), -1 = none
-  uint32_t code_pts;     // its two raw byte values: point 0 | point 1 << 8
+  uint64_t code_pts;     // its two raw values: 1-byte column point 0 | point 1 << 8; 4-byte
+                         // column point 0 | point 1 << 32
   uint16_t* chunk_cnt;   // [nchunks]
   uint32_t* sb_sum;      // [nsb], zeroed before the count
   uint32_t* sb_prefix;   // [nsb]
