@@ -98,10 +98,11 @@ sel_status sel_ctx_set_comm(sel_ctx ctx, int nranks, int rank, const void* nccl_
  * counts (epoch-tagged) into every rank's buffer with system-scope release stores over
  * NVLink/NVSwitch and waits (acquire loads) until all ranks' values of that epoch arrived.
  * Once set, EVERY cross-rank combination of the context uses it instead of NCCL: sel_count's
- * sum, sel_pushdown's offsets, sel_count_batch / sel_count_sampled's sums, and sel_execute's
- * one exchange per call — which runs inside the push-down's prefix kernel, fused with the
- * materialisation it gates, also in prepared (graph) executes. A communicator is then not
- * needed; if one is set as well, its nranks/rank must agree.
+ * sum (run by the count kernel's last CTA, fused with the count), sel_pushdown's offsets,
+ * sel_count_batch / sel_count_sampled's sums, and sel_execute's one exchange per call — which
+ * runs inside the push-down's prefix kernel, fused with the materialisation it gates, also in
+ * prepared (graph) executes. A communicator is then not needed; if one is set as well, its
+ * nranks/rank must agree.
  * sel_ctx_peer_handle: allocates the context's buffer (on first call) and writes its 64-byte
  *   CUDA IPC handle to out64 (host memory), to be shared out of band (torch.distributed).
  *   Errors: SEL_E_ARG, SEL_E_STATE (context destroyed), SEL_E_CUDA.
@@ -161,9 +162,9 @@ sel_status sel_table_register(sel_ctx ctx, const sel_column* cols, uint32_t ncol
 void sel_table_release(sel_table table);
 
 /* ---- probes --------------------------------------------------------------------------------
- * sel_count: exact |{ i : P(row i) }| over the table's rows. With a
- * communicator it is the sum over all ranks (one 8-byte NCCL all-reduce) and every rank gets
- * the global count. Enqueues on `cuda_stream` (a cudaStream_t; NULL = legacy default stream)
+ * sel_count: exact |{ i : P(row i) }| over the table's rows. With peers
+ * or a communicator it is the sum over all ranks (one exchange: the peer-memory exchange fused
+ * into the count kernel, or one 8-byte NCCL all-reduce) and every rank gets the global count. Enqueues on `cuda_stream` (a cudaStream_t; NULL = legacy default stream)
  * and blocks until the count is on the host (the optimizer needs the number).
  * `prog` is host memory, copied during the call.
  * Returns the count, or SEL_ERR (SEL_E_ARG, SEL_E_PROGRAM, SEL_E_TYPE, SEL_E_CUDA, SEL_E_NCCL). */
@@ -204,9 +205,10 @@ uint64_t sel_count_ex(sel_table table, const void* prog, size_t prog_bytes, uint
  * GLOBAL count > max_size "throw" — *out_materialized = 0, nothing is written, *out_local_count
  * and *out_global_offset are set to 0 — else materialise exactly like sel_pushdown (from the kept
  * selection) and set *out_materialized = 1. Returns the global count or SEL_ERR. Arguments as
- * sel_pushdown; out_materialized may be NULL. With a communicator the call issues exactly one
- * collective, gated or not: an all-gather of the per-rank counts, whose sum is the global count
- * the gate compares and whose exclusive prefix is *out_global_offset (every rank must call it). */
+ * sel_pushdown; out_materialized may be NULL. With peers or a communicator the call issues
+ * exactly one collective, gated or not: an exchange (peer memory) or all-gather (NCCL) of the
+ * per-rank counts, whose sum is the global count the gate compares and whose exclusive prefix
+ * is *out_global_offset (every rank must call it). */
 uint64_t sel_execute(sel_table table, const void* prog, size_t prog_bytes,
                      const uint32_t* proj_cols, uint32_t nproj, uint64_t max_size,
                      uint32_t* out_rowids, void* const* out_cols, uint64_t capacity_rows,
@@ -262,7 +264,7 @@ void sel_prepared_release(sel_prepared prepared);
  *   *out_local_count with its capacity ("throw" -> revert).
  *   out_local_count (host, may be NULL): selected rows in this shard.
  *   out_global_offset (host, may be NULL): exclusive prefix of the per-rank counts in rank order
- *   (0 without a communicator) = this shard's position in the global ascending result.
+ *   (0 with one rank) = this shard's position in the global ascending result.
  * Returns the global count (sum over ranks), or SEL_ERR. Blocks like sel_count.
  * Errors: as sel_count, plus SEL_E_ARG for a bad projection index or null outputs with
  * capacity_rows > 0. */
