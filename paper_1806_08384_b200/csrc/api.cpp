@@ -180,6 +180,8 @@ struct sel_ctx_s {
   uint32_t* peer_epoch = nullptr;     // device exchange counter
   uint32_t* h_peer_err = nullptr;     // host-mapped timeout flag
   std::map<std::string, void*> imported;  // sel_ctx_import_buffer: IPC handle -> mapped base
+  char* hist_buf = nullptr;           // sel_histogram scratch (keys, sorted keys, sort temp, stats)
+  size_t hist_cap = 0;
   PeerXchg xg{};
 };
 
@@ -761,6 +763,9 @@ void release_ctx_resources(sel_ctx c) {
   c->peer_opened.clear();
   for (auto& kv : c->imported) cudaIpcCloseMemHandle(kv.second);
   c->imported.clear();
+  if (c->hist_buf) cudaFree(c->hist_buf);
+  c->hist_buf = nullptr;
+  c->hist_cap = 0;
   if (c->peer_ptrs) cudaFree(c->peer_ptrs);
   if (c->peer_buf) cudaFree(c->peer_buf);
   if (c->peer_epoch) cudaFree(c->peer_epoch);
@@ -1667,9 +1672,18 @@ sel_status sel_histogram(sel_table t, uint32_t col, uint32_t stride, uint32_t ph
   const size_t tb = histogram_temp_bytes(std::max<uint64_t>(m, 1));
   const size_t kb = std::max<uint64_t>(m, 1) * sizeof(uint32_t);
   const size_t ob = (size_t)nbuckets * (2 * sizeof(uint32_t) + 2 * sizeof(uint64_t));
-  char* buf = nullptr;
-  cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&buf), 2 * kb + tb + ob + 64, stream);
-  if (e != cudaSuccess) return set_error(SEL_E_CUDA, cuda_msg("cudaMallocAsync(histogram)", e));
+  const size_t need = 2 * kb + tb + ob + 64;
+  cudaError_t e = cudaSuccess;
+  if (c->hist_cap < need) {   // grows only (kept by the context for the next histogram)
+    e = sync_stream(c, stream);
+    if (e == cudaSuccess && c->hist_buf) e = cudaFree(c->hist_buf);
+    c->hist_buf = nullptr;
+    c->hist_cap = 0;
+    if (e == cudaSuccess) e = cudaMalloc(reinterpret_cast<void**>(&c->hist_buf), need);
+    if (e != cudaSuccess) return set_error(SEL_E_CUDA, cuda_msg("cudaMalloc(histogram)", e));
+    c->hist_cap = need;
+  }
+  char* buf = c->hist_buf;
   uint32_t* keys = reinterpret_cast<uint32_t*>(buf);
   uint32_t* sorted = keys + kb / sizeof(uint32_t);
   uint64_t* rows = reinterpret_cast<uint64_t*>(buf + ((2 * kb + 7) & ~size_t(7)));
@@ -1685,7 +1699,6 @@ sel_status sel_histogram(sel_table t, uint32_t col, uint32_t stride, uint32_t ph
   if (e == cudaSuccess) e = cudaMemcpyAsync(out_distinct, distinct, nbuckets * sizeof(uint64_t), cudaMemcpyDeviceToHost, stream);
   if (e == cudaSuccess) e = cudaMemcpyAsync(hlo.data(), lo, nbuckets * sizeof(uint32_t), cudaMemcpyDeviceToHost, stream);
   if (e == cudaSuccess) e = cudaMemcpyAsync(hhi.data(), hi, nbuckets * sizeof(uint32_t), cudaMemcpyDeviceToHost, stream);
-  cudaFreeAsync(buf, stream);
   if (e == cudaSuccess) e = sync_stream(c, stream);
   if (e != cudaSuccess) return set_error(sync_code(e), cuda_msg("histogram", e));
   for (uint32_t b = 0; b < nbuckets; ++b) {   // keys back to values; an empty bucket reports 0, 0
