@@ -32,3 +32,16 @@ def test_bench_two_ranks_same_device(cuda_device):
     assert d["n_gpus"] == 2 and d["config"]["selected"] == 100_200
     assert d["config"]["exchange"].startswith("peers")
     assert d["e2e"]["h2d_bytes_per_step"] > 0 and d["value"] > 0
+
+
+def test_multi_gpu_example_two_ranks(cuda_device):
+    """examples/multi_gpu_probe.py under torchrun (2 ranks on one GPU): count, Execute, gather to
+    rank 0 and Algorithm 1's driver across ranks."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+           "--master-addr", "127.0.0.1", "--master-port", str(_port()),
+           "examples/multi_gpu_probe.py", "--same-device", "--rows", "600000"]
+    out = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0, out.stdout[-2000:] + out.stderr[-3000:]
+    assert "exact count  |sigma(R)| = 100,200 of 600,000" in out.stdout
+    assert "gathered     100,200 ascending row ids on rank 0" in out.stdout
+    assert "algorithm 1  R: evaluated, count 100,200" in out.stdout
