@@ -207,12 +207,15 @@ class ClockSampler:
                         self.reasons.add(k)
             except Exception:
                 pass
-            time.sleep(0.005)
+            time.sleep(0.001)
 
     def __enter__(self):
         if self.nv is not None:
             self._t = threading.Thread(target=self._run, daemon=True)
             self._t.start()
+            t0 = time.time()
+            while not self.samples and time.time() - t0 < 1.0:   # sampling before the region
+                time.sleep(0.0005)
         return self
 
     def __exit__(self, *a):
@@ -494,7 +497,7 @@ def run_ours(args):
     coded = coded_columns(prog, T.types, proj) if pd_path == 1 else set()
     cb, pb, step_b = algo_bytes(T, pc, proj, local_count, pd_path, consts, coded)
     my_bytes = step_b
-    t = torch.tensor([dev_ms, my_bytes, cb, pb, statistics.mean(count_ms), statistics.mean(push_ms)],
+    t = torch.tensor([dev_ms, my_bytes, cb, pb, statistics.median(count_ms), statistics.median(push_ms)],
                      dtype=torch.float64, device=_red_dev(dev))
     if world > 1:
         tmax = t.clone(); dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
@@ -511,8 +514,8 @@ def run_ours(args):
     peak_note = "MEASURED_PEAKS.json hbm_gbs (copy, read+write)"
     if not hbm:
         hbm, peak_note = 6650.0, "fallback 6.65 TB/s (B200_PROFILING.md)"
-    push_k = statistics.mean(push_ms)
-    count_k = statistics.mean(count_ms)
+    push_k = statistics.median(push_ms)
+    count_k = statistics.median(count_ms)
     push_gbs = pb / (push_k / 1000) / 1e9
     count_gbs = cb / (count_k / 1000) / 1e9
 
@@ -674,9 +677,9 @@ def run_ours(args):
                  "achieved_sector": round(push_sector_gbs, 2),
                  "frac_sector": round(push_sector_gbs / hbm, 4)}
     for r in (roof_count, roof_push):
-        r["ms_source"] = ("mean of the library's CUDA events around the kernel on its stream, over "
-                          "a second pass of the same steps right after the timed region (events "
-                          "inside the timed graph would add ~20 us per step)")
+        r["ms_source"] = ("median of the library's CUDA events around the kernel on its stream, "
+                          "over a second pass of the same steps right after the timed region "
+                          "(events inside the timed graph would add ~20 us per step)")
     for r in (roof_count, roof_push):   # the same achieved rate against SURVEY §8(d)'s other peaks
         r["frac_nominal_8tbs"] = round(r["achieved"] / 8000.0, 4)
         if read_peak:
