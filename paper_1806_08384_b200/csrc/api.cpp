@@ -22,6 +22,7 @@ using namespace sel;
 // ---- thread-local error state ----------------------------------------------------------------
 namespace {
 constexpr uint64_t kTwoPassMinRows = 3ull << 20;  // sel_pushdown: two passes from here
+constexpr uint64_t kDenseSplitMinRows = 8ull << 20;  // whole-chunk copy kernel from here (§6)
 thread_local sel_status g_status = SEL_OK;
 thread_local std::string g_message;
 
@@ -158,6 +159,7 @@ struct sel_ctx_s {
   uint64_t two_pass_min_rows = kTwoPassMinRows;
   bool fast_enabled = true;  // count fast path (SEL_FAST=0: interpreter only)
   bool code_enabled = true;  // coded projections (SEL_CODED=0: gather them)
+  bool dense_split = true;   // fully selected chunks copied whole (SEL_DENSE_SPLIT=0: not)
   bool graph_comm = true;    // prepared executes with a communicator are captured (SEL_GRAPH_COMM=0: not)
   int prefetch_mode = -1;   // -1 auto, 0 off, 1 on
   bool keep_values = false;  // SEL_KEEP_VALUES=1: executes also keep projected predicate values
@@ -485,7 +487,7 @@ sel_status ensure_selection(sel_ctx c, uint64_t nchunks) {
   cudaError_t e = cudaMalloc(&c->sel.bits, cap * 32 * sizeof(uint32_t));
   if (e == cudaSuccess) e = cudaMalloc(&c->sel.which, cap * 32 * sizeof(uint32_t));
   if (e == cudaSuccess) e = cudaMalloc(&c->sel.chunk_cnt, cap * sizeof(uint16_t));
-  if (e == cudaSuccess) e = cudaMalloc(&c->sel.sb_sum, nsb * sizeof(uint32_t));
+  if (e == cudaSuccess) e = cudaMalloc(&c->sel.sb_sum, (nsb + 1) * sizeof(uint32_t));   // + full flag
   if (e == cudaSuccess) e = cudaMalloc(&c->sel.sb_prefix, nsb * sizeof(uint32_t));
   if (e != cudaSuccess) return set_error(SEL_E_CUDA, cuda_msg("cudaMalloc(selection)", e));
   c->sel_cap_chunks = cap;
@@ -538,6 +540,8 @@ sel_status sel_ctx_create(int cuda_device, sel_ctx* out) {
   c->prefetch_mode = pf ? (std::strcmp(pf, "1") == 0 ? 1 : 0) : -1;
   const char* kv = std::getenv("SEL_KEEP_VALUES");
   c->keep_values = kv && std::strcmp(kv, "1") == 0;
+  const char* ds = std::getenv("SEL_DENSE_SPLIT");
+  c->dense_split = !(ds && std::strcmp(ds, "0") == 0);
   const char* cd = std::getenv("SEL_CODED");
   c->code_enabled = !(cd && std::strcmp(cd, "0") == 0);
   const char* gc = std::getenv("SEL_GRAPH_COMM");
@@ -1106,7 +1110,8 @@ sel_status enqueue_count(sel_table t, const Plan& plan, uint32_t flags, const ui
     if (flags & SEL_KEEP_SELECTION) {
       if (ensure_selection(c, nchunks) != SEL_OK) return g_status;
       const uint64_t nsb = (nchunks + kSbChunks - 1) / kSbChunks;
-      e = cudaMemsetAsync(c->sel.sb_sum, 0, nsb * sizeof(uint32_t), stream);
+      c->sel.full_slot = (uint32_t)nsb;   // the flag word right after this table's sums
+      e = cudaMemsetAsync(c->sel.sb_sum, 0, (nsb + 1) * sizeof(uint32_t), stream);
       if (e != cudaSuccess) return set_error(SEL_E_CUDA, cuda_msg("cudaMemsetAsync(selection)", e));
       c->kept_table = nullptr;  // valid again only once this probe has completed
       c->kept_cols.clear();
@@ -1239,6 +1244,7 @@ sel_status enqueue_pushdown_sel(sel_table t, const Plan& plan, const uint32_t* p
     p->gate = gate ? 1u : 0u;
     p->gate_max = gate_max;
     p->global_out = global_out ? 1u : 0u;
+    p->dense_split = (c->dense_split && n >= kDenseSplitMinRows) ? 1u : 0u;
     p->n_proj = capacity_rows > 0 ? nproj : 0;
     for (uint32_t j = 0; j < p->n_proj; ++j) {
       p->proj_src[j] = t->cols[proj_cols[j]].data;

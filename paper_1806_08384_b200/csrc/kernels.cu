@@ -835,6 +835,7 @@ __device__ __forceinline__ void keep_chunk(const SelectionBufs& sb, uint64_t c, 
   }
   if (lane == 0) {
     sb.chunk_cnt[c] = (uint16_t)cc;
+    if (cc == (uint32_t)kChunkRows) sb.sb_sum[sb.full_slot] = 1u;   // dense_chunks_kernel has work
 #if SEL_SB_ATOMICS
     if (cc) atomicAdd(&sb.sb_sum[c >> kSbShift], cc);
 #endif
@@ -1239,6 +1240,14 @@ __global__ void __launch_bounds__(kThreads, SEL_PD_MINB) pushdown_sel_kernel(con
     for (int g = 0; g < kBlockChunks; ++g) {
       const uint32_t cg = __shfl_sync(0xFFFFFFFFu, cntv, g);
       if (cg == 0) continue;
+      if (!CODED && p.dense_split && cg == kChunkRows && gbase + staged + kChunkRows <= p.capacity) {
+        __syncwarp();   // a full chunk is copied whole by dense_chunks_kernel: skip its positions
+        flush_rows<CODED>(p, bbase, gbase, staged, my, lane, out_ids);
+        __syncwarp();
+        gbase += staged + kChunkRows;
+        staged = 0;
+        continue;
+      }
       if (staged + cg > kStageCap) {
         __syncwarp();
         flush_rows<CODED>(p, bbase, gbase, staged, my, lane, out_ids);
@@ -1259,6 +1268,86 @@ __global__ void __launch_bounds__(kThreads, SEL_PD_MINB) pushdown_sel_kernel(con
   }
 }
 
+
+// ---- fully selected chunks: whole-chunk copies beside the push-down ---------------------------
+// Dense selections and clustered layouts select whole 1024-row chunks; pushdown_sel leaves those
+// (p.dense_split) to this kernel: ids are a run, gathered projections are copies with 16-byte
+// loads (8 in flight per lane; the chunk is 16-byte aligned) and coalesced stores at the output
+// position (which need not be aligned); kept slots and constants as in copy_kept. Its own
+// kernel, so that the 32-register push-down kernel does not carry the copy's registers.
+template <class T>
+__device__ __forceinline__ void copy_chunk(const void* src_v, void* dst_v, uint64_t cbase,
+                                           uint64_t gbase, int lane) {
+  constexpr int PER = 16 / sizeof(T);
+  constexpr int N16 = kChunkRows * sizeof(T) / 16;
+  const uint4* src = reinterpret_cast<const uint4*>(static_cast<const T*>(src_v) + cbase);
+  T* __restrict__ dst = static_cast<T*>(dst_v) + gbase;
+#pragma unroll 1
+  for (int h = 0; h < (N16 + 255) / 256; ++h) {
+    uint4 v[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int k = h * 256 + i * 32 + lane;
+      if (k < N16) v[i] = ld_stream_v4(src + k);
+    }
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int k = h * 256 + i * 32 + lane;
+      if (k < N16) {
+        const T* e = reinterpret_cast<const T*>(&v[i]);
+#pragma unroll
+        for (int j = 0; j < PER; ++j) dst[(uint64_t)k * PER + j] = e[j];
+      }
+    }
+  }
+}
+
+template <class P>
+__global__ void __launch_bounds__(kThreads) dense_chunks_kernel(const __grid_constant__ P p,
+                                                                uint64_t n, SelectionBufs sb,
+                                                                uint32_t* __restrict__ out_ids,
+                                                                const uint64_t* __restrict__ gate_count) {
+  if (p.gate && *gate_count > p.gate_max) return;  // Algorithm 1's "throw": nothing written
+  if (sb.sb_sum[sb.full_slot] == 0u) return;        // the count saw no fully selected chunk
+  const uint64_t goff = p.global_out ? gate_count[kOffsetSlot - kGateSlot] : 0ull;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const uint64_t nchunks = (n + kChunkRows - 1) / kChunkRows;
+  const uint64_t nblocks = (nchunks + kBlockChunks - 1) / kBlockChunks;
+  const uint64_t gw = (uint64_t)blockIdx.x * kWarpsPerCta + warp;
+  const uint64_t nw = (uint64_t)gridDim.x * kWarpsPerCta;
+  for (uint64_t blk = gw; blk < nblocks; blk += nw) {
+    const uint64_t c0 = blk * kBlockChunks;
+    const uint32_t cntv = (lane < kBlockChunks && c0 + lane < nchunks) ? sb.chunk_cnt[c0 + lane] : 0u;
+    if (!__ballot_sync(0xFFFFFFFFu, cntv == (uint32_t)kChunkRows && lane < kBlockChunks)) continue;
+    const uint64_t first = (c0 >> kSbShift) << kSbShift;
+    uint32_t part = 0;
+    if (first + lane < c0) part += sb.chunk_cnt[first + lane];
+    if (first + 32 + lane < c0) part += sb.chunk_cnt[first + 32 + lane];
+    uint64_t gbase = goff + (uint64_t)sb.sb_prefix[c0 >> kSbShift] + __reduce_add_sync(0xFFFFFFFFu, part);
+#pragma unroll 1
+    for (int g = 0; g < kBlockChunks; ++g) {
+      const uint32_t cg = __shfl_sync(0xFFFFFFFFu, cntv, g);
+      if (cg == (uint32_t)kChunkRows && gbase + kChunkRows <= p.capacity) {
+        const uint64_t c = c0 + g, cbase = c * kChunkRows;
+        const uint32_t idbase = (uint32_t)(p.row_offset + cbase);
+#pragma unroll 8
+        for (uint32_t q = lane; q < (uint32_t)kChunkRows; q += 32) out_ids[gbase + q] = idbase + q;
+        if (p.n_direct) copy_kept(p, sb, c, gbase, kChunkRows, lane);   // kept slots / constants
+#pragma unroll 1
+        for (uint32_t j = 0; j < p.n_proj; ++j) {
+          if (p.proj_cap_off[j] != kNoCapture) continue;
+          switch (p.proj_wclass[j]) {
+            case W1: copy_chunk<uint8_t>(p.proj_src[j], p.proj_dst[j], cbase, gbase, lane); break;
+            case W2: copy_chunk<uint16_t>(p.proj_src[j], p.proj_dst[j], cbase, gbase, lane); break;
+            case W4: copy_chunk<uint32_t>(p.proj_src[j], p.proj_dst[j], cbase, gbase, lane); break;
+            default: copy_chunk<uint64_t>(p.proj_src[j], p.proj_dst[j], cbase, gbase, lane); break;
+          }
+        }
+      }
+      gbase += cg;
+    }
+  }
+}
 
 // ---- batch of programs over one scan -------------------------------------
 // Every column of the batch is loaded once per chunk; each distinct leaf on it is evaluated once
@@ -1477,6 +1566,9 @@ int launch_pushdown_sel_small(const DevProgramSmall& p, uint64_t n, uint32_t* ou
   else
     pushdown_sel_kernel<DevProgramSmall, false><<<grid, kThreads, 0, (cudaStream_t)st>>>(p, n, sb, out_ids,
                                                                                 s.result + kGateSlot);
+  if (p.dense_split && !p.coded)
+    dense_chunks_kernel<DevProgramSmall><<<grid, kThreads, 0, (cudaStream_t)st>>>(p, n, sb, out_ids,
+                                                                     s.result + kGateSlot);
   return (int)cudaGetLastError();
 }
 int launch_pushdown_sel_large(const DevProgramLarge& p, uint64_t n, uint32_t* out_ids, int grid,
@@ -1497,6 +1589,9 @@ int launch_pushdown_sel_large(const DevProgramLarge& p, uint64_t n, uint32_t* ou
   else
     pushdown_sel_kernel<DevProgramLarge, false><<<grid, kThreads, 0, (cudaStream_t)st>>>(p, n, sb, out_ids,
                                                                                 s.result + kGateSlot);
+  if (p.dense_split && !p.coded)
+    dense_chunks_kernel<DevProgramLarge><<<grid, kThreads, 0, (cudaStream_t)st>>>(p, n, sb, out_ids,
+                                                                     s.result + kGateSlot);
   return (int)cudaGetLastError();
 }
 int launch_pushdown_small(const DevProgramSmall& p, uint64_t n, uint32_t* out_ids, int grid,

@@ -83,6 +83,8 @@ struct DevProgramT {
                          // kLeafStaged; offset = span[iv_begin] >> 32), 0 = none
   uint32_t n_direct;     // push-down from a selection: projections that are kept or constant
   uint32_t coded;        // push-down from a selection: a projection is kCodedProj
+  uint32_t dense_split;  // push-down from a selection: fully selected chunks are left to
+                         // dense_chunks_kernel (whole-chunk copies)
   uint32_t global_out;   // push-down from a selection: the outputs are the GLOBAL result
                          // (sel_execute_to): positions start at Scratch::result[kOffsetSlot]
   // Count kernel fast path (template-specialised conjunctive forms): when
@@ -166,6 +168,8 @@ struct SelectionBufs {
   uint16_t* chunk_cnt;   // [nchunks]
   uint32_t* sb_sum;      // [nsb], zeroed before the count
   uint32_t* sb_prefix;   // [nsb]
+  uint32_t full_slot;    // sb_sum[full_slot] (= nsb): nonzero once the count saw a fully
+                         // selected chunk (dense_chunks_kernel has work)
   // Kept values of projected predicate columns: chunk c's selected values, compacted in row
   // order, at keep_slot[k] + c * 1024 * width (written by the count, copied by the push-down).
   uint32_t n_keep;

@@ -517,3 +517,32 @@ def test_count_async_and_user_graph_capture(ctx, cuda_device):
     e.count_async(encode(Cmp("=", 0, 1), [INT32]), o)
     torch.cuda.synchronize()
     assert int(o) == 0
+
+
+def test_fully_selected_chunks_dense_copy(ctx):
+    """Tables of >= 8M rows leave fully selected 1024-row chunks to the whole-chunk copy kernel
+    (dense_chunks_kernel) beside the push-down: clustered and dense selections, full chunks next
+    to partial ones and a ragged tail, kept/constant projections, capacity cuts inside and at a
+    full chunk; every materialisation path vs the oracle."""
+    rng = np.random.default_rng(88)
+    n = 12_000_037
+    x = np.arange(n, dtype=np.int32)
+    y = rng.integers(-(1 << 31), (1 << 31) - 1, n, dtype=np.int64).astype(np.int32)
+    z = (np.arange(n) % 7).astype(np.uint8)
+    types = [INT32, INT32, DICT8]
+    cols = [x, y, z]
+    t = register(ctx, cols, types)
+    for node in [Cmp("<", 0, 9_000_123), Cmp(">=", 0, 3_000_000),
+                 And(Cmp("<", 0, 9_000_123), Cmp(">", 1, 0)),
+                 Or(Cmp("<", 0, 2_048_000), Cmp(">", 1, 2_000_000_000)),
+                 And(Cmp(">=", 0, 1_000_000), Cmp("=", 2, 3))]:
+        check_parity(t, cols, types, node, proj=[1, 2, 0])
+    prog = encode(Cmp("<", 0, 9_000_123), types)
+    for cap in (4_096, 5_000, 1_000_000):            # a capacity cut at / inside a full chunk
+        want_c, want_ids, _ = oracle.pushdown(cols, types, prog, capacity=cap)
+        t.count(prog, keep_selection=True)
+        r = t.pushdown(prog, project=[1], capacity=cap)
+        assert r.count == want_c and r.gated
+        np.testing.assert_array_equal(r.rowids.cpu().numpy().view(np.uint32), want_ids)
+        np.testing.assert_array_equal(r.columns[1].cpu().numpy(), y[want_ids])
+    t.release()
