@@ -799,9 +799,10 @@ __device__ __forceinline__ void st_evict_last(uint32_t* p, uint32_t v) {
 
 // coded: also keep the coded leaf's point-1 matches (wm, the count's quad layout) row-major.
 template <class P, bool KEEP>
-__device__ __forceinline__ void keep_chunk(const SelectionBufs& sb, uint64_t c, int lane, uint32_t m,
-                                           char* wsmem, uint32_t wm = 0u, bool coded = false) {
-  if (!KEEP) return;
+// Returns the chunk's selected-row count (every lane; 0 without KEEP).
+__device__ __forceinline__ uint32_t keep_chunk(const SelectionBufs& sb, uint64_t c, int lane, uint32_t m,
+                                               char* wsmem, uint32_t wm = 0u, bool coded = false) {
+  if (!KEEP) return 0u;
   if (coded) st_evict_last(sb.which + c * 32 + lane, to_row_major(wm, lane));
   const uint32_t t = to_row_major(m, lane);          // the push-down stages from row-major masks
   if (sb.n_keep) {
@@ -835,11 +836,11 @@ __device__ __forceinline__ void keep_chunk(const SelectionBufs& sb, uint64_t c, 
   }
   if (lane == 0) {
     sb.chunk_cnt[c] = (uint16_t)cc;
-    if (cc == (uint32_t)kChunkRows) sb.sb_sum[sb.full_slot] = 1u;   // dense_chunks_kernel has work
 #if SEL_SB_ATOMICS
     if (cc) atomicAdd(&sb.sb_sum[c >> kSbShift], cc);
 #endif
   }
+  return cc;
 }
 
 // NW warps per CTA: 8 normally; 32 when staged key sets leave room for one CTA per SM only.
@@ -861,6 +862,7 @@ __global__ void __launch_bounds__(NW * 32, NW == kWarpsPerCta ? (FASTN ? SEL_FAS
   extern __shared__ __align__(16) char s_dyn[];
   char* wsmem = KEEP ? s_dyn + (size_t)warp * sb.warp_smem : nullptr;
   uint32_t cnt = 0;
+  bool full = false;   // this warp kept a fully selected chunk (raises the flag once, below)
   // Stage the program's key sets in shared memory (after the warps' areas), once per CTA.
   uint32_t bm_sbase = kNoStage;
   if (p.bm_smem) {
@@ -892,7 +894,7 @@ __global__ void __launch_bounds__(NW * 32, NW == kWarpsPerCta ? (FASTN ? SEL_FAS
       uint32_t wm = 0;
       const uint32_t m = eval_fast<FASTN, KEEP>(p, c * kChunkRows, lane, wsmem, &wm);
       cnt += __popc(m);
-      keep_chunk<P, KEEP>(sb, c, lane, m, wsmem, wm, KEEP && p.fast_code >= 0);
+      full |= keep_chunk<P, KEEP>(sb, c, lane, m, wsmem, wm, KEEP && p.fast_code >= 0) == kChunkRows;
     }
   } else {
     if (lane == 0 && p.prefetch && gw < ns_full) prefetch_chunk(p, phase + gw * stride);
@@ -901,7 +903,7 @@ __global__ void __launch_bounds__(NW * 32, NW == kWarpsPerCta ? (FASTN ? SEL_FAS
       if (lane == 0 && p.prefetch && s + nw < ns_full) prefetch_chunk(p, c + nw * stride);
       const uint32_t m = eval_program<false, KEEP>(p, c * kChunkRows, lane, kChunkRows, wsmem, bm_sbase);
       cnt += __popc(m);
-      keep_chunk<P, KEEP>(sb, c, lane, m, wsmem);
+      full |= keep_chunk<P, KEEP>(sb, c, lane, m, wsmem) == kChunkRows;
     }
   }
   if (tail_sampled && gw == ns_full % nw) {
@@ -915,8 +917,11 @@ __global__ void __launch_bounds__(NW * 32, NW == kWarpsPerCta ? (FASTN ? SEL_FAS
       const uint32_t pt1 = w4 ? (uint32_t)p.lo[p.leaf[s].iv_begin + 1] : (p.fast_pts[s][1] & 0xFFu);
       wm = which_tail(p.col[p.leaf[s].slot], nfull * kChunkRows, lane, rem, pt1, w4);
     }
-    keep_chunk<P, KEEP>(sb, nfull, lane, m, wsmem, wm, coded);
+    keep_chunk<P, KEEP>(sb, nfull, lane, m, wsmem, wm, coded);   // a tail chunk is never full
   }
+  // dense_chunks_kernel has work: one store per warp (one per chunk contended on the word: C5 at
+  // s = 1 count 0.62 -> 1.36 ms)
+  if (KEEP && full && lane == 0) sb.sb_sum[sb.full_slot] = 1u;
   cnt = __reduce_add_sync(0xFFFFFFFFu, cnt);
 
   __shared__ uint32_t s_warp[NW];
