@@ -713,7 +713,11 @@ def run_ours(args):
             "pushdown_path": pd_path,
             "clocks": clk.summary(),
             "e2e": e2e,
-            "gpu_launches": (3 if pd_path == 1 else 2) * args.steps,
+            # count + push-down (+ the superblock prefix on the selection path, + the whole-chunk
+            # copy on uncoded selection push-downs of >= 8 Mi local rows: DESIGN.md §5)
+            "gpu_launches": ((3 + int(not coded and (e - s) >= (8 << 20)
+                                      and os.environ.get("SEL_DENSE_SPLIT", "1") != "0"))
+                             if pd_path == 1 else 2) * args.steps,
             "cpu_baseline": cpu,
         }
         emit(line)
