@@ -1276,33 +1276,44 @@ __global__ void __launch_bounds__(kThreads, SEL_PD_MINB) pushdown_sel_kernel(con
 
 // ---- fully selected chunks: whole-chunk copies beside the push-down ---------------------------
 // Dense selections and clustered layouts select whole 1024-row chunks; pushdown_sel leaves those
-// (p.dense_split) to this kernel: ids are a run, gathered projections are copies with 16-byte
-// loads (8 in flight per lane; the chunk is 16-byte aligned) and coalesced stores at the output
-// position (which need not be aligned); kept slots and constants as in copy_kept. Its own
+// (p.dense_split) to this kernel: ids are a run, gathered projections are copies (8 loads in
+// flight per lane; 16-byte loads and stores when the output position is 16-byte aligned, else
+// element-wise); kept slots and constants as in copy_kept. Its own
 // kernel, so that the 32-register push-down kernel does not carry the copy's registers.
 template <class T>
 __device__ __forceinline__ void copy_chunk(const void* src_v, void* dst_v, uint64_t cbase,
                                            uint64_t gbase, int lane) {
-  constexpr int PER = 16 / sizeof(T);
-  constexpr int N16 = kChunkRows * sizeof(T) / 16;
-  const uint4* src = reinterpret_cast<const uint4*>(static_cast<const T*>(src_v) + cbase);
   T* __restrict__ dst = static_cast<T*>(dst_v) + gbase;
+  if ((reinterpret_cast<uintptr_t>(dst) & 15u) == 0) {
+    // output position 16-byte aligned (every full chunk of a run of them): 16-byte stores too
+    constexpr int N16 = kChunkRows * sizeof(T) / 16;
+    const uint4* src = reinterpret_cast<const uint4*>(static_cast<const T*>(src_v) + cbase);
+    uint4* d4 = reinterpret_cast<uint4*>(dst);
 #pragma unroll 1
-  for (int h = 0; h < (N16 + 255) / 256; ++h) {
-    uint4 v[8];
+    for (int h = 0; h < (N16 + 255) / 256; ++h) {
+      uint4 v[8];
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      const int k = h * 256 + i * 32 + lane;
-      if (k < N16) v[i] = ld_stream_v4(src + k);
-    }
-#pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      const int k = h * 256 + i * 32 + lane;
-      if (k < N16) {
-        const T* e = reinterpret_cast<const T*>(&v[i]);
-#pragma unroll
-        for (int j = 0; j < PER; ++j) dst[(uint64_t)k * PER + j] = e[j];
+      for (int i = 0; i < 8; ++i) {
+        const int k = h * 256 + i * 32 + lane;
+        if (k < N16) v[i] = ld_stream_v4(src + k);
       }
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const int k = h * 256 + i * 32 + lane;
+        if (k < N16) d4[k] = v[i];
+      }
+    }
+  } else {
+    // unaligned output: element-wise, both sides coalesced (16-byte loads with 4-byte-strided
+    // stores touched every store sector PER times: 2.5x the written sectors in ncu)
+    const T* __restrict__ src = static_cast<const T*>(src_v) + cbase;
+#pragma unroll 1
+    for (int h = 0; h < kChunkRows; h += 256) {
+      T v[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) v[i] = __ldcs(src + h + i * 32 + lane);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) dst[h + i * 32 + lane] = v[i];
     }
   }
 }

@@ -1,7 +1,9 @@
 """BASELINE.json config 5: the selectivity sweep 1e-6 .. 1.0 on the 1e9-row table, count vs
 push-down compaction cost, scattered (x = (a i + b) mod N) and clustered (x = i)
 layouts. Per selectivity: the Execute step (count keeping the selection -> materialise ids + y),
-the kernel times, and the closed-form count check (count(x < t) = t). One JSON line per point."""
+the kernel times, and the closed-form count check (count(x < t) = t). One JSON line per point.
+Env: ROWS, SWEEP_LAYOUTS="scattered,clustered", SWEEP_S="1e-6,...,1.0", SWEEP_EAGER=1 (execute()
+calls instead of the prepared graph, for ncu: scripts/profile.sh notes why)."""
 import json
 import os
 import statistics
@@ -14,19 +16,40 @@ import paper_1806_08384_b200 as sel  # noqa: E402
 from selgen import configs, encode  # noqa: E402
 
 
+class _Eager:
+    """The prepared execute's run()/release() through plain execute() calls."""
+
+    def __init__(self, t, prog, n, out):
+        self.t, self.prog, self.n, self.out = t, prog, n, out
+
+    def run(self):
+        return self.t.execute(self.prog, project=["y"], max_size=self.n, capacity=self.n,
+                              out=self.out).count
+
+    def release(self):
+        pass
+
+
 def main():
     dev = torch.device("cuda:0")
     n = int(os.environ.get("ROWS", configs.C5_ROWS))
     ctx = sel.Context(dev)
-    for layout in ("scattered", "clustered"):
+    layouts = os.environ.get("SWEEP_LAYOUTS", "scattered,clustered").split(",")
+    sels = [float(x) for x in os.environ.get("SWEEP_S", "1e-6,1e-5,1e-4,1e-3,1e-2,0.1,0.5,1.0").split(",")]
+    eager = os.environ.get("SWEEP_EAGER") == "1"
+    for layout in layouts:
         T = configs.gen_sweep(n, device=dev, layout=layout)
         t = sel.Table(ctx, ["x", "y"], T.types, [c.data for c in T.columns])
         out_ids = torch.empty(n, dtype=torch.int32, device=dev)
         out_y = torch.empty(n, dtype=torch.int32, device=dev)
-        for s in (1e-6, 1e-5, 1e-4, 1e-3, 1e-2, 0.1, 0.5, 1.0):
+        for s in sels:
             thr = configs.sweep_threshold(n, s)
             prog = encode(configs.sweep_probe(thr), T.types)
-            q = t.prepare_execute(prog, project=["y"], max_size=n, capacity=n, out=(out_ids, [out_y]))
+            if eager:
+                q = _Eager(t, prog, n, (out_ids, [out_y]))
+            else:
+                q = t.prepare_execute(prog, project=["y"], max_size=n, capacity=n,
+                                      out=(out_ids, [out_y]))
             for _ in range(3):
                 q.run()
             torch.cuda.synchronize()

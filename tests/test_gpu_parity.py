@@ -535,7 +535,9 @@ def test_fully_selected_chunks_dense_copy(ctx):
     for node in [Cmp("<", 0, 9_000_123), Cmp(">=", 0, 3_000_000),
                  And(Cmp("<", 0, 9_000_123), Cmp(">", 1, 0)),
                  Or(Cmp("<", 0, 2_048_000), Cmp(">", 1, 2_000_000_000)),
-                 And(Cmp(">=", 0, 1_000_000), Cmp("=", 2, 3))]:
+                 And(Cmp(">=", 0, 1_000_000), Cmp("=", 2, 3)),
+                 # scattered rows first: the full chunks after them land at unaligned positions
+                 Or(Cmp(">", 1, 2_000_000_000), Cmp(">=", 0, 6_000_000))]:
         check_parity(t, cols, types, node, proj=[1, 2, 0])
     prog = encode(Cmp("<", 0, 9_000_123), types)
     for cap in (4_096, 5_000, 1_000_000):            # a capacity cut at / inside a full chunk
