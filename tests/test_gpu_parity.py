@@ -522,8 +522,8 @@ def test_count_async_and_user_graph_capture(ctx, cuda_device):
 def test_fully_selected_chunks_dense_copy(ctx):
     """Tables of >= 8M rows leave fully selected 1024-row chunks to the whole-chunk copy kernel
     (dense_chunks_kernel) beside the push-down: clustered and dense selections, full chunks next
-    to partial ones and a ragged tail, kept/constant projections, capacity cuts inside and at a
-    full chunk; every materialisation path vs the oracle."""
+    to partial and dense-not-full ones and a ragged tail, kept/constant projections, capacity cuts
+    inside and at a full chunk; every materialisation path vs the oracle."""
     rng = np.random.default_rng(88)
     n = 12_000_037
     x = np.arange(n, dtype=np.int32)
@@ -537,10 +537,15 @@ def test_fully_selected_chunks_dense_copy(ctx):
                  Or(Cmp("<", 0, 2_048_000), Cmp(">", 1, 2_000_000_000)),
                  And(Cmp(">=", 0, 1_000_000), Cmp("=", 2, 3)),
                  # scattered rows first: the full chunks after them land at unaligned positions
-                 Or(Cmp(">", 1, 2_000_000_000), Cmp(">=", 0, 6_000_000))]:
+                 Or(Cmp(">", 1, 2_000_000_000), Cmp(">=", 0, 6_000_000)),
+                 # dense, not full chunks; 8-byte-free mix of widths; the ragged tail dense
+                 Cmp(">", 1, -1_500_000_000), Cmp("<", 1, 0),
+                 And(Cmp(">=", 0, 11_000_000), Not(Cmp("=", 2, 5)))]:
         check_parity(t, cols, types, node, proj=[1, 2, 0])
-    prog = encode(Cmp("<", 0, 9_000_123), types)
-    for cap in (4_096, 5_000, 1_000_000):            # a capacity cut at / inside a full chunk
+    for node, cap in [(Cmp("<", 0, 9_000_123), c) for c in (4_096, 5_000, 1_000_000)] + \
+                     [(Cmp(">", 1, -1_500_000_000), c) for c in (4_000, 5_000, 777_777)]:
+        # a capacity cut at / inside a full (then a dense) chunk
+        prog = encode(node, types)
         want_c, want_ids, _ = oracle.pushdown(cols, types, prog, capacity=cap)
         t.count(prog, keep_selection=True)
         r = t.pushdown(prog, project=[1], capacity=cap)
