@@ -413,6 +413,22 @@ int sel_abi_version(void);
  * Maximum program size: 12 + 8 * (128 + 512) = 5,132 bytes.
  */
 
+/*
+ * Environment (read once, by sel_ctx_create; for A/B measurement and diagnosis — none of them
+ * changes a result, only which kernel variant or launch shape produces it; DESIGN.md §5-§7
+ * gives the measurements behind each default):
+ *   SEL_FAST=0               conjunctions through the postfix interpreter, not the fast path
+ *   SEL_CODED=0              no coded projections (two-point columns read by the push-down)
+ *   SEL_DENSE_SPLIT=0        no whole-chunk copy kernel for fully selected chunks
+ *   SEL_KEEP_VALUES=1        the keeping count also keeps projected predicate columns' values
+ *   SEL_PREFETCH=0|1         force the count's L2 bulk prefetch of the next chunk off / on
+ *   SEL_GRAPH_COMM=0         no cross-rank collective inside prepared (graph) executes
+ *   SEL_PUSHDOWN_PATH=single|two   sel_pushdown always single-pass / always two passes
+ *   SEL_TWO_PASS_MIN_ROWS=n  shard size from which sel_pushdown takes two passes (3*2^20)
+ *   SEL_COUNT_NW=8           8-warp count CTAs even when staged key sets allow 32
+ *   SEL_CTAS_PER_SM=k        cap the count kernels' resident CTAs per SM (grid = 148 * k)
+ */
+
 #ifdef __cplusplus
 }
 #endif
