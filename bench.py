@@ -714,8 +714,8 @@ def run_ours(args):
             "clocks": clk.summary(),
             "e2e": e2e,
             # count + push-down (+ the superblock prefix on the selection path, + the whole-chunk
-            # copy on uncoded selection push-downs of >= 8 Mi local rows: DESIGN.md §5)
-            "gpu_launches": ((3 + int(not coded and (e - s) >= (8 << 20)
+            # copy on selection push-downs of >= 8 Mi local rows: DESIGN.md §5)
+            "gpu_launches": ((3 + int((e - s) >= (8 << 20)
                                       and os.environ.get("SEL_DENSE_SPLIT", "1") != "0"))
                              if pd_path == 1 else 2) * args.steps,
             "cpu_baseline": cpu,

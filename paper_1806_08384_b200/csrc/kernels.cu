@@ -1245,7 +1245,7 @@ __global__ void __launch_bounds__(kThreads, SEL_PD_MINB) pushdown_sel_kernel(con
     for (int g = 0; g < kBlockChunks; ++g) {
       const uint32_t cg = __shfl_sync(0xFFFFFFFFu, cntv, g);
       if (cg == 0) continue;
-      if (!CODED && p.dense_split && cg == kChunkRows && gbase + staged + kChunkRows <= p.capacity) {
+      if (p.dense_split && cg == kChunkRows && gbase + staged + kChunkRows <= p.capacity) {
         __syncwarp();   // a full chunk is copied whole by dense_chunks_kernel: skip its positions
         flush_rows<CODED>(p, bbase, gbase, staged, my, lane, out_ids);
         __syncwarp();
@@ -1351,6 +1351,28 @@ __global__ void __launch_bounds__(kThreads) dense_chunks_kernel(const __grid_con
         if (p.n_direct) copy_kept(p, sb, c, gbase, kChunkRows, lane);   // kept slots / constants
 #pragma unroll 1
         for (uint32_t j = 0; j < p.n_proj; ++j) {
+          if (p.proj_cap_off[j] == kCodedProj) {
+            // the value from each row's code bit (the keeping count's row-major word: bit b of
+            // word L = row 32L + b), as flush_rows does for staged rows; the column is not read
+            const uint64_t pts = (uint64_t)(uintptr_t)p.proj_src[j];
+            const uint32_t wl = sb.which[c * 32 + lane];
+            if (p.proj_wclass[j] == W1) {
+              uint8_t* __restrict__ dst = static_cast<uint8_t*>(p.proj_dst[j]) + gbase;
+#pragma unroll 8
+              for (int i = 0; i < 32; ++i) {
+                const uint32_t w = __shfl_sync(0xFFFFFFFFu, wl, i);
+                dst[32 * i + lane] = (uint8_t)(pts >> (((w >> lane) & 1u) ? 8 : 0));
+              }
+            } else {
+              uint32_t* __restrict__ dst = static_cast<uint32_t*>(p.proj_dst[j]) + gbase;
+#pragma unroll 8
+              for (int i = 0; i < 32; ++i) {
+                const uint32_t w = __shfl_sync(0xFFFFFFFFu, wl, i);
+                dst[32 * i + lane] = (uint32_t)(pts >> (((w >> lane) & 1u) ? 32 : 0));
+              }
+            }
+            continue;
+          }
           if (p.proj_cap_off[j] != kNoCapture) continue;
           switch (p.proj_wclass[j]) {
             case W1: copy_chunk<uint8_t>(p.proj_src[j], p.proj_dst[j], cbase, gbase, lane); break;
@@ -1582,7 +1604,7 @@ int launch_pushdown_sel_small(const DevProgramSmall& p, uint64_t n, uint32_t* ou
   else
     pushdown_sel_kernel<DevProgramSmall, false><<<grid, kThreads, 0, (cudaStream_t)st>>>(p, n, sb, out_ids,
                                                                                 s.result + kGateSlot);
-  if (p.dense_split && !p.coded)
+  if (p.dense_split)
     dense_chunks_kernel<DevProgramSmall><<<grid, kThreads, 0, (cudaStream_t)st>>>(p, n, sb, out_ids,
                                                                      s.result + kGateSlot);
   return (int)cudaGetLastError();
@@ -1605,7 +1627,7 @@ int launch_pushdown_sel_large(const DevProgramLarge& p, uint64_t n, uint32_t* ou
   else
     pushdown_sel_kernel<DevProgramLarge, false><<<grid, kThreads, 0, (cudaStream_t)st>>>(p, n, sb, out_ids,
                                                                                 s.result + kGateSlot);
-  if (p.dense_split && !p.coded)
+  if (p.dense_split)
     dense_chunks_kernel<DevProgramLarge><<<grid, kThreads, 0, (cudaStream_t)st>>>(p, n, sb, out_ids,
                                                                      s.result + kGateSlot);
   return (int)cudaGetLastError();

@@ -553,3 +553,37 @@ def test_fully_selected_chunks_dense_copy(ctx):
         np.testing.assert_array_equal(r.rowids.cpu().numpy().view(np.uint32), want_ids)
         np.testing.assert_array_equal(r.columns[1].cpu().numpy(), y[want_ids])
     t.release()
+
+
+def test_fully_selected_chunks_coded(ctx):
+    """Coded projections (a conjunction pins the projected column to two values: an IN of two
+    points on a 1- or 4-byte column; the keeping count keeps one code bit per row) through the
+    whole-chunk copy: full chunks take each row's value from its code bit in dense_chunks_kernel,
+    partial ones in the push-down's staging; capacity cuts at and inside a full chunk."""
+    rng = np.random.default_rng(89)
+    n = 12_000_037
+    x = np.arange(n, dtype=np.int32)
+    z = rng.integers(0, 7, n).astype(np.uint8)
+    z[:6_000_000] = rng.choice(np.array([1, 4], np.uint8), 6_000_000)
+    w = rng.integers(-(1 << 31), (1 << 31) - 1, n, dtype=np.int64).astype(np.int32)
+    w[2_000_000:10_000_000] = rng.choice(np.array([-5, 100_000], np.int32), 8_000_000)
+    types = [INT32, DICT8, INT32]
+    cols = [x, z, w]
+    t = register(ctx, cols, types)
+    plan_cases = [(And(Cmp("<", 0, 9_000_123), In(1, (1, 4))), [1, 2, 0]),
+                  (And(In(2, (-5, 100_000)), Cmp(">=", 0, 1_000_000)), [2, 1]),
+                  (In(1, (4, 1)), [1]),
+                  (And(In(1, (1, 4)), In(2, (100_000, -5))), [2, 0, 1])]
+    for node, proj in plan_cases:
+        check_parity(t, cols, types, node, proj=proj)
+    node = And(Cmp("<", 0, 9_000_123), In(1, (1, 4)))
+    prog = encode(node, types)
+    for cap in (4_096, 5_000, 1_000_000):
+        want_c, want_ids, _ = oracle.pushdown(cols, types, prog, capacity=cap)
+        t.count(prog, keep_selection=True)
+        r = t.pushdown(prog, project=[1, 0], capacity=cap)
+        assert r.count == want_c and r.gated
+        np.testing.assert_array_equal(r.rowids.cpu().numpy().view(np.uint32), want_ids)
+        np.testing.assert_array_equal(r.columns[1].cpu().numpy(), z[want_ids])
+        np.testing.assert_array_equal(r.columns[0].cpu().numpy(), x[want_ids])
+    t.release()
