@@ -62,6 +62,10 @@ def _load():
         L.oracle_count_bm.restype = u64
         L.oracle_count_bm.argtypes = [vp, vp, ctypes.c_uint32, u64, ctypes.c_char_p, sz, vp, vp,
                                       ctypes.c_uint32, ip]
+        L.oracle_pushdown_mt_bm.restype = u64
+        L.oracle_pushdown_mt_bm.argtypes = [vp, vp, ctypes.c_uint32, u64, ctypes.c_char_p, sz, vp,
+                                            ctypes.c_uint32, u64, vp, vp, u64, ctypes.c_int, vp,
+                                            vp, ctypes.c_uint32, ip]
         L.oracle_pushdown_bm.restype = u64
         L.oracle_pushdown_bm.argtypes = [vp, vp, ctypes.c_uint32, u64, ctypes.c_char_p, sz, vp,
                                          ctypes.c_uint32, u64, vp, vp, u64, vp, vp,
@@ -153,3 +157,30 @@ def pushdown(columns: Sequence, types: Sequence[int], prog: bytes, proj: Sequenc
         raise OracleError(st.value)
     k = min(int(r), cap)
     return int(r), ids[:k].copy(), [o[:k].copy() for o in outs]
+
+
+def pushdown_mt(columns: Sequence, types: Sequence[int], prog: bytes, proj: Sequence[int] = (),
+                capacity: int | None = None, row_offset: int = 0, bitmaps=None,
+                nthreads: int | None = None):
+    """The same result as pushdown(), computed over contiguous row shards on `nthreads` host
+    threads and concatenated in shard order (oracle.c oracle_pushdown_mt_bm); for checking whole
+    full-size tables. Pinned equal to pushdown() in tests/test_oracle_pins.py."""
+    arrs, ptrs, tys = _marshal(columns, types)
+    n = len(arrs[0]) if arrs else 0
+    nthreads = int(nthreads or os.cpu_count() or 1)
+    st = ctypes.c_int(0)
+    keep, wp, nb, k = _bitmaps(bitmaps)
+    cnt = count_mt(columns, types, prog, nthreads, bitmaps=bitmaps)
+    cap = cnt if capacity is None else min(int(capacity), cnt)
+    ids = np.empty(max(cap, 1), dtype=np.uint32)
+    outs = [np.empty(max(cap, 1), dtype=_NP[types[j]]) for j in proj]
+    optrs = (ctypes.c_void_p * max(len(outs), 1))(*[o.ctypes.data for o in outs])
+    pj = np.asarray(list(proj), dtype=np.uint32)
+    r = _load().oracle_pushdown_mt_bm(ptrs, tys.ctypes.data, len(arrs), n, prog, len(prog),
+                                      pj.ctypes.data if len(pj) else None, len(pj), row_offset,
+                                      ids.ctypes.data, optrs, cap, nthreads, wp, nb.ctypes.data,
+                                      k, ctypes.byref(st))
+    if st.value != 0:
+        raise OracleError(st.value)
+    assert int(r) == cnt
+    return int(r), ids[:cap], [o[:cap] for o in outs]

@@ -440,3 +440,113 @@ uint64_t oracle_count_mt(const void* const* cols, const int32_t* types, uint32_t
                          int* status) {
   return oracle_count_mt_bm(cols, types, ncols, n, prog, len, nthreads, NULL, NULL, 0, status);
 }
+
+/* Row-sharded push-down over `nthreads` POSIX threads, so that whole full-size tables can be
+ * checked in a test (tests/test_gpu_fullsize.py). It is the plain definition applied to
+ * contiguous shards and concatenated — nothing else:
+ *   1. shard t = rows [n*t/T, n*(t+1)/T); its count c_t = oracle_count_bm over the shard;
+ *   2. o_t = c_0 + ... + c_{t-1} (the shard's position in the ascending result);
+ *   3. shard t runs oracle_pushdown_bm over its rows with row ids offset by its first row, writing
+ *      output positions [o_t, o_t + c_t) truncated at `capacity` (Algorithm 1's gate).
+ * Because shards are contiguous and each shard's ids ascend, the concatenation is exactly the
+ * single-threaded oracle_pushdown's result (pinned equal in tests/test_oracle_pins.py). */
+typedef struct {
+  const void* const* cols;
+  const int32_t* types;
+  uint32_t ncols;
+  uint64_t begin, end;
+  const uint8_t* prog;
+  size_t len;
+  const uint32_t* proj;
+  uint32_t nproj;
+  uint64_t row_offset;
+  uint32_t* out_ids;       /* already shifted to the shard's output position */
+  void** out_cols;         /* already shifted */
+  uint64_t capacity;       /* rows this shard may write */
+  const uint64_t* const* bm_words;
+  const uint64_t* bm_nbits;
+  uint32_t nbm;
+  uint64_t result;
+  int status;
+  const void* shifted[256];
+} pd_shard_t;
+
+static void* pd_shard_main(void* arg) {
+  pd_shard_t* s = (pd_shard_t*)arg;
+  for (uint32_t c = 0; c < s->ncols; c++)
+    s->shifted[c] = (const char*)s->cols[c] + s->begin * width_of(s->types[c]);
+  int st;
+  s->result = oracle_pushdown_bm(s->shifted, s->types, s->ncols, s->end - s->begin, s->prog,
+                                 s->len, s->proj, s->nproj, s->row_offset + s->begin, s->out_ids,
+                                 (void* const*)s->out_cols, s->capacity, s->bm_words, s->bm_nbits,
+                                 s->nbm, &st);
+  s->status = st;
+  return NULL;
+}
+
+uint64_t oracle_pushdown_mt_bm(const void* const* cols, const int32_t* types, uint32_t ncols,
+                               uint64_t n, const uint8_t* prog, size_t len, const uint32_t* proj,
+                               uint32_t nproj, uint64_t row_offset, uint32_t* out_ids,
+                               void* const* out_cols, uint64_t capacity, int nthreads,
+                               const uint64_t* const* bm_words, const uint64_t* bm_nbits,
+                               uint32_t nbm, int* status) {
+  int s = oracle_check(prog, len, types, ncols);
+  for (uint32_t j = 0; s == O_OK && j < nproj; j++)
+    if (proj[j] >= ncols) s = O_E_ARG;
+  if (s == O_OK && ncols > 256) s = O_E_ARG;
+  if (status) *status = s;
+  if (s != O_OK) return UINT64_MAX;
+  if (nthreads < 1) nthreads = 1;
+  /* 1. per-shard counts (the multi-threaded count's shards) */
+  shard_t* cs = (shard_t*)calloc((size_t)nthreads, sizeof(shard_t));
+  pd_shard_t* ps = (pd_shard_t*)calloc((size_t)nthreads, sizeof(pd_shard_t));
+  pthread_t* th = (pthread_t*)calloc((size_t)nthreads, sizeof(pthread_t));
+  void** shifted_outs = (void**)calloc((size_t)nthreads * (nproj ? nproj : 1), sizeof(void*));
+  for (int t = 0; t < nthreads; t++) {
+    cs[t].cols = cols; cs[t].types = types; cs[t].ncols = ncols;
+    cs[t].begin = n * (uint64_t)t / (uint64_t)nthreads;
+    cs[t].end = n * (uint64_t)(t + 1) / (uint64_t)nthreads;
+    cs[t].prog = prog; cs[t].len = len;
+    cs[t].bm_words = bm_words; cs[t].bm_nbits = bm_nbits; cs[t].nbm = nbm;
+    pthread_create(&th[t], NULL, shard_main, &cs[t]);
+  }
+  int failed = O_OK;
+  for (int t = 0; t < nthreads; t++) {
+    pthread_join(th[t], NULL);
+    if (cs[t].status != O_OK) failed = cs[t].status;
+  }
+  /* 2. + 3. exclusive offsets, then each shard writes its slice */
+  uint64_t total = 0;
+  if (failed == O_OK) {
+    for (int t = 0; t < nthreads; t++) {
+      const uint64_t off = total;
+      total += cs[t].result;
+      pd_shard_t* p = &ps[t];
+      p->cols = cols; p->types = types; p->ncols = ncols;
+      p->begin = cs[t].begin; p->end = cs[t].end;
+      p->prog = prog; p->len = len; p->proj = proj; p->nproj = nproj;
+      p->row_offset = row_offset;
+      p->capacity = off < capacity ? capacity - off : 0;
+      if (p->capacity > cs[t].result) p->capacity = cs[t].result;
+      p->out_ids = out_ids + (p->capacity ? off : 0);
+      p->out_cols = shifted_outs + (size_t)t * (nproj ? nproj : 1);
+      for (uint32_t j = 0; j < nproj; j++)
+        p->out_cols[j] = (char*)out_cols[j] + (p->capacity ? off : 0) * width_of(types[proj[j]]);
+      p->bm_words = bm_words; p->bm_nbits = bm_nbits; p->nbm = nbm;
+      pthread_create(&th[t], NULL, pd_shard_main, p);
+    }
+    for (int t = 0; t < nthreads; t++) {
+      pthread_join(th[t], NULL);
+      if (ps[t].status != O_OK) failed = ps[t].status;
+    }
+  }
+  free(cs);
+  free(ps);
+  free(th);
+  free(shifted_outs);
+  if (failed != O_OK) {
+    if (status) *status = failed;
+    return UINT64_MAX;
+  }
+  return total;
+}

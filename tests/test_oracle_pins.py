@@ -476,6 +476,67 @@ def test_count_mt_matches_count():
     assert e.value.status == 1
 
 
+def test_pushdown_mt_matches_pushdown():
+    """The row-sharded push-down (oracle_pushdown_mt_bm, used to check whole full-size tables in
+    tests/test_gpu_fullsize.py) returns exactly oracle_pushdown's ids and gathered bytes: every
+    thread count (incl. more threads than rows: empty shards), capacity cuts inside and between
+    shards (Algorithm 1's gate), row offsets, key sets, every column type, and
+    errors propagate."""
+    rng = np.random.default_rng(405)
+    types = [INT32, DICT8, INT64, FLOAT32, DICT16, DICT32, DATE32]
+    n = 1777
+    cols, pools = random_table(rng, types, n)
+    bms = random_bitmaps(rng, pools)
+    proj = list(range(7)) + [2]
+    for i in range(25):
+        prog = encode(random_program(rng, types, pools, max_depth=3, n_bitmaps=len(bms)), types)
+        full, ids, outs = oracle.pushdown(cols, types, prog, proj=proj, bitmaps=bms,
+                                          row_offset=123 * i)
+        for nt in (1, 2, 7, 16) + ((2500,) if i < 3 else ()):   # 2500 > n: empty shards
+            caps = (None, 0, 1, full // 3, full, full + 9) if nt in (7, 2500) else (None,)
+            for cap in caps:
+                c, ids2, outs2 = oracle.pushdown_mt(cols, types, prog, proj=proj, capacity=cap,
+                                                    row_offset=123 * i, bitmaps=bms, nthreads=nt)
+                k = full if cap is None else min(cap, full)
+                assert c == full
+                np.testing.assert_array_equal(ids2, ids[:k])
+                for a, b in zip(outs2, outs):
+                    assert a.tobytes() == b[:k].tobytes()
+    with pytest.raises(oracle.OracleError) as e:
+        oracle.pushdown_mt(cols, types, encode(InSet(0, 9), types), bitmaps=bms, nthreads=4)
+    assert e.value.status == 1
+    empty = [c[:0] for c in cols]
+    c, ids0, outs0 = oracle.pushdown_mt(empty, types, encode(Cmp("<", 0, 5), types), proj=[1],
+                                        nthreads=4)
+    assert c == 0 and len(ids0) == 0 and len(outs0[0]) == 0
+
+
+def test_pushdown_mt_closed_forms():
+    """The sharded push-down against the closed forms, not only against oracle_pushdown: C2's
+    tuple multiset (P3) and the affine threshold (P4) at 1/1000 scale, on 16 threads."""
+    T = configs.gen_c2(600_000)
+    cols = [c.numpy() for c in T.columns]
+    for node in configs.c2_probes().values():
+        want_count, want_ids = _closed_form(T, node)
+        c, ids, (d,) = oracle.pushdown_mt(cols, T.types, encode(node, T.types), proj=[3],
+                                          nthreads=16)
+        assert c == want_count == 100_200
+        np.testing.assert_array_equal(ids, want_ids)
+        np.testing.assert_array_equal(d, cols[3][want_ids])
+    n = 1_000_000
+    S = configs.gen_sweep(n)
+    x, y = S.col("x").numpy(), S.col("y").numpy()
+    a, b, a_inv = S.meta["affine"]
+    for s in (1e-4, 0.1, 0.5):
+        t = configs.sweep_threshold(n, s)
+        c, ids, (yy,) = oracle.pushdown_mt([x, y], S.types, encode(configs.sweep_probe(t), S.types),
+                                           proj=[1], nthreads=16)
+        v = np.arange(t, dtype=np.int64)
+        assert c == t
+        np.testing.assert_array_equal(ids, np.sort((a_inv * ((v - b) % n)) % n))
+        np.testing.assert_array_equal(yy, y[ids])
+
+
 # ---- oracle/synopsis.py: the equi-depth histogram baseline (SURVEY §8f NEXT(4)) ----------------
 
 def test_equi_depth_paper_example_49_3():
