@@ -1,25 +1,45 @@
-"""Full-size parity on the BASELINE.json configs, in bench.py's launch configuration.
+"""Whole-table parity on every BASELINE.json config at full size (north_star: "bit-exact
+counts and row-id sets vs the CPU oracle on all configs"; exact cardinality, PAPER.md:233;
+COUNT by iterating every tuple).
 
-C1 (60K rows) is checked element by element against the oracle. C3 (300M), C4 (480M) and
-C5 (1e9) are too large for the oracle to scan whole within a test, so they are checked
-  * on sampled windows: zero-copy sub-tables registered over 1M-row windows of the resident
-    columns (row offsets exercise the shard path) are compared with the oracle on the same rows;
-  * by properties that hold at any size: count(P) + count(NOT P) = N, the push-down count equals
-    the probe count, its row ids are strictly increasing and inside [0, N), projected values
-    equal the column at those ids, and every row id of a sampled window matches the oracle's;
-  * C5 by its closed form: count(x < t) = t and ids = sort((v - b)/a mod N).
+Every row of every table is checked: the whole resident columns are copied to the host and the
+oracle (oracle_count_mt / oracle_pushdown_mt: the plain row-at-a-time definition over contiguous
+row shards on the host's threads, concatenated — pinned equal to the single-threaded oracle in
+tests/test_oracle_pins.py) computes the exact count, the complete ascending row-id array and every
+projected column; the GPU's count, row ids and projected bytes must equal them element by element.
+
+  C0  TPC-H SF-50 orders (75M rows): Listings 5.1-5.3 and Q5's year
+  C1  TPC-H SF-0.01 lineitem (60K rows): Listing 1.1 and Q3/Q5/Q10
+  C2  the worked example (600M rows): Listing 3.1's three encodings (its closed form is checked
+      in tests/test_gpu_parity.py as well)
+  C3  TPC-H SF-50 lineitem (300M rows): Q3/Q5/Q10 and Listing 1.1
+  C4  SSB SF-80 lineorder (480M rows): Q1.1-Q1.3, Q3.1, Q3.4, Q4.2
+  C5  1e9-row sweep, every selectivity 1e-6 .. 1 (plus its closed form)
+  C6  SSB SF-80 lineorder for Q2.x (480M rows): the key-set semijoin probes Q2.1-Q2.3
+
+The probe bench.py times for a config (bench.workload) runs in bench.py's launch configuration:
+a prepared Execute (CUDA graph, capacity = the count, its projection) replayed twice; the other
+probes through sel_execute. The bench probe is also materialised by sel_pushdown without a kept
+selection (the two-pass path at these sizes). count(NOT P) = N - count(P) (G1, two-valued logic)
+is asserted beside each probe.
 """
+
+import os
 
 import numpy as np
 import pytest
 import torch
 
+import bench
 import oracle
 import paper_1806_08384_b200 as sel
 from selgen import configs, encode
-from selgen.program import Not
+from selgen.program import Const, Not
 
 pytestmark = pytest.mark.gpu
+
+NTHREADS = os.cpu_count() or 1
+_NPV = {1: np.int32, 2: np.int64, 3: np.float32, 4: np.int32, 5: np.uint8, 6: np.uint16, 7: np.uint32}
 
 
 @pytest.fixture(scope="module")
@@ -29,106 +49,143 @@ def ctx(cuda_device):
     c.close()
 
 
-def _np(col, s, e):
-    return col.data[s:e].cpu().numpy().view(
-        {1: np.int32, 2: np.int64, 3: np.float32, 4: np.int32, 5: np.uint8, 6: np.uint16, 7: np.uint32}[col.ctype])
+def _host(col):
+    return col.data.cpu().numpy().view(_NPV[col.ctype])
 
 
-def _windows(n, k, size, seed):
-    rng = np.random.default_rng(seed)
-    starts = sorted(set(int(x) // 1024 * 1024 for x in rng.integers(0, max(1, n - size), k)))
-    return [(s, min(n, s + size)) for s in starts] + [(max(0, n - 777_777) // 1024 * 1024, n)]  # + the tail
+def _same(gpu, want, what):
+    got = gpu.cpu().numpy()
+    got = got.view(want.dtype) if got.dtype.itemsize == want.dtype.itemsize else got
+    assert got.shape == want.shape, (what, got.shape, want.shape)
+    assert np.array_equal(got, want), (what, int(np.flatnonzero(got != want)[0]))
 
 
-def check_large(ctx, T, probes, proj, seed):
+def whole_table_parity(ctx, T, probes, proj, bench_probe=None, bitmaps=None):
+    """Count, row ids and projected columns of every probe vs the oracle over the WHOLE table."""
     n = T.n_rows
     names = [c.name for c in T.columns]
+    host = [_host(c) for c in T.columns]
     t = sel.Table(ctx, names, T.types, [c.data for c in T.columns])
+    pnames = [names[j] for j in proj]
+    checked = 0
     for name, node in probes.items():
         prog = encode(node, T.types)
-        cnt = t.count(prog)
-        assert cnt + t.count(encode(Not(node), T.types)) == n, name
-        res = t.execute(prog, project=[names[j] for j in proj], max_size=n, capacity=cnt)
-        assert res.materialized and res.count == cnt and res.rowids.numel() == cnt
-        ids = res.rowids.to(torch.int64) & 0xFFFFFFFF
-        if cnt > 1:
-            assert bool((ids[1:] > ids[:-1]).all()), name
-        if cnt:
-            assert int(ids[0]) >= 0 and int(ids[-1]) < n
-        for j in proj:
-            assert torch.equal(res.columns[names[j]], T.columns[j].data[ids]), (name, names[j])
-        for (s, e) in _windows(n, 6, 1_000_000, seed):
-            host = [_np(c, s, e) for c in T.columns]
-            want_c, want_ids, _ = oracle.pushdown(host, T.types, prog, row_offset=s)
-            # the resident columns, registered as a zero-copy shard of the window
-            w = sel.Table(ctx, names, T.types, [c.data[s:e] for c in T.columns], row_offset=s,
-                          global_rows=n)
-            assert w.count(prog) == want_c, (name, s, e)
-            lo = int(torch.searchsorted(ids, torch.tensor(s, device=ids.device)))
-            hi = int(torch.searchsorted(ids, torch.tensor(e, device=ids.device)))
-            np.testing.assert_array_equal(ids[lo:hi].cpu().numpy().astype(np.uint32), want_ids)
-            w.release()
+        want_c, want_ids, want_cols = oracle.pushdown_mt(host, T.types, prog, proj=proj,
+                                                         bitmaps=bitmaps, nthreads=NTHREADS)
+        assert t.count(prog) == want_c, name
+        assert t.count(encode(Not(node), T.types)) == n - want_c, name
+        cap = max(want_c, 1)
+        if name == bench_probe:
+            prep = t.prepare_execute(prog, project=pnames, max_size=n, capacity=cap)
+            for _ in range(2):
+                assert prep.run() == want_c and prep.materialized, name
+            res = prep.result()
+        else:
+            res = t.execute(prog, project=pnames, max_size=n, capacity=cap)
+            assert res.materialized, name
+        assert res.count == want_c and res.local_count == want_c, name
+        _same(res.rowids, want_ids, (name, "rowids"))
+        for pn, w in zip(pnames, want_cols):
+            _same(res.columns[pn], w, (name, pn))
+        if name == bench_probe:
+            prep.release()
+            t.count(encode(Const(True), T.types), keep_selection=True)   # drop the selection
+            pd = t.pushdown(prog, project=pnames, capacity=cap)
+            assert pd.count == want_c, name
+            _same(pd.rowids, want_ids, (name, "pushdown rowids"))
+            for pn, w in zip(pnames, want_cols):
+                _same(pd.columns[pn], w, (name, "pushdown", pn))
+            del pd
+        del res, want_ids, want_cols
+        checked += 1
+    t.release()
+    return checked
+
+
+def _bench(name):
+    n, gen, node, proj, desc = bench.workload(name, 0)
+    return n, gen, node, proj
+
+
+def test_c0_orders_sf50_whole(ctx):
+    n, gen, node, proj = _bench("c0")
+    T = gen(0, n, ctx.device)
+    probes = configs.orders_probes()
+    probes = {k: v for k, v in probes.items() if k not in ("attr1",)}   # attr1 == l5.1
+    assert whole_table_parity(ctx, T, probes, proj, bench_probe="q5_orderdate") == len(probes)
+    # the paper's fixed points (PAPER.md:442, 453-455) on the same rows
+    t = sel.Table(ctx, [c.name for c in T.columns], T.types, [c.data for c in T.columns])
+    assert t.count(encode(probes["l5.1"], T.types)) == 1
+    assert t.count(encode(probes["l5.2"], T.types)) == n
     t.release()
 
 
-def test_c1_lineitem_sf001_exact(ctx):
-    T = configs.gen_lineitem(60_000, device=ctx.device)
-    host = [c.data.cpu().numpy().view({1: np.int32, 2: np.int64, 4: np.int32, 5: np.uint8}[c.ctype])
-            for c in T.columns]
-    t = sel.Table(ctx, [c.name for c in T.columns], T.types, [c.data for c in T.columns])
-    for name, node in configs.lineitem_probes(T).items():
-        prog = encode(node, T.types)
-        want_c, want_ids, want_cols = oracle.pushdown(host, T.types, prog, proj=[0, 3])
-        assert t.count(prog) == want_c, name
-        res = t.execute(prog, project=["l_orderkey", "l_extendedprice"], max_size=60_000)
-        np.testing.assert_array_equal(res.rowids.cpu().numpy().view(np.uint32), want_ids)
-        np.testing.assert_array_equal(res.columns["l_extendedprice"].cpu().numpy(), want_cols[1])
-
-
-def test_c3_lineitem_sf50(ctx):
-    T = configs.gen_lineitem(300_000_000, device=ctx.device,
-                             columns=["l_orderkey", "l_discount", "l_extendedprice", "l_returnflag",
-                                      "l_shipdate", "l_shipmode"])
+def test_c1_lineitem_sf001_whole(ctx):
+    n, gen, node, proj = _bench("c1")
+    T = gen(0, n, ctx.device)
     probes = configs.lineitem_probes(T)
-    check_large(ctx, T, probes, [T.index("l_orderkey"), T.index("l_extendedprice"),
-                                 T.index("l_discount")], seed=3)
+    assert probes["listing1"] is not None
+    assert whole_table_parity(ctx, T, probes, proj, bench_probe="listing1") == 4
 
 
-def test_c4_lineorder_sf80(ctx):
-    T = configs.gen_lineorder(480_000_000, device=ctx.device)
-    check_large(ctx, T, configs.lineorder_probes(), [3], seed=4)
+def test_c2_worked_example_whole(ctx):
+    n, gen, node, proj = _bench("c2")
+    T = gen(0, n, ctx.device)
+    probes = configs.c2_probes()
+    assert whole_table_parity(ctx, T, probes, proj, bench_probe="listing") == 3
 
 
-def test_c5_sweep_1e9_closed_form(ctx):
-    n = configs.C5_ROWS
-    T = configs.gen_sweep(n, device=ctx.device)
+def test_c3_lineitem_sf50_whole(ctx):
+    n, gen, node, proj = _bench("c3")
+    T = gen(0, n, ctx.device)
+    probes = configs.lineitem_probes(T)
+    assert whole_table_parity(ctx, T, probes, proj, bench_probe="q10") == 4
+
+
+def test_c4_lineorder_sf80_whole(ctx):
+    n, gen, node, proj = _bench("c4")
+    T = gen(0, n, ctx.device)
+    probes = configs.lineorder_probes()
+    assert whole_table_parity(ctx, T, probes, proj, bench_probe="q1.1") == 6
+
+
+def test_c5_sweep_1e9_whole(ctx):
+    """Every selectivity of the sweep against the oracle over all 1e9 rows, and the closed form
+    (count(x < t) = t, ids = sort(a^-1 (v - b) mod N)) at every selectivity."""
+    n, gen, node, proj = _bench("c5")
+    T = gen(0, n, ctx.device)
+    probes = {f"s={s:g}": configs.sweep_probe(configs.sweep_threshold(n, s))
+              for s in configs.C5_SELECTIVITIES}
+    assert whole_table_parity(ctx, T, probes, proj, bench_probe="s=0.01") == 8
     a, b, a_inv = T.meta["affine"]
     t = sel.Table(ctx, ["x", "y"], T.types, [c.data for c in T.columns])
     for s in configs.C5_SELECTIVITIES:
         thr = configs.sweep_threshold(n, s)
-        prog = encode(configs.sweep_probe(thr), T.types)
-        assert t.count(prog) == thr, s
-        if thr <= 50_000_000:
-            res = t.execute(prog, project=["y"], max_size=n, capacity=thr)
-            assert res.count == thr
-            v = torch.arange(thr, dtype=torch.int64, device=ctx.device)
-            want = torch.sort((a_inv * ((v - b) % n)) % n).values
-            got = res.rowids.to(torch.int64) & 0xFFFFFFFF
-            assert torch.equal(got, want), s
-            assert torch.equal(res.columns["y"], T.col("y").data[got])
-
-
-def test_c0_orders_sf50_paper_probes(ctx):
-    """C0 (SURVEY §8d optional context): TPC-H SF-50 orders, 75M rows, with the paper's Table 5.1 /
-    5.2 probes — `o_orderkey = 1` selects exactly one row and `o_orderkey >= 1` every row
-     — the Listing 5.3 attribute sweep and Q5's one-year range (15.2 % of
-    orders), on sampled windows and properties."""
-    T = configs.gen_orders(75_000_000, device=ctx.device)
-    probes = configs.orders_probes()
-    t = sel.Table(ctx, [c.name for c in T.columns], T.types, [c.data for c in T.columns])
-    assert t.count(encode(probes["l5.1"], T.types)) == 1
-    assert t.count(encode(probes["l5.2"], T.types)) == 75_000_000
-    q5 = t.count(encode(probes["q5_orderdate"], T.types))
-    assert abs(q5 / 75_000_000 - 365 / 2406) < 0.002
+        res = t.execute(encode(configs.sweep_probe(thr), T.types), project=["y"], max_size=n,
+                        capacity=max(thr, 1))
+        assert res.count == thr
+        v = torch.arange(thr, dtype=torch.int64, device=ctx.device)
+        want = torch.sort((a_inv * ((v - b) % n)) % n).values
+        assert torch.equal(res.rowids.to(torch.int64) & 0xFFFFFFFF, want), s
+        del res, v, want
     t.release()
-    check_large(ctx, T, {k: probes[k] for k in ("attr2", "attr4", "q5_orderdate")}, [0, 1], 50)
+
+
+def test_c6_ssb_q2_semijoin_whole(cuda_device):
+    """The NEXT(3) key-set probes over all 480M rows; a fresh context so that
+    the key sets get ids 0 and 1 as the probes name them."""
+    c = sel.Context(cuda_device)
+    try:
+        n, gen, node, proj = _bench("c6")
+        T = gen(0, n, c.device)
+        for name, (node, bms) in configs.q2_probes(80).items():
+            words = [torch.from_numpy(w.view(np.int64).copy()).to(c.device) for w, _ in bms]
+            ids = [c.register_bitmap(w, nb) for w, (_, nb) in zip(words, bms)]
+            assert ids == [0, 1]
+            assert whole_table_parity(c, T, {name: node}, proj,
+                                      bench_probe="q2.1" if name == "q2.1" else None,
+                                      bitmaps=bms) == 1
+            for i in ids:
+                c.release_bitmap(i)
+    finally:
+        c.close()
