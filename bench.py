@@ -43,6 +43,10 @@ def parse():
                     help="time table.execute() per step instead of the prepared (graph) execute")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=8)
+    ap.add_argument("--ref-rows", type=int, default=60_000_000,
+                    help="--impl reference: rows of the workload each oracle step runs on")
+    ap.add_argument("--cpu-rows", type=int, default=0,
+                    help="rows of the CPU oracle baseline (0: the whole table)")
     ap.add_argument("--comm1", action="store_true",
                     help="testing: give the N=1 context a one-rank NCCL communicator (the N>1 "
                          "collectives on the step's critical path, without peers)")
@@ -50,6 +54,9 @@ def parse():
                     help="testing: every rank on cuda:0 (torch.distributed over gloo; the ranks "
                          "time-slice one GPU, so timings are meaningless) to exercise the N > 1 "
                          "path on a one-GPU box")
+    ap.add_argument("--xchg", default=os.environ.get("SEL_XCHG", "peers"), choices=["peers", "nccl"],
+                    help="N > 1: the cross-rank exchange — the library's own over peer memory "
+                         "(NCCL on every rank if any rank cannot map the others) or NCCL")
     ap.add_argument("--peers1", action="store_true",
                     help="testing: give the N=1 context a one-rank peer exchange (the N>1 "
                          "exchange on the step's critical path)")
@@ -207,7 +214,7 @@ class ClockSampler:
                         self.reasons.add(k)
             except Exception:
                 pass
-            time.sleep(0.001)
+            time.sleep(0.0002)
 
     def __enter__(self):
         if self.nv is not None:
@@ -223,10 +230,20 @@ class ClockSampler:
         if self.nv is not None:
             self._t.join()
 
+    def mark(self):
+        """End of the timed region: samples after this cover the same steps' second pass (the
+        per-kernel timing pass), which keeps the GPU under the same load."""
+        self.n_timed = len(self.samples)
+
     def summary(self):
-        med = statistics.median(self.samples) if self.samples else None
+        xs = self.samples
+        nt = getattr(self, "n_timed", len(xs))
+        med = statistics.median(xs) if xs else None
         return {"sm_mhz": med, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
-                "samples": len(self.samples)}
+                "samples": len(xs), "samples_timed_region": nt,
+                "sm_mhz_timed_region": statistics.median(xs[:nt]) if nt else None,
+                "sm_mhz_min": min(xs) if xs else None,
+                "window": "the timed steps and the same steps' per-kernel timing pass right after"}
 
 
 def measured_peaks():
@@ -251,16 +268,37 @@ def ncu_traffic(kernel, config, applies=True):
 # ---- the oracle as baseline / reference arm ------------------------------------------------------
 
 def cpu_baseline(host_cols, table_like, prog, proj, prog_cols, nthreads, bitmaps=None):
-    """The oracle as it stands on a bounded sample: count on all host threads, push-down on one."""
+    """The oracle as it stands (SURVEY §8(d) CPU protocol), outside any timed GPU region:
+    all_cores     — count (oracle_count_mt) + push-down (oracle_pushdown_mt) on `nthreads`;
+    single_thread — count (oracle_count) + push-down (oracle_pushdown) on one thread.
+    Both over the rows given; each records its seconds, GB/s of the step's algorithmic bytes and
+    rows/s. Returns (all_cores, single_thread, count)."""
     import oracle
-    t0 = time.perf_counter()
-    cnt = oracle.count_mt(host_cols, table_like.types, prog, nthreads, bitmaps=bitmaps)
-    t1 = time.perf_counter()
-    c2, ids, outs = oracle.pushdown(host_cols, table_like.types, prog, proj=proj, bitmaps=bitmaps)
-    t2 = time.perf_counter()
-    assert c2 == cnt
-    _, _, step_b = algo_bytes(table_like, prog_cols, proj, cnt, 0)
-    return step_b, t2 - t0, t1 - t0, t2 - t1, cnt
+    types = table_like.types
+    rows = len(host_cols[0]) if host_cols else 0
+
+    def leg(threads):
+        t0 = time.perf_counter()
+        if threads > 1:
+            cnt = oracle.count_mt(host_cols, types, prog, threads, bitmaps=bitmaps)
+            t1 = time.perf_counter()
+            c2, _, _ = oracle.pushdown_mt(host_cols, types, prog, proj=proj, bitmaps=bitmaps,
+                                          nthreads=threads)
+        else:
+            cnt = oracle.count(host_cols, types, prog, bitmaps=bitmaps)
+            t1 = time.perf_counter()
+            c2, _, _ = oracle.pushdown(host_cols, types, prog, proj=proj, bitmaps=bitmaps)
+        t2 = time.perf_counter()
+        assert c2 == cnt
+        _, _, step_b = algo_bytes(table_like, prog_cols, proj, cnt, 0)
+        return {"threads": threads, "rows": rows, "count_s": round(t1 - t0, 3),
+                "pushdown_s": round(t2 - t1, 3), "step_s": round(t2 - t0, 3),
+                "gbs": round(step_b / (t2 - t0) / 1e9, 3),
+                "rows_per_s": round(rows / (t2 - t0))}, cnt
+
+    allc, cnt = leg(nthreads)
+    single, _ = leg(1)
+    return allc, single, cnt
 
 
 def cpu_model():
@@ -284,7 +322,7 @@ def run_reference(args):
         return
     n, gen, node, proj, desc = workload(args.config, args.rows)
     bms = key_sets(args.config)
-    sample = min(n, 12_000_000)
+    sample = min(n, args.ref_rows)
     T = gen(0, sample, "cpu")
     cols = [c.numpy() for c in T.columns]
     prog = encode(node, T.types)
@@ -294,7 +332,8 @@ def run_reference(args):
     def step():
         t0 = time.perf_counter()
         cnt = oracle.count_mt(cols, T.types, prog, nthreads, bitmaps=bms)
-        c2, ids, outs = oracle.pushdown(cols, T.types, prog, proj=proj, bitmaps=bms)
+        c2, ids, outs = oracle.pushdown_mt(cols, T.types, prog, proj=proj, bitmaps=bms,
+                                           nthreads=nthreads)
         return time.perf_counter() - t0, cnt
     for _ in range(args.warmup):
         step()
@@ -314,7 +353,7 @@ def run_reference(args):
                        "sample_rows": sample},
             "cpu_baseline": {"value": round(value, 3), "unit": "GB/s", "cores": nthreads,
                              "kind": "oracle", "cpu_model": cpu_model(),
-                             "sample": f"first {sample} rows of the workload; count on {nthreads} threads (oracle_count_mt), push-down single-threaded (oracle_pushdown)"},
+                             "sample": f"first {sample} of {n} rows of the workload per step; count (oracle_count_mt) and push-down (oracle_pushdown_mt) on {nthreads} threads"},
             "e2e": {"value": round(value, 3), "unit": "GB/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     emit(line)
@@ -328,52 +367,6 @@ _GLOO = False
 def _red_dev(dev):
     """Device of the small tensors reduced over torch.distributed (CPU under --same-device/gloo)."""
     return "cpu" if _GLOO else dev
-
-
-def setup_exchange(ctx, sel, sdist, dist, dev):
-    """Cross-rank combination for N > 1: the library's own exchange over peer memory
-    (CUDA IPC + NVLink stores, fused into the push-down's prefix kernel; include/sel.h
-    sel_ctx_set_peers) when every rank can map every other rank's buffer — tried first on a
-    throw-away context, agreed by all ranks — else NCCL. SEL_XCHG=nccl forces NCCL."""
-    import torch
-    ok = os.environ.get("SEL_XCHG", "peers") != "nccl"
-    why = "SEL_XCHG=nccl"
-    if ok:
-        # every rank reaches each collective below whatever fails locally (no rank left waiting)
-        mapped = False
-        try:
-            h = ctx.peer_handle()
-        except Exception as ex:  # noqa: BLE001 - any failure falls back to NCCL on every rank
-            h, ok, why = None, False, f"peers unavailable: {type(ex).__name__}: {ex}"
-        handles = [None] * dist.get_world_size()
-        dist.all_gather_object(handles, h)
-        if ok and all(x is not None for x in handles):
-            try:
-                ctx.set_peers(len(handles), dist.get_rank(), handles)
-                mapped = True
-                # one real exchange: a count over a one-row table on every rank must see all ranks
-                from selgen.program import Const, encode, INT32
-                one = torch.zeros(1, dtype=torch.int32, device=dev)
-                probe = sel.Table(ctx, ["x"], [INT32], [one], row_offset=dist.get_rank(),
-                                  global_rows=dist.get_world_size())
-                got = probe.count(encode(Const(True), [INT32]))
-                probe.release()
-                if got != dist.get_world_size():
-                    ok, why = False, f"peer exchange counted {got} of {dist.get_world_size()}"
-            except Exception as ex:  # noqa: BLE001
-                ok, why = False, f"peers unavailable: {type(ex).__name__}: {ex}"
-        else:
-            ok = False
-        flag = torch.tensor([1 if ok else 0], dtype=torch.int32, device=_red_dev(dev))
-        dist.all_reduce(flag, op=dist.ReduceOp.MIN)
-        ok = bool(flag.item())
-        if not ok and mapped:
-            ctx.drop_peers()
-            why = why if why != "SEL_XCHG=nccl" else "a rank could not map the peers' buffers"
-    if ok:
-        return "peers (CUDA IPC, NVLink release stores, fused into the prefix kernel)"
-    sdist.setup_comm(ctx)
-    return f"nccl ({why})"
 
 
 def run_ours(args):
@@ -409,7 +402,7 @@ def run_ours(args):
     ctx = sel.Context(dev)
     xchg = None
     if world > 1:
-        xchg = setup_exchange(ctx, sel, sdist, dist, dev)
+        xchg = sdist.setup_exchange(ctx, args.xchg)
     elif args.comm1:
         ctx.set_comm(1, 0, sel.Context.new_unique_id())
         xchg = "nccl (one rank)"
@@ -483,15 +476,16 @@ def run_ours(args):
             step("latency")
         ev1.record(stream)
         torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
-    dev_ms = ev0.elapsed_time(ev1)
-    ctx.enable_timing(True)
-    for _ in range(3):
-        step(None)
-    for _ in range(args.steps):
-        step("kernels")
-    ctx.enable_timing(False)
+        clk.mark()
+        if world > 1:
+            dist.barrier()
+        dev_ms = ev0.elapsed_time(ev1)
+        ctx.enable_timing(True)
+        for _ in range(3):
+            step(None)
+        for _ in range(max(args.steps, 20)):
+            step("kernels")
+        ctx.enable_timing(False)
     pd_path = ctx.last_pushdown_path()
     consts = const_columns(prog, T.types)
     coded = coded_columns(prog, T.types, proj) if pd_path == 1 else set()
@@ -621,19 +615,23 @@ def run_ours(args):
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
-        host_cols = [c.data[: min(T.n_rows, 60_000_000)].cpu().numpy().view(
+        nrows = T.n_rows if not args.cpu_rows else min(T.n_rows, args.cpu_rows)
+        host_cols = [c.data[:nrows].cpu().numpy().view(
             {1: np.int32, 2: np.int64, 3: np.float32, 4: np.int32, 5: np.uint8, 6: np.uint16,
              7: np.uint32}[c.ctype]) for c in T.columns]
-        ns = len(host_cols[0])
         nthreads = os.cpu_count() or 1
         sample_table = type("S", (), {})()
-        sample_table.columns, sample_table.n_rows, sample_table.types = T.columns, ns, T.types
-        by, dt, t_cnt, t_push, cnt = cpu_baseline(host_cols, sample_table, prog, proj, pc, nthreads,
-                                                  bitmaps=bms)
-        cpu = {"value": round(by / dt / 1e9, 3), "unit": "GB/s", "cores": nthreads, "kind": "oracle",
+        sample_table.columns, sample_table.n_rows, sample_table.types = T.columns, nrows, T.types
+        allc, single, cnt = cpu_baseline(host_cols, sample_table, prog, proj, pc, nthreads,
+                                         bitmaps=bms)
+        what = "the whole table" if nrows == T.n_rows else f"the first {nrows} of {n} rows"
+        cpu = {"value": allc["gbs"], "unit": "GB/s", "cores": nthreads, "kind": "oracle",
                "cpu_model": cpu_model(),
-               "sample": f"first {ns} of {n} rows; count on {nthreads} threads ({t_cnt:.2f} s), "
-                         f"push-down on 1 thread ({t_push:.2f} s)"}
+               "sample": f"{what}: count (oracle_count_mt) + push-down (oracle_pushdown_mt) on "
+                         f"{nthreads} threads, {allc['step_s']} s; single_thread: oracle_count + "
+                         f"oracle_pushdown on 1 thread, {single['step_s']} s",
+               "all_cores": allc, "single_thread": single}
+        del host_cols
 
     push_name = "pushdown_sel_kernel" if pd_path == 1 else "pushdown_kernel"
     # Sector-granular minimum of the push-down: a gather must move every 32-byte
@@ -646,6 +644,10 @@ def run_ours(args):
             return 0
         return int(torch.unique_consecutive(ids64 // (32 // width)).numel())
     write_b = local_count * (4 + sum(w_all[j] for j in proj))
+    def lines(width):      # 128-byte lines holding a selected row: the DRAM fetch granularity of
+        if local_count == 0:   # scattered gathers measured by ncu (~90-128 B per gathered value)
+            return 0
+        return int(torch.unique_consecutive(ids64 // (128 // width)).numel())
     if pd_path == 1:
         # projected predicate columns whose values the count kept (SEL_KEEP_VALUES=1, within
         # 8 B/row) are copied contiguously from their slots: count x width, not sectors
@@ -661,9 +663,17 @@ def run_ours(args):
                      + sum(32 * sectors(w_all[j]) for j in set(proj)
                            if j not in kept and j not in consts and j not in coded)
                      + write_b)
+        pb_line = (T.n_rows // 8 + 2 * ((T.n_rows + 1023) // 1024)
+                   + len(coded) * (T.n_rows // 8)
+                   + sum(local_count * w_all[j] for j in kept)
+                   + sum(128 * lines(w_all[j]) for j in set(proj)
+                         if j not in kept and j not in consts and j not in coded)
+                   + write_b)
     else:
         pb_sector = (T.n_rows * sum(w_all[j] for j in pc)
                      + sum(32 * sectors(w_all[j]) for j in set(proj) if j not in pc) + write_b)
+        pb_line = (T.n_rows * sum(w_all[j] for j in pc)
+                   + sum(128 * lines(w_all[j]) for j in set(proj) if j not in pc) + write_b)
     roof_count = {"bound": "hbm", "achieved": round(count_gbs, 2), "peak": hbm, "unit": "GB/s",
                   "frac": round(count_gbs / hbm, 4), "traffic": ncu_traffic("count_kernel", args.config, world == 1 and not args.rows),
                   "kernel": "count_kernel", "ms": round(count_k, 4),
@@ -675,7 +685,12 @@ def run_ours(args):
                  "algorithmic_bytes_per_launch": int(pb), "peak_source": peak_note,
                  "sector_bytes_per_launch": int(pb_sector),
                  "achieved_sector": round(push_sector_gbs, 2),
-                 "frac_sector": round(push_sector_gbs / hbm, 4)}
+                 "frac_sector": round(push_sector_gbs / hbm, 4),
+                 # the DRAM-granularity floor: every 128-byte line holding a selected row of a
+                 # gathered column is fetched whole (ncu: ~90-128 B per scattered 4-byte gather)
+                 "line_bytes_per_launch": int(pb_line),
+                 "achieved_line": round(pb_line / (push_k / 1000) / 1e9, 2),
+                 "frac_line": round(pb_line / (push_k / 1000) / 1e9 / hbm, 4)}
     for r in (roof_count, roof_push):
         r["ms_source"] = ("median of the library's CUDA events around the kernel on its stream, "
                           "over a second pass of the same steps right after the timed region "

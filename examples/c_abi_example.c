@@ -57,7 +57,21 @@ static size_t build_program(uint8_t* out) {
     }                                                                             \
   } while (0)
 
-int main(void) {
+/* Write `bytes` of `p` to dir/name (the test harness compares them with the CPU oracle). */
+static int dump(const char* dir, const char* name, const void* p, size_t bytes) {
+  char path[4096];
+  snprintf(path, sizeof path, "%s/%s", dir, name);
+  FILE* f = fopen(path, "wb");
+  if (!f) return 1;
+  const size_t w = fwrite(p, 1, bytes, f);
+  fclose(f);
+  return w != bytes;
+}
+
+/* usage: c_abi_example [dump_dir] — with dump_dir, the table, the program bytes and the
+ * Execute's row ids and projected column are written there (tests/test_c_abi.py checks them
+ * against the oracle). */
+int main(int argc, char** argv) {
   const uint64_t n = 1000003;              /* ragged: not a multiple of 1024 */
   int32_t* a = malloc(n * 4);
   int32_t* b = malloc(n * 4);
@@ -111,6 +125,12 @@ int main(void) {
       if (hids[k] != i || hb[k] != b[i]) { printf("mismatch at %llu\n", (unsigned long long)k); return 4; }
       ++k;
     }
+  }
+  if (argc > 1 && (dump(argv[1], "A.bin", a, n * 4) || dump(argv[1], "B.bin", b, n * 4) ||
+                   dump(argv[1], "C.bin", c, n) || dump(argv[1], "prog.bin", prog, len) ||
+                   dump(argv[1], "ids.bin", hids, count * 4) || dump(argv[1], "projB.bin", hb, count * 4))) {
+    fprintf(stderr, "cannot write to %s\n", argv[1]);
+    return 7;
   }
   r = sel_execute(t, prog, len, pcol, 1, count - 1, ids, outs, count, &local, &off, &materialized, NULL);
   if (r != want || materialized) return 5;

@@ -31,6 +31,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--rows", type=int, default=60_000_000)
     ap.add_argument("--same-device", action="store_true")
+    ap.add_argument("--xchg", default="peers", choices=["peers", "nccl"])
     args = ap.parse_args()
     rank, world = int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1"))
     local = 0 if args.same_device else int(os.environ.get("LOCAL_RANK", "0"))
@@ -45,12 +46,8 @@ def main():
     s, e = sdist.shard_range(n, world, rank)
     T = configs.gen_c2(n, s, e - s, device=dev)
     ctx = sel.Context(dev)
-    try:
-        sdist.setup_peers(ctx)
-        exchange = "peers"
-    except sel.SelError:          # (a real deployment agrees on this across ranks: see bench.py)
-        sdist.setup_comm(ctx)
-        exchange = "nccl"
+    # one mechanism agreed by every rank (peer memory if every rank maps every buffer, else NCCL)
+    exchange = sdist.setup_exchange(ctx, args.xchg) if world > 1 else "none (one rank)"
     t = sel.Table(ctx, ["A", "B", "C", "D"], T.types, [c.data for c in T.columns],
                   row_offset=s, global_rows=n)
     listing = configs.c2_probes()["listing"]
@@ -77,7 +74,7 @@ def main():
                    if d.role == "evaluated" else ""))
     assert count == total == round(0.167 * n) and ok
     t.release()
-    if world > 1 and exchange == "peers":
+    if world > 1 and exchange.startswith("peers"):
         ctx.drop_peers()
     dist.barrier()
     ctx.close()

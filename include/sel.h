@@ -109,15 +109,25 @@ sel_status sel_ctx_set_comm(sel_ctx ctx, int nranks, int rank, const void* nccl_
  * sel_ctx_set_peers: `handles` = nranks consecutive 64-byte handles, rank r's at 64*r (this
  *   rank's own entry is ignored). 1 <= nranks <= 32; the ranks may share a device (IPC maps
  *   a buffer of the same GPU too). Collective in effect: every rank must call it and then
- *   issue the same sequence of probes. A wait longer than ~10 s (a rank missing) makes the
- *   call fail with SEL_E_STATE instead of hanging.
+ *   issue the same sequence of probes. A wait longer than the peer timeout (10 s unless
+ *   sel_ctx_set_peer_timeout; a rank missing) makes the call fail with SEL_E_STATE instead of
+ *   hanging. A failed exchange writes nothing: its gathered counts and sums are all-ones
+ *   (UINT64_MAX), never a partial sum, so the gated push-down of an Execute (also one writing
+ *   into another rank's buffers, sel_execute_to) stores no row. The failure is sticky: every
+ *   later probe of the context fails with SEL_E_STATE until every rank drops its peers and sets
+ *   them again (the ranks' exchange epochs are out of step).
  *   nranks == 0 drops the peers again (unmaps the others' buffers; handles may be NULL) — e.g.
  *   when not every rank could map every buffer and all fall back to a communicator; every rank
- *   should drop its peers before any rank destroys its context.
+ *   should drop its peers before any rank destroys its context. Dropping also resets the
+ *   exchange (epoch 0, an empty buffer, no failure).
  *   Errors: SEL_E_ARG (bad ranks, disagreeing with the communicator), SEL_E_STATE (already
  *   set, or no handle exported yet), SEL_E_CUDA (cudaIpcOpenMemHandle failed). */
 sel_status sel_ctx_peer_handle(sel_ctx ctx, void* out64);
 sel_status sel_ctx_set_peers(sel_ctx ctx, int nranks, int rank, const void* handles);
+/* The peer exchange's wait bound in milliseconds (1 .. 3,600,000; default 10,000): the failure
+ * detection of SURVEY §5 for the library's own collective. Takes effect for the next probe
+ * (prepared executes re-capture). Errors: SEL_E_ARG. */
+sel_status sel_ctx_set_peer_timeout(sel_ctx ctx, uint64_t timeout_ms);
 
 /* Gather to one rank over peer memory ("an optional gather-to-one-rank uses P2P
  * writes at the offset"). sel_ctx_export_buffer: a 72-byte handle (CUDA IPC handle of the
@@ -282,6 +292,18 @@ uint64_t sel_pushdown(sel_table table, const void* prog, size_t prog_bytes,
  * SEL_TWO_PASS_MIN_ROWS=<n> moves the threshold. Path 2 leaves its selection kept, so a repeated
  * sel_pushdown of the same program takes path 1. */
 int sel_ctx_last_pushdown_path(sel_ctx ctx);
+
+/* How the context's last materialisation from a kept selection (path 1 or 2 above, also inside
+ * sel_execute) wrote its projections — diagnostics and tests, no effect on results. Bits:
+ * SEL_PD_CODED (a projection written from the kept code bits of a two-point leaf, the column not
+ * read), SEL_PD_WHOLE_CHUNKS (fully selected 1024-row chunks left to the whole-chunk copy kernel),
+ * SEL_PD_CONSTANT (a projection pinned to one value by the conjunction, filled), SEL_PD_KEPT_VALUES
+ * (a projection copied from values the count kept). 0 for other paths; -1 for a null ctx. */
+#define SEL_PD_CODED 1
+#define SEL_PD_WHOLE_CHUNKS 2
+#define SEL_PD_CONSTANT 4
+#define SEL_PD_KEPT_VALUES 8
+int sel_ctx_last_pushdown_flags(sel_ctx ctx);
 
 /* Choose the path sel_pushdown takes when no kept selection matches (overrides the environment
  * above): mode -1 = automatic (two passes at >= 3·2^20 local rows, else the single pass), 0 = always

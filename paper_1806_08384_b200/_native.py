@@ -14,20 +14,22 @@ SEL_OK, SEL_E_ARG, SEL_E_ALIGN, SEL_E_TYPE, SEL_E_PROGRAM, SEL_E_TOO_LARGE, SEL_
     SEL_E_NCCL, SEL_E_STATE = range(9)
 SEL_ERR = (1 << 64) - 1
 SEL_KEEP_SELECTION = 1
+SEL_PD_CODED, SEL_PD_WHOLE_CHUNKS, SEL_PD_CONSTANT, SEL_PD_KEPT_VALUES = 1, 2, 4, 8
 STATUS_NAMES = {0: "SEL_OK", 1: "SEL_E_ARG", 2: "SEL_E_ALIGN", 3: "SEL_E_TYPE",
                 4: "SEL_E_PROGRAM", 5: "SEL_E_TOO_LARGE", 6: "SEL_E_CUDA", 7: "SEL_E_NCCL",
                 8: "SEL_E_STATE"}
 
 # Every symbol include/sel.h declares (tests check the library exports exactly these).
 EXPORTS = ["sel_ctx_create", "sel_ctx_set_comm", "sel_nccl_unique_id", "sel_ctx_destroy",
-           "sel_ctx_peer_handle", "sel_ctx_set_peers", "sel_ctx_export_buffer",
+           "sel_ctx_peer_handle", "sel_ctx_set_peers", "sel_ctx_set_peer_timeout",
+           "sel_ctx_export_buffer",
            "sel_ctx_import_buffer", "sel_execute_to",
            "sel_ctx_set_timing", "sel_ctx_last_kernel_ms", "sel_table_register",
            "sel_table_release", "sel_count", "sel_count_async", "sel_count_ex", "sel_execute", "sel_pushdown",
            "sel_ctx_last_times", "sel_count_batch", "sel_count_sampled", "sel_histogram",
            "sel_bitmap_register", "sel_bitmap_release",
            "sel_prepare_execute", "sel_prepared_execute", "sel_prepared_release",
-           "sel_ctx_last_pushdown_path", "sel_ctx_set_pushdown_path", "sel_program_check",
+           "sel_ctx_last_pushdown_path", "sel_ctx_last_pushdown_flags", "sel_ctx_set_pushdown_path", "sel_program_check",
            "sel_program_path", "sel_program_plan_json", "sel_last_error",
            "sel_last_error_message", "sel_abi_version"]
 
@@ -60,6 +62,7 @@ def lib() -> ctypes.CDLL:
         "sel_ctx_set_comm": (i32, [vp, i32, i32, vp]),
         "sel_ctx_peer_handle": (i32, [vp, vp]),
         "sel_ctx_set_peers": (i32, [vp, i32, i32, vp]),
+        "sel_ctx_set_peer_timeout": (i32, [vp, u64]),
         "sel_ctx_export_buffer": (i32, [vp, vp, vp]),
         "sel_ctx_import_buffer": (i32, [vp, vp, ctypes.POINTER(ctypes.c_void_p)]),
         "sel_nccl_unique_id": (i32, [vp]),
@@ -88,6 +91,7 @@ def lib() -> ctypes.CDLL:
         "sel_prepared_release": (None, [vp]),
         "sel_ctx_last_times": (i32, [vp, ctypes.POINTER(ctypes.c_float), ctypes.POINTER(ctypes.c_float)]),
         "sel_ctx_last_pushdown_path": (i32, [vp]),
+        "sel_ctx_last_pushdown_flags": (i32, [vp]),
         "sel_ctx_set_pushdown_path": (i32, [vp, i32]),
         "sel_pushdown": (u64, [vp, ctypes.c_char_p, sz, vp, u32, vp, vp, u64,
                                ctypes.POINTER(u64), ctypes.POINTER(u64), vp]),

@@ -27,6 +27,21 @@ _OUT_DTYPE = {INT32: torch.int32, INT64: torch.int64, FLOAT32: torch.float32, DA
               DICT8: torch.uint8, DICT16: torch.int16, DICT32: torch.int32}
 
 
+def _fit_capacity(capacity, default: int, out) -> int:
+    """Rows the kernels may write: `capacity`, or `default` when None; never more than the caller's
+    buffers hold when `out` = (rowids, [columns]) is given (a larger explicit capacity would let
+    the kernels write past them: refused)."""
+    if out is None:
+        return int(default if capacity is None else capacity)
+    rowids, outs = out
+    room = min([int(rowids.numel())] + [int(o.numel()) for o in outs])
+    if capacity is None:
+        return min(int(default), room)
+    if int(capacity) > room:
+        raise ValueError(f"capacity {capacity} exceeds the output buffers ({room} rows)")
+    return int(capacity)
+
+
 def _stream_ptr(stream, device) -> int:
     s = stream if stream is not None else torch.cuda.current_stream(device)
     return int(s.cuda_stream)
@@ -71,6 +86,12 @@ class Context:
         check(lib().sel_ctx_set_peers(self._h, nranks, rank, buf))
         self.nranks, self.rank = nranks, rank
 
+    def set_peer_timeout(self, ms: int) -> None:
+        """Bound of the peer exchange's waits (include/sel.h sel_ctx_set_peer_timeout): a rank
+        that does not take part within `ms` fails the probe (and, sticky, every later one until
+        the peers are dropped and set again) instead of hanging."""
+        check(lib().sel_ctx_set_peer_timeout(self._h, int(ms)))
+
     def drop_peers(self) -> None:
         """Unmap the other ranks' exchange buffers (every rank before any rank closes)."""
         check(lib().sel_ctx_set_peers(self._h, 0, 0, None))
@@ -101,6 +122,11 @@ class Context:
         """1: the last pushdown materialised from a kept selection; 2: two passes inside the call
         (keeping count, then 1's materialisation); 0: single pass; -1: none."""
         return int(lib().sel_ctx_last_pushdown_path(self._h))
+
+    def last_pushdown_flags(self) -> int:
+        """SEL_PD_* bits of the last materialisation from a kept selection (include/sel.h):
+        coded / whole-chunk copies / constant fills / kept values; diagnostics."""
+        return int(lib().sel_ctx_last_pushdown_flags(self._h))
 
     def set_pushdown_path(self, mode: int) -> None:
         """Path of a pushdown without a matching kept selection: -1 automatic (two passes at
@@ -172,8 +198,7 @@ class PreparedExecute:
         proj = table._col_indices(project)
         if max_size is None:
             max_size = (1 << 64) - 2
-        if capacity is None:
-            capacity = min(int(max_size), table.local_rows)
+        capacity = _fit_capacity(capacity, min(int(max_size), table.local_rows), out)
         dev = table.ctx.device
         if out is None:
             rowids = torch.empty(max(capacity, 1), dtype=torch.int32, device=dev)
@@ -365,8 +390,7 @@ class Table:
         proj = self._col_indices(project)
         if max_size is None:
             max_size = (1 << 64) - 2
-        if capacity is None:
-            capacity = min(int(max_size), self.local_rows)
+        capacity = _fit_capacity(capacity, min(int(max_size), self.local_rows), out)
         dev = self.ctx.device
         if out is None:
             rowids = torch.empty(max(capacity, 1), dtype=torch.int32, device=dev)
@@ -418,8 +442,12 @@ class Table:
         capacity is the single-pass gated form (count > capacity => truncated, see `.gated`)."""
         prog = self.program(pred)
         proj = [self.names.index(p) if isinstance(p, str) else int(p) for p in project]
-        if capacity is None:
+        if capacity is None and out is None:
             capacity = self._local_count(prog, stream, proj)
+        elif capacity is None:
+            capacity = _fit_capacity(None, self._local_count(prog, stream, proj), out)
+        else:
+            capacity = _fit_capacity(capacity, capacity, out)
         dev = self.ctx.device
         if out is None:
             rowids = torch.empty(max(capacity, 1), dtype=torch.int32, device=dev)

@@ -153,6 +153,7 @@ struct sel_ctx_s {
   void* slot_buf[kMaxKeep] = {};     // value slots, nchunks * 1024 * width bytes each
   uint64_t slot_cap[kMaxKeep] = {};  // bytes allocated per slot
   int last_pd_path = -1;
+  int last_pd_flags = 0;   // SEL_PD_* of the last materialisation from a kept selection
   bool force_single = false;
   // sel_pushdown without a kept selection: two passes (keeping count -> materialise from it) at
   // >= two_pass_min_rows local rows, else the single pass (SEL_PUSHDOWN_PATH=single|two forces)
@@ -176,6 +177,8 @@ struct sel_ctx_s {
   // the library's own exchange over peer memory (sel_ctx_set_peers; sel_internal.h PeerXchg)
   bool comm_failed = false;          // an asynchronous NCCL error aborted the communicator
   bool peers = false;
+  bool peer_failed = false;           // a peer exchange timed out: probes fail until re-set
+  uint64_t peer_timeout_ns = 10000000000ull;  // sel_ctx_set_peer_timeout
   uint64_t* peer_buf = nullptr;       // this rank's symmetric buffer (exported by CUDA IPC)
   uint64_t** peer_ptrs = nullptr;     // device array of the n buffers as mapped here
   std::vector<void*> peer_opened;     // IPC mappings to close
@@ -240,10 +243,11 @@ cudaError_t sync_stream(sel_ctx c, cudaStream_t s) {
 }
 
 // After a synchronisation that followed peer exchanges: a timed-out wait (a rank missing) is an
-// error of the call (the flag is reset).
+// error of the call, and sticky: the ranks' exchange epochs are out of step, so every later probe
+// of the context fails (plan_for) until the peers are dropped and set again (like comm_failed).
 sel_status peer_status(sel_ctx c) {
   if (c->peers && c->h_peer_err && *(volatile uint32_t*)c->h_peer_err) {
-    *(volatile uint32_t*)c->h_peer_err = 0;
+    c->peer_failed = true;
     return set_error(SEL_E_STATE, "peer exchange timed out (a rank did not take part)");
   }
   return SEL_OK;
@@ -433,6 +437,9 @@ size_t count_slots(const Plan& plan) {
 sel_status plan_for(sel_table t, const void* prog, size_t bytes, Plan* plan) {
   if (t->ctx->comm_failed)
     return set_error(SEL_E_NCCL, "the communicator failed earlier (a rank was lost); context unusable");
+  if (t->ctx->peer_failed)
+    return set_error(SEL_E_STATE, "a peer exchange failed earlier (a rank did not take part); "
+                                  "drop the peers and set them again on every rank");
   Program P;
   std::string msg;
   const int st = decode_program(prog, bytes, t->types.data(), (uint32_t)t->types.size(), &P, &msg);
@@ -707,10 +714,21 @@ sel_status sel_ctx_set_peers(sel_ctx ctx, int nranks, int rank, const void* hand
     if (ctx->peer_ptrs) cudaFree(ctx->peer_ptrs);
     ctx->peer_ptrs = nullptr;
     ctx->xg = PeerXchg{};
+    // a new group starts in step: epoch 0, an empty buffer, no failure, no stale gate word
+    // (every rank drops before any rank sets its peers again, as for the first set)
+    bool clean = true;
+    if (ctx->peer_buf)
+      clean = cudaMemset(ctx->peer_buf, 0, 2 * (size_t)kMaxPeers * kMaxXchgVals * sizeof(uint64_t)) ==
+                  cudaSuccess &&
+              cudaMemset(ctx->peer_epoch, 0, sizeof(uint32_t)) == cudaSuccess;
+    clean = clean && cudaMemset(ctx->s.result + kGateSlot, 0, 2 * sizeof(uint64_t)) == cudaSuccess &&
+            cudaDeviceSynchronize() == cudaSuccess;
+    if (ctx->h_peer_err) *(volatile uint32_t*)ctx->h_peer_err = 0;
+    ctx->peer_failed = false;
     if (ctx->peers && !ctx->comm) ctx->nranks = 1, ctx->rank = 0;
     ctx->peers = false;
     ++ctx->alloc_gen;
-    return SEL_OK;
+    return clean ? SEL_OK : set_error(SEL_E_CUDA, "resetting the exchange buffer failed");
   }
   if (!ctx || !handles || nranks < 1 || nranks > kMaxPeers || rank < 0 || rank >= nranks)
     return set_error(SEL_E_ARG, "bad peer arguments");
@@ -750,7 +768,7 @@ sel_status sel_ctx_set_peers(sel_ctx ctx, int nranks, int rank, const void* hand
   }
   ctx->peer_opened = opened;
   ctx->peer_ptrs = dptrs;
-  ctx->xg = PeerXchg{dptrs, ctx->peer_buf, ctx->peer_epoch, derr, nranks, rank};
+  ctx->xg = PeerXchg{dptrs, ctx->peer_buf, ctx->peer_epoch, derr, nranks, rank, ctx->peer_timeout_ns};
   ctx->peers = true;
   ctx->nranks = nranks;
   ctx->rank = rank;
@@ -818,6 +836,16 @@ void sel_ctx_destroy(sel_ctx c) {
   release_ctx_resources(c);
   c->destroyed = true;
   if (c->live_tables == 0) delete c;
+}
+
+sel_status sel_ctx_set_peer_timeout(sel_ctx ctx, uint64_t timeout_ms) {
+  clear_error();
+  if (!ctx || timeout_ms == 0 || timeout_ms > 3600000ull)
+    return set_error(SEL_E_ARG, "timeout must be 1 ms .. 1 h");
+  ctx->peer_timeout_ns = timeout_ms * 1000000ull;
+  ctx->xg.timeout_ns = ctx->peer_timeout_ns;
+  ++ctx->alloc_gen;   // prepared executes bake the exchange parameters: re-capture
+  return SEL_OK;
 }
 
 sel_status sel_ctx_set_timing(sel_ctx ctx, int enable) {
@@ -1008,6 +1036,9 @@ sel_status sel_ctx_last_times(sel_ctx ctx, float* count_ms, float* pushdown_ms) 
 }
 
 int sel_ctx_last_pushdown_path(sel_ctx ctx) { return ctx ? ctx->last_pd_path : -1; }
+int sel_ctx_last_pushdown_flags(sel_ctx ctx) {
+  return ctx ? (ctx->last_pd_path == 1 || ctx->last_pd_path == 2 ? ctx->last_pd_flags : 0) : -1;
+}
 
 }  // extern "C"
 
@@ -1269,15 +1300,25 @@ sel_status enqueue_pushdown_sel(sel_table t, const Plan& plan, const uint32_t* p
   };
   const uint64_t nblocks = (ntiles + kSelBlockChunks - 1) / kSelBlockChunks;
   const uint64_t units = (nblocks + kWarpsPerCta - 1) / kWarpsPerCta;
+  auto flags_of = [](const auto& p) {
+    int f = (p.coded ? SEL_PD_CODED : 0) | (p.dense_split ? SEL_PD_WHOLE_CHUNKS : 0);
+    for (uint32_t j = 0; j < p.n_proj; ++j) {
+      if (p.proj_cap_off[j] == kConstProj) f |= SEL_PD_CONSTANT;
+      else if (p.proj_cap_off[j] >= kKeptBase && p.proj_cap_off[j] < kCodedProj) f |= SEL_PD_KEPT_VALUES;
+    }
+    return f;
+  };
   int le;
   if (nproj <= (uint32_t)DevProgramSmall::kMaxProj) {
     DevProgramSmall p;
     fill_sel(&p);
+    c->last_pd_flags = flags_of(p);
     le = launch_pushdown_sel_small(p, n, out_rowids, grid_for(c, units, occupancy_pushdown_sel_small()),
                                    c->s, c->sel, stream, gate_ranks, xg, c->rank);
   } else {
     static thread_local DevProgramLarge p;
     fill_sel(&p);
+    c->last_pd_flags = flags_of(p);
     le = launch_pushdown_sel_large(p, n, out_rowids, grid_for(c, units, occupancy_pushdown_sel_large()),
                                    c->s, c->sel, stream, gate_ranks, xg, c->rank);
   }

@@ -84,16 +84,20 @@ __device__ __forceinline__ uint64_t globaltimer_ns() {
   return t;
 }
 
-// Run by all threads of ONE CTA (blockDim.x >= 32); see PeerXchg.
+// Run by all threads of ONE CTA (blockDim.x >= 32); see PeerXchg. A wait beyond x.timeout_ns (a
+// rank did not take part) fails the whole exchange: every value written to out and sums is then
+// kXchgFailed, never a partial sum.
 __device__ void peer_gather_block(const PeerXchg& x, const uint64_t* src, int k, uint64_t* out,
                                   uint64_t* sums) {
   __shared__ uint32_t s_e;
+  __shared__ int s_fail;
   __shared__ uint64_t s_v[kMaxXchgVals];
   __shared__ uint64_t s_got[kMaxPeers * kMaxXchgVals];
   const int t = threadIdx.x;
   if (t == 0) {
     s_e = *x.epoch + 1u;
     *x.epoch = s_e;
+    s_fail = 0;
   }
   if (t < k) s_v[t] = src[t];
   __syncthreads();
@@ -112,8 +116,9 @@ __device__ void peer_gather_block(const PeerXchg& x, const uint64_t* src, int k,
     if ((w >> 32) != e) {
       const uint64_t t0 = globaltimer_ns();
       while (((w = ld_acquire_sys(slot)) >> 32) != e) {
-        if (globaltimer_ns() - t0 > 10000000000ull) {  // ~10 s: a rank is missing
+        if (globaltimer_ns() - t0 > x.timeout_ns) {  // a rank is missing
           atomicExch(x.err, 1u);
+          s_fail = 1;
           w = 0;
           break;
         }
@@ -123,12 +128,13 @@ __device__ void peer_gather_block(const PeerXchg& x, const uint64_t* src, int k,
     s_got[i] = w & 0xFFFFFFFFull;
   }
   __syncthreads();
+  const bool fail = s_fail != 0;
   if (out)
-    for (int i = t; i < x.n * k; i += blockDim.x) out[i] = s_got[i];
+    for (int i = t; i < x.n * k; i += blockDim.x) out[i] = fail ? kXchgFailed : s_got[i];
   if (sums && t < k) {
     uint64_t acc = 0;
     for (int r = 0; r < x.n; ++r) acc += s_got[r * k + t];
-    sums[t] = acc;
+    sums[t] = fail ? kXchgFailed : acc;
   }
   __syncthreads();
 }
@@ -1075,6 +1081,8 @@ __global__ void __launch_bounds__(1024) superblock_prefix_kernel(const uint32_t*
                                                                  int rank) {
   const uint32_t t = threadIdx.x, lane = t & 31, warp = t >> 5;
   if (xg.n > 0) peer_gather_block(xg, out_count + kGateSlot, 1, out_count + 1, out_count + kGateSlot);
+  // a failed exchange left kXchgFailed in the gate slot: the push-down kernels write nothing
+  const bool failed = xg.n > 0 && out_count[kGateSlot] == kXchgFailed;
   if (gate_ranks > 0 && t == 0) {
     uint64_t g = 0;
     for (int r = 0; r < gate_ranks; ++r) g += out_count[1 + r];
@@ -1085,7 +1093,7 @@ __global__ void __launch_bounds__(1024) superblock_prefix_kernel(const uint32_t*
   if (t == 0) {   // this rank's position in the rank-ordered global result (sel_execute_to)
     uint64_t off = 0;
     for (int r = 0; r < rank && r < nr; ++r) off += out_count[1 + r];
-    out_count[kOffsetSlot] = off;
+    out_count[kOffsetSlot] = failed ? kXchgFailed : off;
   }
   const uint32_t per = (nsb + 1023u) / 1024u;
   const uint32_t b = min(nsb, t * per), e = min(nsb, b + per);
@@ -1207,7 +1215,8 @@ __global__ void __launch_bounds__(kThreads, SEL_PD_MINB) pushdown_sel_kernel(con
                                                                    uint64_t n, SelectionBufs sb,
                                                                    uint32_t* __restrict__ out_ids,
                                                                    const uint64_t* __restrict__ gate_count) {
-  if (p.gate && *gate_count > p.gate_max) return;  // Algorithm 1's "throw": nothing written
+  // Algorithm 1's "throw" (nothing written), or a failed peer exchange (kXchgFailed)
+  if (*gate_count == kXchgFailed || (p.gate && *gate_count > p.gate_max)) return;
   // sel_execute_to: positions in the global result start at this rank's offset (prefix kernel)
   const uint64_t goff = p.global_out ? gate_count[kOffsetSlot - kGateSlot] : 0ull;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -1323,7 +1332,7 @@ __global__ void __launch_bounds__(kThreads) dense_chunks_kernel(const __grid_con
                                                                 uint64_t n, SelectionBufs sb,
                                                                 uint32_t* __restrict__ out_ids,
                                                                 const uint64_t* __restrict__ gate_count) {
-  if (p.gate && *gate_count > p.gate_max) return;  // Algorithm 1's "throw": nothing written
+  if (*gate_count == kXchgFailed || (p.gate && *gate_count > p.gate_max)) return;  // as pushdown_sel
   if (sb.sb_sum[sb.full_slot] == 0u) return;        // the count saw no fully selected chunk
   const uint64_t goff = p.global_out ? gate_count[kOffsetSlot - kGateSlot] : 0ull;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;

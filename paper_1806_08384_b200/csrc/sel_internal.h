@@ -197,7 +197,12 @@ constexpr int kMirrorMax = 512;  // read-back mirror below kGateSlot (superblock
 // half e&1 carry epoch e (acquire loads). Values are < 2^32 (per-rank counts). A rank can run at
 // most one exchange ahead of another (it cannot finish e+1 before every rank has written e+1,
 // which each does only after finishing e), so the parity halves never mix two exchanges. A wait
-// that exceeds ~10 s sets *err (host-mapped) and gives up instead of hanging.
+// that exceeds timeout_ns (10 s unless sel_ctx_set_peer_timeout) sets *err (host-mapped) and gives
+// up instead of hanging: every gathered value and sum of that exchange becomes kXchgFailed, so the
+// gated push-down kernels that follow write nothing (a global count of kXchgFailed exceeds every
+// maxSize and they also test for it), and the host fails the call and every later probe of the
+// context (SEL_E_STATE) until the peers are dropped and set again.
+constexpr uint64_t kXchgFailed = ~0ull;
 constexpr int kMaxPeers = 32;
 constexpr int kMaxXchgVals = 32;
 struct PeerXchg {
@@ -206,6 +211,7 @@ struct PeerXchg {
   uint32_t* epoch;         // device counter, bumped once per exchange
   uint32_t* err;           // host-mapped flag: nonzero after a timed-out wait
   int n, rank;
+  uint64_t timeout_ns;     // a wait longer than this is a failed exchange
 };
 
 // Device-side scratch owned by a context.

@@ -49,6 +49,59 @@ def setup_peers(ctx: Context, group=None) -> Context:
     return ctx
 
 
+def setup_exchange(ctx: Context, mechanism: str = "peers", group=None) -> str:
+    """Join the group with one exchange mechanism that EVERY rank agrees on (collective):
+    "peers" — the library's own exchange over peer memory (CUDA IPC + NVLink stores, fused into
+    the count and push-down kernels; include/sel.h sel_ctx_set_peers) when every rank can map
+    every other rank's buffer and a real test exchange sees all ranks, else NCCL on every rank;
+    "nccl" — the library's NCCL communicator (an 8-byte all-reduce per count, an all-gather per
+    Execute). Every rank reaches every collective below whatever fails locally, so no rank is left
+    waiting and no two ranks use different mechanisms. Returns a description of the mechanism."""
+    import torch
+    from selgen.program import Const, INT32, encode   # the test exchange's one-row program
+    if mechanism not in ("peers", "nccl"):
+        raise ValueError("mechanism must be 'peers' or 'nccl'")
+    world, rank = dist.get_world_size(group), dist.get_rank(group)
+    ok, why, mapped = mechanism == "peers", f"requested {mechanism}", False
+    if ok:
+        try:
+            h = ctx.peer_handle()
+        except Exception as ex:  # noqa: BLE001 - any failure falls back to NCCL on every rank
+            h, ok, why = None, False, f"peers unavailable: {type(ex).__name__}: {ex}"
+        handles = [None] * world
+        dist.all_gather_object(handles, h, group=group)
+        if ok and all(x is not None for x in handles):
+            try:
+                ctx.set_peers(world, rank, handles)
+                mapped = True
+                one = torch.zeros(1, dtype=torch.int32, device=ctx.device)
+                probe = Table(ctx, ["x"], [INT32], [one], row_offset=rank, global_rows=world)
+                got = probe.count(encode(Const(True), [INT32]))
+                probe.release()
+                if got != world:
+                    ok, why = False, f"peer exchange counted {got} of {world}"
+            except Exception as ex:  # noqa: BLE001
+                ok, why = False, f"peers unavailable: {type(ex).__name__}: {ex}"
+        else:
+            ok = False
+            if why.startswith("requested"):
+                why = "a rank could not export its buffer"
+        on_cpu = dist.get_backend(group) == "gloo"
+        flag = torch.tensor([1 if ok else 0], dtype=torch.int32,
+                            device="cpu" if on_cpu else ctx.device)
+        dist.all_reduce(flag, op=dist.ReduceOp.MIN, group=group)
+        if not bool(flag.item()):
+            if mapped:
+                ctx.drop_peers()
+            if ok:
+                why = "another rank could not map the peers' buffers"
+            ok = False
+    if ok:
+        return "peers (CUDA IPC, NVLink release stores, fused into the count / prefix kernels)"
+    setup_comm(ctx, group)
+    return f"nccl ({why})"
+
+
 def gather_execute(table: Table, pred, project, max_size: int, root: int = 0, group=None):
     """Algorithm 1's Execute over the sharded table with the result gathered on rank `root`
     (SURVEY §8e's optional gather-to-one-rank): the root allocates the global outputs

@@ -7,14 +7,24 @@ is Listing 3.1 of the paper. Strings are mapped to dictionary
 host through the column's sorted dictionary (code order = string order); an unknown string in
 an equality/IN becomes a FALSE leaf, and string range bounds become the matching code bounds.
 Dates (datetime.date) become DATE32 days since 1970-01-01.
+
+FLOAT32 columns compare against the EXACT value of a Python constant (SQL: the binary32 value
+widened, compared with the literal). A constant float32 cannot represent exactly is never equal to
+any row, and a range bound is moved to the float32 neighbour on the side the operator needs:
+x < 0.7 becomes x <= (largest float32 below 0.7), x >= 0.7 becomes x >= (smallest float32 above
+it); = becomes FALSE, an IN drops such values, BETWEEN moves each bound inward. The program always
+carries float32 bits (include/sel.h), so this is decided here, on the host.
 """
 
 from __future__ import annotations
 
 import bisect
 import datetime
+import math
 import struct
 from dataclasses import dataclass
+
+import numpy as np
 
 INT32, INT64, FLOAT32, DATE32, DICT8, DICT16, DICT32 = 1, 2, 3, 4, 5, 6, 7
 _OPS = {"=": 0x10, "<": 0x11, ">": 0x12, "<=": 0x13, ">=": 0x14}
@@ -142,6 +152,37 @@ def col(name: str) -> Col:
 
 # ---- encoding --------------------------------------------------------------------------------
 
+def _f32_neighbours(v):
+    """(lo, hi) float32 values with lo <= v <= hi and nothing in float32 strictly between;
+    lo == hi iff v is exactly a float32 (or +-inf). NaN gives (nan, nan)."""
+    if isinstance(v, float) and math.isnan(v):
+        return float("nan"), float("nan")
+    with np.errstate(over="ignore"):
+        f = np.float32(float(v))           # nearest (double rounding for huge ints: fixed below)
+        while float(f) > v:                # Python compares int/float values exactly
+            f = np.nextafter(f, np.float32(-np.inf))
+        while float(f) < v and float(np.nextafter(f, np.float32(np.inf))) <= v:
+            f = np.nextafter(f, np.float32(np.inf))
+        if float(f) == v:
+            return float(f), float(f)
+        return float(f), float(np.nextafter(f, np.float32(np.inf)))   # f < v < next
+
+
+def _exact_f32_cmp(op, v):
+    """(op', c) with `x op v` == `x op' c` for every float32 x (c a float32), or None when the
+    leaf is constant FALSE (an inexact equality)."""
+    lo, hi = _f32_neighbours(v)
+    if lo == hi or math.isnan(lo):
+        return op, lo
+    if op == "=":
+        return None
+    if op in ("<", "<="):
+        return "<=", lo
+    return ">=", hi
+
+
+# ---- encoding --------------------------------------------------------------------------------
+
 class _Writer:
     def __init__(self, schema):
         self.schema = schema            # list of (name, type, dictionary or None)
@@ -196,8 +237,15 @@ class _Writer:
             if isinstance(e.value, str):
                 self._string_cmp(e, c, t)
                 return
-            k = self.const_slot(self.value(e.name, e.value), t)
-            self.instrs.append((_OPS[e.op], c, k, 0))
+            v, op = self.value(e.name, e.value), e.op
+            if t == FLOAT32:
+                r = _exact_f32_cmp(op, v)
+                if r is None:
+                    self.leaf_false()
+                    return
+                op, v = r
+            k = self.const_slot(v, t)
+            self.instrs.append((_OPS[op], c, k, 0))
         elif isinstance(e, _InSet):
             self.instrs.append((0x31, self.index[e.name], e.bitmap, 0))
         elif isinstance(e, _Between):
@@ -209,6 +257,9 @@ class _Writer:
                 if hi < 0 or lo > (1 << (8 * {DICT8: 1, DICT16: 2}.get(t, 4))) - 1:
                     self.leaf_false()
                     return
+            if t == FLOAT32:       # each bound inward to a float32 (exact range semantics)
+                lo = _f32_neighbours(lo)[1]
+                hi = _f32_neighbours(hi)[0]
             a = self.const_slot(lo, t)
             b = self.const_slot(hi, t)
             self.instrs.append((0x20, c, a, b))
@@ -217,6 +268,8 @@ class _Writer:
             t = self.schema[c][1]
             vals = [self.value(e.name, v) for v in e.values]
             vals = [v for v in vals if v is not None]
+            if t == FLOAT32:       # a value no float32 equals never matches
+                vals = [r[1] for r in (_exact_f32_cmp("=", v) for v in vals) if r is not None]
             if not vals:
                 self.leaf_false()
                 return
@@ -245,6 +298,10 @@ class _Writer:
         # string order == code order: x < s  <=>  code < first code >= s
         if e.op in ("<", ">="):
             bound = self.value(e.name, e.value, "lo")
+            if bound > (1 << (8 * {DICT8: 1, DICT16: 2}.get(t, 4))) - 1:
+                # s sorts after every string of a full dictionary: every code is < the bound
+                self.instrs.append((0x01 if e.op == "<" else 0x02, 0, 0, 0))
+                return
             self.instrs.append((_OPS[e.op], c, self.const_slot(bound, t), 0))
         else:  # "<=", ">": compare against the last code <= s
             bound = self.value(e.name, e.value, "hi")

@@ -199,3 +199,65 @@ def test_builder_bytes_match_generator():
     ]
     for expr, node in cases:
         assert sel.predicate.compile_predicate(expr, schema) == encode(node, types)
+
+
+def test_builder_float32_constants_exact():
+    """a FLOAT32 leaf compares the column with the EXACT constant (SQL semantics of a
+    binary32 value against a literal): builder + oracle select exactly the rows Python's exact
+    float/int comparison selects, for constants float32 cannot represent (0.7, 1e-46, 1e39,
+    2**60 + 1) and ones it can (0.5, -0.0, inf), under every operator, BETWEEN and IN."""
+    import operator
+    import struct as st
+    xs = [0.7, 0.69999999, 0.70000005, -0.7, 0.5, -0.0, 0.0, 1e-45, -1e-45, 3.4028234663852886e38,
+          float("inf"), float("-inf"), float("nan"), 2.0 ** 60, 1.0, 1e30]
+    x = np.array(xs + [float(np.nextafter(np.float32(v), np.float32(np.inf))) for v in xs[:5]]
+                 + [float(np.nextafter(np.float32(v), np.float32(-np.inf))) for v in xs[:5]],
+                 dtype=np.float32)
+    vals = [float(v) for v in x]                        # the stored binary32 values, exactly
+    schema = [("f", FLOAT32, None)]
+    cmp = {"<": operator.lt, "<=": operator.le, ">": operator.gt, ">=": operator.ge, "=": operator.eq}
+    ids = lambda e: oracle.pushdown([x], [FLOAT32], sel.predicate.compile_predicate(e, schema))[1]
+    consts = [0.7, -0.7, 1e-46, 1e39, -1e39, 2 ** 60 + 1, 2 ** 60, 0.5, -0.0, float("inf"), 1e-45,
+              0.1, 1 / 3]
+    for c in consts:
+        for op, f in cmp.items():
+            e = {"<": col("f") < c, "<=": col("f") <= c, ">": col("f") > c, ">=": col("f") >= c,
+                 "=": col("f") == c}[op]
+            want = [i for i, v in enumerate(vals) if f(v, c)]
+            np.testing.assert_array_equal(ids(e), want, err_msg=f"{op} {c!r}")
+    for lo, hi in [(0.1, 0.7), (-0.7, 1 / 3), (1e-46, 1e39), (0.5, 0.5), (0.7, 0.7)]:
+        want = [i for i, v in enumerate(vals) if lo <= v <= hi]
+        np.testing.assert_array_equal(ids(col("f").between(lo, hi)), want, err_msg=f"{lo}..{hi}")
+    want = [i for i, v in enumerate(vals) if v in (0.7, 0.5, 1e39) or v == 0.5]
+    np.testing.assert_array_equal(ids(col("f").isin([0.7, 0.5, 1e39])), want)
+    assert sel.predicate.compile_predicate(col("f").isin([0.7, 0.1]), schema) == encode(Const(False), [FLOAT32])
+    # the constant carried is a float32 (bits), so exactly representable constants pass unchanged
+    prog = sel.predicate.compile_predicate(col("f") < 0.5, schema)
+    assert st.unpack("<Q", prog[-8:])[0] == st.unpack("<I", st.pack("<f", 0.5))[0]
+
+
+def test_builder_full_dictionary_bounds_fold():
+    """a string bound sorting after every entry of a FULL DICT8 / DICT16 dictionary
+    folds to TRUE ('<') / FALSE ('>=') instead of failing to encode code 256 / 65536."""
+    for t, size in ((DICT8, 256), (DICT16, 65536)):
+        d = [f"s{i:06d}" for i in range(size)]
+        schema = [("s", t, d)]
+        cp = lambda e: sel.predicate.compile_predicate(e, schema)
+        assert cp(col("s") < "zzz") == encode(Const(True), [t])
+        assert cp(col("s") >= "zzz") == encode(Const(False), [t])
+        assert cp(col("s") < "s000001") == encode(Cmp("<", 0, 1), [t])
+        assert cp(col("s").between("a", "zzz")) == encode(Between(0, 0, size - 1), [t])
+
+
+def test_output_capacity_never_exceeds_caller_buffers():
+    """with caller buffers (out=) the capacity defaults to what they hold and an
+    explicit larger capacity is refused, so no kernel writes past a user tensor."""
+    import torch
+    from paper_1806_08384_b200.api import _fit_capacity
+    ids, cols = torch.empty(10, dtype=torch.int32), [torch.empty(7), torch.empty(12)]
+    assert _fit_capacity(None, 100, (ids, cols)) == 7
+    assert _fit_capacity(None, 5, (ids, cols)) == 5
+    assert _fit_capacity(7, 100, (ids, cols)) == 7
+    with pytest.raises(ValueError):
+        _fit_capacity(8, 100, (ids, cols))
+    assert _fit_capacity(None, 100, None) == 100 and _fit_capacity(3, 100, None) == 3

@@ -103,7 +103,7 @@ def test_shard_range_partitions():
             assert max(e - s for s, e in r) - min(e - s for s, e in r) <= 1
 
 
-# ---- bench.py's choice of exchange at N > 1 (setup_exchange): every rank must agree ----------
+# ---- the choice of exchange at N > 1 (dist.setup_exchange, used by bench.py and the example) ---
 
 def _exchange_worker(rank, world, port, scenario, q):
     import sys
@@ -113,10 +113,12 @@ def _exchange_worker(rank, world, port, scenario, q):
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
-        import bench
+        from paper_1806_08384_b200 import dist as sdist
         log = []
 
         class Ctx:
+            device = "cpu"
+
             def peer_handle(self):
                 if scenario == "handle" and rank == 1:
                     raise RuntimeError("no IPC")
@@ -141,22 +143,16 @@ def _exchange_worker(rank, world, port, scenario, q):
             def release(self):
                 pass
 
-        class Sel:
-            Table = Probe
-
-        class SDist:
-            @staticmethod
-            def setup_comm(ctx):
-                log.append("nccl")
-
-        got = bench.setup_exchange(Ctx(), Sel, SDist, dist, "cpu")
+        sdist.Table = Probe
+        sdist.setup_comm = lambda ctx, group=None: log.append("nccl")
+        got = sdist.setup_exchange(Ctx(), "nccl" if scenario == "nccl" else "peers")
         q.put((rank, got.split(" ")[0], log))
     finally:
         dist.destroy_process_group()
 
 
 @pytest.mark.parametrize("scenario,want", [("ok", "peers"), ("handle", "nccl"),
-                                           ("map", "nccl"), ("verify", "nccl")])
+                                           ("map", "nccl"), ("verify", "nccl"), ("nccl", "nccl")])
 def test_setup_exchange_agreement(scenario, want):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()

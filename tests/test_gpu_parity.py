@@ -579,9 +579,21 @@ def test_fully_selected_chunks_coded(ctx):
     node = And(Cmp("<", 0, 9_000_123), In(1, (1, 4)))
     prog = encode(node, types)
     for cap in (4_096, 5_000, 1_000_000):
+        # Algorithm 1's Execute: the keeping count records the code bits of z (projected), and
+        # the materialisation writes z from them — through the whole-chunk copy too (ADVICE r1:
+        # the capacity cut must be exercised on the CODED path, so assert that it was taken)
         want_c, want_ids, _ = oracle.pushdown(cols, types, prog, capacity=cap)
-        t.count(prog, keep_selection=True)
+        r = t.execute(prog, project=[1, 0], max_size=n, capacity=cap)
+        flags = ctx.last_pushdown_flags()
+        assert flags & sel._native.SEL_PD_CODED and flags & sel._native.SEL_PD_WHOLE_CHUNKS, flags
+        assert r.count == want_c and r.materialized and r.local_count > cap
+        np.testing.assert_array_equal(r.rowids.cpu().numpy().view(np.uint32), want_ids)
+        np.testing.assert_array_equal(r.columns[1].cpu().numpy(), z[want_ids])
+        np.testing.assert_array_equal(r.columns[0].cpu().numpy(), x[want_ids])
+        # the two passes inside sel_pushdown (no kept selection) take the coded path as well
+        _invalidate_selection(t)
         r = t.pushdown(prog, project=[1, 0], capacity=cap)
+        assert ctx.last_pushdown_path() == 2 and ctx.last_pushdown_flags() & sel._native.SEL_PD_CODED
         assert r.count == want_c and r.gated
         np.testing.assert_array_equal(r.rowids.cpu().numpy().view(np.uint32), want_ids)
         np.testing.assert_array_equal(r.columns[1].cpu().numpy(), z[want_ids])

@@ -154,3 +154,98 @@ def test_peers_with_an_empty_shard(tmp_path, cuda_device):
     """Two rows over three ranks: rank 0 holds no row, so its Execute takes the host-gated path
     while the others gate on the device — the exchange sequence must still match."""
     _run(3, 2, tmp_path)
+
+
+def _timeout_worker(rank, world, port, out_path):
+    """A rank that skips an exchange: the other rank's probe times out. Its Execute must fail with
+    SEL_E_STATE and write NOTHING (the failed exchange's sums are the failure marker, which the
+    gated push-down kernels test) — into its own outputs (phase A, rank 0 alone) and into another
+    rank's buffers through sel_execute_to (phase B, rank 1 alone); every later probe of the
+    context fails at once (sticky); after every rank drops and re-sets its peers the group works
+    again. (Each phase recovers before the next: a rank that wrote epoch e and timed out leaves
+    its row behind, which a later lone exchange of the other rank at epoch e would accept —
+    the recovery resets the epochs.)"""
+    sys.path.insert(0, ROOT)
+    import torch
+    import torch.distributed as dist
+    import paper_1806_08384_b200 as sel
+    from paper_1806_08384_b200 import dist as sdist
+    from selgen import configs
+    from selgen.program import encode
+
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank,
+                            world_size=world)
+    dev = torch.device("cuda:0")
+    torch.cuda.set_device(dev)
+    ctx = sel.Context(dev)
+    ctx.set_peer_timeout(300)
+    sdist.setup_peers(ctx)
+    n = 600_000
+    T = configs.gen_c2(n, device="cpu")
+    s, e = sdist.shard_range(n, world, rank)
+    t = sel.Table(ctx, ["A", "B", "C", "D"], T.types,
+                  [c.data[s:e].contiguous().to(dev) for c in T.columns], row_offset=s, global_rows=n)
+    prog = encode(configs.c2_probes()["listing"], T.types)
+    want = t.count(prog)                     # both ranks: a working exchange first
+    ok = [want == n // 6000 * 1002]
+
+    def fails(fn):
+        try:
+            fn()
+            return "no error"
+        except sel.SelError as ex:
+            return ex.status == sel._native.SEL_E_STATE
+
+    def recover():
+        dist.barrier()
+        ctx.drop_peers()
+        dist.barrier()
+        sdist.setup_peers(ctx)
+        ok.append(t.count(prog) == want)
+
+    # phase A: rank 0 alone; its local outputs stay untouched
+    if rank == 0:
+        ids = torch.full((want,), -7, dtype=torch.int32, device=dev)
+        d = torch.full((want,), -7, dtype=torch.int32, device=dev)
+        ok.append(fails(lambda: t.execute(prog, project=["D"], max_size=n, capacity=want,
+                                          out=(ids, [d]))))
+        torch.cuda.synchronize()
+        ok.append(bool((ids == -7).all()) and bool((d == -7).all()))
+        ok.append(fails(lambda: t.count(prog)))            # sticky
+    recover()
+    # phase B: rank 1 alone writes (would write) into rank 0's buffers over peer memory
+    root_ids = torch.full((want,), -7, dtype=torch.int32, device=dev)
+    root_d = torch.full((want,), -7, dtype=torch.int32, device=dev)
+    hs = [[ctx.export_buffer(root_ids), ctx.export_buffer(root_d)] if rank == 0 else None]
+    dist.broadcast_object_list(hs, src=0)
+    ptrs = ([root_ids.data_ptr(), root_d.data_ptr()] if rank == 0
+            else [ctx.import_buffer(h) for h in hs[0]])
+    dist.barrier()
+    if rank == 1:
+        ok.append(fails(lambda: t.execute_to(prog, ["D"], n, want, ptrs[0], ptrs[1:])))
+        torch.cuda.synchronize()
+        ok.append(fails(lambda: t.count(prog)))            # sticky
+    dist.barrier()
+    if rank == 0:
+        ok.append(bool((root_ids == -7).all()) and bool((root_d == -7).all()))   # nothing stored
+    recover()
+    r = t.execute(prog, project=["D"], max_size=n)
+    ok.append(r.materialized and r.count == want)
+    torch.cuda.synchronize()
+    res = [None] * world
+    dist.all_gather_object(res, ok)
+    if rank == 0:
+        with open(out_path, "w") as f:
+            f.write(("ok" if all(x is True for o in res for x in o) else "FAIL") + f" {res}\n")
+    t.release()
+    ctx.drop_peers()
+    dist.barrier()
+    ctx.close()
+    dist.destroy_process_group()
+
+
+def test_peer_timeout_fails_without_writing(tmp_path, cuda_device):
+    import torch.multiprocessing as mp
+    out = str(tmp_path / "timeout.txt")
+    mp.spawn(_timeout_worker, args=(2, _free_port(), out), nprocs=2, join=True)
+    assert open(out).read().startswith("ok"), open(out).read()
