@@ -42,6 +42,10 @@ def parse():
     ap.add_argument("--no-graph", action="store_true",
                     help="time table.execute() per step instead of the prepared (graph) execute")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-configs", action="store_true",
+                    help="skip the other configs' probes (c3, c5) measured beside c2")
+    ap.add_argument("--no-xchg-ab", action="store_true",
+                    help="N > 1: skip timing the other exchange mechanism")
     ap.add_argument("--e2e-steps", type=int, default=8)
     ap.add_argument("--ref-rows", type=int, default=60_000_000,
                     help="--impl reference: rows of the workload each oracle step runs on")
@@ -360,6 +364,133 @@ def run_reference(args):
 
 
 # ---- our arm ---------------------------------------------------------------------------------------
+
+def _max_over_ranks(vals, world, dev):
+    """Element-wise max over ranks of a list of floats (the device-time rule)."""
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor(vals, dtype=torch.float64, device=_red_dev(dev))
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return [float(x) for x in t]
+
+
+def time_prepared(prep, steps, world, dev):
+    """ms per prepared-Execute replay: CUDA events around `steps` replays on the current stream,
+    barrier + synchronize on both sides, max over ranks."""
+    import torch
+    import torch.distributed as dist
+    for _ in range(3):
+        prep.run()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(steps):
+        prep.run()
+    b.record()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    return _max_over_ranks([a.elapsed_time(b) / steps], world, dev)[0]
+
+
+def measure_exchange_ab(args, sel, sdist, T, names, proj_names, prog, n, s, local_count, world,
+                        dev, main_xchg):
+    """N > 1: the same prepared Execute over the other exchange mechanism (a second context), so
+    that one run measures both the library's peer-memory exchange and north_star's NCCL
+    collectives."""
+    other = "nccl" if main_xchg.startswith("peers") else "peers"
+    ctx2 = sel.Context(dev)
+    try:
+        got = sdist.setup_exchange(ctx2, other)
+    except Exception as ex:  # noqa: BLE001 - e.g. NCCL refuses two ranks on one GPU (--same-device)
+        ctx2.close()
+        return {"requested": other, "error": f"{type(ex).__name__}: {ex}"[:300]}
+    t2 = sel.Table(ctx2, names, T.types, [c.data for c in T.columns], row_offset=s, global_rows=n)
+    prep = t2.prepare_execute(prog, project=proj_names, max_size=n, capacity=max(local_count, 1))
+    ms = time_prepared(prep, args.steps, world, dev)
+    c = prep.run()
+    prep.release()
+    t2.release()
+    if got.startswith("peers"):
+        ctx2.drop_peers()
+    import torch.distributed as dist
+    dist.barrier()
+    ctx2.close()
+    return {"requested": other, "exchange": got, "ms_per_step": round(ms, 4), "count": c,
+            "steps": args.steps}
+
+
+def measure_configs(names_, args, sel, sdist, world, rank, dev, hbm):
+    """Other BASELINE.json configs in the same run: for each, the count probe's
+    latency through the public call (host clock, >= 50 warm reps, max over ranks per rep), the
+    count kernel's time (the library's CUDA events, median of 20) and roofline against the
+    measured peak, and the prepared Execute step of bench.workload's probe and projection."""
+    import torch
+    from selgen import encode
+    out = {}
+    for name in names_:
+        n, gen, node, proj, desc = workload(name, 0)
+        s, e = sdist.shard_range(n, world, rank)
+        T = gen(s, e - s, dev)
+        torch.cuda.synchronize()
+        ctx = sel.Context(dev)
+        xchg = sdist.setup_exchange(ctx, args.xchg) if world > 1 else None
+        names = [c.name for c in T.columns]
+        t = sel.Table(ctx, names, T.types, [c.data for c in T.columns], row_offset=s, global_rows=n)
+        prog = encode(node, T.types)
+        pc = prog_columns(node)
+        for _ in range(5):
+            cnt = t.count(prog)
+        lat = []
+        for _ in range(max(50, args.steps)):
+            t0 = time.perf_counter()
+            t.count(prog)
+            lat.append(1000 * (time.perf_counter() - t0))
+        lat = _max_over_ranks(lat, world, dev)
+        ctx.enable_timing(True)
+        kms = []
+        for _ in range(20):
+            t.count(prog)
+            kms.append(ctx.last_kernel_ms())
+        ctx.enable_timing(False)
+        k_ms = _max_over_ranks([statistics.median(kms)], world, dev)[0]
+        cb = (e - s) * sum(T.columns[c].width for c in pc) + 8
+        gbs = cb / (k_ms / 1000) / 1e9
+        local = t.pushdown(prog, capacity=0).local_count
+        prep = t.prepare_execute(prog, project=[names[j] for j in proj], max_size=n,
+                                 capacity=max(local, 1))
+        step_ms = time_prepared(prep, args.steps, world, dev)
+        prep.release()
+        xs = sorted(lat)
+        out[name] = {
+            "workload": desc, "global_rows": n, "rows_per_gpu": e - s, "selected": cnt,
+            "count_probe_ms": {"min": round(xs[0], 4), "median": round(statistics.median(xs), 4),
+                               "p99": round(xs[min(len(xs) - 1, int(0.99 * len(xs)))], 4),
+                               "reps": len(xs), "clock": "host, around Table.count (sel_count)"},
+            "count_kernel": {"bound": "hbm", "ms": round(k_ms, 4),
+                             "algorithmic_bytes_per_launch": int(cb),
+                             "achieved": round(gbs, 2), "peak": hbm, "unit": "GB/s",
+                             "frac": round(gbs / hbm, 4)},
+            "execute_step_ms": round(step_ms, 4),
+            "exchange": xchg}
+        if name == "c3":
+            out[name]["vs_paper_30ms"] = ("the paper's GPU probe overhead was a flat 18-28 ms "
+                                          "(PAPER.md:430, 446); this probe's median is "
+                                          f"{statistics.median(xs):.3f} ms")
+        t.release()
+        if world > 1 and xchg and xchg.startswith("peers"):
+            ctx.drop_peers()
+        if world > 1:
+            import torch.distributed as dist
+            dist.barrier()
+        ctx.close()
+        del T, t
+        torch.cuda.empty_cache()
+    return out
+
 
 _GLOO = False
 
@@ -700,6 +831,13 @@ def run_ours(args):
         if read_peak:
             r["frac_read_stream"] = round(r["achieved"] / read_peak, 4)
     roof_dom = roof_push if push_k >= count_k else roof_count
+    exchange_ab = None
+    if world > 1 and not args.no_xchg_ab:
+        exchange_ab = measure_exchange_ab(args, sel, sdist, T, names, proj_names, prog, n, s,
+                                          local_count, world, dev, xchg or "")
+    other_configs = None
+    if args.config == "c2" and not args.rows and not args.no_configs:
+        other_configs = measure_configs(["c3", "c5"], args, sel, sdist, world, rank, dev, hbm)
     if rank == 0:
         line = {
             "metric": METRIC, "value": round(value_gbs, 3), "unit": "GB/s",
@@ -734,6 +872,8 @@ def run_ours(args):
                                       and os.environ.get("SEL_DENSE_SPLIT", "1") != "0"))
                              if pd_path == 1 else 2) * args.steps,
             "cpu_baseline": cpu,
+            "exchange_ab": exchange_ab,
+            "other_configs": other_configs,
         }
         emit(line)
     if prepared is not None:

@@ -346,13 +346,26 @@ uint64_t sel_count_sampled(sel_table table, const void* prog, size_t prog_bytes,
  * (out_lo/out_hi, the column's values as int64), its rows (out_rows) and its number of distinct
  * values V(b) (out_distinct) — host arrays of nbuckets; an empty bucket (m < B) reports
  * lo = hi = 0, rows = distinct = 0. *out_sample_rows (may be NULL) = m. The
- * paper's equality estimate |sigma_{A=x}(R)| = D / V(b_x), D = T(R) / B, is host arithmetic over
- * these (Python: paper_1806_08384_b200.equi_depth_estimate).
+ * paper's equality estimate |sigma_{A=x}(R)| = D / V(b_x), D = T(R) / B, over these arrays is
+ * sel_equi_depth_estimate below.
  * Errors: SEL_E_ARG (bad stride/phase/nbuckets/column), SEL_E_TYPE (not INT32/DATE32/DICT*),
  * SEL_E_TOO_LARGE (a sample of >= 2^31 rows), SEL_E_CUDA. */
 sel_status sel_histogram(sel_table table, uint32_t col, uint32_t stride, uint32_t phase,
                          uint32_t nbuckets, int64_t* out_lo, int64_t* out_hi, uint64_t* out_rows,
                          uint64_t* out_distinct, uint64_t* out_sample_rows, void* cuda_stream);
+
+/* The synopsis estimators themselves (host arithmetic, no device work):
+ * sel_sample_estimate: the sampling estimator |sigma(R')| * |R| / |R'| of a
+ *   block-sample count (sel_count_sampled): sample_count * table_rows / sample_rows, computed in
+ *   double; 0 when sample_rows is 0.
+ * sel_equi_depth_estimate: the equi-depth equality estimate |sigma_{A=x}(R)| = D / V(b_x) with
+ *   D = table_rows / nbuckets, summed over EVERY bucket b whose [lo_b, hi_b]
+ *   holds x and V(b) > 0 (the reading under which the paper's "30/2 + 30/1 + 30/7 = 49.3" follows
+ *   the formula). lo/hi/distinct: sel_histogram's host arrays of nbuckets.
+ *   Returns the estimate; NaN for null arrays or nbuckets 0. */
+double sel_sample_estimate(uint64_t sample_count, uint64_t sample_rows, uint64_t table_rows);
+double sel_equi_depth_estimate(const int64_t* lo, const int64_t* hi, const uint64_t* distinct,
+                               uint32_t nbuckets, uint64_t table_rows, int64_t value);
 
 /* Validate a program against column types without running it (host only; no GPU needed).
  * Returns SEL_OK or the status sel_count would report for it. */

@@ -31,7 +31,8 @@ EXPORTS = ["sel_ctx_create", "sel_ctx_set_comm", "sel_nccl_unique_id", "sel_ctx_
            "sel_prepare_execute", "sel_prepared_execute", "sel_prepared_release",
            "sel_ctx_last_pushdown_path", "sel_ctx_last_pushdown_flags", "sel_ctx_set_pushdown_path", "sel_program_check",
            "sel_program_path", "sel_program_plan_json", "sel_last_error",
-           "sel_last_error_message", "sel_abi_version"]
+           "sel_last_error_message", "sel_abi_version", "sel_sample_estimate",
+           "sel_equi_depth_estimate"]
 
 
 class sel_column(ctypes.Structure):
@@ -101,6 +102,8 @@ def lib() -> ctypes.CDLL:
         "sel_last_error": (i32, []),
         "sel_last_error_message": (ctypes.c_char_p, []),
         "sel_abi_version": (i32, []),
+        "sel_sample_estimate": (ctypes.c_double, [u64, u64, u64]),
+        "sel_equi_depth_estimate": (ctypes.c_double, [vp, vp, vp, u32, u64, ctypes.c_int64]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)

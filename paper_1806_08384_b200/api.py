@@ -374,8 +374,8 @@ class Table:
                                     ctypes.byref(rows), _stream_ptr(stream, self.ctx.device))
         if r == SEL_ERR:
             raise last_error()
-        est = r * self.global_rows / rows.value if rows.value else 0.0
-        return int(r), int(rows.value), est
+        est = lib().sel_sample_estimate(int(r), int(rows.value), self.global_rows)
+        return int(r), int(rows.value), float(est)
 
     def _col_indices(self, cols):
         return [self.names.index(p) if isinstance(p, str) else int(p) for p in cols]
@@ -505,16 +505,15 @@ def program_path(prog: bytes, types: Sequence[int]) -> int:
 
 
 def equi_depth_estimate(hist: dict, value: int) -> float:
-    """The paper's equi-depth equality estimate: |sigma_{A=x}(R)| = D / V(b_x)
-    with D = T(R) / B, summed over every bucket whose [lo, hi] holds x (a value heavy enough to
-    span buckets — the reading under which the paper's "30/2 + 30/1 + 30/7 = 49.3" follows the
-    formula). A synopsis baseline to set beside the exact count."""
-    d = hist["table_rows"] / len(hist["rows"])
-    est = 0.0
-    for lo, hi, v in zip(hist["lo"], hist["hi"], hist["distinct"]):
-        if v and lo <= value <= hi:
-            est += d / float(v)
-    return est
+    """The paper's equi-depth equality estimate from a Table.histogram() result:
+    include/sel.h sel_equi_depth_estimate (D / V(b_x), D = T(R) / B, summed over every bucket whose
+    [lo, hi] holds x). A synopsis baseline to set beside the exact count."""
+    lo = np.ascontiguousarray(hist["lo"], dtype=np.int64)
+    hi = np.ascontiguousarray(hist["hi"], dtype=np.int64)
+    dv = np.ascontiguousarray(hist["distinct"], dtype=np.uint64)
+    ptr = lambda a: a.ctypes.data_as(ctypes.c_void_p)
+    return float(lib().sel_equi_depth_estimate(ptr(lo), ptr(hi), ptr(dv), len(lo),
+                                               int(hist["table_rows"]), int(value)))
 
 
 def program_plan(prog: bytes, types: Sequence[int]) -> dict:

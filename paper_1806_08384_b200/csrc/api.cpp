@@ -8,6 +8,7 @@
 #include <map>
 #include <cstdio>
 #include <cstdlib>
+#include <cmath>
 #include <cstring>
 #include <string>
 #include <thread>
@@ -1036,6 +1037,21 @@ sel_status sel_ctx_last_times(sel_ctx ctx, float* count_ms, float* pushdown_ms) 
 }
 
 int sel_ctx_last_pushdown_path(sel_ctx ctx) { return ctx ? ctx->last_pd_path : -1; }
+
+double sel_sample_estimate(uint64_t sample_count, uint64_t sample_rows, uint64_t table_rows) {
+  if (sample_rows == 0) return 0.0;
+  return (double)sample_count * (double)table_rows / (double)sample_rows;
+}
+
+double sel_equi_depth_estimate(const int64_t* lo, const int64_t* hi, const uint64_t* distinct,
+                               uint32_t nbuckets, uint64_t table_rows, int64_t value) {
+  if (!lo || !hi || !distinct || nbuckets == 0) return std::nan("");
+  const double d = (double)table_rows / (double)nbuckets;                   // D = T(R) / B
+  double est = 0.0;
+  for (uint32_t b = 0; b < nbuckets; ++b)                                   // D / V(b_x)
+    if (distinct[b] && lo[b] <= value && value <= hi[b]) est += d / (double)distinct[b];
+  return est;
+}
 int sel_ctx_last_pushdown_flags(sel_ctx ctx) {
   return ctx ? (ctx->last_pd_path == 1 || ctx->last_pd_path == 2 ? ctx->last_pd_flags : 0) : -1;
 }

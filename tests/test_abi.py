@@ -261,3 +261,28 @@ def test_output_capacity_never_exceeds_caller_buffers():
     with pytest.raises(ValueError):
         _fit_capacity(8, 100, (ids, cols))
     assert _fit_capacity(None, 100, None) == 100 and _fit_capacity(3, 100, None) == 3
+
+
+def test_synopsis_estimators_in_the_library():
+    """The NEXT(4) estimators are C entry points (sel_sample_estimate, sel_equi_depth_estimate;
+    host arithmetic, no GPU): the paper's printed 49.3 from the oracle's
+    histogram of the paper's example, and agreement with oracle/synopsis.estimate_eq on random
+    histograms; the sampling estimator |sigma(R')| |R| / |R'|."""
+    from oracle import synopsis
+    values = np.array([10] * 15 + [16] * (15 + 30 + 24) + list(range(17, 23)), np.int32)
+    h = synopsis.equi_depth(values, 3)
+    h["table_rows"] = len(values)
+    assert round(sel.equi_depth_estimate(h, 16), 1) == 49.3
+    assert sel.equi_depth_estimate(h, 11) == 15.0 and sel.equi_depth_estimate(h, 99) == 0.0
+    rng = np.random.default_rng(12)
+    for _ in range(200):
+        v = rng.integers(-50, 50, int(rng.integers(1, 400))).astype(np.int32)
+        B = int(rng.integers(1, 20))
+        h = synopsis.equi_depth(v, B)
+        h["table_rows"] = int(rng.integers(len(v), 10 * len(v) + 1))
+        for x in rng.integers(-60, 60, 5):
+            want = synopsis.estimate_eq(h, int(x), h["table_rows"])
+            assert abs(sel.equi_depth_estimate(h, int(x)) - want) <= 1e-9 * max(1.0, want)
+    L = _native.lib()
+    assert L.sel_sample_estimate(7, 100, 1000) == 70.0 and L.sel_sample_estimate(5, 0, 10) == 0.0
+    assert math.isnan(L.sel_equi_depth_estimate(None, None, None, 0, 10, 1))

@@ -32,6 +32,8 @@ def test_bench_two_ranks_same_device(cuda_device):
     assert d["n_gpus"] == 2 and d["config"]["selected"] == 100_200
     assert d["config"]["exchange"].startswith("peers")
     assert d["e2e"]["h2d_bytes_per_step"] > 0 and d["value"] > 0
+    ab = d["exchange_ab"]          # the other mechanism, timed in the same run (NCCL refuses two
+    assert ab["requested"] == "nccl" and ("ms_per_step" in ab or "error" in ab)   # ranks per GPU)
 
 
 def test_multi_gpu_example_two_ranks(cuda_device):
