@@ -134,7 +134,8 @@ struct sel_ctx_s {
   int num_sms = 148;
   int occ_count_small = 1, occ_count_large = 1;
   Scratch s{};
-  uint64_t* h_result = nullptr;   // pinned mirror of Scratch::result (kResultSlots)
+  uint64_t* h_result = nullptr;   // pinned mirror of Scratch::result (kResultSlots), mapped:
+  uint64_t* h_result_dev = nullptr;   // its device address (kernels store the Execute's words)
   uint64_t ticket_base = 0;
   uint32_t epoch = 0;
   ncclComm_t comm = nullptr;
@@ -482,8 +483,7 @@ sel_status ensure_selection(sel_ctx c, uint64_t nchunks) {
   if (c->sel.bits) cudaFree(c->sel.bits);
   if (c->sel.which) cudaFree(c->sel.which);
   if (c->sel.chunk_cnt) cudaFree(c->sel.chunk_cnt);
-  if (c->sel.sb_sum) cudaFree(c->sel.sb_sum);
-  if (c->sel.sb_prefix) cudaFree(c->sel.sb_prefix);
+  if (c->sel.sb_sum) cudaFree(c->sel.sb_sum);   // the base of the sums / prefix / state block
   c->sel = SelectionBufs{};
   c->sel.code_col = -1;
   c->sel_cap_chunks = 0;
@@ -491,12 +491,23 @@ sel_status ensure_selection(sel_ctx c, uint64_t nchunks) {
   ++c->alloc_gen;
   const uint64_t cap = std::max<uint64_t>(nchunks, 1024);
   const uint64_t nsb = (cap + kSbChunks - 1) / kSbChunks;
+  const uint64_t nhb = (cap + kHbChunks - 1) / kHbChunks;
   c->kept_cols.clear();
   cudaError_t e = cudaMalloc(&c->sel.bits, cap * 32 * sizeof(uint32_t));
   if (e == cudaSuccess) e = cudaMalloc(&c->sel.which, cap * 32 * sizeof(uint32_t));
   if (e == cudaSuccess) e = cudaMalloc(&c->sel.chunk_cnt, cap * sizeof(uint16_t));
-  if (e == cudaSuccess) e = cudaMalloc(&c->sel.sb_sum, (nsb + 1) * sizeof(uint32_t));   // + full flag
-  if (e == cudaSuccess) e = cudaMalloc(&c->sel.sb_prefix, nsb * sizeof(uint32_t));
+  // one block: superblock sums (two halves) | hyperblock prefix (+ local count, flag) | state;
+  // all zero to start with (sel_internal.h SelectionBufs)
+  const uint64_t stride = (nsb + 3) & ~3ull;
+  const uint64_t words = 2 * stride + ((nhb + 2 + 3) & ~3ull) + 4;
+  if (e == cudaSuccess) e = cudaMalloc(&c->sel.sb_sum, words * sizeof(uint32_t));
+  if (e == cudaSuccess) e = cudaMemset(c->sel.sb_sum, 0, words * sizeof(uint32_t));
+  if (e == cudaSuccess) e = cudaDeviceSynchronize();
+  if (e == cudaSuccess) {
+    c->sel.sb_stride = (uint32_t)stride;
+    c->sel.hb_prefix = c->sel.sb_sum + 2 * stride;
+    c->sel.state = c->sel.hb_prefix + ((nhb + 2 + 3) & ~3ull);
+  }
   if (e != cudaSuccess) return set_error(SEL_E_CUDA, cuda_msg("cudaMalloc(selection)", e));
   c->sel_cap_chunks = cap;
   return SEL_OK;
@@ -574,7 +585,8 @@ sel_status sel_ctx_create(int cuda_device, sel_ctx* out) {
               cudaMalloc(&c->s.done, sizeof(unsigned int)) == cudaSuccess &&
               cudaMalloc(&c->s.result, kResultSlots * sizeof(uint64_t)) == cudaSuccess &&
               cudaMalloc(&c->s.ticket, sizeof(unsigned long long)) == cudaSuccess &&
-              cudaMallocHost(&c->h_result, kResultSlots * sizeof(uint64_t)) == cudaSuccess &&
+              cudaHostAlloc(&c->h_result, kResultSlots * sizeof(uint64_t), cudaHostAllocMapped) == cudaSuccess &&
+              cudaHostGetDevicePointer(reinterpret_cast<void**>(&c->h_result_dev), c->h_result, 0) == cudaSuccess &&
               cudaMemset(c->s.done, 0, sizeof(unsigned int)) == cudaSuccess &&
               cudaMemset(c->s.ticket, 0, sizeof(unsigned long long)) == cudaSuccess &&
               cudaMemset(c->s.result, 0, kResultSlots * sizeof(uint64_t)) == cudaSuccess &&
@@ -808,7 +820,6 @@ void release_ctx_resources(sel_ctx c) {
   if (c->sel.which) cudaFree(c->sel.which);
   if (c->sel.chunk_cnt) cudaFree(c->sel.chunk_cnt);
   if (c->sel.sb_sum) cudaFree(c->sel.sb_sum);
-  if (c->sel.sb_prefix) cudaFree(c->sel.sb_prefix);
   c->sel = SelectionBufs{};
   c->sel_cap_chunks = 0;
   c->kept_table = nullptr;
@@ -1143,7 +1154,7 @@ sel_status reserve_selection(sel_table t, uint64_t nchunks,
 sel_status enqueue_count(sel_table t, const Plan& plan, uint32_t flags, const uint32_t* keep_cols,
                          uint32_t nkeep, cudaStream_t stream, uint64_t* d_out,
                          bool allreduce = true, const uint32_t* code_cols = nullptr,
-                         uint32_t ncode = 0) {
+                         uint32_t ncode = 0, const ExecFinish* fin = nullptr) {
   sel_ctx c = t->ctx;
   const uint64_t n = t->local_rows;
   const bool scan = n > 0 && plan.path != PATH_CONST;
@@ -1156,10 +1167,6 @@ sel_status enqueue_count(sel_table t, const Plan& plan, uint32_t flags, const ui
     std::vector<int> cap_off(t->cols.size(), -1);
     if (flags & SEL_KEEP_SELECTION) {
       if (ensure_selection(c, nchunks) != SEL_OK) return g_status;
-      const uint64_t nsb = (nchunks + kSbChunks - 1) / kSbChunks;
-      c->sel.full_slot = (uint32_t)nsb;   // the flag word right after this table's sums
-      e = cudaMemsetAsync(c->sel.sb_sum, 0, (nsb + 1) * sizeof(uint32_t), stream);
-      if (e != cudaSuccess) return set_error(SEL_E_CUDA, cuda_msg("cudaMemsetAsync(selection)", e));
       c->kept_table = nullptr;  // valid again only once this probe has completed
       c->kept_cols.clear();
       // projected predicate columns: capture while evaluating, keep the selected values
@@ -1203,7 +1210,8 @@ sel_status enqueue_count(sel_table t, const Plan& plan, uint32_t flags, const ui
     const size_t dyn = keep ? (size_t)keep->warp_smem * kWarpsPerCta : 0;
     Scratch s = c->s;
     s.result = d_out;
-    s.xg = (c->peers && allreduce) ? c->xg : PeerXchg{};   // the exchange fused into the count
+    // the exchange fused into the count (for an Execute inside its finish, `fin`)
+    s.xg = (c->peers && (allreduce || fin)) ? c->xg : PeerXchg{};
     if (c->timing) record(c, c->ev0, stream);
     int le;
     if (fits_block<DevProgramSmall>(plan, nslots, 0)) {
@@ -1240,7 +1248,7 @@ sel_status enqueue_count(sel_table t, const Plan& plan, uint32_t flags, const ui
       if (p.fast_n && !p.bm_smem) occ = occupancy_count_fast((int)p.fast_n, keep != nullptr, dyn);
       const int nw = pick_count_warps(c, p, dyn, occ);
       le = launch_count_small(p, n, grid_for(c, nw == kWarpsPerCta ? units : (nchunks + nw - 1) / nw,
-                                             nw == kWarpsPerCta ? occ : 1), s, keep, stream, nw);
+                                             nw == kWarpsPerCta ? occ : 1), s, keep, stream, nw, fin);
     } else {
       static thread_local DevProgramLarge p;
       pack(plan, t, &p);
@@ -1252,7 +1260,7 @@ sel_status enqueue_count(sel_table t, const Plan& plan, uint32_t flags, const ui
                            : (p.bm_smem ? occupancy_count_dyn_large(p.bm_smem) : c->occ_count_large);
       const int nw = pick_count_warps(c, p, dyn, occ);
       le = launch_count_large(p, n, grid_for(c, nw == kWarpsPerCta ? units : (nchunks + nw - 1) / nw,
-                                             nw == kWarpsPerCta ? occ : 1), s, keep, stream, nw);
+                                             nw == kWarpsPerCta ? occ : 1), s, keep, stream, nw, fin);
     }
     if (le != cudaSuccess) return set_error(SEL_E_CUDA, cuda_msg("count kernel launch", (cudaError_t)le));
     if (c->timing) record(c, c->ev1, stream);
@@ -1279,7 +1287,8 @@ sel_status enqueue_pushdown_sel(sel_table t, const Plan& plan, const uint32_t* p
                                 uint32_t nproj, uint32_t* out_rowids, void* const* out_cols,
                                 uint64_t capacity_rows, bool gate, uint64_t gate_max,
                                 cudaStream_t stream, int gate_ranks = 0,
-                                const PeerXchg* xg = nullptr, bool global_out = false) {
+                                const PeerXchg* xg = nullptr, bool global_out = false,
+                                bool finished = false, uint64_t* host = nullptr) {
   sel_ctx c = t->ctx;
   const auto consts = const_columns(t, plan);
   const uint64_t n = t->local_rows;
@@ -1330,13 +1339,13 @@ sel_status enqueue_pushdown_sel(sel_table t, const Plan& plan, const uint32_t* p
     fill_sel(&p);
     c->last_pd_flags = flags_of(p);
     le = launch_pushdown_sel_small(p, n, out_rowids, grid_for(c, units, occupancy_pushdown_sel_small()),
-                                   c->s, c->sel, stream, gate_ranks, xg, c->rank);
+                                   c->s, c->sel, stream, gate_ranks, xg, c->rank, finished, host);
   } else {
     static thread_local DevProgramLarge p;
     fill_sel(&p);
     c->last_pd_flags = flags_of(p);
     le = launch_pushdown_sel_large(p, n, out_rowids, grid_for(c, units, occupancy_pushdown_sel_large()),
-                                   c->s, c->sel, stream, gate_ranks, xg, c->rank);
+                                   c->s, c->sel, stream, gate_ranks, xg, c->rank, finished, host);
   }
   if (le != cudaSuccess) return set_error(SEL_E_CUDA, cuda_msg("push-down kernel launch", (cudaError_t)le));
   c->last_pd_path = 1;
@@ -1367,45 +1376,41 @@ sel_status gather_counts(sel_ctx c, uint64_t local, void* cuda_stream) {
   return peer_status(c);
 }
 
-// The device work of a device-gated Execute on `stream` (sel_execute, prepared executes): count
-// keeping the selection (local count -> result[kGateSlot]); with a communicator the all-gather of
-// the per-rank counts into result[1..nranks] (the prefix kernel then sums them into
-// result[kGateSlot]); the gated materialisation; D2H copies of result[kGateSlot] and of the
-// per-rank counts (result[1..nranks]) or the local count (result[0]).
+// The device work of a device-gated Execute on `stream` (sel_execute, prepared executes): the
+// count keeping the selection (local count -> result[kGateSlot]) whose last CTA also leaves the
+// superblock prefix and — without NCCL — finishes the result words (ExecFinish: the peer exchange,
+// the gate count, the mirror and the offset, stored into the pinned host mirror too); with NCCL
+// the all-gather of the per-rank counts into result[1..nranks] and a 1-CTA kernel finishing the
+// same words; then the gated materialisation. No copy: the host reads its pinned mirror after its
+// one synchronisation (more than kMirrorMax ranks: two D2H copies instead).
 sel_status enqueue_execute(sel_table t, const Plan& plan, const uint32_t* proj, uint32_t nproj,
                            uint32_t nkeep, uint64_t max_size, uint32_t* out_rowids,
                            void* const* outs, uint64_t capacity, cudaStream_t s,
                            bool global_out = false) {
   sel_ctx c = t->ctx;
+  const bool nccl_gate = c->comm && !c->peers;
+  const int nr = multi(c) ? c->nranks : 0;
+  uint64_t* host = nr <= kMirrorMax ? c->h_result_dev : nullptr;
+  const ExecFinish fin{c->s.result, host, 0, c->rank};
   sel_status st = enqueue_count(t, plan, SEL_KEEP_SELECTION, proj, nkeep, s, c->s.result + kGateSlot,
-                                false, proj, nproj);
+                                false, proj, nproj, nccl_gate ? nullptr : &fin);
   if (st != SEL_OK) return st;
-  if (c->comm && !c->peers) {  // SURVEY §8a a4 + a7 in one collective
+  if (nccl_gate) {  // SURVEY §8a a4 + a7 in one collective
     ncclResult_t r = nccl().AllGather(c->s.result + kGateSlot, c->s.result + 1, 1, ncclUint64,
                                       c->comm, s);
     if (r != ncclSuccess) return set_error(SEL_E_NCCL, nccl_msg("ncclAllGather", r));
   }
   if (c->timing) record(c, c->ev2, s);
-  // with peers the exchange runs inside the prefix kernel, right before the gated push-down
   st = enqueue_pushdown_sel(t, plan, proj, nproj, out_rowids, outs, capacity, true, max_size, s,
-                            c->comm && !c->peers ? c->nranks : 0, c->peers ? &c->xg : nullptr,
-                            global_out);
+                            nccl_gate ? c->nranks : 0, nullptr, global_out, !nccl_gate, host);
   if (st != SEL_OK) return st;
   if (c->timing) record(c, c->ev3, s);
-  // one copy: the prefix kernel mirrored the words read back right below the gate slot
-  const int nr = multi(c) ? c->nranks : 0;
-  cudaError_t e;
-  if (nr <= kMirrorMax) {
-    const int lo = kGateSlot - (nr > 0 ? nr : 1);
-    e = cudaMemcpyAsync(c->h_result + lo, c->s.result + lo, (kGateSlot + 1 - lo) * sizeof(uint64_t),
+  if (host) return SEL_OK;
+  cudaError_t e = cudaMemcpyAsync(c->h_result + kGateSlot, c->s.result + kGateSlot, sizeof(uint64_t),
+                                  cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess)
+    e = cudaMemcpyAsync(c->h_result + 1, c->s.result + 1, nr * sizeof(uint64_t),
                         cudaMemcpyDeviceToHost, s);
-  } else {
-    e = cudaMemcpyAsync(c->h_result + kGateSlot, c->s.result + kGateSlot, sizeof(uint64_t),
-                        cudaMemcpyDeviceToHost, s);
-    if (e == cudaSuccess)
-      e = cudaMemcpyAsync(c->h_result + 1, c->s.result + 1, nr * sizeof(uint64_t),
-                          cudaMemcpyDeviceToHost, s);
-  }
   if (e != cudaSuccess) return set_error(SEL_E_CUDA, cuda_msg("cudaMemcpyAsync (execute)", e));
   return SEL_OK;
 }
@@ -1468,8 +1473,16 @@ uint64_t sel_count_ex(sel_table t, const void* prog, size_t prog_bytes, uint32_t
   const bool scan = n > 0 && plan.path != PATH_CONST;
   if ((flags & SEL_KEEP_SELECTION) && !scan) c->kept_table = nullptr;
   if (!scan && !multi(c)) return plan.path == PATH_CONST && plan.const_value ? n : 0;
-  if (enqueue_count(t, plan, flags, keep_cols, nkeep, stream, c->s.result) != SEL_OK) return SEL_ERR;
-  cudaError_t e = cudaMemcpyAsync(c->h_result, c->s.result, sizeof(uint64_t), cudaMemcpyDeviceToHost, stream);
+  // without an NCCL all-reduce after it the count kernel stores the count into the pinned host
+  // word itself (ExecFinish::host); otherwise one 8-byte copy follows the collective
+  const bool direct = scan && !(c->comm && !c->peers);
+  const ExecFinish fin{nullptr, c->h_result_dev, 0, c->rank};
+  if (enqueue_count(t, plan, flags, keep_cols, nkeep, stream, c->s.result, true, nullptr, 0,
+                    direct ? &fin : nullptr) != SEL_OK)
+    return SEL_ERR;
+  cudaError_t e = direct ? cudaSuccess
+                         : cudaMemcpyAsync(c->h_result, c->s.result, sizeof(uint64_t),
+                                           cudaMemcpyDeviceToHost, stream);
   if (e == cudaSuccess) e = sync_stream(c, stream);
   if (e != cudaSuccess) return fail64(sync_code(e), cuda_msg("count result", e));
   if (peer_status(c) != SEL_OK) return SEL_ERR;

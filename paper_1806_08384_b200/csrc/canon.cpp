@@ -90,45 +90,46 @@ int decode_program(const void* bytes, size_t len, const int* types, uint32_t nco
   for (unsigned i = 0; i < n_instr; ++i) {
     const uint8_t* q = b + kHeader + kSlot * i;
     Instr in{q[0], q[1], le16(q + 2), le16(q + 4)};
-    const std::string at = " at instruction " + std::to_string(i);
-    if (le16(q + 6) != 0) return fail(S_E_PROGRAM, "instruction reserved field nonzero" + at);
+    // the position suffix of an error message (built only on failure: no allocation per probe)
+    const auto at = [i] { return " at instruction " + std::to_string(i); };
+    if (le16(q + 6) != 0) return fail(S_E_PROGRAM, "instruction reserved field nonzero" + at());
     const bool leaf = is_leaf_op(in.op);
     const bool logic = in.op == OP_TRUE || in.op == OP_FALSE || in.op == OP_AND ||
                        in.op == OP_OR || in.op == OP_NOT;
-    if (!leaf && !logic) return fail(S_E_PROGRAM, "unknown opcode" + at);
+    if (!leaf && !logic) return fail(S_E_PROGRAM, "unknown opcode" + at());
     if (logic && (in.col | in.a | in.b) != 0)
-      return fail(S_E_PROGRAM, "logic opcode with nonzero operands" + at);
+      return fail(S_E_PROGRAM, "logic opcode with nonzero operands" + at());
     if (leaf) {
-      if (in.col >= ncols) return fail(S_E_PROGRAM, "column index out of range" + at);
+      if (in.col >= ncols) return fail(S_E_PROGRAM, "column index out of range" + at());
       if (in.op == OP_BETWEEN) {
         if (in.a >= n_consts || in.b >= n_consts)
-          return fail(S_E_PROGRAM, "BETWEEN constant out of range" + at);
+          return fail(S_E_PROGRAM, "BETWEEN constant out of range" + at());
       } else if (in.op == OP_IN) {
         if (in.b == 0 || in.b > kMaxIn || (unsigned)in.a + in.b > n_consts)
-          return fail(S_E_PROGRAM, "IN list out of range" + at);
+          return fail(S_E_PROGRAM, "IN list out of range" + at());
       } else if (in.op == OP_IN_BITMAP) {
-        if (in.b != 0) return fail(S_E_PROGRAM, "IN_BITMAP with nonzero b" + at);
+        if (in.b != 0) return fail(S_E_PROGRAM, "IN_BITMAP with nonzero b" + at());
       } else if (in.b != 0 || in.a >= n_consts) {
-        return fail(S_E_PROGRAM, "comparison constant out of range" + at);
+        return fail(S_E_PROGRAM, "comparison constant out of range" + at());
       }
     }
     const unsigned need = in.op == OP_AND || in.op == OP_OR ? 2u : in.op == OP_NOT ? 1u : 0u;
-    if (depth < need) return fail(S_E_PROGRAM, "stack underflow" + at);
+    if (depth < need) return fail(S_E_PROGRAM, "stack underflow" + at());
     depth = depth - need + 1;
-    if (depth > kMaxDepth) return fail(S_E_PROGRAM, "stack deeper than 16" + at);
+    if (depth > kMaxDepth) return fail(S_E_PROGRAM, "stack deeper than 16" + at());
     if (leaf) {
       const int t = types[in.col];
       unsigned first = in.a, last = in.a;
       if (in.op == OP_IN) last = in.a + in.b - 1u;
       if (in.op == OP_IN_BITMAP) {
-        if (t == T_FLOAT32) return fail(S_E_TYPE, "IN_BITMAP on a FLOAT32 column" + at);
+        if (t == T_FLOAT32) return fail(S_E_TYPE, "IN_BITMAP on a FLOAT32 column" + at());
       } else if (in.op == OP_BETWEEN) {
         if (!fits(t, out->consts[in.a]) || !fits(t, out->consts[in.b]))
-          return fail(S_E_TYPE, "BETWEEN constant not representable in its column" + at);
+          return fail(S_E_TYPE, "BETWEEN constant not representable in its column" + at());
       } else {
         for (unsigned k = first; k <= last; ++k)
           if (!fits(t, out->consts[k]))
-            return fail(S_E_TYPE, "constant not representable in its column" + at);
+            return fail(S_E_TYPE, "constant not representable in its column" + at());
       }
     }
     out->ins[i] = in;

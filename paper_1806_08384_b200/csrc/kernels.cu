@@ -19,6 +19,10 @@
 // lost). Every loop enclosing eval_leaf is therefore kept rolled; tests/test_gpu_parity.py
 // exercises multi-interval leaves of every width in both kernels.
 #include <cuda_runtime.h>
+
+#include <map>
+#include <mutex>
+#include <tuple>
 #include <stdint.h>
 
 #include <type_traits>
@@ -27,9 +31,6 @@
 
 #include "sel_internal.h"
 
-#ifndef SEL_SB_ATOMICS
-#define SEL_SB_ATOMICS 1   // 0: superblock sums by a separate kernel (measured equal, one more launch)
-#endif
 
 namespace sel {
 namespace {
@@ -137,6 +138,124 @@ __device__ void peer_gather_block(const PeerXchg& x, const uint64_t* src, int k,
     sums[t] = fail ? kXchgFailed : acc;
   }
   __syncthreads();
+}
+
+// ExecFinish (sel_internal.h), run by all threads of ONE CTA; `local` = this rank's count, already
+// in R[kGateSlot] when an exchange (xg.n > 0) or no rank combination (gate_ranks == 0) follows.
+__device__ void finish_execute(const ExecFinish& f, const PeerXchg& xg, uint64_t local) {
+  uint64_t* R = f.result;
+  const uint32_t t = threadIdx.x;
+  if (xg.n > 0) peer_gather_block(xg, R + kGateSlot, 1, R + 1, R + kGateSlot);  // ends in a barrier
+  // a failed exchange left kXchgFailed in the gate slot: the push-down kernels write nothing
+  const bool failed = xg.n > 0 && R[kGateSlot] == kXchgFailed;
+  const int nr = xg.n > 0 ? xg.n : f.gate_ranks;
+  if (t == 0) {
+    if (f.gate_ranks > 0 && xg.n == 0) {   // NCCL: the all-gathered counts are summed here
+      uint64_t g = 0;
+      for (int r = 0; r < f.gate_ranks; ++r) g += R[1 + r];
+      R[kGateSlot] = g;
+    }
+    uint64_t off = 0;   // this rank's position in the rank-ordered global result (sel_execute_to)
+    for (int r = 0; r < f.rank && r < nr; ++r) off += R[1 + r];
+    R[kOffsetSlot] = failed ? kXchgFailed : off;
+    if (nr == 0) R[kGateSlot - 1] = local;
+  }
+  if (nr > 0 && nr <= kMirrorMax)
+    for (int i = (int)t; i < nr; i += (int)blockDim.x) R[kGateSlot - nr + i] = R[1 + i];
+  if (f.host) {   // the pinned mirror: the host reads it after its one synchronisation
+    __syncthreads();
+    const int lo = kGateSlot - (nr > 0 ? nr : 1);
+    for (int i = lo + (int)t; i <= kOffsetSlot; i += (int)blockDim.x) f.host[i] = R[i];
+  }
+}
+
+// The kept selection's half of the superblock sums (sel_internal.h SelectionBufs), after its count.
+__device__ __forceinline__ const uint32_t* kept_sb(const SelectionBufs& sb) {
+  return sb.sb_sum + (size_t)((sb.state[0] - 1u) & 1u) * sb.sb_stride;
+}
+
+// Output position of chunk c0's first selected row in the local result: hyperblock prefix +
+// superblock sums before c0 within its hyperblock + chunk counts before c0 within its superblock
+// (every lane; loads issued together).
+__device__ __forceinline__ uint64_t kept_base(const SelectionBufs& sb, const uint32_t* sbs,
+                                              uint64_t c0, int lane) {
+  const uint64_t s0 = c0 >> kSbShift, first = s0 << kSbShift;
+  const uint64_t sfirst = (c0 >> kHbShift) << (kHbShift - kSbShift);
+  uint32_t part = 0;
+  if (first + lane < c0) part += sb.chunk_cnt[first + lane];
+  if (first + 32 + lane < c0) part += sb.chunk_cnt[first + 32 + lane];
+  if (sfirst + lane < s0) part += sbs[sfirst + lane];
+  if (sfirst + 32 + lane < s0) part += sbs[sfirst + 32 + lane];
+  const uint32_t hp = sb.hb_prefix[c0 >> kHbShift];
+  return (uint64_t)hp + __reduce_add_sync(0xFFFFFFFFu, part);
+}
+
+// The last CTA of a keeping count (NW warps): the exclusive prefix of the hyperblock sums, each
+// summed here from this count's superblock sums (thread t sums whole hyperblocks with 16-byte
+// loads, all issued together; <= 4 per thread), the local count and the full-chunk flag beside
+// it, and the epoch advanced (this count's half of the superblock sums becomes the selection's;
+// the next count zeroes the other one, nsb words).
+template <int NW>
+__device__ void finish_selection(const SelectionBufs& sb, uint64_t n, uint32_t local, uint32_t e,
+                                 const uint32_t* my_sb) {
+  constexpr uint32_t T = NW * 32;
+  constexpr uint32_t kSbPerHb = 1u << (kHbShift - kSbShift);
+  const uint32_t t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  const uint64_t nchunks = (n + kChunkRows - 1) / kChunkRows;
+  const uint32_t nsb = (uint32_t)((nchunks + kSbChunks - 1) / kSbChunks);
+  const uint32_t nsb4 = (nsb + 3u) & ~3u;   // the half is zero-padded to a multiple of 4 words
+  const uint32_t nhb = (uint32_t)((nchunks + kHbChunks - 1) / kHbChunks);
+  const uint32_t per = (nhb + T - 1) / T;   // <= 4: nhb <= 1024 (tables < 2^32 rows)
+  const uint32_t b = min(nhb, t * per), end = min(nhb, b + per);
+  const uint4* q = reinterpret_cast<const uint4*>(my_sb);
+  uint32_t v[4], sum = 0;
+#pragma unroll
+  for (uint32_t k = 0; k < 4; ++k) {
+    v[k] = 0u;
+    if (b + k < end) {
+      const uint32_t w0 = (b + k) * kSbPerHb;
+      uint4 x[kSbPerHb / 4];
+#pragma unroll
+      for (uint32_t i = 0; i < kSbPerHb / 4; ++i)
+        x[i] = w0 + 4 * i < nsb4 ? __ldcg(q + w0 / 4 + i) : make_uint4(0, 0, 0, 0);
+#pragma unroll
+      for (uint32_t i = 0; i < kSbPerHb / 4; ++i) v[k] += x[i].x + x[i].y + x[i].z + x[i].w;
+    }
+    sum += v[k];
+  }
+  uint32_t incl = sum;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const uint32_t x = __shfl_up_sync(0xFFFFFFFFu, incl, d);
+    if (lane >= (uint32_t)d) incl += x;
+  }
+  __shared__ uint32_t s_w[NW];
+  if (lane == 31) s_w[warp] = incl;
+  __syncthreads();
+  if (warp == 0) {
+    const uint32_t w = lane < (uint32_t)NW ? s_w[lane] : 0u;
+    uint32_t wi = w;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const uint32_t x = __shfl_up_sync(0xFFFFFFFFu, wi, d);
+      if (lane >= (uint32_t)d) wi += x;
+    }
+    if (lane < (uint32_t)NW) s_w[lane] = wi - w;
+  }
+  __syncthreads();
+  uint32_t run = s_w[warp] + incl - sum;
+#pragma unroll
+  for (uint32_t k = 0; k < 4; ++k) {
+    if (b + k < end) sb.hb_prefix[b + k] = run;
+    run += v[k];
+  }
+  if (t == 0) {
+    sb.hb_prefix[nhb] = local;
+    sb.hb_prefix[nhb + 1] = __ldcg(sb.state + 3);   // the full-chunk flag, reset for the next count
+    sb.state[3] = 0u;
+    sb.state[1 + (e & 1u)] = nsb;
+    sb.state[0] = e + 1u;
+  }
 }
 
 // Prefetch every predicate column of chunk `c` into L2 (issued by one lane a chunk ahead).
@@ -798,19 +917,33 @@ __device__ __forceinline__ uint32_t to_row_major(uint32_t m, int lane) {
 }
 
 __device__ __forceinline__ void st_evict_last(uint32_t* p, uint32_t v) {
+#if SEL_AB_PLAINST == 1   // A/B: a plain store
+  *p = v;
+#elif SEL_AB_PLAINST == 2   // A/B: the hinted store without the compiler memory barrier
+  uint64_t pol;
+  asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+  asm volatile("st.global.L2::cache_hint.u32 [%0], %1, %2;" ::"l"(p), "r"(v), "l"(pol));
+#else
   uint64_t pol;
   asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
   asm volatile("st.global.L2::cache_hint.u32 [%0], %1, %2;" ::"l"(p), "r"(v), "l"(pol) : "memory");
+#endif
 }
 
 // coded: also keep the coded leaf's point-1 matches (wm, the count's quad layout) row-major.
 template <class P, bool KEEP>
 // Returns the chunk's selected-row count (every lane; 0 without KEEP).
-__device__ __forceinline__ uint32_t keep_chunk(const SelectionBufs& sb, uint64_t c, int lane, uint32_t m,
-                                               char* wsmem, uint32_t wm = 0u, bool coded = false) {
+__device__ __forceinline__ uint32_t keep_chunk(const SelectionBufs& sb, uint32_t* sbs, uint64_t c, int lane,
+                                               uint32_t m, char* wsmem, uint32_t wm = 0u,
+                                               bool coded = false) {
   if (!KEEP) return 0u;
+#if SEL_KEEP_QUAD   // A/B only (timing of the transposition; the push-down needs row-major)
+  if (coded) st_evict_last(sb.which + c * 32 + lane, wm);
+  const uint32_t t = m;
+#else
   if (coded) st_evict_last(sb.which + c * 32 + lane, to_row_major(wm, lane));
   const uint32_t t = to_row_major(m, lane);          // the push-down stages from row-major masks
+#endif
   if (sb.n_keep) {
     sb.bits[c * 32 + lane] = t;
   } else {
@@ -818,7 +951,9 @@ __device__ __forceinline__ uint32_t keep_chunk(const SelectionBufs& sb, uint64_t
     // being written back while the scan streams its columns (measured: C5 count 0.638 -> 0.629
     // ms, C4 push-down 0.176 -> 0.160 ms). With kept values the slots compete for L2 and the
     // policy hurt (C2 0.913 -> 0.968 ms), so it is not used there.
+#if !SEL_AB_NOMASK   // A/B only: the cost of the mask store (the push-down needs it)
     st_evict_last(sb.bits + c * 32 + lane, t);
+#endif
   }
   uint32_t cc;
   if (sb.n_keep) {
@@ -840,12 +975,12 @@ __device__ __forceinline__ uint32_t keep_chunk(const SelectionBufs& sb, uint64_t
   } else {
     cc = __reduce_add_sync(0xFFFFFFFFu, (uint32_t)__popc(m));
   }
+#if !SEL_AB_NOCNT    // A/B only: the cost of the count store and the superblock atomic
   if (lane == 0) {
     sb.chunk_cnt[c] = (uint16_t)cc;
-#if SEL_SB_ATOMICS
-    if (cc) atomicAdd(&sb.sb_sum[c >> kSbShift], cc);
-#endif
+    if (cc) atomicAdd(sbs + (c >> kSbShift), cc);
   }
+#endif
   return cc;
 }
 
@@ -859,7 +994,8 @@ __global__ void __launch_bounds__(NW * 32, NW == kWarpsPerCta ? (FASTN ? SEL_FAS
                                                          uint64_t* __restrict__ partials,
                                                          unsigned int* __restrict__ done,
                                                          uint64_t* __restrict__ out,
-                                                         SelectionBufs sb, const PeerXchg xg) {
+                                                         SelectionBufs sb, const PeerXchg xg,
+                                                         const ExecFinish fin) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const uint64_t nfull = n / kChunkRows;
   const uint32_t rem = (uint32_t)(n % kChunkRows);
@@ -869,6 +1005,19 @@ __global__ void __launch_bounds__(NW * 32, NW == kWarpsPerCta ? (FASTN ? SEL_FAS
   char* wsmem = KEEP ? s_dyn + (size_t)warp * sb.warp_smem : nullptr;
   uint32_t cnt = 0;
   bool full = false;   // this warp kept a fully selected chunk (raises the flag once, below)
+  // keeping counts: this count's half of the superblock sums (zero: the count before the last one
+  // used it), and the other half — the previous selection's, dead from here on — zeroed for the
+  // next count while this one runs
+  uint32_t epoch = 0;
+  uint32_t* my_sb = nullptr;
+  if constexpr (KEEP) {
+    epoch = *(volatile const uint32_t*)sb.state;
+    my_sb = sb.sb_sum + (size_t)(epoch & 1u) * sb.sb_stride;
+    uint32_t* other = sb.sb_sum + (size_t)((epoch + 1u) & 1u) * sb.sb_stride;
+    const uint32_t ext = sb.state[1 + ((epoch + 1u) & 1u)];
+    for (uint32_t i = blockIdx.x * (NW * 32) + threadIdx.x; i < ext; i += gridDim.x * (NW * 32))
+      other[i] = 0u;
+  }
   // Stage the program's key sets in shared memory (after the warps' areas), once per CTA.
   uint32_t bm_sbase = kNoStage;
   if (p.bm_smem) {
@@ -900,7 +1049,7 @@ __global__ void __launch_bounds__(NW * 32, NW == kWarpsPerCta ? (FASTN ? SEL_FAS
       uint32_t wm = 0;
       const uint32_t m = eval_fast<FASTN, KEEP>(p, c * kChunkRows, lane, wsmem, &wm);
       cnt += __popc(m);
-      full |= keep_chunk<P, KEEP>(sb, c, lane, m, wsmem, wm, KEEP && p.fast_code >= 0) == kChunkRows;
+      full |= keep_chunk<P, KEEP>(sb, my_sb, c, lane, m, wsmem, wm, KEEP && p.fast_code >= 0) == kChunkRows;
     }
   } else {
     if (lane == 0 && p.prefetch && gw < ns_full) prefetch_chunk(p, phase + gw * stride);
@@ -909,7 +1058,7 @@ __global__ void __launch_bounds__(NW * 32, NW == kWarpsPerCta ? (FASTN ? SEL_FAS
       if (lane == 0 && p.prefetch && s + nw < ns_full) prefetch_chunk(p, c + nw * stride);
       const uint32_t m = eval_program<false, KEEP>(p, c * kChunkRows, lane, kChunkRows, wsmem, bm_sbase);
       cnt += __popc(m);
-      full |= keep_chunk<P, KEEP>(sb, c, lane, m, wsmem) == kChunkRows;
+      full |= keep_chunk<P, KEEP>(sb, my_sb, c, lane, m, wsmem) == kChunkRows;
     }
   }
   if (tail_sampled && gw == ns_full % nw) {
@@ -923,12 +1072,14 @@ __global__ void __launch_bounds__(NW * 32, NW == kWarpsPerCta ? (FASTN ? SEL_FAS
       const uint32_t pt1 = w4 ? (uint32_t)p.lo[p.leaf[s].iv_begin + 1] : (p.fast_pts[s][1] & 0xFFu);
       wm = which_tail(p.col[p.leaf[s].slot], nfull * kChunkRows, lane, rem, pt1, w4);
     }
-    keep_chunk<P, KEEP>(sb, nfull, lane, m, wsmem, wm, coded);   // a tail chunk is never full
+    keep_chunk<P, KEEP>(sb, my_sb, nfull, lane, m, wsmem, wm, coded);   // a tail chunk is never full
   }
   // dense_chunks_kernel has work: one store per warp (one per chunk contended on the word: C5 at
   // s = 1 count 0.62 -> 1.36 ms)
-  if (KEEP && full && lane == 0) sb.sb_sum[sb.full_slot] = 1u;
+  if (KEEP && full && lane == 0) sb.state[3] = 1u;
   cnt = __reduce_add_sync(0xFFFFFFFFu, cnt);
+  // the superblock atomics and the flag of every thread are read by the last CTA (finish_selection)
+  if (KEEP) __threadfence();
 
   __shared__ uint32_t s_warp[NW];
   __shared__ bool s_last;
@@ -949,6 +1100,7 @@ __global__ void __launch_bounds__(NW * 32, NW == kWarpsPerCta ? (FASTN ? SEL_FAS
     for (uint32_t b = threadIdx.x; b < gridDim.x; b += (NW * 32)) s += ((volatile uint64_t*)partials)[b];
     for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xFFFFFFFFu, s, o);
     __shared__ uint64_t s_sum[NW];
+    __shared__ uint64_t s_total;
     if (lane == 0) s_sum[warp] = s;
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -957,12 +1109,25 @@ __global__ void __launch_bounds__(NW * 32, NW == kWarpsPerCta ? (FASTN ? SEL_FAS
       for (int w = 0; w < NW; ++w) t += s_sum[w];
       *out = t;
       *done = 0u;
+      s_total = t;
     }
-    // sel_count with peers: the count's collective fused into the same kernel — the last CTA
-    // exchanges the local count over peer memory and leaves the global sum in *out
-    if (xg.n > 0) {
+    __syncthreads();
+    const uint64_t local = s_total;
+    // keeping counts: the superblock prefix the push-down starts from (no kernel in between)
+    if constexpr (KEEP) finish_selection<NW>(sb, n, (uint32_t)local, epoch, my_sb);
+    if (fin.result) {
+      // a device-gated Execute: its result words (and, with peers, the exchange) right here
       __syncthreads();
-      peer_gather_block(xg, out, 1, nullptr, out);
+      finish_execute(fin, xg, local);
+    } else {
+      if (xg.n > 0) {
+        // sel_count with peers: the count's collective fused into the same kernel — the last CTA
+        // exchanges the local count over peer memory and leaves the global sum in *out
+        __syncthreads();
+        peer_gather_block(xg, out, 1, nullptr, out);
+      }
+      // sel_count: the count straight into the pinned host word (no copy after the kernel)
+      if (fin.host && threadIdx.x == 0) fin.host[0] = *out;
     }
   }
 }
@@ -1039,24 +1204,6 @@ __global__ void __launch_bounds__(kThreads, 3) pushdown_kernel(
 
 
 // ---- push-down from a kept selection ------------------------------------------------------------
-#if !SEL_SB_ATOMICS
-// Per-64-chunk sums of the kept chunk counts (one warp per superblock, 2 counts per lane).
-__global__ void __launch_bounds__(kThreads) superblock_sum_kernel(const uint16_t* __restrict__ cnt,
-                                                                  uint64_t nchunks,
-                                                                  uint32_t* __restrict__ sb_sum) {
-  const int lane = threadIdx.x & 31;
-  const uint64_t nsb = (nchunks + kSbChunks - 1) / kSbChunks;
-  const uint64_t w = (uint64_t)blockIdx.x * kWarpsPerCta + (threadIdx.x >> 5);
-  const uint64_t nw = (uint64_t)gridDim.x * kWarpsPerCta;
-  for (uint64_t sb = w; sb < nsb; sb += nw) {
-    const uint64_t c = sb * kSbChunks + lane;
-    uint32_t v = (c < nchunks ? cnt[c] : 0u) + (c + 32 < nchunks ? cnt[c + 32] : 0u);
-    v = __reduce_add_sync(0xFFFFFFFFu, v);
-    if (lane == 0) sb_sum[sb] = v;
-  }
-}
-
-#endif
 
 // Exclusive prefix of the per-64-chunk sums kept by the count kernel (one CTA; <= 65536 sums).
 __global__ void __launch_bounds__(256) peer_exchange_kernel(const PeerXchg x, const uint64_t* src,
@@ -1064,69 +1211,15 @@ __global__ void __launch_bounds__(256) peer_exchange_kernel(const PeerXchg x, co
   peer_gather_block(x, src, k, out, sums);
 }
 
-// gate_ranks > 0 (sel_execute with a communicator): result[1..gate_ranks] holds the all-gathered
-// per-rank counts; their sum, the global count, is written to result[kGateSlot] for the gate of
-// the push-down kernel that follows (one collective per Execute instead of two).
-// With peers (xg.n > 0; sel_execute over peer memory) the exchange of the local count in
-// out_count[kGateSlot] runs first, fused here: gathered into out_count[1..n], summed into
-// out_count[kGateSlot].
-// The result words the host reads back are mirrored right below result[kGateSlot] so that one
-// copy fetches them (kMirrorMax ranks at most): the gathered per-rank counts at
-// [kGateSlot - nr, kGateSlot), or, without ranks, the local count at kGateSlot - 1. The
-// superblock sums stay: a kept selection serves any number of push-downs.
-__global__ void __launch_bounds__(1024) superblock_prefix_kernel(const uint32_t* __restrict__ sb_sum,
-                                                                 uint32_t* __restrict__ sb_prefix,
-                                                                 uint32_t nsb, uint64_t* __restrict__ out_count,
-                                                                 int gate_ranks, const PeerXchg xg,
-                                                                 int rank) {
-  const uint32_t t = threadIdx.x, lane = t & 31, warp = t >> 5;
-  if (xg.n > 0) peer_gather_block(xg, out_count + kGateSlot, 1, out_count + 1, out_count + kGateSlot);
-  // a failed exchange left kXchgFailed in the gate slot: the push-down kernels write nothing
-  const bool failed = xg.n > 0 && out_count[kGateSlot] == kXchgFailed;
-  if (gate_ranks > 0 && t == 0) {
-    uint64_t g = 0;
-    for (int r = 0; r < gate_ranks; ++r) g += out_count[1 + r];
-    out_count[kGateSlot] = g;
-  }
-  const int nr = xg.n > 0 ? xg.n : gate_ranks;
-  if (nr > 0 && nr <= kMirrorMax && (int)t < nr) out_count[kGateSlot - nr + t] = out_count[1 + t];
-  if (t == 0) {   // this rank's position in the rank-ordered global result (sel_execute_to)
-    uint64_t off = 0;
-    for (int r = 0; r < rank && r < nr; ++r) off += out_count[1 + r];
-    out_count[kOffsetSlot] = failed ? kXchgFailed : off;
-  }
-  const uint32_t per = (nsb + 1023u) / 1024u;
-  const uint32_t b = min(nsb, t * per), e = min(nsb, b + per);
-  uint32_t local = 0;
-  for (uint32_t i = b; i < e; ++i) local += sb_sum[i];
-  uint32_t incl = local;
-#pragma unroll
-  for (int d = 1; d < 32; d <<= 1) {
-    const uint32_t v = __shfl_up_sync(0xFFFFFFFFu, incl, d);
-    if (lane >= (uint32_t)d) incl += v;
-  }
-  __shared__ uint32_t s_w[32];
-  if (lane == 31) s_w[warp] = incl;
-  __syncthreads();
-  if (warp == 0) {
-    uint32_t w = s_w[lane], wi = w;
-#pragma unroll
-    for (int d = 1; d < 32; d <<= 1) {
-      const uint32_t v = __shfl_up_sync(0xFFFFFFFFu, wi, d);
-      if (lane >= (uint32_t)d) wi += v;
-    }
-    s_w[lane] = wi - w;
-    if (lane == 31) {
-      *out_count = wi;
-      if (nr == 0) out_count[kGateSlot - 1] = wi;
-    }
-  }
-  __syncthreads();
-  uint32_t run = s_w[warp] + incl - local;
-  for (uint32_t i = b; i < e; ++i) {
-    sb_prefix[i] = run;
-    run += sb_sum[i];
-  }
+// The kept selection's local count into result[0] and the result words of ExecFinish (sel_execute
+// with a communicator: after the all-gather of the per-rank counts; sel_pushdown from a kept
+// selection: the local count only). One CTA.
+__global__ void __launch_bounds__(256) selection_result_kernel(const uint32_t* __restrict__ hb_prefix,
+                                                               uint32_t nhb, const ExecFinish f,
+                                                               const PeerXchg xg) {
+  const uint64_t local = hb_prefix[nhb];
+  if (threadIdx.x == 0) f.result[0] = local;
+  finish_execute(f, xg, local);
 }
 
 // Flush `k` staged rows (block-relative, ascending) to output positions [gbase, gbase + k): row
@@ -1226,9 +1319,9 @@ __global__ void __launch_bounds__(kThreads, SEL_PD_MINB) pushdown_sel_kernel(con
   const uint64_t nblocks = (nchunks + kBlockChunks - 1) / kBlockChunks;
   const uint64_t gw = (uint64_t)blockIdx.x * kWarpsPerCta + warp;
   const uint64_t nw = (uint64_t)gridDim.x * kWarpsPerCta;
+  const uint32_t* sbs = kept_sb(sb);
   for (uint64_t blk = gw; blk < nblocks; blk += nw) {
     const uint64_t c0 = blk * kBlockChunks;
-    const uint64_t first = (c0 >> kSbShift) << kSbShift;
     // --- metadata, all loads independent ---
     const uint32_t cntv = (lane < kBlockChunks && c0 + lane < nchunks) ? sb.chunk_cnt[c0 + lane] : 0u;
     uint32_t m[kBlockChunks];
@@ -1240,14 +1333,11 @@ __global__ void __launch_bounds__(kThreads, SEL_PD_MINB) pushdown_sel_kernel(con
       asm volatile("applypriority.global.L2::evict_normal [%0], 128;" ::"l"(sb.bits + (c0 + lane) * 32) : "memory");
     if (CODED && lane < kBlockChunks && c0 + lane < nchunks)
       asm volatile("applypriority.global.L2::evict_normal [%0], 128;" ::"l"(sb.which + (c0 + lane) * 32) : "memory");
-    uint32_t part = 0;
-    if (first + lane < c0) part += sb.chunk_cnt[first + lane];
-    if (first + 32 + lane < c0) part += sb.chunk_cnt[first + 32 + lane];
-    const uint32_t sbp = sb.sb_prefix[c0 >> kSbShift];
+    const uint64_t kb = kept_base(sb, sbs, c0, lane);
     // --- offsets ---
     const uint32_t total = __reduce_add_sync(0xFFFFFFFFu, cntv);
     if (total == 0) continue;
-    uint64_t gbase = goff + (uint64_t)sbp + __reduce_add_sync(0xFFFFFFFFu, part);
+    uint64_t gbase = goff + kb;
     const uint64_t bbase = c0 * kChunkRows;
     uint32_t staged = 0;
 #pragma unroll
@@ -1333,7 +1423,9 @@ __global__ void __launch_bounds__(kThreads) dense_chunks_kernel(const __grid_con
                                                                 uint32_t* __restrict__ out_ids,
                                                                 const uint64_t* __restrict__ gate_count) {
   if (*gate_count == kXchgFailed || (p.gate && *gate_count > p.gate_max)) return;  // as pushdown_sel
-  if (sb.sb_sum[sb.full_slot] == 0u) return;        // the count saw no fully selected chunk
+  const uint64_t nhb = ((n + kChunkRows - 1) / kChunkRows + kHbChunks - 1) / kHbChunks;
+  if (sb.hb_prefix[nhb + 1] == 0u) return;   // the count saw no fully selected chunk
+  const uint32_t* sbs = kept_sb(sb);
   const uint64_t goff = p.global_out ? gate_count[kOffsetSlot - kGateSlot] : 0ull;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const uint64_t nchunks = (n + kChunkRows - 1) / kChunkRows;
@@ -1344,11 +1436,7 @@ __global__ void __launch_bounds__(kThreads) dense_chunks_kernel(const __grid_con
     const uint64_t c0 = blk * kBlockChunks;
     const uint32_t cntv = (lane < kBlockChunks && c0 + lane < nchunks) ? sb.chunk_cnt[c0 + lane] : 0u;
     if (!__ballot_sync(0xFFFFFFFFu, cntv == (uint32_t)kChunkRows && lane < kBlockChunks)) continue;
-    const uint64_t first = (c0 >> kSbShift) << kSbShift;
-    uint32_t part = 0;
-    if (first + lane < c0) part += sb.chunk_cnt[first + lane];
-    if (first + 32 + lane < c0) part += sb.chunk_cnt[first + 32 + lane];
-    uint64_t gbase = goff + (uint64_t)sb.sb_prefix[c0 >> kSbShift] + __reduce_add_sync(0xFFFFFFFFu, part);
+    uint64_t gbase = goff + kept_base(sb, sbs, c0, lane);
 #pragma unroll 1
     for (int g = 0; g < kBlockChunks; ++g) {
       const uint32_t cg = __shfl_sync(0xFFFFFFFFu, cntv, g);
@@ -1541,105 +1629,105 @@ __global__ void __launch_bounds__(kThreads) count_batch_kernel(const __grid_cons
   }
 }
 
+// Memoised per (kernel, threads, shared memory, device): the grid of every probe is sized from it,
+// and the runtime query costs microseconds of host time per launch.
 template <class Kern>
 int occupancy_of(Kern k, size_t dyn_smem, int threads = kThreads) {
+  static std::mutex mu;
+  static std::map<std::tuple<const void*, size_t, int, int>, int> memo;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const auto key = std::make_tuple(reinterpret_cast<const void*>(k), dyn_smem, threads, dev);
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    const auto it = memo.find(key);
+    if (it != memo.end()) return it->second;
+  }
   int blocks = 0;
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, k, threads, dyn_smem) != cudaSuccess) return 1;
-  return blocks > 0 ? blocks : 1;
+  blocks = blocks > 0 ? blocks : 1;
+  std::lock_guard<std::mutex> lk(mu);
+  memo[key] = blocks;
+  return blocks;
 }
 
 }  // namespace
 
 template <int FASTN>
 void launch_count_fast(const DevProgramSmall& p, uint64_t n, int grid, const Scratch& s,
-                       const SelectionBufs* keep, cudaStream_t stream) {
+                       const SelectionBufs* keep, cudaStream_t stream, const ExecFinish& fin) {
   if (keep)
-    count_kernel<DevProgramSmall, true, kWarpsPerCta, FASTN><<<grid, kThreads, (size_t)keep->warp_smem * kWarpsPerCta, stream>>>(p, n, s.partials, s.done, s.result, *keep, s.xg);
+    count_kernel<DevProgramSmall, true, kWarpsPerCta, FASTN><<<grid, kThreads, (size_t)keep->warp_smem * kWarpsPerCta, stream>>>(p, n, s.partials, s.done, s.result, *keep, s.xg, fin);
   else
-    count_kernel<DevProgramSmall, false, kWarpsPerCta, FASTN><<<grid, kThreads, 0, stream>>>(p, n, s.partials, s.done, s.result, SelectionBufs{}, s.xg);
+    count_kernel<DevProgramSmall, false, kWarpsPerCta, FASTN><<<grid, kThreads, 0, stream>>>(p, n, s.partials, s.done, s.result, SelectionBufs{}, s.xg, fin);
 }
 
 template <class P>
 int launch_count_t(const P& p, uint64_t n, int grid, const Scratch& s, const SelectionBufs* keep,
-                   int nw, void* st) {
+                   int nw, void* st, const ExecFinish* finp) {
   cudaStream_t stream = (cudaStream_t)st;
+  const ExecFinish fin = finp ? *finp : ExecFinish{};
   if constexpr (std::is_same<P, DevProgramSmall>::value) {
     if (p.fast_n > 0 && nw == kWarpsPerCta && !p.bm_smem) {
       switch (p.fast_n) {
-        case 1: launch_count_fast<1>(p, n, grid, s, keep, stream); break;
-        case 2: launch_count_fast<2>(p, n, grid, s, keep, stream); break;
-        case 3: launch_count_fast<3>(p, n, grid, s, keep, stream); break;
-        default: launch_count_fast<4>(p, n, grid, s, keep, stream); break;
+        case 1: launch_count_fast<1>(p, n, grid, s, keep, stream, fin); break;
+        case 2: launch_count_fast<2>(p, n, grid, s, keep, stream, fin); break;
+        case 3: launch_count_fast<3>(p, n, grid, s, keep, stream, fin); break;
+        default: launch_count_fast<4>(p, n, grid, s, keep, stream, fin); break;
       }
       return (int)cudaGetLastError();
     }
   }
   if (nw == 32) {
     if (keep)
-      count_kernel<P, true, 32><<<grid, 32 * 32, (size_t)keep->warp_smem * 32 + p.bm_smem, stream>>>(p, n, s.partials, s.done, s.result, *keep, s.xg);
+      count_kernel<P, true, 32><<<grid, 32 * 32, (size_t)keep->warp_smem * 32 + p.bm_smem, stream>>>(p, n, s.partials, s.done, s.result, *keep, s.xg, fin);
     else
-      count_kernel<P, false, 32><<<grid, 32 * 32, p.bm_smem, stream>>>(p, n, s.partials, s.done, s.result, SelectionBufs{}, s.xg);
+      count_kernel<P, false, 32><<<grid, 32 * 32, p.bm_smem, stream>>>(p, n, s.partials, s.done, s.result, SelectionBufs{}, s.xg, fin);
   } else {
     if (keep)
-      count_kernel<P, true, kWarpsPerCta><<<grid, kThreads, (size_t)keep->warp_smem * kWarpsPerCta + p.bm_smem, stream>>>(p, n, s.partials, s.done, s.result, *keep, s.xg);
+      count_kernel<P, true, kWarpsPerCta><<<grid, kThreads, (size_t)keep->warp_smem * kWarpsPerCta + p.bm_smem, stream>>>(p, n, s.partials, s.done, s.result, *keep, s.xg, fin);
     else
-      count_kernel<P, false, kWarpsPerCta><<<grid, kThreads, p.bm_smem, stream>>>(p, n, s.partials, s.done, s.result, SelectionBufs{}, s.xg);
+      count_kernel<P, false, kWarpsPerCta><<<grid, kThreads, p.bm_smem, stream>>>(p, n, s.partials, s.done, s.result, SelectionBufs{}, s.xg, fin);
   }
   return (int)cudaGetLastError();
 }
 int launch_count_small(const DevProgramSmall& p, uint64_t n, int grid, const Scratch& s,
-                       const SelectionBufs* keep, void* st, int nw) {
-  return launch_count_t(p, n, grid, s, keep, nw, st);
+                       const SelectionBufs* keep, void* st, int nw, const ExecFinish* fin) {
+  return launch_count_t(p, n, grid, s, keep, nw, st, fin);
 }
 int launch_count_large(const DevProgramLarge& p, uint64_t n, int grid, const Scratch& s,
-                       const SelectionBufs* keep, void* st, int nw) {
-  return launch_count_t(p, n, grid, s, keep, nw, st);
+                       const SelectionBufs* keep, void* st, int nw, const ExecFinish* fin) {
+  return launch_count_t(p, n, grid, s, keep, nw, st, fin);
+}
+template <class P>
+int launch_pushdown_sel_t(const P& p, uint64_t n, uint32_t* out_ids, int grid, const Scratch& s,
+                          const SelectionBufs& sb, void* st, int gate_ranks, const PeerXchg* xg,
+                          int rank, bool finished, uint64_t* host) {
+  cudaStream_t stream = (cudaStream_t)st;
+  if (!finished) {
+    const uint64_t nchunks = (n + kChunkRows - 1) / kChunkRows;
+    const uint32_t nhb = (uint32_t)((nchunks + kHbChunks - 1) / kHbChunks);
+    selection_result_kernel<<<1, 256, 0, stream>>>(sb.hb_prefix, nhb,
+                                                   ExecFinish{s.result, host, gate_ranks, rank},
+                                                   xg ? *xg : PeerXchg{});
+  }
+  if (p.coded)
+    pushdown_sel_kernel<P, true><<<grid, kThreads, 0, stream>>>(p, n, sb, out_ids, s.result + kGateSlot);
+  else
+    pushdown_sel_kernel<P, false><<<grid, kThreads, 0, stream>>>(p, n, sb, out_ids, s.result + kGateSlot);
+  if (p.dense_split)
+    dense_chunks_kernel<P><<<grid, kThreads, 0, stream>>>(p, n, sb, out_ids, s.result + kGateSlot);
+  return (int)cudaGetLastError();
 }
 int launch_pushdown_sel_small(const DevProgramSmall& p, uint64_t n, uint32_t* out_ids, int grid,
                               const Scratch& s, const SelectionBufs& sb, void* st, int gate_ranks,
-                              const PeerXchg* xg, int rank) {
-  const PeerXchg none{};
-  const uint64_t nchunks = (n + kChunkRows - 1) / kChunkRows;
-  const uint32_t nsb = (uint32_t)((nchunks + kSbChunks - 1) / kSbChunks);
-#if !SEL_SB_ATOMICS
-  superblock_sum_kernel<<<(unsigned)(nsb < 148ull * 16 * kWarpsPerCta ? (nsb + kWarpsPerCta - 1) / kWarpsPerCta : 148ull * 16), kThreads, 0,
-                          (cudaStream_t)st>>>(sb.chunk_cnt, nchunks, sb.sb_sum);
-#endif
-  superblock_prefix_kernel<<<1, 1024, 0, (cudaStream_t)st>>>(sb.sb_sum, sb.sb_prefix, nsb, s.result,
-                                                               gate_ranks, xg ? *xg : none, rank);
-  if (p.coded)
-    pushdown_sel_kernel<DevProgramSmall, true><<<grid, kThreads, 0, (cudaStream_t)st>>>(p, n, sb, out_ids,
-                                                                                s.result + kGateSlot);
-  else
-    pushdown_sel_kernel<DevProgramSmall, false><<<grid, kThreads, 0, (cudaStream_t)st>>>(p, n, sb, out_ids,
-                                                                                s.result + kGateSlot);
-  if (p.dense_split)
-    dense_chunks_kernel<DevProgramSmall><<<grid, kThreads, 0, (cudaStream_t)st>>>(p, n, sb, out_ids,
-                                                                     s.result + kGateSlot);
-  return (int)cudaGetLastError();
+                              const PeerXchg* xg, int rank, bool finished, uint64_t* host) {
+  return launch_pushdown_sel_t(p, n, out_ids, grid, s, sb, st, gate_ranks, xg, rank, finished, host);
 }
 int launch_pushdown_sel_large(const DevProgramLarge& p, uint64_t n, uint32_t* out_ids, int grid,
                               const Scratch& s, const SelectionBufs& sb, void* st, int gate_ranks,
-                              const PeerXchg* xg, int rank) {
-  const PeerXchg none{};
-  const uint64_t nchunks = (n + kChunkRows - 1) / kChunkRows;
-  const uint32_t nsb = (uint32_t)((nchunks + kSbChunks - 1) / kSbChunks);
-#if !SEL_SB_ATOMICS
-  superblock_sum_kernel<<<(unsigned)(nsb < 148ull * 16 * kWarpsPerCta ? (nsb + kWarpsPerCta - 1) / kWarpsPerCta : 148ull * 16), kThreads, 0,
-                          (cudaStream_t)st>>>(sb.chunk_cnt, nchunks, sb.sb_sum);
-#endif
-  superblock_prefix_kernel<<<1, 1024, 0, (cudaStream_t)st>>>(sb.sb_sum, sb.sb_prefix, nsb, s.result,
-                                                               gate_ranks, xg ? *xg : none, rank);
-  if (p.coded)
-    pushdown_sel_kernel<DevProgramLarge, true><<<grid, kThreads, 0, (cudaStream_t)st>>>(p, n, sb, out_ids,
-                                                                                s.result + kGateSlot);
-  else
-    pushdown_sel_kernel<DevProgramLarge, false><<<grid, kThreads, 0, (cudaStream_t)st>>>(p, n, sb, out_ids,
-                                                                                s.result + kGateSlot);
-  if (p.dense_split)
-    dense_chunks_kernel<DevProgramLarge><<<grid, kThreads, 0, (cudaStream_t)st>>>(p, n, sb, out_ids,
-                                                                     s.result + kGateSlot);
-  return (int)cudaGetLastError();
+                              const PeerXchg* xg, int rank, bool finished, uint64_t* host) {
+  return launch_pushdown_sel_t(p, n, out_ids, grid, s, sb, st, gate_ranks, xg, rank, finished, host);
 }
 int launch_pushdown_small(const DevProgramSmall& p, uint64_t n, uint32_t* out_ids, int grid,
                           const Scratch& s, uint64_t ticket_base, uint32_t epoch, void* st) {

@@ -150,14 +150,21 @@ int occupancy_count_batch();
 
 // A kept selection (sel_count_ex with SEL_KEEP_SELECTION): per chunk of 1024 rows, 32 row-major
 // mask words (word L, bit b = row 32L + b of the chunk) and the chunk's count; per superblock of
-// 64 chunks, the sum of
-// its counts and (filled by the push-down) its exclusive prefix.
+// 64 chunks the sum of its chunk counts (atomics during the count); per hyperblock of 4096
+// chunks the exclusive prefix of those sums, which the count's last CTA forms (<= 1024
+// hyperblocks for 2^32 rows). A push-down block's output position is the hyperblock prefix + the
+// superblock sums before it within its hyperblock + the chunk counts before it within its
+// superblock (two loads per lane each). No memset, no scan kernel per probe: the superblock sums
+// alternate between two halves by the parity of the device's keeping-count epoch (state[0]), and
+// a count zeroes the other half (the previous, now dead, selection's) while it runs.
 #ifndef SEL_BLOCK_CHUNKS
 #define SEL_BLOCK_CHUNKS 4   // A/B 2/4/8: 4 best (C5 push-down 0.233 -> 0.206 ms, C3 0.240 -> 0.232, C2 equal)
 #endif
 constexpr int kSelBlockChunks = SEL_BLOCK_CHUNKS;   // push-down from a selection: chunks per warp block
 constexpr int kSbShift = 6;
 constexpr uint64_t kSbChunks = 1ull << kSbShift;
+constexpr int kHbShift = 12;                          // chunks per hyperblock: 4096
+constexpr uint64_t kHbChunks = 1ull << kHbShift;
 constexpr int kMaxKeep = 8;
 struct SelectionBufs {
   uint32_t* bits;        // [nchunks * 32]
@@ -166,10 +173,13 @@ struct SelectionBufs {
   uint64_t code_pts;     // its two raw values: 1-byte column point 0 | point 1 << 8; 4-byte
                          // column point 0 | point 1 << 32
   uint16_t* chunk_cnt;   // [nchunks]
-  uint32_t* sb_sum;      // [nsb], zeroed before the count
-  uint32_t* sb_prefix;   // [nsb]
-  uint32_t full_slot;    // sb_sum[full_slot] (= nsb): nonzero once the count saw a fully
-                         // selected chunk (dense_chunks_kernel has work)
+  uint32_t* sb_sum;      // two halves of sb_stride words (a multiple of 4), zero beyond nsb; the
+                         // selection's half is (state[0] - 1) & 1
+  uint32_t sb_stride;
+  uint32_t* hb_prefix;   // [nhb + 2]: exclusive prefix, [nhb] the local count, [nhb + 1] the flag
+                         // (a fully selected chunk was kept: dense_chunks_kernel has work)
+  uint32_t* state;       // [4]: [0] keeping counts so far, [1 + h] words of half h to zero,
+                         // [3] the full-chunk flag while a count runs
   // Kept values of projected predicate columns: chunk c's selected values, compacted in row
   // order, at keep_slot[k] + c * 1024 * width (written by the count, copied by the push-down).
   uint32_t n_keep;
@@ -214,6 +224,22 @@ struct PeerXchg {
   uint64_t timeout_ns;     // a wait longer than this is a failed exchange
 };
 
+// The result words of a device-gated Execute (sel_execute), finished by ONE CTA right after the
+// count: with peers the exchange of the local count in result[kGateSlot] (gathered into
+// result[1..n], their sum into result[kGateSlot]); with gate_ranks > 0 (NCCL: result[1..gate_ranks]
+// all-gathered before) their sum into result[kGateSlot]; the words the host reads back mirrored
+// right below result[kGateSlot] (the gathered counts at [kGateSlot - nr, kGateSlot), or the local
+// count at kGateSlot - 1) and this rank's offset in the rank-ordered result at
+// result[kOffsetSlot]; with `host` (the context's pinned mirror, device-accessible) the mirror and
+// the gate stored there as well, so that no copy follows. result == nullptr: nothing to finish
+// (a count with host != nullptr stores its count, after the exchange, to host[0]).
+struct ExecFinish {
+  uint64_t* result;
+  uint64_t* host;
+  int gate_ranks;
+  int rank;
+};
+
 // Device-side scratch owned by a context.
 struct Scratch {
   uint64_t* partials;      // per-CTA partial counts (count kernel)
@@ -247,23 +273,28 @@ int launch_set_u64(uint64_t* p, uint64_t v, void* stream);
 // projected predicate columns; the leaves carry the capture offsets and keep->warp_smem is set).
 // nw: warps per CTA, kWarpsPerCta or 32 (one 1024-thread CTA per SM when staged key sets fill
 // the shared memory; keep->warp_smem must then be 0).
+// fin (keeping counts of a device-gated Execute): the count's last CTA also finishes the
+// Execute's result words (ExecFinish; with s.xg.n > 0 through the peer exchange) — no kernel, no
+// copy between the count and the gated materialisation.
 int launch_count_small(const DevProgramSmall& p, uint64_t n, int grid, const Scratch& s,
-                       const SelectionBufs* keep, void* stream, int nw = kWarpsPerCta);
+                       const SelectionBufs* keep, void* stream, int nw = kWarpsPerCta,
+                       const ExecFinish* fin = nullptr);
 int launch_count_large(const DevProgramLarge& p, uint64_t n, int grid, const Scratch& s,
-                       const SelectionBufs* keep, void* stream, int nw = kWarpsPerCta);
-// Push-down from a kept selection: superblock prefix (writes the local count to s.result[0]; with
-// gate_ranks > 0 also s.result[kGateSlot] = sum of the gathered s.result[1..gate_ranks]) and the
-// compaction/gather kernel.
-// xg != nullptr (sel_execute with peers): the prefix kernel first runs the peer exchange of the
-// local count in s.result[kGateSlot] (gathered into s.result[1..n], the sum into kGateSlot).
-// rank: this rank (for the offset of sel_execute_to: the sum of the gathered counts of the ranks
-// before it, written to s.result[kOffsetSlot]).
+                       const SelectionBufs* keep, void* stream, int nw = kWarpsPerCta,
+                       const ExecFinish* fin = nullptr);
+// Push-down from a kept selection (the count left the superblock prefix): unless `finished` (the
+// count finished the Execute's result words, fin above), a 1-CTA kernel first writes the kept
+// local count to s.result[0] and finishes the result words (ExecFinish with gate_ranks, rank,
+// host; xg != nullptr: through the peer exchange); then the compaction/gather kernel and, with
+// p.dense_split, the whole-chunk copy kernel.
 int launch_pushdown_sel_small(const DevProgramSmall& p, uint64_t n, uint32_t* out_ids, int grid,
                               const Scratch& s, const SelectionBufs& sb, void* stream,
-                              int gate_ranks = 0, const PeerXchg* xg = nullptr, int rank = 0);
+                              int gate_ranks = 0, const PeerXchg* xg = nullptr, int rank = 0,
+                              bool finished = false, uint64_t* host = nullptr);
 int launch_pushdown_sel_large(const DevProgramLarge& p, uint64_t n, uint32_t* out_ids, int grid,
                               const Scratch& s, const SelectionBufs& sb, void* stream,
-                              int gate_ranks = 0, const PeerXchg* xg = nullptr, int rank = 0);
+                              int gate_ranks = 0, const PeerXchg* xg = nullptr, int rank = 0,
+                              bool finished = false, uint64_t* host = nullptr);
 int launch_pushdown_small(const DevProgramSmall& p, uint64_t n, uint32_t* out_ids, int grid,
                           const Scratch& s, uint64_t ticket_base, uint32_t epoch, void* stream);
 int launch_pushdown_large(const DevProgramLarge& p, uint64_t n, uint32_t* out_ids, int grid,
