@@ -1,5 +1,5 @@
 """Builds libsel.so in-tree with nvcc for sm_100a (no JIT cache: the .so travels with the repo
-snapshot to the GPU box). Host code (canon.cpp, api.cpp) and kernels (kernels.cu) link into one
+snapshot to the GPU box). Host code (canon.cpp and the context/plan/probe/synopsis/graph units) and kernels (kernels.cu) link into one
 shared library with a static CUDA runtime; NCCL is dlopen'd at run time."""
 
 from __future__ import annotations
@@ -12,8 +12,9 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libsel.so")
-SOURCES = [os.path.join(CSRC, f) for f in ("kernels.cu", "canon.cpp", "api.cpp")]
-HEADERS = [os.path.join(CSRC, f) for f in ("sel_internal.h", "canon.h")] + \
+SOURCES = [os.path.join(CSRC, f) for f in ("kernels.cu", "canon.cpp", "context.cpp", "plan.cpp",
+                                            "probe.cpp", "synopsis.cpp", "graph.cpp")]
+HEADERS = [os.path.join(CSRC, f) for f in ("sel_internal.h", "canon.h", "host.h")] + \
           [os.path.join(ROOT, "include", "sel.h")]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 

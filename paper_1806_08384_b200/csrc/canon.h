@@ -48,7 +48,7 @@ int decode_program(const void* bytes, size_t len, const int* types, uint32_t nco
 // Canonicalises a decoded, validated program (see sel_internal.h). Always succeeds.
 void plan_program(const Program& prog, const int* types, Plan* out);
 
-// Key-space helpers, exported for the device-parameter packing in api.cpp.
+// Key-space helpers, exported for the device-parameter packing in plan.cpp (host.h).
 int key_bits(int type);
 uint64_t key_sign_bias(int type);   // XOR applied to a key to get the raw lower bound
 

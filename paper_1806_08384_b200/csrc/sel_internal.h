@@ -1,4 +1,4 @@
-// sel_internal.h — libsel internals shared by the host planner (canon.cpp, api.cpp) and the
+// sel_internal.h — libsel internals shared by the host planner (canon.cpp, host.h units) and the
 // sm_100a kernels (kernels.cu). Not part of the ABI (include/sel.h is).
 //
 // A validated predicate program (include/sel.h format) is canonicalised on the host into
