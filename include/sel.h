@@ -100,7 +100,7 @@ sel_status sel_ctx_set_comm(sel_ctx ctx, int nranks, int rank, const void* nccl_
  * Once set, EVERY cross-rank combination of the context uses it instead of NCCL: sel_count's
  * sum (run by the count kernel's last CTA, fused with the count), sel_pushdown's offsets,
  * sel_count_batch / sel_count_sampled's sums, and sel_execute's one exchange per call — which
- * runs inside the push-down's prefix kernel, fused with the materialisation it gates, also in
+ * runs inside the count kernel's last CTA, right before the materialisation it gates, also in
  * prepared (graph) executes. A communicator is then not needed; if one is set as well, its
  * nranks/rank must agree.
  * sel_ctx_peer_handle: allocates the context's buffer (on first call) and writes its 64-byte

@@ -196,7 +196,7 @@ constexpr int kMaxRanks = 1024;
 constexpr int kGateSlot = 1 + kMaxRanks;
 constexpr int kOffsetSlot = 2 + kMaxRanks;   // this rank's global output offset (sel_execute_to)
 constexpr int kResultSlots = 3 + kMaxRanks;
-constexpr int kMirrorMax = 512;  // read-back mirror below kGateSlot (superblock_prefix_kernel)
+constexpr int kMirrorMax = 512;  // read-back mirror below kGateSlot (ExecFinish)
 
 // The library's own exchange over peer memory (sel_ctx_set_peers; SURVEY §8e "a one-shot peer
 // write of each rank's count into a symmetric buffer over NVLink plus a flag"). Every rank owns a

@@ -97,7 +97,7 @@ def setup_exchange(ctx: Context, mechanism: str = "peers", group=None) -> str:
                 why = "another rank could not map the peers' buffers"
             ok = False
     if ok:
-        return "peers (CUDA IPC, NVLink release stores, fused into the count / prefix kernels)"
+        return "peers (CUDA IPC, NVLink release stores, fused into the count kernel)"
     setup_comm(ctx, group)
     return f"nccl ({why})"
 

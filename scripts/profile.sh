@@ -8,8 +8,9 @@ TAG=${1:-r1}; shift || true
 ARGS=${*:-"--steps 3 --warmup 3 --no-cpu --no-e2e --no-graph"}
 mkdir -p gpurun_out
 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
+    -k regex:'count_kernel|pushdown|selection_result|dense_chunks|peer_exchange' \
     --log-file gpurun_out/launches_${TAG}.csv python bench.py $ARGS > gpurun_out/launches_${TAG}.out 2>&1
-for K in count_kernel pushdown_sel_kernel superblock_prefix_kernel; do
+for K in count_kernel pushdown_sel_kernel dense_chunks_kernel; do
   ncu --set full --clock-control none --import-source on -k regex:${K} -s 3 -c 1 \
       -o gpurun_out/prof_${TAG}_${K} -f python bench.py $ARGS > gpurun_out/prof_${TAG}_${K}.out 2>&1
 done

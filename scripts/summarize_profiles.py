@@ -14,8 +14,8 @@ import subprocess
 import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-OUR = ("count_kernel", "pushdown_kernel", "pushdown_sel_kernel", "superblock_prefix_kernel",
-       "dense_chunks_kernel")
+OUR = ("count_kernel", "pushdown_kernel", "pushdown_sel_kernel", "selection_result_kernel",
+       "dense_chunks_kernel", "superblock_prefix_kernel")
 KEYS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
         "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed",
         "sm__throughput.avg.pct_of_peak_sustained_elapsed",
