@@ -1078,8 +1078,9 @@ __global__ void __launch_bounds__(NW * 32, NW == kWarpsPerCta ? (FASTN ? SEL_FAS
   // s = 1 count 0.62 -> 1.36 ms)
   if (KEEP && full && lane == 0) sb.state[3] = 1u;
   cnt = __reduce_add_sync(0xFFFFFFFFu, cnt);
-  // the superblock atomics and the flag of every thread are read by the last CTA (finish_selection)
-  if (KEEP) __threadfence();
+  // the superblock atomics and the full-chunk flag (lane 0 of each warp) are read by the last CTA
+  // (finish_selection); the masks are read by later kernels only
+  if (KEEP && lane == 0) __threadfence();
 
   __shared__ uint32_t s_warp[NW];
   __shared__ bool s_last;
@@ -1284,17 +1285,13 @@ __device__ __forceinline__ void copy_kept(const P& p, const SelectionBufs& sb, u
   }
 }
 
-#ifndef SEL_BLOCK_CHUNKS
-#define SEL_BLOCK_CHUNKS 4
-#endif
 #ifndef SEL_STAGE_CAP
 #define SEL_STAGE_CAP 1024
 #endif
 #ifndef SEL_PD_MINB
 #define SEL_PD_MINB 8
 #endif
-constexpr int kBlockChunks = SEL_BLOCK_CHUNKS;         // chunks per warp block
-static_assert(kBlockChunks * kChunkRows <= kCodeBit, "staged rows must leave the code bit free");
+constexpr int kBlockChunks = kSelBlockChunks;          // whole-chunk copy kernel: chunks per warp block
 constexpr uint32_t kStageCap = SEL_STAGE_CAP;          // staged rows per warp before a flush
 
 // Warp blocks of 4 contiguous chunks, grid-stride. All of a block's metadata — its 4 chunk counts,
@@ -1303,7 +1300,7 @@ constexpr uint32_t kStageCap = SEL_STAGE_CAP;          // staged rows per warp b
 // superblock prefix plus that partial sum; empty chunks are skipped without touching any column;
 // the selected rows of the block are staged and flushed with batched gathers into one contiguous
 // output range. No ticket, no look-back, no predicate evaluation.
-template <class P, bool CODED>
+template <class P, bool CODED, int BC>
 __global__ void __launch_bounds__(kThreads, SEL_PD_MINB) pushdown_sel_kernel(const __grid_constant__ P p,
                                                                    uint64_t n, SelectionBufs sb,
                                                                    uint32_t* __restrict__ out_ids,
@@ -1313,25 +1310,26 @@ __global__ void __launch_bounds__(kThreads, SEL_PD_MINB) pushdown_sel_kernel(con
   // sel_execute_to: positions in the global result start at this rank's offset (prefix kernel)
   const uint64_t goff = p.global_out ? gate_count[kOffsetSlot - kGateSlot] : 0ull;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  static_assert(BC * kChunkRows <= kCodeBit, "staged rows must leave the code bit free");
   __shared__ uint16_t s_stage[kWarpsPerCta][kStageCap];
   uint16_t* my = s_stage[warp];
   const uint64_t nchunks = (n + kChunkRows - 1) / kChunkRows;
-  const uint64_t nblocks = (nchunks + kBlockChunks - 1) / kBlockChunks;
+  const uint64_t nblocks = (nchunks + BC - 1) / BC;
   const uint64_t gw = (uint64_t)blockIdx.x * kWarpsPerCta + warp;
   const uint64_t nw = (uint64_t)gridDim.x * kWarpsPerCta;
   const uint32_t* sbs = kept_sb(sb);
   for (uint64_t blk = gw; blk < nblocks; blk += nw) {
-    const uint64_t c0 = blk * kBlockChunks;
+    const uint64_t c0 = blk * BC;
     // --- metadata, all loads independent ---
-    const uint32_t cntv = (lane < kBlockChunks && c0 + lane < nchunks) ? sb.chunk_cnt[c0 + lane] : 0u;
-    uint32_t m[kBlockChunks];
+    const uint32_t cntv = (lane < BC && c0 + lane < nchunks) ? sb.chunk_cnt[c0 + lane] : 0u;
+    uint32_t m[BC];
 #pragma unroll
-    for (int g = 0; g < kBlockChunks; ++g) m[g] = c0 + g < nchunks ? sb.bits[(c0 + g) * 32 + lane] : 0u;
+    for (int g = 0; g < BC; ++g) m[g] = c0 + g < nchunks ? sb.bits[(c0 + g) * 32 + lane] : 0u;
     // the count stored the masks evict_last (keep_chunk): hand their L2 lines back to the normal
     // replacement order once read (one 128-byte line per chunk)
-    if (sb.n_keep == 0 && lane < kBlockChunks && c0 + lane < nchunks)
+    if (sb.n_keep == 0 && lane < BC && c0 + lane < nchunks)
       asm volatile("applypriority.global.L2::evict_normal [%0], 128;" ::"l"(sb.bits + (c0 + lane) * 32) : "memory");
-    if (CODED && lane < kBlockChunks && c0 + lane < nchunks)
+    if (CODED && lane < BC && c0 + lane < nchunks)
       asm volatile("applypriority.global.L2::evict_normal [%0], 128;" ::"l"(sb.which + (c0 + lane) * 32) : "memory");
     const uint64_t kb = kept_base(sb, sbs, c0, lane);
     // --- offsets ---
@@ -1341,7 +1339,7 @@ __global__ void __launch_bounds__(kThreads, SEL_PD_MINB) pushdown_sel_kernel(con
     const uint64_t bbase = c0 * kChunkRows;
     uint32_t staged = 0;
 #pragma unroll
-    for (int g = 0; g < kBlockChunks; ++g) {
+    for (int g = 0; g < BC; ++g) {
       const uint32_t cg = __shfl_sync(0xFFFFFFFFu, cntv, g);
       if (cg == 0) continue;
       if (p.dense_split && cg == kChunkRows && gbase + staged + kChunkRows <= p.capacity) {
@@ -1702,7 +1700,7 @@ int launch_count_large(const DevProgramLarge& p, uint64_t n, int grid, const Scr
 template <class P>
 int launch_pushdown_sel_t(const P& p, uint64_t n, uint32_t* out_ids, int grid, const Scratch& s,
                           const SelectionBufs& sb, void* st, int gate_ranks, const PeerXchg* xg,
-                          int rank, bool finished, uint64_t* host) {
+                          int rank, bool finished, uint64_t* host, int block_chunks) {
   cudaStream_t stream = (cudaStream_t)st;
   if (!finished) {
     const uint64_t nchunks = (n + kChunkRows - 1) / kChunkRows;
@@ -1711,23 +1709,34 @@ int launch_pushdown_sel_t(const P& p, uint64_t n, uint32_t* out_ids, int grid, c
                                                    ExecFinish{s.result, host, gate_ranks, rank},
                                                    xg ? *xg : PeerXchg{});
   }
-  if (p.coded)
-    pushdown_sel_kernel<P, true><<<grid, kThreads, 0, stream>>>(p, n, sb, out_ids, s.result + kGateSlot);
-  else
-    pushdown_sel_kernel<P, false><<<grid, kThreads, 0, stream>>>(p, n, sb, out_ids, s.result + kGateSlot);
+  if (block_chunks == 2) {
+    if (p.coded)
+      pushdown_sel_kernel<P, true, 2><<<grid, kThreads, 0, stream>>>(p, n, sb, out_ids, s.result + kGateSlot);
+    else
+      pushdown_sel_kernel<P, false, 2><<<grid, kThreads, 0, stream>>>(p, n, sb, out_ids, s.result + kGateSlot);
+  } else {
+    if (p.coded)
+      pushdown_sel_kernel<P, true, 4><<<grid, kThreads, 0, stream>>>(p, n, sb, out_ids, s.result + kGateSlot);
+    else
+      pushdown_sel_kernel<P, false, 4><<<grid, kThreads, 0, stream>>>(p, n, sb, out_ids, s.result + kGateSlot);
+  }
   if (p.dense_split)
     dense_chunks_kernel<P><<<grid, kThreads, 0, stream>>>(p, n, sb, out_ids, s.result + kGateSlot);
   return (int)cudaGetLastError();
 }
 int launch_pushdown_sel_small(const DevProgramSmall& p, uint64_t n, uint32_t* out_ids, int grid,
                               const Scratch& s, const SelectionBufs& sb, void* st, int gate_ranks,
-                              const PeerXchg* xg, int rank, bool finished, uint64_t* host) {
-  return launch_pushdown_sel_t(p, n, out_ids, grid, s, sb, st, gate_ranks, xg, rank, finished, host);
+                              const PeerXchg* xg, int rank, bool finished, uint64_t* host,
+                              int block_chunks) {
+  return launch_pushdown_sel_t(p, n, out_ids, grid, s, sb, st, gate_ranks, xg, rank, finished, host,
+                               block_chunks);
 }
 int launch_pushdown_sel_large(const DevProgramLarge& p, uint64_t n, uint32_t* out_ids, int grid,
                               const Scratch& s, const SelectionBufs& sb, void* st, int gate_ranks,
-                              const PeerXchg* xg, int rank, bool finished, uint64_t* host) {
-  return launch_pushdown_sel_t(p, n, out_ids, grid, s, sb, st, gate_ranks, xg, rank, finished, host);
+                              const PeerXchg* xg, int rank, bool finished, uint64_t* host,
+                              int block_chunks) {
+  return launch_pushdown_sel_t(p, n, out_ids, grid, s, sb, st, gate_ranks, xg, rank, finished, host,
+                               block_chunks);
 }
 int launch_pushdown_small(const DevProgramSmall& p, uint64_t n, uint32_t* out_ids, int grid,
                           const Scratch& s, uint64_t ticket_base, uint32_t epoch, void* st) {
@@ -1868,8 +1877,8 @@ int occupancy_count_keep_large(size_t dyn) { return occupancy_of(count_kernel<De
 int occupancy_count_large() { return occupancy_of(count_kernel<DevProgramLarge, false, kWarpsPerCta>, 0); }
 int occupancy_count_dyn_small(size_t dyn) { return occupancy_of(count_kernel<DevProgramSmall, false, kWarpsPerCta>, dyn); }
 int occupancy_count_dyn_large(size_t dyn) { return occupancy_of(count_kernel<DevProgramLarge, false, kWarpsPerCta>, dyn); }
-int occupancy_pushdown_sel_small() { return occupancy_of(pushdown_sel_kernel<DevProgramSmall, false>, 0); }
-int occupancy_pushdown_sel_large() { return occupancy_of(pushdown_sel_kernel<DevProgramLarge, false>, 0); }
+int occupancy_pushdown_sel_small() { return occupancy_of(pushdown_sel_kernel<DevProgramSmall, false, kSelBlockChunks>, 0); }
+int occupancy_pushdown_sel_large() { return occupancy_of(pushdown_sel_kernel<DevProgramLarge, false, kSelBlockChunks>, 0); }
 int occupancy_pushdown_small(size_t dyn_smem) { return occupancy_of(pushdown_kernel<DevProgramSmall>, dyn_smem); }
 int occupancy_pushdown_large(size_t dyn_smem) { return occupancy_of(pushdown_kernel<DevProgramLarge>, dyn_smem); }
 

@@ -205,7 +205,8 @@ sel_status enqueue_pushdown_sel(sel_table t, const Plan& plan, const uint32_t* p
       if (p->proj_cap_off[j] != kNoCapture) ++p->n_direct;
     }
   };
-  const uint64_t nblocks = (ntiles + kSelBlockChunks - 1) / kSelBlockChunks;
+  const int bc = pushdown_block_chunks(n);
+  const uint64_t nblocks = (ntiles + bc - 1) / bc;
   const uint64_t units = (nblocks + kWarpsPerCta - 1) / kWarpsPerCta;
   auto flags_of = [](const auto& p) {
     int f = (p.coded ? SEL_PD_CODED : 0) | (p.dense_split ? SEL_PD_WHOLE_CHUNKS : 0);
@@ -221,13 +222,13 @@ sel_status enqueue_pushdown_sel(sel_table t, const Plan& plan, const uint32_t* p
     fill_sel(&p);
     c->last_pd_flags = flags_of(p);
     le = launch_pushdown_sel_small(p, n, out_rowids, grid_for(c, units, occupancy_pushdown_sel_small()),
-                                   c->s, c->sel, stream, gate_ranks, xg, c->rank, finished, host);
+                                   c->s, c->sel, stream, gate_ranks, xg, c->rank, finished, host, bc);
   } else {
     static thread_local DevProgramLarge p;
     fill_sel(&p);
     c->last_pd_flags = flags_of(p);
     le = launch_pushdown_sel_large(p, n, out_rowids, grid_for(c, units, occupancy_pushdown_sel_large()),
-                                   c->s, c->sel, stream, gate_ranks, xg, c->rank, finished, host);
+                                   c->s, c->sel, stream, gate_ranks, xg, c->rank, finished, host, bc);
   }
   if (le != cudaSuccess) return set_error(SEL_E_CUDA, cuda_msg("push-down kernel launch", (cudaError_t)le));
   c->last_pd_path = 1;

@@ -157,10 +157,15 @@ int occupancy_count_batch();
 // superblock (two loads per lane each). No memset, no scan kernel per probe: the superblock sums
 // alternate between two halves by the parity of the device's keeping-count epoch (state[0]), and
 // a count zeroes the other half (the previous, now dead, selection's) while it runs.
-#ifndef SEL_BLOCK_CHUNKS
-#define SEL_BLOCK_CHUNKS 4   // A/B 2/4/8: 4 best (C5 push-down 0.233 -> 0.206 ms, C3 0.240 -> 0.232, C2 equal)
-#endif
-constexpr int kSelBlockChunks = SEL_BLOCK_CHUNKS;   // push-down from a selection: chunks per warp block
+// Push-down from a selection: chunks per warp block. 4 on large shards (A/B 2/4/8: C5 push-down
+// 0.233 -> 0.206 ms, C3 0.240 -> 0.232, C2 equal, 8 slower); 2 below kSmallBlockRows local rows,
+// where a 4-chunk grid runs too few rounds to balance (step A/B: 75M rows 0.2261 -> 0.2220 ms,
+// 150M equal, 300M 0.7556 -> 0.7681 with 2).
+constexpr int kSelBlockChunks = 4;
+constexpr uint64_t kSmallBlockRows = 150ull << 20;
+inline int pushdown_block_chunks(uint64_t local_rows) {
+  return local_rows < kSmallBlockRows ? 2 : kSelBlockChunks;
+}
 constexpr int kSbShift = 6;
 constexpr uint64_t kSbChunks = 1ull << kSbShift;
 constexpr int kHbShift = 12;                          // chunks per hyperblock: 4096
@@ -287,14 +292,17 @@ int launch_count_large(const DevProgramLarge& p, uint64_t n, int grid, const Scr
 // local count to s.result[0] and finishes the result words (ExecFinish with gate_ranks, rank,
 // host; xg != nullptr: through the peer exchange); then the compaction/gather kernel and, with
 // p.dense_split, the whole-chunk copy kernel.
+// block_chunks: chunks per warp block of the compaction kernel, 2 or 4 (pushdown_block_chunks).
 int launch_pushdown_sel_small(const DevProgramSmall& p, uint64_t n, uint32_t* out_ids, int grid,
                               const Scratch& s, const SelectionBufs& sb, void* stream,
                               int gate_ranks = 0, const PeerXchg* xg = nullptr, int rank = 0,
-                              bool finished = false, uint64_t* host = nullptr);
+                              bool finished = false, uint64_t* host = nullptr,
+                              int block_chunks = kSelBlockChunks);
 int launch_pushdown_sel_large(const DevProgramLarge& p, uint64_t n, uint32_t* out_ids, int grid,
                               const Scratch& s, const SelectionBufs& sb, void* stream,
                               int gate_ranks = 0, const PeerXchg* xg = nullptr, int rank = 0,
-                              bool finished = false, uint64_t* host = nullptr);
+                              bool finished = false, uint64_t* host = nullptr,
+                              int block_chunks = kSelBlockChunks);
 int launch_pushdown_small(const DevProgramSmall& p, uint64_t n, uint32_t* out_ids, int grid,
                           const Scratch& s, uint64_t ticket_base, uint32_t epoch, void* stream);
 int launch_pushdown_large(const DevProgramLarge& p, uint64_t n, uint32_t* out_ids, int grid,
