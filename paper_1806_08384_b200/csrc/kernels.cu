@@ -31,6 +31,10 @@
 
 #include "sel_internal.h"
 
+#ifndef SEL_BATCH_PREFETCH
+#define SEL_BATCH_PREFETCH 1   // batch count: bulk-prefetch a chunk's later columns into L2
+#endif
+
 
 namespace sel {
 namespace {
@@ -1541,6 +1545,17 @@ template <bool TAIL>
 __device__ __forceinline__ void batch_chunk(const BatchProgram& p, uint64_t base, int lane,
                                             uint32_t nvalid, uint32_t* lm, uint32_t* cnt /* [k] */,
                                             uint32_t (&acc)[8]) {
+#if SEL_BATCH_PREFETCH
+  // the chunk's other columns are loaded only after the first one is evaluated: start their DRAM
+  // reads now (TMA bulk prefetch into L2), so that their loads later hit L2
+  if (!TAIL && lane == 0) {
+#pragma unroll 1
+    for (uint32_t c = 1; c < p.n_cols; ++c) {
+      const uint32_t w = 1u << p.col[c].wclass;
+      prefetch_l2(static_cast<const char*>(p.col[c].data) + base * w, kChunkRows * w);
+    }
+  }
+#endif
 #pragma unroll 1
   for (uint32_t c = 0; c < p.n_cols; ++c) batch_column<TAIL>(p, p.col[c], base, lane, nvalid, lm);
   __syncwarp();
