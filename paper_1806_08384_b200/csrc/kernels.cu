@@ -921,17 +921,9 @@ __device__ __forceinline__ uint32_t to_row_major(uint32_t m, int lane) {
 }
 
 __device__ __forceinline__ void st_evict_last(uint32_t* p, uint32_t v) {
-#if SEL_AB_PLAINST == 1   // A/B: a plain store
-  *p = v;
-#elif SEL_AB_PLAINST == 2   // A/B: the hinted store without the compiler memory barrier
-  uint64_t pol;
-  asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
-  asm volatile("st.global.L2::cache_hint.u32 [%0], %1, %2;" ::"l"(p), "r"(v), "l"(pol));
-#else
   uint64_t pol;
   asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
   asm volatile("st.global.L2::cache_hint.u32 [%0], %1, %2;" ::"l"(p), "r"(v), "l"(pol) : "memory");
-#endif
 }
 
 // coded: also keep the coded leaf's point-1 matches (wm, the count's quad layout) row-major.
@@ -941,13 +933,8 @@ __device__ __forceinline__ uint32_t keep_chunk(const SelectionBufs& sb, uint32_t
                                                uint32_t m, char* wsmem, uint32_t wm = 0u,
                                                bool coded = false) {
   if (!KEEP) return 0u;
-#if SEL_KEEP_QUAD   // A/B only (timing of the transposition; the push-down needs row-major)
-  if (coded) st_evict_last(sb.which + c * 32 + lane, wm);
-  const uint32_t t = m;
-#else
   if (coded) st_evict_last(sb.which + c * 32 + lane, to_row_major(wm, lane));
   const uint32_t t = to_row_major(m, lane);          // the push-down stages from row-major masks
-#endif
   if (sb.n_keep) {
     sb.bits[c * 32 + lane] = t;
   } else {
@@ -955,9 +942,7 @@ __device__ __forceinline__ uint32_t keep_chunk(const SelectionBufs& sb, uint32_t
     // being written back while the scan streams its columns (measured: C5 count 0.638 -> 0.629
     // ms, C4 push-down 0.176 -> 0.160 ms). With kept values the slots compete for L2 and the
     // policy hurt (C2 0.913 -> 0.968 ms), so it is not used there.
-#if !SEL_AB_NOMASK   // A/B only: the cost of the mask store (the push-down needs it)
     st_evict_last(sb.bits + c * 32 + lane, t);
-#endif
   }
   uint32_t cc;
   if (sb.n_keep) {
@@ -979,12 +964,10 @@ __device__ __forceinline__ uint32_t keep_chunk(const SelectionBufs& sb, uint32_t
   } else {
     cc = __reduce_add_sync(0xFFFFFFFFu, (uint32_t)__popc(m));
   }
-#if !SEL_AB_NOCNT    // A/B only: the cost of the count store and the superblock atomic
   if (lane == 0) {
     sb.chunk_cnt[c] = (uint16_t)cc;
     if (cc) atomicAdd(sbs + (c >> kSbShift), cc);
   }
-#endif
   return cc;
 }
 
