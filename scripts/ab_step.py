@@ -4,7 +4,8 @@ counts), so slow drifts of the box hit all variants alike. Prints one JSON line 
 (variant, rows) with the median over rounds of each round's median step (CUDA events over
 back-to-back graph launches) and the library's per-kernel times.
 
-    python scripts/ab_step.py <rounds> <rows,rows,...> base=<path|-> name=<path> ...
+    python scripts/ab_step.py <rounds> <rows,rows,...> base=<path|-> name=<path>[@KEY=VAL,...] ...
+    (a variant's @KEY=VAL pairs are set in its subprocess's environment)
     python scripts/ab_step.py --child <rows,...>        (one measurement, used internally)
 """
 import json
@@ -67,11 +68,15 @@ def main():
     variants = [a.split("=", 1) for a in sys.argv[3:]]
     res = {name: [] for name, _ in variants}
     for _ in range(rounds):
-        for name, path in variants:
+        for name, spec in variants:
             env = dict(os.environ)
             env.pop("SEL_LIB", None)
+            path, _, extra = spec.partition("@")
             if path != "-":
                 env["SEL_LIB"] = path
+            for kv in filter(None, extra.split(",")):
+                k, _, v = kv.partition("=")
+                env[k] = v
             r = subprocess.run([sys.executable, __file__, "--child", rows], env=env,
                                capture_output=True, text=True, timeout=600)
             if r.returncode != 0:
