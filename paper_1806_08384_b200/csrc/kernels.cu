@@ -196,12 +196,13 @@ __device__ __forceinline__ uint64_t kept_base(const SelectionBufs& sb, const uin
 
 // The last CTA of a keeping count (NW warps): the exclusive prefix of the hyperblock sums, each
 // summed here from this count's superblock sums (thread t sums whole hyperblocks with 16-byte
-// loads, all issued together; <= 4 per thread), the local count and the full-chunk flag beside
-// it, and the epoch advanced (this count's half of the superblock sums becomes the selection's;
-// the next count zeroes the other one, nsb words).
+// loads, all issued together; <= 4 per thread), the local count (their total, returned: no pass
+// over the per-CTA partials) and the full-chunk flag beside it, and the epoch advanced (this
+// count's half of the superblock sums becomes the selection's; the next count zeroes the other
+// one, nsb words).
 template <int NW>
-__device__ void finish_selection(const SelectionBufs& sb, uint64_t n, uint32_t local, uint32_t e,
-                                 const uint32_t* my_sb) {
+__device__ uint32_t finish_selection(const SelectionBufs& sb, uint64_t n, uint32_t e,
+                                     const uint32_t* my_sb) {
   constexpr uint32_t T = NW * 32;
   constexpr uint32_t kSbPerHb = 1u << (kHbShift - kSbShift);
   const uint32_t t = threadIdx.x, lane = t & 31, warp = t >> 5;
@@ -234,6 +235,7 @@ __device__ void finish_selection(const SelectionBufs& sb, uint64_t n, uint32_t l
     if (lane >= (uint32_t)d) incl += x;
   }
   __shared__ uint32_t s_w[NW];
+  __shared__ uint32_t s_all;
   if (lane == 31) s_w[warp] = incl;
   __syncthreads();
   if (warp == 0) {
@@ -245,8 +247,10 @@ __device__ void finish_selection(const SelectionBufs& sb, uint64_t n, uint32_t l
       if (lane >= (uint32_t)d) wi += x;
     }
     if (lane < (uint32_t)NW) s_w[lane] = wi - w;
+    if (lane == 31) s_all = wi;
   }
   __syncthreads();
+  const uint32_t local = s_all;
   uint32_t run = s_w[warp] + incl - sum;
 #pragma unroll
   for (uint32_t k = 0; k < 4; ++k) {
@@ -260,6 +264,7 @@ __device__ void finish_selection(const SelectionBufs& sb, uint64_t n, uint32_t l
     sb.state[1 + (e & 1u)] = nsb;
     sb.state[0] = e + 1u;
   }
+  return local;
 }
 
 // Prefetch every predicate column of chunk `c` into L2 (issued by one lane a chunk ahead).
@@ -1084,25 +1089,34 @@ __global__ void __launch_bounds__(NW * 32, NW == kWarpsPerCta ? (FASTN ? SEL_FAS
   __syncthreads();
   if (s_last) {
     __threadfence();
-    uint64_t s = 0;
-    for (uint32_t b = threadIdx.x; b < gridDim.x; b += (NW * 32)) s += ((volatile uint64_t*)partials)[b];
-    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xFFFFFFFFu, s, o);
-    __shared__ uint64_t s_sum[NW];
-    __shared__ uint64_t s_total;
-    if (lane == 0) s_sum[warp] = s;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      uint64_t t = 0;
+    uint64_t local;
+    if constexpr (KEEP) {
+      // keeping counts: the hyperblock prefix the push-down starts from (no kernel in between);
+      // its total is the local count
+      local = finish_selection<NW>(sb, n, epoch, my_sb);
+      if (threadIdx.x == 0) {
+        *out = local;
+        *done = 0u;
+      }
+    } else {
+      uint64_t s = 0;
+      for (uint32_t b = threadIdx.x; b < gridDim.x; b += (NW * 32)) s += ((volatile uint64_t*)partials)[b];
+      for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xFFFFFFFFu, s, o);
+      __shared__ uint64_t s_sum[NW];
+      __shared__ uint64_t s_total;
+      if (lane == 0) s_sum[warp] = s;
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        uint64_t t = 0;
 #pragma unroll
-      for (int w = 0; w < NW; ++w) t += s_sum[w];
-      *out = t;
-      *done = 0u;
-      s_total = t;
+        for (int w = 0; w < NW; ++w) t += s_sum[w];
+        *out = t;
+        *done = 0u;
+        s_total = t;
+      }
+      __syncthreads();
+      local = s_total;
     }
-    __syncthreads();
-    const uint64_t local = s_total;
-    // keeping counts: the superblock prefix the push-down starts from (no kernel in between)
-    if constexpr (KEEP) finish_selection<NW>(sb, n, (uint32_t)local, epoch, my_sb);
     if (fin.result) {
       // a device-gated Execute: its result words (and, with peers, the exchange) right here
       __syncthreads();
