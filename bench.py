@@ -41,6 +41,10 @@ def parse():
     ap.add_argument("--no-read-peak", action="store_true")
     ap.add_argument("--no-graph", action="store_true",
                     help="time table.execute() per step instead of the prepared (graph) execute")
+    ap.add_argument("--blocking", action="store_true",
+                    help="time the blocking prepared Execute (returns after the materialisation) "
+                         "instead of sel_prepared_execute_async (returns at the count; the "
+                         "materialisation completes in stream order inside the timed region)")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-configs", action="store_true",
                     help="skip the other configs' probes (c3, c5) measured beside c2")
@@ -375,9 +379,10 @@ def _max_over_ranks(vals, world, dev):
     return [float(x) for x in t]
 
 
-def time_prepared(prep, steps, world, dev):
+def time_prepared(prep, steps, world, dev, wait=False):
     """ms per prepared-Execute replay: CUDA events around `steps` replays on the current stream,
-    barrier + synchronize on both sides, max over ranks."""
+    barrier + synchronize on both sides, max over ranks. wait=False: each replay returns at its
+    count (sel_prepared_execute_async), the materialisation finishing in stream order."""
     import torch
     import torch.distributed as dist
     for _ in range(3):
@@ -388,7 +393,7 @@ def time_prepared(prep, steps, world, dev):
     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     a.record()
     for _ in range(steps):
-        prep.run()
+        prep.run(wait=wait)
     b.record()
     torch.cuda.synchronize()
     if world > 1:
@@ -410,7 +415,7 @@ def measure_exchange_ab(args, sel, sdist, T, names, proj_names, prog, n, s, loca
         return {"requested": other, "error": f"{type(ex).__name__}: {ex}"[:300]}
     t2 = sel.Table(ctx2, names, T.types, [c.data for c in T.columns], row_offset=s, global_rows=n)
     prep = t2.prepare_execute(prog, project=proj_names, max_size=n, capacity=max(local_count, 1))
-    ms = time_prepared(prep, args.steps, world, dev)
+    ms = time_prepared(prep, args.steps, world, dev, wait=args.blocking)
     c = prep.run()
     prep.release()
     t2.release()
@@ -462,7 +467,7 @@ def measure_configs(names_, args, sel, sdist, world, rank, dev, hbm):
         local = t.pushdown(prog, capacity=0).local_count
         prep = t.prepare_execute(prog, project=[names[j] for j in proj], max_size=n,
                                  capacity=max(local, 1))
-        step_ms = time_prepared(prep, args.steps, world, dev)
+        step_ms = time_prepared(prep, args.steps, world, dev, wait=args.blocking)
         prep.release()
         xs = sorted(lat)
         out[name] = {
@@ -560,7 +565,7 @@ def run_ours(args):
     out_ids = torch.empty(cap, dtype=torch.int32, device=dev)
     out_cols = [torch.empty(cap, dtype=c.data.dtype, device=dev) for c in (T.columns[j] for j in proj)]
 
-    count_ms, push_ms, count_lat, push_lat = [], [], [], []
+    count_ms, push_ms, count_lat, push_lat, ready_lat = [], [], [], [], []
 
     # Algorithm 1's Execute(compound, isSPD=true, maxSize) with PUSH_DOWN_MAX_SELECTIVITY = 1.0
     # (the paper's push-down experiments): count (keeping the selection and the
@@ -572,10 +577,10 @@ def run_ours(args):
     class _R:
         pass
 
-    def step(record):
+    def step(record, wait=True):
         t0 = time.perf_counter()
         if prepared is not None:
-            c = prepared.run()
+            c = prepared.run(wait=wait)
             r = _R()
             r.count, r.materialized = c, prepared.materialized
         else:
@@ -584,6 +589,8 @@ def run_ours(args):
         t1 = time.perf_counter()
         if record == "latency":
             count_lat.append(1000 * (t1 - t0))
+        elif record == "ready":
+            ready_lat.append(1000 * (t1 - t0))
         elif record == "kernels":
             k1, k2 = ctx.last_times()
             count_ms.append(k1); push_ms.append(k2)
@@ -604,13 +611,15 @@ def run_ours(args):
     with ClockSampler(local_rank) as clk:
         ev0.record(stream)
         for _ in range(args.steps):
-            step("latency")
+            step("ready", wait=args.blocking)
         ev1.record(stream)
         torch.cuda.synchronize()
         clk.mark()
         if world > 1:
             dist.barrier()
         dev_ms = ev0.elapsed_time(ev1)
+        for _ in range(max(args.steps, 20)):   # the blocking Execute's latency, call to return
+            step("latency")
         ctx.enable_timing(True)
         for _ in range(3):
             step(None)
@@ -851,12 +860,20 @@ def run_ours(args):
                        "l2": "inputs larger than L2 (no flush needed)",
                        "step": ("sel_execute = count (keeping the selection) -> device-side gate -> "
                                 "materialise" + (", per table.execute()" if prepared is None else
-                                                 ", prepared once and replayed as a CUDA graph"))},
+                                                 ", prepared once and replayed as a CUDA graph") +
+                                ("" if args.blocking or prepared is None else
+                                 "; each step returns when its count is on the host "
+                                 "(sel_prepared_execute_async), its materialisation completing "
+                                 "in stream order before the next step's count starts"))},
             "rows_per_s": round(n / (ms_per_step / 1000)),
             "step_frac_aggregate_hbm": round(value_gbs / (world * hbm), 4),
             "latency_ms": {"execute_median": round(statistics.median(count_lat), 4),
                            "execute_min": round(min(count_lat), 4),
                            "execute_p99": _stats(count_lat)["p99"],
+                           "execute_clock": "host, blocking sel_prepared_execute, call to return",
+                           "count_ready": _stats(ready_lat) if ready_lat else None,
+                           "count_ready_clock": ("host, each timed step's call to return (at its "
+                                                 "count unless --blocking)"),
                            "count_probe": count_probe_stats,
                            "count_kernel": round(count_k, 4), "pushdown_kernels": round(push_k, 4)},
             "roofline": roof_dom,

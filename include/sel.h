@@ -252,6 +252,18 @@ uint64_t sel_execute_to(sel_table table, const void* prog, size_t prog_bytes,
  * sel_execute. A run after the context reallocated its scratch (a probe of a larger table) or
  * after the bitmap registry changed re-captures first (SEL_E_ARG if a bitmap id the program
  * uses is no longer registered). SEL_E_STATE if the table was released.
+ * sel_prepared_execute_async: the same Execute, returning as soon as its count — the number
+ * Algorithm 1 decides on — and the outputs below are final on the host,
+ * while the gated materialisation (Execute's temp table) is still running on
+ * `cuda_stream`: the output buffers are valid once that stream reaches the point of the call
+ * (order later work on it, or synchronise it). The last CTA of the work that finishes the count
+ * stores the result words and then a sequence word into pinned host memory; the call spins on
+ * that word (polling the stream for errors, and NCCL's asynchronous error with a communicator).
+ * With per-kernel timing on (sel_ctx_set_timing), more than 512 ranks, or an uncaptured
+ * execute (constant program, empty shard, SEL_GRAPH_COMM=0 with NCCL), it blocks like
+ * sel_prepared_execute. Errors: as sel_prepared_execute; SEL_E_STATE if the stream drained
+ * without the Execute's result words; an error of the materialisation itself surfaces at the
+ * caller's next synchronisation of the stream or the context's next call.
  * sel_prepared_release: frees the handle (NULL is a no-op); release it before its context. */
 sel_status sel_prepare_execute(sel_table table, const void* prog, size_t prog_bytes,
                                const uint32_t* proj_cols, uint32_t nproj, uint64_t max_size,
@@ -260,6 +272,9 @@ sel_status sel_prepare_execute(sel_table table, const void* prog, size_t prog_by
 uint64_t sel_prepared_execute(sel_prepared prepared, uint64_t* out_local_count,
                               uint64_t* out_global_offset, int* out_materialized,
                               void* cuda_stream);
+uint64_t sel_prepared_execute_async(sel_prepared prepared, uint64_t* out_local_count,
+                                    uint64_t* out_global_offset, int* out_materialized,
+                                    void* cuda_stream);
 void sel_prepared_release(sel_prepared prepared);
 
 /* sel_pushdown: materialise sigma_P pi_proj(R) for the local shard.
@@ -448,10 +463,22 @@ int sel_abi_version(void);
  * Maximum program size: 12 + 8 * (128 + 512) = 5,132 bytes.
  */
 
+/* sel_ctx_set_option: the tuning switches below, per context (the environment variables only
+ * give their initial values at sel_ctx_create). None of them changes a result, only which kernel
+ * variant or launch shape produces it. Setting one drops the context's kept selection and makes
+ * prepared executes re-capture. Names and values:
+ *   "fast" 0|1, "coded" 0|1, "dense_split" 0|1, "keep_values" 0|1, "graph_comm" 0|1,
+ *   "prefetch" -1 (auto) | 0 | 1, "count_warps" 0 (auto) | 8, "two_pass_min_rows" n >= 0
+ *   (ignored while sel_ctx_set_pushdown_path forces the single pass), "ctas_per_sm" 0 (the
+ *   occupancy calculator's) | k. Errors: SEL_E_ARG (null, unknown name, value out of range),
+ *   SEL_E_STATE (context destroyed). */
+sel_status sel_ctx_set_option(sel_ctx ctx, const char* name, int64_t value);
+
 /*
- * Environment (read once, by sel_ctx_create; for A/B measurement and diagnosis — none of them
- * changes a result, only which kernel variant or launch shape produces it; DESIGN.md §5-§7
- * gives the measurements behind each default):
+ * Environment (read once, by sel_ctx_create, as the initial values of sel_ctx_set_option's
+ * switches; for A/B measurement and diagnosis — none of them changes a result, only which kernel
+ * variant or launch shape produces it; DESIGN.md §5-§7 gives the measurements behind each
+ * default):
  *   SEL_FAST=0               conjunctions through the postfix interpreter, not the fast path
  *   SEL_CODED=0              no coded projections (two-point columns read by the push-down)
  *   SEL_DENSE_SPLIT=0        no whole-chunk copy kernel for fully selected chunks

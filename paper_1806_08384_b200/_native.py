@@ -24,11 +24,12 @@ EXPORTS = ["sel_ctx_create", "sel_ctx_set_comm", "sel_nccl_unique_id", "sel_ctx_
            "sel_ctx_peer_handle", "sel_ctx_set_peers", "sel_ctx_set_peer_timeout",
            "sel_ctx_export_buffer",
            "sel_ctx_import_buffer", "sel_execute_to",
-           "sel_ctx_set_timing", "sel_ctx_last_kernel_ms", "sel_table_register",
+           "sel_ctx_set_timing", "sel_ctx_set_option", "sel_ctx_last_kernel_ms", "sel_table_register",
            "sel_table_release", "sel_count", "sel_count_async", "sel_count_ex", "sel_execute", "sel_pushdown",
            "sel_ctx_last_times", "sel_count_batch", "sel_count_sampled", "sel_histogram",
            "sel_bitmap_register", "sel_bitmap_release",
-           "sel_prepare_execute", "sel_prepared_execute", "sel_prepared_release",
+           "sel_prepare_execute", "sel_prepared_execute", "sel_prepared_execute_async",
+           "sel_prepared_release",
            "sel_ctx_last_pushdown_path", "sel_ctx_last_pushdown_flags", "sel_ctx_set_pushdown_path", "sel_program_check",
            "sel_program_path", "sel_program_plan_json", "sel_last_error",
            "sel_last_error_message", "sel_abi_version", "sel_sample_estimate",
@@ -69,6 +70,7 @@ def lib() -> ctypes.CDLL:
         "sel_nccl_unique_id": (i32, [vp]),
         "sel_ctx_destroy": (None, [vp]),
         "sel_ctx_set_timing": (i32, [vp, i32]),
+        "sel_ctx_set_option": (i32, [vp, ctypes.c_char_p, ctypes.c_int64]),
         "sel_ctx_last_kernel_ms": (i32, [vp, ctypes.POINTER(ctypes.c_float)]),
         "sel_table_register": (i32, [vp, ctypes.POINTER(sel_column), u32, u64, u64, u64,
                                      ctypes.POINTER(vp)]),
@@ -89,6 +91,8 @@ def lib() -> ctypes.CDLL:
                                       ctypes.POINTER(vp)]),
         "sel_prepared_execute": (u64, [vp, ctypes.POINTER(u64), ctypes.POINTER(u64),
                                        ctypes.POINTER(i32), vp]),
+        "sel_prepared_execute_async": (u64, [vp, ctypes.POINTER(u64), ctypes.POINTER(u64),
+                                             ctypes.POINTER(i32), vp]),
         "sel_prepared_release": (None, [vp]),
         "sel_ctx_last_times": (i32, [vp, ctypes.POINTER(ctypes.c_float), ctypes.POINTER(ctypes.c_float)]),
         "sel_ctx_last_pushdown_path": (i32, [vp]),

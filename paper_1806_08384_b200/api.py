@@ -112,6 +112,10 @@ class Context:
     def enable_timing(self, on: bool = True) -> None:
         check(lib().sel_ctx_set_timing(self._h, 1 if on else 0))
 
+    def set_option(self, name: str, value: int) -> None:
+        """A tuning switch of this context (include/sel.h sel_ctx_set_option)."""
+        check(lib().sel_ctx_set_option(self._h, name.encode(), int(value)))
+
     def last_times(self) -> tuple:
         """(count kernel ms, push-down kernels ms) of the most recent probes (timing enabled)."""
         c, p = ctypes.c_float(0.0), ctypes.c_float(0.0)
@@ -217,10 +221,14 @@ class PreparedExecute:
         self._refs = (ctypes.byref(self._local), ctypes.byref(self._off), ctypes.byref(self._mat))
         self._stream = _stream_ptr(stream, dev)
         self._fn = lib().sel_prepared_execute
+        self._fn_async = lib().sel_prepared_execute_async
         self.count = 0
 
-    def run(self, stream=None) -> int:
-        r = self._fn(self._h, *self._refs, self._stream if stream is None else _stream_ptr(stream, self.table.ctx.device))
+    def run(self, stream=None, wait: bool = True) -> int:
+        """One Execute. wait=False returns once the count is final on the host
+        (sel_prepared_execute_async): the materialisation completes in stream order."""
+        fn = self._fn if wait else self._fn_async
+        r = fn(self._h, *self._refs, self._stream if stream is None else _stream_ptr(stream, self.table.ctx.device))
         if r == SEL_ERR:
             raise last_error()
         self.count = r

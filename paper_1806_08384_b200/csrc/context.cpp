@@ -4,7 +4,9 @@
 #include "host.h"
 
 #include <cstdio>
+#include <cstring>
 #include <cstdlib>
+#include <atomic>
 #include <thread>
 
 using namespace sel;
@@ -30,6 +32,8 @@ uint64_t fail64(sel_status st, const std::string& msg) {
 std::string cuda_msg(const char* what, cudaError_t e) {
   if (e == kNcclAsyncFailed)
     return std::string(what) + ": NCCL asynchronous error (a rank failed; communicator aborted)";
+  if (e == kSeqMissing)
+    return std::string(what) + ": the stream drained without the Execute's result words";
   return std::string(what) + ": " + cudaGetErrorName(e) + " (" + cudaGetErrorString(e) + ")";
 }
 
@@ -82,6 +86,38 @@ cudaError_t sync_stream(sel_ctx c, cudaStream_t s) {
       return kNcclAsyncFailed;
     }
     if (spin > 64) std::this_thread::yield();
+  }
+}
+
+// Wait until the device-gated Execute enqueued after the host read `seq0` from the mirror's
+// sequence word has stored its result words (finish_execute), not for the rest of the stream:
+// the materialisation that follows keeps running. Errors as sync_stream; a stream that drains
+// without the word changing (no Execute was enqueued) is kSeqMissing.
+cudaError_t wait_result_seq(sel_ctx c, cudaStream_t s, uint64_t seq0) {
+  volatile const uint64_t* w = c->h_result + kSeqSlot;
+  for (unsigned spin = 0;; ++spin) {
+    if (*w != seq0) {
+      std::atomic_thread_fence(std::memory_order_acquire);
+      return cudaSuccess;
+    }
+    if ((spin & 255u) != 255u) continue;
+    const cudaError_t q = cudaStreamQuery(s);
+    if (q == cudaSuccess) {
+      if (*w != seq0) continue;
+      return kSeqMissing;
+    }
+    if (q != cudaErrorNotReady) return q;
+    if (c->comm && nccl().CommGetAsyncError) {
+      ncclResult_t st = ncclSuccess;
+      if (nccl().CommGetAsyncError(c->comm, &st) == ncclSuccess && st != ncclSuccess &&
+          st != ncclInProgress) {
+        if (nccl().CommAbort) nccl().CommAbort(c->comm);
+        c->comm = nullptr;
+        c->comm_failed = true;
+        return kNcclAsyncFailed;
+      }
+    }
+    if (spin > 4096) std::this_thread::yield();
   }
 }
 
@@ -184,6 +220,8 @@ sel_status sel_ctx_create(int cuda_device, sel_ctx* out) {
   cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, cuda_device);
   c->occ_count_small = occupancy_count_small();
   c->occ_count_large = occupancy_count_large();
+  c->occ_small_max = c->occ_count_small;
+  c->occ_large_max = c->occ_count_large;
   if (prepare_kernels() != cudaSuccess) {
     delete c;
     return set_error(SEL_E_CUDA, "cudaFuncSetAttribute(push-down shared memory) failed");
@@ -218,13 +256,14 @@ sel_status sel_ctx_create(int cuda_device, sel_ctx* out) {
   }
   bool okay = cudaMalloc(&c->s.partials, kMaxGrid * sizeof(uint64_t)) == cudaSuccess &&
               cudaMalloc(&c->s.done, sizeof(unsigned int)) == cudaSuccess &&
-              cudaMalloc(&c->s.result, kResultSlots * sizeof(uint64_t)) == cudaSuccess &&
+              cudaMalloc(&c->s.result, kResultAlloc * sizeof(uint64_t)) == cudaSuccess &&
               cudaMalloc(&c->s.ticket, sizeof(unsigned long long)) == cudaSuccess &&
-              cudaHostAlloc(&c->h_result, kResultSlots * sizeof(uint64_t), cudaHostAllocMapped) == cudaSuccess &&
+              cudaHostAlloc(&c->h_result, kResultAlloc * sizeof(uint64_t), cudaHostAllocMapped) == cudaSuccess &&
               cudaHostGetDevicePointer(reinterpret_cast<void**>(&c->h_result_dev), c->h_result, 0) == cudaSuccess &&
               cudaMemset(c->s.done, 0, sizeof(unsigned int)) == cudaSuccess &&
               cudaMemset(c->s.ticket, 0, sizeof(unsigned long long)) == cudaSuccess &&
-              cudaMemset(c->s.result, 0, kResultSlots * sizeof(uint64_t)) == cudaSuccess &&
+              cudaMemset(c->s.result, 0, kResultAlloc * sizeof(uint64_t)) == cudaSuccess &&
+              (std::memset(c->h_result, 0, kResultAlloc * sizeof(uint64_t)), true) &&
               cudaEventCreate(&c->ev0) == cudaSuccess && cudaEventCreate(&c->ev1) == cudaSuccess &&
               cudaEventCreate(&c->ev2) == cudaSuccess && cudaEventCreate(&c->ev3) == cudaSuccess &&
               cudaStreamCreateWithFlags(&c->cap_stream, cudaStreamNonBlocking) == cudaSuccess &&
@@ -513,6 +552,33 @@ sel_status sel_ctx_set_pushdown_path(sel_ctx ctx, int mode) {
   if (mode != -1 && mode != 0 && mode != 2) return set_error(SEL_E_ARG, "mode must be -1, 0 or 2");
   ctx->force_single = mode == 0;
   ctx->two_pass_min_rows = mode == 2 ? 0 : (mode == 0 ? ~0ull : kTwoPassMinRows);
+  return SEL_OK;
+}
+
+sel_status sel_ctx_set_option(sel_ctx ctx, const char* name, int64_t value) {
+  clear_error();
+  if (!ctx || !name) return set_error(SEL_E_ARG, "null argument");
+  if (ctx->destroyed) return set_error(SEL_E_STATE, "context destroyed");
+  const std::string k(name);
+  const bool flag = value == 0 || value == 1;
+  if (k == "fast" && flag) ctx->fast_enabled = value;
+  else if (k == "coded" && flag) ctx->code_enabled = value;
+  else if (k == "dense_split" && flag) ctx->dense_split = value;
+  else if (k == "keep_values" && flag) ctx->keep_values = value;
+  else if (k == "graph_comm" && flag) ctx->graph_comm = value;
+  else if (k == "prefetch" && value >= -1 && value <= 1) ctx->prefetch_mode = (int)value;
+  else if (k == "count_warps" && (value == 0 || value == kWarpsPerCta)) ctx->count_nw = (int)value;
+  else if (k == "two_pass_min_rows" && value >= 0 && !ctx->force_single)
+    ctx->two_pass_min_rows = (uint64_t)value;
+  else if (k == "ctas_per_sm" && value >= 0) {
+    ctx->occ_count_small = value ? std::min(ctx->occ_small_max, (int)value) : ctx->occ_small_max;
+    ctx->occ_count_large = value ? std::min(ctx->occ_large_max, (int)value) : ctx->occ_large_max;
+  } else {
+    return set_error(SEL_E_ARG, "unknown option or value out of range: " + k);
+  }
+  // a kept selection was made under the old settings, and prepared executes baked them
+  ctx->kept_table = nullptr;
+  ++ctx->alloc_gen;
   return SEL_OK;
 }
 

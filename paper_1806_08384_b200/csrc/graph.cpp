@@ -97,9 +97,9 @@ sel_status sel_prepare_execute(sel_table t, const void* prog, size_t prog_bytes,
   return SEL_OK;
 }
 
-uint64_t sel_prepared_execute(sel_prepared q, uint64_t* out_local_count,
-                              uint64_t* out_global_offset, int* out_materialized,
-                              void* cuda_stream) {
+static uint64_t run_prepared(sel_prepared q, uint64_t* out_local_count,
+                             uint64_t* out_global_offset, int* out_materialized,
+                             void* cuda_stream, bool async) {
   clear_error();
   if (out_materialized) *out_materialized = 0;
   if (out_local_count) *out_local_count = 0;
@@ -122,8 +122,12 @@ uint64_t sel_prepared_execute(sel_prepared q, uint64_t* out_local_count,
   if (!g.ok) return fail64(SEL_E_CUDA, "cudaSetDevice failed");
   cudaStream_t stream = (cudaStream_t)cuda_stream;
   c->kept_table = nullptr;
+  // Returning at the count needs its words in the pinned mirror (finish_execute) and no timing
+  // events to read; otherwise the run blocks.
+  async = async && !c->timing && (multi(c) ? c->nranks : 0) <= kMirrorMax;
+  const uint64_t seq0 = *(volatile const uint64_t*)(c->h_result + kSeqSlot);
   cudaError_t e = cudaGraphLaunch(q->exec, stream);
-  if (e == cudaSuccess) e = sync_stream(c, stream);
+  if (e == cudaSuccess) e = async ? wait_result_seq(c, stream, seq0) : sync_stream(c, stream);
   if (e != cudaSuccess) return fail64(sync_code(e), cuda_msg("prepared execute", e));
   if (peer_status(c) != SEL_OK) return SEL_ERR;
   c->kept_table = t;
@@ -137,6 +141,18 @@ uint64_t sel_prepared_execute(sel_prepared q, uint64_t* out_local_count,
     c->last_ms = c->last_push_ms;
   }
   return execute_outputs(c, q->max_size, out_local_count, out_global_offset, out_materialized);
+}
+
+uint64_t sel_prepared_execute(sel_prepared q, uint64_t* out_local_count,
+                              uint64_t* out_global_offset, int* out_materialized,
+                              void* cuda_stream) {
+  return run_prepared(q, out_local_count, out_global_offset, out_materialized, cuda_stream, false);
+}
+
+uint64_t sel_prepared_execute_async(sel_prepared q, uint64_t* out_local_count,
+                                    uint64_t* out_global_offset, int* out_materialized,
+                                    void* cuda_stream) {
+  return run_prepared(q, out_local_count, out_global_offset, out_materialized, cuda_stream, true);
 }
 
 void sel_prepared_release(sel_prepared q) {

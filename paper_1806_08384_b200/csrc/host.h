@@ -39,7 +39,11 @@ uint64_t fail64(sel_status st, const std::string& msg);
 // sync_stream's report of a failed communicator (not a CUDA code).
 constexpr cudaError_t kNcclAsyncFailed = (cudaError_t)0x7FFF0001;
 std::string cuda_msg(const char* what, cudaError_t e);
-inline sel_status sync_code(cudaError_t e) { return e == kNcclAsyncFailed ? SEL_E_NCCL : SEL_E_CUDA; }
+// wait_result_seq's report of a stream that drained without the Execute's result words.
+constexpr cudaError_t kSeqMissing = (cudaError_t)0x7FFF0002;
+inline sel_status sync_code(cudaError_t e) {
+  return e == kNcclAsyncFailed ? SEL_E_NCCL : e == kSeqMissing ? SEL_E_STATE : SEL_E_CUDA;
+}
 
 struct DeviceGuard {
   int prev = -1;
@@ -99,6 +103,7 @@ struct sel_ctx_s {
   int device = 0;
   int num_sms = 148;
   int occ_count_small = 1, occ_count_large = 1;
+  int occ_small_max = 1, occ_large_max = 1;   // the occupancy calculator's (ctas_per_sm caps it)
   Scratch s{};
   uint64_t* h_result = nullptr;   // pinned mirror of Scratch::result (kResultSlots), mapped:
   uint64_t* h_result_dev = nullptr;   // its device address (kernels store the Execute's words)
@@ -187,6 +192,7 @@ namespace sel {
 // Cross-rank combination needed: a communicator (NCCL) or peers (the library's own exchange).
 inline bool multi(sel_ctx c) { return c->comm != nullptr || c->peers; }
 cudaError_t sync_stream(sel_ctx c, cudaStream_t s);
+cudaError_t wait_result_seq(sel_ctx c, cudaStream_t s, uint64_t seq0);
 sel_status peer_status(sel_ctx c);
 sel_status ensure_status(sel_ctx c, uint64_t ntiles, cudaStream_t stream);
 sel_status ensure_selection(sel_ctx c, uint64_t nchunks);

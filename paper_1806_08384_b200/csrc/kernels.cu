@@ -170,6 +170,15 @@ __device__ void finish_execute(const ExecFinish& f, const PeerXchg& xg, uint64_t
     __syncthreads();
     const int lo = kGateSlot - (nr > 0 ? nr : 1);
     for (int i = lo + (int)t; i <= kOffsetSlot; i += (int)blockDim.x) f.host[i] = R[i];
+    // then the sequence word, ordered after every thread's mirror stores (barrier + system-scope
+    // fence): sel_prepared_execute_async returns once it changes
+    __syncthreads();
+    if (t == 0) {
+      const uint64_t q = R[kSeqSlot] + 1u;
+      R[kSeqSlot] = q;
+      __threadfence_system();
+      f.host[kSeqSlot] = q;
+    }
   }
 }
 

@@ -201,6 +201,12 @@ constexpr int kMaxRanks = 1024;
 constexpr int kGateSlot = 1 + kMaxRanks;
 constexpr int kOffsetSlot = 2 + kMaxRanks;   // this rank's global output offset (sel_execute_to)
 constexpr int kResultSlots = 3 + kMaxRanks;
+// One word past the result slots: the device-gated Execute's sequence number. finish_execute
+// bumps result[kSeqSlot] and stores it to the pinned mirror after the mirror's other words
+// (fence at system scope in between), so that a host spinning on it (sel_prepared_execute_async)
+// knows the count is final without waiting for the materialisation.
+constexpr int kSeqSlot = kResultSlots;
+constexpr int kResultAlloc = kResultSlots + 1;
 constexpr int kMirrorMax = 512;  // read-back mirror below kGateSlot (ExecFinish)
 
 // The library's own exchange over peer memory (sel_ctx_set_peers; SURVEY §8e "a one-shot peer

@@ -42,6 +42,16 @@ def child(rows):
             b.record()
             torch.cuda.synchronize()
             steps.append(a.elapsed_time(b) / 40)
+        asteps = []
+        if hasattr(q, "_fn_async"):   # the same steps returning at the count (async Execute)
+            for _ in range(5):
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record()
+                for _ in range(40):
+                    q.run(wait=False)
+                b.record()
+                torch.cuda.synchronize()
+                asteps.append(a.elapsed_time(b) / 40)
         ctx.enable_timing(True)
         ks = []
         for _ in range(20):
@@ -49,6 +59,7 @@ def child(rows):
             ks.append(ctx.last_times())
         ctx.enable_timing(False)
         out[n] = {"step": statistics.median(steps),
+                  "step_async": statistics.median(asteps) if asteps else None,
                   "count": statistics.median(k[0] for k in ks),
                   "pushdown": statistics.median(k[1] for k in ks)}
         q.release()
@@ -91,6 +102,8 @@ def main():
             print(json.dumps({"variant": name, "rows": int(n), "rounds": len(xs),
                               **{k: round(statistics.median(x[k] for x in xs), 4)
                                  for k in ("step", "count", "pushdown")},
+                              "step_async": (round(statistics.median(x["step_async"] for x in xs), 4)
+                                             if all(x.get("step_async") for x in xs) else None),
                               "step_all": [round(x["step"], 4) for x in xs]}), flush=True)
 
 

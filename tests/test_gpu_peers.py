@@ -63,7 +63,8 @@ def _worker(rank, world, port, n_global, out_path):
         g = t.execute(prog, project=["D"], max_size=max(r["count"] - 1, 0), capacity=8)
         r["gated"] = (g.count, g.materialized)
         q = t.prepare_execute(prog, project=["D"], max_size=n_global)
-        c1, c2 = q.run(), q.run()
+        c1, c2 = q.run(), q.run(wait=False)   # the second returns at its count (async)
+        torch.cuda.synchronize()
         res = q.result()
         r["prep"] = (c1, c2, res.offset, res.rowids.cpu().numpy().view(np.uint32).copy())
         q.release()

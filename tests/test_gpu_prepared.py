@@ -193,3 +193,89 @@ def test_prepared_with_single_rank_communicator(cuda_device):
         h.release()
     t.release()
     c.close()
+
+
+def _check_async(q, cols, types, prog, proj, stream=None):
+    """sel_prepared_execute_async: the count is final at return; the outputs once the stream is."""
+    want_c, want_ids, want_cols = oracle.pushdown(cols, types, prog, proj=proj)
+    assert q.run(wait=False) == want_c
+    assert q.materialized and q.local_count == want_c
+    (stream or torch.cuda.current_stream(q.table.ctx.device)).synchronize()
+    r = q.result()
+    np.testing.assert_array_equal(r.rowids.cpu().numpy().view(np.uint32), want_ids)
+    for j, c in enumerate(proj):
+        np.testing.assert_array_equal(r.columns[c].cpu().numpy().view(want_cols[j].dtype), want_cols[j])
+    return want_c
+
+
+def test_prepared_async_parity_and_interleaving(pctx):
+    """Async runs back to back (each launched while the previous materialisation may still run),
+    interleaved with blocking runs, plain counts and executes of the same context, and a gated
+    async run that writes nothing."""
+    n = 3_006_000                            # ragged: 560 rows in the tail chunk
+    T = configs.gen_c2(n)
+    cols = [c.numpy().copy() for c in T.columns]
+    t = register(pctx, cols, T.types)
+    prog = encode(configs.c2_probes()["listing"], T.types)
+    proj = configs.C2_PROJECT
+    want = oracle.count(cols, T.types, prog)
+    q = t.prepare_execute(prog, project=proj, max_size=n)
+    for _ in range(20):                      # no synchronisation between the runs
+        assert q.run(wait=False) == want and q.materialized
+    _check_async(q, cols, T.types, prog, proj)
+    assert _check(q, cols, T.types, prog, proj) == want
+    # a second prepared execute (other program) alternating with the first
+    prog2 = encode(configs.c2_probes()["between_in"], T.types)
+    q2 = t.prepare_execute(prog2, project=[3], max_size=n)
+    want2 = oracle.count(cols, T.types, prog2)
+    for _ in range(5):
+        assert q.run(wait=False) == want
+        assert q2.run(wait=False) == want2
+    _check_async(q2, cols, T.types, prog2, [3])
+    _check_async(q, cols, T.types, prog, proj)
+    # other calls of the context between async runs
+    assert t.count(prog) == want
+    assert q.run(wait=False) == want
+    assert t.execute(prog, project=[3], max_size=n).count == want
+    _check_async(q, cols, T.types, prog, proj)
+    # the gate: count > max_size writes nothing, also when returning at the count
+    ids = torch.full((want,), -7, dtype=torch.int32, device=pctx.device)
+    outs = [torch.full((want,), 5, dtype=d, device=pctx.device) for d in (torch.int32, torch.uint8, torch.int32)]
+    g = t.prepare_execute(prog, project=proj, max_size=want - 1, capacity=want, out=(ids, outs))
+    assert g.run(wait=False) == want and not g.materialized and g.local_count == 0
+    torch.cuda.synchronize(pctx.device)
+    assert bool((ids == -7).all()) and all(bool((o == 5).all()) for o in outs)
+    # with timing on the call blocks (the events are read at return) and still agrees
+    pctx.enable_timing(True)
+    try:
+        assert q.run(wait=False) == want
+        c_ms, p_ms = pctx.last_times()
+        assert c_ms > 0 and p_ms > 0
+    finally:
+        pctx.enable_timing(False)
+    for h in (q, q2, g):
+        h.release()
+    t.release()
+
+
+def test_prepared_async_non_graph_and_communicator(cuda_device):
+    """The async call on the uncaptured cases (constant program) and with a one-rank NCCL
+    communicator (the result words come from the kernel after the all-gather)."""
+    c = sel.Context(cuda_device)
+    c.set_comm(1, 0, sel.Context.new_unique_id())
+    n = 600_000
+    T = configs.gen_c2(n)
+    cols = [x.numpy() for x in T.columns]
+    t = register(c, cols, T.types)
+    prog = encode(configs.c2_probes()["listing"], T.types)
+    q = t.prepare_execute(prog, project=configs.C2_PROJECT, max_size=n)
+    for _ in range(3):
+        assert _check_async(q, cols, T.types, prog, configs.C2_PROJECT) == 100_200
+    qc = t.prepare_execute(encode(Const(True), T.types), project=[3], max_size=n)
+    assert qc.run(wait=False) == n and qc.materialized
+    torch.cuda.synchronize(cuda_device)
+    np.testing.assert_array_equal(qc.result().columns[3].cpu().numpy(), cols[3])
+    for h in (q, qc):
+        h.release()
+    t.release()
+    c.close()
