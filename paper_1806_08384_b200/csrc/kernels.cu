@@ -363,6 +363,25 @@ __device__ __forceinline__ void load_w2(const void* col, uint64_t base, int lane
   }
 }
 
+// A chunk of a 1-byte column as 8 words per lane (word k = rows 4(32k + lane) .. +3; bytes past
+// nvalid are 0).
+template <bool TAIL>
+__device__ __forceinline__ void load_w1_words(const void* col, uint64_t base, int lane,
+                                              uint32_t nvalid, uint32_t (&x)[8]) {
+  const uint8_t* c = static_cast<const uint8_t*>(col) + base;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    const uint32_t r0 = 4u * (32u * k + lane);
+    if (!TAIL || r0 + 3 < nvalid) {
+      x[k] = ld_stream_u32(c + r0);
+    } else {
+      const uint32_t a = r0 + 0 < nvalid ? c[r0 + 0] : 0u, b = r0 + 1 < nvalid ? c[r0 + 1] : 0u,
+                     d = r0 + 2 < nvalid ? c[r0 + 2] : 0u;
+      x[k] = a | (b << 8) | (d << 16);
+    }
+  }
+}
+
 template <bool TAIL>
 __device__ __forceinline__ void load_w1(const void* col, uint64_t base, int lane, uint32_t nvalid,
                                         uint32_t (&v)[32], char* cap) {
@@ -1522,26 +1541,52 @@ __device__ __forceinline__ void batch_column(const BatchProgram& p, const BatchC
     return;
   }
   uint32_t v[32];
-  if (C.wclass == W4) {
+  if (C.wclass == W1 && C.swar) {
+    // every leaf on this 1-byte column is 1..4 points: test four rows per 32-bit word (SWAR, the
+    // count fast path's s1_nibble; bit 4k+e = byte e of word k, the layout of load_w1)
+    uint32_t x[8];
+    load_w1_words<TAIL>(C.data, base, lane, nvalid, x);
+#pragma unroll 1
+    for (uint32_t l = C.leaf_begin; l < (uint32_t)C.leaf_begin + C.leaf_count; ++l) {
+      const int np = p.leaf_pts[l];
+      uint32_t pts[4];
+#pragma unroll
+      for (int t = 0; t < 4; ++t)
+        pts[t] = t < np ? (uint32_t)p.lo[p.leaf_iv_begin[l] + t] * 0x01010101u : 0u;
+      uint32_t m = 0;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) m |= s1_nibble(x[k], pts, np) << (4 * k);
+      lm[l * 32 + lane] = m;
+    }
+    return;
+  }
+  if (C.wclass == W1) {
+    load_w1<TAIL>(C.data, base, lane, nvalid, v, nullptr);
+  } else if (C.wclass == W4) {
     load_w4<TAIL>(C.data, base, lane, nvalid, v, nullptr);
     if (C.fkey) {
 #pragma unroll
       for (int i = 0; i < 32; ++i) v[i] = fkey(v[i]);
     }
-  } else if (C.wclass == W1) {
-    load_w1<TAIL>(C.data, base, lane, nvalid, v, nullptr);
   } else {
     load_w2<TAIL>(C.data, base, lane, nvalid, v, nullptr);
   }
 #pragma unroll 1
   for (uint32_t l = C.leaf_begin; l < (uint32_t)C.leaf_begin + C.leaf_count; ++l) {
     uint32_t m = 0;
-#pragma unroll 1
-    for (int t = 0; t < p.leaf_iv_count[l]; ++t) {
-      const uint32_t lo = (uint32_t)p.lo[p.leaf_iv_begin[l] + t];
-      const uint32_t sp = (uint32_t)p.span[p.leaf_iv_begin[l] + t];
+    const int niv = p.leaf_iv_count[l];
+    if (niv == 1 && p.span[p.leaf_iv_begin[l]] == 0) {   // one point: an equality per row
+      const uint32_t a = (uint32_t)p.lo[p.leaf_iv_begin[l]];
 #pragma unroll
-      for (int i = 0; i < 32; ++i) m |= (v[i] - lo <= sp) ? (1u << i) : 0u;
+      for (int i = 0; i < 32; ++i) m |= (v[i] == a) ? (1u << i) : 0u;
+    } else {
+#pragma unroll 1
+      for (int t = 0; t < niv; ++t) {
+        const uint32_t lo = (uint32_t)p.lo[p.leaf_iv_begin[l] + t];
+        const uint32_t sp = (uint32_t)p.span[p.leaf_iv_begin[l] + t];
+#pragma unroll
+        for (int i = 0; i < 32; ++i) m |= (v[i] - lo <= sp) ? (1u << i) : 0u;
+      }
     }
     lm[l * 32 + lane] = m;
   }

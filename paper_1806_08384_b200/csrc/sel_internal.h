@@ -127,7 +127,8 @@ struct BatchColumn {
   const void* data;
   uint8_t wclass, fkey;
   uint16_t leaf_begin, leaf_count;  // its leaves are [leaf_begin, leaf_begin + leaf_count)
-  uint16_t pad;
+  uint8_t swar;                     // 1-byte column whose every leaf is 1..4 points (leaf_pts)
+  uint8_t pad;
 };
 struct BatchProgram {
   uint32_t n_cols, n_leaves, n_ops, n_progs;
@@ -139,6 +140,8 @@ struct BatchProgram {
   BatchColumn col[kBatchMaxCols];
   uint16_t leaf_iv_begin[kBatchMaxLeaves];
   uint16_t leaf_iv_count[kBatchMaxLeaves];
+  // a leaf on a 1-byte column whose intervals are 1..4 single points: their count; 0 otherwise
+  uint8_t leaf_pts[kBatchMaxLeaves];
   uint8_t op[512];
   uint8_t arg[512];
   uint64_t lo[1024];

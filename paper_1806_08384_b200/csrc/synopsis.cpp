@@ -198,6 +198,9 @@ sel_status sel_count_batch(sel_table t, const void* const* progs, const size_t* 
       leaf_id[{col, (int)i}] = (int)nl;
       bp.leaf_iv_begin[nl] = (uint16_t)niv;
       bp.leaf_iv_count[nl] = (uint16_t)lst[i].size();
+      bool points = C.wclass == W1 && !lst[i].empty() && lst[i].size() <= 4;
+      for (const Interval& x : lst[i]) points = points && x.lo == x.hi;
+      bp.leaf_pts[nl] = points ? (uint8_t)lst[i].size() : 0;
       for (const Interval& x : lst[i]) {
         bp.lo[niv] = x.lo ^ bias;
         bp.span[niv] = x.hi - x.lo;
@@ -206,6 +209,8 @@ sel_status sel_count_batch(sel_table t, const void* const* progs, const size_t* 
       ++nl;
     }
     C.leaf_count = (uint16_t)(nl - C.leaf_begin);
+    C.swar = C.wclass == W1 ? 1 : 0;
+    for (uint32_t l = C.leaf_begin; l < nl; ++l) C.swar = C.swar && bp.leaf_pts[l] ? 1 : 0;
   }
   bp.n_leaves = nl;
   uint32_t nop = 0;

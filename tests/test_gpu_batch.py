@@ -70,3 +70,23 @@ def test_worked_example_leaf_vs_joint(ctx):
     # estimates (0.2, 0.167, 0.167, 0.27) the error is 111x (tests/golden/worked_example.json).
     independence = np.prod([c / n for c in got[:4]])
     assert got[4] / n > 3 * independence
+
+
+@pytest.mark.parametrize("n", [5, 1027, 70_001])
+def test_batch_byte_point_leaves(ctx, n):
+    """1-byte columns: leaves of 1..4 points take the packed (SWAR) test, the others (5+ points,
+    ranges, NOT) the unpacked one — both kinds on the same column in one batch, key 0 (the tail's
+    fill byte) and 255 included, plus a 4-byte point leaf (the equality loop); ragged tails."""
+    rng = np.random.default_rng(n + 5)
+    types = [DICT8, DICT8, INT32]
+    cols = [rng.integers(0, 6, n).astype(np.uint8), rng.integers(0, 256, n).astype(np.uint8),
+            rng.integers(-3, 4, n).astype(np.int32)]
+    t = sel.Table(ctx, ["a", "b", "x"], types, _gpu(cols, types, ctx.device))
+    nodes = [Cmp("=", 0, 0), In(0, (0, 5)), In(0, (1, 2, 3)), In(0, (0, 1, 2, 5)),
+             In(0, (0, 1, 2, 3, 4)), Between(0, 1, 3), Not(Cmp("=", 0, 0)),
+             And(In(1, (0, 255, 17)), Cmp("=", 2, 0)), Cmp("=", 1, 255), Cmp("<", 1, 128),
+             And(In(0, (0, 4)), In(1, (200, 201))), Cmp("=", 2, -3)]
+    for lo in range(0, len(nodes), 6):
+        progs = [encode(x, types) for x in nodes[lo:lo + 6] + nodes[:2]]
+        got = t.count_batch(progs)
+        assert got == [oracle.count(cols, types, p) for p in progs], nodes[lo:lo + 6]
