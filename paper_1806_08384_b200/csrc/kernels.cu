@@ -31,6 +31,12 @@
 
 #include "sel_internal.h"
 
+#ifndef SEL_BATCH_MINB
+// batch count: 4 resident CTAs per SM (<= 64 registers; 62 used, no spills). A/B on the worked
+// example's five programs: 0.845 -> 0.822-0.830 ms against the unbounded 79 registers (3 CTAs);
+// 5 CTAs 0.828-0.839, a next-chunk L2 prefetch 0.833 alone, 0.840-0.851 with 4 CTAs
+#define SEL_BATCH_MINB 4
+#endif
 #ifndef SEL_BATCH_PREFETCH
 #define SEL_BATCH_PREFETCH 1   // batch count: bulk-prefetch a chunk's later columns into L2
 #endif
@@ -1663,7 +1669,7 @@ __device__ __forceinline__ void batch_chunk(const BatchProgram& p, uint64_t base
   __syncwarp();
 }
 
-__global__ void __launch_bounds__(kThreads) count_batch_kernel(const __grid_constant__ BatchProgram p,
+__global__ void __launch_bounds__(kThreads, SEL_BATCH_MINB) count_batch_kernel(const __grid_constant__ BatchProgram p,
                                                                uint64_t n, uint64_t* __restrict__ out) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   __shared__ uint32_t s_lm[kWarpsPerCta][kBatchMaxLeaves * 32];

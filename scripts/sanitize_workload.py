@@ -102,6 +102,11 @@ assert q.run() == want[0] == r1.count
 for r in (r1, q.result()):
     assert np.array_equal(r.rowids.cpu().numpy().view(np.uint32), want[1])
     assert np.array_equal(r.columns[2].cpu().numpy(), want[2][1])
+# the async run (returns at the count; sequence word in pinned memory), back to back
+for _ in range(3):
+    assert q.run(wait=False) == want[0]
+torch.cuda.synchronize()
+assert np.array_equal(q.result().rowids.cpu().numpy().view(np.uint32), want[1])
 q.release()
 # sel_execute_to into the context's own buffers (offset 0)
 ids = torch.empty(want[0], dtype=torch.int32, device=dev)

@@ -58,6 +58,9 @@ def main():
             q = t.prepare_execute(prog, project=proj, max_size=n)
             q.run()
             check("prepared", q.result())
+            assert q.run(wait=False) == wc, ("prepared-async", n, types, node)
+            torch.cuda.synchronize()
+            check("prepared-async", q.result())
             q.release()
             b = t.count_batch([prog, encode(random_program(rng, types, pools, max_depth=2), types)])
             assert b[0] == wc, ("batch", n, types, node)
