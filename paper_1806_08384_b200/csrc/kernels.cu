@@ -970,42 +970,10 @@ template <class P, bool KEEP>
 // Returns the chunk's selected-row count (every lane; 0 without KEEP).
 __device__ __forceinline__ uint32_t keep_chunk(const SelectionBufs& sb, uint32_t* sbs, uint64_t c, int lane,
                                                uint32_t m, char* wsmem, uint32_t wm = 0u,
-                                               bool coded = false, uint32_t* mstage = nullptr) {
+                                               bool coded = false) {
   if (!KEEP) return 0u;
-  const uint32_t t = to_row_major(m, lane);          // the push-down stages from row-major masks
-#if SEL_MASK_BULK
-  // A/B: the chunk's mask (and code-bit) line staged in shared memory and written by one TMA
-  // bulk store per line instead of 32 lane stores
-  if (!sb.n_keep && mstage) {
-    if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
-    __syncwarp();
-    mstage[lane] = t;
-    if (coded) mstage[32 + lane] = to_row_major(wm, lane);
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    __syncwarp();
-    if (lane == 0) {
-      const uint32_t s0 = (uint32_t)__cvta_generic_to_shared(mstage);
-      if (SEL_MASK_BULK == 1) {
-        uint64_t pol;
-        asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
-        asm volatile("cp.async.bulk.global.shared::cta.bulk_group.L2::cache_hint [%0], [%1], 128, %2;"
-                     ::"l"(sb.bits + c * 32), "r"(s0), "l"(pol) : "memory");
-        if (coded)
-          asm volatile("cp.async.bulk.global.shared::cta.bulk_group.L2::cache_hint [%0], [%1], 128, %2;"
-                       ::"l"(sb.which + c * 32), "r"(s0 + 128u), "l"(pol) : "memory");
-      } else {
-        asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], 128;"
-                     ::"l"(sb.bits + c * 32), "r"(s0) : "memory");
-        if (coded)
-          asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], 128;"
-                       ::"l"(sb.which + c * 32), "r"(s0 + 128u) : "memory");
-      }
-      asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-    }
-  } else
-#endif
-  {
   if (coded) st_evict_last(sb.which + c * 32 + lane, to_row_major(wm, lane));
+  const uint32_t t = to_row_major(m, lane);          // the push-down stages from row-major masks
   if (sb.n_keep) {
     sb.bits[c * 32 + lane] = t;
   } else {
@@ -1014,7 +982,6 @@ __device__ __forceinline__ uint32_t keep_chunk(const SelectionBufs& sb, uint32_t
     // ms, C4 push-down 0.176 -> 0.160 ms). With kept values the slots compete for L2 and the
     // policy hurt (C2 0.913 -> 0.968 ms), so it is not used there.
     st_evict_last(sb.bits + c * 32 + lane, t);
-  }
   }
   uint32_t cc;
   if (sb.n_keep) {
@@ -1046,9 +1013,6 @@ __device__ __forceinline__ uint32_t keep_chunk(const SelectionBufs& sb, uint32_t
 // NW warps per CTA: 8 normally; 32 when staged key sets leave room for one CTA per SM only.
 // FASTN > 0: the program is a conjunction of FASTN fast-path leaves (p.fast_n == FASTN).
 template <class P, bool KEEP, int NW, int FASTN = 0>
-#ifndef SEL_MASK_BULK
-#define SEL_MASK_BULK 0
-#endif
 #ifndef SEL_FAST_MINB
 #define SEL_FAST_MINB 3   // fast path: <= 85 registers (A/B: 2-6; 3 best on C2, C4, C5)
 #endif
@@ -1065,12 +1029,6 @@ __global__ void __launch_bounds__(NW * 32, NW == kWarpsPerCta ? (FASTN ? SEL_FAS
   const uint64_t nw = (uint64_t)gridDim.x * NW;
   extern __shared__ __align__(16) char s_dyn[];
   char* wsmem = KEEP ? s_dyn + (size_t)warp * sb.warp_smem : nullptr;
-#if SEL_MASK_BULK
-  __shared__ __align__(128) uint32_t s_mstage[NW][64];
-  uint32_t* mstage = KEEP ? s_mstage[warp] : nullptr;
-#else
-  uint32_t* mstage = nullptr;
-#endif
   uint32_t cnt = 0;
   bool full = false;   // this warp kept a fully selected chunk (raises the flag once, below)
   // keeping counts: this count's half of the superblock sums (zero: the count before the last one
@@ -1117,7 +1075,7 @@ __global__ void __launch_bounds__(NW * 32, NW == kWarpsPerCta ? (FASTN ? SEL_FAS
       uint32_t wm = 0;
       const uint32_t m = eval_fast<FASTN, KEEP>(p, c * kChunkRows, lane, wsmem, &wm);
       cnt += __popc(m);
-      full |= keep_chunk<P, KEEP>(sb, my_sb, c, lane, m, wsmem, wm, KEEP && p.fast_code >= 0, mstage) == kChunkRows;
+      full |= keep_chunk<P, KEEP>(sb, my_sb, c, lane, m, wsmem, wm, KEEP && p.fast_code >= 0) == kChunkRows;
     }
   } else {
     if (lane == 0 && p.prefetch && gw < ns_full) prefetch_chunk(p, phase + gw * stride);
@@ -1126,7 +1084,7 @@ __global__ void __launch_bounds__(NW * 32, NW == kWarpsPerCta ? (FASTN ? SEL_FAS
       if (lane == 0 && p.prefetch && s + nw < ns_full) prefetch_chunk(p, c + nw * stride);
       const uint32_t m = eval_program<false, KEEP>(p, c * kChunkRows, lane, kChunkRows, wsmem, bm_sbase);
       cnt += __popc(m);
-      full |= keep_chunk<P, KEEP>(sb, my_sb, c, lane, m, wsmem, 0u, false, mstage) == kChunkRows;
+      full |= keep_chunk<P, KEEP>(sb, my_sb, c, lane, m, wsmem) == kChunkRows;
     }
   }
   if (tail_sampled && gw == ns_full % nw) {
@@ -1140,11 +1098,8 @@ __global__ void __launch_bounds__(NW * 32, NW == kWarpsPerCta ? (FASTN ? SEL_FAS
       const uint32_t pt1 = w4 ? (uint32_t)p.lo[p.leaf[s].iv_begin + 1] : (p.fast_pts[s][1] & 0xFFu);
       wm = which_tail(p.col[p.leaf[s].slot], nfull * kChunkRows, lane, rem, pt1, w4);
     }
-    keep_chunk<P, KEEP>(sb, my_sb, nfull, lane, m, wsmem, wm, coded, mstage);   // a tail chunk is never full
+    keep_chunk<P, KEEP>(sb, my_sb, nfull, lane, m, wsmem, wm, coded);   // a tail chunk is never full
   }
-#if SEL_MASK_BULK
-  if (KEEP && mstage && lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
-#endif
   // dense_chunks_kernel has work: one store per warp (one per chunk contended on the word: C5 at
   // s = 1 count 0.62 -> 1.36 ms)
   if (KEEP && full && lane == 0) sb.state[3] = 1u;
