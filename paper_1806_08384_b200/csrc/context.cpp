@@ -568,8 +568,9 @@ sel_status sel_ctx_set_option(sel_ctx ctx, const char* name, int64_t value) {
   else if (k == "graph_comm" && flag) ctx->graph_comm = value;
   else if (k == "prefetch" && value >= -1 && value <= 1) ctx->prefetch_mode = (int)value;
   else if (k == "count_warps" && (value == 0 || value == kWarpsPerCta)) ctx->count_nw = (int)value;
-  else if (k == "two_pass_min_rows" && value >= 0 && !ctx->force_single)
-    ctx->two_pass_min_rows = (uint64_t)value;
+  else if (k == "two_pass_min_rows" && value >= 0) {
+    if (!ctx->force_single) ctx->two_pass_min_rows = (uint64_t)value;   // else: ignored (sel.h)
+  }
   else if (k == "ctas_per_sm" && value >= 0) {
     ctx->occ_count_small = value ? std::min(ctx->occ_small_max, (int)value) : ctx->occ_small_max;
     ctx->occ_count_large = value ? std::min(ctx->occ_large_max, (int)value) : ctx->occ_large_max;

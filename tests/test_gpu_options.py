@@ -76,5 +76,8 @@ def test_option_errors(cuda_device):
             with pytest.raises(sel.SelError) as e:
                 ctx.set_option(name, value)
             assert e.value.status == 1, (name, value)
+        ctx.set_pushdown_path(0)                 # forced single pass: the threshold is ignored
+        ctx.set_option("two_pass_min_rows", 0)
+        ctx.set_pushdown_path(-1)
     finally:
         ctx.close()
