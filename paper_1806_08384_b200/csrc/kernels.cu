@@ -176,8 +176,10 @@ __device__ void finish_execute(const ExecFinish& f, const PeerXchg& xg, uint64_t
     __syncthreads();
     const int lo = kGateSlot - (nr > 0 ? nr : 1);
     for (int i = lo + (int)t; i <= kOffsetSlot; i += (int)blockDim.x) f.host[i] = R[i];
-    // then the sequence word, ordered after every thread's mirror stores (barrier + system-scope
-    // fence): sel_prepared_execute_async returns once it changes
+    // then the sequence word, ordered after every thread's mirror stores (barrier, then thread
+    // 0's system-scope fence, cumulative over what the barrier ordered before it — the pattern of
+    // a grid barrier's arrival): sel_prepared_execute_async returns once it changes. (A fence in
+    // every writer before the barrier as well: +3 us per Execute, profiles/r2/ab/)
     __syncthreads();
     if (t == 0) {
       const uint64_t q = R[kSeqSlot] + 1u;
@@ -391,19 +393,8 @@ __device__ __forceinline__ void load_w1_words(const void* col, uint64_t base, in
 template <bool TAIL>
 __device__ __forceinline__ void load_w1(const void* col, uint64_t base, int lane, uint32_t nvalid,
                                         uint32_t (&v)[32], char* cap) {
-  const uint8_t* c = static_cast<const uint8_t*>(col) + base;
   uint32_t x[8];
-#pragma unroll
-  for (int k = 0; k < 8; ++k) {
-    const uint32_t r0 = 4u * (32u * k + lane);
-    if (!TAIL || r0 + 3 < nvalid) {
-      x[k] = ld_stream_u32(c + r0);
-    } else {
-      const uint32_t a = r0 + 0 < nvalid ? c[r0 + 0] : 0u, b = r0 + 1 < nvalid ? c[r0 + 1] : 0u,
-                     d = r0 + 2 < nvalid ? c[r0 + 2] : 0u;
-      x[k] = a | (b << 8) | (d << 16);
-    }
-  }
+  load_w1_words<TAIL>(col, base, lane, nvalid, x);
 #pragma unroll
   for (int k = 0; k < 8; ++k) {
     if (cap) reinterpret_cast<uint32_t*>(cap)[32 * k + lane] = x[k];

@@ -90,3 +90,29 @@ def test_batch_byte_point_leaves(ctx, n):
         progs = [encode(x, types) for x in nodes[lo:lo + 6] + nodes[:2]]
         got = t.count_batch(progs)
         assert got == [oracle.count(cols, types, p) for p in progs], nodes[lo:lo + 6]
+
+
+@pytest.mark.parametrize("n", [7, 1030, 65_539])
+def test_batch_one_sided_leaves(ctx, n):
+    """One-interval leaves reaching the key minimum or maximum take one compare per row (signed for
+    INT32/DATE32, unsigned for DICT32/DICT16, key space for FLOAT32) — at the type's extremes,
+    around zero and with NaNs; the two-sided and point leaves of the same columns beside them."""
+    rng = np.random.default_rng(n + 9)
+    types = [INT32, DATE32, DICT32, DICT16, FLOAT32]
+    i32 = np.iinfo(np.int32)
+    x = rng.choice(np.array([i32.min, i32.min + 1, -5, -1, 0, 1, 5, i32.max - 1, i32.max], np.int32), n)
+    d = rng.integers(-3000, 3000, n).astype(np.int32)
+    k = rng.choice(np.array([0, 1, 7, 2**31 - 1, 2**31, 2**32 - 2, 2**32 - 1], np.uint64), n).astype(np.uint32).view(np.int32)
+    h = rng.integers(0, 1 << 16, n).astype(np.uint16).view(np.int16)
+    f = rng.choice(np.array([-np.inf, -1.5, -0.0, 0.0, 2.5, np.inf, np.nan], np.float32), n)
+    cols = [x, d, k, h, f]
+    t = sel.Table(ctx, ["x", "d", "k", "h", "f"], types, _gpu(cols, types, ctx.device))
+    nodes = [Cmp("<", 0, 0), Cmp("<=", 0, -1), Cmp(">", 0, -5), Cmp(">=", 0, int(i32.max)),
+             Cmp("<", 0, int(i32.min) + 1), Cmp("<", 1, 100), Cmp(">=", 1, -2999), Between(1, -10, 10),
+             Cmp("<=", 2, 7), Cmp(">", 2, 2**31 - 1), Cmp(">=", 2, 2**32 - 1), Cmp("=", 2, 0),
+             Cmp("<", 3, 1000), Cmp(">", 3, 65534), Cmp("<", 4, 0.0), Cmp(">=", 4, -1.5),
+             Cmp(">", 4, 2.5), Not(Cmp("<", 0, 5))]
+    for lo in range(0, len(nodes), 6):
+        progs = [encode(x_, types) for x_ in nodes[lo:lo + 6]]
+        got = t.count_batch(progs)
+        assert got == [oracle.count(cols, types, p) for p in progs], nodes[lo:lo + 6]
