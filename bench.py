@@ -883,10 +883,13 @@ def run_ours(args):
             "pushdown_path": pd_path,
             "clocks": clk.summary(),
             "e2e": e2e,
-            # count + push-down (+ the superblock prefix on the selection path, + the whole-chunk
-            # copy on selection push-downs of >= 8 Mi local rows: DESIGN.md §5)
-            "gpu_launches": ((3 + int((e - s) >= (8 << 20)
-                                      and os.environ.get("SEL_DENSE_SPLIT", "1") != "0"))
+            # per step: the count and the push-down; on the selection path also the whole-chunk
+            # copy (>= 8 Mi local rows) and, when NCCL carries the exchange, the 1-CTA kernel that
+            # finishes the result words after its all-gather (else the count's last CTA does;
+            # DESIGN.md §5)
+            "gpu_launches": ((2 + int((e - s) >= (8 << 20)
+                                      and os.environ.get("SEL_DENSE_SPLIT", "1") != "0")
+                              + int(bool(xchg) and str(xchg).startswith("nccl")))
                              if pd_path == 1 else 2) * args.steps,
             "cpu_baseline": cpu,
             "exchange_ab": exchange_ab,
