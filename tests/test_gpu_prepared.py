@@ -279,3 +279,30 @@ def test_prepared_async_non_graph_and_communicator(cuda_device):
         h.release()
     t.release()
     c.close()
+
+
+def test_prepared_async_capacity_cut(pctx):
+    """Capacity below the count (the gated single-pass use without the gate firing): the async run
+    returns the exact count and, once the stream has passed, exactly the first `capacity` selected
+    rows (ascending) with nothing past them."""
+    n = 606_000
+    T = configs.gen_c2(n)
+    cols = [c.numpy() for c in T.columns]
+    t = register(pctx, cols, T.types)
+    prog = encode(configs.c2_probes()["listing"], T.types)
+    want_c, want_ids, want_cols = oracle.pushdown(cols, T.types, prog, proj=configs.C2_PROJECT)
+    for cap in (1, 1023, 1024, 4097, want_c - 1):
+        ids = torch.full((cap + 64,), -7, dtype=torch.int32, device=pctx.device)
+        outs = [torch.full((cap + 64,), 5, dtype=d, device=pctx.device)
+                for d in (torch.int32, torch.uint8, torch.int32)]
+        q = t.prepare_execute(prog, project=configs.C2_PROJECT, max_size=n, capacity=cap,
+                              out=(ids, outs))
+        assert q.run(wait=False) == want_c and q.materialized and q.local_count == want_c
+        torch.cuda.synchronize(pctx.device)
+        np.testing.assert_array_equal(ids[:cap].cpu().numpy().view(np.uint32), want_ids[:cap])
+        assert bool((ids[cap:] == -7).all())
+        for o, w in zip(outs, want_cols):
+            np.testing.assert_array_equal(o[:cap].cpu().numpy().view(w.dtype), w[:cap])
+            assert bool((o[cap:] == 5).all())
+        q.release()
+    t.release()
