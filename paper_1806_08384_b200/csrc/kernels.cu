@@ -1772,7 +1772,12 @@ int launch_pushdown_sel_t(const P& p, uint64_t n, uint32_t* out_ids, int grid, c
                                                    ExecFinish{s.result, host, gate_ranks, rank},
                                                    xg ? *xg : PeerXchg{});
   }
-  if (block_chunks == 2) {
+  if (block_chunks == 1) {
+    if (p.coded)
+      pushdown_sel_kernel<P, true, 1><<<grid, kThreads, 0, stream>>>(p, n, sb, out_ids, s.result + kGateSlot);
+    else
+      pushdown_sel_kernel<P, false, 1><<<grid, kThreads, 0, stream>>>(p, n, sb, out_ids, s.result + kGateSlot);
+  } else if (block_chunks == 2) {
     if (p.coded)
       pushdown_sel_kernel<P, true, 2><<<grid, kThreads, 0, stream>>>(p, n, sb, out_ids, s.result + kGateSlot);
     else

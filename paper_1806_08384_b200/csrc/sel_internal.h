@@ -161,13 +161,20 @@ int occupancy_count_batch();
 // alternate between two halves by the parity of the device's keeping-count epoch (state[0]), and
 // a count zeroes the other half (the previous, now dead, selection's) while it runs.
 // Push-down from a selection: chunks per warp block. 4 on large shards (A/B 2/4/8: C5 push-down
-// 0.233 -> 0.206 ms, C3 0.240 -> 0.232, C2 equal, 8 slower); 2 below kSmallBlockRows local rows,
-// where a 4-chunk grid runs too few rounds to balance (step A/B: 75M rows 0.2261 -> 0.2220 ms,
-// 150M equal, 300M 0.7556 -> 0.7681 with 2).
+// 0.233 -> 0.206 ms, C3 0.240 -> 0.232, C2 equal, 8 slower); fewer below kSmallBlockRows local
+// rows, where a 4-chunk grid runs too few rounds to balance (step A/B: 75M rows 0.2261 -> 0.2220
+// ms with 2, 150M equal, 300M 0.7556 -> 0.7681 with 2; then 1 against 2: 75M async step 0.2159
+// -> 0.2125 ms, 37.5M equal).
 constexpr int kSelBlockChunks = 4;
-constexpr uint64_t kSmallBlockRows = 150ull << 20;
+#ifndef SEL_SMALL_BLOCK_ROWS
+#define SEL_SMALL_BLOCK_ROWS (150ull << 20)
+#endif
+constexpr uint64_t kSmallBlockRows = SEL_SMALL_BLOCK_ROWS;
+#ifndef SEL_SMALL_BC
+#define SEL_SMALL_BC 1   // chunks per block below kSmallBlockRows (1 or 2)
+#endif
 inline int pushdown_block_chunks(uint64_t local_rows) {
-  return local_rows < kSmallBlockRows ? 2 : kSelBlockChunks;
+  return local_rows < kSmallBlockRows ? SEL_SMALL_BC : kSelBlockChunks;
 }
 constexpr int kSbShift = 6;
 constexpr uint64_t kSbChunks = 1ull << kSbShift;
@@ -301,7 +308,7 @@ int launch_count_large(const DevProgramLarge& p, uint64_t n, int grid, const Scr
 // local count to s.result[0] and finishes the result words (ExecFinish with gate_ranks, rank,
 // host; xg != nullptr: through the peer exchange); then the compaction/gather kernel and, with
 // p.dense_split, the whole-chunk copy kernel.
-// block_chunks: chunks per warp block of the compaction kernel, 2 or 4 (pushdown_block_chunks).
+// block_chunks: chunks per warp block of the compaction kernel, 1, 2 or 4 (pushdown_block_chunks).
 int launch_pushdown_sel_small(const DevProgramSmall& p, uint64_t n, uint32_t* out_ids, int grid,
                               const Scratch& s, const SelectionBufs& sb, void* stream,
                               int gate_ranks = 0, const PeerXchg* xg = nullptr, int rank = 0,
