@@ -261,9 +261,10 @@ uint64_t sel_execute_to(sel_table table, const void* prog, size_t prog_bytes,
  * that word (polling the stream for errors, and NCCL's asynchronous error with a communicator).
  * With per-kernel timing on (sel_ctx_set_timing), more than 512 ranks, or an uncaptured
  * execute (constant program, empty shard, SEL_GRAPH_COMM=0 with NCCL), it blocks like
- * sel_prepared_execute. Until that stream has passed the materialisation, enqueue the context's
- * next calls on the same stream (or synchronise it first): they reuse the context's selection and
- * scratch buffers, which the materialisation is still reading.
+ * sel_prepared_execute. The context's later calls reuse its selection and scratch buffers, which
+ * the materialisation may still be reading: a call on another stream is ordered after it by the
+ * library (an event wait), except while that stream is being captured into the caller's own CUDA
+ * graph, where ordering it is the caller's part.
  * Errors: as sel_prepared_execute; SEL_E_STATE if the stream drained
  * without the Execute's result words; an error of the materialisation itself surfaces at the
  * caller's next synchronisation of the stream or the context's next call.

@@ -121,6 +121,18 @@ cudaError_t wait_result_seq(sel_ctx c, cudaStream_t s, uint64_t seq0) {
   }
 }
 
+cudaStream_t ordered_stream(sel_ctx c, void* cuda_stream) {
+  cudaStream_t s = (cudaStream_t)cuda_stream;
+  if (c->async_pending && s != c->async_stream) {
+    // not inside the caller's stream capture (an event recorded outside it cannot be waited on
+    // there); a captured probe is ordered by the caller
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    if (cudaStreamIsCapturing(s, &cs) == cudaSuccess && cs == cudaStreamCaptureStatusNone)
+      cudaStreamWaitEvent(s, c->async_ev, 0);
+  }
+  return s;
+}
+
 // After a synchronisation that followed peer exchanges: a timed-out wait (a rank missing) is an
 // error of the call, and sticky: the ranks' exchange epochs are out of step, so every later probe
 // of the context fails (plan_for) until the peers are dropped and set again (like comm_failed).
@@ -264,6 +276,7 @@ sel_status sel_ctx_create(int cuda_device, sel_ctx* out) {
               cudaMemset(c->s.ticket, 0, sizeof(unsigned long long)) == cudaSuccess &&
               cudaMemset(c->s.result, 0, kResultAlloc * sizeof(uint64_t)) == cudaSuccess &&
               (std::memset(c->h_result, 0, kResultAlloc * sizeof(uint64_t)), true) &&
+              cudaEventCreateWithFlags(&c->async_ev, cudaEventDisableTiming) == cudaSuccess &&
               cudaEventCreate(&c->ev0) == cudaSuccess && cudaEventCreate(&c->ev1) == cudaSuccess &&
               cudaEventCreate(&c->ev2) == cudaSuccess && cudaEventCreate(&c->ev3) == cudaSuccess &&
               cudaStreamCreateWithFlags(&c->cap_stream, cudaStreamNonBlocking) == cudaSuccess &&
@@ -504,6 +517,9 @@ void release_ctx_resources(sel_ctx c) {
     c->slot_buf[k] = nullptr;
     c->slot_cap[k] = 0;
   }
+  if (c->async_ev) cudaEventDestroy(c->async_ev);
+  c->async_ev = nullptr;
+  c->async_pending = false;
   if (c->ev0) cudaEventDestroy(c->ev0);
   if (c->ev1) cudaEventDestroy(c->ev1);
   if (c->ev2) cudaEventDestroy(c->ev2);

@@ -120,13 +120,18 @@ static uint64_t run_prepared(sel_prepared q, uint64_t* out_local_count,
                        out_local_count, out_global_offset, out_materialized, cuda_stream);
   DeviceGuard g(c->device);
   if (!g.ok) return fail64(SEL_E_CUDA, "cudaSetDevice failed");
-  cudaStream_t stream = (cudaStream_t)cuda_stream;
+  cudaStream_t stream = ordered_stream(c, cuda_stream);
   c->kept_table = nullptr;
   // Returning at the count needs its words in the pinned mirror (finish_execute) and no timing
   // events to read; otherwise the run blocks.
   async = async && !c->timing && (multi(c) ? c->nranks : 0) <= kMirrorMax;
   const uint64_t seq0 = *(volatile const uint64_t*)(c->h_result + kSeqSlot);
   cudaError_t e = cudaGraphLaunch(q->exec, stream);
+  if (e == cudaSuccess && async) {   // later calls on other streams order after this one
+    e = cudaEventRecord(c->async_ev, stream);
+    c->async_pending = e == cudaSuccess;
+    c->async_stream = stream;
+  }
   if (e == cudaSuccess) e = async ? wait_result_seq(c, stream, seq0) : sync_stream(c, stream);
   if (e != cudaSuccess) return fail64(sync_code(e), cuda_msg("prepared execute", e));
   if (peer_status(c) != SEL_OK) return SEL_ERR;

@@ -112,6 +112,11 @@ struct sel_ctx_s {
   ncclComm_t comm = nullptr;
   int nranks = 1, rank = 0;
   bool timing = false;
+  // the last sel_prepared_execute_async: its materialisation may still be running on
+  // async_stream; calls on another stream wait for this event first (ordered_stream)
+  cudaEvent_t async_ev = nullptr;
+  cudaStream_t async_stream = nullptr;
+  bool async_pending = false;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;   // count kernel
   cudaEvent_t ev2 = nullptr, ev3 = nullptr;   // push-down kernels (sel_execute times both)
   float last_ms = 0.f;
@@ -193,6 +198,8 @@ namespace sel {
 inline bool multi(sel_ctx c) { return c->comm != nullptr || c->peers; }
 cudaError_t sync_stream(sel_ctx c, cudaStream_t s);
 cudaError_t wait_result_seq(sel_ctx c, cudaStream_t s, uint64_t seq0);
+// The caller's stream of a probe, ordered after an async Execute still running on another stream.
+cudaStream_t ordered_stream(sel_ctx c, void* cuda_stream);
 sel_status peer_status(sel_ctx c);
 sel_status ensure_status(sel_ctx c, uint64_t ntiles, cudaStream_t stream);
 sel_status ensure_selection(sel_ctx c, uint64_t nchunks);

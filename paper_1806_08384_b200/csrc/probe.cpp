@@ -239,7 +239,7 @@ sel_status enqueue_pushdown_sel(sel_table t, const Plan& plan, const uint32_t* p
 // blocking (used where a rank has nothing of its own to enqueue but must match the collectives of
 // the others).
 sel_status gather_counts(sel_ctx c, uint64_t local, void* cuda_stream) {
-  cudaStream_t stream = (cudaStream_t)cuda_stream;
+  cudaStream_t stream = ordered_stream(c, cuda_stream);
   DeviceGuard g(c->device);
   if (!g.ok) return set_error(SEL_E_CUDA, "cudaSetDevice failed");
   c->h_result[0] = local;
@@ -352,7 +352,7 @@ uint64_t sel_count_ex(sel_table t, const void* prog, size_t prog_bytes, uint32_t
   if (c->destroyed) return fail64(SEL_E_STATE, "context destroyed");
   Plan plan;
   if (plan_for(t, prog, prog_bytes, &plan) != SEL_OK) return SEL_ERR;
-  cudaStream_t stream = (cudaStream_t)cuda_stream;
+  cudaStream_t stream = ordered_stream(c, cuda_stream);
   DeviceGuard g(c->device);
   if (!g.ok) return fail64(SEL_E_CUDA, "cudaSetDevice failed");
   c->last_ms = 0.f;
@@ -392,7 +392,7 @@ sel_status sel_count_async(sel_table t, const void* prog, size_t prog_bytes, uin
   if (c->destroyed) return set_error(SEL_E_STATE, "context destroyed");
   Plan plan;
   if (plan_for(t, prog, prog_bytes, &plan) != SEL_OK) return g_status;
-  cudaStream_t stream = (cudaStream_t)cuda_stream;
+  cudaStream_t stream = ordered_stream(c, cuda_stream);
   DeviceGuard g(c->device);
   if (!g.ok) return set_error(SEL_E_CUDA, "cudaSetDevice failed");
   const uint64_t n = t->local_rows;
@@ -428,7 +428,7 @@ uint64_t pushdown_impl(sel_table t, const void* prog, size_t prog_bytes, const u
     return SEL_ERR;
   Plan plan;
   if (plan_for(t, prog, prog_bytes, &plan) != SEL_OK) return SEL_ERR;
-  cudaStream_t stream = (cudaStream_t)cuda_stream;
+  cudaStream_t stream = ordered_stream(c, cuda_stream);
   DeviceGuard g(c->device);
   if (!g.ok) return fail64(SEL_E_CUDA, "cudaSetDevice failed");
   c->last_ms = 0.f;
@@ -635,7 +635,7 @@ static uint64_t execute_impl(sel_table t, const void* prog, size_t prog_bytes,
     if (multi(c)) {
       local = scan ? 0 : (plan.path == PATH_CONST && plan.const_value ? t->local_rows : 0);
       if (scan) {
-        cudaStream_t stream = (cudaStream_t)cuda_stream;
+        cudaStream_t stream = ordered_stream(c, cuda_stream);
         DeviceGuard g(c->device);
         if (!g.ok) return fail64(SEL_E_CUDA, "cudaSetDevice failed");
         if (enqueue_count(t, plan, SEL_KEEP_SELECTION, proj_cols, nkeep, stream, c->s.result,
@@ -686,7 +686,7 @@ static uint64_t execute_impl(sel_table t, const void* prog, size_t prog_bytes,
   // the selection -> global count into result[kGateSlot] (without a communicator the count
   // itself; with one, the sum of the all-gathered per-rank counts) -> the push-down kernels
   // read it and write nothing if count > maxSize -> one D2H.
-  cudaStream_t stream = (cudaStream_t)cuda_stream;
+  cudaStream_t stream = ordered_stream(c, cuda_stream);
   DeviceGuard g(c->device);
   if (!g.ok) return fail64(SEL_E_CUDA, "cudaSetDevice failed");
   c->last_ms = 0.f;

@@ -34,7 +34,7 @@ sel_status sel_histogram(sel_table t, uint32_t col, uint32_t stride, uint32_t ph
   }
   if (m >= (1ull << 31)) return set_error(SEL_E_TOO_LARGE, "sample of 2^31 rows or more");
   if (out_sample_rows) *out_sample_rows = m;
-  cudaStream_t stream = (cudaStream_t)cuda_stream;
+  cudaStream_t stream = ordered_stream(c, cuda_stream);
   DeviceGuard g(c->device);
   if (!g.ok) return set_error(SEL_E_CUDA, "cudaSetDevice failed");
   const size_t tb = histogram_temp_bytes(std::max<uint64_t>(m, 1));
@@ -86,7 +86,7 @@ uint64_t sel_count_sampled(sel_table t, const void* prog, size_t prog_bytes, uin
   if (c->destroyed) return fail64(SEL_E_STATE, "context destroyed");
   Plan plan;
   if (plan_for(t, prog, prog_bytes, &plan) != SEL_OK) return SEL_ERR;
-  cudaStream_t stream = (cudaStream_t)cuda_stream;
+  cudaStream_t stream = ordered_stream(c, cuda_stream);
   DeviceGuard g(c->device);
   if (!g.ok) return fail64(SEL_E_CUDA, "cudaSetDevice failed");
   const uint64_t n = t->local_rows;
@@ -242,7 +242,7 @@ sel_status sel_count_batch(sel_table t, const void* const* progs, const size_t* 
     for (size_t i = 0; i < P.op.size(); ++i)
       if (P.op[i] == DOP_LEAF) bp.conj_set[k] |= 1u << leaf_id[prog_leaf[k][P.arg[i]]];
   }
-  cudaStream_t stream = (cudaStream_t)cuda_stream;
+  cudaStream_t stream = ordered_stream(c, cuda_stream);
   DeviceGuard g(c->device);
   if (!g.ok) return set_error(SEL_E_CUDA, "cudaSetDevice failed");
   const uint64_t n = t->local_rows;

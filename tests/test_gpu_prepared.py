@@ -306,3 +306,32 @@ def test_prepared_async_capacity_cut(pctx):
             assert bool((o[cap:] == 5).all())
         q.release()
     t.release()
+
+
+def test_prepared_async_then_other_stream(pctx):
+    """An async Execute on stream A, then at once a keeping count and an Execute of another program
+    on stream B (they overwrite the context's selection): the library orders B after A's
+    materialisation, so both results equal the oracle. Repeated to give a race room to show."""
+    n = 6_000_000
+    T = configs.gen_c2(n)
+    cols = [c.numpy() for c in T.columns]
+    t = register(pctx, cols, T.types)
+    prog = encode(configs.c2_probes()["listing"], T.types)
+    prog2 = encode(Cmp("<", 1, 1500), T.types)
+    want_c, want_ids, want_cols = oracle.pushdown(cols, T.types, prog, proj=configs.C2_PROJECT)
+    want2_c, want2_ids, _ = oracle.pushdown(cols, T.types, prog2, proj=[3])
+    sa, sb = torch.cuda.Stream(pctx.device), torch.cuda.Stream(pctx.device)
+    q = t.prepare_execute(prog, project=configs.C2_PROJECT, max_size=n, stream=sa)
+    for _ in range(4):
+        assert q.run(wait=False) == want_c
+        assert t.count(prog2, stream=sb, keep_selection=True) == want2_c
+        r2 = t.execute(prog2, project=[3], max_size=n, stream=sb)
+        torch.cuda.synchronize(pctx.device)
+        r = q.result()
+        np.testing.assert_array_equal(r.rowids.cpu().numpy().view(np.uint32), want_ids)
+        for j, c in enumerate(configs.C2_PROJECT):
+            np.testing.assert_array_equal(r.columns[c].cpu().numpy().view(want_cols[j].dtype), want_cols[j])
+        assert r2.count == want2_c
+        np.testing.assert_array_equal(r2.rowids.cpu().numpy().view(np.uint32), want2_ids)
+    q.release()
+    t.release()
