@@ -127,8 +127,11 @@ cudaStream_t ordered_stream(sel_ctx c, void* cuda_stream) {
     // not inside the caller's stream capture (an event recorded outside it cannot be waited on
     // there); a captured probe is ordered by the caller
     cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
-    if (cudaStreamIsCapturing(s, &cs) == cudaSuccess && cs == cudaStreamCaptureStatusNone)
+    if (cudaStreamIsCapturing(s, &cs) != cudaSuccess) {
+      (void)cudaGetLastError();   // e.g. the legacy stream while another thread captures: no wait
+    } else if (cs == cudaStreamCaptureStatusNone) {
       cudaStreamWaitEvent(s, c->async_ev, 0);
+    }
   }
   return s;
 }
